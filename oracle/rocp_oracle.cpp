@@ -1,0 +1,1006 @@
+// rocp_oracle.cpp -- CPU restatement of the reference ROCP hot path.
+// TEST INFRASTRUCTURE ONLY (see rocp_oracle.h for scope, citations and the two
+// documented substitutions).  Written as plain loops over definitions; it does
+// not share code with the CUDA product (paper_2007_10798_b200/csrc), so the
+// GPU path is checked against an independent implementation of the same
+// canonical arithmetic.
+//
+// Build: oracle/Makefile (-O3 -ffp-contract=off; every fused multiply-add is an
+// explicit std::fma, everything else is a separately rounded IEEE operation).
+
+#include "rocp_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& what) {
+    g_err = what;
+    return code;
+}
+
+using Index = int64_t;
+using Dims = std::vector<Index>;
+
+// ---------------------------------------------------------------------------
+// Column-major dense matrix (layout of Eigen::MatrixXd, tensor.hpp:10).
+struct Mat {
+    Index rows = 0, cols = 0;
+    std::vector<double> v;
+    Mat() = default;
+    Mat(Index r, Index c, double fill = 0.0) : rows(r), cols(c), v(size_t(r * c), fill) {}
+    double& operator()(Index i, Index j) { return v[size_t(i + j * rows)]; }
+    double operator()(Index i, Index j) const { return v[size_t(i + j * rows)]; }
+    bool all_finite() const {
+        for (double x : v)
+            if (!std::isfinite(x)) return false;
+        return true;
+    }
+};
+
+Mat from_ptr(const double* p, Index r, Index c) {
+    Mat m(r, c);
+    if (r * c != 0) std::memcpy(m.v.data(), p, sizeof(double) * size_t(r * c));
+    return m;
+}
+
+void to_ptr(const Mat& m, double* p) {
+    if (m.rows * m.cols != 0) std::memcpy(p, m.v.data(), sizeof(double) * size_t(m.rows * m.cols));
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based RNG: Philox4x32-10 (Salmon et al., SC'11), written from the
+// published round function.  Substitutes std::mt19937_64 (kruskal.hpp:10) in
+// draw_samples (sampling.cpp:47-55) only.
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
+
+void philox(const uint32_t in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = in[0], c1 = in[1], c2 = in[2], c3 = in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {
+            k0 += kPhiloxW0;
+            k1 += kPhiloxW1;
+        }
+        const uint64_t p0 = uint64_t(kPhiloxM0) * c0;
+        const uint64_t p1 = uint64_t(kPhiloxM1) * c2;
+        const uint32_t hi0 = uint32_t(p0 >> 32), lo0 = uint32_t(p0);
+        const uint32_t hi1 = uint32_t(p1 >> 32), lo1 = uint32_t(p1);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0;
+        c1 = n1;
+        c2 = n2;
+        c3 = n3;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+// One uniform column index j in [1, co] for sample c (canonical RNG):
+// counter = (c, mode, iteration, batch), key = (lo32 seed, hi32 seed),
+// u = out0 | out1 << 32, j = 1 + floor(u * co / 2^64).
+Index draw_one(uint64_t seed, uint32_t batch, uint32_t iteration, uint32_t mode, uint32_t c,
+               Index co) {
+    const uint32_t ctr[4] = {c, mode, iteration, batch};
+    const uint32_t key[2] = {uint32_t(seed), uint32_t(seed >> 32)};
+    uint32_t out[4];
+    philox(ctr, key, out);
+    const uint64_t u = uint64_t(out[0]) | (uint64_t(out[1]) << 32);
+    const unsigned __int128 prod = (unsigned __int128)u * (unsigned __int128)uint64_t(co);
+    return Index(uint64_t(prod >> 64)) + 1;
+}
+
+// ---------------------------------------------------------------------------
+// tensor.cpp restatements.
+bool check_dims(const Dims& d) {
+    if (d.size() < 2) return false;  // tensor.cpp:11-17
+    for (Index x : d)
+        if (x < 1) return false;
+    return true;
+}
+
+Index element_count(const Dims& d) {  // tensor.cpp:54-58
+    Index n = 1;
+    for (Index x : d) n *= x;
+    return n;
+}
+
+Index codomain(const Dims& d, int mode) {  // tensor.cpp:60-66
+    Index n = 1;
+    for (size_t k = 0; k < d.size(); ++k)
+        if (int(k) + 1 != mode) n *= d[k];
+    return n;
+}
+
+std::vector<Index> strides_of(const Dims& d) {  // tensor.cpp:68-76
+    std::vector<Index> s(d.size());
+    Index acc = 1;
+    for (size_t k = 0; k < d.size(); ++k) {
+        s[k] = acc;
+        acc *= d[k];
+    }
+    return s;
+}
+
+// decode_index (tensor.cpp:96-109): per-mode 1-based indices {i_k, k != mode},
+// increasing mode order, lowest co-mode fastest.
+void decode(Index j, const Dims& d, int mode, Index* multi) {
+    Index rem = j - 1;
+    int pos = 0;
+    for (size_t k = 0; k < d.size(); ++k) {
+        if (int(k) + 1 == mode) continue;
+        multi[pos++] = rem % d[k] + 1;
+        rem /= d[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Canonical sample reduction: chunks of 32 consecutive samples,
+// each an fma chain from +0.0 in increasing sample order; chunk partials are
+// summed in increasing chunk order starting from the first partial.
+constexpr Index kChunk = 32;
+
+template <class A, class B>
+double sample_dot(Index s, A a, B b) {
+    double total = 0.0;
+    for (Index c0 = 0; c0 < s; c0 += kChunk) {
+        double p = 0.0;
+        const Index c1 = std::min(s, c0 + kChunk);
+        for (Index c = c0; c < c1; ++c) p = std::fma(a(c), b(c), p);
+        total = (c0 == 0) ? p : total + p;
+    }
+    return total;
+}
+
+Mat gram_of(const Mat& z) {  // Z^T Z (solve.cpp:41, rocp.cpp:63,108)
+    const Index s = z.rows, R = z.cols;
+    Mat g(R, R);
+    for (Index r2 = 0; r2 < R; ++r2)
+        for (Index r1 = 0; r1 < R; ++r1)
+            g(r1, r2) = sample_dot(
+                s, [&](Index c) { return z(c, r1); }, [&](Index c) { return z(c, r2); });
+    return g;
+}
+
+Mat contract_of(const Mat& x, const Mat& z) {  // X_s Z (solve.cpp:42, rocp.cpp:107)
+    const Index I = x.rows, s = x.cols, R = z.cols;
+    Mat out(I, R);
+    for (Index r = 0; r < R; ++r)
+        for (Index i = 0; i < I; ++i)
+            out(i, r) = sample_dot(
+                s, [&](Index c) { return x(i, c); }, [&](Index c) { return z(c, r); });
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Canonical solve_gram (solve.cpp:9-35 semantics).
+// Unpivoted LDL^T; regularize (G + 1e-12 tr(G) I) when the factorization shows
+// a non-positive pivot or a pivot ratio above kGramConditionLimit (1e12,
+// solve.hpp:15); zero solution when max diag <= 0 (solve.cpp:21-26).
+constexpr double kGramConditionLimit = 1e12;
+
+struct Ldl {
+    std::vector<double> l;  // R x R column-major unit lower (strict part used)
+    std::vector<double> d;  // R
+};
+
+// Returns the factorization of a (R x R, symmetric, column-major).  Updates
+// only i >= j, then mirrors, so every element sees the same operation sequence.
+Ldl ldlt(const std::vector<double>& a_in, int R) {
+    std::vector<double> a = a_in;
+    Ldl f;
+    f.l.assign(size_t(R) * R, 0.0);
+    f.d.assign(size_t(R), 0.0);
+    std::vector<double> lk(size_t(R), 0.0);
+    for (int k = 0; k < R; ++k) {
+        const double dk = a[size_t(k + k * R)];
+        f.d[size_t(k)] = dk;
+        for (int i = k + 1; i < R; ++i)
+            lk[size_t(i)] = (dk != 0.0) ? a[size_t(i + k * R)] / dk : 0.0;
+        for (int j = k + 1; j < R; ++j) {
+            const double ajk = a[size_t(j + k * R)];
+            for (int i = j; i < R; ++i)
+                a[size_t(i + j * R)] = std::fma(-lk[size_t(i)], ajk, a[size_t(i + j * R)]);
+        }
+        for (int j = k + 1; j < R; ++j)
+            for (int i = j; i < R; ++i) a[size_t(j + i * R)] = a[size_t(i + j * R)];
+        for (int i = k + 1; i < R; ++i) f.l[size_t(i + k * R)] = lk[size_t(i)];
+        f.l[size_t(k + k * R)] = 1.0;
+    }
+    return f;
+}
+
+bool needs_regularization(const Ldl& f) {
+    double dmin = f.d[0], dmax = f.d[0];
+    for (double x : f.d) {
+        if (x < dmin) dmin = x;
+        if (x > dmax) dmax = x;
+    }
+    return !(dmin > 0.0) || dmax > kGramConditionLimit * dmin;
+}
+
+// Solves y^T G = b^T for one row b (length R): forward L, diagonal, backward L^T.
+void ldlt_solve_row(const Ldl& f, int R, const double* b, Index bstride, double* y,
+                    Index ystride) {
+    std::vector<double> w(static_cast<size_t>(R));
+    for (int j = 0; j < R; ++j) {
+        double acc = b[size_t(j) * bstride];
+        for (int k = 0; k < j; ++k) acc = std::fma(-f.l[size_t(j + k * R)], w[size_t(k)], acc);
+        w[size_t(j)] = acc;
+    }
+    for (int j = 0; j < R; ++j) {
+        const double dj = f.d[size_t(j)];
+        w[size_t(j)] = (std::fabs(dj) > std::numeric_limits<double>::min()) ? w[size_t(j)] / dj
+                                                                            : 0.0;
+    }
+    // Backward substitution, updates applied in DEcreasing k.
+    for (int j = R - 1; j >= 0; --j) {
+        double acc = w[size_t(j)];
+        for (int k = R - 1; k > j; --k)
+            acc = std::fma(-f.l[size_t(k + j * R)], w[size_t(k)], acc);
+        w[size_t(j)] = acc;
+    }
+    for (int j = 0; j < R; ++j) y[size_t(j) * ystride] = w[size_t(j)];
+}
+
+Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized) {
+    const int R = int(gram.rows);
+    const Index I = rhs.rows;
+    Mat out(I, R);
+    double maxdiag = gram(0, 0);
+    for (int k = 1; k < R; ++k)
+        if (gram(k, k) > maxdiag) maxdiag = gram(k, k);
+    if (maxdiag <= 0.0) {  // solve.cpp:21-26
+        if (regularized) *regularized = true;
+        return out;
+    }
+    Ldl f = ldlt(gram.v, R);
+    if (needs_regularization(f)) {  // solve.cpp:28-33
+        double tr = gram(0, 0);
+        for (int k = 1; k < R; ++k) tr = tr + gram(k, k);
+        const double lambda = 1e-12 * tr;
+        std::vector<double> g = gram.v;
+        for (int k = 0; k < R; ++k) g[size_t(k + k * R)] = g[size_t(k + k * R)] + lambda;
+        f = ldlt(g, R);
+        if (regularized) *regularized = true;
+    }
+    for (Index i = 0; i < I; ++i) ldlt_solve_row(f, R, &rhs.v[size_t(i)], I, &out.v[size_t(i)], I);
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Sampling restatements (sampling.cpp).
+struct IndexSet {
+    int mode = 0;
+    Dims dims;
+    std::vector<Index> rows;     // 1-based column indices
+    std::vector<Index> decoded;  // s x (N-1) row-major, 1-based
+    Index count() const { return Index(rows.size()); }
+    int n_other() const { return int(dims.size()) - 1; }
+    Index at(Index c, int k) const { return decoded[size_t(c * n_other() + k)]; }
+};
+
+bool make_from_rows(const Dims& d, int mode, const Index* rows, Index s, IndexSet* out) {
+    const Index co = codomain(d, mode);
+    out->mode = mode;
+    out->dims = d;
+    out->rows.assign(rows, rows + s);
+    out->decoded.assign(size_t(s) * (d.size() - 1), 0);
+    for (Index c = 0; c < s; ++c) {
+        if (rows[c] < 1 || rows[c] > co) return false;  // tensor.cpp:98-99
+        decode(rows[c], d, mode, &out->decoded[size_t(c) * (d.size() - 1)]);
+    }
+    return true;
+}
+
+IndexSet draw(const Dims& d, int mode, Index s, uint64_t seed, uint32_t batch, uint32_t iter) {
+    const Index co = codomain(d, mode);
+    std::vector<Index> rows(static_cast<size_t>(s));
+    for (Index c = 0; c < s; ++c) rows[size_t(c)] = draw_one(seed, batch, iter, uint32_t(mode), uint32_t(c), co);
+    IndexSet idx;
+    make_from_rows(d, mode, rows.data(), s, &idx);
+    return idx;
+}
+
+// sample_unfolding (sampling.cpp:57-79): column c = fibre of the sample.
+Mat gather(const double* t, const Dims& d, const IndexSet& idx) {
+    const std::vector<Index> st = strides_of(d);
+    const int mode = idx.mode;
+    const Index ms = st[size_t(mode - 1)], I = d[size_t(mode - 1)];
+    Mat out(I, idx.count());
+    for (Index c = 0; c < idx.count(); ++c) {
+        Index base = 0;
+        int pos = 0;
+        for (size_t k = 0; k < d.size(); ++k) {
+            if (int(k) + 1 == mode) continue;
+            base += (idx.at(c, pos++) - 1) * st[k];
+        }
+        for (Index i = 0; i < I; ++i) out(i, c) = t[size_t(base + i * ms)];
+    }
+    return out;
+}
+
+// sampled_khatri_rao (sampling.cpp:81-105): start from 1.0, multiply factor rows
+// left to right in factors_excluding order (decreasing mode).
+bool skr(const IndexSet& idx, const std::vector<const Mat*>& f, Mat* z_out) {
+    const int n_other = idx.n_other();
+    if (int(f.size()) != n_other) return false;
+    const Index R = f.empty() ? 0 : f[0]->cols;
+    Mat z(idx.count(), R, 1.0);
+    for (int l = 0; l < n_other; ++l) {
+        const Mat& fl = *f[size_t(l)];
+        const int k = n_other - 1 - l;
+        for (Index c = 0; c < idx.count(); ++c) {
+            const Index i = idx.at(c, k);
+            if (i > fl.rows) return false;
+            for (Index r = 0; r < R; ++r) z(c, r) = z(c, r) * fl(i - 1, r);
+        }
+    }
+    *z_out = std::move(z);
+    return true;
+}
+
+// factors_excluding (kruskal.cpp:44-53): U(N), ..., U(mode+1), U(mode-1), ..., U(1).
+std::vector<const Mat*> excluding(const std::vector<Mat>& fs, int mode) {
+    std::vector<const Mat*> out;
+    for (int k = int(fs.size()); k >= 1; --k)
+        if (k != mode) out.push_back(&fs[size_t(k - 1)]);
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Canonical fitness (kruskal.cpp:55-89 semantics).
+// Per mode-1 fibre: lane partial l = fma chain over i1 = l, l+32, ... of d*d;
+// butterfly combine (offsets 16,8,4,2,1), value of lane 0.  Fibre values are
+// combined by hsum (groups of 256: 8 lane-strided adds then a butterfly,
+// repeated until one value).
+double butterfly32(double q[32]) {
+    for (int off = 16; off >= 1; off >>= 1) {
+        double nq[32];
+        for (int l = 0; l < 32; ++l) nq[l] = q[l] + q[l ^ off];
+        std::memcpy(q, nq, sizeof(nq));
+    }
+    return q[0];
+}
+
+double group_sum256(const double* v, Index n) {
+    double q[32];
+    for (int l = 0; l < 32; ++l) q[l] = (l < n) ? v[l] : 0.0;
+    for (int m = 1; m < 8; ++m)
+        for (int l = 0; l < 32; ++l) {
+            const Index idx = Index(l) + 32 * m;
+            q[l] = q[l] + ((idx < n) ? v[idx] : 0.0);
+        }
+    return butterfly32(q);
+}
+
+double hsum(std::vector<double> v) {
+    if (v.empty()) return 0.0;
+    while (v.size() > 1) {
+        std::vector<double> nv;
+        for (size_t g = 0; g < v.size(); g += 256)
+            nv.push_back(group_sum256(&v[g], Index(std::min<size_t>(256, v.size() - g))));
+        v.swap(nv);
+    }
+    return v[0];
+}
+
+// Returns sum of squares of (x_hat - x) (or of x when factors == nullptr).
+double fit_sumsq(const double* t, const Dims& d, const std::vector<Mat>* fs) {
+    const Index I1 = d[0];
+    const Index nfib = element_count(d) / I1;
+    const int N = int(d.size());
+    const Index R = fs ? (*fs)[0].cols : 0;
+    std::vector<double> fib(static_cast<size_t>(nfib));
+    std::vector<Index> multi(static_cast<size_t>(N - 1));
+    std::vector<double> w(static_cast<size_t>(R));
+    for (Index j = 0; j < nfib; ++j) {
+        if (fs) {
+            decode(j + 1, d, 1, multi.data());  // (i_2..i_N)
+            for (Index r = 0; r < R; ++r) {
+                double acc = (*fs)[size_t(N - 1)](multi[size_t(N - 2)] - 1, r);  // U(N)
+                for (int m = N - 1; m >= 2; --m) acc = acc * (*fs)[size_t(m - 1)](multi[size_t(m - 2)] - 1, r);
+                w[size_t(r)] = acc;
+            }
+        }
+        double q[32];
+        for (int l = 0; l < 32; ++l) q[l] = 0.0;
+        const double* col = t + j * I1;
+        for (Index i = 0; i < I1; ++i) {
+            double v = col[i];
+            if (fs) {
+                double xh = 0.0;
+                for (Index r = 0; r < R; ++r) xh = std::fma((*fs)[0](i, r), w[size_t(r)], xh);
+                v = xh - v;
+            }
+            q[i % 32] = std::fma(v, v, q[i % 32]);
+        }
+        fib[size_t(j)] = butterfly32(q);
+    }
+    return hsum(std::move(fib));
+}
+
+// Sampled residual |X_s - U Z^T|_F / |X_s|_F (north-star item 5; no reference
+// counterpart).  Canonical order: per
+// sample column, lane partials over rows (lane = i % 32, fma chain of e*e in
+// increasing i, u.z an fma chain over r from +0.0), butterfly, then hsum.
+double sampled_residual(const Mat& x, const Mat& u, const Mat& z) {
+    const Index I = x.rows, S = x.cols, R = z.cols;
+    std::vector<double> num(static_cast<size_t>(S)), den(static_cast<size_t>(S));
+    for (Index c = 0; c < S; ++c) {
+        double qn[32], qd[32];
+        for (int l = 0; l < 32; ++l) qn[l] = qd[l] = 0.0;
+        for (Index i = 0; i < I; ++i) {
+            double uz = 0.0;
+            for (Index r = 0; r < R; ++r) uz = std::fma(u(i, r), z(c, r), uz);
+            const double xv = x(i, c);
+            const double e = xv - uz;
+            qn[i % 32] = std::fma(e, e, qn[i % 32]);
+            qd[i % 32] = std::fma(xv, xv, qd[i % 32]);
+        }
+        num[size_t(c)] = butterfly32(qn);
+        den[size_t(c)] = butterfly32(qd);
+    }
+    const double n = hsum(std::move(num)), d = hsum(std::move(den));
+    return d > 0.0 ? std::sqrt(n) / std::sqrt(d) : 0.0;
+}
+
+bool dims_from(const int64_t* dims, int order, Dims* d) {
+    if (!dims || order < 2) return false;
+    d->assign(dims, dims + order);
+    return check_dims(*d);
+}
+
+// Solve one sampled LS (solve.cpp:37-44).
+Mat sampled_ls(const Mat& z, const Mat& x, bool* reg, bool* under) {
+    if (under && z.rows < z.cols) *under = true;
+    const Mat g = gram_of(z);
+    const Mat rhs = contract_of(x, z);
+    return solve_gram_m(g, rhs, reg);
+}
+
+}  // namespace
+
+// ===========================================================================
+// Stream state (rocp.hpp:15-24, 85-107).
+struct orc_stream {
+    int order = 0;
+    int rank = 0;
+    Index s = 0;
+    Dims head;
+    std::vector<Mat> factors;  // head factors U(1..N-1); slot N unused
+    Mat temporal;              // capacity rows >= t_len
+    std::vector<Mat> p, q;
+    Index t_len = 0;
+    bool regularized = false;
+    std::vector<double> last_resid;  // per stage of the last consume
+};
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    philox(ctr, key, out);
+}
+
+int64_t orc_codomain_size(const int64_t* dims, int order, int mode) {
+    Dims d;
+    if (!dims_from(dims, order, &d) || mode < 1 || mode > order) return -1;
+    return codomain(d, mode);
+}
+
+int orc_linear_index(const int64_t* multi, const int64_t* dims, int order, int mode, int64_t* j) {
+    // tensor.cpp:78-94
+    Dims d;
+    if (!dims_from(dims, order, &d) || mode < 1 || mode > order)
+        return fail(ORC_E_DOMAIN, "mode out of range");
+    Index acc = 1, stride = 1;
+    int pos = 0;
+    for (int k = 0; k < order; ++k) {
+        if (k + 1 == mode) continue;
+        const Index i = multi[pos++];
+        if (i < 1 || i > d[size_t(k)]) return fail(ORC_E_DOMAIN, "multi-index out of range");
+        acc += (i - 1) * stride;
+        stride *= d[size_t(k)];
+    }
+    *j = acc;
+    return ORC_OK;
+}
+
+int orc_decode_index(int64_t j, const int64_t* dims, int order, int mode, int64_t* multi) {
+    Dims d;
+    if (!dims_from(dims, order, &d) || mode < 1 || mode > order)
+        return fail(ORC_E_DOMAIN, "mode out of range");
+    if (j < 1 || j > codomain(d, mode)) return fail(ORC_E_DOMAIN, "column index out of range");
+    decode(j, d, mode, multi);
+    return ORC_OK;
+}
+
+int64_t orc_auto_sample_count(int rank) {  // sampling.cpp:40-45
+    if (rank < 1) return -1;
+    const double s = 10.0 * rank * std::log(double(rank));
+    return std::max<Index>(rank, Index(std::ceil(s)));
+}
+
+int orc_from_rows(const int64_t* dims, int order, int mode, const int64_t* rows, int64_t s,
+                  int64_t* decoded) {
+    Dims d;
+    if (!dims_from(dims, order, &d) || mode < 1 || mode > order)
+        return fail(ORC_E_DOMAIN, "bad dims/mode");
+    IndexSet idx;
+    if (!make_from_rows(d, mode, rows, s, &idx)) return fail(ORC_E_DOMAIN, "column index out of range");
+    std::copy(idx.decoded.begin(), idx.decoded.end(), decoded);
+    return ORC_OK;
+}
+
+int orc_draw_samples(const int64_t* dims, int order, int mode, int64_t s, uint64_t seed,
+                     uint32_t batch, uint32_t iteration, int64_t* rows, int64_t* decoded) {
+    Dims d;
+    if (!dims_from(dims, order, &d) || mode < 1 || mode > order)
+        return fail(ORC_E_DOMAIN, "bad dims/mode");
+    if (s < 1) return fail(ORC_E_DOMAIN, "sample count must be positive");  // sampling.cpp:48-49
+    IndexSet idx = draw(d, mode, s, seed, batch, iteration);
+    std::copy(idx.rows.begin(), idx.rows.end(), rows);
+    if (decoded) std::copy(idx.decoded.begin(), idx.decoded.end(), decoded);
+    return ORC_OK;
+}
+
+int orc_sample_unfolding(const double* t, const int64_t* dims, int order, int mode,
+                         const int64_t* decoded, int64_t s, double* out) {
+    Dims d;
+    if (!dims_from(dims, order, &d) || mode < 1 || mode > order)
+        return fail(ORC_E_DOMAIN, "bad dims/mode");
+    IndexSet idx;
+    idx.mode = mode;
+    idx.dims = d;
+    idx.rows.assign(size_t(s), 0);
+    idx.decoded.assign(decoded, decoded + s * (order - 1));
+    for (Index c = 0; c < s; ++c)
+        for (int k = 0, pos = 0; k < order; ++k) {
+            if (k + 1 == mode) continue;
+            const Index i = idx.at(c, pos++);
+            if (i < 1 || i > d[size_t(k)]) return fail(ORC_E_DOMAIN, "decoded index out of range");
+        }
+    to_ptr(gather(t, d, idx), out);
+    return ORC_OK;
+}
+
+int orc_sampled_khatri_rao(const int64_t* decoded, int64_t s, int n_other,
+                           const double* const* factors, const int64_t* factor_rows, int rank,
+                           double* z) {
+    IndexSet idx;
+    idx.dims.assign(size_t(n_other + 1), 1);
+    idx.rows.assign(size_t(s), 0);
+    idx.decoded.assign(decoded, decoded + s * n_other);
+    std::vector<Mat> fs;
+    for (int l = 0; l < n_other; ++l) fs.push_back(from_ptr(factors[l], factor_rows[l], rank));
+    std::vector<const Mat*> fp;
+    for (auto& m : fs) fp.push_back(&m);
+    Mat out;
+    if (!skr(idx, fp, &out)) return fail(ORC_E_DOMAIN, "sampled_khatri_rao: decoded index exceeds factor rows");
+    to_ptr(out, z);
+    return ORC_OK;
+}
+
+void orc_gram(const double* z, int64_t s, int rank, double* g) {
+    to_ptr(gram_of(from_ptr(z, s, rank)), g);
+}
+
+void orc_contract(const double* x, int64_t rows, int64_t s, const double* z, int rank, double* out) {
+    to_ptr(contract_of(from_ptr(x, rows, s), from_ptr(z, s, rank)), out);
+}
+
+int orc_solve_gram(const double* gram, const double* rhs, int64_t rows, int rank, double* out,
+                   int* regularized) {
+    if (rank < 1) return fail(ORC_E_DOMAIN, "solve_gram: empty gram");
+    bool reg = false;
+    to_ptr(solve_gram_m(from_ptr(gram, rank, rank), from_ptr(rhs, rows, rank), &reg), out);
+    if (regularized) *regularized = reg;
+    return ORC_OK;
+}
+
+int orc_solve_sampled_ls(const double* z, const double* x, int64_t s, int64_t rows, int rank,
+                         double* out, int* regularized, int* underdetermined) {
+    bool reg = false, under = false;
+    to_ptr(sampled_ls(from_ptr(z, s, rank), from_ptr(x, rows, s), &reg, &under), out);
+    if (regularized) *regularized = reg;
+    if (underdetermined) *underdetermined = under;
+    return ORC_OK;
+}
+
+int orc_model_fitness(const double* t, const int64_t* dims, int order,
+                      const double* const* factors, int rank, double* fit) {
+    Dims d;
+    if (!dims_from(dims, order, &d)) return fail(ORC_E_DOMAIN, "bad dims");
+    std::vector<Mat> fs;
+    for (int n = 0; n < order; ++n) fs.push_back(from_ptr(factors[n], d[size_t(n)], rank));
+    const double nsq = fit_sumsq(t, d, nullptr);
+    if (nsq == 0.0) return fail(ORC_E_DOMAIN, "fitness undefined for zero-norm reference tensor");
+    const double rsq = fit_sumsq(t, d, &fs);
+    *fit = 1.0 - std::sqrt(rsq) / std::sqrt(nsq);  // kruskal.cpp:84
+    return ORC_OK;
+}
+
+int orc_reconstruct(const double* const* factors, const int64_t* dims, int order, int rank,
+                    double* out) {
+    // Elementwise CP reconstruction in the canonical per-element order (same
+    // x_hat as fit_sumsq).
+    Dims d;
+    if (!dims_from(dims, order, &d)) return fail(ORC_E_DOMAIN, "bad dims");
+    std::vector<Mat> fs;
+    for (int n = 0; n < order; ++n) fs.push_back(from_ptr(factors[n], d[size_t(n)], rank));
+    const Index I1 = d[0], nfib = element_count(d) / I1;
+    std::vector<Index> multi(static_cast<size_t>(order - 1));
+    std::vector<double> w(static_cast<size_t>(rank));
+    for (Index j = 0; j < nfib; ++j) {
+        decode(j + 1, d, 1, multi.data());
+        for (int r = 0; r < rank; ++r) {
+            double acc = fs[size_t(order - 1)](multi[size_t(order - 2)] - 1, r);
+            for (int m = order - 1; m >= 2; --m) acc = acc * fs[size_t(m - 1)](multi[size_t(m - 2)] - 1, r);
+            w[size_t(r)] = acc;
+        }
+        for (Index i = 0; i < I1; ++i) {
+            double xh = 0.0;
+            for (int r = 0; r < rank; ++r) xh = std::fma(fs[0](i, r), w[size_t(r)], xh);
+            out[size_t(j * I1 + i)] = xh;
+        }
+    }
+    return ORC_OK;
+}
+
+int orc_khatri_rao(const double* a, int64_t m, const double* b, int64_t p, int rank, double* out) {
+    // matrix_ops.cpp:7-17: row p' + m'*P is a(m',:) .* b(p',:).
+    for (int r = 0; r < rank; ++r)
+        for (Index i = 0; i < m; ++i)
+            for (Index k = 0; k < p; ++k)
+                out[size_t((i * p + k) + Index(r) * m * p)] = a[size_t(i + Index(r) * m)] * b[size_t(k + Index(r) * p)];
+    return ORC_OK;
+}
+
+int orc_cprand(const double* t, const int64_t* dims, int order, int rank, int64_t samples,
+               double tol, int max_iters, uint64_t seed, double* const* factors,
+               double* const* best_kr, double* best_fitness, int* iterations, int* regularized,
+               int* err_sweep, double* fit_trace) {
+    // cprand.cpp:12-69
+    Dims d;
+    if (!dims_from(dims, order, &d)) return fail(ORC_E_DOMAIN, "bad dims");
+    if (rank < 1) return fail(ORC_E_DOMAIN, "cprand_decompose: rank must be positive");
+    if (max_iters < 1) return fail(ORC_E_DOMAIN, "cprand_decompose: need at least one sweep");
+    const double nsq = fit_sumsq(t, d, nullptr);
+    if (nsq == 0.0) return fail(ORC_E_DOMAIN, "cprand_decompose: zero tensor");
+    const Index s = samples > 0 ? samples : orc_auto_sample_count(rank);
+
+    std::vector<Mat> model;
+    for (int n = 0; n < order; ++n) model.push_back(from_ptr(factors[n], d[size_t(n)], rank));
+    std::vector<Mat> best_model;
+    double best = -std::numeric_limits<double>::infinity();
+    double prev = best;
+    bool reg_any = false;
+    int sweep = 0;
+    while (sweep < max_iters) {
+        ++sweep;
+        for (int n = 1; n <= order; ++n) {
+            const IndexSet idx = draw(d, n, s, seed, 0u, uint32_t(sweep));
+            Mat z;
+            skr(idx, excluding(model, n), &z);
+            const Mat xs = gather(t, d, idx);
+            bool reg = false;
+            model[size_t(n - 1)] = sampled_ls(z, xs, &reg, nullptr);
+            reg_any = reg_any || reg;
+            if (!model[size_t(n - 1)].all_finite()) {
+                if (err_sweep) *err_sweep = sweep;
+                return fail(ORC_E_NUMERICAL, "cprand_decompose: non-finite factor update (sweep " + std::to_string(sweep) + ")");
+            }
+        }
+        const double rsq = fit_sumsq(t, d, &model);
+        const double fit = 1.0 - std::sqrt(rsq) / std::sqrt(nsq);
+        if (fit_trace) fit_trace[sweep - 1] = fit;
+        if (!std::isfinite(fit)) {
+            if (err_sweep) *err_sweep = sweep;
+            return fail(ORC_E_NUMERICAL, "cprand_decompose: non-finite fitness (sweep " + std::to_string(sweep) + ")");
+        }
+        if (fit > best) {
+            best = fit;
+            best_model = model;
+        }
+        if (std::fabs(fit - prev) < tol) break;
+        prev = fit;
+    }
+    // Z_best rebuild: one fresh draw per non-temporal mode (cprand.cpp:61-67),
+    // keyed (batch 0, iteration 0).
+    for (int n = 1; n < order; ++n) {
+        const IndexSet idx = draw(d, n, s, seed, 0u, 0u);
+        Mat z;
+        skr(idx, excluding(best_model, n), &z);
+        to_ptr(z, best_kr[n - 1]);
+    }
+    for (int n = 0; n < order; ++n) to_ptr(best_model[size_t(n)], factors[n]);
+    *best_fitness = best;
+    *iterations = sweep;
+    if (regularized) *regularized = reg_any;
+    return ORC_OK;
+}
+
+int orc_stream_new(int order, const int64_t* head_dims, int rank, int64_t s, int literal_init,
+                   const double* const* factors, int64_t t_init, const double* const* best_kr,
+                   int regularized, orc_stream** out) {
+    // RocpStream ctor + init_state (rocp.cpp:45-69, 133-142).
+    if (order < 2 || rank < 1 || s < 1) return fail(ORC_E_DOMAIN, "init_state: bad arguments");
+    auto* st = new orc_stream;
+    st->order = order;
+    st->rank = rank;
+    st->s = s;
+    st->head.assign(head_dims, head_dims + order - 1);
+    for (int n = 0; n < order - 1; ++n) st->factors.push_back(from_ptr(factors[n], st->head[size_t(n)], rank));
+    st->factors.emplace_back();
+    st->temporal = from_ptr(factors[order - 1], t_init, rank);
+    st->t_len = t_init;
+    st->regularized = regularized != 0;
+    for (int n = 0; n < order - 1; ++n) {
+        const Mat z = from_ptr(best_kr[n], s, rank);
+        Mat q = gram_of(z);
+        const Mat& u = st->factors[size_t(n)];
+        Mat p(u.rows, rank);
+        if (literal_init) {
+            p = u;
+        } else {  // P = U Q, fma chain over k from +0.0
+            for (int r = 0; r < rank; ++r)
+                for (Index i = 0; i < u.rows; ++i) {
+                    double acc = 0.0;
+                    for (int k = 0; k < rank; ++k) acc = std::fma(u(i, k), q(k, r), acc);
+                    p(i, r) = acc;
+                }
+        }
+        st->p.push_back(std::move(p));
+        st->q.push_back(std::move(q));
+    }
+    *out = st;
+    return ORC_OK;
+}
+
+void orc_stream_free(orc_stream* st) { delete st; }
+
+static Dims slab_dims(const orc_stream* st, int64_t batch) {
+    Dims d = st->head;
+    d.push_back(batch);
+    return d;
+}
+
+int orc_stream_update_last_mode_with(orc_stream* st, const double* x_new, int64_t batch,
+                                     const int64_t* rows, int64_t s, double* u_new, double* z_s,
+                                     int* regularized) {
+    // rocp.cpp:71-84
+    const Dims d = slab_dims(st, batch);
+    IndexSet idx;
+    if (!make_from_rows(d, st->order, rows, s, &idx)) return fail(ORC_E_DOMAIN, "bad index set");
+    Mat z;
+    skr(idx, excluding(st->factors, st->order), &z);
+    const Mat xs = gather(x_new, d, idx);
+    bool reg = false;
+    const Mat u = sampled_ls(z, xs, &reg, nullptr);
+    st->last_resid.assign(size_t(st->order), 0.0);
+    st->last_resid[0] = sampled_residual(xs, u, z);
+    to_ptr(u, u_new);
+    if (z_s) to_ptr(z, z_s);
+    if (regularized) *regularized = reg;
+    return ORC_OK;
+}
+
+int orc_stream_append_temporal(orc_stream* st, const double* u_new, int64_t batch) {
+    // rocp.cpp:152-156 (geometric growth; old rows untouched)
+    const int R = st->rank;
+    if (st->temporal.rows < st->t_len + batch) {
+        const Index cap = std::max<Index>(2 * st->temporal.rows, st->t_len + batch);
+        Mat grown(cap, R);
+        for (int r = 0; r < R; ++r)
+            for (Index i = 0; i < st->t_len; ++i) grown(i, r) = st->temporal(i, r);
+        st->temporal = std::move(grown);
+    }
+    for (int r = 0; r < R; ++r)
+        for (Index b = 0; b < batch; ++b) st->temporal(st->t_len + b, r) = u_new[size_t(b + Index(r) * batch)];
+    return ORC_OK;
+}
+
+int orc_stream_update_mode_with(orc_stream* st, const double* x_new, int64_t batch,
+                                const double* u_new, int mode, const int64_t* rows, int64_t s,
+                                double* z_new, double* x_s, int* regularized) {
+    // rocp.cpp:96-113 with slab_factors_excluding (rocp.cpp:25-34)
+    if (mode < 1 || mode >= st->order)
+        return fail(ORC_E_DOMAIN, "update_mode_with: index set must be over a non-temporal mode");
+    const Dims d = slab_dims(st, batch);
+    IndexSet idx;
+    if (!make_from_rows(d, mode, rows, s, &idx)) return fail(ORC_E_DOMAIN, "bad index set");
+    const Mat un = from_ptr(u_new, batch, st->rank);
+    std::vector<const Mat*> fs{&un};
+    for (int k = st->order - 1; k >= 1; --k)
+        if (k != mode) fs.push_back(&st->factors[size_t(k - 1)]);
+    Mat z;
+    skr(idx, fs, &z);
+    const Mat xs = gather(x_new, d, idx);
+    const Mat inc = contract_of(xs, z);
+    const Mat g = gram_of(z);
+    Mat& p = st->p[size_t(mode - 1)];
+    Mat& q = st->q[size_t(mode - 1)];
+    for (size_t e = 0; e < p.v.size(); ++e) p.v[e] = p.v[e] + inc.v[e];
+    for (size_t e = 0; e < q.v.size(); ++e) q.v[e] = q.v[e] + g.v[e];
+    bool reg = false;
+    st->factors[size_t(mode - 1)] = solve_gram_m(q, p, &reg);
+    if (st->last_resid.size() == size_t(st->order))
+        st->last_resid[size_t(mode)] = sampled_residual(xs, st->factors[size_t(mode - 1)], z);
+    if (z_new) to_ptr(z, z_new);
+    if (x_s) to_ptr(xs, x_s);
+    if (regularized) *regularized = reg;
+    return ORC_OK;
+}
+
+int orc_stream_finish_batch(orc_stream* st, int64_t batch) {
+    st->t_len += batch;
+    return ORC_OK;
+}
+
+int orc_stream_consume(orc_stream* st, const double* x_new, int64_t batch, uint64_t seed,
+                       uint32_t batch_id) {
+    // RocpStream::consume (rocp.cpp:144-160): temporal draw (mode N), solve,
+    // append, then modes 1..N-1 Gauss-Seidel.
+    const Dims d = slab_dims(st, batch);
+    const int N = st->order;
+    const Index s = st->s;
+    const IndexSet it = draw(d, N, s, seed, batch_id, 0u);
+    std::vector<double> u_new(static_cast<size_t>(batch * st->rank));
+    int reg = 0;
+    int rc = orc_stream_update_last_mode_with(st, x_new, batch, it.rows.data(), s, u_new.data(),
+                                              nullptr, &reg);
+    if (rc) return rc;
+    st->regularized = st->regularized || reg;
+    orc_stream_append_temporal(st, u_new.data(), batch);
+    for (int n = 1; n < N; ++n) {
+        const IndexSet idx = draw(d, n, s, seed, batch_id, 0u);
+        int r2 = 0;
+        rc = orc_stream_update_mode_with(st, x_new, batch, u_new.data(), n, idx.rows.data(), s,
+                                         nullptr, nullptr, &r2);
+        if (rc) return rc;
+        // update_mode_with's flag is not propagated by consume (rocp.cpp:124),
+        // matching the reference.
+    }
+    st->t_len += batch;
+    return ORC_OK;
+}
+
+int orc_stream_get(const orc_stream* st, int what, int mode, double* out) {
+    switch (what) {
+        case 0: to_ptr(st->factors[size_t(mode - 1)], out); return ORC_OK;
+        case 1: to_ptr(st->p[size_t(mode - 1)], out); return ORC_OK;
+        case 2: to_ptr(st->q[size_t(mode - 1)], out); return ORC_OK;
+        case 3: {
+            const int R = st->rank;
+            for (int r = 0; r < R; ++r)
+                for (Index i = 0; i < st->t_len; ++i) out[size_t(i + Index(r) * st->t_len)] = st->temporal(i, r);
+            return ORC_OK;
+        }
+    }
+    return fail(ORC_E_DOMAIN, "bad selector");
+}
+
+int orc_stream_set(orc_stream* st, int what, int mode, const double* in) {
+    switch (what) {
+        case 0: { Mat& m = st->factors[size_t(mode - 1)]; std::memcpy(m.v.data(), in, m.v.size() * 8); return ORC_OK; }
+        case 1: { Mat& m = st->p[size_t(mode - 1)]; std::memcpy(m.v.data(), in, m.v.size() * 8); return ORC_OK; }
+        case 2: { Mat& m = st->q[size_t(mode - 1)]; std::memcpy(m.v.data(), in, m.v.size() * 8); return ORC_OK; }
+    }
+    return fail(ORC_E_DOMAIN, "bad selector");
+}
+
+int64_t orc_stream_t_len(const orc_stream* st) { return st->t_len; }
+
+int orc_stream_last_residuals(const orc_stream* st, double* out) {
+    if (st->last_resid.size() != size_t(st->order)) return fail(ORC_E_DOMAIN, "no consume yet");
+    std::copy(st->last_resid.begin(), st->last_resid.end(), out);
+    return ORC_OK;
+}
+
+int orc_sampled_residual(const double* x, int64_t rows, int64_t s, const double* u,
+                         const double* z, int rank, double* out) {
+    *out = sampled_residual(from_ptr(x, rows, s), from_ptr(u, rows, rank), from_ptr(z, s, rank));
+    return ORC_OK;
+}
+int orc_stream_regularized(const orc_stream* st) { return st->regularized ? 1 : 0; }
+
+// ---- exact online baseline (baselines.cpp:142-195), plain loops -------------
+static Mat full_kr_excluding(const std::vector<Mat>& fs, int mode) {
+    // khatri_rao_list(factors_excluding(m, mode)) (matrix_ops.cpp:19-26)
+    std::vector<const Mat*> ex = excluding(fs, mode);
+    Mat acc = *ex[0];
+    for (size_t i = 1; i < ex.size(); ++i) {
+        const Mat& b = *ex[i];
+        Mat out(acc.rows * b.rows, acc.cols);
+        for (Index r = 0; r < acc.cols; ++r)
+            for (Index m = 0; m < acc.rows; ++m)
+                for (Index p = 0; p < b.rows; ++p) out(m * b.rows + p, r) = acc(m, r) * b(p, r);
+        acc = std::move(out);
+    }
+    return acc;
+}
+
+static Mat unfold_m(const double* t, const Dims& d, int mode) {
+    IndexSet all;
+    const Index co = codomain(d, mode);
+    std::vector<Index> rows(static_cast<size_t>(co));
+    for (Index j = 0; j < co; ++j) rows[size_t(j)] = j + 1;
+    make_from_rows(d, mode, rows.data(), co, &all);
+    return gather(t, d, all);
+}
+
+static Mat plain_mul(const Mat& a, const Mat& b) {  // a (m x k) * b (k x n), sequential k
+    Mat out(a.rows, b.cols);
+    for (Index j = 0; j < b.cols; ++j)
+        for (Index i = 0; i < a.rows; ++i) {
+            double acc = 0.0;
+            for (Index k = 0; k < a.cols; ++k) acc = std::fma(a(i, k), b(k, j), acc);
+            out(i, j) = acc;
+        }
+    return out;
+}
+
+static Mat transpose_m(const Mat& a) {
+    Mat t(a.cols, a.rows);
+    for (Index j = 0; j < a.cols; ++j)
+        for (Index i = 0; i < a.rows; ++i) t(j, i) = a(i, j);
+    return t;
+}
+
+int orc_online_full_init(const double* x, const int64_t* dims, int order,
+                         const double* const* factors, int rank, double* const* p,
+                         double* const* q) {
+    Dims d;
+    if (!dims_from(dims, order, &d)) return fail(ORC_E_DOMAIN, "bad dims");
+    std::vector<Mat> fs;
+    for (int n = 0; n < order; ++n) fs.push_back(from_ptr(factors[n], d[size_t(n)], rank));
+    for (int n = 1; n < order; ++n) {
+        const Mat z = full_kr_excluding(fs, n);
+        to_ptr(plain_mul(unfold_m(x, d, n), z), p[n - 1]);
+        to_ptr(plain_mul(transpose_m(z), z), q[n - 1]);
+    }
+    return ORC_OK;
+}
+
+int orc_online_full_update(const double* x_new, const int64_t* dims, int order,
+                           double* const* factors_head, int rank, double* const* p,
+                           double* const* q, double* u_new_out) {
+    Dims d;
+    if (!dims_from(dims, order, &d)) return fail(ORC_E_DOMAIN, "bad dims");
+    const Index B = d.back();
+    std::vector<Mat> fs;
+    for (int n = 0; n < order - 1; ++n) fs.push_back(from_ptr(factors_head[n], d[size_t(n)], rank));
+    fs.push_back(Mat(B, rank));  // placeholder for the temporal slot
+    const Mat zh = full_kr_excluding(fs, order);
+    const Mat u_new = solve_gram_m(plain_mul(transpose_m(zh), zh), plain_mul(unfold_m(x_new, d, order), zh), nullptr);
+    fs.back() = u_new;
+    for (int n = 1; n < order; ++n) {
+        const Mat z = full_kr_excluding(fs, n);  // u_new first, decreasing modes
+        Mat pm = from_ptr(p[n - 1], d[size_t(n - 1)], rank);
+        Mat qm = from_ptr(q[n - 1], rank, rank);
+        const Mat inc = plain_mul(unfold_m(x_new, d, n), z);
+        const Mat g = plain_mul(transpose_m(z), z);
+        for (size_t e = 0; e < pm.v.size(); ++e) pm.v[e] = pm.v[e] + inc.v[e];
+        for (size_t e = 0; e < qm.v.size(); ++e) qm.v[e] = qm.v[e] + g.v[e];
+        fs[size_t(n - 1)] = solve_gram_m(qm, pm, nullptr);
+        to_ptr(pm, p[n - 1]);
+        to_ptr(qm, q[n - 1]);
+        to_ptr(fs[size_t(n - 1)], factors_head[n - 1]);
+    }
+    to_ptr(u_new, u_new_out);
+    return ORC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,530 @@
+"""B200-native ROCP hot path (randomized online CP decomposition, arXiv 2007.10798).
+
+The product is librocp_b200.so (CUDA, sm_100a) behind the C ABI in
+include/rocp_b200.h.  This module is a thin Python host mirror of the
+reference's C++ API (reference proj/include/rocp/*.hpp) over that ABI, used by
+the tests and bench.py.  There is no CPU fallback: if the shared library is
+missing or no GPU is present, calls fail loudly.
+
+Reference interfaces mirrored (file:line in /root/reference/proj):
+  draw_samples / sample_unfolding / sampled_khatri_rao   sampling.hpp:35-48
+  solve_gram / solve_sampled_ls                          solve.hpp:17-24
+  model_fitness                                          kruskal.hpp:38-39
+  cprand_decompose -> InitResult                         cprand.hpp:19-37
+  RocpStream (consume, model, state)                     rocp.hpp:85-107
+  update_last_mode_with / update_mode_with (replay)      rocp.hpp:52-75
+Matrices are numpy column-major (Fortran) arrays, like Eigen::MatrixXd.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import weakref
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "librocp_b200.so")
+
+# status codes (include/rocp_b200.h)
+OK, E_DOMAIN, E_NUMERICAL, E_CUDA, E_NCCL, E_OOM, E_STATE = range(7)
+
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+# Every symbol declared in include/rocp_b200.h: (name, restype, argtypes).
+SIGNATURES = [
+    ("rocp_create", C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
+    ("rocp_destroy", None, [_vp]),
+    ("rocp_last_error", C.c_char_p, [_vp]),
+    ("rocp_synchronize", C.c_int, [_vp]),
+    ("rocp_kernel_launches", C.c_uint64, [_vp]),
+    ("rocp_nccl_id_size", C.c_int, []),
+    ("rocp_nccl_get_unique_id", C.c_int, [_vp]),
+    ("rocp_tensor_create", C.c_int, [_vp, _i64p, C.c_int, _f64p, C.POINTER(_vp)]),
+    ("rocp_tensor_slab", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.POINTER(_vp)]),
+    ("rocp_tensor_free", None, [_vp]),
+    ("rocp_tensor_upload", C.c_int, [_vp, _vp, _f64p]),
+    ("rocp_tensor_download", C.c_int, [_vp, _vp, _f64p]),
+    ("rocp_tensor_device_ptr", _vp, [_vp]),
+    ("rocp_tensor_numel", C.c_int64, [_vp]),
+    ("rocp_generate_synthetic", C.c_int, [_vp, _vp, C.POINTER(_f64p), C.c_int, C.c_int,
+                                          C.c_double, C.c_uint64]),
+    ("rocp_draw_samples", C.c_int, [_vp, _i64p, C.c_int, C.c_int, C.c_int64, C.c_uint64,
+                                    C.c_uint32, C.c_uint32, _i64p, _i64p]),
+    ("rocp_decode_rows", C.c_int, [_vp, _i64p, C.c_int, C.c_int, _i64p, C.c_int64, _i64p]),
+    ("rocp_sample_unfolding", C.c_int, [_vp, _vp, C.c_int, _i64p, C.c_int64, _f64p]),
+    ("rocp_sampled_khatri_rao", C.c_int, [_vp, _i64p, C.c_int64, C.c_int, C.POINTER(_f64p),
+                                          _i64p, C.c_int, _f64p]),
+    ("rocp_gram", C.c_int, [_vp, _f64p, C.c_int64, C.c_int, _f64p]),
+    ("rocp_contract", C.c_int, [_vp, _f64p, C.c_int64, C.c_int64, _f64p, C.c_int, _f64p]),
+    ("rocp_solve_gram", C.c_int, [_vp, _f64p, _f64p, C.c_int64, C.c_int, _f64p,
+                                  C.POINTER(C.c_int)]),
+    ("rocp_solve_sampled_ls", C.c_int, [_vp, _f64p, _f64p, C.c_int64, C.c_int64, C.c_int, _f64p,
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("rocp_model_fitness", C.c_int, [_vp, _vp, C.POINTER(_f64p), C.c_int, _f64p]),
+    ("rocp_cprand", C.c_int, [_vp, _vp, C.c_int, C.c_int64, C.c_double, C.c_int, C.c_uint64,
+                              C.POINTER(_f64p), C.POINTER(_f64p), _f64p, C.POINTER(C.c_int),
+                              C.POINTER(C.c_int), C.POINTER(C.c_int), _f64p]),
+    ("rocp_stream_create", C.c_int, [_vp, C.c_int, _i64p, C.c_int, C.c_int64, C.c_int,
+                                     C.POINTER(_f64p), C.c_int64, C.POINTER(_f64p), C.c_int,
+                                     C.c_int64, C.POINTER(_vp)]),
+    ("rocp_stream_create_from_init", C.c_int, [_vp, C.c_int, C.c_int64, C.POINTER(_vp)]),
+    ("rocp_stream_free", None, [_vp]),
+    ("rocp_stream_consume", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32]),
+    ("rocp_stream_consume_host", C.c_int, [_vp, _f64p, C.c_int64, C.c_uint64, C.c_uint32]),
+    ("rocp_stream_consume_range", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                            C.c_uint32]),
+    ("rocp_stream_update_last_mode_with", C.c_int, [_vp, _vp, _i64p, C.c_int64, _f64p, _f64p,
+                                                    C.POINTER(C.c_int)]),
+    ("rocp_stream_append_temporal", C.c_int, [_vp, _f64p, C.c_int64]),
+    ("rocp_stream_update_mode_with", C.c_int, [_vp, _vp, _f64p, C.c_int, _i64p, C.c_int64, _f64p,
+                                               _f64p, C.POINTER(C.c_int)]),
+    ("rocp_stream_finish_batch", C.c_int, [_vp, C.c_int64]),
+    ("rocp_stream_get", C.c_int, [_vp, C.c_int, C.c_int, _f64p]),
+    ("rocp_stream_set", C.c_int, [_vp, C.c_int, C.c_int, _f64p]),
+    ("rocp_stream_t_len", C.c_int64, [_vp]),
+    ("rocp_stream_regularized", C.c_int, [_vp]),
+    ("rocp_stream_last_residuals", C.c_int, [_vp, _f64p]),
+    ("rocp_stream_checkpoint", C.c_int, [_vp]),
+    ("rocp_stream_restore", C.c_int, [_vp]),
+]
+
+
+def build(verbose=False):
+    """Compile librocp_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    r = subprocess.run(["make", "-C", _HERE], capture_output=not verbose, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("building librocp_b200.so failed:\n" + (r.stdout or "") + (r.stderr or ""))
+
+
+_lib = None
+
+
+def lib():
+    """Load librocp_b200.so; raise if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(make -C paper_2007_10798_b200); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class RocpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[rocp status {code}] {msg}")
+        self.code = code
+
+
+class DomainError(RocpError, ValueError):
+    """std::domain_error in the reference."""
+
+
+class NumericalError(RocpError):
+    """rocp::NumericalError (errors.hpp:10-20); carries the sweep."""
+
+    def __init__(self, code, msg, sweep=0):
+        super().__init__(code, msg)
+        self.sweep = sweep
+
+
+def _check(dev_handle, rc, sweep=0):
+    if rc == OK:
+        return
+    msg = lib().rocp_last_error(dev_handle)
+    msg = msg.decode() if msg else ""
+    if rc == E_DOMAIN:
+        raise DomainError(rc, msg)
+    if rc == E_NUMERICAL:
+        raise NumericalError(rc, msg, sweep)
+    raise RocpError(rc, msg)
+
+
+def _p(a, t=_f64p):
+    return a.ctypes.data_as(t)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _f64(a):
+    return np.asfortranarray(a, dtype=np.float64)
+
+
+def _ptr_array(mats):
+    arr = (_f64p * max(len(mats), 1))()
+    for k, m in enumerate(mats):
+        arr[k] = m.ctypes.data_as(_f64p)
+    return arr
+
+
+def auto_sample_count(rank):
+    """s = max(R, ceil(10 R ln R)) (sampling.cpp:40-45)."""
+    if rank < 1:
+        raise DomainError(E_DOMAIN, "rank must be positive")
+    return max(rank, int(np.ceil(10.0 * rank * np.log(float(rank)))))
+
+
+class Device:
+    """One handle per GPU (rocp_dev)."""
+
+    def __init__(self, device=0, world=1, rank=0, nccl_id=None):
+        h = C.c_void_p()
+        rc = lib().rocp_create(device, world, rank, nccl_id, C.byref(h))
+        if rc != OK:
+            raise RocpError(rc, f"rocp_create(device={device}) failed (is a GPU visible?)")
+        self.h = h
+        self._children = weakref.WeakSet()  # streams/tensors freed before the handle
+
+    def _adopt(self, obj):
+        self._children.add(obj)
+
+    def close(self):
+        if getattr(self, "h", None):
+            for ch in list(self._children):
+                ch._free()
+            lib().rocp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc, sweep=0):
+        _check(self.h, rc, sweep)
+
+    def synchronize(self):
+        self.check(lib().rocp_synchronize(self.h))
+
+    @property
+    def kernel_launches(self):
+        return int(lib().rocp_kernel_launches(self.h))
+
+    def tensor(self, dims, host=None):
+        return DeviceTensor(self, dims, host)
+
+
+class DeviceTensor:
+    """Device-resident DenseTensor (tensor.hpp:17-49), fp64, first index fastest."""
+
+    def __init__(self, dev, dims, host=None, _handle=None, _parent=None):
+        self.dev = dev
+        self.dims = [int(x) for x in dims]
+        self._parent = _parent
+        if _handle is not None:
+            self.h = _handle
+            dev._adopt(self)
+            return
+        d = _i64(self.dims)
+        h = C.c_void_p()
+        hp = None
+        if host is not None:
+            host = np.ascontiguousarray(host, dtype=np.float64).ravel(order="K")
+            if host.size != int(np.prod(self.dims)):
+                raise DomainError(E_DOMAIN, "data length does not match product of extents")
+            hp = _p(host)
+        dev.check(lib().rocp_tensor_create(dev.h, _p(d, _i64p), len(d), hp, C.byref(h)))
+        self.h = h
+        dev._adopt(self)
+
+    def _free(self):
+        if getattr(self, "h", None):
+            lib().rocp_tensor_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self._free()
+
+    @property
+    def numel(self):
+        return int(np.prod(self.dims))
+
+    def slab(self, t0, length):
+        h = C.c_void_p()
+        self.dev.check(lib().rocp_tensor_slab(self.dev.h, self.h, t0, length, C.byref(h)))
+        dims = list(self.dims)
+        dims[-1] = length
+        return DeviceTensor(self.dev, dims, _handle=h, _parent=self)
+
+    def download(self):
+        out = np.empty(self.numel, dtype=np.float64)
+        self.dev.check(lib().rocp_tensor_download(self.dev.h, self.h, _p(out)))
+        return out
+
+    def upload(self, host):
+        host = np.ascontiguousarray(host, dtype=np.float64).ravel(order="K")
+        self.dev.check(lib().rocp_tensor_upload(self.dev.h, self.h, _p(host)))
+
+    def generate(self, factors, snr_db=None, noise_seed=0):
+        """gen_synthetic semantics (synthetic.cpp:8-31) with the given factors."""
+        fs = [_f64(f) for f in factors]
+        self.dev.check(lib().rocp_generate_synthetic(
+            self.dev.h, self.h, _ptr_array(fs), fs[0].shape[1], 0 if snr_db is None else 1,
+            0.0 if snr_db is None else float(snr_db), noise_seed))
+
+
+# ---- primitives --------------------------------------------------------------
+def draw_samples(dev, dims, mode, s, seed, batch=0, iteration=0):
+    d = _i64(dims)
+    rows = np.zeros(max(s, 1), dtype=np.int64)
+    dec = np.zeros(max(s, 1) * (len(d) - 1), dtype=np.int64)
+    dev.check(lib().rocp_draw_samples(dev.h, _p(d, _i64p), len(d), mode, s, seed, batch, iteration,
+                                      _p(rows, _i64p), _p(dec, _i64p)))
+    return rows[:s], dec[: s * (len(d) - 1)].reshape(s, len(d) - 1)
+
+
+def decode_rows(dev, dims, mode, rows):
+    d, r = _i64(dims), _i64(rows)
+    dec = np.zeros(len(r) * (len(d) - 1), dtype=np.int64)
+    dev.check(lib().rocp_decode_rows(dev.h, _p(d, _i64p), len(d), mode, _p(r, _i64p), len(r),
+                                     _p(dec, _i64p)))
+    return dec.reshape(len(r), len(d) - 1)
+
+
+def sample_unfolding(dev, tensor, mode, rows):
+    r = _i64(rows)
+    out = np.zeros((tensor.dims[mode - 1], len(r)), order="F")
+    dev.check(lib().rocp_sample_unfolding(dev.h, tensor.h, mode, _p(r, _i64p), len(r), _p(out)))
+    return out
+
+
+def sampled_khatri_rao(dev, decoded, factors):
+    dec = _i64(decoded)
+    fs = [_f64(f) for f in factors]
+    R = fs[0].shape[1]
+    rows = _i64([f.shape[0] for f in fs])
+    z = np.zeros((dec.shape[0], R), order="F")
+    dev.check(lib().rocp_sampled_khatri_rao(dev.h, _p(dec, _i64p), dec.shape[0], len(fs),
+                                            _ptr_array(fs), _p(rows, _i64p), R, _p(z)))
+    return z
+
+
+def gram(dev, z):
+    z = _f64(z)
+    g = np.zeros((z.shape[1], z.shape[1]), order="F")
+    dev.check(lib().rocp_gram(dev.h, _p(z), z.shape[0], z.shape[1], _p(g)))
+    return g
+
+
+def contract(dev, x, z):
+    x, z = _f64(x), _f64(z)
+    out = np.zeros((x.shape[0], z.shape[1]), order="F")
+    dev.check(lib().rocp_contract(dev.h, _p(x), x.shape[0], x.shape[1], _p(z), z.shape[1], _p(out)))
+    return out
+
+
+def solve_gram(dev, g, rhs):
+    g, rhs = _f64(g), _f64(rhs)
+    if g.shape[0] != g.shape[1]:
+        raise DomainError(E_DOMAIN, "solve_gram: gram matrix must be square")
+    if rhs.shape[1] != g.shape[0]:
+        raise DomainError(E_DOMAIN, "solve_gram: rhs column count must match gram size")
+    out = np.zeros(rhs.shape, order="F")
+    reg = C.c_int(0)
+    dev.check(lib().rocp_solve_gram(dev.h, _p(g), _p(rhs), rhs.shape[0], g.shape[0], _p(out),
+                                    C.byref(reg)))
+    return out, bool(reg.value)
+
+
+def solve_sampled_ls(dev, z, x):
+    z, x = _f64(z), _f64(x)
+    if x.shape[1] != z.shape[0]:
+        raise DomainError(E_DOMAIN, "solve_sampled_ls: sample counts of z_s and x_s differ")
+    out = np.zeros((x.shape[0], z.shape[1]), order="F")
+    reg, und = C.c_int(0), C.c_int(0)
+    dev.check(lib().rocp_solve_sampled_ls(dev.h, _p(z), _p(x), z.shape[0], x.shape[0], z.shape[1],
+                                          _p(out), C.byref(reg), C.byref(und)))
+    return out, bool(reg.value), bool(und.value)
+
+
+def model_fitness(dev, tensor, factors):
+    fs = [_f64(f) for f in factors]
+    fit = C.c_double(0)
+    dev.check(lib().rocp_model_fitness(dev.h, tensor.h, _ptr_array(fs), fs[0].shape[1],
+                                       C.byref(fit)))
+    return fit.value
+
+
+# ---- cprand / stream -----------------------------------------------------------
+class InitResult:
+    """InitResult (cprand.hpp:19-26)."""
+
+    def __init__(self, model, best_sampled_kr, best_fitness, iterations, regularized, fit_trace,
+                 samples):
+        self.model = model
+        self.best_sampled_kr = best_sampled_kr
+        self.best_sampled_factors = [model[n] for n in range(len(model) - 1)]
+        self.best_fitness = best_fitness
+        self.iterations = iterations
+        self.regularized = regularized
+        self.fit_trace = fit_trace
+        self.samples = samples
+
+
+def cprand_decompose(dev, tensor, rank, init_factors, seed, samples=0, tol=1e-4, max_iters=100):
+    """cprand_decompose (cprand.cpp:12-69); init_factors = random_model(...) output."""
+    N = len(tensor.dims)
+    fs = [np.array(f, dtype=np.float64, order="F", copy=True) for f in init_factors]
+    s = samples if samples > 0 else auto_sample_count(rank)
+    kr = [np.zeros((s, rank), order="F") for _ in range(N - 1)]
+    best, iters, reg, errs = C.c_double(0), C.c_int(0), C.c_int(0), C.c_int(0)
+    trace = np.zeros(max(max_iters, 1))
+    rc = lib().rocp_cprand(dev.h, tensor.h, rank, samples, tol, max_iters, seed, _ptr_array(fs),
+                           _ptr_array(kr), C.byref(best), C.byref(iters), C.byref(reg),
+                           C.byref(errs), _p(trace))
+    dev.check(rc, sweep=errs.value)
+    return InitResult(fs, kr, best.value, iters.value, bool(reg.value), trace[: iters.value], s)
+
+
+class RocpStream:
+    """RocpStream (rocp.hpp:85-107), device-resident state."""
+
+    def __init__(self, dev, init=None, s=None, literal_init=False, t_capacity=0,
+                 from_device_init=False):
+        self.dev = dev
+        h = C.c_void_p()
+        if from_device_init:
+            dev.check(lib().rocp_stream_create_from_init(dev.h, int(literal_init), t_capacity,
+                                                         C.byref(h)))
+            self.h = h
+            dev._adopt(self)
+            self.order = int(init.order) if hasattr(init, "order") else None
+            self._shape_from(init)
+            return
+        model = init.model
+        self.order = len(model)
+        self.rank = model[0].shape[1]
+        self.head = [m.shape[0] for m in model[:-1]]
+        s = init.samples if s is None else s
+        fs = [_f64(f) for f in model]
+        kr = [_f64(z) for z in init.best_sampled_kr]
+        for z in kr:
+            if z.shape[0] != s:
+                raise DomainError(E_DOMAIN, "init_state: sampled Khatri-Rao row count differs from s")
+        hd = _i64(self.head)
+        t_init = model[-1].shape[0]
+        dev.check(lib().rocp_stream_create(dev.h, self.order, _p(hd, _i64p), self.rank, s,
+                                           int(literal_init), _ptr_array(fs), t_init,
+                                           _ptr_array(kr), int(init.regularized),
+                                           max(t_capacity, t_init), C.byref(h)))
+        self.h = h
+        self.s = s
+        dev._adopt(self)
+
+    def _shape_from(self, init):
+        model = init.model
+        self.order = len(model)
+        self.rank = model[0].shape[1]
+        self.head = [m.shape[0] for m in model[:-1]]
+        self.s = init.samples
+
+    def _free(self):
+        if getattr(self, "h", None):
+            lib().rocp_stream_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self._free()
+
+    def _check_mode(self, mode):
+        if not 1 <= mode < self.order:
+            raise DomainError(E_DOMAIN, "update_mode_with: index set must be over a non-temporal mode")
+
+    def consume(self, x_new, seed, batch_id):
+        if isinstance(x_new, DeviceTensor):
+            self.dev.check(lib().rocp_stream_consume(self.h, x_new.h, seed, batch_id))
+        else:
+            x = np.ascontiguousarray(x_new, dtype=np.float64).ravel(order="K")
+            head = int(np.prod(self.head))
+            if x.size % head:
+                raise DomainError(E_DOMAIN, "batch head extents do not match stream")
+            self.dev.check(lib().rocp_stream_consume_host(self.h, _p(x), x.size // head, seed,
+                                                          batch_id))
+
+    def consume_range(self, x, t0, batch, nb, seed, first_batch_id):
+        self.dev.check(lib().rocp_stream_consume_range(self.h, x.h, t0, batch, nb, seed,
+                                                       first_batch_id))
+
+    def update_last_mode_with(self, x_new, rows):
+        r = _i64(rows)
+        B = x_new.dims[-1]
+        u = np.zeros((B, self.rank), order="F")
+        z = np.zeros((len(r), self.rank), order="F")
+        reg = C.c_int(0)
+        self.dev.check(lib().rocp_stream_update_last_mode_with(self.h, x_new.h, _p(r, _i64p), len(r),
+                                                               _p(u), _p(z), C.byref(reg)))
+        return u, z, bool(reg.value)
+
+    def append_temporal(self, u_new):
+        u = _f64(u_new)
+        self.dev.check(lib().rocp_stream_append_temporal(self.h, _p(u), u.shape[0]))
+
+    def update_mode_with(self, x_new, u_new, mode, rows):
+        self._check_mode(mode)
+        r = _i64(rows)
+        u = _f64(u_new)
+        z = np.zeros((len(r), self.rank), order="F")
+        xs = np.zeros((self.head[mode - 1], len(r)), order="F")
+        reg = C.c_int(0)
+        self.dev.check(lib().rocp_stream_update_mode_with(self.h, x_new.h, _p(u), mode, _p(r, _i64p),
+                                                          len(r), _p(z), _p(xs), C.byref(reg)))
+        return z, xs, bool(reg.value)
+
+    def finish_batch(self, batch):
+        self.dev.check(lib().rocp_stream_finish_batch(self.h, batch))
+
+    def _get(self, what, mode, shape):
+        out = np.zeros(shape, order="F")
+        self.dev.check(lib().rocp_stream_get(self.h, what, mode, _p(out)))
+        return out
+
+    def factor(self, mode):
+        return self._get(0, mode, (self.head[mode - 1], self.rank))
+
+    def p(self, mode):
+        return self._get(1, mode, (self.head[mode - 1], self.rank))
+
+    def q(self, mode):
+        return self._get(2, mode, (self.rank, self.rank))
+
+    def temporal(self):
+        return self._get(3, 0, (self.t_len, self.rank))
+
+    def set(self, what, mode, arr):
+        a = _f64(arr)
+        self.dev.check(lib().rocp_stream_set(self.h, what, mode, _p(a)))
+
+    def model(self):
+        """RocpStream::model (rocp.cpp:162-168)."""
+        return [self.factor(n) for n in range(1, self.order)] + [self.temporal()]
+
+    @property
+    def t_len(self):
+        return int(lib().rocp_stream_t_len(self.h))
+
+    @property
+    def regularized(self):
+        return bool(lib().rocp_stream_regularized(self.h))
+
+    def last_residuals(self):
+        out = np.zeros(self.order)
+        self.dev.check(lib().rocp_stream_last_residuals(self.h, _p(out)))
+        return out
+
+    def checkpoint(self):
+        self.dev.check(lib().rocp_stream_checkpoint(self.h))
+
+    def restore(self):
+        self.dev.check(lib().rocp_stream_restore(self.h))

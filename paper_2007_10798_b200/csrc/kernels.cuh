@@ -1,0 +1,694 @@
+// kernels.cuh -- sm_100a kernels of the ROCP sampled-update hot path.
+//
+// Every floating-point result follows the canonical operation order of
+// DESIGN.md section 3 so the CPU oracle (oracle/, an independent
+// implementation) reproduces it bit for bit.  Compiled with -fmad=false: the
+// only fused multiply-adds are the explicit __fma_rn calls below.
+//
+// Device layouts:
+//   tensor   float64, first index fastest (reference tensor.hpp:14-16)
+//   factors, P, temporal factor, Z_s: row-major (row i's R values contiguous)
+//   X_s      I_n x S column-major, column c = sampled fibre c (the reference's
+//            sample_unfolding output, sampling.cpp:66-77)
+//   idx      S x (N-1) int32 0-based co-mode indices, increasing mode order
+//   base     S int64 flat offset of each sampled fibre's first element
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rocpk {
+
+constexpr int kMaxOrder = 8;
+constexpr int kChunk = 32;       // canonical sample-reduction chunk
+constexpr int kGroup = 256;      // canonical hsum group
+constexpr double kGramConditionLimit = 1e12;  // reference solve.hpp:15
+
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Counter RNG: Philox4x32-10, key bumped after each round (equivalent to the
+// published bump-before-rounds-1..9 schedule).
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c[0];
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * c[2];
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0;
+        const uint32_t n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1: draw (or decode explicit rows) + Eq.(1) decode + fibre base offset.
+// Replaces draw_samples / SampleIndexSet::from_rows / decode_index
+// (sampling.cpp:11-55, tensor.cpp:96-109).
+struct DrawJob {
+    uint64_t seed;
+    uint32_t batch, iteration, mode;  // mode 1-based
+    int n_other;
+    int32_t s;
+    int64_t co;                    // co-domain size
+    int64_t ext[kMaxOrder];        // co-mode extents, increasing mode order
+    int64_t tstride[kMaxOrder];    // tensor strides of the co-modes
+    const int64_t* in_rows;        // explicit 1-based rows (replay) or nullptr (draw)
+    int64_t* rows;                 // optional 1-based output
+    int32_t* idx;                  // s x n_other, 0-based
+    int64_t* base;                 // s
+};
+struct DrawBatch {
+    int njobs;
+    DrawJob job[kMaxOrder];
+};
+
+__global__ void k_draw(const DrawBatch b) {
+    const DrawJob& J = b.job[blockIdx.y];
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < J.s; c += gridDim.x * blockDim.x) {
+        int64_t j0;
+        if (J.in_rows) {
+            j0 = J.in_rows[c] - 1;
+        } else {
+            uint32_t ctr[4] = {uint32_t(c), J.mode, J.iteration, J.batch};
+            philox4x32_10(ctr, uint32_t(J.seed), uint32_t(J.seed >> 32));
+            const uint64_t u = uint64_t(ctr[0]) | (uint64_t(ctr[1]) << 32);
+            j0 = int64_t(__umul64hi(u, uint64_t(J.co)));
+        }
+        if (J.rows) J.rows[c] = j0 + 1;
+        int64_t rem = j0, base = 0;
+        for (int k = 0; k < J.n_other; ++k) {
+            const int64_t e = J.ext[k];
+            const int64_t q = rem / e;
+            const int64_t ik = rem - q * e;
+            rem = q;
+            J.idx[int64_t(c) * J.n_other + k] = int32_t(ik);
+            base += ik * J.tstride[k];
+        }
+        J.base[c] = base;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: sampled-fibre gather, X_s(i, c) = T[base_c + i * ms].  Replaces
+// sample_unfolding (sampling.cpp:57-79).  Grid-stride over (i, c) with i
+// fastest: coalesced writes, coalesced reads for the contiguous mode-1 fibres,
+// and UNROLL independent loads in flight per thread for the strided modes
+// (each element its own 32-B sector).
+struct GatherJob {
+    const double* t;
+    const int64_t* base;
+    int64_t ms;  // mode stride
+    int32_t I;   // fibre length (I_n)
+    int32_t s;
+    double* out;
+};
+struct GatherBatch {
+    int njobs;
+    GatherJob job[kMaxOrder];
+};
+
+template <int UNROLL>
+__global__ void __launch_bounds__(256) k_gather(const GatherBatch b) {
+    const GatherJob& J = b.job[blockIdx.y];
+    const uint32_t total = uint32_t(J.I) * uint32_t(J.s);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * UNROLL) {
+        double v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const uint32_t e = e0 + u * stride;
+            if (e < total) {
+                const uint32_t c = e / uint32_t(J.I);
+                const uint32_t i = e - c * uint32_t(J.I);
+                v[u] = __ldg(J.t + J.base[c] + int64_t(i) * J.ms);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const uint32_t e = e0 + u * stride;
+            if (e < total) J.out[e] = v[u];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: sampled Khatri-Rao, Z(c, r) = 1.0 * F_0(i_0(c), r) * F_1(...) * ...
+// factors in factors_excluding order (decreasing mode), left to right exactly
+// as sampled_khatri_rao (sampling.cpp:90-103).  Factors row-major.
+struct SkrJob {
+    const int32_t* idx;
+    int n_other;
+    int32_t s;
+    int R;
+    const double* f[kMaxOrder];
+    double* z;  // s x R row-major
+};
+
+__global__ void k_skr(const SkrJob J) {
+    const int32_t total = J.s * J.R;
+    for (int32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int32_t c = e / J.R;
+        const int32_t r = e - c * J.R;
+        double z = 1.0;
+        for (int l = 0; l < J.n_other; ++l) {
+            const int k = J.n_other - 1 - l;
+            const int32_t i = J.idx[int64_t(c) * J.n_other + k];
+            z = z * J.f[l][int64_t(i) * J.R + r];
+        }
+        J.z[e] = z;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Last-block combine helper: returns true in exactly one block, after all
+// blocks' global writes are visible.  Resets the counter for reuse (graph
+// safe, one kernel at a time per counter).
+__device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(counter, 1u);
+        is_last = (prev == gridDim.x * gridDim.y * gridDim.z - 1);
+        if (is_last) *counter = 0u;
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
+// ---------------------------------------------------------------------------
+// K4a: Gram G = Z^T Z (solve.cpp:41, rocp.cpp:108) in the canonical chunked
+// order.  One block per 32-sample chunk writes its R x R chunk partials; the
+// last block sums them in increasing chunk order and optionally accumulates
+// (Q + G, rocp.cpp:108).
+__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int32_t s, int R,
+                                              double* __restrict__ partial, unsigned int* counter,
+                                              const double* acc_base, double* __restrict__ out) {
+    extern __shared__ double zs[];  // kChunk x R
+    const int k = blockIdx.x;
+    const int c0 = k * kChunk;
+    const int cn = min(kChunk, s - c0);
+    for (int t = threadIdx.x; t < kChunk * R; t += blockDim.x) {
+        const int cc = t / R;
+        zs[t] = (cc < cn) ? Z[int64_t(c0) * R + t] : 0.0;
+    }
+    __syncthreads();
+    const int RR = R * R;
+    for (int p = threadIdx.x; p < RR; p += blockDim.x) {
+        const int r1 = p % R, r2 = p / R;
+        double acc = 0.0;
+        for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zs[cc * R + r1], zs[cc * R + r2], acc);
+        partial[int64_t(k) * RR + p] = acc;
+    }
+    if (!last_block_arrive(counter)) return;
+    const int nk = gridDim.x;
+    for (int p = threadIdx.x; p < RR; p += blockDim.x) {
+        const volatile double* vp = partial;
+        double tot = vp[p];
+        for (int kk = 1; kk < nk; ++kk) tot = tot + vp[int64_t(kk) * RR + p];
+        out[p] = acc_base ? acc_base[p] + tot : tot;  // column-major == row-major (symmetric)
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4b: skinny contraction out = X_s Z (I x S times S x R; solve.cpp:42,
+// rocp.cpp:107), canonical chunked order, optionally out = base + X_s Z.
+// Thread per (row i, RB consecutive r); Z chunk staged in shared memory
+// (broadcast reads); X_s loads coalesced along i.
+template <int RB>
+__global__ void __launch_bounds__(128) k_contract(const double* __restrict__ X, int32_t I, int32_t s,
+                                                  const double* __restrict__ Z, int R,
+                                                  const double* base, double* __restrict__ out) {
+    __shared__ double zs[kChunk][RB];
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r0 = blockIdx.y * RB;
+    double tot[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) tot[j] = 0.0;
+    for (int32_t c0 = 0; c0 < s; c0 += kChunk) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kChunk * RB; t += blockDim.x) {
+            const int cc = t / RB, rr = t % RB;
+            zs[cc][rr] = (c0 + cc < s && r0 + rr < R) ? Z[int64_t(c0 + cc) * R + r0 + rr] : 0.0;
+        }
+        __syncthreads();
+        double p[RB];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) p[j] = 0.0;
+        const int cn = min(kChunk, s - c0);
+        if (i < I) {
+            const double* xc = X + int64_t(c0) * I + i;
+            if (cn == kChunk) {
+#pragma unroll 8
+                for (int cc = 0; cc < kChunk; ++cc) {
+                    const double x = __ldg(xc + int64_t(cc) * I);
+#pragma unroll
+                    for (int j = 0; j < RB; ++j) p[j] = __fma_rn(x, zs[cc][j], p[j]);
+                }
+            } else {
+                for (int cc = 0; cc < cn; ++cc) {
+                    const double x = __ldg(xc + int64_t(cc) * I);
+#pragma unroll
+                    for (int j = 0; j < RB; ++j) p[j] = __fma_rn(x, zs[cc][j], p[j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) tot[j] = (c0 == 0) ? p[j] : tot[j] + p[j];
+    }
+    if (i < I) {
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const int r = r0 + j;
+            if (r < R) {
+                const int64_t o = int64_t(i) * R + r;
+                out[o] = base ? base[o] + tot[j] : tot[j];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: solve_gram (solve.cpp:9-35), canonical form:
+// zero solution if max diag <= 0; unpivoted LDL^T; regularize with
+// 1e-12 tr(G) when a pivot is <= 0 or max/min pivot > 1e12; then per row
+// forward (increasing k), diagonal, backward (decreasing k) substitution.
+// Every block factors G redundantly in shared memory and solves its rows.
+// flags[0] |= 1 if regularized; flags[1] = nonfinite_code if any output is
+// not finite (cprand's NumericalError check, cprand.cpp:42-43).
+template <int MAXR>
+__global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int R,
+                                               const double* __restrict__ RHS, int32_t rows,
+                                               double* __restrict__ OUT, int* flags,
+                                               int nonfinite_code) {
+    // A holds the working lower triangle (A[i][j], i >= j); the strict upper
+    // triangle stores the multipliers, L(i, k) at A[k][i] (never touched by
+    // the trailing updates, which only write i >= j > k).
+    __shared__ double A[MAXR][MAXR + 1];
+    __shared__ double D[MAXR];
+    __shared__ int s_mode;  // 0 = zero solution, 1 = solve
+    __shared__ int s_reg;
+    const int tid = threadIdx.x;
+
+    auto load = [&](double lambda) {
+        for (int t = tid; t < R * R; t += blockDim.x) {
+            const int i = t % R, j = t / R;
+            if (i >= j) A[i][j] = (i == j) ? G[t] + lambda : G[t];
+        }
+    };
+    auto factor = [&]() {
+        for (int k = 0; k < R; ++k) {
+            __syncthreads();
+            const double dk = A[k][k];
+            for (int i = k + 1 + tid; i < R; i += blockDim.x)
+                A[k][i] = (dk != 0.0) ? A[i][k] / dk : 0.0;
+            if (tid == 0) D[k] = dk;
+            __syncthreads();
+            const int m = R - k - 1;  // trailing size
+            for (int t = tid; t < m * m; t += blockDim.x) {
+                const int i = k + 1 + t % m, j = k + 1 + t / m;
+                if (j <= i) A[i][j] = __fma_rn(-A[k][i], A[j][k], A[i][j]);
+            }
+        }
+        __syncthreads();
+    };
+
+    if (tid == 0) {
+        double maxdiag = G[0];
+        for (int k = 1; k < R; ++k)
+            if (G[k * R + k] > maxdiag) maxdiag = G[k * R + k];
+        s_mode = (maxdiag <= 0.0) ? 0 : 1;
+        s_reg = (s_mode == 0) ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_mode == 1) {
+        load(0.0);
+        factor();
+        if (tid == 0) {
+            double dmin = D[0], dmax = D[0];
+            for (int k = 0; k < R; ++k) {
+                if (D[k] < dmin) dmin = D[k];
+                if (D[k] > dmax) dmax = D[k];
+            }
+            s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+        }
+        __syncthreads();
+        if (s_reg) {
+            double tr = G[0];
+            for (int k = 1; k < R; ++k) tr = tr + G[k * R + k];
+            load(1e-12 * tr);
+            factor();
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0 && s_reg && flags) atomicOr(flags, 1);
+
+    const int32_t row = blockIdx.x * blockDim.x + tid;
+    if (row >= rows) return;
+    double w[MAXR];
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j) w[j] = (j < R) ? RHS[int64_t(row) * R + j] : 0.0;
+    bool finite = true;
+    if (s_mode == 0) {
+#pragma unroll
+        for (int j = 0; j < MAXR; ++j) w[j] = 0.0;
+    } else {
+        // forward: w[j] -= L(j,k) w[k], k increasing (same bits as the row-wise
+        // oracle loop); L(j,k) = A[k][j]
+#pragma unroll
+        for (int k = 0; k < MAXR; ++k) {
+            if (k < R) {
+#pragma unroll
+                for (int j = k + 1; j < MAXR; ++j)
+                    if (j < R) w[j] = __fma_rn(-A[k][j], w[k], w[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < MAXR; ++j) {
+            if (j < R) {
+                const double dj = D[j];
+                w[j] = (fabs(dj) > 2.2250738585072014e-308) ? w[j] / dj : 0.0;
+            }
+        }
+        // backward: w[j] -= L(k,j) w[k], k decreasing; L(k,j) = A[j][k]
+#pragma unroll
+        for (int k = MAXR - 1; k >= 0; --k) {
+            if (k < R) {
+#pragma unroll
+                for (int j = 0; j < k; ++j) w[j] = __fma_rn(-A[j][k], w[k], w[j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j) {
+        if (j < R) {
+            OUT[int64_t(row) * R + j] = w[j];
+            finite = finite && isfinite(w[j]);
+        }
+    }
+    if (!finite && flags) flags[1] = nonfinite_code;
+}
+
+// ---------------------------------------------------------------------------
+// Warp / group reductions of the canonical fitness order.
+__device__ __forceinline__ double butterfly32(double q) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) q = q + __shfl_xor_sync(0xffffffffu, q, off);
+    return q;
+}
+
+// Sum of v[0..n) (n <= 256, missing = +0.0) by one warp: lane-strided then butterfly.
+// GLOBAL = true reads through L2 (__ldcg): the values may have been written by
+// other blocks.  GLOBAL = false for shared-memory input.
+template <bool GLOBAL>
+__device__ __forceinline__ double ld_sum(const double* p) {
+    if constexpr (GLOBAL) return __ldcg(p);
+    else return *p;
+}
+template <bool GLOBAL>
+__device__ __forceinline__ double group_sum256_warp(const double* v, int n, int lane) {
+    double q = (lane < n) ? ld_sum<GLOBAL>(v + lane) : 0.0;
+#pragma unroll
+    for (int m = 1; m < 8; ++m) {
+        const int t = lane + 32 * m;
+        q = q + ((t < n) ? ld_sum<GLOBAL>(v + t) : 0.0);
+    }
+    return butterfly32(q);
+}
+
+// hsum of v[0..n) in place by one block (8 warps); result in v[0].  v is
+// global scratch (n entries) visible to this block.
+__device__ void block_hsum_inplace(double* v, int64_t n, double* tmp) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    while (n > 1) {
+        const int64_t ng = (n + kGroup - 1) / kGroup;
+        for (int64_t g = warp; g < ng; g += nw) {
+            const double r = group_sum256_warp<true>(v + g * kGroup, int(min64(kGroup, n - g * kGroup)), lane);
+            if (lane == 0) tmp[g] = r;
+        }
+        __syncthreads();
+        __threadfence_block();
+        for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) v[g] = tmp[g];
+        __syncthreads();
+        __threadfence_block();
+        n = ng;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7: fused fitness, sum over the tensor of (x_hat - x)^2 (with_model) or x^2,
+// never materialising x_hat or the full Khatri-Rao product (replaces
+// reconstruct + fitness, kruskal.cpp:55-89).  Block = 256 threads handles a
+// group of 256 mode-1 fibres: w_j (the KR row of fibre j) in shared memory,
+// each warp runs 8 fibres at a time with lanes over i1 (U1 row reused across
+// the 8 fibres), butterfly per fibre, group_sum256 per group; the last block
+// reduces the group partials with hsum.
+struct FitJob {
+    const double* t;
+    int64_t I1;
+    int64_t nfib;
+    int N;
+    int R;
+    int with_model;
+    const double* U[kMaxOrder];  // row-major factors (U[0] = mode 1)
+    int64_t dims[kMaxOrder];
+    double* group_partial;  // ngroups
+    double* group_tmp;      // ngroups
+    unsigned int* counter;
+    double* out;            // 1 value
+};
+
+constexpr int kFitFibres = 8;
+
+__global__ void __launch_bounds__(256) k_fitness(const FitJob J) {
+    extern __shared__ double smem[];
+    double* W = smem;                       // 256 x R
+    double* F = smem + kGroup * J.R;        // 256
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ngroups = (J.nfib + kGroup - 1) / kGroup;
+    for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int64_t j0 = g * kGroup;
+        __syncthreads();
+        if (J.with_model) {
+            const int64_t j = j0 + threadIdx.x;
+            if (j < J.nfib) {
+                int64_t idx[kMaxOrder];
+                int64_t rem = j;
+                for (int m = 1; m < J.N; ++m) {
+                    const int64_t q = rem / J.dims[m];
+                    idx[m] = rem - q * J.dims[m];
+                    rem = q;
+                }
+                for (int r = 0; r < J.R; ++r) {
+                    double acc = J.U[J.N - 1][idx[J.N - 1] * J.R + r];
+                    for (int m = J.N - 2; m >= 1; --m) acc = acc * J.U[m][idx[m] * J.R + r];
+                    W[threadIdx.x * J.R + r] = acc;
+                }
+            }
+        }
+        __syncthreads();
+        for (int pass = 0; pass < 32 / kFitFibres; ++pass) {
+            const int jj = warp * 32 + pass * kFitFibres;
+            double acc[kFitFibres];
+#pragma unroll
+            for (int q = 0; q < kFitFibres; ++q) acc[q] = 0.0;
+            int nv = int(min64(kFitFibres, J.nfib - (j0 + jj)));
+            if (nv > 0) {
+                for (int64_t i1 = lane; i1 < J.I1; i1 += 32) {
+                    double x[kFitFibres], xh[kFitFibres];
+#pragma unroll
+                    for (int q = 0; q < kFitFibres; ++q) {
+                        x[q] = (q < nv) ? __ldcs(J.t + (j0 + jj + q) * J.I1 + i1) : 0.0;
+                        xh[q] = 0.0;
+                    }
+                    if (J.with_model) {
+                        const double* u = J.U[0] + i1 * J.R;
+                        for (int r = 0; r < J.R; ++r) {
+                            const double ur = __ldg(u + r);
+#pragma unroll
+                            for (int q = 0; q < kFitFibres; ++q)
+                                xh[q] = __fma_rn(ur, W[(jj + q) * J.R + r], xh[q]);
+                        }
+#pragma unroll
+                        for (int q = 0; q < kFitFibres; ++q) {
+                            const double d = xh[q] - x[q];
+                            acc[q] = __fma_rn(d, d, acc[q]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < kFitFibres; ++q) acc[q] = __fma_rn(x[q], x[q], acc[q]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kFitFibres; ++q) {
+                const double f = butterfly32(acc[q]);
+                if (lane == 0) F[jj + q] = (q < nv) ? f : 0.0;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int n = int(min64(kGroup, J.nfib - j0));
+            const double r = group_sum256_warp<false>(F, n, lane);
+            if (lane == 0) J.group_partial[g] = r;
+        }
+    }
+    if (!last_block_arrive(J.counter)) return;
+    block_hsum_inplace(J.group_partial, ngroups, J.group_tmp);
+    if (threadIdx.x == 0) *J.out = J.group_partial[0];
+}
+
+// ---------------------------------------------------------------------------
+// Sampled residual |X_s - U Z^T|^2 and |X_s|^2, one warp per
+// sample column; partials per column, last block hsums both.
+struct ResidJob {
+    const double* X;  // I x S col-major
+    const double* U;  // I x R row-major
+    const double* Z;  // S x R row-major
+    int32_t I, S;
+    int R;
+    double* col_num;  // S
+    double* col_den;  // S
+    double* tmp;      // S
+    unsigned int* counter;
+    double* out;      // 2 values: num, den
+};
+
+__global__ void __launch_bounds__(256) k_residual(const ResidJob J) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    for (int32_t c = blockIdx.x * nw + warp; c < J.S; c += gridDim.x * nw) {
+        double qn = 0.0, qd = 0.0;
+        const double* z = J.Z + int64_t(c) * J.R;
+        for (int32_t i = lane; i < J.I; i += 32) {
+            double uz = 0.0;
+            const double* u = J.U + int64_t(i) * J.R;
+            for (int r = 0; r < J.R; ++r) uz = __fma_rn(u[r], z[r], uz);
+            const double xv = J.X[int64_t(c) * J.I + i];
+            const double e = xv - uz;
+            qn = __fma_rn(e, e, qn);
+            qd = __fma_rn(xv, xv, qd);
+        }
+        qn = butterfly32(qn);
+        qd = butterfly32(qd);
+        if (lane == 0) {
+            J.col_num[c] = qn;
+            J.col_den[c] = qd;
+        }
+    }
+    if (!last_block_arrive(J.counter)) return;
+    block_hsum_inplace(J.col_num, J.S, J.tmp);
+    block_hsum_inplace(J.col_den, J.S, J.tmp);
+    if (threadIdx.x == 0) {
+        J.out[0] = J.col_num[0];
+        J.out[1] = J.col_den[0];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// init_state (rocp.cpp:57-64): P = U Q, P[i][r] = fma chain over k from +0.0.
+__global__ void k_mul_uq(const double* __restrict__ U, int32_t I, int R, const double* __restrict__ Q,
+                         double* __restrict__ P) {
+    const int64_t total = int64_t(I) * R;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e / R;
+        const int r = int(e - i * R);
+        double acc = 0.0;
+        for (int k = 0; k < R; ++k) acc = __fma_rn(U[i * R + k], Q[k * R + r], acc);
+        P[e] = acc;
+    }
+}
+
+// Row-major <-> column-major transpose of an I x R matrix.
+__global__ void k_transpose(const double* __restrict__ in, int64_t rows, int64_t cols,
+                            double* __restrict__ out) {
+    // in: rows x cols row-major -> out: rows x cols column-major
+    const int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e / cols, j = e - i * cols;
+        out[j * rows + i] = in[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic data (gen_synthetic semantics, synthetic.cpp:8-31): signal in the
+// canonical x_hat order, Philox/Box-Muller noise keyed by the flat index,
+// deterministic fixed-grid norm partials.
+struct SynJob {
+    double* t;
+    int64_t numel;
+    int64_t I1;
+    int N, R;
+    const double* U[kMaxOrder];
+    int64_t dims[kMaxOrder];
+    uint64_t seed;
+    double* part_sig;    // gridDim.x
+    double* part_noise;  // gridDim.x
+};
+
+__device__ __forceinline__ double noise_at(uint64_t seed, int64_t e) {
+    uint32_t c[4] = {uint32_t(uint64_t(e)), uint32_t(uint64_t(e) >> 32), 0x6e6f6973u, 0u};
+    philox4x32_10(c, uint32_t(seed), uint32_t(seed >> 32));
+    const uint64_t a = (uint64_t(c[0]) | (uint64_t(c[1]) << 32)) >> 11;
+    const uint64_t b = (uint64_t(c[2]) | (uint64_t(c[3]) << 32)) >> 11;
+    const double u1 = 1.0 - double(a) * 0x1.0p-53;  // (0, 1]
+    const double u2 = double(b) * 0x1.0p-53;
+    return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+__global__ void __launch_bounds__(256) k_synth_signal(const SynJob J) {
+    __shared__ double red_s[256], red_n[256];
+    double ps = 0.0, pn = 0.0;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < J.numel; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i1 = e % J.I1;
+        int64_t rem = e / J.I1;
+        int64_t idx[kMaxOrder];
+        for (int m = 1; m < J.N; ++m) {
+            const int64_t q = rem / J.dims[m];
+            idx[m] = rem - q * J.dims[m];
+            rem = q;
+        }
+        double xh = 0.0;
+        for (int r = 0; r < J.R; ++r) {
+            double w = J.U[J.N - 1][idx[J.N - 1] * J.R + r];
+            for (int m = J.N - 2; m >= 1; --m) w = w * J.U[m][idx[m] * J.R + r];
+            xh = __fma_rn(J.U[0][i1 * J.R + r], w, xh);
+        }
+        J.t[e] = xh;
+        ps = __fma_rn(xh, xh, ps);
+        if (J.part_noise) {
+            const double n = noise_at(J.seed, e);
+            pn = __fma_rn(n, n, pn);
+        }
+    }
+    red_s[threadIdx.x] = ps;
+    red_n[threadIdx.x] = pn;
+    __syncthreads();
+    for (int off = 128; off >= 1; off >>= 1) {
+        if (threadIdx.x < off) {
+            red_s[threadIdx.x] = red_s[threadIdx.x] + red_s[threadIdx.x + off];
+            red_n[threadIdx.x] = red_n[threadIdx.x] + red_n[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        J.part_sig[blockIdx.x] = red_s[0];
+        if (J.part_noise) J.part_noise[blockIdx.x] = red_n[0];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_synth_noise(double* t, int64_t numel, uint64_t seed,
+                                                     const double* scale_ptr) {
+    const double scale = *scale_ptr;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < numel; e += int64_t(gridDim.x) * blockDim.x)
+        t[e] = t[e] + scale * noise_at(seed, e);
+}
+
+}  // namespace rocpk

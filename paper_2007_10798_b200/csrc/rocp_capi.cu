@@ -1,0 +1,1345 @@
+// rocp_capi.cu -- host orchestration of the B200 ROCP hot path behind the
+// C ABI declared in include/rocp_b200.h.
+//
+// One rocp_dev per GPU owns a CUDA stream, pooled counters/flags and the
+// device-resident result of the last cprand.  rocp_stream owns every device
+// buffer the online update needs (factors, P/Q, temporal factor, per-stage
+// index/gather/KR scratch), allocated once at creation: consume never
+// allocates (reference contract: constant state footprint, test_rocp.cpp:258-267).
+//
+// Control flow mirrors the reference line by line (citations inline); the
+// arithmetic lives in kernels.cuh.
+
+#include "../../include/rocp_b200.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+using namespace rocpk;
+
+namespace {
+
+struct RocpError {
+    rocp_status code;
+    std::string msg;
+    int sweep = 0;
+};
+
+[[noreturn]] void throw_domain(const std::string& m) { throw RocpError{ROCP_E_DOMAIN, m}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation)
+            throw RocpError{ROCP_E_OOM, std::string(what) + ": " + cudaGetErrorString(e)};
+        throw RocpError{ROCP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+// Owning device buffer.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    }
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+int64_t prod(const std::vector<int64_t>& d) {
+    int64_t n = 1;
+    for (int64_t x : d) n *= x;
+    return n;
+}
+
+int64_t auto_sample_count(int rank) {  // sampling.cpp:40-45
+    if (rank < 1) throw_domain("rank must be positive");
+    const double s = 10.0 * rank * std::log(double(rank));
+    return std::max<int64_t>(rank, int64_t(std::ceil(s)));
+}
+
+std::vector<int64_t> strides_of(const std::vector<int64_t>& d) {  // tensor.cpp:68-76
+    std::vector<int64_t> s(d.size());
+    int64_t acc = 1;
+    for (size_t k = 0; k < d.size(); ++k) { s[k] = acc; acc *= d[k]; }
+    return s;
+}
+
+// Host column-major <-> device row-major conversions.
+std::vector<double> colmajor_to_rowmajor(const double* a, int64_t rows, int64_t cols) {
+    std::vector<double> out(size_t(rows * cols));
+    for (int64_t j = 0; j < cols; ++j)
+        for (int64_t i = 0; i < rows; ++i) out[size_t(i * cols + j)] = a[i + j * rows];
+    return out;
+}
+void rowmajor_to_colmajor(const double* a, int64_t rows, int64_t cols, double* out) {
+    for (int64_t i = 0; i < rows; ++i)
+        for (int64_t j = 0; j < cols; ++j) out[i + j * rows] = a[size_t(i * cols + j)];
+}
+
+}  // namespace
+
+// ===========================================================================
+struct rocp_dev {
+    int device = 0;
+    int world = 1, rank = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    DBuf<unsigned int> counters;  // zeroed; one per last-block kernel in flight
+    DBuf<int> flags;              // [0] regularized, [1] non-finite code
+    DBuf<double> scalars;         // small results
+    DBuf<double> scratch_a, scratch_b;  // reduction partials
+    int num_sms = 148;
+    // device-resident result of the last rocp_cprand (for stream_create_from_init)
+    struct Init {
+        bool valid = false;
+        std::vector<int64_t> dims;
+        int rank = 0;
+        int64_t s = 0;
+        bool regularized = false;
+        std::vector<DBuf<double>> factors;  // row-major I_n x R, best iterate
+        std::vector<DBuf<double>> best_kr;  // N-1, s x R row-major
+    } init;
+};
+
+struct rocp_tensor {
+    std::vector<int64_t> dims;
+    double* d = nullptr;
+    bool owned = false;
+    int64_t numel = 0;
+    ~rocp_tensor() {
+        if (owned && d) cudaFree(d);
+    }
+};
+
+namespace {
+
+void set_err(rocp_dev* dev, const RocpError& e) {
+    if (dev) dev->err = e.msg;
+}
+
+// ---- launch helpers ---------------------------------------------------------
+void after_launch(rocp_dev* dev, const char* name) {
+    dev->launches++;
+    cuda_check(cudaGetLastError(), name);
+}
+
+int grid_for(int64_t work, int block, int cap) {
+    int64_t g = (work + block - 1) / block;
+    return int(std::max<int64_t>(1, std::min<int64_t>(g, cap)));
+}
+
+// Fills a DrawJob for `mode` over tensor dims `d` (sampling.cpp:47-55 +
+// decode_all sampling.cpp:11-20 + the base offset of sample_unfolding
+// sampling.cpp:68-74).
+DrawJob make_draw(const std::vector<int64_t>& d, int mode, int64_t s, uint64_t seed, uint32_t batch,
+                  uint32_t iteration, const int64_t* in_rows, int64_t* rows, int32_t* idx,
+                  int64_t* base) {
+    DrawJob j{};
+    j.seed = seed;
+    j.batch = batch;
+    j.iteration = iteration;
+    j.mode = uint32_t(mode);
+    j.n_other = int(d.size()) - 1;
+    j.s = int32_t(s);
+    const std::vector<int64_t> st = strides_of(d);
+    int64_t co = 1;
+    int pos = 0;
+    for (size_t k = 0; k < d.size(); ++k) {
+        if (int(k) + 1 == mode) continue;
+        j.ext[pos] = d[k];
+        j.tstride[pos] = st[k];
+        co *= d[k];
+        ++pos;
+    }
+    j.co = co;
+    j.in_rows = in_rows;
+    j.rows = rows;
+    j.idx = idx;
+    j.base = base;
+    return j;
+}
+
+void launch_draw(rocp_dev* dev, const DrawBatch& b, int64_t max_s) {
+    dim3 grid(grid_for(max_s, 128, 64), b.njobs);
+    k_draw<<<grid, 128, 0, dev->stream>>>(b);
+    after_launch(dev, "k_draw");
+}
+
+void launch_gather(rocp_dev* dev, const GatherBatch& b, int64_t max_elems) {
+    constexpr int kUnroll = 4;
+    dim3 grid(grid_for((max_elems + kUnroll - 1) / kUnroll, 256, dev->num_sms * 8), b.njobs);
+    k_gather<kUnroll><<<grid, 256, 0, dev->stream>>>(b);
+    after_launch(dev, "k_gather");
+}
+
+void launch_skr(rocp_dev* dev, const SkrJob& j) {
+    k_skr<<<grid_for(int64_t(j.s) * j.R, 256, dev->num_sms * 4), 256, 0, dev->stream>>>(j);
+    after_launch(dev, "k_skr");
+}
+
+void launch_gram(rocp_dev* dev, const double* Z, int64_t s, int R, const double* acc_base,
+                 double* out) {
+    const int nk = int((s + kChunk - 1) / kChunk);
+    dev->scratch_a.ensure(size_t(nk) * R * R);
+    k_gram<<<nk, 256, size_t(kChunk) * R * sizeof(double), dev->stream>>>(
+        Z, int32_t(s), R, dev->scratch_a.p, dev->counters.p + 0, acc_base, out);
+    after_launch(dev, "k_gram");
+}
+
+template <int RB>
+void launch_contract_rb(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
+                        const double* base, double* out) {
+    dim3 grid(unsigned((I + 127) / 128), unsigned((R + RB - 1) / RB));
+    k_contract<RB><<<grid, 128, 0, dev->stream>>>(X, int32_t(I), int32_t(s), Z, R, base, out);
+    after_launch(dev, "k_contract");
+}
+
+void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
+                     const double* base, double* out) {
+    if (R % 10 == 0) launch_contract_rb<10>(dev, X, I, s, Z, R, base, out);
+    else if (R % 8 == 0) launch_contract_rb<8>(dev, X, I, s, Z, R, base, out);
+    else if (R % 5 == 0) launch_contract_rb<5>(dev, X, I, s, Z, R, base, out);
+    else if (R % 4 == 0) launch_contract_rb<4>(dev, X, I, s, Z, R, base, out);
+    else if (R <= 4) launch_contract_rb<4>(dev, X, I, s, Z, R, base, out);
+    else launch_contract_rb<8>(dev, X, I, s, Z, R, base, out);
+}
+
+// flags: [0] |= 1 when regularized, [1] = nonfinite_code on a non-finite output.
+void launch_solve(rocp_dev* dev, const double* G, int R, const double* RHS, int64_t rows, double* OUT,
+                  int* flags, int nonfinite_code) {
+    const int grid = int(std::max<int64_t>(1, (rows + 255) / 256));
+    if (R <= 16) k_solve<16><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    else if (R <= 32) k_solve<32><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    else k_solve<64><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    after_launch(dev, "k_solve");
+}
+
+// Sum of squares of (x_hat - x) (factors != null) or x, canonical order.
+// Result left in dev->scalars.p[slot].
+void launch_fitness(rocp_dev* dev, const rocp_tensor* t, const std::vector<const double*>* factors,
+                    int R, int slot) {
+    FitJob j{};
+    j.t = t->d;
+    j.I1 = t->dims[0];
+    j.nfib = t->numel / t->dims[0];
+    j.N = int(t->dims.size());
+    j.R = factors ? R : 0;
+    j.with_model = factors ? 1 : 0;
+    for (int n = 0; n < j.N; ++n) {
+        j.dims[n] = t->dims[size_t(n)];
+        j.U[n] = factors ? (*factors)[size_t(n)] : nullptr;
+    }
+    const int64_t ngroups = (j.nfib + kGroup - 1) / kGroup;
+    dev->scratch_a.ensure(size_t(ngroups));
+    dev->scratch_b.ensure(size_t(ngroups));
+    j.group_partial = dev->scratch_a.p;
+    j.group_tmp = dev->scratch_b.p;
+    j.counter = dev->counters.p + 1;
+    j.out = dev->scalars.p + slot;
+    const size_t smem = (size_t(kGroup) * j.R + kGroup) * sizeof(double);
+    const int grid = int(std::min<int64_t>(ngroups, int64_t(dev->num_sms) * 4));
+    k_fitness<<<grid, 256, smem, dev->stream>>>(j);
+    after_launch(dev, "k_fitness");
+}
+
+void launch_residual(rocp_dev* dev, const double* X, int64_t I, int64_t S, const double* U,
+                     const double* Z, int R, double* out2) {
+    ResidJob j{};
+    j.X = X;
+    j.U = U;
+    j.Z = Z;
+    j.I = int32_t(I);
+    j.S = int32_t(S);
+    j.R = R;
+    dev->scratch_b.ensure(size_t(3 * S));
+    j.col_num = dev->scratch_b.p;
+    j.col_den = dev->scratch_b.p + S;
+    j.tmp = dev->scratch_b.p + 2 * S;
+    j.counter = dev->counters.p + 2;
+    j.out = out2;
+    k_residual<<<grid_for(S, 8, dev->num_sms * 2), 256, 0, dev->stream>>>(j);
+    after_launch(dev, "k_residual");
+}
+
+void upload_rowmajor(rocp_dev* dev, const double* host_col, int64_t rows, int64_t cols, double* d) {
+    std::vector<double> rm = colmajor_to_rowmajor(host_col, rows, cols);
+    CK(cudaMemcpyAsync(d, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+    CK(cudaStreamSynchronize(dev->stream));
+}
+
+void download_colmajor(rocp_dev* dev, const double* d, int64_t rows, int64_t cols, double* host_col) {
+    std::vector<double> rm(size_t(rows * cols));
+    if (!rm.empty()) {
+        CK(cudaMemcpyAsync(rm.data(), d, rm.size() * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+    }
+    rowmajor_to_colmajor(rm.data(), rows, cols, host_col);
+}
+
+template <class F>
+rocp_status guarded(rocp_dev* dev, F&& f, int* err_sweep = nullptr) {
+    try {
+        f();
+        return ROCP_OK;
+    } catch (const RocpError& e) {
+        set_err(dev, e);
+        if (err_sweep && e.code == ROCP_E_NUMERICAL) *err_sweep = e.sweep;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (dev) dev->err = e.what();
+        return ROCP_E_STATE;
+    }
+}
+
+void check_tensor_dims(const std::vector<int64_t>& d) {  // tensor.cpp:11-17
+    if (d.size() < 2) throw_domain("tensor order must be at least 2");
+    if (d.size() > size_t(kMaxOrder)) throw_domain("tensor order above 8 is not supported");
+    for (int64_t x : d)
+        if (x < 1) throw_domain("tensor extents must be positive");
+}
+
+void check_rank(int R) {
+    if (R < 1) throw_domain("rank must be positive");
+    if (R > 64) throw_domain("rank above 64 is not supported by the B200 solve kernel");
+}
+
+}  // namespace
+
+// ===========================================================================
+// Stream state (RocpStream, rocp.hpp:85-107 + ComplementaryState :15-24).
+struct rocp_stream {
+    rocp_dev* dev = nullptr;
+    int N = 0, R = 0;
+    int64_t s = 0;
+    std::vector<int64_t> head;
+    std::vector<DBuf<double>> U, P, Q;  // n = 1..N-1: I_n x R row-major, R x R
+    DBuf<double> temporal;              // t_cap x R row-major
+    int64_t t_len = 0, t_cap = 0;
+    bool regularized = false;
+    // per-stage scratch: stage 0 = temporal, stage n = mode n
+    int64_t max_batch = 0;
+    std::vector<DBuf<int32_t>> idx;
+    std::vector<DBuf<int64_t>> base, rows;
+    std::vector<DBuf<double>> X, Z;
+    DBuf<double> G_t, RHS_t;  // temporal Gram / rhs
+    DBuf<double> resid;       // N x 2 (num, den) of the last consume
+    DBuf<double> staging;     // host-slab staging for consume_host
+    DBuf<int> flags;          // [0] temporal regularized (stream flag), [1] unused,
+                              // [2] last mode-solve regularized, [3] unused
+    bool track_residual = true;
+    // checkpoint copies (device)
+    std::vector<DBuf<double>> ckU, ckP, ckQ;
+    int64_t ck_t_len = -1;
+    bool ck_reg = false;
+    // CUDA graphs of consume_range keyed by their baked parameters
+    std::map<std::tuple<const double*, int64_t, int64_t, int64_t, uint64_t, uint32_t, int64_t>,
+             std::pair<cudaGraphExec_t, uint64_t>>
+        graphs;
+    ~rocp_stream() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+    }
+
+    int64_t stage_rows(int stage, int64_t batch) const { return stage == 0 ? batch : head[size_t(stage - 1)]; }
+
+    void ensure_batch(int64_t batch) {
+        if (batch <= max_batch) return;
+        max_batch = batch;
+        X[0].alloc(size_t(batch * s));
+        RHS_t.alloc(size_t(batch * R));
+    }
+};
+
+namespace {
+
+std::vector<int64_t> slab_dims(const rocp_stream* st, int64_t batch) {
+    std::vector<int64_t> d = st->head;
+    d.push_back(batch);
+    return d;
+}
+
+void check_head_dims(const rocp_stream* st, const rocp_tensor* x) {  // rocp.cpp:14-21
+    if (x->dims.size() != st->head.size() + 1) throw_domain("batch order does not match stream order");
+    for (size_t k = 0; k < st->head.size(); ++k)
+        if (x->dims[k] != st->head[k]) throw_domain("batch head extents do not match stream");
+}
+
+// Temporal stage of consume (update_last_mode_with, rocp.cpp:71-84): SKR of
+// factors_excluding(head, N) = U(N-1..1), gram, rhs, solve into the temporal
+// factor rows [t_len, t_len + B).
+void stage_temporal(rocp_stream* st, int64_t B, double* u_out) {
+    rocp_dev* dev = st->dev;
+    SkrJob sj{};
+    sj.idx = st->idx[0].p;
+    sj.n_other = st->N - 1;
+    sj.s = int32_t(st->s);
+    sj.R = st->R;
+    int l = 0;
+    for (int k = st->N - 1; k >= 1; --k) sj.f[l++] = st->U[size_t(k - 1)].p;
+    sj.z = st->Z[0].p;
+    launch_skr(dev, sj);
+    launch_gram(dev, st->Z[0].p, st->s, st->R, nullptr, st->G_t.p);
+    launch_contract(dev, st->X[0].p, B, st->s, st->Z[0].p, st->R, nullptr, st->RHS_t.p);
+    launch_solve(dev, st->G_t.p, st->R, st->RHS_t.p, B, u_out, st->flags.p, 0);  // rocp.cpp:150
+    if (st->track_residual) launch_residual(dev, st->X[0].p, B, st->s, u_out, st->Z[0].p, st->R, st->resid.p);
+}
+
+// Mode-n stage (update_mode_with, rocp.cpp:96-113 with slab_factors_excluding
+// rocp.cpp:25-34): Z over [u_new, U(N-1..1) \ n], P += X_s Z, Q += Z^T Z,
+// U(n) = solve_gram(Q, P).
+void stage_mode(rocp_stream* st, int n, int64_t B, const double* u_new) {
+    rocp_dev* dev = st->dev;
+    (void)B;
+    SkrJob sj{};
+    sj.idx = st->idx[size_t(n)].p;
+    sj.n_other = st->N - 1;
+    sj.s = int32_t(st->s);
+    sj.R = st->R;
+    int l = 0;
+    sj.f[l++] = u_new;
+    for (int k = st->N - 1; k >= 1; --k)
+        if (k != n) sj.f[l++] = st->U[size_t(k - 1)].p;
+    sj.z = st->Z[size_t(n)].p;
+    launch_skr(dev, sj);
+    double* Pn = st->P[size_t(n - 1)].p;
+    double* Qn = st->Q[size_t(n - 1)].p;
+    const int64_t In = st->head[size_t(n - 1)];
+    launch_gram(dev, st->Z[size_t(n)].p, st->s, st->R, Qn, Qn);
+    launch_contract(dev, st->X[size_t(n)].p, In, st->s, st->Z[size_t(n)].p, st->R, Pn, Pn);
+    launch_solve(dev, Qn, st->R, Pn, In, st->U[size_t(n - 1)].p, st->flags.p + 2, 0);
+    if (st->track_residual)
+        launch_residual(dev, st->X[size_t(n)].p, In, st->s, st->U[size_t(n - 1)].p, st->Z[size_t(n)].p,
+                        st->R, st->resid.p + 2 * n);
+}
+
+// Draw + gather every stage of one batch (indices never depend on factors, so
+// all N draws and all N gathers are one launch each).
+void draw_and_gather(rocp_stream* st, const rocp_tensor* x, uint64_t seed, uint32_t batch_id,
+                     const int64_t* in_rows_stage0, const int64_t* in_rows_mode, int only_mode) {
+    rocp_dev* dev = st->dev;
+    const int64_t B = x->dims.back();
+    const std::vector<int64_t> d = slab_dims(st, B);
+    const std::vector<int64_t> strides = strides_of(d);
+    DrawBatch db{};
+    GatherBatch gb{};
+    int64_t max_elems = 0;
+    for (int stage = 0; stage < st->N; ++stage) {
+        if (only_mode >= 0 && stage != only_mode) continue;
+        const int mode = stage == 0 ? st->N : stage;
+        const int64_t* in_rows = stage == 0 ? in_rows_stage0 : in_rows_mode;
+        db.job[db.njobs++] = make_draw(d, mode, st->s, seed, batch_id, 0u, in_rows, st->rows[size_t(stage)].p,
+                                       st->idx[size_t(stage)].p, st->base[size_t(stage)].p);
+        GatherJob g{};
+        g.t = x->d;
+        g.base = st->base[size_t(stage)].p;
+        g.ms = strides[size_t(mode - 1)];
+        g.I = int32_t(d[size_t(mode - 1)]);
+        g.s = int32_t(st->s);
+        g.out = st->X[size_t(stage)].p;
+        gb.job[gb.njobs++] = g;
+        max_elems = std::max<int64_t>(max_elems, int64_t(g.I) * g.s);
+    }
+    launch_draw(dev, db, st->s);
+    launch_gather(dev, gb, max_elems);
+}
+
+void enqueue_consume(rocp_stream* st, const rocp_tensor* x, uint64_t seed, uint32_t batch_id) {
+    const int64_t B = x->dims.back();
+    st->ensure_batch(B);
+    if (st->t_len + B > st->t_cap) throw_domain("temporal capacity exceeded (raise t_capacity)");
+    draw_and_gather(st, x, seed, batch_id, nullptr, nullptr, -1);
+    double* u_new = st->temporal.p + st->t_len * st->R;  // rocp.cpp:152-156, appended in place
+    stage_temporal(st, B, u_new);
+    for (int n = 1; n < st->N; ++n) stage_mode(st, n, B, u_new);  // rocp.cpp:122-130
+    st->t_len += B;                                               // rocp.cpp:159
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, rocp_dev** out) {
+    (void)nccl_id;
+    auto dev = std::make_unique<rocp_dev>();
+    rocp_status st = guarded(dev.get(), [&] {
+        if (world != 1 || rank != 0) throw_domain("this build runs one GPU per handle (world = 1)");
+        CK(cudaSetDevice(device));
+        dev->device = device;
+        dev->world = world;
+        dev->rank = rank;
+        CK(cudaStreamCreateWithFlags(&dev->stream, cudaStreamNonBlocking));
+        CK(cudaDeviceGetAttribute(&dev->num_sms, cudaDevAttrMultiProcessorCount, device));
+        dev->counters.alloc(16);
+        CK(cudaMemset(dev->counters.p, 0, 16 * sizeof(unsigned int)));
+        dev->flags.alloc(4);
+        CK(cudaMemset(dev->flags.p, 0, 4 * sizeof(int)));
+        dev->scalars.alloc(16);
+        CK(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int((size_t(kGroup) * 64 + kGroup) * sizeof(double))));
+    });
+    if (st != ROCP_OK) {
+        static thread_local std::string last;
+        last = dev->err;
+        *out = nullptr;
+        return st;
+    }
+    *out = dev.release();
+    return ROCP_OK;
+}
+
+void rocp_destroy(rocp_dev* dev) {
+    if (!dev) return;
+    cudaSetDevice(dev->device);
+    cudaStreamSynchronize(dev->stream);
+    dev->init = rocp_dev::Init{};
+    cudaStreamDestroy(dev->stream);
+    delete dev;
+}
+
+const char* rocp_last_error(const rocp_dev* dev) { return dev ? dev->err.c_str() : "null handle"; }
+
+rocp_status rocp_synchronize(rocp_dev* dev) {
+    return guarded(dev, [&] { CK(cudaStreamSynchronize(dev->stream)); });
+}
+
+uint64_t rocp_kernel_launches(const rocp_dev* dev) { return dev ? dev->launches : 0; }
+
+int rocp_nccl_id_size(void) { return 0; }
+rocp_status rocp_nccl_get_unique_id(void* out) {
+    (void)out;
+    return ROCP_E_NCCL;
+}
+
+// ---- tensors ---------------------------------------------------------------
+rocp_status rocp_tensor_create(rocp_dev* dev, const int64_t* dims, int order, const double* host,
+                               rocp_tensor** out) {
+    return guarded(dev, [&] {
+        std::vector<int64_t> d(dims, dims + order);
+        check_tensor_dims(d);
+        auto t = std::make_unique<rocp_tensor>();
+        t->dims = d;
+        t->numel = prod(d);
+        t->owned = true;
+        CK(cudaMalloc(&t->d, size_t(t->numel) * sizeof(double)));
+        if (host)
+            CK(cudaMemcpyAsync(t->d, host, size_t(t->numel) * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+        else
+            CK(cudaMemsetAsync(t->d, 0, size_t(t->numel) * sizeof(double), dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        *out = t.release();
+    });
+}
+
+rocp_status rocp_tensor_slab(rocp_dev* dev, const rocp_tensor* t, int64_t t0, int64_t len,
+                             rocp_tensor** out) {
+    return guarded(dev, [&] {
+        const int64_t T = t->dims.back();
+        if (t0 < 0 || len < 1 || t0 + len > T) throw_domain("slab out of range");
+        auto v = std::make_unique<rocp_tensor>();
+        v->dims = t->dims;
+        v->dims.back() = len;
+        v->numel = prod(v->dims);
+        const int64_t slice = t->numel / T;
+        v->d = t->d + t0 * slice;
+        v->owned = false;
+        *out = v.release();
+    });
+}
+
+void rocp_tensor_free(rocp_tensor* t) { delete t; }
+
+rocp_status rocp_tensor_upload(rocp_dev* dev, rocp_tensor* t, const double* host) {
+    return guarded(dev, [&] {
+        CK(cudaMemcpyAsync(t->d, host, size_t(t->numel) * sizeof(double), cudaMemcpyHostToDevice, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+    });
+}
+
+rocp_status rocp_tensor_download(rocp_dev* dev, const rocp_tensor* t, double* host) {
+    return guarded(dev, [&] {
+        CK(cudaMemcpyAsync(host, t->d, size_t(t->numel) * sizeof(double), cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+    });
+}
+
+double* rocp_tensor_device_ptr(rocp_tensor* t) { return t ? t->d : nullptr; }
+int64_t rocp_tensor_numel(const rocp_tensor* t) { return t ? t->numel : 0; }
+
+rocp_status rocp_generate_synthetic(rocp_dev* dev, rocp_tensor* t, const double* const* factors,
+                                    int rank, int has_noise, double snr_db, uint64_t noise_seed) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        const int N = int(t->dims.size());
+        std::vector<DBuf<double>> U;
+        SynJob j{};
+        for (int n = 0; n < N; ++n) {
+            U.emplace_back(size_t(t->dims[size_t(n)] * rank));
+            upload_rowmajor(dev, factors[n], t->dims[size_t(n)], rank, U.back().p);
+            j.U[n] = U.back().p;
+            j.dims[n] = t->dims[size_t(n)];
+        }
+        j.t = t->d;
+        j.numel = t->numel;
+        j.I1 = t->dims[0];
+        j.N = N;
+        j.R = rank;
+        j.seed = noise_seed;
+        const int grid = dev->num_sms * 8;  // fixed: deterministic partial layout
+        DBuf<double> ps(static_cast<size_t>(grid)), pn(static_cast<size_t>(grid));
+        j.part_sig = ps.p;
+        j.part_noise = has_noise ? pn.p : nullptr;
+        k_synth_signal<<<grid, 256, 0, dev->stream>>>(j);
+        after_launch(dev, "k_synth_signal");
+        if (has_noise) {
+            std::vector<double> hs(static_cast<size_t>(grid)), hn(static_cast<size_t>(grid));
+            CK(cudaMemcpyAsync(hs.data(), ps.p, hs.size() * 8, cudaMemcpyDeviceToHost, dev->stream));
+            CK(cudaMemcpyAsync(hn.data(), pn.p, hn.size() * 8, cudaMemcpyDeviceToHost, dev->stream));
+            CK(cudaStreamSynchronize(dev->stream));
+            double ss = 0.0, nn = 0.0;
+            for (int b = 0; b < grid; ++b) { ss += hs[size_t(b)]; nn += hn[size_t(b)]; }
+            // |noise|^2 = |signal|^2 * 10^(-snr/10), scaled after the draw (synthetic.cpp:26-27)
+            const double scale = std::sqrt(ss) * std::pow(10.0, -snr_db / 20.0) / std::sqrt(nn);
+            CK(cudaMemcpyAsync(dev->scalars.p + 15, &scale, 8, cudaMemcpyHostToDevice, dev->stream));
+            k_synth_noise<<<grid, 256, 0, dev->stream>>>(t->d, t->numel, noise_seed, dev->scalars.p + 15);
+            after_launch(dev, "k_synth_noise");
+        }
+        CK(cudaStreamSynchronize(dev->stream));
+    });
+}
+
+// ---- primitives --------------------------------------------------------------
+rocp_status rocp_draw_samples(rocp_dev* dev, const int64_t* dims, int order, int mode, int64_t s,
+                              uint64_t seed, uint32_t batch, uint32_t iteration, int64_t* rows,
+                              int64_t* decoded) {
+    return guarded(dev, [&] {
+        std::vector<int64_t> d(dims, dims + order);
+        check_tensor_dims(d);
+        if (mode < 1 || mode > order) throw_domain("mode out of range");
+        if (s < 1) throw_domain("sample count must be positive");  // sampling.cpp:48-49
+        DBuf<int64_t> drows(static_cast<size_t>(s)), dbase(static_cast<size_t>(s));
+        DBuf<int32_t> didx(static_cast<size_t>(s) * (order - 1));
+        DrawBatch b{};
+        b.job[b.njobs++] = make_draw(d, mode, s, seed, batch, iteration, nullptr, drows.p, didx.p, dbase.p);
+        launch_draw(dev, b, s);
+        CK(cudaMemcpyAsync(rows, drows.p, size_t(s) * 8, cudaMemcpyDeviceToHost, dev->stream));
+        std::vector<int32_t> hidx(size_t(s) * (order - 1));
+        CK(cudaMemcpyAsync(hidx.data(), didx.p, hidx.size() * 4, cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        if (decoded)
+            for (size_t e = 0; e < hidx.size(); ++e) decoded[e] = int64_t(hidx[e]) + 1;
+    });
+}
+
+rocp_status rocp_decode_rows(rocp_dev* dev, const int64_t* dims, int order, int mode,
+                             const int64_t* rows, int64_t s, int64_t* decoded) {
+    return guarded(dev, [&] {
+        std::vector<int64_t> d(dims, dims + order);
+        check_tensor_dims(d);
+        if (mode < 1 || mode > order) throw_domain("mode out of range");
+        int64_t co = 1;
+        for (int k = 0; k < order; ++k)
+            if (k + 1 != mode) co *= d[size_t(k)];
+        for (int64_t c = 0; c < s; ++c)
+            if (rows[c] < 1 || rows[c] > co) throw_domain("column index out of range");  // tensor.cpp:98-99
+        DBuf<int64_t> din(static_cast<size_t>(s)), dbase(static_cast<size_t>(s));
+        DBuf<int32_t> didx(static_cast<size_t>(s) * (order - 1));
+        CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
+        DrawBatch b{};
+        b.job[b.njobs++] = make_draw(d, mode, s, 0, 0, 0, din.p, nullptr, didx.p, dbase.p);
+        launch_draw(dev, b, s);
+        std::vector<int32_t> hidx(size_t(s) * (order - 1));
+        CK(cudaMemcpyAsync(hidx.data(), didx.p, hidx.size() * 4, cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        for (size_t e = 0; e < hidx.size(); ++e) decoded[e] = int64_t(hidx[e]) + 1;
+    });
+}
+
+rocp_status rocp_sample_unfolding(rocp_dev* dev, const rocp_tensor* t, int mode,
+                                  const int64_t* rows, int64_t s, double* out) {
+    return guarded(dev, [&] {
+        const std::vector<int64_t>& d = t->dims;
+        const int order = int(d.size());
+        if (mode < 1 || mode > order) throw_domain("mode out of range");
+        if (s < 1) throw_domain("sample count must be positive");
+        int64_t co = 1;
+        for (int k = 0; k < order; ++k)
+            if (k + 1 != mode) co *= d[size_t(k)];
+        for (int64_t c = 0; c < s; ++c)
+            if (rows[c] < 1 || rows[c] > co)
+                throw_domain("sample_unfolding: index set drawn against different dims");
+        const int64_t I = d[size_t(mode - 1)];
+        DBuf<int64_t> din(static_cast<size_t>(s)), dbase(static_cast<size_t>(s));
+        DBuf<int32_t> didx(static_cast<size_t>(s) * (order - 1));
+        DBuf<double> dout(static_cast<size_t>(I * s));
+        CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
+        DrawBatch b{};
+        b.job[b.njobs++] = make_draw(d, mode, s, 0, 0, 0, din.p, nullptr, didx.p, dbase.p);
+        launch_draw(dev, b, s);
+        GatherBatch gb{};
+        GatherJob g{};
+        g.t = t->d;
+        g.base = dbase.p;
+        g.ms = strides_of(d)[size_t(mode - 1)];
+        g.I = int32_t(I);
+        g.s = int32_t(s);
+        g.out = dout.p;
+        gb.job[gb.njobs++] = g;
+        launch_gather(dev, gb, I * s);
+        CK(cudaMemcpyAsync(out, dout.p, size_t(I * s) * 8, cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+    });
+}
+
+rocp_status rocp_sampled_khatri_rao(rocp_dev* dev, const int64_t* decoded, int64_t s, int n_other,
+                                    const double* const* factors, const int64_t* factor_rows,
+                                    int rank, double* z) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        if (n_other < 1 || n_other >= kMaxOrder) throw_domain("sampled_khatri_rao: factor count mismatch");
+        for (int64_t c = 0; c < s; ++c)
+            for (int k = 0; k < n_other; ++k) {
+                const int64_t i = decoded[c * n_other + k];
+                const int l = n_other - 1 - k;
+                if (i < 1 || i > factor_rows[l])
+                    throw_domain("sampled_khatri_rao: decoded index exceeds factor rows");  // sampling.cpp:99-100
+            }
+        std::vector<int32_t> hidx(size_t(s) * n_other);
+        for (size_t e = 0; e < hidx.size(); ++e) hidx[e] = int32_t(decoded[e] - 1);
+        DBuf<int32_t> didx(hidx.size());
+        CK(cudaMemcpyAsync(didx.p, hidx.data(), hidx.size() * 4, cudaMemcpyHostToDevice, dev->stream));
+        std::vector<DBuf<double>> F;
+        SkrJob j{};
+        for (int l = 0; l < n_other; ++l) {
+            F.emplace_back(size_t(factor_rows[l] * rank));
+            upload_rowmajor(dev, factors[l], factor_rows[l], rank, F.back().p);
+            j.f[l] = F.back().p;
+        }
+        DBuf<double> dz(static_cast<size_t>(s * rank));
+        j.idx = didx.p;
+        j.n_other = n_other;
+        j.s = int32_t(s);
+        j.R = rank;
+        j.z = dz.p;
+        launch_skr(dev, j);
+        download_colmajor(dev, dz.p, s, rank, z);
+    });
+}
+
+rocp_status rocp_gram(rocp_dev* dev, const double* z, int64_t s, int rank, double* g) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        DBuf<double> dz(static_cast<size_t>(s * rank)), dg(static_cast<size_t>(rank * rank));
+        upload_rowmajor(dev, z, s, rank, dz.p);
+        launch_gram(dev, dz.p, s, rank, nullptr, dg.p);
+        CK(cudaMemcpyAsync(g, dg.p, size_t(rank * rank) * 8, cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+    });
+}
+
+rocp_status rocp_contract(rocp_dev* dev, const double* x, int64_t rows, int64_t s, const double* z,
+                          int rank, double* out) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        DBuf<double> dx(static_cast<size_t>(rows * s)), dz(static_cast<size_t>(s * rank)), dout(static_cast<size_t>(rows * rank));
+        CK(cudaMemcpyAsync(dx.p, x, size_t(rows * s) * 8, cudaMemcpyHostToDevice, dev->stream));
+        upload_rowmajor(dev, z, s, rank, dz.p);
+        launch_contract(dev, dx.p, rows, s, dz.p, rank, nullptr, dout.p);
+        download_colmajor(dev, dout.p, rows, rank, out);
+    });
+}
+
+rocp_status rocp_solve_gram(rocp_dev* dev, const double* gram, const double* rhs, int64_t rows,
+                            int rank, double* out, int* regularized) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        DBuf<double> dg(static_cast<size_t>(rank * rank)), drhs(static_cast<size_t>(std::max<int64_t>(rows, 1) * rank)),
+            dout(size_t(std::max<int64_t>(rows, 1) * rank));
+        CK(cudaMemcpyAsync(dg.p, gram, size_t(rank * rank) * 8, cudaMemcpyHostToDevice, dev->stream));
+        if (rows > 0) upload_rowmajor(dev, rhs, rows, rank, drhs.p);
+        CK(cudaMemsetAsync(dev->flags.p, 0, 2 * sizeof(int), dev->stream));
+        launch_solve(dev, dg.p, rank, drhs.p, rows, dout.p, dev->flags.p, 1);
+        int hf[2];
+        CK(cudaMemcpyAsync(hf, dev->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+        if (rows > 0) download_colmajor(dev, dout.p, rows, rank, out);
+        CK(cudaStreamSynchronize(dev->stream));
+        if (regularized) *regularized = hf[0] & 1;
+    });
+}
+
+rocp_status rocp_solve_sampled_ls(rocp_dev* dev, const double* z, const double* x, int64_t s,
+                                  int64_t rows, int rank, double* out, int* regularized,
+                                  int* underdetermined) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        if (underdetermined) *underdetermined = (s < rank) ? 1 : 0;  // solve.cpp:40
+        DBuf<double> dz(static_cast<size_t>(s * rank)), dx(static_cast<size_t>(rows * s)), dg(static_cast<size_t>(rank * rank)),
+            drhs(size_t(rows * rank)), dout(size_t(rows * rank));
+        upload_rowmajor(dev, z, s, rank, dz.p);
+        CK(cudaMemcpyAsync(dx.p, x, size_t(rows * s) * 8, cudaMemcpyHostToDevice, dev->stream));
+        launch_gram(dev, dz.p, s, rank, nullptr, dg.p);
+        launch_contract(dev, dx.p, rows, s, dz.p, rank, nullptr, drhs.p);
+        CK(cudaMemsetAsync(dev->flags.p, 0, 2 * sizeof(int), dev->stream));
+        launch_solve(dev, dg.p, rank, drhs.p, rows, dout.p, dev->flags.p, 1);
+        int hf[2];
+        CK(cudaMemcpyAsync(hf, dev->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+        download_colmajor(dev, dout.p, rows, rank, out);
+        if (regularized) *regularized = hf[0] & 1;
+    });
+}
+
+rocp_status rocp_model_fitness(rocp_dev* dev, const rocp_tensor* t, const double* const* factors,
+                               int rank, double* fit) {
+    return guarded(dev, [&] {
+        check_rank(rank);
+        const int N = int(t->dims.size());
+        std::vector<DBuf<double>> U;
+        std::vector<const double*> ptrs;
+        for (int n = 0; n < N; ++n) {
+            U.emplace_back(size_t(t->dims[size_t(n)] * rank));
+            upload_rowmajor(dev, factors[n], t->dims[size_t(n)], rank, U.back().p);
+            ptrs.push_back(U.back().p);
+        }
+        launch_fitness(dev, t, nullptr, rank, 0);
+        launch_fitness(dev, t, &ptrs, rank, 1);
+        double h[2];
+        CK(cudaMemcpyAsync(h, dev->scalars.p, sizeof(h), cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        if (h[0] == 0.0) throw_domain("fitness undefined for zero-norm reference tensor");  // kruskal.cpp:75-76
+        *fit = 1.0 - std::sqrt(h[1]) / std::sqrt(h[0]);                                 // kruskal.cpp:84
+    });
+}
+
+// ---- cprand (cprand.cpp:12-69) ------------------------------------------------
+rocp_status rocp_cprand(rocp_dev* dev, const rocp_tensor* t, int rank, int64_t samples, double tol,
+                        int max_iters, uint64_t seed, double* const* factors,
+                        double* const* best_kr, double* best_fitness, int* iterations,
+                        int* regularized, int* err_sweep, double* fit_trace) {
+    return guarded(
+        dev,
+        [&] {
+            if (rank < 1) throw_domain("cprand_decompose: rank must be positive");  // cprand.cpp:14-15
+            check_rank(rank);
+            if (max_iters < 1) throw_domain("cprand_decompose: need at least one sweep");  // :16-17
+            const std::vector<int64_t>& d = t->dims;
+            const int N = int(d.size());
+            launch_fitness(dev, t, nullptr, rank, 0);
+            double nsq = 0.0;
+            CK(cudaMemcpyAsync(&nsq, dev->scalars.p, 8, cudaMemcpyDeviceToHost, dev->stream));
+            CK(cudaStreamSynchronize(dev->stream));
+            if (nsq == 0.0) throw_domain("cprand_decompose: zero tensor");  // :18-19
+            const int64_t s = samples > 0 ? samples : auto_sample_count(rank);  // :23
+            const std::vector<int64_t> strides = strides_of(d);
+
+            std::vector<DBuf<double>> U, best;
+            std::vector<const double*> uptr;
+            std::vector<DBuf<int32_t>> idx;
+            std::vector<DBuf<int64_t>> base;
+            std::vector<DBuf<double>> X, Z, G, RHS;
+            for (int n = 0; n < N; ++n) {
+                const int64_t In = d[size_t(n)];
+                U.emplace_back(size_t(In * rank));
+                upload_rowmajor(dev, factors[n], In, rank, U.back().p);  // model = random_model(...) (:25)
+                best.emplace_back(size_t(In * rank));
+                uptr.push_back(U.back().p);
+                idx.emplace_back(size_t(s) * (N - 1));
+                base.emplace_back(size_t(s));
+                X.emplace_back(size_t(In * s));
+                Z.emplace_back(size_t(s * rank));
+                G.emplace_back(size_t(rank * rank));
+                RHS.emplace_back(size_t(In * rank));
+            }
+            double best_fit = -std::numeric_limits<double>::infinity();
+            double prev = best_fit;
+            bool reg_any = false;
+            int sweep = 0;
+            CK(cudaMemsetAsync(dev->flags.p, 0, 2 * sizeof(int), dev->stream));
+            while (sweep < max_iters) {  // :32
+                ++sweep;
+                // All N draws and gathers of the sweep up front: indices never depend on factors.
+                DrawBatch db{};
+                GatherBatch gb{};
+                int64_t max_elems = 0;
+                for (int n = 1; n <= N; ++n) {
+                    db.job[db.njobs++] = make_draw(d, n, s, seed, 0u, uint32_t(sweep), nullptr, nullptr,
+                                                   idx[size_t(n - 1)].p, base[size_t(n - 1)].p);
+                    GatherJob g{};
+                    g.t = t->d;
+                    g.base = base[size_t(n - 1)].p;
+                    g.ms = strides[size_t(n - 1)];
+                    g.I = int32_t(d[size_t(n - 1)]);
+                    g.s = int32_t(s);
+                    g.out = X[size_t(n - 1)].p;
+                    gb.job[gb.njobs++] = g;
+                    max_elems = std::max<int64_t>(max_elems, int64_t(g.I) * g.s);
+                }
+                launch_draw(dev, db, s);
+                launch_gather(dev, gb, max_elems);
+                for (int n = 1; n <= N; ++n) {  // :35-45
+                    SkrJob sj{};
+                    sj.idx = idx[size_t(n - 1)].p;
+                    sj.n_other = N - 1;
+                    sj.s = int32_t(s);
+                    sj.R = rank;
+                    int l = 0;
+                    for (int k = N; k >= 1; --k)
+                        if (k != n) sj.f[l++] = U[size_t(k - 1)].p;  // factors_excluding (kruskal.cpp:44-53)
+                    sj.z = Z[size_t(n - 1)].p;
+                    launch_skr(dev, sj);
+                    launch_gram(dev, sj.z, s, rank, nullptr, G[size_t(n - 1)].p);
+                    launch_contract(dev, X[size_t(n - 1)].p, d[size_t(n - 1)], s, sj.z, rank, nullptr,
+                                    RHS[size_t(n - 1)].p);
+                    launch_solve(dev, G[size_t(n - 1)].p, rank, RHS[size_t(n - 1)].p, d[size_t(n - 1)],
+                                 U[size_t(n - 1)].p, dev->flags.p, sweep);
+                }
+                launch_fitness(dev, t, &uptr, rank, 1);  // :47
+                double rsq = 0.0;
+                int hf[2];
+                CK(cudaMemcpyAsync(&rsq, dev->scalars.p + 1, 8, cudaMemcpyDeviceToHost, dev->stream));
+                CK(cudaMemcpyAsync(hf, dev->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+                CK(cudaStreamSynchronize(dev->stream));
+                reg_any = reg_any || (hf[0] & 1);
+                if (hf[1] != 0) {  // :42-43
+                    RocpError e{ROCP_E_NUMERICAL,
+                                "cprand_decompose: non-finite factor update (sweep " + std::to_string(hf[1]) + ")"};
+                    e.sweep = hf[1];
+                    throw e;
+                }
+                const double fit = 1.0 - std::sqrt(rsq) / std::sqrt(nsq);
+                if (fit_trace) fit_trace[sweep - 1] = fit;
+                if (!std::isfinite(fit)) {  // :48-49
+                    RocpError e{ROCP_E_NUMERICAL,
+                                "cprand_decompose: non-finite fitness (sweep " + std::to_string(sweep) + ")"};
+                    e.sweep = sweep;
+                    throw e;
+                }
+                if (fit > best_fit) {  // :50-53
+                    best_fit = fit;
+                    for (int n = 0; n < N; ++n)
+                        CK(cudaMemcpyAsync(best[size_t(n)].p, U[size_t(n)].p, U[size_t(n)].n * 8,
+                                           cudaMemcpyDeviceToDevice, dev->stream));
+                }
+                if (std::fabs(fit - prev) < tol) break;  // :54
+                prev = fit;
+            }
+            // Z_best rebuild, one fresh draw per non-temporal mode (:61-67),
+            // keyed (batch 0, iteration 0).
+            rocp_dev::Init init;
+            init.dims = d;
+            init.rank = rank;
+            init.s = s;
+            init.regularized = reg_any;
+            DrawBatch db{};
+            for (int n = 1; n < N; ++n)
+                db.job[db.njobs++] = make_draw(d, n, s, seed, 0u, 0u, nullptr, nullptr, idx[size_t(n - 1)].p,
+                                               base[size_t(n - 1)].p);
+            launch_draw(dev, db, s);
+            for (int n = 1; n < N; ++n) {
+                SkrJob sj{};
+                sj.idx = idx[size_t(n - 1)].p;
+                sj.n_other = N - 1;
+                sj.s = int32_t(s);
+                sj.R = rank;
+                int l = 0;
+                for (int k = N; k >= 1; --k)
+                    if (k != n) sj.f[l++] = best[size_t(k - 1)].p;
+                init.best_kr.emplace_back(size_t(s * rank));
+                sj.z = init.best_kr.back().p;
+                launch_skr(dev, sj);
+                if (best_kr) download_colmajor(dev, sj.z, s, rank, best_kr[n - 1]);
+            }
+            for (int n = 0; n < N; ++n) download_colmajor(dev, best[size_t(n)].p, d[size_t(n)], rank, factors[n]);
+            init.factors = std::move(best);
+            init.valid = true;
+            dev->init = std::move(init);
+            *best_fitness = best_fit;
+            *iterations = sweep;
+            if (regularized) *regularized = reg_any ? 1 : 0;
+        },
+        err_sweep);
+}
+
+// ---- stream ------------------------------------------------------------------
+namespace {
+
+rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int rank, int64_t s,
+                        int64_t t_init, int64_t t_capacity) {
+    if (order < 2 || order > kMaxOrder) throw_domain("stream order must be in [2, 8]");
+    check_rank(rank);
+    if (s < 1) throw_domain("init_state: sample count must be positive");
+    auto st = std::make_unique<rocp_stream>();
+    st->dev = dev;
+    st->N = order;
+    st->R = rank;
+    st->s = s;
+    st->head.assign(head_dims, head_dims + order - 1);
+    st->t_len = t_init;
+    st->t_cap = std::max<int64_t>(t_capacity, t_init);
+    st->temporal.alloc(size_t(std::max<int64_t>(st->t_cap, 1) * rank));
+    for (int n = 1; n < order; ++n) {
+        const int64_t In = st->head[size_t(n - 1)];
+        st->U.emplace_back(size_t(In * rank));
+        st->P.emplace_back(size_t(In * rank));
+        st->Q.emplace_back(size_t(rank * rank));
+    }
+    for (int stage = 0; stage < order; ++stage) {
+        st->idx.emplace_back(size_t(s) * (order - 1));
+        st->base.emplace_back(size_t(s));
+        st->rows.emplace_back(size_t(s));
+        st->Z.emplace_back(size_t(s * rank));
+        st->X.emplace_back(stage == 0 ? 0 : size_t(st->head[size_t(stage - 1)] * s));
+    }
+    st->G_t.alloc(size_t(rank * rank));
+    st->resid.alloc(size_t(2 * order));
+    st->flags.alloc(4);
+    CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));
+    // Reduction scratch sized once: consume (and its CUDA graph) never allocates.
+    dev->scratch_a.ensure(size_t((s + kChunk - 1) / kChunk) * rank * rank);
+    dev->scratch_b.ensure(size_t(3 * s));
+    CK(cudaMemsetAsync(st->resid.p, 0, size_t(2 * order) * 8, dev->stream));
+    st->ensure_batch(1);
+    return st.release();
+}
+
+// init_state (rocp.cpp:45-69): Q = Z^T Z, P = U Q (or U with literal_init).
+void init_pq(rocp_stream* st, const std::vector<const double*>& z_dev, bool literal) {
+    rocp_dev* dev = st->dev;
+    for (int n = 1; n < st->N; ++n) {
+        launch_gram(dev, z_dev[size_t(n - 1)], st->s, st->R, nullptr, st->Q[size_t(n - 1)].p);
+        const int64_t In = st->head[size_t(n - 1)];
+        if (literal) {
+            CK(cudaMemcpyAsync(st->P[size_t(n - 1)].p, st->U[size_t(n - 1)].p, size_t(In * st->R) * 8,
+                               cudaMemcpyDeviceToDevice, dev->stream));
+        } else {
+            k_mul_uq<<<grid_for(In * st->R, 256, dev->num_sms * 4), 256, 0, dev->stream>>>(
+                st->U[size_t(n - 1)].p, int32_t(In), st->R, st->Q[size_t(n - 1)].p, st->P[size_t(n - 1)].p);
+            after_launch(dev, "k_mul_uq");
+        }
+    }
+    CK(cudaStreamSynchronize(dev->stream));
+}
+
+}  // namespace
+
+rocp_status rocp_stream_create(rocp_dev* dev, int order, const int64_t* head_dims, int rank,
+                               int64_t s, int literal_init, const double* const* factors,
+                               int64_t t_init, const double* const* best_kr, int regularized,
+                               int64_t t_capacity, rocp_stream** out) {
+    return guarded(dev, [&] {
+        std::unique_ptr<rocp_stream> st(new_stream(dev, order, head_dims, rank, s, t_init, t_capacity));
+        st->regularized = regularized != 0;
+        for (int n = 1; n < order; ++n)
+            upload_rowmajor(dev, factors[n - 1], st->head[size_t(n - 1)], rank, st->U[size_t(n - 1)].p);
+        if (t_init > 0) upload_rowmajor(dev, factors[order - 1], t_init, rank, st->temporal.p);
+        std::vector<DBuf<double>> zb;
+        std::vector<const double*> zp;
+        for (int n = 1; n < order; ++n) {
+            zb.emplace_back(size_t(s * rank));
+            upload_rowmajor(dev, best_kr[n - 1], s, rank, zb.back().p);
+            zp.push_back(zb.back().p);
+        }
+        init_pq(st.get(), zp, literal_init != 0);
+        *out = st.release();
+    });
+}
+
+rocp_status rocp_stream_create_from_init(rocp_dev* dev, int literal_init, int64_t t_capacity,
+                                         rocp_stream** out) {
+    return guarded(dev, [&] {
+        if (!dev->init.valid) throw RocpError{ROCP_E_STATE, "no device-resident cprand result"};
+        const auto& in = dev->init;
+        const int N = int(in.dims.size());
+        std::unique_ptr<rocp_stream> st(new_stream(dev, N, in.dims.data(), in.rank, in.s, in.dims.back(), t_capacity));
+        st->regularized = in.regularized;
+        for (int n = 1; n < N; ++n)
+            CK(cudaMemcpyAsync(st->U[size_t(n - 1)].p, in.factors[size_t(n - 1)].p, in.factors[size_t(n - 1)].n * 8,
+                               cudaMemcpyDeviceToDevice, dev->stream));
+        CK(cudaMemcpyAsync(st->temporal.p, in.factors[size_t(N - 1)].p, in.factors[size_t(N - 1)].n * 8,
+                           cudaMemcpyDeviceToDevice, dev->stream));
+        std::vector<const double*> zp;
+        for (auto& z : in.best_kr) zp.push_back(z.p);
+        init_pq(st.get(), zp, literal_init != 0);
+        *out = st.release();
+    });
+}
+
+void rocp_stream_free(rocp_stream* st) {
+    if (!st) return;
+    cudaStreamSynchronize(st->dev->stream);
+    delete st;
+}
+
+rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint64_t seed,
+                                uint32_t batch_id) {
+    return guarded(st->dev, [&] {
+        check_head_dims(st, x_new);  // rocp.cpp:145
+        enqueue_consume(st, x_new, seed, batch_id);
+    });
+}
+
+rocp_status rocp_stream_consume_host(rocp_stream* st, const double* x_new, int64_t batch,
+                                     uint64_t seed, uint32_t batch_id) {
+    return guarded(st->dev, [&] {
+        if (batch < 1) throw_domain("batch must hold at least one slice");
+        rocp_dev* dev = st->dev;
+        const int64_t numel = prod(st->head) * batch;
+        st->staging.ensure(size_t(numel));
+        CK(cudaMemcpyAsync(st->staging.p, x_new, size_t(numel) * 8, cudaMemcpyHostToDevice, dev->stream));
+        rocp_tensor view;
+        view.dims = slab_dims(st, batch);
+        view.numel = numel;
+        view.d = st->staging.p;
+        view.owned = false;
+        enqueue_consume(st, &view, seed, batch_id);
+    });
+}
+
+rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int64_t t0,
+                                      int64_t batch, int64_t nb, uint64_t seed,
+                                      uint32_t first_batch_id) {
+    return guarded(st->dev, [&] {
+        check_head_dims(st, x);
+        if (batch < 1 || nb < 1 || t0 < 0 || t0 + batch * nb > x->dims.back())
+            throw_domain("consume_range: slab range out of bounds");
+        rocp_dev* dev = st->dev;
+        const int64_t slice = x->numel / x->dims.back();
+        auto key = std::make_tuple(static_cast<const double*>(x->d), t0, batch, nb, seed, first_batch_id, st->t_len);
+        auto it = st->graphs.find(key);
+        if (it == st->graphs.end()) {
+            st->ensure_batch(batch);
+            const int64_t t_len0 = st->t_len;
+            const uint64_t l0 = dev->launches;
+            cudaGraph_t graph;
+            CK(cudaStreamBeginCapture(dev->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (int64_t b = 0; b < nb; ++b) {
+                    rocp_tensor view;
+                    view.dims = slab_dims(st, batch);
+                    view.numel = slice * batch;
+                    view.d = x->d + (t0 + b * batch) * slice;
+                    enqueue_consume(st, &view, seed, first_batch_id + uint32_t(b));
+                }
+            } catch (...) {
+                cudaStreamEndCapture(dev->stream, &graph);
+                st->t_len = t_len0;
+                throw;
+            }
+            CK(cudaStreamEndCapture(dev->stream, &graph));
+            cudaGraphExec_t exec;
+            CK(cudaGraphInstantiate(&exec, graph, 0));
+            cudaGraphDestroy(graph);
+            const uint64_t nodes = dev->launches - l0;
+            dev->launches = l0;
+            st->t_len = t_len0;
+            it = st->graphs.emplace(key, std::make_pair(exec, nodes)).first;
+        }
+        CK(cudaGraphLaunch(it->second.first, dev->stream));
+        dev->launches += it->second.second;
+        st->t_len += batch * nb;
+    });
+}
+
+rocp_status rocp_stream_update_last_mode_with(rocp_stream* st, const rocp_tensor* x_new,
+                                              const int64_t* rows, int64_t s, double* u_new,
+                                              double* z_s, int* regularized) {
+    return guarded(st->dev, [&] {
+        check_head_dims(st, x_new);
+        if (s != st->s) throw_domain("index set size must equal the stream sample count");
+        rocp_dev* dev = st->dev;
+        const int64_t B = x_new->dims.back();
+        st->ensure_batch(B);
+        int64_t co = prod(st->head);
+        for (int64_t c = 0; c < s; ++c)
+            if (rows[c] < 1 || rows[c] > co) throw_domain("column index out of range");
+        DBuf<int64_t> din(static_cast<size_t>(s));
+        CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
+        draw_and_gather(st, x_new, 0, 0, din.p, nullptr, 0);
+        DBuf<double> du(static_cast<size_t>(B * st->R));
+        int saved[4];
+        CK(cudaMemcpyAsync(saved, st->flags.p, sizeof(saved), cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        CK(cudaMemsetAsync(st->flags.p, 0, sizeof(int), dev->stream));
+        stage_temporal(st, B, du.p);
+        int hf[2];
+        CK(cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        // the replay seam does not touch the stream's own flag (rocp.cpp:71-84 is pure)
+        CK(cudaMemcpyAsync(st->flags.p, saved, sizeof(int), cudaMemcpyHostToDevice, dev->stream));
+        download_colmajor(dev, du.p, B, st->R, u_new);
+        if (z_s) download_colmajor(dev, st->Z[0].p, s, st->R, z_s);
+        if (regularized) *regularized = hf[0] & 1;
+    });
+}
+
+rocp_status rocp_stream_append_temporal(rocp_stream* st, const double* u_new, int64_t batch) {
+    return guarded(st->dev, [&] {
+        if (st->t_len + batch > st->t_cap) throw_domain("temporal capacity exceeded");
+        std::vector<double> rm = colmajor_to_rowmajor(u_new, batch, st->R);
+        CK(cudaMemcpyAsync(st->temporal.p + st->t_len * st->R, rm.data(), rm.size() * 8, cudaMemcpyHostToDevice,
+                           st->dev->stream));
+        CK(cudaStreamSynchronize(st->dev->stream));
+    });
+}
+
+rocp_status rocp_stream_update_mode_with(rocp_stream* st, const rocp_tensor* x_new,
+                                         const double* u_new, int mode, const int64_t* rows,
+                                         int64_t s, double* z_new, double* x_s, int* regularized) {
+    return guarded(st->dev, [&] {
+        check_head_dims(st, x_new);
+        if (mode < 1 || mode >= st->N)
+            throw_domain("update_mode_with: index set must be over a non-temporal mode");  // rocp.cpp:100-101
+        if (s != st->s) throw_domain("index set size must equal the stream sample count");
+        rocp_dev* dev = st->dev;
+        const int64_t B = x_new->dims.back();
+        const std::vector<int64_t> d = slab_dims(st, B);
+        int64_t co = 1;
+        for (int k = 0; k < st->N; ++k)
+            if (k + 1 != mode) co *= d[size_t(k)];
+        for (int64_t c = 0; c < s; ++c)
+            if (rows[c] < 1 || rows[c] > co) throw_domain("column index out of range");
+        DBuf<int64_t> din(static_cast<size_t>(s));
+        CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
+        DBuf<double> du(static_cast<size_t>(B * st->R));
+        upload_rowmajor(dev, u_new, B, st->R, du.p);
+        draw_and_gather(st, x_new, 0, 0, nullptr, din.p, mode);
+        CK(cudaMemsetAsync(st->flags.p + 2, 0, sizeof(int), dev->stream));
+        stage_mode(st, mode, B, du.p);
+        int hf[4];
+        CK(cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+        if (z_new) download_colmajor(dev, st->Z[size_t(mode)].p, s, st->R, z_new);
+        if (x_s) {
+            const int64_t In = st->head[size_t(mode - 1)];
+            CK(cudaMemcpyAsync(x_s, st->X[size_t(mode)].p, size_t(In * s) * 8, cudaMemcpyDeviceToHost, dev->stream));
+        }
+        CK(cudaStreamSynchronize(dev->stream));
+        if (regularized) *regularized = hf[2] & 1;
+    });
+}
+
+rocp_status rocp_stream_finish_batch(rocp_stream* st, int64_t batch) {
+    return guarded(st->dev, [&] { st->t_len += batch; });
+}
+
+rocp_status rocp_stream_get(rocp_stream* st, int what, int mode, double* out) {
+    return guarded(st->dev, [&] {
+        rocp_dev* dev = st->dev;
+        if (what == 3) {
+            download_colmajor(dev, st->temporal.p, st->t_len, st->R, out);
+            return;
+        }
+        if (mode < 1 || mode >= st->N) throw_domain("mode out of range");
+        const int64_t In = st->head[size_t(mode - 1)];
+        if (what == 0) download_colmajor(dev, st->U[size_t(mode - 1)].p, In, st->R, out);
+        else if (what == 1) download_colmajor(dev, st->P[size_t(mode - 1)].p, In, st->R, out);
+        else if (what == 2) download_colmajor(dev, st->Q[size_t(mode - 1)].p, st->R, st->R, out);
+        else throw_domain("bad selector");
+    });
+}
+
+rocp_status rocp_stream_set(rocp_stream* st, int what, int mode, const double* in) {
+    return guarded(st->dev, [&] {
+        rocp_dev* dev = st->dev;
+        if (mode < 1 || mode >= st->N) throw_domain("mode out of range");
+        const int64_t In = st->head[size_t(mode - 1)];
+        if (what == 0) upload_rowmajor(dev, in, In, st->R, st->U[size_t(mode - 1)].p);
+        else if (what == 1) upload_rowmajor(dev, in, In, st->R, st->P[size_t(mode - 1)].p);
+        else if (what == 2) upload_rowmajor(dev, in, st->R, st->R, st->Q[size_t(mode - 1)].p);
+        else throw_domain("bad selector");
+    });
+}
+
+rocp_status rocp_stream_checkpoint(rocp_stream* st) {
+    return guarded(st->dev, [&] {
+        rocp_dev* dev = st->dev;
+        if (st->ckU.empty()) {
+            for (int n = 1; n < st->N; ++n) {
+                st->ckU.emplace_back(st->U[size_t(n - 1)].n);
+                st->ckP.emplace_back(st->P[size_t(n - 1)].n);
+                st->ckQ.emplace_back(st->Q[size_t(n - 1)].n);
+            }
+        }
+        for (int n = 0; n < st->N - 1; ++n) {
+            CK(cudaMemcpyAsync(st->ckU[size_t(n)].p, st->U[size_t(n)].p, st->U[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
+            CK(cudaMemcpyAsync(st->ckP[size_t(n)].p, st->P[size_t(n)].p, st->P[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
+            CK(cudaMemcpyAsync(st->ckQ[size_t(n)].p, st->Q[size_t(n)].p, st->Q[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
+        }
+        int hf[4];
+        CK(cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        st->ck_t_len = st->t_len;
+        st->ck_reg = st->regularized || (hf[0] & 1);
+    });
+}
+
+rocp_status rocp_stream_restore(rocp_stream* st) {
+    return guarded(st->dev, [&] {
+        if (st->ck_t_len < 0) throw RocpError{ROCP_E_STATE, "no checkpoint"};
+        rocp_dev* dev = st->dev;
+        for (int n = 0; n < st->N - 1; ++n) {
+            CK(cudaMemcpyAsync(st->U[size_t(n)].p, st->ckU[size_t(n)].p, st->U[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
+            CK(cudaMemcpyAsync(st->P[size_t(n)].p, st->ckP[size_t(n)].p, st->P[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
+            CK(cudaMemcpyAsync(st->Q[size_t(n)].p, st->ckQ[size_t(n)].p, st->Q[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
+        }
+        const int f0 = st->ck_reg ? 1 : 0;
+        CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));
+        if (f0) CK(cudaMemcpyAsync(st->flags.p, &f0, sizeof(int), cudaMemcpyHostToDevice, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
+        st->t_len = st->ck_t_len;  // temporal rows beyond t_len are rewritten by the next consume
+    });
+}
+
+int64_t rocp_stream_t_len(const rocp_stream* st) { return st ? st->t_len : -1; }
+
+int rocp_stream_regularized(rocp_stream* st) {
+    // The reference's consume raises the stream flag from the temporal solve
+    // only (rocp.cpp:150); flags[0] accumulates device-side.
+    int hf[2] = {0, 0};
+    cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, st->dev->stream);
+    cudaStreamSynchronize(st->dev->stream);
+    return (st->regularized || (hf[0] & 1)) ? 1 : 0;
+}
+
+rocp_status rocp_stream_last_residuals(rocp_stream* st, double* out) {
+    return guarded(st->dev, [&] {
+        std::vector<double> h(size_t(2 * st->N));
+        CK(cudaMemcpyAsync(h.data(), st->resid.p, h.size() * 8, cudaMemcpyDeviceToHost, st->dev->stream));
+        CK(cudaStreamSynchronize(st->dev->stream));
+        for (int k = 0; k < st->N; ++k) {
+            const double num = h[size_t(2 * k)], den = h[size_t(2 * k + 1)];
+            out[k] = den > 0.0 ? std::sqrt(num) / std::sqrt(den) : 0.0;
+        }
+    });
+}
+
+}  // extern "C"
