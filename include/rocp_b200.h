@@ -57,6 +57,12 @@ const char* rocp_last_error(const rocp_dev* dev);
 rocp_status rocp_synchronize(rocp_dev* dev);
 /* Number of kernels this library launched on dev since creation. */
 uint64_t rocp_kernel_launches(const rocp_dev* dev);
+/* CUDA-event timers on the handle's stream (8 slots): record, then the
+ * elapsed milliseconds between two recorded slots (waits for the second). */
+rocp_status rocp_timer_record(rocp_dev* dev, int slot);
+rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms);
+/* The handle's cudaStream_t (for callers that interoperate). */
+void* rocp_cuda_stream(rocp_dev* dev);
 /* Size of the NCCL unique id blob (for the host bootstrap), 0 if no NCCL. */
 int rocp_nccl_id_size(void);
 rocp_status rocp_nccl_get_unique_id(void* out);
@@ -169,6 +175,15 @@ int rocp_stream_regularized(rocp_stream* st);
  * with the counter RNG, (seed, next batch id) is the only other state). */
 rocp_status rocp_stream_checkpoint(rocp_stream* st);
 rocp_status rocp_stream_restore(rocp_stream* st);
+/* Sampled residual per batch: 0 off, 1 temporal solve only (default), 2 every
+ * stage. */
+rocp_status rocp_stream_set_residual_tracking(rocp_stream* st, int level);
+/* CUDA events around every window gather launch (the HBM-bound kernel):
+ * enable, then read the per-launch milliseconds (resets the list). */
+rocp_status rocp_stream_time_gather(rocp_stream* st, int enable);
+rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* count);
+/* Elements (and useful bytes) the current window's gather moves per launch. */
+rocp_status rocp_stream_window_bytes(rocp_stream* st, int64_t* useful, int64_t* elements);
 /* Sampled residual of the last consume (north-star item 5): per stage
  * (temporal, then modes 1..N-1) |X_s - U Z_s^T|_F / |X_s|_F.  out[N]. */
 rocp_status rocp_stream_last_residuals(rocp_stream* st, double* out);

@@ -145,19 +145,28 @@ void decode(Index j, const Dims& d, int mode, Index* multi) {
 }
 
 // ---------------------------------------------------------------------------
-// Canonical sample reduction: chunks of 32 consecutive samples,
-// each an fma chain from +0.0 in increasing sample order; chunk partials are
-// summed in increasing chunk order starting from the first partial.
+// Canonical sample reduction, two levels:
+//   chunk k      = 32 consecutive samples, an fma chain from +0.0 in
+//                  increasing sample order -> p_k
+//   superchunk m = chunks 8m..8m+7 (256 samples), q_m = p_8m + p_8m+1 + ...
+//                  summed in increasing order starting from p_8m
+//   total        = q_0 + q_1 + ... in increasing order starting from q_0.
 constexpr Index kChunk = 32;
+constexpr Index kSuper = 8;  // chunks per superchunk
 
 template <class A, class B>
 double sample_dot(Index s, A a, B b) {
     double total = 0.0;
-    for (Index c0 = 0; c0 < s; c0 += kChunk) {
-        double p = 0.0;
-        const Index c1 = std::min(s, c0 + kChunk);
-        for (Index c = c0; c < c1; ++c) p = std::fma(a(c), b(c), p);
-        total = (c0 == 0) ? p : total + p;
+    for (Index m0 = 0; m0 < s; m0 += kChunk * kSuper) {
+        double q = 0.0;
+        const Index m1 = std::min(s, m0 + kChunk * kSuper);
+        for (Index c0 = m0; c0 < m1; c0 += kChunk) {
+            double p = 0.0;
+            const Index c1 = std::min(m1, c0 + kChunk);
+            for (Index c = c0; c < c1; ++c) p = std::fma(a(c), b(c), p);
+            q = (c0 == m0) ? p : q + p;
+        }
+        total = (m0 == 0) ? q : total + q;
     }
     return total;
 }
@@ -172,13 +181,36 @@ Mat gram_of(const Mat& z) {  // Z^T Z (solve.cpp:41, rocp.cpp:63,108)
     return g;
 }
 
-Mat contract_of(const Mat& x, const Mat& z) {  // X_s Z (solve.cpp:42, rocp.cpp:107)
+// X_s Z (solve.cpp:42, rocp.cpp:107).  Same per-output operation sequence as
+// sample_dot; the loops run over rows innermost so the compiler vectorises
+// across independent outputs (the baseline is a fair single-thread port).
+Mat contract_of(const Mat& x, const Mat& z) {
     const Index I = x.rows, s = x.cols, R = z.cols;
     Mat out(I, R);
-    for (Index r = 0; r < R; ++r)
-        for (Index i = 0; i < I; ++i)
-            out(i, r) = sample_dot(
-                s, [&](Index c) { return x(i, c); }, [&](Index c) { return z(c, r); });
+    std::vector<double> p(static_cast<size_t>(I)), q(static_cast<size_t>(I));
+    for (Index r = 0; r < R; ++r) {
+        double* tot = &out.v[size_t(r * I)];
+        for (Index m0 = 0; m0 < s; m0 += kChunk * kSuper) {
+            const Index m1 = std::min(s, m0 + kChunk * kSuper);
+            for (Index c0 = m0; c0 < m1; c0 += kChunk) {
+                std::fill(p.begin(), p.end(), 0.0);
+                const Index c1 = std::min(m1, c0 + kChunk);
+                for (Index c = c0; c < c1; ++c) {
+                    const double zc = z(c, r);
+                    const double* xc = &x.v[size_t(c * I)];
+                    for (Index i = 0; i < I; ++i) p[size_t(i)] = std::fma(xc[i], zc, p[size_t(i)]);
+                }
+                if (c0 == m0)
+                    for (Index i = 0; i < I; ++i) q[size_t(i)] = p[size_t(i)];
+                else
+                    for (Index i = 0; i < I; ++i) q[size_t(i)] = q[size_t(i)] + p[size_t(i)];
+            }
+            if (m0 == 0)
+                for (Index i = 0; i < I; ++i) tot[i] = q[size_t(i)];
+            else
+                for (Index i = 0; i < I; ++i) tot[i] = tot[i] + q[size_t(i)];
+        }
+    }
     return out;
 }
 
@@ -437,16 +469,26 @@ double fit_sumsq(const double* t, const Dims& d, const std::vector<Mat>* fs) {
 double sampled_residual(const Mat& x, const Mat& u, const Mat& z) {
     const Index I = x.rows, S = x.cols, R = z.cols;
     std::vector<double> num(static_cast<size_t>(S)), den(static_cast<size_t>(S));
+    std::vector<double> uz(static_cast<size_t>(I));
     for (Index c = 0; c < S; ++c) {
+        // uz(i) = fma chain over r from +0.0, vectorised across i
+        std::fill(uz.begin(), uz.end(), 0.0);
+        for (Index r = 0; r < R; ++r) {
+            const double zc = z(c, r);
+            const double* ur = &u.v[size_t(r * I)];
+            for (Index i = 0; i < I; ++i) uz[size_t(i)] = std::fma(ur[i], zc, uz[size_t(i)]);
+        }
         double qn[32], qd[32];
         for (int l = 0; l < 32; ++l) qn[l] = qd[l] = 0.0;
-        for (Index i = 0; i < I; ++i) {
-            double uz = 0.0;
-            for (Index r = 0; r < R; ++r) uz = std::fma(u(i, r), z(c, r), uz);
-            const double xv = x(i, c);
-            const double e = xv - uz;
-            qn[i % 32] = std::fma(e, e, qn[i % 32]);
-            qd[i % 32] = std::fma(xv, xv, qd[i % 32]);
+        const double* xc = &x.v[size_t(c * I)];
+        for (Index i0 = 0; i0 < I; i0 += 32) {
+            const int nl = int(std::min<Index>(32, I - i0));
+            for (int l = 0; l < nl; ++l) {
+                const double xv = xc[i0 + l];
+                const double e = xv - uz[size_t(i0 + l)];
+                qn[l] = std::fma(e, e, qn[l]);
+                qd[l] = std::fma(xv, xv, qd[l]);
+            }
         }
         num[size_t(c)] = butterfly32(qn);
         den[size_t(c)] = butterfly32(qd);
@@ -483,6 +525,7 @@ struct orc_stream {
     std::vector<Mat> p, q;
     Index t_len = 0;
     bool regularized = false;
+    int resid_level = 1;             // 0 none, 1 temporal stage only, 2 every stage
     std::vector<double> last_resid;  // per stage of the last consume
 };
 
@@ -790,7 +833,7 @@ int orc_stream_update_last_mode_with(orc_stream* st, const double* x_new, int64_
     bool reg = false;
     const Mat u = sampled_ls(z, xs, &reg, nullptr);
     st->last_resid.assign(size_t(st->order), 0.0);
-    st->last_resid[0] = sampled_residual(xs, u, z);
+    if (st->resid_level >= 1) st->last_resid[0] = sampled_residual(xs, u, z);
     to_ptr(u, u_new);
     if (z_s) to_ptr(z, z_s);
     if (regularized) *regularized = reg;
@@ -836,7 +879,7 @@ int orc_stream_update_mode_with(orc_stream* st, const double* x_new, int64_t bat
     for (size_t e = 0; e < q.v.size(); ++e) q.v[e] = q.v[e] + g.v[e];
     bool reg = false;
     st->factors[size_t(mode - 1)] = solve_gram_m(q, p, &reg);
-    if (st->last_resid.size() == size_t(st->order))
+    if (st->resid_level >= 2 && st->last_resid.size() == size_t(st->order))
         st->last_resid[size_t(mode)] = sampled_residual(xs, st->factors[size_t(mode - 1)], z);
     if (z_new) to_ptr(z, z_new);
     if (x_s) to_ptr(xs, x_s);
@@ -902,6 +945,11 @@ int orc_stream_set(orc_stream* st, int what, int mode, const double* in) {
 }
 
 int64_t orc_stream_t_len(const orc_stream* st) { return st->t_len; }
+
+int orc_stream_set_residual_level(orc_stream* st, int level) {
+    st->resid_level = level;
+    return ORC_OK;
+}
 
 int orc_stream_last_residuals(const orc_stream* st, double* out) {
     if (st->last_resid.size() != size_t(st->order)) return fail(ORC_E_DOMAIN, "no consume yet");

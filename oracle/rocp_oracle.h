@@ -126,7 +126,9 @@ int orc_stream_finish_batch(orc_stream* st, int64_t batch);
 int orc_stream_get(const orc_stream* st, int what, int mode, double* out);
 int orc_stream_set(orc_stream* st, int what, int mode, const double* in);
 int64_t orc_stream_t_len(const orc_stream* st);
-/* Sampled residuals of the last consume: [temporal, mode 1, ..., mode N-1]. */
+/* Sampled residuals of the last consume: [temporal, mode 1, ..., mode N-1];
+ * level 0 none, 1 temporal stage only (default), 2 every stage. */
+int orc_stream_set_residual_level(orc_stream* st, int level);
 int orc_stream_last_residuals(const orc_stream* st, double* out);
 int orc_sampled_residual(const double* x, int64_t rows, int64_t s, const double* u,
                          const double* z, int rank, double* out);

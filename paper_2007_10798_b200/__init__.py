@@ -90,6 +90,13 @@ SIGNATURES = [
     ("rocp_stream_last_residuals", C.c_int, [_vp, _f64p]),
     ("rocp_stream_checkpoint", C.c_int, [_vp]),
     ("rocp_stream_restore", C.c_int, [_vp]),
+    ("rocp_timer_record", C.c_int, [_vp, C.c_int]),
+    ("rocp_timer_elapsed_ms", C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
+    ("rocp_cuda_stream", _vp, [_vp]),
+    ("rocp_stream_set_residual_tracking", C.c_int, [_vp, C.c_int]),
+    ("rocp_stream_time_gather", C.c_int, [_vp, C.c_int]),
+    ("rocp_stream_gather_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
+    ("rocp_stream_window_bytes", C.c_int, [_vp, _i64p, _i64p]),
 ]
 
 
@@ -215,6 +222,14 @@ class Device:
     def tensor(self, dims, host=None):
         return DeviceTensor(self, dims, host)
 
+    def timer_record(self, slot):
+        self.check(lib().rocp_timer_record(self.h, slot))
+
+    def timer_elapsed_ms(self, a, b):
+        ms = C.c_float(0)
+        self.check(lib().rocp_timer_elapsed_ms(self.h, a, b, C.byref(ms)))
+        return float(ms.value)
+
 
 class DeviceTensor:
     """Device-resident DenseTensor (tensor.hpp:17-49), fp64, first index fastest."""
@@ -258,8 +273,11 @@ class DeviceTensor:
         dims[-1] = length
         return DeviceTensor(self.dev, dims, _handle=h, _parent=self)
 
-    def download(self):
-        out = np.empty(self.numel, dtype=np.float64)
+    def download(self, out=None):
+        if out is None:
+            out = np.empty(self.numel, dtype=np.float64)
+        if out.size != self.numel or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise DomainError(E_DOMAIN, "download target must be a contiguous float64 array of numel")
         self.dev.check(lib().rocp_tensor_download(self.dev.h, self.h, _p(out)))
         return out
 
@@ -522,6 +540,23 @@ class RocpStream:
         out = np.zeros(self.order)
         self.dev.check(lib().rocp_stream_last_residuals(self.h, _p(out)))
         return out
+
+    def set_residual_tracking(self, enable):
+        self.dev.check(lib().rocp_stream_set_residual_tracking(self.h, int(enable)))
+
+    def time_gather(self, enable):
+        self.dev.check(lib().rocp_stream_time_gather(self.h, int(enable)))
+
+    def gather_times(self, max_n=4096):
+        buf = (C.c_float * max_n)()
+        cnt = C.c_int(0)
+        self.dev.check(lib().rocp_stream_gather_times(self.h, buf, max_n, C.byref(cnt)))
+        return [float(buf[k]) for k in range(min(cnt.value, max_n))]
+
+    def window_bytes(self):
+        u, e = C.c_int64(0), C.c_int64(0)
+        self.dev.check(lib().rocp_stream_window_bytes(self.h, C.byref(u), C.byref(e)))
+        return int(u.value), int(e.value)
 
     def checkpoint(self):
         self.dev.check(lib().rocp_stream_checkpoint(self.h))

@@ -21,6 +21,8 @@ namespace rocpk {
 
 constexpr int kMaxOrder = 8;
 constexpr int kChunk = 32;       // canonical sample-reduction chunk
+constexpr int kSuper = 8;        // chunks per canonical superchunk (256 samples)
+constexpr int kSuperSamples = kChunk * kSuper;
 constexpr int kGroup = 256;      // canonical hsum group
 constexpr double kGramConditionLimit = 1e12;  // reference solve.hpp:15
 
@@ -50,9 +52,13 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 // ---------------------------------------------------------------------------
 // K1: draw (or decode explicit rows) + Eq.(1) decode + fibre base offset.
 // Replaces draw_samples / SampleIndexSet::from_rows / decode_index
-// (sampling.cpp:11-55, tensor.cpp:96-109).
+// (sampling.cpp:11-55, tensor.cpp:96-109).  One launch serves any number of
+// jobs (blockIdx.y = job), so every draw of a whole stream window is one
+// launch: sample indices never depend on factors.
 struct DrawJob {
     uint64_t seed;
+    const uint64_t* seed_ptr;      // if set, the seed is read from device memory
+    const uint32_t* batch_ptr;     // if set, batch = *batch_ptr + batch (window offset)
     uint32_t batch, iteration, mode;  // mode 1-based
     int n_other;
     int32_t s;
@@ -64,20 +70,18 @@ struct DrawJob {
     int32_t* idx;                  // s x n_other, 0-based
     int64_t* base;                 // s
 };
-struct DrawBatch {
-    int njobs;
-    DrawJob job[kMaxOrder];
-};
 
-__global__ void k_draw(const DrawBatch b) {
-    const DrawJob& J = b.job[blockIdx.y];
+__global__ void __launch_bounds__(128) k_draw(const DrawJob* __restrict__ jobs) {
+    const DrawJob& J = jobs[blockIdx.y];
+    const uint64_t seed = J.seed_ptr ? *J.seed_ptr : J.seed;
+    const uint32_t batch = J.batch_ptr ? *J.batch_ptr + J.batch : J.batch;
     for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < J.s; c += gridDim.x * blockDim.x) {
         int64_t j0;
         if (J.in_rows) {
             j0 = J.in_rows[c] - 1;
         } else {
-            uint32_t ctr[4] = {uint32_t(c), J.mode, J.iteration, J.batch};
-            philox4x32_10(ctr, uint32_t(J.seed), uint32_t(J.seed >> 32));
+            uint32_t ctr[4] = {uint32_t(c), J.mode, J.iteration, batch};
+            philox4x32_10(ctr, uint32_t(seed), uint32_t(seed >> 32));
             const uint64_t u = uint64_t(ctr[0]) | (uint64_t(ctr[1]) << 32);
             j0 = int64_t(__umul64hi(u, uint64_t(J.co)));
         }
@@ -95,11 +99,19 @@ __global__ void k_draw(const DrawBatch b) {
     }
 }
 
+__global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+__global__ void k_set_i32(int* p, int n, int v) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
+}
+
 // ---------------------------------------------------------------------------
 // K2: sampled-fibre gather, X_s(i, c) = T[base_c + i * ms].  Replaces
-// sample_unfolding (sampling.cpp:57-79).  Grid-stride over (i, c) with i
-// fastest: coalesced writes, coalesced reads for the contiguous mode-1 fibres,
-// and UNROLL independent loads in flight per thread for the strided modes
+// sample_unfolding (sampling.cpp:57-79).  HBM-bound: the whole stream
+// window's gathers (every batch, every stage) are one launch over a flat tile
+// list, each tile kGatherTile consecutive elements of one job with i fastest:
+// coalesced writes, coalesced reads along the contiguous mode-1 fibres, and
+// kGatherUnroll independent loads in flight per thread for the strided modes
 // (each element its own 32-B sector).
 struct GatherJob {
     const double* t;
@@ -109,32 +121,37 @@ struct GatherJob {
     int32_t s;
     double* out;
 };
-struct GatherBatch {
-    int njobs;
-    GatherJob job[kMaxOrder];
+struct GatherTile {
+    int32_t job;
+    uint32_t e0;
 };
+constexpr int kGatherThreads = 256;
+constexpr int kGatherUnroll = 8;
+constexpr int kGatherTile = kGatherThreads * kGatherUnroll;
 
-template <int UNROLL>
-__global__ void __launch_bounds__(256) k_gather(const GatherBatch b) {
-    const GatherJob& J = b.job[blockIdx.y];
+__global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherJob* __restrict__ jobs,
+                                                           const GatherTile* __restrict__ tiles) {
+    const GatherTile tile = tiles[blockIdx.x];
+    const GatherJob& J = jobs[tile.job];
     const uint32_t total = uint32_t(J.I) * uint32_t(J.s);
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * UNROLL) {
-        double v[UNROLL];
+    const double* __restrict__ t = J.t;
+    const int64_t* __restrict__ base = J.base;
+    const int64_t ms = J.ms;
+    const uint32_t I = uint32_t(J.I);
+    double v[kGatherUnroll];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const uint32_t e = e0 + u * stride;
-            if (e < total) {
-                const uint32_t c = e / uint32_t(J.I);
-                const uint32_t i = e - c * uint32_t(J.I);
-                v[u] = __ldg(J.t + J.base[c] + int64_t(i) * J.ms);
-            }
+    for (int u = 0; u < kGatherUnroll; ++u) {
+        const uint32_t e = tile.e0 + u * kGatherThreads + threadIdx.x;
+        if (e < total) {
+            const uint32_t c = e / I;
+            const uint32_t i = e - c * I;
+            v[u] = __ldcs(t + __ldg(base + c) + int64_t(i) * ms);
         }
+    }
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const uint32_t e = e0 + u * stride;
-            if (e < total) J.out[e] = v[u];
-        }
+    for (int u = 0; u < kGatherUnroll; ++u) {
+        const uint32_t e = tile.e0 + u * kGatherThreads + threadIdx.x;
+        if (e < total) J.out[e] = v[u];
     }
 }
 
@@ -211,67 +228,141 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int3
     if (!last_block_arrive(counter)) return;
     const int nk = gridDim.x;
     for (int p = threadIdx.x; p < RR; p += blockDim.x) {
-        const volatile double* vp = partial;
-        double tot = vp[p];
-        for (int kk = 1; kk < nk; ++kk) tot = tot + vp[int64_t(kk) * RR + p];
+        // two-level canonical combine: superchunks of kSuper chunks
+        double tot = 0.0;
+        for (int m0 = 0; m0 < nk; m0 += kSuper) {
+            const int m1 = min(nk, m0 + kSuper);
+            double pk[kSuper];
+#pragma unroll
+            for (int u = 0; u < kSuper; ++u)
+                pk[u] = (m0 + u < m1) ? __ldcg(partial + int64_t(m0 + u) * RR + p) : 0.0;
+            double q = pk[0];
+#pragma unroll
+            for (int u = 1; u < kSuper; ++u)
+                if (m0 + u < m1) q = q + pk[u];
+            tot = (m0 == 0) ? q : tot + q;
+        }
         out[p] = acc_base ? acc_base[p] + tot : tot;  // column-major == row-major (symmetric)
     }
 }
 
 // ---------------------------------------------------------------------------
 // K4b: skinny contraction out = X_s Z (I x S times S x R; solve.cpp:42,
-// rocp.cpp:107), canonical chunked order, optionally out = base + X_s Z.
-// Thread per (row i, RB consecutive r); Z chunk staged in shared memory
-// (broadcast reads); X_s loads coalesced along i.
+// rocp.cpp:107), canonical two-level order, optionally out = base + X_s Z.
+// Block = (32-row tile, one 256-sample superchunk): the X_s tile (32 x 256)
+// and the Z tile (256 x R) are staged in shared memory with cp.async (all
+// loads in flight at once: one memory round trip per block), then each thread
+// (row lane, r-group of RB outputs) runs the 8 chunk fma chains from shared
+// memory.  With more than one superchunk, partials go to `partial` and the
+// last block of each row tile combines them in superchunk order.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+constexpr int kRowTile = 32;
+
+__device__ __forceinline__ bool last_arrive_of(unsigned int* counter, unsigned int expected) {
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(counter, 1u);
+        is_last = (prev == expected - 1);
+        if (is_last) *counter = 0u;
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
 template <int RB>
-__global__ void __launch_bounds__(128) k_contract(const double* __restrict__ X, int32_t I, int32_t s,
+__global__ void __launch_bounds__(256) k_contract(const double* __restrict__ X, int32_t I, int32_t S,
                                                   const double* __restrict__ Z, int R,
-                                                  const double* base, double* __restrict__ out) {
-    __shared__ double zs[kChunk][RB];
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r0 = blockIdx.y * RB;
-    double tot[RB];
+                                                  const double* base, double* out,
+                                                  double* __restrict__ partial,
+                                                  unsigned int* __restrict__ counters) {
+    extern __shared__ double sm[];
+    const int RP = int(blockDim.x >> 5) * RB;    // R padded to the r-groups (zero columns)
+    double* xs = sm;                            // [256][32]
+    double* zs = sm + kSuperSamples * kRowTile;  // [256][RP]
+    const int tile = blockIdx.x, m = blockIdx.y, nsuper = gridDim.y;
+    const int i0 = tile * kRowTile;
+    const int c0 = m * kSuperSamples;
+    const int cn = min(kSuperSamples, S - c0);
+    const int rows = min(kRowTile, I - i0);
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kRowTile * cn; e += blockDim.x) {
+        const int c = e >> 5, r = e & 31;
+        if (r < rows) cp_async8(xs + e, X + int64_t(c0 + c) * I + i0 + r);
+        else xs[e] = 0.0;
+    }
+    for (int e = tid; e < cn * RP; e += blockDim.x) {
+        const int c = e / RP, r = e - c * RP;
+        if (r < R) cp_async8(zs + e, Z + int64_t(c0 + c) * R + r);
+        else zs[e] = 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int lane = tid & 31, rg = tid >> 5;
+    const int r0 = rg * RB;
+    double q[RB];
 #pragma unroll
-    for (int j = 0; j < RB; ++j) tot[j] = 0.0;
-    for (int32_t c0 = 0; c0 < s; c0 += kChunk) {
-        __syncthreads();
-        for (int t = threadIdx.x; t < kChunk * RB; t += blockDim.x) {
-            const int cc = t / RB, rr = t % RB;
-            zs[cc][rr] = (c0 + cc < s && r0 + rr < R) ? Z[int64_t(c0 + cc) * R + r0 + rr] : 0.0;
-        }
-        __syncthreads();
+    for (int j = 0; j < RB; ++j) q[j] = 0.0;
+    for (int k = 0; k < kSuper; ++k) {
+        const int cc0 = k * kChunk;
+        if (cc0 >= cn) break;
+        const int ccn = min(kChunk, cn - cc0);
         double p[RB];
 #pragma unroll
         for (int j = 0; j < RB; ++j) p[j] = 0.0;
-        const int cn = min(kChunk, s - c0);
-        if (i < I) {
-            const double* xc = X + int64_t(c0) * I + i;
-            if (cn == kChunk) {
+        if (ccn == kChunk) {
 #pragma unroll 8
-                for (int cc = 0; cc < kChunk; ++cc) {
-                    const double x = __ldg(xc + int64_t(cc) * I);
+            for (int cc = 0; cc < kChunk; ++cc) {
+                const double x = xs[(cc0 + cc) * kRowTile + lane];
+                const double* zr = zs + (cc0 + cc) * RP + r0;
 #pragma unroll
-                    for (int j = 0; j < RB; ++j) p[j] = __fma_rn(x, zs[cc][j], p[j]);
-                }
-            } else {
-                for (int cc = 0; cc < cn; ++cc) {
-                    const double x = __ldg(xc + int64_t(cc) * I);
+                for (int j = 0; j < RB; ++j) p[j] = __fma_rn(x, zr[j], p[j]);
+            }
+        } else {
+            for (int cc = 0; cc < ccn; ++cc) {
+                const double x = xs[(cc0 + cc) * kRowTile + lane];
+                const double* zr = zs + (cc0 + cc) * RP + r0;
 #pragma unroll
-                    for (int j = 0; j < RB; ++j) p[j] = __fma_rn(x, zs[cc][j], p[j]);
-                }
+                for (int j = 0; j < RB; ++j) p[j] = __fma_rn(x, zr[j], p[j]);
             }
         }
 #pragma unroll
-        for (int j = 0; j < RB; ++j) tot[j] = (c0 == 0) ? p[j] : tot[j] + p[j];
+        for (int j = 0; j < RB; ++j) q[j] = (k == 0) ? p[j] : q[j] + p[j];
     }
-    if (i < I) {
+    const int i = i0 + lane;
+    const bool live = lane < rows;
+    if (nsuper == 1) {
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                if (r0 + j >= R) break;
+                const int64_t o = int64_t(i) * R + r0 + j;
+                out[o] = base ? base[o] + q[j] : q[j];
+            }
+        }
+        return;
+    }
+    if (live) {
+#pragma unroll
+        for (int j = 0; j < RB; ++j)
+            if (r0 + j < R) partial[(int64_t(m) * I + i) * R + r0 + j] = q[j];
+    }
+    if (!last_arrive_of(counters + tile, unsigned(nsuper))) return;
+    if (live) {
 #pragma unroll
         for (int j = 0; j < RB; ++j) {
-            const int r = r0 + j;
-            if (r < R) {
-                const int64_t o = int64_t(i) * R + r;
-                out[o] = base ? base[o] + tot[j] : tot[j];
-            }
+            if (r0 + j >= R) break;
+            const int64_t o = int64_t(i) * R + r0 + j;
+            double tot = __ldcg(partial + o);
+            for (int mm = 1; mm < nsuper; ++mm) tot = tot + __ldcg(partial + int64_t(mm) * I * R + o);
+            out[o] = base ? base[o] + tot : tot;
         }
     }
 }
@@ -296,6 +387,7 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
     __shared__ double D[MAXR];
     __shared__ int s_mode;  // 0 = zero solution, 1 = solve
     __shared__ int s_reg;
+    __shared__ double s_tr;
     const int tid = threadIdx.x;
 
     auto load = [&](double lambda) {
@@ -321,10 +413,15 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
         __syncthreads();
     };
 
+    for (int k = tid; k < R; k += blockDim.x) D[k] = G[k * R + k];  // diagonal, staged
+    __syncthreads();
     if (tid == 0) {
-        double maxdiag = G[0];
+        double maxdiag = D[0];
         for (int k = 1; k < R; ++k)
-            if (G[k * R + k] > maxdiag) maxdiag = G[k * R + k];
+            if (D[k] > maxdiag) maxdiag = D[k];
+        double tr = D[0];
+        for (int k = 1; k < R; ++k) tr = tr + D[k];
+        s_tr = tr;
         s_mode = (maxdiag <= 0.0) ? 0 : 1;
         s_reg = (s_mode == 0) ? 1 : 0;
     }
@@ -342,9 +439,7 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
         }
         __syncthreads();
         if (s_reg) {
-            double tr = G[0];
-            for (int k = 1; k < R; ++k) tr = tr + G[k * R + k];
-            load(1e-12 * tr);
+            load(1e-12 * s_tr);
             factor();
         }
     }

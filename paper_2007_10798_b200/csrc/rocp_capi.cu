@@ -107,6 +107,18 @@ void rowmajor_to_colmajor(const double* a, int64_t rows, int64_t cols, double* o
         for (int64_t j = 0; j < cols; ++j) out[i + j * rows] = a[size_t(i * cols + j)];
 }
 
+// Device copies of a list of draw jobs and gather jobs (+ the flat tile list
+// of the gather).  Built on the host, uploaded once, then launched any number
+// of times (also from inside CUDA graphs).
+struct JobList {
+    DBuf<DrawJob> draw;
+    DBuf<GatherJob> gather;
+    DBuf<GatherTile> tiles;
+    int ndraw = 0, ngather = 0, ntiles = 0;
+    int64_t max_s = 0;
+    int64_t gather_elems = 0;
+};
+
 }  // namespace
 
 // ===========================================================================
@@ -120,6 +132,11 @@ struct rocp_dev {
     DBuf<int> flags;              // [0] regularized, [1] non-finite code
     DBuf<double> scalars;         // small results
     DBuf<double> scratch_a, scratch_b;  // reduction partials
+    JobList jobs;                       // draw/gather job scratch of the primitives and cprand
+    DBuf<double> contract_partial;      // split-superchunk contraction partials
+    DBuf<unsigned int> tile_counters;   // per-row-tile arrival counters (self-resetting)
+    DBuf<int64_t> rows_in;              // explicit index scratch of the primitives
+    cudaEvent_t timer[8] = {};          // rocp_timer_* slots
     int num_sms = 148;
     // device-resident result of the last rocp_cprand (for stream_create_from_init)
     struct Init {
@@ -168,6 +185,8 @@ DrawJob make_draw(const std::vector<int64_t>& d, int mode, int64_t s, uint64_t s
                   int64_t* base) {
     DrawJob j{};
     j.seed = seed;
+    j.seed_ptr = nullptr;
+    j.batch_ptr = nullptr;
     j.batch = batch;
     j.iteration = iteration;
     j.mode = uint32_t(mode);
@@ -191,16 +210,55 @@ DrawJob make_draw(const std::vector<int64_t>& d, int mode, int64_t s, uint64_t s
     return j;
 }
 
-void launch_draw(rocp_dev* dev, const DrawBatch& b, int64_t max_s) {
-    dim3 grid(grid_for(max_s, 128, 64), b.njobs);
-    k_draw<<<grid, 128, 0, dev->stream>>>(b);
+GatherJob make_gather(const double* t, const std::vector<int64_t>& d, int mode, int64_t s,
+                      const int64_t* base, double* out) {
+    GatherJob g{};
+    g.t = t;
+    g.base = base;
+    g.ms = strides_of(d)[size_t(mode - 1)];
+    g.I = int32_t(d[size_t(mode - 1)]);
+    g.s = int32_t(s);
+    g.out = out;
+    return g;
+}
+
+void upload_jobs(rocp_dev* dev, JobList& L, const std::vector<DrawJob>& dj,
+                 const std::vector<GatherJob>& gj) {
+    std::vector<GatherTile> tiles;
+    L.gather_elems = 0;
+    for (size_t k = 0; k < gj.size(); ++k) {
+        const uint32_t total = uint32_t(gj[k].I) * uint32_t(gj[k].s);
+        L.gather_elems += total;
+        for (uint32_t e0 = 0; e0 < total; e0 += kGatherTile) tiles.push_back(GatherTile{int32_t(k), e0});
+    }
+    L.max_s = 0;
+    for (const DrawJob& j : dj) L.max_s = std::max<int64_t>(L.max_s, j.s);
+    L.draw.ensure(std::max<size_t>(dj.size(), 1));
+    L.gather.ensure(std::max<size_t>(gj.size(), 1));
+    L.tiles.ensure(std::max<size_t>(tiles.size(), 1));
+    if (!dj.empty())
+        CK(cudaMemcpyAsync(L.draw.p, dj.data(), dj.size() * sizeof(DrawJob), cudaMemcpyHostToDevice, dev->stream));
+    if (!gj.empty())
+        CK(cudaMemcpyAsync(L.gather.p, gj.data(), gj.size() * sizeof(GatherJob), cudaMemcpyHostToDevice, dev->stream));
+    if (!tiles.empty())
+        CK(cudaMemcpyAsync(L.tiles.p, tiles.data(), tiles.size() * sizeof(GatherTile), cudaMemcpyHostToDevice,
+                           dev->stream));
+    CK(cudaStreamSynchronize(dev->stream));
+    L.ndraw = int(dj.size());
+    L.ngather = int(gj.size());
+    L.ntiles = int(tiles.size());
+}
+
+void launch_draw(rocp_dev* dev, const JobList& L) {
+    if (L.ndraw == 0) return;
+    dim3 grid(grid_for(L.max_s, 128, 64), unsigned(L.ndraw));
+    k_draw<<<grid, 128, 0, dev->stream>>>(L.draw.p);
     after_launch(dev, "k_draw");
 }
 
-void launch_gather(rocp_dev* dev, const GatherBatch& b, int64_t max_elems) {
-    constexpr int kUnroll = 4;
-    dim3 grid(grid_for((max_elems + kUnroll - 1) / kUnroll, 256, dev->num_sms * 8), b.njobs);
-    k_gather<kUnroll><<<grid, 256, 0, dev->stream>>>(b);
+void launch_gather(rocp_dev* dev, const JobList& L) {
+    if (L.ntiles == 0) return;
+    k_gather<<<L.ntiles, kGatherThreads, 0, dev->stream>>>(L.gather.p, L.tiles.p);
     after_launch(dev, "k_gather");
 }
 
@@ -218,22 +276,83 @@ void launch_gram(rocp_dev* dev, const double* Z, int64_t s, int R, const double*
     after_launch(dev, "k_gram");
 }
 
+// Contraction launch: r-groups of RB <= 10 outputs per thread (32 rows per
+// warp), 256-sample superchunks split across blocks.
+constexpr int kMaxContractGroups = 8;
+
+int contract_groups(int R, int* rb) {
+    const int ng = (R + 9) / 10;
+    *rb = (R + ng - 1) / ng;
+    return ng;
+}
+
+size_t contract_smem(int R) {
+    int rb;
+    const int ng = contract_groups(R, &rb);
+    return (size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * ng * rb) * sizeof(double);
+}
+
 template <int RB>
-void launch_contract_rb(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
+void launch_contract_rb(rocp_dev* dev, int ng, const double* X, int64_t I, int64_t s, const double* Z, int R,
                         const double* base, double* out) {
-    dim3 grid(unsigned((I + 127) / 128), unsigned((R + RB - 1) / RB));
-    k_contract<RB><<<grid, 128, 0, dev->stream>>>(X, int32_t(I), int32_t(s), Z, R, base, out);
+    const int tiles = int((I + kRowTile - 1) / kRowTile);
+    const int nsuper = int((s + kSuperSamples - 1) / kSuperSamples);
+    if (nsuper > 1) {
+        if (dev->contract_partial.n < size_t(nsuper) * I * R || dev->tile_counters.n < size_t(tiles))
+            throw RocpError{ROCP_E_STATE, "contraction scratch not reserved (internal)"};
+    }
+    const dim3 grid{unsigned(tiles), unsigned(nsuper), 1u};
+    k_contract<RB><<<grid, 32 * ng, contract_smem(R), dev->stream>>>(
+        X, int32_t(I), int32_t(s), Z, R, base, out, dev->contract_partial.p, dev->tile_counters.p);
     after_launch(dev, "k_contract");
+}
+
+// Reserves the split-superchunk scratch (outside any graph capture).
+void reserve_contract(rocp_dev* dev, int64_t I, int64_t s, int R) {
+    const int64_t tiles = (I + kRowTile - 1) / kRowTile;
+    const int64_t nsuper = (s + kSuperSamples - 1) / kSuperSamples;
+    if (nsuper <= 1) return;
+    if (dev->contract_partial.n < size_t(nsuper * I * R)) {
+        CK(cudaStreamSynchronize(dev->stream));
+        dev->contract_partial.alloc(size_t(nsuper * I * R));
+    }
+    if (dev->tile_counters.n < size_t(tiles)) {
+        CK(cudaStreamSynchronize(dev->stream));
+        dev->tile_counters.alloc(size_t(tiles));
+        CK(cudaMemset(dev->tile_counters.p, 0, size_t(tiles) * sizeof(unsigned int)));
+    }
 }
 
 void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
                      const double* base, double* out) {
-    if (R % 10 == 0) launch_contract_rb<10>(dev, X, I, s, Z, R, base, out);
-    else if (R % 8 == 0) launch_contract_rb<8>(dev, X, I, s, Z, R, base, out);
-    else if (R % 5 == 0) launch_contract_rb<5>(dev, X, I, s, Z, R, base, out);
-    else if (R % 4 == 0) launch_contract_rb<4>(dev, X, I, s, Z, R, base, out);
-    else if (R <= 4) launch_contract_rb<4>(dev, X, I, s, Z, R, base, out);
-    else launch_contract_rb<8>(dev, X, I, s, Z, R, base, out);
+    int rb;
+    const int ng = contract_groups(R, &rb);
+    switch (rb) {
+        case 1: launch_contract_rb<1>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 2: launch_contract_rb<2>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 3: launch_contract_rb<3>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 4: launch_contract_rb<4>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 5: launch_contract_rb<5>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 6: launch_contract_rb<6>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 7: launch_contract_rb<7>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 8: launch_contract_rb<8>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 9: launch_contract_rb<9>(dev, ng, X, I, s, Z, R, base, out); break;
+        default: launch_contract_rb<10>(dev, ng, X, I, s, Z, R, base, out); break;
+    }
+}
+
+void set_contract_smem_attrs() {
+    const int mx = int((size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * 70) * sizeof(double));
+    CK(cudaFuncSetAttribute(k_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(k_contract<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 }
 
 // flags: [0] |= 1 when regularized, [1] = nonfinite_code on a non-finite output.
@@ -339,6 +458,27 @@ void check_rank(int R) {
 
 // ===========================================================================
 // Stream state (RocpStream, rocp.hpp:85-107 + ComplementaryState :15-24).
+//
+// A "window" holds the sample indices and gathered fibres of nb consecutive
+// batches: all N*nb draws are one launch, all N*nb gathers are one launch
+// (indices never depend on factors), then the factor-dependent chain runs
+// batch by batch, stage by stage (Gauss-Seidel, rocp.cpp:122-130) -- captured
+// once into a CUDA graph per (nb, B, t_len) for consume_range.
+struct Window {
+    int64_t nb = 0, B = 0;     // capacity
+    DBuf<int32_t> idx;         // [b][stage] S x (N-1)
+    DBuf<int64_t> base, rows;  // [b][stage] S
+    DBuf<double> X;            // [b][stage] I_stage x S (column-major)
+    std::vector<int64_t> xoff;
+    JobList jobs;
+    // key of the uploaded job list
+    const double* key_x = nullptr;
+    int64_t key_t0 = -1, key_B = -1, key_nb = -1, key_slice = -1;
+    const int64_t* key_rows0 = nullptr;
+    const int64_t* key_rowsm = nullptr;
+    int key_only = -2;
+};
+
 struct rocp_stream {
     rocp_dev* dev = nullptr;
     int N = 0, R = 0;
@@ -348,37 +488,33 @@ struct rocp_stream {
     DBuf<double> temporal;              // t_cap x R row-major
     int64_t t_len = 0, t_cap = 0;
     bool regularized = false;
-    // per-stage scratch: stage 0 = temporal, stage n = mode n
-    int64_t max_batch = 0;
-    std::vector<DBuf<int32_t>> idx;
-    std::vector<DBuf<int64_t>> base, rows;
-    std::vector<DBuf<double>> X, Z;
-    DBuf<double> G_t, RHS_t;  // temporal Gram / rhs
-    DBuf<double> resid;       // N x 2 (num, den) of the last consume
-    DBuf<double> staging;     // host-slab staging for consume_host
-    DBuf<int> flags;          // [0] temporal regularized (stream flag), [1] unused,
-                              // [2] last mode-solve regularized, [3] unused
-    bool track_residual = true;
+    Window win;
+    std::vector<DBuf<double>> Z;  // per stage, S x R row-major (reused across batches)
+    DBuf<double> G_t, RHS_t;      // temporal Gram / rhs
+    DBuf<double> resid;           // N x 2 (num, den) of the last batch
+    DBuf<double> staging;         // host-slab staging for consume_host
+    DBuf<int> flags;              // [0] temporal regularized (stream flag), [2] last mode solve
+    DBuf<uint64_t> seed_dev;      // draw seed (device, so graphs need no re-capture)
+    DBuf<uint32_t> batch_dev;     // first batch id of the window (device)
+    int resid_level = 1;          // 0 none, 1 temporal stage (default), 2 every stage
     // checkpoint copies (device)
     std::vector<DBuf<double>> ckU, ckP, ckQ;
     int64_t ck_t_len = -1;
     bool ck_reg = false;
-    // CUDA graphs of consume_range keyed by their baked parameters
-    std::map<std::tuple<const double*, int64_t, int64_t, int64_t, uint64_t, uint32_t, int64_t>,
-             std::pair<cudaGraphExec_t, uint64_t>>
-        graphs;
+    // gather timing (events around each window gather launch)
+    bool time_gather = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_events;
+    size_t gather_events_used = 0;
+    // CUDA graphs of the chain keyed by (nb, B, t_len)
+    std::map<std::tuple<int64_t, int64_t, int64_t>, std::pair<cudaGraphExec_t, uint64_t>> graphs;
     ~rocp_stream() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+        for (auto& e : gather_events) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
     }
-
     int64_t stage_rows(int stage, int64_t batch) const { return stage == 0 ? batch : head[size_t(stage - 1)]; }
-
-    void ensure_batch(int64_t batch) {
-        if (batch <= max_batch) return;
-        max_batch = batch;
-        X[0].alloc(size_t(batch * s));
-        RHS_t.alloc(size_t(batch * R));
-    }
 };
 
 namespace {
@@ -395,13 +531,114 @@ void check_head_dims(const rocp_stream* st, const rocp_tensor* x) {  // rocp.cpp
         if (x->dims[k] != st->head[k]) throw_domain("batch head extents do not match stream");
 }
 
-// Temporal stage of consume (update_last_mode_with, rocp.cpp:71-84): SKR of
-// factors_excluding(head, N) = U(N-1..1), gram, rhs, solve into the temporal
-// factor rows [t_len, t_len + B).
-void stage_temporal(rocp_stream* st, int64_t B, double* u_out) {
+void clear_graphs(rocp_stream* st) {
+    for (auto& kv : st->graphs) cudaGraphExecDestroy(kv.second.first);
+    st->graphs.clear();
+}
+
+// Ensures the window arena holds nb batches of B slices.
+void ensure_window(rocp_stream* st, int64_t nb, int64_t B) {
+    Window& W = st->win;
+    if (nb <= W.nb && B <= W.B) return;
+    const int64_t nbn = std::max(nb, W.nb), Bn = std::max(B, W.B);
+    const int N = st->N;
+    const int64_t S = st->s;
+    W.idx.alloc(size_t(nbn * N * S * (N - 1)));
+    W.base.alloc(size_t(nbn * N * S));
+    W.rows.alloc(size_t(nbn * N * S));
+    W.xoff.assign(size_t(nbn * N), 0);
+    int64_t off = 0;
+    for (int64_t b = 0; b < nbn; ++b)
+        for (int stage = 0; stage < N; ++stage) {
+            W.xoff[size_t(b * N + stage)] = off;
+            off += st->stage_rows(stage, Bn) * S;
+        }
+    W.X.alloc(size_t(off));
+    W.nb = nbn;
+    W.B = Bn;
+    reserve_contract(st->dev, Bn, S, st->R);
+    for (int n = 1; n < N; ++n) reserve_contract(st->dev, st->head[size_t(n - 1)], S, st->R);
+    W.key_x = nullptr;
+    st->RHS_t.alloc(size_t(Bn * st->R));
+    clear_graphs(st);  // graphs hold arena pointers
+}
+
+int32_t* win_idx(rocp_stream* st, int64_t b, int stage) {
+    return st->win.idx.p + (b * st->N + stage) * st->s * (st->N - 1);
+}
+int64_t* win_base(rocp_stream* st, int64_t b, int stage) { return st->win.base.p + (b * st->N + stage) * st->s; }
+int64_t* win_rows(rocp_stream* st, int64_t b, int stage) { return st->win.rows.p + (b * st->N + stage) * st->s; }
+double* win_x(rocp_stream* st, int64_t b, int stage) { return st->win.X.p + st->win.xoff[size_t(b * st->N + stage)]; }
+
+// Builds (or reuses) the draw + gather job lists of nb consecutive slabs of B
+// slices starting at x (device pointer, slice = elements per slice).  Batch
+// ids come from st->batch_dev + b, the seed from st->seed_dev, so the lists
+// are reused across calls.  rows0/rowsm: explicit index sets (replay seams);
+// only_stage >= 0 restricts to one stage.
+void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice, int64_t B, int64_t nb,
+                    const int64_t* rows0, const int64_t* rowsm, int only_stage) {
+    ensure_window(st, nb, B);
+    Window& W = st->win;
+    if (W.key_x == x && W.key_t0 == t0 && W.key_B == B && W.key_nb == nb && W.key_slice == slice &&
+        W.key_rows0 == rows0 && W.key_rowsm == rowsm && W.key_only == only_stage)
+        return;
+    const std::vector<int64_t> d = slab_dims(st, B);
+    std::vector<DrawJob> dj;
+    std::vector<GatherJob> gj;
+    for (int64_t b = 0; b < nb; ++b) {
+        const double* xb = x + (t0 + b * B) * slice;
+        for (int stage = 0; stage < st->N; ++stage) {
+            if (only_stage >= 0 && stage != only_stage) continue;
+            const int mode = stage == 0 ? st->N : stage;
+            DrawJob j = make_draw(d, mode, st->s, 0, uint32_t(b), 0u, stage == 0 ? rows0 : rowsm,
+                                  win_rows(st, b, stage), win_idx(st, b, stage), win_base(st, b, stage));
+            j.seed_ptr = st->seed_dev.p;
+            j.batch_ptr = st->batch_dev.p;
+            dj.push_back(j);
+            gj.push_back(make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage)));
+        }
+    }
+    upload_jobs(st->dev, W.jobs, dj, gj);
+    W.key_x = x;
+    W.key_t0 = t0;
+    W.key_B = B;
+    W.key_nb = nb;
+    W.key_slice = slice;
+    W.key_rows0 = rows0;
+    W.key_rowsm = rowsm;
+    W.key_only = only_stage;
+}
+
+// Draw + gather of the prepared window (seed / first batch id set on device).
+void enqueue_draw_gather(rocp_stream* st, uint64_t seed, uint32_t first_batch_id) {
+    rocp_dev* dev = st->dev;
+    k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
+    after_launch(dev, "k_set_u64");
+    k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
+    after_launch(dev, "k_set_u32");
+    launch_draw(dev, st->win.jobs);
+    if (st->time_gather) {
+        if (st->gather_events_used == st->gather_events.size()) {
+            cudaEvent_t a, b;
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&b));
+            st->gather_events.emplace_back(a, b);
+        }
+        auto& ev = st->gather_events[st->gather_events_used++];
+        CK(cudaEventRecord(ev.first, dev->stream));
+        launch_gather(dev, st->win.jobs);
+        CK(cudaEventRecord(ev.second, dev->stream));
+    } else {
+        launch_gather(dev, st->win.jobs);
+    }
+}
+
+// Temporal stage of batch b (update_last_mode_with, rocp.cpp:71-84): SKR of
+// factors_excluding(head, N) = U(N-1..1), gram, rhs, solve into u_out.
+void stage_temporal(rocp_stream* st, int64_t b, int64_t B, double* u_out) {
     rocp_dev* dev = st->dev;
     SkrJob sj{};
-    sj.idx = st->idx[0].p;
+    sj.idx = win_idx(st, b, 0);
     sj.n_other = st->N - 1;
     sj.s = int32_t(st->s);
     sj.R = st->R;
@@ -409,20 +646,20 @@ void stage_temporal(rocp_stream* st, int64_t B, double* u_out) {
     for (int k = st->N - 1; k >= 1; --k) sj.f[l++] = st->U[size_t(k - 1)].p;
     sj.z = st->Z[0].p;
     launch_skr(dev, sj);
+    const double* X = win_x(st, b, 0);
     launch_gram(dev, st->Z[0].p, st->s, st->R, nullptr, st->G_t.p);
-    launch_contract(dev, st->X[0].p, B, st->s, st->Z[0].p, st->R, nullptr, st->RHS_t.p);
+    launch_contract(dev, X, B, st->s, st->Z[0].p, st->R, nullptr, st->RHS_t.p);
     launch_solve(dev, st->G_t.p, st->R, st->RHS_t.p, B, u_out, st->flags.p, 0);  // rocp.cpp:150
-    if (st->track_residual) launch_residual(dev, st->X[0].p, B, st->s, u_out, st->Z[0].p, st->R, st->resid.p);
+    if (st->resid_level >= 1) launch_residual(dev, X, B, st->s, u_out, st->Z[0].p, st->R, st->resid.p);
 }
 
-// Mode-n stage (update_mode_with, rocp.cpp:96-113 with slab_factors_excluding
-// rocp.cpp:25-34): Z over [u_new, U(N-1..1) \ n], P += X_s Z, Q += Z^T Z,
-// U(n) = solve_gram(Q, P).
-void stage_mode(rocp_stream* st, int n, int64_t B, const double* u_new) {
+// Mode-n stage of batch b (update_mode_with, rocp.cpp:96-113 with
+// slab_factors_excluding rocp.cpp:25-34): Z over [u_new, U(N-1..1) \ n],
+// P += X_s Z, Q += Z^T Z, U(n) = solve_gram(Q, P).
+void stage_mode(rocp_stream* st, int64_t b, int n, const double* u_new) {
     rocp_dev* dev = st->dev;
-    (void)B;
     SkrJob sj{};
-    sj.idx = st->idx[size_t(n)].p;
+    sj.idx = win_idx(st, b, n);
     sj.n_other = st->N - 1;
     sj.s = int32_t(st->s);
     sj.R = st->R;
@@ -435,54 +672,36 @@ void stage_mode(rocp_stream* st, int n, int64_t B, const double* u_new) {
     double* Pn = st->P[size_t(n - 1)].p;
     double* Qn = st->Q[size_t(n - 1)].p;
     const int64_t In = st->head[size_t(n - 1)];
+    const double* X = win_x(st, b, n);
     launch_gram(dev, st->Z[size_t(n)].p, st->s, st->R, Qn, Qn);
-    launch_contract(dev, st->X[size_t(n)].p, In, st->s, st->Z[size_t(n)].p, st->R, Pn, Pn);
+    launch_contract(dev, X, In, st->s, st->Z[size_t(n)].p, st->R, Pn, Pn);
     launch_solve(dev, Qn, st->R, Pn, In, st->U[size_t(n - 1)].p, st->flags.p + 2, 0);
-    if (st->track_residual)
-        launch_residual(dev, st->X[size_t(n)].p, In, st->s, st->U[size_t(n - 1)].p, st->Z[size_t(n)].p,
-                        st->R, st->resid.p + 2 * n);
+    if (st->resid_level >= 2)
+        launch_residual(dev, X, In, st->s, st->U[size_t(n - 1)].p, st->Z[size_t(n)].p, st->R, st->resid.p + 2 * n);
 }
 
-// Draw + gather every stage of one batch (indices never depend on factors, so
-// all N draws and all N gathers are one launch each).
-void draw_and_gather(rocp_stream* st, const rocp_tensor* x, uint64_t seed, uint32_t batch_id,
-                     const int64_t* in_rows_stage0, const int64_t* in_rows_mode, int only_mode) {
-    rocp_dev* dev = st->dev;
-    const int64_t B = x->dims.back();
-    const std::vector<int64_t> d = slab_dims(st, B);
-    const std::vector<int64_t> strides = strides_of(d);
-    DrawBatch db{};
-    GatherBatch gb{};
-    int64_t max_elems = 0;
-    for (int stage = 0; stage < st->N; ++stage) {
-        if (only_mode >= 0 && stage != only_mode) continue;
-        const int mode = stage == 0 ? st->N : stage;
-        const int64_t* in_rows = stage == 0 ? in_rows_stage0 : in_rows_mode;
-        db.job[db.njobs++] = make_draw(d, mode, st->s, seed, batch_id, 0u, in_rows, st->rows[size_t(stage)].p,
-                                       st->idx[size_t(stage)].p, st->base[size_t(stage)].p);
-        GatherJob g{};
-        g.t = x->d;
-        g.base = st->base[size_t(stage)].p;
-        g.ms = strides[size_t(mode - 1)];
-        g.I = int32_t(d[size_t(mode - 1)]);
-        g.s = int32_t(st->s);
-        g.out = st->X[size_t(stage)].p;
-        gb.job[gb.njobs++] = g;
-        max_elems = std::max<int64_t>(max_elems, int64_t(g.I) * g.s);
+// Factor-dependent chain of nb batches (RocpStream::consume, rocp.cpp:144-160):
+// temporal solve appended in place (rocp.cpp:152-156), then modes 1..N-1.
+void enqueue_chain(rocp_stream* st, int64_t nb, int64_t B) {
+    for (int64_t b = 0; b < nb; ++b) {
+        double* u_new = st->temporal.p + (st->t_len + b * B) * st->R;
+        stage_temporal(st, b, B, u_new);
+        for (int n = 1; n < st->N; ++n) stage_mode(st, b, n, u_new);
     }
-    launch_draw(dev, db, st->s);
-    launch_gather(dev, gb, max_elems);
 }
 
-void enqueue_consume(rocp_stream* st, const rocp_tensor* x, uint64_t seed, uint32_t batch_id) {
-    const int64_t B = x->dims.back();
-    st->ensure_batch(B);
-    if (st->t_len + B > st->t_cap) throw_domain("temporal capacity exceeded (raise t_capacity)");
-    draw_and_gather(st, x, seed, batch_id, nullptr, nullptr, -1);
-    double* u_new = st->temporal.p + st->t_len * st->R;  // rocp.cpp:152-156, appended in place
-    stage_temporal(st, B, u_new);
-    for (int n = 1; n < st->N; ++n) stage_mode(st, n, B, u_new);  // rocp.cpp:122-130
-    st->t_len += B;                                               // rocp.cpp:159
+void check_capacity(rocp_stream* st, int64_t add) {
+    if (st->t_len + add > st->t_cap) throw_domain("temporal capacity exceeded (raise t_capacity)");
+}
+
+// One batch on a device slab (no graph).
+void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uint32_t batch_id) {
+    check_capacity(st, B);
+    const int64_t slice = prod(st->head);
+    prepare_window(st, x, 0, slice, B, 1, nullptr, nullptr, -1);
+    enqueue_draw_gather(st, seed, batch_id);
+    enqueue_chain(st, 1, B);
+    st->t_len += B;  // rocp.cpp:159
 }
 
 }  // namespace
@@ -508,6 +727,7 @@ rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, ro
         dev->scalars.alloc(16);
         CK(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int((size_t(kGroup) * 64 + kGroup) * sizeof(double))));
+        set_contract_smem_attrs();
     });
     if (st != ROCP_OK) {
         static thread_local std::string last;
@@ -524,11 +744,32 @@ void rocp_destroy(rocp_dev* dev) {
     cudaSetDevice(dev->device);
     cudaStreamSynchronize(dev->stream);
     dev->init = rocp_dev::Init{};
+    for (cudaEvent_t& e : dev->timer)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(dev->stream);
     delete dev;
 }
 
 const char* rocp_last_error(const rocp_dev* dev) { return dev ? dev->err.c_str() : "null handle"; }
+
+rocp_status rocp_timer_record(rocp_dev* dev, int slot) {
+    return guarded(dev, [&] {
+        if (slot < 0 || slot >= 8) throw_domain("timer slot out of range");
+        if (!dev->timer[slot]) CK(cudaEventCreate(&dev->timer[slot]));
+        CK(cudaEventRecord(dev->timer[slot], dev->stream));
+    });
+}
+
+rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms) {
+    return guarded(dev, [&] {
+        if (a < 0 || a >= 8 || b < 0 || b >= 8 || !dev->timer[a] || !dev->timer[b])
+            throw_domain("timer slot not recorded");
+        CK(cudaEventSynchronize(dev->timer[b]));
+        CK(cudaEventElapsedTime(ms, dev->timer[a], dev->timer[b]));
+    });
+}
+
+void* rocp_cuda_stream(rocp_dev* dev) { return dev ? static_cast<void*>(dev->stream) : nullptr; }
 
 rocp_status rocp_synchronize(rocp_dev* dev) {
     return guarded(dev, [&] { CK(cudaStreamSynchronize(dev->stream)); });
@@ -650,9 +891,8 @@ rocp_status rocp_draw_samples(rocp_dev* dev, const int64_t* dims, int order, int
         if (s < 1) throw_domain("sample count must be positive");  // sampling.cpp:48-49
         DBuf<int64_t> drows(static_cast<size_t>(s)), dbase(static_cast<size_t>(s));
         DBuf<int32_t> didx(static_cast<size_t>(s) * (order - 1));
-        DrawBatch b{};
-        b.job[b.njobs++] = make_draw(d, mode, s, seed, batch, iteration, nullptr, drows.p, didx.p, dbase.p);
-        launch_draw(dev, b, s);
+        upload_jobs(dev, dev->jobs, {make_draw(d, mode, s, seed, batch, iteration, nullptr, drows.p, didx.p, dbase.p)}, {});
+        launch_draw(dev, dev->jobs);
         CK(cudaMemcpyAsync(rows, drows.p, size_t(s) * 8, cudaMemcpyDeviceToHost, dev->stream));
         std::vector<int32_t> hidx(size_t(s) * (order - 1));
         CK(cudaMemcpyAsync(hidx.data(), didx.p, hidx.size() * 4, cudaMemcpyDeviceToHost, dev->stream));
@@ -676,9 +916,8 @@ rocp_status rocp_decode_rows(rocp_dev* dev, const int64_t* dims, int order, int 
         DBuf<int64_t> din(static_cast<size_t>(s)), dbase(static_cast<size_t>(s));
         DBuf<int32_t> didx(static_cast<size_t>(s) * (order - 1));
         CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
-        DrawBatch b{};
-        b.job[b.njobs++] = make_draw(d, mode, s, 0, 0, 0, din.p, nullptr, didx.p, dbase.p);
-        launch_draw(dev, b, s);
+        upload_jobs(dev, dev->jobs, {make_draw(d, mode, s, 0, 0, 0, din.p, nullptr, didx.p, dbase.p)}, {});
+        launch_draw(dev, dev->jobs);
         std::vector<int32_t> hidx(size_t(s) * (order - 1));
         CK(cudaMemcpyAsync(hidx.data(), didx.p, hidx.size() * 4, cudaMemcpyDeviceToHost, dev->stream));
         CK(cudaStreamSynchronize(dev->stream));
@@ -704,19 +943,10 @@ rocp_status rocp_sample_unfolding(rocp_dev* dev, const rocp_tensor* t, int mode,
         DBuf<int32_t> didx(static_cast<size_t>(s) * (order - 1));
         DBuf<double> dout(static_cast<size_t>(I * s));
         CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
-        DrawBatch b{};
-        b.job[b.njobs++] = make_draw(d, mode, s, 0, 0, 0, din.p, nullptr, didx.p, dbase.p);
-        launch_draw(dev, b, s);
-        GatherBatch gb{};
-        GatherJob g{};
-        g.t = t->d;
-        g.base = dbase.p;
-        g.ms = strides_of(d)[size_t(mode - 1)];
-        g.I = int32_t(I);
-        g.s = int32_t(s);
-        g.out = dout.p;
-        gb.job[gb.njobs++] = g;
-        launch_gather(dev, gb, I * s);
+        upload_jobs(dev, dev->jobs, {make_draw(d, mode, s, 0, 0, 0, din.p, nullptr, didx.p, dbase.p)},
+                    {make_gather(t->d, d, mode, s, dbase.p, dout.p)});
+        launch_draw(dev, dev->jobs);
+        launch_gather(dev, dev->jobs);
         CK(cudaMemcpyAsync(out, dout.p, size_t(I * s) * 8, cudaMemcpyDeviceToHost, dev->stream));
         CK(cudaStreamSynchronize(dev->stream));
     });
@@ -775,6 +1005,7 @@ rocp_status rocp_contract(rocp_dev* dev, const double* x, int64_t rows, int64_t 
         DBuf<double> dx(static_cast<size_t>(rows * s)), dz(static_cast<size_t>(s * rank)), dout(static_cast<size_t>(rows * rank));
         CK(cudaMemcpyAsync(dx.p, x, size_t(rows * s) * 8, cudaMemcpyHostToDevice, dev->stream));
         upload_rowmajor(dev, z, s, rank, dz.p);
+        reserve_contract(dev, rows, s, rank);
         launch_contract(dev, dx.p, rows, s, dz.p, rank, nullptr, dout.p);
         download_colmajor(dev, dout.p, rows, rank, out);
     });
@@ -809,6 +1040,7 @@ rocp_status rocp_solve_sampled_ls(rocp_dev* dev, const double* z, const double* 
         upload_rowmajor(dev, z, s, rank, dz.p);
         CK(cudaMemcpyAsync(dx.p, x, size_t(rows * s) * 8, cudaMemcpyHostToDevice, dev->stream));
         launch_gram(dev, dz.p, s, rank, nullptr, dg.p);
+        reserve_contract(dev, rows, s, rank);
         launch_contract(dev, dx.p, rows, s, dz.p, rank, nullptr, drhs.p);
         CK(cudaMemsetAsync(dev->flags.p, 0, 2 * sizeof(int), dev->stream));
         launch_solve(dev, dg.p, rank, drhs.p, rows, dout.p, dev->flags.p, 1);
@@ -880,6 +1112,7 @@ rocp_status rocp_cprand(rocp_dev* dev, const rocp_tensor* t, int rank, int64_t s
                 G.emplace_back(size_t(rank * rank));
                 RHS.emplace_back(size_t(In * rank));
             }
+            for (int n = 0; n < N; ++n) reserve_contract(dev, d[size_t(n)], s, rank);
             double best_fit = -std::numeric_limits<double>::infinity();
             double prev = best_fit;
             bool reg_any = false;
@@ -888,24 +1121,16 @@ rocp_status rocp_cprand(rocp_dev* dev, const rocp_tensor* t, int rank, int64_t s
             while (sweep < max_iters) {  // :32
                 ++sweep;
                 // All N draws and gathers of the sweep up front: indices never depend on factors.
-                DrawBatch db{};
-                GatherBatch gb{};
-                int64_t max_elems = 0;
+                std::vector<DrawJob> dj;
+                std::vector<GatherJob> gj;
                 for (int n = 1; n <= N; ++n) {
-                    db.job[db.njobs++] = make_draw(d, n, s, seed, 0u, uint32_t(sweep), nullptr, nullptr,
-                                                   idx[size_t(n - 1)].p, base[size_t(n - 1)].p);
-                    GatherJob g{};
-                    g.t = t->d;
-                    g.base = base[size_t(n - 1)].p;
-                    g.ms = strides[size_t(n - 1)];
-                    g.I = int32_t(d[size_t(n - 1)]);
-                    g.s = int32_t(s);
-                    g.out = X[size_t(n - 1)].p;
-                    gb.job[gb.njobs++] = g;
-                    max_elems = std::max<int64_t>(max_elems, int64_t(g.I) * g.s);
+                    dj.push_back(make_draw(d, n, s, seed, 0u, uint32_t(sweep), nullptr, nullptr,
+                                           idx[size_t(n - 1)].p, base[size_t(n - 1)].p));
+                    gj.push_back(make_gather(t->d, d, n, s, base[size_t(n - 1)].p, X[size_t(n - 1)].p));
                 }
-                launch_draw(dev, db, s);
-                launch_gather(dev, gb, max_elems);
+                upload_jobs(dev, dev->jobs, dj, gj);
+                launch_draw(dev, dev->jobs);
+                launch_gather(dev, dev->jobs);
                 for (int n = 1; n <= N; ++n) {  // :35-45
                     SkrJob sj{};
                     sj.idx = idx[size_t(n - 1)].p;
@@ -960,11 +1185,12 @@ rocp_status rocp_cprand(rocp_dev* dev, const rocp_tensor* t, int rank, int64_t s
             init.rank = rank;
             init.s = s;
             init.regularized = reg_any;
-            DrawBatch db{};
+            std::vector<DrawJob> dj;
             for (int n = 1; n < N; ++n)
-                db.job[db.njobs++] = make_draw(d, n, s, seed, 0u, 0u, nullptr, nullptr, idx[size_t(n - 1)].p,
-                                               base[size_t(n - 1)].p);
-            launch_draw(dev, db, s);
+                dj.push_back(make_draw(d, n, s, seed, 0u, 0u, nullptr, nullptr, idx[size_t(n - 1)].p,
+                                       base[size_t(n - 1)].p));
+            upload_jobs(dev, dev->jobs, dj, {});
+            launch_draw(dev, dev->jobs);
             for (int n = 1; n < N; ++n) {
                 SkrJob sj{};
                 sj.idx = idx[size_t(n - 1)].p;
@@ -1013,22 +1239,18 @@ rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int 
         st->P.emplace_back(size_t(In * rank));
         st->Q.emplace_back(size_t(rank * rank));
     }
-    for (int stage = 0; stage < order; ++stage) {
-        st->idx.emplace_back(size_t(s) * (order - 1));
-        st->base.emplace_back(size_t(s));
-        st->rows.emplace_back(size_t(s));
-        st->Z.emplace_back(size_t(s * rank));
-        st->X.emplace_back(stage == 0 ? 0 : size_t(st->head[size_t(stage - 1)] * s));
-    }
+    for (int stage = 0; stage < order; ++stage) st->Z.emplace_back(size_t(s * rank));
     st->G_t.alloc(size_t(rank * rank));
     st->resid.alloc(size_t(2 * order));
     st->flags.alloc(4);
+    st->seed_dev.alloc(1);
+    st->batch_dev.alloc(1);
     CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));
     // Reduction scratch sized once: consume (and its CUDA graph) never allocates.
     dev->scratch_a.ensure(size_t((s + kChunk - 1) / kChunk) * rank * rank);
     dev->scratch_b.ensure(size_t(3 * s));
     CK(cudaMemsetAsync(st->resid.p, 0, size_t(2 * order) * 8, dev->stream));
-    st->ensure_batch(1);
+    ensure_window(st.get(), 1, 1);
     return st.release();
 }
 
@@ -1104,7 +1326,7 @@ rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint6
                                 uint32_t batch_id) {
     return guarded(st->dev, [&] {
         check_head_dims(st, x_new);  // rocp.cpp:145
-        enqueue_consume(st, x_new, seed, batch_id);
+        consume_one(st, x_new->d, x_new->dims.back(), seed, batch_id);
     });
 }
 
@@ -1114,14 +1336,12 @@ rocp_status rocp_stream_consume_host(rocp_stream* st, const double* x_new, int64
         if (batch < 1) throw_domain("batch must hold at least one slice");
         rocp_dev* dev = st->dev;
         const int64_t numel = prod(st->head) * batch;
-        st->staging.ensure(size_t(numel));
+        if (st->staging.n < size_t(numel)) {
+            CK(cudaStreamSynchronize(dev->stream));
+            st->staging.alloc(size_t(numel));
+        }
         CK(cudaMemcpyAsync(st->staging.p, x_new, size_t(numel) * 8, cudaMemcpyHostToDevice, dev->stream));
-        rocp_tensor view;
-        view.dims = slab_dims(st, batch);
-        view.numel = numel;
-        view.d = st->staging.p;
-        view.owned = false;
-        enqueue_consume(st, &view, seed, batch_id);
+        consume_one(st, st->staging.p, batch, seed, batch_id);
     });
 }
 
@@ -1132,27 +1352,21 @@ rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int
         check_head_dims(st, x);
         if (batch < 1 || nb < 1 || t0 < 0 || t0 + batch * nb > x->dims.back())
             throw_domain("consume_range: slab range out of bounds");
+        check_capacity(st, batch * nb);
         rocp_dev* dev = st->dev;
         const int64_t slice = x->numel / x->dims.back();
-        auto key = std::make_tuple(static_cast<const double*>(x->d), t0, batch, nb, seed, first_batch_id, st->t_len);
+        prepare_window(st, x->d, t0, slice, batch, nb, nullptr, nullptr, -1);
+        enqueue_draw_gather(st, seed, first_batch_id);
+        auto key = std::make_tuple(nb, batch, st->t_len);
         auto it = st->graphs.find(key);
         if (it == st->graphs.end()) {
-            st->ensure_batch(batch);
-            const int64_t t_len0 = st->t_len;
             const uint64_t l0 = dev->launches;
             cudaGraph_t graph;
             CK(cudaStreamBeginCapture(dev->stream, cudaStreamCaptureModeThreadLocal));
             try {
-                for (int64_t b = 0; b < nb; ++b) {
-                    rocp_tensor view;
-                    view.dims = slab_dims(st, batch);
-                    view.numel = slice * batch;
-                    view.d = x->d + (t0 + b * batch) * slice;
-                    enqueue_consume(st, &view, seed, first_batch_id + uint32_t(b));
-                }
+                enqueue_chain(st, nb, batch);
             } catch (...) {
                 cudaStreamEndCapture(dev->stream, &graph);
-                st->t_len = t_len0;
                 throw;
             }
             CK(cudaStreamEndCapture(dev->stream, &graph));
@@ -1161,7 +1375,6 @@ rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int
             cudaGraphDestroy(graph);
             const uint64_t nodes = dev->launches - l0;
             dev->launches = l0;
-            st->t_len = t_len0;
             it = st->graphs.emplace(key, std::make_pair(exec, nodes)).first;
         }
         CK(cudaGraphLaunch(it->second.first, dev->stream));
@@ -1178,27 +1391,28 @@ rocp_status rocp_stream_update_last_mode_with(rocp_stream* st, const rocp_tensor
         if (s != st->s) throw_domain("index set size must equal the stream sample count");
         rocp_dev* dev = st->dev;
         const int64_t B = x_new->dims.back();
-        st->ensure_batch(B);
-        int64_t co = prod(st->head);
+        const int64_t co = prod(st->head);
         for (int64_t c = 0; c < s; ++c)
             if (rows[c] < 1 || rows[c] > co) throw_domain("column index out of range");
         DBuf<int64_t> din(static_cast<size_t>(s));
         CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
-        draw_and_gather(st, x_new, 0, 0, din.p, nullptr, 0);
+        prepare_window(st, x_new->d, 0, prod(st->head), B, 1, din.p, nullptr, 0);
+        enqueue_draw_gather(st, 0, 0);
         DBuf<double> du(static_cast<size_t>(B * st->R));
-        int saved[4];
-        CK(cudaMemcpyAsync(saved, st->flags.p, sizeof(saved), cudaMemcpyDeviceToHost, dev->stream));
+        int saved = 0;
+        CK(cudaMemcpyAsync(&saved, st->flags.p, sizeof(int), cudaMemcpyDeviceToHost, dev->stream));
         CK(cudaStreamSynchronize(dev->stream));
         CK(cudaMemsetAsync(st->flags.p, 0, sizeof(int), dev->stream));
-        stage_temporal(st, B, du.p);
-        int hf[2];
-        CK(cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
+        stage_temporal(st, 0, B, du.p);
+        int hf = 0;
+        CK(cudaMemcpyAsync(&hf, st->flags.p, sizeof(int), cudaMemcpyDeviceToHost, dev->stream));
         CK(cudaStreamSynchronize(dev->stream));
-        // the replay seam does not touch the stream's own flag (rocp.cpp:71-84 is pure)
-        CK(cudaMemcpyAsync(st->flags.p, saved, sizeof(int), cudaMemcpyHostToDevice, dev->stream));
+        // the replay seam leaves the stream's own flag untouched (rocp.cpp:71-84 is pure)
+        CK(cudaMemcpyAsync(st->flags.p, &saved, sizeof(int), cudaMemcpyHostToDevice, dev->stream));
         download_colmajor(dev, du.p, B, st->R, u_new);
         if (z_s) download_colmajor(dev, st->Z[0].p, s, st->R, z_s);
-        if (regularized) *regularized = hf[0] & 1;
+        if (regularized) *regularized = hf & 1;
+        st->win.key_x = nullptr;  // din is released: the job list must not be reused
     });
 }
 
@@ -1232,18 +1446,20 @@ rocp_status rocp_stream_update_mode_with(rocp_stream* st, const rocp_tensor* x_n
         CK(cudaMemcpyAsync(din.p, rows, size_t(s) * 8, cudaMemcpyHostToDevice, dev->stream));
         DBuf<double> du(static_cast<size_t>(B * st->R));
         upload_rowmajor(dev, u_new, B, st->R, du.p);
-        draw_and_gather(st, x_new, 0, 0, nullptr, din.p, mode);
+        prepare_window(st, x_new->d, 0, prod(st->head), B, 1, nullptr, din.p, mode);
+        enqueue_draw_gather(st, 0, 0);
         CK(cudaMemsetAsync(st->flags.p + 2, 0, sizeof(int), dev->stream));
-        stage_mode(st, mode, B, du.p);
+        stage_mode(st, 0, mode, du.p);
         int hf[4];
         CK(cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
         if (z_new) download_colmajor(dev, st->Z[size_t(mode)].p, s, st->R, z_new);
         if (x_s) {
             const int64_t In = st->head[size_t(mode - 1)];
-            CK(cudaMemcpyAsync(x_s, st->X[size_t(mode)].p, size_t(In * s) * 8, cudaMemcpyDeviceToHost, dev->stream));
+            CK(cudaMemcpyAsync(x_s, win_x(st, 0, mode), size_t(In * s) * 8, cudaMemcpyDeviceToHost, dev->stream));
         }
         CK(cudaStreamSynchronize(dev->stream));
         if (regularized) *regularized = hf[2] & 1;
+        st->win.key_x = nullptr;
     });
 }
 
@@ -1311,15 +1527,51 @@ rocp_status rocp_stream_restore(rocp_stream* st) {
             CK(cudaMemcpyAsync(st->P[size_t(n)].p, st->ckP[size_t(n)].p, st->P[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
             CK(cudaMemcpyAsync(st->Q[size_t(n)].p, st->ckQ[size_t(n)].p, st->Q[size_t(n)].n * 8, cudaMemcpyDeviceToDevice, dev->stream));
         }
-        const int f0 = st->ck_reg ? 1 : 0;
-        CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));
-        if (f0) CK(cudaMemcpyAsync(st->flags.p, &f0, sizeof(int), cudaMemcpyHostToDevice, dev->stream));
-        CK(cudaStreamSynchronize(dev->stream));
+        // asynchronous: flags reset by a kernel, no host synchronisation
+        k_set_i32<<<1, 32, 0, dev->stream>>>(st->flags.p, 4, 0);
+        after_launch(dev, "k_set_i32");
+        if (st->ck_reg) {
+            k_set_i32<<<1, 32, 0, dev->stream>>>(st->flags.p, 1, 1);
+            after_launch(dev, "k_set_i32");
+        }
         st->t_len = st->ck_t_len;  // temporal rows beyond t_len are rewritten by the next consume
     });
 }
 
 int64_t rocp_stream_t_len(const rocp_stream* st) { return st ? st->t_len : -1; }
+
+rocp_status rocp_stream_set_residual_tracking(rocp_stream* st, int enable) {
+    return guarded(st->dev, [&] {
+        if (enable < 0 || enable > 2) throw_domain("residual level must be 0, 1 or 2");
+        if (st->resid_level != enable) clear_graphs(st);
+        st->resid_level = enable;
+    });
+}
+
+rocp_status rocp_stream_time_gather(rocp_stream* st, int enable) {
+    return guarded(st->dev, [&] {
+        st->time_gather = enable != 0;
+        st->gather_events_used = 0;
+    });
+}
+
+rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* count) {
+    return guarded(st->dev, [&] {
+        CK(cudaStreamSynchronize(st->dev->stream));
+        const int n = int(std::min<size_t>(st->gather_events_used, size_t(std::max(max, 0))));
+        for (int k = 0; k < n; ++k)
+            CK(cudaEventElapsedTime(ms + k, st->gather_events[size_t(k)].first, st->gather_events[size_t(k)].second));
+        *count = int(st->gather_events_used);
+        st->gather_events_used = 0;
+    });
+}
+
+rocp_status rocp_stream_window_bytes(rocp_stream* st, int64_t* useful, int64_t* elements) {
+    return guarded(st->dev, [&] {
+        *elements = st->win.jobs.gather_elems;
+        *useful = st->win.jobs.gather_elems * int64_t(sizeof(double));
+    });
+}
 
 int rocp_stream_regularized(rocp_stream* st) {
     // The reference's consume raises the stream flag from the temporal solve
