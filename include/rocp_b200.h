@@ -182,6 +182,12 @@ rocp_status rocp_stream_set_residual_tracking(rocp_stream* st, int level);
  * enable, then read the per-launch milliseconds (resets the list). */
 rocp_status rocp_stream_time_gather(rocp_stream* st, int enable);
 rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* count);
+/* Profiling aid: globaltimer stamps of the persistent chain kernel, 8 per
+ * (batch, stage) of the last window: stage start, phase-1 items done (block
+ * 0), last-block start/end, after barrier 1, phase 2 done (block 0), after
+ * barrier 2.  enable toggles recording; out may be NULL. */
+rocp_status rocp_stream_chain_trace(rocp_stream* st, int enable, uint64_t* out, int64_t max,
+                                    int64_t* count);
 /* Elements (and useful bytes) the current window's gather moves per launch. */
 rocp_status rocp_stream_window_bytes(rocp_stream* st, int64_t* useful, int64_t* elements);
 /* Sampled residual of the last consume (north-star item 5): per stage

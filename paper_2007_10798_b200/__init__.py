@@ -97,6 +97,7 @@ SIGNATURES = [
     ("rocp_stream_time_gather", C.c_int, [_vp, C.c_int]),
     ("rocp_stream_gather_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
     ("rocp_stream_window_bytes", C.c_int, [_vp, _i64p, _i64p]),
+    ("rocp_stream_chain_trace", C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
 ]
 
 
@@ -552,6 +553,18 @@ class RocpStream:
         cnt = C.c_int(0)
         self.dev.check(lib().rocp_stream_gather_times(self.h, buf, max_n, C.byref(cnt)))
         return [float(buf[k]) for k in range(min(cnt.value, max_n))]
+
+    def chain_trace(self, enable=None, fetch=True):
+        if enable is not None and not fetch:
+            self.dev.check(lib().rocp_stream_chain_trace(self.h, int(enable), None, 0, None))
+            return None
+        n = C.c_int64(0)
+        self.dev.check(lib().rocp_stream_chain_trace(self.h, int(bool(enable)), None, 0, C.byref(n)))
+        buf = np.zeros(max(n.value, 1), dtype=np.uint64)
+        self.dev.check(lib().rocp_stream_chain_trace(self.h, int(bool(enable)),
+                                                     buf.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                     n.value, C.byref(n)))
+        return buf[: n.value].reshape(-1, 16)
 
     def window_bytes(self):
         u, e = C.c_int64(0), C.c_int64(0)

@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 namespace rocpk {
 
@@ -120,7 +121,17 @@ struct GatherJob {
     int32_t I;   // fibre length (I_n)
     int32_t s;
     double* out;
+    int tiled;   // 0: I x s column-major; 1: row-tiled (see xs_offset)
 };
+
+// Row-tiled X_s layout (stream windows): rows in tiles of 32, each tile's
+// 32 x S block stored column after column, so the (32-row tile, 256-sample
+// superchunk) operand of the contraction is ONE contiguous 64 KB block (a
+// single TMA bulk copy).  Element (i, c) of an I x S operand:
+__host__ __device__ __forceinline__ int64_t xs_offset(int64_t i, int64_t c, int64_t S) {
+    return ((i >> 5) * S + c) * 32 + (i & 31);
+}
+__host__ __device__ __forceinline__ int64_t xs_size(int64_t I, int64_t S) { return ((I + 31) / 32) * 32 * S; }
 struct GatherTile {
     int32_t job;
     uint32_t e0;
@@ -151,7 +162,15 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherJob* __re
 #pragma unroll
     for (int u = 0; u < kGatherUnroll; ++u) {
         const uint32_t e = tile.e0 + u * kGatherThreads + threadIdx.x;
-        if (e < total) J.out[e] = v[u];
+        if (e < total) {
+            if (J.tiled) {
+                const uint32_t c = e / I;
+                const uint32_t i = e - c * I;
+                J.out[xs_offset(i, c, J.s)] = v[u];
+            } else {
+                J.out[e] = v[u];
+            }
+        }
     }
 }
 
@@ -282,7 +301,7 @@ __global__ void __launch_bounds__(256) k_contract(const double* __restrict__ X, 
                                                   const double* __restrict__ Z, int R,
                                                   const double* base, double* out,
                                                   double* __restrict__ partial,
-                                                  unsigned int* __restrict__ counters) {
+                                                  unsigned int* __restrict__ counters, int tiled) {
     extern __shared__ double sm[];
     const int RP = int(blockDim.x >> 5) * RB;    // R padded to the r-groups (zero columns)
     double* xs = sm;                            // [256][32]
@@ -295,7 +314,7 @@ __global__ void __launch_bounds__(256) k_contract(const double* __restrict__ X, 
     const int tid = threadIdx.x;
     for (int e = tid; e < kRowTile * cn; e += blockDim.x) {
         const int c = e >> 5, r = e & 31;
-        if (r < rows) cp_async8(xs + e, X + int64_t(c0 + c) * I + i0 + r);
+        if (r < rows) cp_async8(xs + e, X + (tiled ? xs_offset(i0 + r, c0 + c, S) : int64_t(c0 + c) * I + i0 + r));
         else xs[e] = 0.0;
     }
     for (int e = tid; e < cn * RP; e += blockDim.x) {
@@ -644,7 +663,8 @@ __global__ void __launch_bounds__(256) k_fitness(const FitJob J) {
 // Sampled residual |X_s - U Z^T|^2 and |X_s|^2, one warp per
 // sample column; partials per column, last block hsums both.
 struct ResidJob {
-    const double* X;  // I x S col-major
+    int tiled;
+    const double* X;  // I x S col-major (or row-tiled)
     const double* U;  // I x R row-major
     const double* Z;  // S x R row-major
     int32_t I, S;
@@ -666,7 +686,7 @@ __global__ void __launch_bounds__(256) k_residual(const ResidJob J) {
             double uz = 0.0;
             const double* u = J.U + int64_t(i) * J.R;
             for (int r = 0; r < J.R; ++r) uz = __fma_rn(u[r], z[r], uz);
-            const double xv = J.X[int64_t(c) * J.I + i];
+            const double xv = J.X[J.tiled ? xs_offset(i, c, J.S) : int64_t(c) * J.I + i];
             const double e = xv - uz;
             qn = __fma_rn(e, e, qn);
             qd = __fma_rn(xv, xv, qd);
@@ -784,6 +804,531 @@ __global__ void __launch_bounds__(256) k_synth_noise(double* t, int64_t numel, u
     const double scale = *scale_ptr;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < numel; e += int64_t(gridDim.x) * blockDim.x)
         t[e] = t[e] + scale * noise_at(seed, e);
+}
+
+
+// ===========================================================================
+// K6: persistent stream chain.  One cooperative launch runs the whole
+// factor-dependent chain of a window of nb batches (RocpStream::consume,
+// rocp.cpp:144-160, after the hoisted draw + gather): for every batch the
+// temporal stage (update_last_mode_with, rocp.cpp:71-84), then modes
+// 1..N-1 (update_mode_with, rocp.cpp:96-113, Gauss-Seidel).  Per stage:
+//   stage start  contraction blocks start a TMA bulk copy of their X_s tile
+//                (row-tiled layout: one contiguous 64 KB block; X_s never
+//                depends on factors)
+//   phase 0      sampled Khatri-Rao Z (S x RP, zero-padded), all blocks | barrier
+//   phase 1      concurrently:
+//                - contraction blocks: Z tile by TMA, warp w = chunk w of the
+//                  superchunk (32 rows x all r per lane), chunk partials
+//                  combined in order -> superchunk partials of X_s Z
+//                - Gram blocks: (superchunk, output range) partials; the last
+//                  to arrive combines (Q += G), factors (canonical LDL^T, one
+//                  barrier per pivot) and publishes L, D
+//                - idle blocks of the temporal stage: sampled residual of the
+//                  previous batch's temporal solve                   | barrier
+//   phase 2      warp per row: combine partials, P += X_s Z, forward /
+//                diagonal / backward solve -> U(n) or u_new row      | barrier
+// Arithmetic is exactly that of the per-stage kernels above (bitwise equal).
+
+struct ChainParams {
+    int N, R, S, nb, B, nsuper, resid_level;
+    int32_t head[kMaxOrder];
+    double* U[kMaxOrder];  // U[n-1], n = 1..N-1, row-major I_n x R
+    double* P[kMaxOrder];
+    double* Q[kMaxOrder];
+    double* temporal;      // row-major; batch b's rows start at t_len0 + b*B
+    int64_t t_len0;
+    const int32_t* idx_base;  // window: [b][stage] S x (N-1)
+    const double* X_base;     // window: [b][stage] row-tiled I_stage x S
+    const int64_t* xoff;      // [b*N + stage]
+    double* zbuf;             // (N+1) x S x RP: Z per stage; temporal Z alternates slots 0 / N
+    double* gpart;            // nsuper x R x R
+    double* cpart;            // nsuper x rows x R
+    double* LD;               // R x R (L(i,k) at [k*R + i], i > k) + R (D)
+    int* mode_flag;           // [0]: 0 = zero solution, 1 = solve
+    int* flags;               // stream flags ([0] temporal regularized, [2] mode solve)
+    double* resid;            // N x 2 (num, den) of the last batch
+    double* rpart;            // 3 x S
+    unsigned int* counter;    // [0] Gram arrivals, [1] residual arrivals
+    unsigned long long* trace;  // optional phase timestamps (globaltimer ns), 16 per stage
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers ----------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int kChainThreads = 256;
+constexpr int kCRB = 8;        // padding unit of R (RP = multiple of 8)
+constexpr int kLdStride = 65;  // smem row stride of the factorization triangle (R <= 64)
+constexpr int kGramSplit = 4;  // Gram output ranges per superchunk
+constexpr int kResidCols = 64; // columns per residual item
+constexpr int kMaxPairsPerThread = (64 * 65 / 2 + kChainThreads - 1) / kChainThreads;
+
+__device__ __forceinline__ int chain_zslot(int st, int b, int N) { return st == 0 ? ((b & 1) ? N : 0) : st; }
+
+// Canonical LDL^T of G (R x R column-major in smem) by one block, one barrier
+// per pivot step; same per-element operation sequence as k_solve / the oracle.
+// Thread t owns the lower-triangle pairs t, t + 256, ... (column order).
+// d_{k+1} is formed redundantly in registers by every thread that needs it
+// (its last update), so the diagonal entry is never written in the step that
+// finishes it.  L(i,k) at A[k*kLdStride + i].
+__device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double lambda, const double* G,
+                                           const unsigned short* pairs, int npairs) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    int pi[kMaxPairsPerThread], pj[kMaxPairsPerThread];
+#pragma unroll
+    for (int u = 0; u < kMaxPairsPerThread; ++u) {
+        const int pp = tid + u * nt;
+        pi[u] = (pp < npairs) ? (pairs[pp] >> 8) : -1;
+        pj[u] = (pp < npairs) ? (pairs[pp] & 0xff) : -1;
+    }
+    for (int t = tid; t < R * R; t += nt) {
+        const int i = t % R, j = t / R;
+        if (i >= j) A[i * kLdStride + j] = (i == j) ? G[t] + lambda : G[t];
+    }
+    __syncthreads();
+    const double d0 = A[0];
+    if (tid == 0) D[0] = d0;
+    for (int i = 1 + tid; i < R; i += nt) A[i] = (d0 != 0.0) ? A[i * kLdStride] / d0 : 0.0;
+    __syncthreads();
+    for (int k = 0; k + 1 < R; ++k) {
+        const double* rowk = A + k * kLdStride;  // L(., k) in the strict upper part
+        const double dn = __fma_rn(-rowk[k + 1], A[(k + 1) * kLdStride + k], A[(k + 1) * kLdStride + k + 1]);
+        if (tid == 0) D[k + 1] = dn;
+#pragma unroll
+        for (int u = 0; u < kMaxPairsPerThread; ++u) {
+            const int i = pi[u], j = pj[u];
+            if (j > k && !(i == j && j == k + 1)) {
+                const double v = __fma_rn(-rowk[i], A[j * kLdStride + k], A[i * kLdStride + j]);
+                if (j == k + 1) A[(k + 1) * kLdStride + i] = (dn != 0.0) ? v / dn : 0.0;
+                A[i * kLdStride + j] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Row solves of phase 2: warp per row, lanes own entries j and j + 32.
+__device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
+                                             int rows, int R, int nsuper, double* out, const double* Ls,
+                                             const double* Ds, int mode) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int j0 = lane, j1 = lane + 32;
+    const bool v0 = j0 < R, v1 = j1 < R;
+    for (int row = blockIdx.x + warp * gridDim.x; row < rows; row += gridDim.x * nw) {
+        double w0 = 0.0, w1 = 0.0;
+        if (v0) {
+            double tot = __ldcg(cpart + int64_t(row) * R + j0);
+            for (int m = 1; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j0);
+            if (st > 0) {
+                double* pr = Prow_base + int64_t(row) * R + j0;
+                tot = __ldcg(pr) + tot;
+                *pr = tot;
+            }
+            w0 = tot;
+        }
+        if (v1) {
+            double tot = __ldcg(cpart + int64_t(row) * R + j1);
+            for (int m = 1; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j1);
+            if (st > 0) {
+                double* pr = Prow_base + int64_t(row) * R + j1;
+                tot = __ldcg(pr) + tot;
+                *pr = tot;
+            }
+            w1 = tot;
+        }
+        if (mode == 0) {
+            w0 = 0.0;
+            w1 = 0.0;
+        } else {
+            for (int k = 0; k < R; ++k) {  // forward, k increasing
+                const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+                if (v0 && j0 > k) w0 = __fma_rn(-Ls[k * R + j0], wk, w0);
+                if (v1 && j1 > k) w1 = __fma_rn(-Ls[k * R + j1], wk, w1);
+            }
+            if (v0) w0 = (fabs(Ds[j0]) > 2.2250738585072014e-308) ? w0 / Ds[j0] : 0.0;
+            if (v1) w1 = (fabs(Ds[j1]) > 2.2250738585072014e-308) ? w1 / Ds[j1] : 0.0;
+            for (int k = R - 1; k >= 0; --k) {  // backward, k decreasing
+                const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+                if (j0 < k) w0 = __fma_rn(-Ls[j0 * R + k], wk, w0);
+                if (v1 && j1 < k) w1 = __fma_rn(-Ls[j1 * R + k], wk, w1);
+            }
+        }
+        if (v0) out[int64_t(row) * R + j0] = w0;
+        if (v1) out[int64_t(row) * R + j1] = w1;
+    }
+}
+
+// One warp's chunk of the contraction: lane = row, NG groups of 8 r's at a
+// time; z rows read as broadcast 16-byte loads.
+template <int NG>
+__device__ __forceinline__ void chain_chunk(const double* __restrict__ xs, const double* __restrict__ zs, int RP,
+                                           int g0, int cc0, int ccn, int lane, double* cps, int warp) {
+    double acc[NG * kCRB];
+#pragma unroll
+    for (int a = 0; a < NG * kCRB; ++a) acc[a] = 0.0;
+    if (ccn == kChunk) {
+#pragma unroll 4
+        for (int cc = 0; cc < kChunk; ++cc) {
+            const double x = xs[(cc0 + cc) * kRowTile + lane];
+            const double2* zr = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RP + g0 * kCRB);
+#pragma unroll
+            for (int q = 0; q < NG * kCRB / 2; ++q) {
+                const double2 zz = zr[q];
+                acc[2 * q] = __fma_rn(x, zz.x, acc[2 * q]);
+                acc[2 * q + 1] = __fma_rn(x, zz.y, acc[2 * q + 1]);
+            }
+        }
+    } else {
+        for (int cc = 0; cc < ccn; ++cc) {
+            const double x = xs[(cc0 + cc) * kRowTile + lane];
+            const double2* zr = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RP + g0 * kCRB);
+#pragma unroll
+            for (int q = 0; q < NG * kCRB / 2; ++q) {
+                const double2 zz = zr[q];
+                acc[2 * q] = __fma_rn(x, zz.x, acc[2 * q]);
+                acc[2 * q + 1] = __fma_rn(x, zz.y, acc[2 * q + 1]);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NG * kCRB; ++a) cps[(warp * RP + g0 * kCRB + a) * kRowTile + lane] = acc[a];
+}
+
+// Sampled residual column partials of batch rb's temporal solve (DESIGN.md
+// 3.6), columns [c0, c0 + cn); the last residual block hsums all S columns.
+__device__ __noinline__ void chain_residual_item(const ChainParams& p, int rb, int c0, int cn, int nres, int RP,
+                                                 double* sm) {
+    const int N = p.N, R = p.R, S = p.S, Bq = p.B;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* u_rb = p.temporal + (p.t_len0 + int64_t(rb) * Bq) * R;
+    const double* XT = p.X_base + p.xoff[rb * N + 0];
+    const double* ZT = p.zbuf + int64_t(chain_zslot(0, rb, N)) * S * RP;
+    double* us = sm;                    // B x R
+    double* zs = us + Bq * R;           // cn x RP
+    double* xs = zs + kResidCols * RP;  // cn x B
+    for (int e = tid; e < Bq * R; e += blockDim.x) us[e] = __ldcg(u_rb + e);
+    for (int e = tid; e < cn * RP; e += blockDim.x) zs[e] = __ldcg(ZT + int64_t(c0) * RP + e);
+    for (int e = tid; e < cn * Bq; e += blockDim.x) {
+        const int c = e / Bq, i = e - c * Bq;
+        xs[e] = XT[xs_offset(i, c0 + c, S)];
+    }
+    __syncthreads();
+    for (int c = warp; c < cn; c += blockDim.x >> 5) {
+        double qn = 0.0, qd = 0.0;
+        const double* z = zs + c * RP;
+        for (int i = lane; i < Bq; i += 32) {
+            double uz = 0.0;
+            const double* u = us + i * R;
+            for (int r = 0; r < R; ++r) uz = __fma_rn(u[r], z[r], uz);
+            const double xv = xs[c * Bq + i];
+            const double e = xv - uz;
+            qn = __fma_rn(e, e, qn);
+            qd = __fma_rn(xv, xv, qd);
+        }
+        qn = butterfly32(qn);
+        qd = butterfly32(qd);
+        if (lane == 0) {
+            p.rpart[c0 + c] = qn;
+            p.rpart[S + c0 + c] = qd;
+        }
+    }
+    if (last_arrive_of(p.counter + 1, unsigned(nres))) {
+        block_hsum_inplace(p.rpart, S, p.rpart + 2 * S);
+        block_hsum_inplace(p.rpart + S, S, p.rpart + 2 * S);
+        if (tid == 0) {
+            p.resid[0] = __ldcg(p.rpart);
+            p.resid[1] = __ldcg(p.rpart + S);
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) double sm[];
+    __shared__ unsigned short pairs[64 * 65 / 2];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int s_mode, s_reg;
+    __shared__ double s_tr;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
+    const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
+    const int RR = R * R;
+    const int G = gridDim.x;
+    const int npairs = R * (R + 1) / 2;
+    unsigned phase = 0;
+    if (tid == 0) {
+        int off = 0;
+        for (int j = 0; j < R; ++j)
+            for (int i = j; i < R; ++i) pairs[off++] = (unsigned short)((i << 8) | j);
+        mbar_init(&bar, 1);
+    }
+    __syncthreads();
+    const int n_gram = nsuper * kGramSplit;
+    const int gram_blocks = min(n_gram, max(1, G / 4));
+    const int cblocks = G - gram_blocks;  // contraction / residual blocks
+    const bool is_gram_block = int(blockIdx.x) >= cblocks;
+    const int nres = (S + kResidCols - 1) / kResidCols;
+
+    double* xs = sm;                             // [256][32]  (64 KB, TMA destination)
+    double* zs = sm + kSuperSamples * kRowTile;  // [256][RP]  (TMA destination)
+    double* cps = zs + kSuperSamples * RP;       // [8 chunks][RP][32]
+
+    for (int b = 0; b < p.nb; ++b) {
+        double* u_new = p.temporal + (p.t_len0 + int64_t(b) * p.B) * R;
+        for (int st = 0; st < N; ++st) {
+            const double* F[kMaxOrder];
+            {
+                int l = 0;
+                if (st > 0) F[l++] = u_new;
+                for (int k = N - 1; k >= 1; --k)
+                    if (k != st) F[l++] = p.U[k - 1];
+                for (; l < kMaxOrder; ++l) F[l] = nullptr;
+            }
+            const int rows = (st == 0) ? p.B : p.head[st - 1];
+            const double* X = p.X_base + p.xoff[b * N + st];
+            const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+            double* Z = p.zbuf + int64_t(chain_zslot(st, b, N)) * S * RP;
+            const int tiles = (rows + kRowTile - 1) / kRowTile;
+            const int n_contract = tiles * nsuper;
+            unsigned long long* tr = p.trace ? p.trace + (int64_t(b) * N + st) * 16 : nullptr;
+            if (tr && blockIdx.x == 0 && tid == 0) tr[0] = gtimer();
+
+            // stage start: TMA the first X_s tile of this block (independent of factors)
+            const bool contract_block = !is_gram_block && int(blockIdx.x) < n_contract;
+            if (contract_block && tid == 0) {
+                // complete_tx lands on the barrier's current phase; the matching
+                // arrive.expect_tx (X + Z bytes) is issued in phase 1.
+                const int item = blockIdx.x, tile = item % tiles, m = item / tiles;
+                const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                fence_proxy_async();
+                tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+            }
+
+            // ---------------- phase 0: Z = sampled Khatri-Rao rows (sampling.cpp:90-103), stride RP
+            for (int e = blockIdx.x * blockDim.x + tid; e < S * RP; e += G * blockDim.x) {
+                const int c = e / RP, r = e - c * RP;
+                double z = 0.0;
+                if (r < R) {
+                    z = 1.0;
+#pragma unroll
+                    for (int l = 0; l < kMaxOrder - 1; ++l) {
+                        if (l < n_other) {
+                            const int k = n_other - 1 - l;
+                            const int32_t i = __ldg(idx + int64_t(c) * n_other + k);
+                            z = z * __ldcg(F[l] + int64_t(i) * R + r);
+                        }
+                    }
+                }
+                Z[e] = z;
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA in phase 1
+            grid.sync();
+            if (tr && blockIdx.x == 0 && tid == 0) tr[1] = gtimer();
+
+            // ---------------- phase 1
+            if (is_gram_block) {
+                for (int gi = blockIdx.x - cblocks; gi < n_gram; gi += gram_blocks) {
+                    const int m = gi / kGramSplit, part = gi % kGramSplit;
+                    const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                    const int nk = (cn + kChunk - 1) / kChunk;
+                    const int pp0 = (RR * part) / kGramSplit, pp1 = (RR * (part + 1)) / kGramSplit;
+                    const int npp = pp1 - pp0;
+                    double* gz = sm;                           // cn x RP
+                    double* gcp = sm + kSuperSamples * 64;     // [8][npp]
+                    if (tid == 0) {
+                        fence_proxy_async();
+                        mbar_expect_tx(&bar, unsigned(cn * RP * 8));
+                        tma_load_1d(gz, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    for (int u = tid; u < nk * npp; u += blockDim.x) {
+                        const int k = u / npp, pp = pp0 + (u - k * npp);
+                        const int r1 = pp % R, r2 = pp / R;
+                        const int cc0 = k * kChunk, ccn = min(kChunk, cn - cc0);
+                        double acc = 0.0;
+                        for (int cc = 0; cc < ccn; ++cc)
+                            acc = __fma_rn(gz[(cc0 + cc) * RP + r1], gz[(cc0 + cc) * RP + r2], acc);
+                        gcp[k * npp + (pp - pp0)] = acc;
+                    }
+                    __syncthreads();
+                    for (int q = tid; q < npp; q += blockDim.x) {
+                        double v = gcp[q];
+                        for (int k = 1; k < nk; ++k) v = v + gcp[k * npp + q];
+                        p.gpart[int64_t(m) * RR + pp0 + q] = v;
+                    }
+                    __syncthreads();
+                    if (last_arrive_of(p.counter, unsigned(n_gram))) {
+                        if (tr && tid == 0) tr[3] = gtimer();
+                        double* A = sm;                  // [64][65]
+                        double* D = A + 64 * kLdStride;  // 64
+                        double* Gs = D + 64;             // R x R column-major
+                        // Gram combine in superchunk order; Q += G for the modes (rocp.cpp:108)
+                        for (int pp = tid; pp < RR; pp += blockDim.x) {
+                            double tot = __ldcg(p.gpart + pp);
+                            for (int mm = 1; mm < nsuper; ++mm) tot = tot + __ldcg(p.gpart + int64_t(mm) * RR + pp);
+                            if (st > 0) {
+                                tot = __ldcg(p.Q[st - 1] + pp) + tot;
+                                p.Q[st - 1][pp] = tot;
+                            }
+                            Gs[pp] = tot;
+                        }
+                        __syncthreads();
+                        if (tr && tid == 0) tr[10] = gtimer();
+                        // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
+                        if (tid == 0) {
+                            double maxdiag = Gs[0];
+                            for (int k = 1; k < R; ++k)
+                                if (Gs[k * R + k] > maxdiag) maxdiag = Gs[k * R + k];
+                            double trc = Gs[0];
+                            for (int k = 1; k < R; ++k) trc = trc + Gs[k * R + k];
+                            s_tr = trc;
+                            s_mode = (maxdiag <= 0.0) ? 0 : 1;
+                            s_reg = (s_mode == 0) ? 1 : 0;
+                        }
+                        __syncthreads();
+                        if (s_mode == 1) {
+                            ldlt_one_sync(A, D, R, 0.0, Gs, pairs, npairs);
+                            if (tid == 0) {
+                                double dmin = D[0], dmax = D[0];
+                                for (int k = 0; k < R; ++k) {
+                                    if (D[k] < dmin) dmin = D[k];
+                                    if (D[k] > dmax) dmax = D[k];
+                                }
+                                s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+                            }
+                            __syncthreads();
+                            if (s_reg) ldlt_one_sync(A, D, R, 1e-12 * s_tr, Gs, pairs, npairs);
+                        }
+                        __syncthreads();
+                        if (tr && tid == 0) tr[11] = gtimer();
+                        for (int t = tid; t < RR; t += blockDim.x) {
+                            const int k = t / R, i = t % R;
+                            p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
+                        }
+                        for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
+                        if (tid == 0) {
+                            p.mode_flag[0] = s_mode;
+                            if (s_reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
+                            if (tr) tr[4] = gtimer();
+                        }
+                        __syncthreads();
+                    }
+                }
+            } else {
+                for (int item = blockIdx.x; item < n_contract; item += cblocks) {
+                    const int tile = item % tiles, m = item / tiles;
+                    const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                    const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
+                    if (tid == 0) {
+                        fence_proxy_async();
+                        if (item != int(blockIdx.x))  // later items: X tile now
+                            tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+                        tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + cn * RP * 8));
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[8] = gtimer();
+                    // warp w = chunk w of the superchunk; lane = row; all r-groups
+                    const int cc0 = warp * kChunk;
+                    const int ccn = min(kChunk, cn - cc0);
+                    if (ccn > 0) {
+                        for (int g0 = 0; g0 < ng; g0 += 4) {
+                            const int ngp = min(4, ng - g0);
+                            if (ngp == 4) chain_chunk<4>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
+                            else if (ngp == 3) chain_chunk<3>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
+                            else if (ngp == 2) chain_chunk<2>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
+                            else chain_chunk<1>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
+                        }
+                    }
+                    __syncthreads();
+                    // superchunk partial = chunk partials in increasing chunk order
+                    const int nk = (cn + kChunk - 1) / kChunk;
+                    for (int e = tid; e < R * kRowTile; e += blockDim.x) {
+                        const int r = e >> 5, l2 = e & 31;
+                        if (l2 < nrows) {
+                            double q = cps[r * kRowTile + l2];
+                            for (int k = 1; k < nk; ++k) q = q + cps[(k * RP + r) * kRowTile + l2];
+                            p.cpart[(int64_t(m) * rows + i0 + l2) * R + r] = q;
+                        }
+                    }
+                    __syncthreads();
+                    if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[9] = gtimer();
+                }
+                // idle blocks of the temporal stage: residual of the previous batch
+                if (st == 0 && b > 0 && p.resid_level >= 1) {
+                    const int first = n_contract < cblocks ? n_contract : cblocks;
+                    const int nblk = cblocks - first;
+                    if (nblk > 0) {
+                        if (int(blockIdx.x) >= first)
+                            for (int ri = blockIdx.x - first; ri < nres; ri += nblk)
+                                chain_residual_item(p, b - 1, ri * kResidCols, min(kResidCols, S - ri * kResidCols),
+                                                    nres, RP, sm);
+                    } else if (blockIdx.x == 0) {
+                        for (int ri = 0; ri < nres; ++ri)
+                            chain_residual_item(p, b - 1, ri * kResidCols, min(kResidCols, S - ri * kResidCols),
+                                                nres, RP, sm);
+                    }
+                }
+            }
+            if (tr && blockIdx.x == 0 && tid == 0) tr[2] = gtimer();
+            grid.sync();
+            if (tr && blockIdx.x == 0 && tid == 0) tr[5] = gtimer();
+
+            // ---------------- phase 2: row solves
+            if (int(blockIdx.x) < rows) {
+                double* Ls = sm;  // R x R, L(i,k) at [k*R + i]
+                double* Ds = sm + RR;
+                for (int t = tid; t < RR + R; t += blockDim.x) Ls[t] = __ldcg(p.LD + t);
+                __syncthreads();
+                const int mode = __ldcg(p.mode_flag);
+                double* out = (st == 0) ? u_new : p.U[st - 1];
+                chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ds, mode);
+            }
+            if (tr && blockIdx.x == 0 && tid == 0) tr[6] = gtimer();
+            grid.sync();
+            if (tr && blockIdx.x == 0 && tid == 0) tr[7] = gtimer();
+        }
+    }
+    // residual of the window's last batch
+    if (p.resid_level >= 1 && p.nb > 0) {
+        for (int ri = blockIdx.x; ri < nres; ri += G)
+            chain_residual_item(p, p.nb - 1, ri * kResidCols, min(kResidCols, S - ri * kResidCols), nres, RP, sm);
+    }
 }
 
 }  // namespace rocpk

@@ -211,8 +211,9 @@ DrawJob make_draw(const std::vector<int64_t>& d, int mode, int64_t s, uint64_t s
 }
 
 GatherJob make_gather(const double* t, const std::vector<int64_t>& d, int mode, int64_t s,
-                      const int64_t* base, double* out) {
+                      const int64_t* base, double* out, int tiled = 0) {
     GatherJob g{};
+    g.tiled = tiled;
     g.t = t;
     g.base = base;
     g.ms = strides_of(d)[size_t(mode - 1)];
@@ -294,7 +295,7 @@ size_t contract_smem(int R) {
 
 template <int RB>
 void launch_contract_rb(rocp_dev* dev, int ng, const double* X, int64_t I, int64_t s, const double* Z, int R,
-                        const double* base, double* out) {
+                        const double* base, double* out, int tiled) {
     const int tiles = int((I + kRowTile - 1) / kRowTile);
     const int nsuper = int((s + kSuperSamples - 1) / kSuperSamples);
     if (nsuper > 1) {
@@ -303,15 +304,15 @@ void launch_contract_rb(rocp_dev* dev, int ng, const double* X, int64_t I, int64
     }
     const dim3 grid{unsigned(tiles), unsigned(nsuper), 1u};
     k_contract<RB><<<grid, 32 * ng, contract_smem(R), dev->stream>>>(
-        X, int32_t(I), int32_t(s), Z, R, base, out, dev->contract_partial.p, dev->tile_counters.p);
+        X, int32_t(I), int32_t(s), Z, R, base, out, dev->contract_partial.p, dev->tile_counters.p, tiled);
     after_launch(dev, "k_contract");
 }
 
 // Reserves the split-superchunk scratch (outside any graph capture).
-void reserve_contract(rocp_dev* dev, int64_t I, int64_t s, int R) {
+void reserve_contract(rocp_dev* dev, int64_t I, int64_t s, int R, bool always = false) {
     const int64_t tiles = (I + kRowTile - 1) / kRowTile;
     const int64_t nsuper = (s + kSuperSamples - 1) / kSuperSamples;
-    if (nsuper <= 1) return;
+    if (nsuper <= 1 && !always) return;
     if (dev->contract_partial.n < size_t(nsuper * I * R)) {
         CK(cudaStreamSynchronize(dev->stream));
         dev->contract_partial.alloc(size_t(nsuper * I * R));
@@ -324,20 +325,20 @@ void reserve_contract(rocp_dev* dev, int64_t I, int64_t s, int R) {
 }
 
 void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
-                     const double* base, double* out) {
+                     const double* base, double* out, int tiled = 0) {
     int rb;
     const int ng = contract_groups(R, &rb);
     switch (rb) {
-        case 1: launch_contract_rb<1>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 2: launch_contract_rb<2>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 3: launch_contract_rb<3>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 4: launch_contract_rb<4>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 5: launch_contract_rb<5>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 6: launch_contract_rb<6>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 7: launch_contract_rb<7>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 8: launch_contract_rb<8>(dev, ng, X, I, s, Z, R, base, out); break;
-        case 9: launch_contract_rb<9>(dev, ng, X, I, s, Z, R, base, out); break;
-        default: launch_contract_rb<10>(dev, ng, X, I, s, Z, R, base, out); break;
+        case 1: launch_contract_rb<1>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 2: launch_contract_rb<2>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 3: launch_contract_rb<3>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 4: launch_contract_rb<4>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 5: launch_contract_rb<5>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 6: launch_contract_rb<6>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 7: launch_contract_rb<7>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 8: launch_contract_rb<8>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        case 9: launch_contract_rb<9>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
+        default: launch_contract_rb<10>(dev, ng, X, I, s, Z, R, base, out, tiled); break;
     }
 }
 
@@ -394,8 +395,9 @@ void launch_fitness(rocp_dev* dev, const rocp_tensor* t, const std::vector<const
 }
 
 void launch_residual(rocp_dev* dev, const double* X, int64_t I, int64_t S, const double* U,
-                     const double* Z, int R, double* out2) {
+                     const double* Z, int R, double* out2, int tiled = 0) {
     ResidJob j{};
+    j.tiled = tiled;
     j.X = X;
     j.U = U;
     j.Z = Z;
@@ -470,6 +472,7 @@ struct Window {
     DBuf<int64_t> base, rows;  // [b][stage] S
     DBuf<double> X;            // [b][stage] I_stage x S (column-major)
     std::vector<int64_t> xoff;
+    DBuf<int64_t> xoff_dev;
     JobList jobs;
     // key of the uploaded job list
     const double* key_x = nullptr;
@@ -494,6 +497,11 @@ struct rocp_stream {
     DBuf<double> resid;           // N x 2 (num, den) of the last batch
     DBuf<double> staging;         // host-slab staging for consume_host
     DBuf<int> flags;              // [0] temporal regularized (stream flag), [2] last mode solve
+    DBuf<double> zbuf, gpart, LD, rpart;  // persistent-chain scratch
+    DBuf<int> mode_flag;
+    bool trace_on = false;             // chain phase timestamps (profiling aid)
+    DBuf<unsigned long long> trace;
+    int64_t trace_n = 0;
     DBuf<uint64_t> seed_dev;      // draw seed (device, so graphs need no re-capture)
     DBuf<uint32_t> batch_dev;     // first batch id of the window (device)
     int resid_level = 1;          // 0 none, 1 temporal stage (default), 2 every stage
@@ -551,13 +559,15 @@ void ensure_window(rocp_stream* st, int64_t nb, int64_t B) {
     for (int64_t b = 0; b < nbn; ++b)
         for (int stage = 0; stage < N; ++stage) {
             W.xoff[size_t(b * N + stage)] = off;
-            off += st->stage_rows(stage, Bn) * S;
+            off += xs_size(st->stage_rows(stage, Bn), S);  // row-tiled layout
         }
     W.X.alloc(size_t(off));
+    W.xoff_dev.alloc(W.xoff.size());
+    CK(cudaMemcpy(W.xoff_dev.p, W.xoff.data(), W.xoff.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     W.nb = nbn;
     W.B = Bn;
-    reserve_contract(st->dev, Bn, S, st->R);
-    for (int n = 1; n < N; ++n) reserve_contract(st->dev, st->head[size_t(n - 1)], S, st->R);
+    reserve_contract(st->dev, Bn, S, st->R, true);
+    for (int n = 1; n < N; ++n) reserve_contract(st->dev, st->head[size_t(n - 1)], S, st->R, true);
     W.key_x = nullptr;
     st->RHS_t.alloc(size_t(Bn * st->R));
     clear_graphs(st);  // graphs hold arena pointers
@@ -595,7 +605,7 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
             j.seed_ptr = st->seed_dev.p;
             j.batch_ptr = st->batch_dev.p;
             dj.push_back(j);
-            gj.push_back(make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage)));
+            gj.push_back(make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage), 1));
         }
     }
     upload_jobs(st->dev, W.jobs, dj, gj);
@@ -648,9 +658,9 @@ void stage_temporal(rocp_stream* st, int64_t b, int64_t B, double* u_out) {
     launch_skr(dev, sj);
     const double* X = win_x(st, b, 0);
     launch_gram(dev, st->Z[0].p, st->s, st->R, nullptr, st->G_t.p);
-    launch_contract(dev, X, B, st->s, st->Z[0].p, st->R, nullptr, st->RHS_t.p);
+    launch_contract(dev, X, B, st->s, st->Z[0].p, st->R, nullptr, st->RHS_t.p, 1);
     launch_solve(dev, st->G_t.p, st->R, st->RHS_t.p, B, u_out, st->flags.p, 0);  // rocp.cpp:150
-    if (st->resid_level >= 1) launch_residual(dev, X, B, st->s, u_out, st->Z[0].p, st->R, st->resid.p);
+    if (st->resid_level >= 1) launch_residual(dev, X, B, st->s, u_out, st->Z[0].p, st->R, st->resid.p, 1);
 }
 
 // Mode-n stage of batch b (update_mode_with, rocp.cpp:96-113 with
@@ -674,10 +684,10 @@ void stage_mode(rocp_stream* st, int64_t b, int n, const double* u_new) {
     const int64_t In = st->head[size_t(n - 1)];
     const double* X = win_x(st, b, n);
     launch_gram(dev, st->Z[size_t(n)].p, st->s, st->R, Qn, Qn);
-    launch_contract(dev, X, In, st->s, st->Z[size_t(n)].p, st->R, Pn, Pn);
+    launch_contract(dev, X, In, st->s, st->Z[size_t(n)].p, st->R, Pn, Pn, 1);
     launch_solve(dev, Qn, st->R, Pn, In, st->U[size_t(n - 1)].p, st->flags.p + 2, 0);
     if (st->resid_level >= 2)
-        launch_residual(dev, X, In, st->s, st->U[size_t(n - 1)].p, st->Z[size_t(n)].p, st->R, st->resid.p + 2 * n);
+        launch_residual(dev, X, In, st->s, st->U[size_t(n - 1)].p, st->Z[size_t(n)].p, st->R, st->resid.p + 2 * n, 1);
 }
 
 // Factor-dependent chain of nb batches (RocpStream::consume, rocp.cpp:144-160):
@@ -690,6 +700,82 @@ void enqueue_chain(rocp_stream* st, int64_t nb, int64_t B) {
     }
 }
 
+size_t chain_smem(int R, int B) {
+    const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
+    const size_t tiles = (size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * RP +
+                          size_t(kSuper) * RP * kRowTile) * sizeof(double);
+    const size_t gram = (size_t(kSuperSamples) * 64 + size_t(kSuper) * ((R * R + kGramSplit - 1) / kGramSplit)) *
+                        sizeof(double);
+    const size_t fact = (size_t(64) * kLdStride + 64 + 64 * 64) * sizeof(double);
+    const size_t resid = (size_t(B) * R + size_t(kResidCols) * RP + size_t(kResidCols) * B) * sizeof(double);
+    return std::max(std::max(tiles, gram), std::max(fact, resid));
+}
+
+void launch_chain_k(rocp_stream* st, const ChainParams& p) {
+    rocp_dev* dev = st->dev;
+    const size_t smem = chain_smem(st->R, p.B);
+    static int max_dyn = 0;
+    if (max_dyn == 0) {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device));
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, k_chain));
+        max_dyn = optin - int(fa.sharedSizeBytes);
+        CK(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+    }
+    if (smem > size_t(max_dyn)) throw_domain("batch too large for the persistent chain kernel's shared memory");
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain, kChainThreads, smem));
+    if (per_sm < 1) throw RocpError{ROCP_E_CUDA, "k_chain does not fit on an SM"};
+    const int grid = dev->num_sms;  // one persistent block per SM
+    void* args[] = {const_cast<ChainParams*>(&p)};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_chain), dim3(grid), dim3(kChainThreads), args,
+                                   smem, dev->stream));
+    after_launch(dev, "k_chain");
+}
+
+// The whole factor-dependent chain of the prepared window as ONE cooperative
+// persistent kernel (kernels.cuh K6).
+void launch_chain(rocp_stream* st, int64_t nb, int64_t B) {
+    ChainParams p{};
+    p.N = st->N;
+    p.R = st->R;
+    p.S = int(st->s);
+    p.nb = int(nb);
+    p.B = int(B);
+    p.nsuper = int((st->s + kSuperSamples - 1) / kSuperSamples);
+    p.resid_level = st->resid_level;
+    for (int n = 1; n < st->N; ++n) {
+        p.head[n - 1] = int32_t(st->head[size_t(n - 1)]);
+        p.U[n - 1] = st->U[size_t(n - 1)].p;
+        p.P[n - 1] = st->P[size_t(n - 1)].p;
+        p.Q[n - 1] = st->Q[size_t(n - 1)].p;
+    }
+    p.temporal = st->temporal.p;
+    p.t_len0 = st->t_len;
+    p.idx_base = st->win.idx.p;
+    p.X_base = st->win.X.p;
+    p.xoff = st->win.xoff_dev.p;
+    p.zbuf = st->zbuf.p;
+    p.gpart = st->gpart.p;
+    p.cpart = st->dev->contract_partial.p;
+    p.LD = st->LD.p;
+    p.mode_flag = st->mode_flag.p;
+    p.flags = st->flags.p;
+    p.resid = st->resid.p;
+    p.rpart = st->rpart.p;
+    p.counter = st->dev->counters.p + 4;
+    if (st->trace_on) {
+        st->trace.ensure(size_t(nb * st->N * 16));
+        CK(cudaMemsetAsync(st->trace.p, 0, size_t(nb * st->N * 16) * 8, st->dev->stream));
+        st->trace_n = nb * st->N * 16;
+        p.trace = st->trace.p;
+    } else {
+        p.trace = nullptr;
+    }
+    launch_chain_k(st, p);
+}
+
 void check_capacity(rocp_stream* st, int64_t add) {
     if (st->t_len + add > st->t_cap) throw_domain("temporal capacity exceeded (raise t_capacity)");
 }
@@ -700,7 +786,8 @@ void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uin
     const int64_t slice = prod(st->head);
     prepare_window(st, x, 0, slice, B, 1, nullptr, nullptr, -1);
     enqueue_draw_gather(st, seed, batch_id);
-    enqueue_chain(st, 1, B);
+    if (st->resid_level <= 1) launch_chain(st, 1, B);
+    else enqueue_chain(st, 1, B);
     st->t_len += B;  // rocp.cpp:159
 }
 
@@ -1245,6 +1332,11 @@ rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int 
     st->flags.alloc(4);
     st->seed_dev.alloc(1);
     st->batch_dev.alloc(1);
+    st->zbuf.alloc(size_t((order + 1) * s * (((rank + kCRB - 1) / kCRB) * kCRB)));
+    st->gpart.alloc(size_t(((s + kSuperSamples - 1) / kSuperSamples) * rank * rank));
+    st->LD.alloc(size_t(rank * rank + rank));
+    st->rpart.alloc(size_t(3 * s));
+    st->mode_flag.alloc(4);
     CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));
     // Reduction scratch sized once: consume (and its CUDA graph) never allocates.
     dev->scratch_a.ensure(size_t((s + kChunk - 1) / kChunk) * rank * rank);
@@ -1357,28 +1449,32 @@ rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int
         const int64_t slice = x->numel / x->dims.back();
         prepare_window(st, x->d, t0, slice, batch, nb, nullptr, nullptr, -1);
         enqueue_draw_gather(st, seed, first_batch_id);
-        auto key = std::make_tuple(nb, batch, st->t_len);
-        auto it = st->graphs.find(key);
-        if (it == st->graphs.end()) {
-            const uint64_t l0 = dev->launches;
-            cudaGraph_t graph;
-            CK(cudaStreamBeginCapture(dev->stream, cudaStreamCaptureModeThreadLocal));
-            try {
-                enqueue_chain(st, nb, batch);
-            } catch (...) {
-                cudaStreamEndCapture(dev->stream, &graph);
-                throw;
+        if (st->resid_level <= 1) {
+            launch_chain(st, nb, batch);
+        } else {
+            auto key = std::make_tuple(nb, batch, st->t_len);
+            auto it = st->graphs.find(key);
+            if (it == st->graphs.end()) {
+                const uint64_t l0 = dev->launches;
+                cudaGraph_t graph;
+                CK(cudaStreamBeginCapture(dev->stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    enqueue_chain(st, nb, batch);
+                } catch (...) {
+                    cudaStreamEndCapture(dev->stream, &graph);
+                    throw;
+                }
+                CK(cudaStreamEndCapture(dev->stream, &graph));
+                cudaGraphExec_t exec;
+                CK(cudaGraphInstantiate(&exec, graph, 0));
+                cudaGraphDestroy(graph);
+                const uint64_t nodes = dev->launches - l0;
+                dev->launches = l0;
+                it = st->graphs.emplace(key, std::make_pair(exec, nodes)).first;
             }
-            CK(cudaStreamEndCapture(dev->stream, &graph));
-            cudaGraphExec_t exec;
-            CK(cudaGraphInstantiate(&exec, graph, 0));
-            cudaGraphDestroy(graph);
-            const uint64_t nodes = dev->launches - l0;
-            dev->launches = l0;
-            it = st->graphs.emplace(key, std::make_pair(exec, nodes)).first;
+            CK(cudaGraphLaunch(it->second.first, dev->stream));
+            dev->launches += it->second.second;
         }
-        CK(cudaGraphLaunch(it->second.first, dev->stream));
-        dev->launches += it->second.second;
         st->t_len += batch * nb;
     });
 }
@@ -1453,11 +1549,16 @@ rocp_status rocp_stream_update_mode_with(rocp_stream* st, const rocp_tensor* x_n
         int hf[4];
         CK(cudaMemcpyAsync(hf, st->flags.p, sizeof(hf), cudaMemcpyDeviceToHost, dev->stream));
         if (z_new) download_colmajor(dev, st->Z[size_t(mode)].p, s, st->R, z_new);
+        std::vector<double> xt;
+        const int64_t In = st->head[size_t(mode - 1)];
         if (x_s) {
-            const int64_t In = st->head[size_t(mode - 1)];
-            CK(cudaMemcpyAsync(x_s, win_x(st, 0, mode), size_t(In * s) * 8, cudaMemcpyDeviceToHost, dev->stream));
+            xt.resize(size_t(xs_size(In, s)));
+            CK(cudaMemcpyAsync(xt.data(), win_x(st, 0, mode), xt.size() * 8, cudaMemcpyDeviceToHost, dev->stream));
         }
         CK(cudaStreamSynchronize(dev->stream));
+        if (x_s)
+            for (int64_t c = 0; c < s; ++c)
+                for (int64_t i = 0; i < In; ++i) x_s[i + c * In] = xt[size_t(xs_offset(i, c, s))];
         if (regularized) *regularized = hf[2] & 1;
         st->win.key_x = nullptr;
     });
@@ -1563,6 +1664,18 @@ rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* c
             CK(cudaEventElapsedTime(ms + k, st->gather_events[size_t(k)].first, st->gather_events[size_t(k)].second));
         *count = int(st->gather_events_used);
         st->gather_events_used = 0;
+    });
+}
+
+rocp_status rocp_stream_chain_trace(rocp_stream* st, int enable, uint64_t* out, int64_t max, int64_t* count) {
+    return guarded(st->dev, [&] {
+        st->trace_on = enable != 0;
+        if (out && max > 0 && st->trace_n > 0) {
+            CK(cudaStreamSynchronize(st->dev->stream));
+            const int64_t n = std::min(max, st->trace_n);
+            CK(cudaMemcpy(out, st->trace.p, size_t(n) * 8, cudaMemcpyDeviceToHost));
+        }
+        if (count) *count = st->trace_n;
     });
 }
 

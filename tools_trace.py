@@ -1,0 +1,49 @@
+"""Profiling aid: per-phase timeline of the persistent chain kernel (globaltimer stamps)."""
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import paper_2007_10798_b200 as rocp
+
+dims, R, t_init, B = [1000, 1000, 1000], 20, 100, 25
+if len(sys.argv) > 1:
+    cfg = json.loads(sys.argv[1])
+    dims, R, t_init, B = cfg["dims"], cfg["R"], cfg["t_init"], cfg["B"]
+S = max(R, int(np.ceil(10 * R * np.log(R))))
+g = np.random.default_rng(0)
+dev = rocp.Device(0)
+X = dev.tensor(dims)
+X.generate([np.asfortranarray(g.standard_normal((d, R))) for d in dims], snr_db=20.0, noise_seed=1)
+init = rocp.cprand_decompose(dev, X.slab(0, t_init), R,
+                             [np.asfortranarray(g.standard_normal((d, R))) for d in dims[:-1] + [t_init]], seed=3)
+st = rocp.RocpStream(dev, init, S, t_capacity=dims[-1] + 8)
+st.checkpoint()
+nb = (dims[-1] - t_init) // B
+for k in range(3):
+    st.restore()
+    st.consume_range(X, t_init, B, nb, 100 + k, 1)
+st.chain_trace(True, fetch=False)
+st.restore()
+st.consume_range(X, t_init, B, nb, 200, 1)
+tr = st.chain_trace(False).astype(np.int64)
+N = len(dims)
+
+
+def med(a):
+    a = a[np.isfinite(a)]
+    return np.median(a) / 1e3 if a.size else float("nan")
+
+
+for stg in range(N):
+    t = tr[stg::N].astype(float)
+    t[t == 0] = np.nan
+    z = lambda k: t[:, k] - t[:, 1]
+    print(f"stage {stg}: p0+sync={med(t[:,1]-t[:,0]):.2f} | item0 load={med(t[:,8]-t[:,1]):.2f} "
+          f"compute={med(t[:,9]-t[:,8]):.2f} p1end(b0)={med(z(2)):.2f} | gram->factor start={med(z(3)):.2f} "
+          f"combine={med(t[:,10]-t[:,3]):.2f} factor={med(t[:,11]-t[:,10]):.2f} publish={med(t[:,4]-t[:,11]):.2f} | "
+          f"sync1 done={med(z(5)):.2f} p2={med(t[:,6]-t[:,5]):.2f} sync2={med(t[:,7]-t[:,6]):.2f} | "
+          f"total={med(t[:,7]-t[:,0]):.2f} us")
+print("whole window us:", (tr[-1, 7] - tr[0, 0]) / 1e3)
