@@ -841,8 +841,9 @@ struct ChainParams {
     const int32_t* idx_base;  // window: [b][stage] S x (N-1)
     const double* X_base;     // window: [b][stage] row-tiled I_stage x S
     const int64_t* xoff;      // [b*N + stage]
-    double* zbuf;             // (N+1) x S x RP: Z per stage; temporal Z alternates slots 0 / N
-    double* gpart;            // nsuper x R x R
+    double* zbuf;             // nb x S x RP: the temporal Z of each batch (window residual pass)
+    double* gch;              // N x S x RP: Z of the mode stages
+    double* gpart;            // nsuper x R x R Gram superchunk partials
     double* cpart;            // nsuper x rows x R
     double* LD;               // R x R (L(i,k) at [k*R + i], i > k) + R (D)
     int* mode_flag;           // [0]: 0 = zero solution, 1 = solve
@@ -938,6 +939,48 @@ __device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double l
     }
 }
 
+// Canonical LDL^T for R <= MAXR <= 32 by ONE warp, no block barriers: lane i
+// holds row i of the lower triangle in registers.  Step k: d_k = lane k's
+// r[k] (final), l(i,k) = r[k] / d_k on lanes i > k, then r[j] = fma(-l(i,k),
+// a(j,k), r[j]) for k < j <= i with a(j,k) = lane j's r[k] broadcast by a
+// shuffle.  Identical per-element operation sequence to ldlt_one_sync /
+// k_solve / the oracle.  L(i,k) at A[k*kLdStride + i], D in D[].
+template <int MAXR>
+__device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, double* A, double* D, double* col) {
+    // Upper-triangle registers (j > lane) and lanes >= R receive harmless
+    // updates but are never read as lower entries.  d_k travels by shuffle
+    // (critical path); the column a(., k) is published to shared memory one
+    // step ahead so its loads overlap the divide.  Dividends of inactive
+    // lanes are 1.0: a zero dividend would take the divide's slow path.
+    const int lane = threadIdx.x & 31;
+    double r[MAXR];
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j)
+        r[j] = (lane < R && j <= lane) ? ((j == lane) ? G[lane + j * R] + lambda : G[lane + j * R]) : 0.0;
+    col[lane] = r[0];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+        if (k < R) {
+            const double* cb = col + (k & 1) * 32;
+            const double dk = __shfl_sync(0xffffffffu, r[k], k);
+            double ajk[MAXR];
+#pragma unroll
+            for (int j = k + 1; j < MAXR; ++j) ajk[j] = cb[j];
+            const bool act = lane > k && lane < R;
+            const double num = act ? r[k] : 1.0;
+            const double q = num / dk;
+            const double l = (act && dk != 0.0) ? q : 0.0;
+            if (lane == 0) D[k] = dk;
+            if (act) A[k * kLdStride + lane] = l;
+#pragma unroll
+            for (int j = k + 1; j < MAXR; ++j) r[j] = __fma_rn(-l, ajk[j], r[j]);
+            if (k + 1 < MAXR) col[((k + 1) & 1) * 32 + lane] = r[k + 1];
+            __syncwarp();
+        }
+    }
+}
+
 // Row solves of phase 2: warp per row, lanes own entries j and j + 32.
 __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
                                              int rows, int R, int nsuper, double* out, const double* Ls,
@@ -990,10 +1033,11 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
 }
 
 // One warp's chunk of the contraction: lane = row, NG groups of 8 r's at a
-// time; z rows read as broadcast 16-byte loads.
+// time (x loaded once per sample), z rows read as broadcast 16-byte loads.
+// Partials go to cps[(warp * CW + j) * 32 + lane], j < NG * 8.
 template <int NG>
 __device__ __forceinline__ void chain_chunk(const double* __restrict__ xs, const double* __restrict__ zs, int RP,
-                                           int g0, int cc0, int ccn, int lane, double* cps, int warp) {
+                                           int g0, int cc0, int ccn, int lane, double* cps, int warp, int CW) {
     double acc[NG * kCRB];
 #pragma unroll
     for (int a = 0; a < NG * kCRB; ++a) acc[a] = 0.0;
@@ -1022,57 +1066,20 @@ __device__ __forceinline__ void chain_chunk(const double* __restrict__ xs, const
         }
     }
 #pragma unroll
-    for (int a = 0; a < NG * kCRB; ++a) cps[(warp * RP + g0 * kCRB + a) * kRowTile + lane] = acc[a];
+    for (int a = 0; a < NG * kCRB; ++a) cps[(warp * CW + a) * kRowTile + lane] = acc[a];
 }
 
-// Sampled residual column partials of batch rb's temporal solve (DESIGN.md
-// 3.6), columns [c0, c0 + cn); the last residual block hsums all S columns.
-__device__ __noinline__ void chain_residual_item(const ChainParams& p, int rb, int c0, int cn, int nres, int RP,
-                                                 double* sm) {
-    const int N = p.N, R = p.R, S = p.S, Bq = p.B;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* u_rb = p.temporal + (p.t_len0 + int64_t(rb) * Bq) * R;
-    const double* XT = p.X_base + p.xoff[rb * N + 0];
-    const double* ZT = p.zbuf + int64_t(chain_zslot(0, rb, N)) * S * RP;
-    double* us = sm;                    // B x R
-    double* zs = us + Bq * R;           // cn x RP
-    double* xs = zs + kResidCols * RP;  // cn x B
-    for (int e = tid; e < Bq * R; e += blockDim.x) us[e] = __ldcg(u_rb + e);
-    for (int e = tid; e < cn * RP; e += blockDim.x) zs[e] = __ldcg(ZT + int64_t(c0) * RP + e);
-    for (int e = tid; e < cn * Bq; e += blockDim.x) {
-        const int c = e / Bq, i = e - c * Bq;
-        xs[e] = XT[xs_offset(i, c0 + c, S)];
-    }
-    __syncthreads();
-    for (int c = warp; c < cn; c += blockDim.x >> 5) {
-        double qn = 0.0, qd = 0.0;
-        const double* z = zs + c * RP;
-        for (int i = lane; i < Bq; i += 32) {
-            double uz = 0.0;
-            const double* u = us + i * R;
-            for (int r = 0; r < R; ++r) uz = __fma_rn(u[r], z[r], uz);
-            const double xv = xs[c * Bq + i];
-            const double e = xv - uz;
-            qn = __fma_rn(e, e, qn);
-            qd = __fma_rn(xv, xv, qd);
-        }
-        qn = butterfly32(qn);
-        qd = butterfly32(qd);
-        if (lane == 0) {
-            p.rpart[c0 + c] = qn;
-            p.rpart[S + c0 + c] = qd;
-        }
-    }
-    if (last_arrive_of(p.counter + 1, unsigned(nres))) {
-        block_hsum_inplace(p.rpart, S, p.rpart + 2 * S);
-        block_hsum_inplace(p.rpart + S, S, p.rpart + 2 * S);
-        if (tid == 0) {
-            p.resid[0] = __ldcg(p.rpart);
-            p.resid[1] = __ldcg(p.rpart + S);
-        }
-    }
-    __syncthreads();
-}
+// Shared-memory map of k_chain (doubles):
+//   [0, 8192)                X_s tile (TMA); phase B: L/D (TMA); Gram items: Z tile + chunk partials
+//   [8192, 8192 + 256*RP)    contraction Z tile (TMA)
+//   then                     contraction chunk partials [8][CW][32]
+//   [16384, ...)             factor block: A [64][65], D[64], G [64*64], column buffer [64]
+constexpr int kSmXs = 0;
+constexpr int kSmZs = kSuperSamples * kRowTile;  // 8192
+constexpr int kSmFact = 16384;
+constexpr int kSmTotal = 27136;                  // doubles
+constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
+constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
 
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
     namespace cg = cooperative_groups;
@@ -1085,6 +1092,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
     const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
+    const int NGP = (RP <= 32) ? 4 : 1;  // r-groups per contraction pass
+    const int CW = NGP * kCRB;           // chunk-partial width
     const int RR = R * R;
     const int G = gridDim.x;
     const int npairs = R * (R + 1) / 2;
@@ -1096,15 +1105,31 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
         mbar_init(&bar, 1);
     }
     __syncthreads();
-    const int n_gram = nsuper * kGramSplit;
+    const int n_gram = nsuper * kGramSplitC;
     const int gram_blocks = min(n_gram, max(1, G / 4));
-    const int cblocks = G - gram_blocks;  // contraction / residual blocks
+    const int cblocks = G - gram_blocks;  // contraction blocks: [0, cblocks)
     const bool is_gram_block = int(blockIdx.x) >= cblocks;
-    const int nres = (S + kResidCols - 1) / kResidCols;
+    double* xs = sm + kSmXs;
+    double* zs = sm + kSmZs;
+    double* cps = zs + kSuperSamples * RP;
+    const int ztotal = S * RP;
 
-    double* xs = sm;                             // [256][32]  (64 KB, TMA destination)
-    double* zs = sm + kSuperSamples * kRowTile;  // [256][RP]  (TMA destination)
-    double* cps = zs + kSuperSamples * RP;       // [8 chunks][RP][32]
+    // idx of this thread's phase-0 Z elements of stage (b, st), in registers; loaded one
+    // phase ahead so the phase-0 critical path is a single L2 gather.
+    int32_t nidx[kZU][kMaxOrder - 1];
+    auto load_idx = [&](int b, int st) {
+        if (b >= p.nb) return;
+        const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+#pragma unroll
+        for (int u = 0; u < kZU; ++u) {
+            const int e = (blockIdx.x + u * G) * blockDim.x + tid;
+            const int c = e / RP;
+#pragma unroll
+            for (int l = 0; l < kMaxOrder - 1; ++l)
+                nidx[u][l] = (e < ztotal && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
+        }
+    };
+    load_idx(0, 0);
 
     for (int b = 0; b < p.nb; ++b) {
         double* u_new = p.temporal + (p.t_len0 + int64_t(b) * p.B) * R;
@@ -1119,40 +1144,63 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             }
             const int rows = (st == 0) ? p.B : p.head[st - 1];
             const double* X = p.X_base + p.xoff[b * N + st];
-            const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
-            double* Z = p.zbuf + int64_t(chain_zslot(st, b, N)) * S * RP;
+            // Z of this stage: the temporal Z is kept per batch for the residual pass
+            double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * RP : p.gch + int64_t(st) * S * RP;
             const int tiles = (rows + kRowTile - 1) / kRowTile;
             const int n_contract = tiles * nsuper;
             unsigned long long* tr = p.trace ? p.trace + (int64_t(b) * N + st) * 16 : nullptr;
             if (tr && blockIdx.x == 0 && tid == 0) tr[0] = gtimer();
 
-            // stage start: TMA the first X_s tile of this block (independent of factors)
+            // stage start: TMA the first X_s tile of this block (independent of factors);
+            // its arrive.expect_tx is issued with the Z tile in phase 1.
             const bool contract_block = !is_gram_block && int(blockIdx.x) < n_contract;
             if (contract_block && tid == 0) {
-                // complete_tx lands on the barrier's current phase; the matching
-                // arrive.expect_tx (X + Z bytes) is issued in phase 1.
                 const int item = blockIdx.x, tile = item % tiles, m = item / tiles;
                 const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                 fence_proxy_async();
                 tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
             }
 
-            // ---------------- phase 0: Z = sampled Khatri-Rao rows (sampling.cpp:90-103), stride RP
-            for (int e = blockIdx.x * blockDim.x + tid; e < S * RP; e += G * blockDim.x) {
-                const int c = e / RP, r = e - c * RP;
-                double z = 0.0;
-                if (r < R) {
-                    z = 1.0;
+            // ---------------- phase 0: Z (S x RP, zero padded) over all blocks
+            // (sampling.cpp:90-103: 1.0 * F_0 * F_1 * ... left to right)
+            {
+                double f[kZU][kMaxOrder - 1];
 #pragma unroll
-                    for (int l = 0; l < kMaxOrder - 1; ++l) {
-                        if (l < n_other) {
-                            const int k = n_other - 1 - l;
-                            const int32_t i = __ldg(idx + int64_t(c) * n_other + k);
-                            z = z * __ldcg(F[l] + int64_t(i) * R + r);
+                for (int u = 0; u < kZU; ++u) {
+                    const int e = (blockIdx.x + u * G) * blockDim.x + tid;
+                    const int c = e / RP, r = e - c * RP;
+                    const bool live = e < ztotal && r < R;
+#pragma unroll
+                    for (int l = 0; l < kMaxOrder - 1; ++l)
+                        f[u][l] = (live && l < n_other) ? __ldcg(F[l] + int64_t(nidx[u][l]) * R + r) : 1.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kZU; ++u) {
+                    const int e = (blockIdx.x + u * G) * blockDim.x + tid;
+                    if (e < ztotal) {
+                        const int r = e % RP;
+                        double z = 0.0;
+                        if (r < R) {
+                            z = 1.0;
+#pragma unroll
+                            for (int l = 0; l < kMaxOrder - 1; ++l)
+                                if (l < n_other) z = z * f[u][l];
                         }
+                        Z[e] = z;
                     }
                 }
-                Z[e] = z;
+                for (int e = (blockIdx.x + kZU * G) * blockDim.x + tid; e < ztotal; e += G * blockDim.x) {
+                    // rare tail (S * RP > kZU * G * 256): direct
+                    const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+                    const int c = e / RP, r = e - c * RP;
+                    double z = 0.0;
+                    if (r < R) {
+                        z = 1.0;
+                        for (int l = 0; l < n_other; ++l)
+                            z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c) * n_other + (n_other - 1 - l))) * R + r);
+                    }
+                    Z[e] = z;
+                }
             }
             asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA in phase 1
             grid.sync();
@@ -1161,17 +1209,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // ---------------- phase 1
             if (is_gram_block) {
                 for (int gi = blockIdx.x - cblocks; gi < n_gram; gi += gram_blocks) {
-                    const int m = gi / kGramSplit, part = gi % kGramSplit;
+                    const int m = gi / kGramSplitC, part = gi % kGramSplitC;
                     const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                     const int nk = (cn + kChunk - 1) / kChunk;
-                    const int pp0 = (RR * part) / kGramSplit, pp1 = (RR * (part + 1)) / kGramSplit;
+                    const int pp0 = (RR * part) / kGramSplitC, pp1 = (RR * (part + 1)) / kGramSplitC;
                     const int npp = pp1 - pp0;
-                    double* gz = sm;                           // cn x RP
-                    double* gcp = sm + kSuperSamples * 64;     // [8][npp]
+                    double* gz = sm;                       // cn x RP
+                    double* gcp = sm + kSuperSamples * 64;  // [8][npp]
                     if (tid == 0) {
                         fence_proxy_async();
-                        mbar_expect_tx(&bar, unsigned(cn * RP * 8));
                         tma_load_1d(gz, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        mbar_expect_tx(&bar, unsigned(cn * RP * 8));
                     }
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
@@ -1179,9 +1227,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         const int k = u / npp, pp = pp0 + (u - k * npp);
                         const int r1 = pp % R, r2 = pp / R;
                         const int cc0 = k * kChunk, ccn = min(kChunk, cn - cc0);
+                        const double* za = gz + cc0 * RP + r1;
+                        const double* zb = gz + cc0 * RP + r2;
                         double acc = 0.0;
-                        for (int cc = 0; cc < ccn; ++cc)
-                            acc = __fma_rn(gz[(cc0 + cc) * RP + r1], gz[(cc0 + cc) * RP + r2], acc);
+                        if (ccn == kChunk) {
+#pragma unroll 8
+                            for (int cc = 0; cc < kChunk; ++cc) acc = __fma_rn(za[cc * RP], zb[cc * RP], acc);
+                        } else {
+                            for (int cc = 0; cc < ccn; ++cc) acc = __fma_rn(za[cc * RP], zb[cc * RP], acc);
+                        }
                         gcp[k * npp + (pp - pp0)] = acc;
                     }
                     __syncthreads();
@@ -1191,62 +1245,86 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         p.gpart[int64_t(m) * RR + pp0 + q] = v;
                     }
                     __syncthreads();
-                    if (last_arrive_of(p.counter, unsigned(n_gram))) {
-                        if (tr && tid == 0) tr[3] = gtimer();
-                        double* A = sm;                  // [64][65]
-                        double* D = A + 64 * kLdStride;  // 64
-                        double* Gs = D + 64;             // R x R column-major
-                        // Gram combine in superchunk order; Q += G for the modes (rocp.cpp:108)
-                        for (int pp = tid; pp < RR; pp += blockDim.x) {
-                            double tot = __ldcg(p.gpart + pp);
-                            for (int mm = 1; mm < nsuper; ++mm) tot = tot + __ldcg(p.gpart + int64_t(mm) * RR + pp);
-                            if (st > 0) {
-                                tot = __ldcg(p.Q[st - 1] + pp) + tot;
-                                p.Q[st - 1][pp] = tot;
-                            }
-                            Gs[pp] = tot;
+                }
+                if (last_arrive_of(p.counter, unsigned(gram_blocks))) {
+                    if (tr && tid == 0) tr[3] = gtimer();
+                    double* A = sm + kSmFact;        // [64][65]
+                    double* D = A + 64 * kLdStride;  // 64
+                    double* Gs = D + 64;             // R x R column-major
+                    double* colb = Gs + 64 * 64;     // 64
+                    // Gram combine in superchunk order; Q += G for the modes (rocp.cpp:108)
+                    for (int pp = tid; pp < RR; pp += blockDim.x) {
+                        double v[8];
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * RR + pp) : 0.0;
+                        double tot = v[0];
+#pragma unroll
+                        for (int m = 1; m < 8; ++m)
+                            if (m < nsuper) tot = tot + v[m];
+                        for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * RR + pp);
+                        if (st > 0) {
+                            tot = __ldcg(p.Q[st - 1] + pp) + tot;
+                            p.Q[st - 1][pp] = tot;
                         }
-                        __syncthreads();
-                        if (tr && tid == 0) tr[10] = gtimer();
-                        // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
-                        if (tid == 0) {
-                            double maxdiag = Gs[0];
-                            for (int k = 1; k < R; ++k)
-                                if (Gs[k * R + k] > maxdiag) maxdiag = Gs[k * R + k];
-                            double trc = Gs[0];
-                            for (int k = 1; k < R; ++k) trc = trc + Gs[k * R + k];
-                            s_tr = trc;
-                            s_mode = (maxdiag <= 0.0) ? 0 : 1;
-                            s_reg = (s_mode == 0) ? 1 : 0;
+                        Gs[pp] = tot;
+                    }
+                    __syncthreads();
+                    if (tr && tid == 0) tr[10] = gtimer();
+                    // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
+                    if (tid == 0) {
+                        double maxdiag = Gs[0], trc = Gs[0];
+#pragma unroll 8
+                        for (int k = 1; k < R; ++k) {
+                            const double dg = Gs[k * R + k];
+                            if (dg > maxdiag) maxdiag = dg;
+                            trc = trc + dg;
                         }
-                        __syncthreads();
-                        if (s_mode == 1) {
-                            ldlt_one_sync(A, D, R, 0.0, Gs, pairs, npairs);
-                            if (tid == 0) {
-                                double dmin = D[0], dmax = D[0];
-                                for (int k = 0; k < R; ++k) {
-                                    if (D[k] < dmin) dmin = D[k];
-                                    if (D[k] > dmax) dmax = D[k];
-                                }
-                                s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+                        s_tr = trc;
+                        s_mode = (maxdiag <= 0.0) ? 0 : 1;
+                        s_reg = (s_mode == 0) ? 1 : 0;
+                    }
+                    __syncthreads();
+                    if (tr && tid == 0) tr[12] = gtimer();
+                    auto factor = [&](double lambda) {
+                        if (R <= 32) {
+                            if (warp == 0) {
+                                if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, D, colb);
+                                else ldlt_warp<32>(Gs, lambda, R, A, D, colb);
                             }
                             __syncthreads();
-                            if (s_reg) ldlt_one_sync(A, D, R, 1e-12 * s_tr, Gs, pairs, npairs);
+                        } else {
+                            ldlt_one_sync(A, D, R, lambda, Gs, pairs, npairs);
                         }
-                        __syncthreads();
-                        if (tr && tid == 0) tr[11] = gtimer();
-                        for (int t = tid; t < RR; t += blockDim.x) {
-                            const int k = t / R, i = t % R;
-                            p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
-                        }
-                        for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
+                    };
+                    if (s_mode == 1) {
+                        factor(0.0);
+                        if (tr && tid == 0) tr[13] = gtimer();
                         if (tid == 0) {
-                            p.mode_flag[0] = s_mode;
-                            if (s_reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
-                            if (tr) tr[4] = gtimer();
+                            double dmin = D[0], dmax = D[0];
+#pragma unroll 8
+                            for (int k = 0; k < R; ++k) {
+                                const double dk = D[k];
+                                if (dk < dmin) dmin = dk;
+                                if (dk > dmax) dmax = dk;
+                            }
+                            s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
                         }
                         __syncthreads();
+                        if (s_reg) factor(1e-12 * s_tr);
                     }
+                    __syncthreads();
+                    if (tr && tid == 0) tr[11] = gtimer();
+                    for (int t = tid; t < RR; t += blockDim.x) {
+                        const int k = t / R, i = t % R;
+                        p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
+                    }
+                    for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
+                    if (tid == 0) {
+                        p.mode_flag[0] = s_mode;
+                        if (s_reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
+                        if (tr) tr[4] = gtimer();
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
                 }
             } else {
                 for (int item = blockIdx.x; item < n_contract; item += cblocks) {
@@ -1263,71 +1341,117 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
                     if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[8] = gtimer();
-                    // warp w = chunk w of the superchunk; lane = row; all r-groups
+                    const int nk = (cn + kChunk - 1) / kChunk;
                     const int cc0 = warp * kChunk;
                     const int ccn = min(kChunk, cn - cc0);
-                    if (ccn > 0) {
-                        for (int g0 = 0; g0 < ng; g0 += 4) {
-                            const int ngp = min(4, ng - g0);
-                            if (ngp == 4) chain_chunk<4>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
-                            else if (ngp == 3) chain_chunk<3>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
-                            else if (ngp == 2) chain_chunk<2>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
-                            else chain_chunk<1>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp);
+                    for (int g0 = 0; g0 < ng; g0 += NGP) {
+                        if (ccn > 0) {  // warp w = chunk w of the superchunk; lane = row
+                            const int ngp = min(NGP, ng - g0);
+                            if (ngp == 4) chain_chunk<4>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                            else if (ngp == 3) chain_chunk<3>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                            else if (ngp == 2) chain_chunk<2>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                            else chain_chunk<1>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
                         }
-                    }
-                    __syncthreads();
-                    // superchunk partial = chunk partials in increasing chunk order
-                    const int nk = (cn + kChunk - 1) / kChunk;
-                    for (int e = tid; e < R * kRowTile; e += blockDim.x) {
-                        const int r = e >> 5, l2 = e & 31;
-                        if (l2 < nrows) {
-                            double q = cps[r * kRowTile + l2];
-                            for (int k = 1; k < nk; ++k) q = q + cps[(k * RP + r) * kRowTile + l2];
-                            p.cpart[(int64_t(m) * rows + i0 + l2) * R + r] = q;
+                        __syncthreads();
+                        // superchunk partial = chunk partials in increasing chunk order
+                        for (int e = tid; e < CW * kRowTile; e += blockDim.x) {
+                            const int rl = e >> 5, l2 = e & 31, r = g0 * kCRB + rl;
+                            if (l2 < nrows && r < R) {
+                                double qq = cps[rl * kRowTile + l2];
+                                for (int k = 1; k < nk; ++k) qq = qq + cps[(k * CW + rl) * kRowTile + l2];
+                                p.cpart[(int64_t(m) * rows + i0 + l2) * R + r] = qq;
+                            }
                         }
+                        __syncthreads();
                     }
-                    __syncthreads();
                     if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[9] = gtimer();
-                }
-                // idle blocks of the temporal stage: residual of the previous batch
-                if (st == 0 && b > 0 && p.resid_level >= 1) {
-                    const int first = n_contract < cblocks ? n_contract : cblocks;
-                    const int nblk = cblocks - first;
-                    if (nblk > 0) {
-                        if (int(blockIdx.x) >= first)
-                            for (int ri = blockIdx.x - first; ri < nres; ri += nblk)
-                                chain_residual_item(p, b - 1, ri * kResidCols, min(kResidCols, S - ri * kResidCols),
-                                                    nres, RP, sm);
-                    } else if (blockIdx.x == 0) {
-                        for (int ri = 0; ri < nres; ++ri)
-                            chain_residual_item(p, b - 1, ri * kResidCols, min(kResidCols, S - ri * kResidCols),
-                                                nres, RP, sm);
-                    }
                 }
             }
             if (tr && blockIdx.x == 0 && tid == 0) tr[2] = gtimer();
+            __syncthreads();
             grid.sync();
             if (tr && blockIdx.x == 0 && tid == 0) tr[5] = gtimer();
 
-            // ---------------- phase 2: row solves
-            if (int(blockIdx.x) < rows) {
-                double* Ls = sm;  // R x R, L(i,k) at [k*R + i]
-                double* Ds = sm + RR;
-                for (int t = tid; t < RR + R; t += blockDim.x) Ls[t] = __ldcg(p.LD + t);
-                __syncthreads();
-                const int mode = __ldcg(p.mode_flag);
-                double* out = (st == 0) ? u_new : p.U[st - 1];
-                chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ds, mode);
+            // ---------------- phase B: row solves; idle blocks load the next stage's idx
+            {
+                const int nb2 = (st + 1 < N) ? b : b + 1, ns2 = (st + 1 < N) ? st + 1 : 0;
+                if (int(blockIdx.x) < rows) {
+                    double* Ls = sm;  // R x R, L(i,k) at [k*R + i], then D
+                    if (tid == 0) {
+                        const unsigned bytes = unsigned(((RR + R + 1) & ~1) * 8);
+                        fence_proxy_async();
+                        tma_load_1d(Ls, p.LD, bytes, &bar);
+                        mbar_expect_tx(&bar, bytes);
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    const int mode = __ldcg(p.mode_flag);
+                    double* out = (st == 0) ? u_new : p.U[st - 1];
+                    chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ls + RR,
+                                    mode);
+                }
+                load_idx(nb2, ns2);
             }
             if (tr && blockIdx.x == 0 && tid == 0) tr[6] = gtimer();
+            __syncthreads();
             grid.sync();
             if (tr && blockIdx.x == 0 && tid == 0) tr[7] = gtimer();
         }
     }
-    // residual of the window's last batch
-    if (p.resid_level >= 1 && p.nb > 0) {
-        for (int ri = blockIdx.x; ri < nres; ri += G)
-            chain_residual_item(p, p.nb - 1, ri * kResidCols, min(kResidCols, S - ri * kResidCols), nres, RP, sm);
+}
+
+// Sampled residual of every batch's temporal solve in a window,
+// after the chain: column partials (warp per column), then hsum per batch.
+struct WinResidParams {
+    int N, R, S, B, RP, nb;
+    const double* temporal;  // row-major; batch b's rows at t_len0 + b*B
+    int64_t t_len0;
+    const double* X_base;
+    const int64_t* xoff;
+    const double* zT;        // nb x S x RP
+    double* cols;            // nb x 3 x S
+    double* out;             // nb x 2 (num, den)
+    double* last_out;        // 2: the last batch's (num, den)
+};
+
+__global__ void __launch_bounds__(256) k_win_resid_cols(const WinResidParams p) {
+    const int b = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + warp;
+    if (c >= p.S) return;
+    const double* u = p.temporal + (p.t_len0 + int64_t(b) * p.B) * p.R;
+    const double* X = p.X_base + p.xoff[b * p.N];
+    const double* z = p.zT + (int64_t(b) * p.S + c) * p.RP;
+    double qn = 0.0, qd = 0.0;
+    for (int i = lane; i < p.B; i += 32) {
+        double uz = 0.0;
+        for (int r = 0; r < p.R; ++r) uz = __fma_rn(u[int64_t(i) * p.R + r], z[r], uz);
+        const double xv = X[xs_offset(i, c, p.S)];
+        const double e = xv - uz;
+        qn = __fma_rn(e, e, qn);
+        qd = __fma_rn(xv, xv, qd);
+    }
+    qn = butterfly32(qn);
+    qd = butterfly32(qd);
+    if (lane == 0) {
+        p.cols[(int64_t(b) * 3 + 0) * p.S + c] = qn;
+        p.cols[(int64_t(b) * 3 + 1) * p.S + c] = qd;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_win_resid_sum(const WinResidParams p) {
+    const int b = blockIdx.x;
+    double* base = p.cols + int64_t(b) * 3 * p.S;
+    block_hsum_inplace(base, p.S, base + 2 * p.S);
+    block_hsum_inplace(base + p.S, p.S, base + 2 * p.S);
+    if (threadIdx.x == 0) {
+        const double num = __ldcg(base), den = __ldcg(base + p.S);
+        p.out[2 * b] = num;
+        p.out[2 * b + 1] = den;
+        if (b == p.nb - 1) {
+            p.last_out[0] = num;
+            p.last_out[1] = den;
+        }
     }
 }
 

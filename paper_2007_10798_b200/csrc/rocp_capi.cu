@@ -473,6 +473,7 @@ struct Window {
     DBuf<double> X;            // [b][stage] I_stage x S (column-major)
     std::vector<int64_t> xoff;
     DBuf<int64_t> xoff_dev;
+    DBuf<double> zT, rcols, rhist;  // temporal Z per batch, residual column partials, per-batch residuals
     JobList jobs;
     // key of the uploaded job list
     const double* key_x = nullptr;
@@ -497,7 +498,7 @@ struct rocp_stream {
     DBuf<double> resid;           // N x 2 (num, den) of the last batch
     DBuf<double> staging;         // host-slab staging for consume_host
     DBuf<int> flags;              // [0] temporal regularized (stream flag), [2] last mode solve
-    DBuf<double> zbuf, gpart, LD, rpart;  // persistent-chain scratch
+    DBuf<double> gpart, LD, rpart, zmodes;  // persistent-chain scratch
     DBuf<int> mode_flag;
     bool trace_on = false;             // chain phase timestamps (profiling aid)
     DBuf<unsigned long long> trace;
@@ -562,6 +563,12 @@ void ensure_window(rocp_stream* st, int64_t nb, int64_t B) {
             off += xs_size(st->stage_rows(stage, Bn), S);  // row-tiled layout
         }
     W.X.alloc(size_t(off));
+    {
+        const int64_t RP = ((st->R + kCRB - 1) / kCRB) * kCRB;
+        W.zT.alloc(size_t(nbn * S * RP));
+        W.rcols.alloc(size_t(nbn * 3 * S));
+        W.rhist.alloc(size_t(nbn * 2));
+    }
     W.xoff_dev.alloc(W.xoff.size());
     CK(cudaMemcpy(W.xoff_dev.p, W.xoff.data(), W.xoff.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     W.nb = nbn;
@@ -701,14 +708,9 @@ void enqueue_chain(rocp_stream* st, int64_t nb, int64_t B) {
 }
 
 size_t chain_smem(int R, int B) {
-    const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
-    const size_t tiles = (size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * RP +
-                          size_t(kSuper) * RP * kRowTile) * sizeof(double);
-    const size_t gram = (size_t(kSuperSamples) * 64 + size_t(kSuper) * ((R * R + kGramSplit - 1) / kGramSplit)) *
-                        sizeof(double);
-    const size_t fact = (size_t(64) * kLdStride + 64 + 64 * 64) * sizeof(double);
-    const size_t resid = (size_t(B) * R + size_t(kResidCols) * RP + size_t(kResidCols) * B) * sizeof(double);
-    return std::max(std::max(tiles, gram), std::max(fact, resid));
+    (void)R;
+    (void)B;
+    return size_t(kSmTotal) * sizeof(double);  // fixed map (kernels.cuh, k_chain)
 }
 
 void launch_chain_k(rocp_stream* st, const ChainParams& p) {
@@ -756,7 +758,8 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B) {
     p.idx_base = st->win.idx.p;
     p.X_base = st->win.X.p;
     p.xoff = st->win.xoff_dev.p;
-    p.zbuf = st->zbuf.p;
+    p.zbuf = st->win.zT.p;
+    p.gch = st->zmodes.p;
     p.gpart = st->gpart.p;
     p.cpart = st->dev->contract_partial.p;
     p.LD = st->LD.p;
@@ -774,6 +777,28 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B) {
         p.trace = nullptr;
     }
     launch_chain_k(st, p);
+    if (st->resid_level >= 1) {  // sampled residual of every batch's temporal solve (off the chain)
+        WinResidParams w{};
+        w.N = st->N;
+        w.R = st->R;
+        w.S = int(st->s);
+        w.B = int(B);
+        w.RP = ((st->R + kCRB - 1) / kCRB) * kCRB;
+        w.nb = int(nb);
+        w.temporal = st->temporal.p;
+        w.t_len0 = st->t_len;
+        w.X_base = st->win.X.p;
+        w.xoff = st->win.xoff_dev.p;
+        w.zT = st->win.zT.p;
+        w.cols = st->win.rcols.p;
+        w.out = st->win.rhist.p;
+        w.last_out = st->resid.p;
+        const dim3 g1{unsigned((st->s + 7) / 8), unsigned(nb), 1u};
+        k_win_resid_cols<<<g1, 256, 0, st->dev->stream>>>(w);
+        after_launch(st->dev, "k_win_resid_cols");
+        k_win_resid_sum<<<unsigned(nb), 256, 0, st->dev->stream>>>(w);
+        after_launch(st->dev, "k_win_resid_sum");
+    }
 }
 
 void check_capacity(rocp_stream* st, int64_t add) {
@@ -1332,9 +1357,9 @@ rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int 
     st->flags.alloc(4);
     st->seed_dev.alloc(1);
     st->batch_dev.alloc(1);
-    st->zbuf.alloc(size_t((order + 1) * s * (((rank + kCRB - 1) / kCRB) * kCRB)));
     st->gpart.alloc(size_t(((s + kSuperSamples - 1) / kSuperSamples) * rank * rank));
-    st->LD.alloc(size_t(rank * rank + rank));
+    st->zmodes.alloc(size_t(order * s * (((rank + kCRB - 1) / kCRB) * kCRB)));
+    st->LD.alloc(size_t(rank * rank + rank + 2));
     st->rpart.alloc(size_t(3 * s));
     st->mode_flag.alloc(4);
     CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));

@@ -20,6 +20,21 @@ __global__ void k_ldlt(const double* G, int R, long long* cyc, double* out) {
     if (threadIdx.x == 0) { cyc[0] = t1 - t0; out[0] = sm[64 * kLdStride + R - 1]; }
 }
 
+__global__ void k_ldlt_warp(const double* G, int R, long long* cyc, double* out) {
+    extern __shared__ double sm[];
+    double* Gs = sm + 64 * kLdStride + 64;
+    for (int t = threadIdx.x; t < R * R; t += blockDim.x) Gs[t] = G[t];
+    __syncthreads();
+    long long t0 = clock64();
+    if (threadIdx.x < 32) {
+        if (R <= 16) ldlt_warp<16>(Gs, 0.0, R, sm, sm + 64 * kLdStride, Gs + R * R);
+        else ldlt_warp<32>(Gs, 0.0, R, sm, sm + 64 * kLdStride, Gs + R * R);
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { cyc[0] = t1 - t0; out[0] = sm[64 * kLdStride + R - 1]; }
+}
+
 int main() {
     for (int R : {10, 16, 20, 50}) {
         double h[64 * 64];
@@ -33,6 +48,15 @@ int main() {
         long long cyc; cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
         printf("R=%d ldlt_one_sync: %lld cycles (%.1f per step) err=%s\n", R, cyc, double(cyc) / R,
                cudaGetErrorString(cudaGetLastError()));
+        double d1; cudaMemcpy(&d1, o, 8, cudaMemcpyDeviceToHost);
+        if (R <= 32) {
+            cudaFuncSetAttribute(k_ldlt_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+            for (int rep = 0; rep < 3; ++rep) k_ldlt_warp<<<1, 256, 80000>>>(G, R, c, o);
+            cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+            double d2; cudaMemcpy(&d2, o, 8, cudaMemcpyDeviceToHost);
+            printf("R=%d ldlt_warp: %lld cycles (%.1f per step) same_last_d=%d err=%s\n", R, cyc, double(cyc) / R,
+                   int(d1 == d2), cudaGetErrorString(cudaGetLastError()));
+        }
     }
     return 0;
 }

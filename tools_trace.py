@@ -40,10 +40,10 @@ def med(a):
 for stg in range(N):
     t = tr[stg::N].astype(float)
     t[t == 0] = np.nan
-    z = lambda k: t[:, k] - t[:, 1]
-    print(f"stage {stg}: p0+sync={med(t[:,1]-t[:,0]):.2f} | item0 load={med(t[:,8]-t[:,1]):.2f} "
-          f"compute={med(t[:,9]-t[:,8]):.2f} p1end(b0)={med(z(2)):.2f} | gram->factor start={med(z(3)):.2f} "
-          f"combine={med(t[:,10]-t[:,3]):.2f} factor={med(t[:,11]-t[:,10]):.2f} publish={med(t[:,4]-t[:,11]):.2f} | "
-          f"sync1 done={med(z(5)):.2f} p2={med(t[:,6]-t[:,5]):.2f} sync2={med(t[:,7]-t[:,6]):.2f} | "
-          f"total={med(t[:,7]-t[:,0]):.2f} us")
+    z = lambda k: t[:, k] - t[:, 0]
+    print(f"stage {stg}: p0+sync={med(z(1)):.2f} | item0 ready={med(t[:,8]-t[:,1]):.2f} compute={med(t[:,9]-t[:,8]):.2f} | "
+          f"gram->factor start={med(t[:,3]-t[:,1]):.2f} combine={med(t[:,10]-t[:,3]):.2f} prologue={med(t[:,12]-t[:,10]):.2f} "
+          f"ldlt={med(t[:,13]-t[:,12]):.2f} check={med(t[:,11]-t[:,13]):.2f} publish={med(t[:,4]-t[:,11]):.2f} | "
+          f"sync1 done={med(z(5)):.2f} rows={med(t[:,6]-t[:,5]):.2f} sync2={med(t[:,7]-t[:,6]):.2f} | total={med(t[:,7]-t[:,0]):.2f} us")
 print("whole window us:", (tr[-1, 7] - tr[0, 0]) / 1e3)
+print("residual of last batch:", st.last_residuals()[0])
