@@ -17,6 +17,7 @@ Matrices are numpy column-major (Fortran) arrays, like Eigen::MatrixXd.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import subprocess
@@ -183,6 +184,20 @@ def auto_sample_count(rank):
     return max(rank, int(np.ceil(10.0 * rank * np.log(float(rank)))))
 
 
+_live_devices = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all_devices():
+    """Deterministic teardown before interpreter finalization: streams and
+    tensors are released before their handle, handles before the CUDA runtime."""
+    for d in list(_live_devices):
+        try:
+            d.close()
+        except Exception:
+            pass
+
+
 class Device:
     """One handle per GPU (rocp_dev)."""
 
@@ -193,13 +208,20 @@ class Device:
             raise RocpError(rc, f"rocp_create(device={device}) failed (is a GPU visible?)")
         self.h = h
         self._children = weakref.WeakSet()  # streams/tensors freed before the handle
+        _live_devices.add(self)
 
     def _adopt(self, obj):
         self._children.add(obj)
 
     def close(self):
         if getattr(self, "h", None):
-            for ch in list(self._children):
+            lib().rocp_synchronize(self.h)
+            # streams first (they reference window arenas), then tensors
+            kids = list(self._children)
+            for ch in kids:
+                if isinstance(ch, RocpStream):
+                    ch._free()
+            for ch in kids:
                 ch._free()
             lib().rocp_destroy(self.h)
             self.h = None

@@ -156,7 +156,14 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherJob* __re
         if (e < total) {
             const uint32_t c = e / I;
             const uint32_t i = e - c * I;
-            v[u] = __ldcs(t + __ldg(base + c) + int64_t(i) * ms);
+            const double* a = t + __ldg(base + c) + int64_t(i) * ms;
+            if (ms == 1) {
+                v[u] = __ldcs(a);  // contiguous mode-1 fibre: full-line fetches are all useful
+            } else {
+                // isolated strided element: ask L2 for a 64-byte fill instead of a full
+                // 128-byte line (halves DRAM bytes per element; profiles/README.md)
+                asm volatile("ld.global.cs.L2::64B.f64 %0, [%1];" : "=d"(v[u]) : "l"(a));
+            }
         }
     }
 #pragma unroll

@@ -1,0 +1,389 @@
+// rocp_api.cpp -- C++ host API (include/rocp_b200/rocp.hpp) over the C ABI.
+// Every call goes to librocp_b200.so (sm_100a kernels); there is no CPU
+// compute path here apart from argument validation, layout bookkeeping and the
+// reference's own host-side random_model.
+
+#include "../../include/rocp_b200/rocp.hpp"
+
+#include "../../include/rocp_b200.h"
+
+#include <cmath>
+#include <memory>
+
+namespace rocp {
+
+namespace {
+
+struct DevHolder {
+    int device = 0;
+    rocp_dev* h = nullptr;
+    ~DevHolder() {
+        if (h) rocp_destroy(h);
+    }
+};
+thread_local DevHolder g_dev;
+
+void raise(rocp_dev* d, rocp_status st, int sweep = 0) {
+    const std::string msg = rocp_last_error(d);
+    if (st == ROCP_E_DOMAIN) throw std::domain_error(msg);
+    if (st == ROCP_E_NUMERICAL) throw NumericalError(msg, sweep);
+    throw std::runtime_error("rocp_b200 status " + std::to_string(int(st)) + ": " + msg);
+}
+
+void check(rocp_status st, int sweep = 0) {
+    if (st != ROCP_OK) raise(device_handle(), st, sweep);
+}
+
+void check_mode(const Dims& dims, int mode) {  // tensor.cpp:19-23
+    if (mode < 1 || mode > static_cast<int>(dims.size()))
+        throw std::domain_error("mode " + std::to_string(mode) + " out of range for order " +
+                                std::to_string(dims.size()));
+}
+
+// RAII device tensor uploaded from a host DenseTensor.
+struct DevTensor {
+    rocp_tensor* t = nullptr;
+    explicit DevTensor(const DenseTensor& x) {
+        check(rocp_tensor_create(device_handle(), x.dims().data(), x.order(), x.data(), &t));
+    }
+    ~DevTensor() {
+        if (t) rocp_tensor_free(t);
+    }
+};
+
+std::vector<const double*> ptrs(const std::vector<Matrix>& ms) {
+    std::vector<const double*> p;
+    for (const Matrix& m : ms) p.push_back(m.data());
+    return p;
+}
+
+}  // namespace
+
+void set_device(int device) {
+    if (g_dev.h && g_dev.device != device) {
+        rocp_destroy(g_dev.h);
+        g_dev.h = nullptr;
+    }
+    g_dev.device = device;
+}
+
+rocp_dev* device_handle() {
+    if (!g_dev.h) {
+        rocp_dev* d = nullptr;
+        if (rocp_create(g_dev.device, 1, 0, nullptr, &d) != ROCP_OK)
+            throw std::runtime_error("rocp_b200: cannot open CUDA device " + std::to_string(g_dev.device));
+        g_dev.h = d;
+    }
+    return g_dev.h;
+}
+
+bool Matrix::allFinite() const {
+    for (double x : v_)
+        if (!std::isfinite(x)) return false;
+    return true;
+}
+
+// ---- tensor -------------------------------------------------------------------------
+Index element_count(const Dims& dims) {
+    Index n = 1;
+    for (Index d : dims) n *= d;
+    return n;
+}
+
+DenseTensor::DenseTensor(Dims dims) : dims_(std::move(dims)) {
+    if (dims_.size() < 2) throw std::domain_error("tensor order must be at least 2");
+    for (Index d : dims_)
+        if (d < 1) throw std::domain_error("tensor extents must be positive");
+    data_.assign(static_cast<size_t>(element_count(dims_)), 0.0);
+}
+
+DenseTensor::DenseTensor(Dims dims, std::vector<double> data) : dims_(std::move(dims)), data_(std::move(data)) {
+    if (dims_.size() < 2) throw std::domain_error("tensor order must be at least 2");
+    for (Index d : dims_)
+        if (d < 1) throw std::domain_error("tensor extents must be positive");
+    if (static_cast<Index>(data_.size()) != element_count(dims_))
+        throw std::domain_error("data length does not match product of extents");
+}
+
+Index codomain_size(const Dims& dims, int mode) {
+    check_mode(dims, mode);
+    return element_count(dims) / dims[static_cast<size_t>(mode - 1)];
+}
+
+Index linear_index(std::span<const Index> multi, const Dims& dims, int mode) {
+    check_mode(dims, mode);
+    if (multi.size() != dims.size() - 1)
+        throw std::domain_error("multi-index must cover all modes except the unfolding mode");
+    Index j = 0, stride = 1;
+    size_t pos = 0;
+    for (size_t k = 0; k < dims.size(); ++k) {
+        if (static_cast<int>(k) + 1 == mode) continue;
+        const Index i = multi[pos++];
+        if (i < 1 || i > dims[k]) throw std::domain_error("multi-index out of range");
+        j += (i - 1) * stride;
+        stride *= dims[k];
+    }
+    return j + 1;
+}
+
+std::vector<Index> decode_index(Index j, const Dims& dims, int mode) {
+    std::vector<Index> out(dims.size() - 1);
+    check(rocp_decode_rows(device_handle(), dims.data(), static_cast<int>(dims.size()), mode, &j, 1, out.data()));
+    return out;
+}
+
+// ---- model --------------------------------------------------------------------------
+Dims KruskalModel::dims() const {
+    Dims d;
+    for (const Matrix& f : factors) d.push_back(f.rows());
+    return d;
+}
+
+KruskalModel random_model(const Dims& dims, int rank, Rng& rng) {
+    KruskalModel m;
+    m.rank = rank;
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (Index d : dims) {
+        Matrix f(d, rank);
+        for (Index i = 0; i < d; ++i)  // i outer, r inner, one distribution across factors
+            for (int r = 0; r < rank; ++r) f(i, r) = gauss(rng);
+        m.factors.push_back(std::move(f));
+    }
+    return m;
+}
+
+std::vector<Matrix> factors_excluding(const KruskalModel& m, int mode) {
+    if (mode < 1 || mode > m.order()) throw std::domain_error("mode out of range");
+    std::vector<Matrix> out;
+    for (int k = m.order(); k >= 1; --k)
+        if (k != mode) out.push_back(m.factors[static_cast<size_t>(k - 1)]);
+    return out;
+}
+
+double model_fitness(const DenseTensor& x, const KruskalModel& m) {
+    if (m.dims() != x.dims()) throw std::domain_error("dims order does not match model");
+    DevTensor t(x);
+    const auto p = ptrs(m.factors);
+    double fit = 0.0;
+    check(rocp_model_fitness(device_handle(), t.t, p.data(), m.rank, &fit));
+    return fit;
+}
+
+// ---- sampling -----------------------------------------------------------------------
+SampleIndexSet SampleIndexSet::from_rows(const Dims& dims, int mode, std::vector<Index> rows) {
+    SampleIndexSet idx;
+    idx.mode = mode;
+    idx.dims = dims;
+    idx.decoded.assign(rows.size() * (dims.size() - 1), 0);
+    if (!rows.empty())
+        check(rocp_decode_rows(device_handle(), dims.data(), static_cast<int>(dims.size()), mode, rows.data(),
+                               static_cast<Index>(rows.size()), idx.decoded.data()));
+    idx.rows = std::move(rows);
+    return idx;
+}
+
+SampleIndexSet SampleIndexSet::all_columns(const Dims& dims, int mode) {
+    const Index co = codomain_size(dims, mode);
+    std::vector<Index> rows(static_cast<size_t>(co));
+    for (Index j = 0; j < co; ++j) rows[static_cast<size_t>(j)] = j + 1;
+    return from_rows(dims, mode, std::move(rows));
+}
+
+Index auto_sample_count(int rank) {  // sampling.cpp:40-45
+    if (rank < 1) throw std::domain_error("rank must be positive");
+    const double s = 10.0 * rank * std::log(static_cast<double>(rank));
+    return std::max<Index>(rank, static_cast<Index>(std::ceil(s)));
+}
+
+SampleIndexSet draw_samples(const Dims& dims, int mode, Index s, CounterKey key) {
+    SampleIndexSet idx;
+    idx.mode = mode;
+    idx.dims = dims;
+    idx.rows.assign(static_cast<size_t>(std::max<Index>(s, 0)), 0);
+    idx.decoded.assign(static_cast<size_t>(std::max<Index>(s, 0)) * (dims.size() - 1), 0);
+    check(rocp_draw_samples(device_handle(), dims.data(), static_cast<int>(dims.size()), mode, s, key.seed,
+                            key.batch, key.iteration, idx.rows.data(), idx.decoded.data()));
+    return idx;
+}
+
+SampleIndexSet draw_samples(const Dims& dims, int mode, Index s, Rng& rng) {
+    return draw_samples(dims, mode, s, CounterKey{rng(), 0, 0});
+}
+
+Matrix sample_unfolding(const DenseTensor& t, const SampleIndexSet& idx) {
+    if (t.dims() != idx.dims) throw std::domain_error("sample_unfolding: index set drawn against different dims");
+    Matrix out(t.dims()[static_cast<size_t>(idx.mode - 1)], idx.count());
+    DevTensor d(t);
+    check(rocp_sample_unfolding(device_handle(), d.t, idx.mode, idx.rows.data(), idx.count(), out.data()));
+    return out;
+}
+
+Matrix sampled_khatri_rao(const SampleIndexSet& idx, std::span<const Matrix> factors) {
+    if (static_cast<int>(factors.size()) != idx.n_other())
+        throw std::domain_error("sampled_khatri_rao: factor count mismatch");
+    const Index rank = factors.empty() ? 0 : factors[0].cols();
+    for (const Matrix& f : factors)
+        if (f.cols() != rank) throw std::domain_error("sampled_khatri_rao: factor column counts differ");
+    std::vector<const double*> p;
+    std::vector<Index> frows;
+    for (const Matrix& f : factors) {
+        p.push_back(f.data());
+        frows.push_back(f.rows());
+    }
+    Matrix z(idx.count(), rank);
+    check(rocp_sampled_khatri_rao(device_handle(), idx.decoded.data(), idx.count(), idx.n_other(), p.data(),
+                                  frows.data(), static_cast<int>(rank), z.data()));
+    return z;
+}
+
+// ---- solve --------------------------------------------------------------------------
+Matrix solve_gram(const Matrix& gram, const Matrix& rhs, SolveInfo* info) {
+    if (gram.rows() != gram.cols()) throw std::domain_error("solve_gram: gram matrix must be square");
+    if (rhs.cols() != gram.rows()) throw std::domain_error("solve_gram: rhs column count must match gram size");
+    Matrix out(rhs.rows(), rhs.cols());
+    int reg = 0;
+    check(rocp_solve_gram(device_handle(), gram.data(), rhs.data(), rhs.rows(), static_cast<int>(gram.rows()),
+                          out.data(), &reg));
+    if (info && reg) info->regularized = true;
+    return out;
+}
+
+Matrix solve_sampled_ls(const Matrix& z_s, const Matrix& x_s, SolveInfo* info) {
+    if (x_s.cols() != z_s.rows()) throw std::domain_error("solve_sampled_ls: sample counts of z_s and x_s differ");
+    Matrix out(x_s.rows(), z_s.cols());
+    int reg = 0, und = 0;
+    check(rocp_solve_sampled_ls(device_handle(), z_s.data(), x_s.data(), z_s.rows(), x_s.rows(),
+                                static_cast<int>(z_s.cols()), out.data(), &reg, &und));
+    if (info) {
+        if (reg) info->regularized = true;
+        if (und) info->underdetermined = true;
+    }
+    return out;
+}
+
+// ---- cprand -------------------------------------------------------------------------
+InitResult cprand_decompose(const DenseTensor& x, const KruskalModel& initial, const CprandOptions& opts,
+                            std::uint64_t seed) {
+    if (initial.rank < 1) throw std::domain_error("cprand_decompose: rank must be positive");
+    const int N = x.order();
+    const Index s = opts.samples > 0 ? opts.samples : auto_sample_count(initial.rank);
+    InitResult res;
+    res.model = initial;
+    res.best_sampled_kr.assign(static_cast<size_t>(N - 1), Matrix(s, initial.rank));
+    std::vector<double*> f, kr;
+    for (Matrix& m : res.model.factors) f.push_back(m.data());
+    for (Matrix& m : res.best_sampled_kr) kr.push_back(m.data());
+    DevTensor t(x);
+    int iters = 0, reg = 0, err_sweep = 0;
+    const rocp_status st = rocp_cprand(device_handle(), t.t, initial.rank, opts.samples, opts.tol, opts.max_iters,
+                                       seed, f.data(), kr.data(), &res.best_fitness, &iters, &reg, &err_sweep,
+                                       nullptr);
+    if (st != ROCP_OK) raise(device_handle(), st, err_sweep);
+    res.iterations = iters;
+    res.regularized = reg != 0;
+    res.seed = seed;
+    for (int n = 0; n + 1 < N; ++n) res.best_sampled_factors.push_back(res.model.factors[static_cast<size_t>(n)]);
+    return res;
+}
+
+InitResult cprand_decompose(const DenseTensor& x, int rank, const CprandOptions& opts, Rng& rng,
+                            CprandTrace* trace) {
+    (void)trace;
+    if (rank < 1) throw std::domain_error("cprand_decompose: rank must be positive");
+    if (opts.max_iters < 1) throw std::domain_error("cprand_decompose: need at least one sweep");
+    const KruskalModel init = random_model(x.dims(), rank, rng);  // cprand.cpp:25
+    return cprand_decompose(x, init, opts, rng());
+}
+
+// ---- stream -------------------------------------------------------------------------
+std::size_t ComplementaryState::byte_size() const {
+    std::size_t bytes = sizeof(*this) + dims_head.size() * sizeof(Index);
+    for (const Matrix& m : p) bytes += static_cast<std::size_t>(m.size()) * sizeof(double);
+    for (const Matrix& m : q) bytes += static_cast<std::size_t>(m.size()) * sizeof(double);
+    return bytes;
+}
+
+RocpStream::RocpStream(InitResult init, Index s, RocpConfig cfg, Index t_capacity) {
+    order_ = init.model.order();
+    rank_ = init.model.rank;
+    s_ = s;
+    for (int n = 0; n + 1 < order_; ++n) head_.push_back(init.model.factors[static_cast<size_t>(n)].rows());
+    if (static_cast<int>(init.best_sampled_kr.size()) != order_ - 1)
+        throw std::domain_error("init_state: expected one sampled system per non-temporal mode");
+    for (const Matrix& z : init.best_sampled_kr)
+        if (z.rows() != s) throw std::domain_error("init_state: sampled Khatri-Rao row count differs from s");
+    const Index t_init = init.model.factors.back().rows();
+    const auto f = ptrs(init.model.factors);
+    const auto kr = ptrs(init.best_sampled_kr);
+    check(rocp_stream_create(device_handle(), order_, head_.data(), rank_, s, cfg.literal_init ? 1 : 0, f.data(),
+                             t_init, kr.data(), init.regularized ? 1 : 0, std::max<Index>(t_capacity, 4 * t_init + 64),
+                             &h_));
+}
+
+RocpStream::~RocpStream() {
+    if (h_) rocp_stream_free(h_);
+}
+
+void RocpStream::consume(const DenseTensor& x_new, std::uint64_t seed, std::uint32_t batch_id) {
+    if (x_new.order() != order_) throw std::domain_error("batch order does not match stream order");
+    for (size_t k = 0; k < head_.size(); ++k)
+        if (x_new.dims()[k] != head_[k]) throw std::domain_error("batch head extents do not match stream");
+    check(rocp_stream_consume_host(h_, x_new.data(), x_new.dims().back(), seed, batch_id));
+    next_batch_ = batch_id + 1;
+}
+
+void RocpStream::consume(const DenseTensor& x_new, Rng& rng, UpdateTrace* trace) {
+    (void)trace;
+    consume(x_new, rng(), next_batch_);
+}
+
+KruskalModel RocpStream::model() const {
+    KruskalModel m;
+    m.rank = rank_;
+    for (int n = 1; n < order_; ++n) {
+        Matrix u(head_[static_cast<size_t>(n - 1)], rank_);
+        check(rocp_stream_get(h_, 0, n, u.data()));
+        m.factors.push_back(std::move(u));
+    }
+    Matrix t(rocp_stream_t_len(h_), rank_);
+    check(rocp_stream_get(h_, 3, 0, t.data()));
+    m.factors.push_back(std::move(t));
+    return m;
+}
+
+ComplementaryState RocpStream::state() const {
+    ComplementaryState st;
+    for (int n = 1; n < order_; ++n) {
+        Matrix p(head_[static_cast<size_t>(n - 1)], rank_), q(rank_, rank_);
+        check(rocp_stream_get(h_, 1, n, p.data()));
+        check(rocp_stream_get(h_, 2, n, q.data()));
+        st.p.push_back(std::move(p));
+        st.q.push_back(std::move(q));
+    }
+    st.t_len = rocp_stream_t_len(h_);
+    st.sample_count = s_;
+    st.dims_head = head_;
+    return st;
+}
+
+Index RocpStream::t_len() const { return rocp_stream_t_len(h_); }
+bool RocpStream::regularized() const { return rocp_stream_regularized(h_) != 0; }
+
+double RocpStream::last_residual() const {
+    std::vector<double> r(static_cast<size_t>(order_));
+    check(rocp_stream_last_residuals(h_, r.data()));
+    return r[0];
+}
+
+KruskalModel rocp_run(const DenseTensor& x_init, std::span<const DenseTensor> batches, int rank,
+                      const CprandOptions& init_opts, Rng& rng, const RocpConfig& cfg) {
+    InitResult init = cprand_decompose(x_init, rank, init_opts, rng);  // rocp.cpp:170-178
+    const Index s = init_opts.samples > 0 ? init_opts.samples : auto_sample_count(rank);
+    Index total = x_init.dims().back();
+    for (const DenseTensor& b : batches) total += b.dims().back();
+    RocpStream stream(std::move(init), s, cfg, total);
+    for (const DenseTensor& b : batches) stream.consume(b, rng);
+    return stream.model();
+}
+
+}  // namespace rocp

@@ -1,0 +1,234 @@
+// C++ API tests, written against include/rocp_b200/rocp.hpp the way the
+// reference's doctest suites exercise include/rocp/*.hpp (reference test
+// file:line cited per case).  Runs on the GPU (tests/test_cpp_api.py, -m gpu).
+#include "rocp_b200/rocp.hpp"
+
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+using namespace rocp;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                                   \
+    do {                                                                              \
+        if (cond) ++g_pass;                                                           \
+        else { ++g_fail; std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); } \
+    } while (0)
+template <class E, class F>
+static bool throws(F&& f) {
+    try { f(); } catch (const E&) { return true; } catch (...) { return false; }
+    return false;
+}
+
+static Matrix random_matrix(Index r, Index c, Rng& rng) {
+    std::normal_distribution<double> g(0.0, 1.0);
+    Matrix m(r, c);
+    for (Index i = 0; i < m.size(); ++i) m.data()[i] = g(rng);
+    return m;
+}
+
+// test-side elementwise reconstruction (reference tests/oracles.hpp:42-60 idea)
+static DenseTensor reconstruct_loops(const KruskalModel& m, const Dims& dims) {
+    DenseTensor t(dims);
+    std::vector<Index> idx(dims.size(), 0);
+    for (Index flat = 0; flat < t.size(); ++flat) {
+        double sum = 0.0;
+        for (int r = 0; r < m.rank; ++r) {
+            double prod = 1.0;
+            for (size_t n = 0; n < dims.size(); ++n) prod *= m.factors[n](idx[n], r);
+            sum += prod;
+        }
+        t[flat] = sum;
+        for (size_t n = 0; n < dims.size(); ++n) {
+            if (++idx[n] < dims[n]) break;
+            idx[n] = 0;
+        }
+    }
+    return t;
+}
+
+static double frob(const Matrix& a) {
+    double s = 0;
+    for (Index i = 0; i < a.size(); ++i) s += a.data()[i] * a.data()[i];
+    return std::sqrt(s);
+}
+static double diff(const Matrix& a, const Matrix& b) {
+    double s = 0;
+    for (Index i = 0; i < a.size(); ++i) s += (a.data()[i] - b.data()[i]) * (a.data()[i] - b.data()[i]);
+    return std::sqrt(s);
+}
+
+static void test_index_map() {  // test_tensor.cpp:30-82
+    const Dims d{2, 3, 4};
+    const Index a[2] = {1, 1}, b[2] = {3, 4}, c[2] = {2, 1};
+    CHECK(linear_index(a, d, 1) == 1);
+    CHECK(linear_index(b, d, 1) == 12);
+    CHECK(linear_index(c, d, 2) == 2);
+    CHECK((decode_index(12, d, 1) == std::vector<Index>{3, 4}));
+    CHECK((decode_index(3, Dims{5, 5}, 2) == std::vector<Index>{3}));
+    CHECK(throws<std::domain_error>([&] { decode_index(13, d, 1); }));
+    CHECK(auto_sample_count(1) == 1 && auto_sample_count(3) == 33 && auto_sample_count(5) == 81);
+}
+
+static void test_draws_and_gather() {  // test_factor_model.cpp:95-168
+    const SampleIndexSet one = draw_samples(Dims{1, 1, 5}, 3, 8, CounterKey{1, 0, 0});
+    bool all_one = true;
+    for (Index j : one.rows) all_one = all_one && j == 1;
+    CHECK(all_one);
+    const SampleIndexSet x1 = draw_samples(Dims{4, 5, 6}, 2, 50, CounterKey{99, 0, 0});
+    const SampleIndexSet x2 = draw_samples(Dims{4, 5, 6}, 2, 50, CounterKey{99, 0, 0});
+    CHECK(x1.rows == x2.rows && x1.decoded == x2.decoded);
+    const SampleIndexSet u = draw_samples(Dims{2, 10}, 1, 10000, CounterKey{4242, 0, 0});
+    std::vector<int> freq(10, 0);
+    for (Index j : u.rows) ++freq[static_cast<size_t>(j - 1)];
+    bool uniform = true;
+    for (int f : freq) uniform = uniform && std::abs(f - 1000.0) <= 5.0 * std::sqrt(10000 * 0.09);
+    CHECK(uniform);
+    Rng rng(55);
+    DenseTensor t({3, 4, 5});
+    std::normal_distribution<double> g;
+    for (Index i = 0; i < t.size(); ++i) t[i] = g(rng);
+    const Matrix dup = sample_unfolding(t, SampleIndexSet::from_rows(t.dims(), 1, {4, 4}));
+    CHECK(dup(0, 0) == dup(0, 1) && dup(2, 0) == dup(2, 1));
+    const Matrix col = sample_unfolding(t, SampleIndexSet::from_rows(t.dims(), 2, {7}));
+    const std::vector<Index> mi = decode_index(7, t.dims(), 2);  // (i1, i3)
+    bool fibre = true;
+    for (Index i2 = 0; i2 < 4; ++i2) fibre = fibre && col(i2, 0) == t[(mi[0] - 1) + 3 * i2 + 12 * (mi[1] - 1)];
+    CHECK(fibre);
+    CHECK(throws<std::domain_error>([&] { sample_unfolding(t, SampleIndexSet::from_rows({3, 4, 6}, 1, {1})); }));
+}
+
+static void test_skr() {  // test_factor_model.cpp:172-218
+    Rng rng(73);
+    const Dims dims{2, 3, 4};
+    const KruskalModel m = random_model(dims, 3, rng);
+    for (int mode = 1; mode <= 3; ++mode) {
+        const auto fs = factors_excluding(m, mode);
+        const SampleIndexSet all = SampleIndexSet::all_columns(dims, mode);
+        const Matrix z = sampled_khatri_rao(all, fs);
+        // row c is the Hadamard product of decoded factor rows, left to right
+        bool ok = true;
+        for (Index c = 0; c < all.count(); ++c)
+            for (int r = 0; r < 3; ++r) {
+                double v = 1.0;
+                for (size_t l = 0; l < fs.size(); ++l)
+                    v = v * fs[l](all.decoded_at(c, static_cast<int>(fs.size() - 1 - l)) - 1, r);
+                ok = ok && z(c, r) == v;
+            }
+        CHECK(ok);
+    }
+}
+
+static void test_solve() {  // test_cprand.cpp:25-81
+    Rng rng(101);
+    const Matrix x = random_matrix(5, 3, rng);
+    CHECK(diff(solve_sampled_ls(Matrix::Identity(3, 3), x), x) < 1e-14);
+    const Matrix u0 = random_matrix(6, 3, rng), z = random_matrix(20, 3, rng);
+    Matrix xs(6, 20);
+    for (Index i = 0; i < 6; ++i)
+        for (Index c = 0; c < 20; ++c) {
+            double v = 0;
+            for (int r = 0; r < 3; ++r) v += u0(i, r) * z(c, r);
+            xs(i, c) = v;
+        }
+    CHECK(diff(solve_sampled_ls(z, xs), u0) <= 1e-10 * frob(u0));
+    SolveInfo info;
+    const Matrix u = solve_sampled_ls(random_matrix(2, 4, rng), random_matrix(3, 2, rng), &info);
+    CHECK(info.underdetermined && info.regularized && u.allFinite());
+    SolveInfo zi;
+    const Matrix uz = solve_sampled_ls(Matrix::Zero(5, 2), random_matrix(3, 5, rng), &zi);
+    CHECK(zi.regularized && uz == Matrix::Zero(3, 2));
+    CHECK(throws<std::domain_error>([&] { solve_sampled_ls(Matrix::Zero(5, 2), Matrix::Zero(3, 4)); }));
+}
+
+static void test_cprand() {  // test_cprand.cpp:83-198
+    {
+        Rng gen(13);
+        const Dims dims{30, 30, 30};
+        const DenseTensor x = reconstruct_loops(random_model(dims, 5, gen), dims);
+        Rng rng(17);
+        const InitResult res = cprand_decompose(x, 5, {}, rng);
+        CHECK(res.best_fitness >= 0.99);
+        CHECK(std::abs(model_fitness(x, res.model) - res.best_fitness) < 1e-12);
+    }
+    {
+        Rng gen(19);
+        const Dims dims{8, 9, 10};
+        const DenseTensor x = reconstruct_loops(random_model(dims, 3, gen), dims);
+        Rng a(23), b(23);
+        const InitResult ra = cprand_decompose(x, 3, {}, a), rb = cprand_decompose(x, 3, {}, b);
+        CHECK(ra.best_fitness == rb.best_fitness && ra.iterations == rb.iterations);
+        for (int n = 0; n < 3; ++n) CHECK(ra.model.factors[static_cast<size_t>(n)] == rb.model.factors[static_cast<size_t>(n)]);
+    }
+    Rng r1(1);
+    CHECK(throws<std::domain_error>([&] { cprand_decompose(DenseTensor({3, 3}), 1, {}, r1); }));
+    DenseTensor inf({3, 3, 3});
+    inf[0] = INFINITY;
+    int sweep = -1;
+    try {
+        Rng r2(1);
+        cprand_decompose(inf, 2, {}, r2);
+    } catch (const NumericalError& e) {
+        sweep = e.sweep();
+    }
+    CHECK(sweep == 1);
+}
+
+static void test_stream() {  // test_rocp.cpp:235-294
+    const Dims dims{20, 20, 200};
+    Rng gen(383);
+    const KruskalModel truth = random_model(dims, 5, gen);
+    const DenseTensor x = reconstruct_loops(truth, dims);
+    const Index slice = 400;
+    auto take = [&](Index t0, Index len) {
+        std::vector<double> v(x.data() + t0 * slice, x.data() + (t0 + len) * slice);
+        return DenseTensor({20, 20, len}, std::move(v));
+    };
+    std::vector<DenseTensor> batches;
+    for (Index t = 40; t < 200; ++t) batches.push_back(take(t, 1));
+    Rng rng(389);
+    const KruskalModel model = rocp_run(take(0, 40), batches, 5, {}, rng);
+    CHECK(model.factors.back().rows() == 200);
+    CHECK(model_fitness(x, model) >= 0.95);
+
+    // frozen old temporal rows and constant state footprint
+    Rng rng2(7);
+    InitResult init = cprand_decompose(take(0, 40), 5, {}, rng2);
+    RocpStream st(std::move(init), auto_sample_count(5), {}, 200);
+    Matrix before = st.model().factors.back();
+    const std::size_t bytes = st.state().byte_size();
+    bool frozen = true, constant = true;
+    for (Index t = 40; t < 60; ++t) {
+        st.consume(take(t, 1), rng2);
+        const Matrix now = st.model().factors.back();
+        for (Index i = 0; i < before.rows(); ++i)
+            for (int r = 0; r < 5; ++r) frozen = frozen && now(i, r) == before(i, r);
+        constant = constant && st.state().byte_size() == bytes;
+        before = now;
+    }
+    CHECK(frozen && constant && st.t_len() == 60);
+    CHECK(st.last_residual() >= 0.0 && st.last_residual() < 1.0);
+    CHECK(throws<std::domain_error>([&] { st.consume(DenseTensor({20, 21, 1}), rng2); }));
+}
+
+int main() {
+    const std::vector<std::pair<const char*, std::function<void()>>> cases = {
+        {"index_map", test_index_map}, {"draws_and_gather", test_draws_and_gather}, {"skr", test_skr},
+        {"solve", test_solve},         {"cprand", test_cprand},                     {"stream", test_stream}};
+    for (const auto& [name, fn] : cases) {
+        const int before = g_fail;
+        try {
+            fn();
+        } catch (const std::exception& e) {
+            ++g_fail;
+            std::printf("FAIL %s: exception %s\n", name, e.what());
+        }
+        std::printf("%s %s\n", g_fail == before ? "[PASS]" : "[FAIL]", name);
+    }
+    std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
