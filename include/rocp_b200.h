@@ -28,6 +28,7 @@
 #ifndef ROCP_B200_H
 #define ROCP_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -63,6 +64,11 @@ rocp_status rocp_timer_record(rocp_dev* dev, int slot);
 rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms);
 /* The handle's cudaStream_t (for callers that interoperate). */
 void* rocp_cuda_stream(rocp_dev* dev);
+/* Page-locked, CUDA-registered host buffer backed by 2 MB (transparent huge)
+ * pages, for host-slab streams (rocp_stream_consume_range_host).  NULL on
+ * failure.  Free with the same size. */
+void* rocp_host_alloc(size_t bytes);
+void rocp_host_free(void* p, size_t bytes);
 /* Size of the NCCL unique id blob (for the host bootstrap), 0 if no NCCL. */
 int rocp_nccl_id_size(void);
 rocp_status rocp_nccl_get_unique_id(void* out);
@@ -143,10 +149,18 @@ void rocp_stream_free(rocp_stream* st);
  * Draws keyed by (seed, batch_id, iteration 0). */
 rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint64_t seed,
                                 uint32_t batch_id);
-/* Same for a host slab (head dims x batch, first index fastest): copies it
- * into a device staging buffer first (the reference-facing call). */
+/* Same for a host slab (head dims x batch, first index fastest): the
+ * reference-facing call.  Only the sampled fibres cross PCIe (see
+ * rocp_stream_consume_range_host). */
 rocp_status rocp_stream_consume_host(rocp_stream* st, const double* x_new, int64_t batch,
                                      uint64_t seed, uint32_t batch_id);
+/* Same for nb consecutive HOST slabs (head dims x nb*batch, first index
+ * fastest): the device draws the window's indices, `threads` host threads
+ * (0 = all) gather only the sampled fibres into pinned staging, and sub-window
+ * copies overlap the device chain.  rocp_stream_consume_host uses this path
+ * with nb = 1. */
+rocp_status rocp_stream_consume_range_host(rocp_stream* st, const double* x, int64_t batch, int64_t nb,
+                                           uint64_t seed, uint32_t first_batch_id, int threads);
 /* Consume nb consecutive slabs of `batch` slices of a device tensor starting
  * at slice t0 (batch ids first_batch_id, first_batch_id+1, ...).  One call,
  * captured once into a CUDA graph per shape. */

@@ -78,6 +78,8 @@ SIGNATURES = [
     ("rocp_stream_consume_host", C.c_int, [_vp, _f64p, C.c_int64, C.c_uint64, C.c_uint32]),
     ("rocp_stream_consume_range", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
                                             C.c_uint32]),
+    ("rocp_stream_consume_range_host", C.c_int, [_vp, _f64p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32,
+                                                 C.c_int]),
     ("rocp_stream_update_last_mode_with", C.c_int, [_vp, _vp, _i64p, C.c_int64, _f64p, _f64p,
                                                     C.POINTER(C.c_int)]),
     ("rocp_stream_append_temporal", C.c_int, [_vp, _f64p, C.c_int64]),
@@ -94,6 +96,8 @@ SIGNATURES = [
     ("rocp_timer_record", C.c_int, [_vp, C.c_int]),
     ("rocp_timer_elapsed_ms", C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     ("rocp_cuda_stream", _vp, [_vp]),
+    ("rocp_host_alloc", _vp, [C.c_size_t]),
+    ("rocp_host_free", None, [_vp, C.c_size_t]),
     ("rocp_stream_set_residual_tracking", C.c_int, [_vp, C.c_int]),
     ("rocp_stream_time_gather", C.c_int, [_vp, C.c_int]),
     ("rocp_stream_gather_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
@@ -252,6 +256,28 @@ class Device:
         ms = C.c_float(0)
         self.check(lib().rocp_timer_elapsed_ms(self.h, a, b, C.byref(ms)))
         return float(ms.value)
+
+
+class HostBuffer:
+    """Huge-page-backed, page-locked host buffer (rocp_host_alloc) viewed as a
+    float64 numpy array; for host-slab streams."""
+
+    def __init__(self, n_doubles):
+        self.nbytes = int(n_doubles) * 8
+        p = lib().rocp_host_alloc(self.nbytes)
+        if not p:
+            raise RocpError(E_OOM, "rocp_host_alloc failed")
+        self.ptr = p
+        self.array = np.ctypeslib.as_array((C.c_double * int(n_doubles)).from_address(p))
+
+    def free(self):
+        if getattr(self, "ptr", None):
+            self.array = None
+            lib().rocp_host_free(self.ptr, self.nbytes)
+            self.ptr = None
+
+    def __del__(self):
+        self.free()
 
 
 class DeviceTensor:
@@ -497,6 +523,14 @@ class RocpStream:
     def consume_range(self, x, t0, batch, nb, seed, first_batch_id):
         self.dev.check(lib().rocp_stream_consume_range(self.h, x.h, t0, batch, nb, seed,
                                                        first_batch_id))
+
+    def consume_range_host(self, x, batch, nb, seed, first_batch_id, threads=0):
+        """nb consecutive host slabs of `batch` slices (flat, first index fastest)."""
+        x = np.ascontiguousarray(x, dtype=np.float64).ravel(order="K")
+        if x.size != int(np.prod(self.head)) * batch * nb:
+            raise DomainError(E_DOMAIN, "host range size does not match head dims x batch x nb")
+        self.dev.check(lib().rocp_stream_consume_range_host(self.h, _p(x), batch, nb, seed, first_batch_id,
+                                                            threads))
 
     def update_last_mode_with(self, x_new, rows):
         r = _i64(rows)

@@ -14,14 +14,23 @@
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
+#include <mutex>
+#include <functional>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -461,6 +470,93 @@ void check_rank(int R) {
 // ===========================================================================
 // Stream state (RocpStream, rocp.hpp:85-107 + ComplementaryState :15-24).
 //
+// Host buffers for host-slab streams: 2 MB-aligned anonymous mapping with
+// transparent huge pages requested (the host gather touches one page per
+// strided element; 2 MB pages keep those walks in the TLB), page-locked and
+// registered with CUDA.
+constexpr size_t kHugePage = size_t(2) << 20;
+
+void* host_alloc_huge(size_t bytes) {
+    const size_t len = (bytes + kHugePage - 1) / kHugePage * kHugePage;
+    void* p = mmap(nullptr, len + kHugePage, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return nullptr;
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + kHugePage - 1) & ~(uintptr_t(kHugePage) - 1);
+    const size_t head = a - reinterpret_cast<uintptr_t>(p);
+    if (head) munmap(p, head);
+    if (kHugePage - head) munmap(reinterpret_cast<void*>(a + len), kHugePage - head);
+    madvise(reinterpret_cast<void*>(a), len, MADV_HUGEPAGE);
+    if (cudaHostRegister(reinterpret_cast<void*>(a), len, cudaHostRegisterDefault) != cudaSuccess) {
+        munmap(reinterpret_cast<void*>(a), len);
+        return nullptr;
+    }
+    return reinterpret_cast<void*>(a);
+}
+
+void host_free_huge(void* p, size_t bytes) {
+    if (!p) return;
+    cudaHostUnregister(p);
+    munmap(p, (bytes + kHugePage - 1) / kHugePage * kHugePage);
+}
+
+// Persistent host worker threads for the host-slab gather (one pool per stream).
+class HostPool {
+public:
+    explicit HostPool(int n) {
+        for (int t = 1; t < n; ++t) th_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    int size() const { return int(th_.size()) + 1; }
+    // Runs fn() on `n` threads (the caller included) and waits for all of them.
+    void run(int n, const std::function<void()>& fn) {
+        n = std::max(1, std::min(n, size()));
+        {
+            std::lock_guard<std::mutex> g(m_);
+            fn_ = &fn;
+            want_ = n - 1;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn();
+        std::unique_lock<std::mutex> g(m_);
+        done_.wait(g, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void()>* f = nullptr;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || (gen_ != seen && want_ > 0); });
+                if (stop_) return;
+                seen = gen_;
+                --want_;
+                f = fn_;
+            }
+            (*f)();
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void()>* fn_ = nullptr;
+    uint64_t gen_ = 0;
+    int want_ = 0, pending_ = 0;
+    bool stop_ = false;
+};
+
 // A "window" holds the sample indices and gathered fibres of nb consecutive
 // batches: all N*nb draws are one launch, all N*nb gathers are one launch
 // (indices never depend on factors), then the factor-dependent chain runs
@@ -475,12 +571,24 @@ struct Window {
     DBuf<int64_t> xoff_dev;
     DBuf<double> zT, rcols, rhist;  // temporal Z per batch, residual column partials, per-batch residuals
     JobList jobs;
+    // host-slab path: pinned staging of the gathered X_s and of the fibre base offsets
+    double* hX = nullptr;
+    size_t hX_n = 0;
+    int64_t* hbase = nullptr;
+    size_t hbase_n = 0;
+    ~Window() {
+        host_free_huge(hX, hX_n * sizeof(double));
+        if (hbase) cudaFreeHost(hbase);
+    }
     // key of the uploaded job list
     const double* key_x = nullptr;
     int64_t key_t0 = -1, key_B = -1, key_nb = -1, key_slice = -1;
     const int64_t* key_rows0 = nullptr;
     const int64_t* key_rowsm = nullptr;
     int key_only = -2;
+    bool key_host = false;
+    const double* key_zc = nullptr;
+    std::vector<int64_t> zc_tile;  // host path: first zero-copy gather tile of each batch
 };
 
 struct rocp_stream {
@@ -506,6 +614,8 @@ struct rocp_stream {
     DBuf<uint64_t> seed_dev;      // draw seed (device, so graphs need no re-capture)
     DBuf<uint32_t> batch_dev;     // first batch id of the window (device)
     int resid_level = 1;          // 0 none, 1 temporal stage (default), 2 every stage
+    int host_threads = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
+    std::unique_ptr<HostPool> pool;  // host-slab gather workers (created on first use)
     // checkpoint copies (device)
     std::vector<DBuf<double>> ckU, ckP, ckQ;
     int64_t ck_t_len = -1;
@@ -592,18 +702,27 @@ double* win_x(rocp_stream* st, int64_t b, int stage) { return st->win.X.p + st->
 // ids come from st->batch_dev + b, the seed from st->seed_dev, so the lists
 // are reused across calls.  rows0/rowsm: explicit index sets (replay seams);
 // only_stage >= 0 restricts to one stage.
+// host_gather: the fibres come from host slabs (consume_range_host); then the
+// gather jobs are only those of the contiguous (mode-1) stages, reading the
+// caller's registered host range in place through zc_src (zero-copy), or none.
 void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice, int64_t B, int64_t nb,
-                    const int64_t* rows0, const int64_t* rowsm, int only_stage) {
+                    const int64_t* rows0, const int64_t* rowsm, int only_stage, bool host_gather = false,
+                    const double* zc_src = nullptr) {
     ensure_window(st, nb, B);
     Window& W = st->win;
     if (W.key_x == x && W.key_t0 == t0 && W.key_B == B && W.key_nb == nb && W.key_slice == slice &&
-        W.key_rows0 == rows0 && W.key_rowsm == rowsm && W.key_only == only_stage)
+        W.key_rows0 == rows0 && W.key_rowsm == rowsm && W.key_only == only_stage && W.key_host == host_gather &&
+        W.key_zc == zc_src)
         return;
     const std::vector<int64_t> d = slab_dims(st, B);
     std::vector<DrawJob> dj;
     std::vector<GatherJob> gj;
+    const std::vector<int64_t> strides = strides_of(d);
+    W.zc_tile.assign(size_t(nb + 1), 0);
+    int64_t ntile = 0;
     for (int64_t b = 0; b < nb; ++b) {
         const double* xb = x + (t0 + b * B) * slice;
+        W.zc_tile[size_t(b)] = ntile;
         for (int stage = 0; stage < st->N; ++stage) {
             if (only_stage >= 0 && stage != only_stage) continue;
             const int mode = stage == 0 ? st->N : stage;
@@ -612,9 +731,16 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
             j.seed_ptr = st->seed_dev.p;
             j.batch_ptr = st->batch_dev.p;
             dj.push_back(j);
-            gj.push_back(make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage), 1));
+            if (!host_gather) {
+                gj.push_back(make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage), 1));
+            } else if (zc_src && strides[size_t(mode - 1)] == 1) {
+                gj.push_back(make_gather(zc_src + (t0 + b * B) * slice, d, mode, st->s, win_base(st, b, stage),
+                                         win_x(st, b, stage), 1));
+                ntile += (int64_t(d[size_t(mode - 1)]) * st->s + kGatherTile - 1) / kGatherTile;
+            }
         }
     }
+    W.zc_tile[size_t(nb)] = ntile;
     upload_jobs(st->dev, W.jobs, dj, gj);
     W.key_x = x;
     W.key_t0 = t0;
@@ -624,6 +750,8 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
     W.key_rows0 = rows0;
     W.key_rowsm = rowsm;
     W.key_only = only_stage;
+    W.key_host = host_gather;
+    W.key_zc = zc_src;
 }
 
 // Draw + gather of the prepared window (seed / first batch id set on device).
@@ -738,7 +866,7 @@ void launch_chain_k(rocp_stream* st, const ChainParams& p) {
 
 // The whole factor-dependent chain of the prepared window as ONE cooperative
 // persistent kernel (kernels.cuh K6).
-void launch_chain(rocp_stream* st, int64_t nb, int64_t B) {
+void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
     ChainParams p{};
     p.N = st->N;
     p.R = st->R;
@@ -755,10 +883,11 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B) {
     }
     p.temporal = st->temporal.p;
     p.t_len0 = st->t_len;
-    p.idx_base = st->win.idx.p;
+    const int64_t RPw = ((st->R + kCRB - 1) / kCRB) * kCRB;
+    p.idx_base = st->win.idx.p + b0 * st->N * st->s * (st->N - 1);
     p.X_base = st->win.X.p;
-    p.xoff = st->win.xoff_dev.p;
-    p.zbuf = st->win.zT.p;
+    p.xoff = st->win.xoff_dev.p + b0 * st->N;
+    p.zbuf = st->win.zT.p + b0 * st->s * RPw;
     p.gch = st->zmodes.p;
     p.gpart = st->gpart.p;
     p.cpart = st->dev->contract_partial.p;
@@ -788,8 +917,8 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B) {
         w.temporal = st->temporal.p;
         w.t_len0 = st->t_len;
         w.X_base = st->win.X.p;
-        w.xoff = st->win.xoff_dev.p;
-        w.zT = st->win.zT.p;
+        w.xoff = st->win.xoff_dev.p + b0 * st->N;
+        w.zT = st->win.zT.p + b0 * st->s * RPw;
         w.cols = st->win.rcols.p;
         w.out = st->win.rhist.p;
         w.last_out = st->resid.p;
@@ -814,6 +943,156 @@ void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uin
     if (st->resid_level <= 1) launch_chain(st, 1, B);
     else enqueue_chain(st, 1, B);
     st->t_len += B;  // rocp.cpp:159
+}
+
+// ---- host-slab path ----------------------------------------------------------
+// For inputs that live in host memory (the reference-facing call), only the
+// sampled fibres cross PCIe: the GPU draws the window's indices, host threads
+// gather the fibres from the caller's slabs into pinned staging in the
+// row-tiled X_s layout, and sub-window H2D copies overlap the persistent chain.
+void host_gather_range(rocp_stream* st, const double* hx, int64_t slice, int64_t B, int64_t b0, int64_t b1,
+                       int threads, bool skip_contiguous) {
+    Window& W = st->win;
+    const int N = st->N;
+    const int64_t S = st->s;
+    const std::vector<int64_t> d = slab_dims(st, B);
+    const std::vector<int64_t> strides = strides_of(d);
+    // Tasks of kFib fibres, claimed dynamically; each fibre is walked on its own
+    // (strided rows on 2 MB pages stay TLB-resident, and the out-of-order core
+    // keeps a fibre's independent loads in flight -- tools/host_gather_bench.cpp:
+    // this beats row-interleaved walks and software prefetch on the GPU box).
+    constexpr int64_t kFib = 16;
+    struct Task {
+        int32_t b, stage;
+        int64_t c0, c1;
+    };
+    std::vector<Task> tasks;
+    for (int pass = 0; pass < 2; ++pass)  // strided stages first: they are the heavy ones
+        for (int64_t b = b0; b < b1; ++b)
+            for (int stage = 0; stage < N; ++stage) {
+                const int mode = stage == 0 ? N : stage;
+                if ((strides[size_t(mode - 1)] == 1) != (pass == 1)) continue;
+                if (pass == 1 && skip_contiguous) continue;  // read by the GPU in place
+                for (int64_t c0 = 0; c0 < S; c0 += kFib)
+                    tasks.push_back(Task{int32_t(b), stage, c0, std::min(S, c0 + kFib)});
+            }
+    std::atomic<size_t> next{0};
+    const std::function<void()> work = [&]() {
+        for (size_t k = next.fetch_add(1, std::memory_order_relaxed); k < tasks.size();
+             k = next.fetch_add(1, std::memory_order_relaxed)) {
+            const Task& tk = tasks[k];
+            const int mode = tk.stage == 0 ? N : tk.stage;
+            const int64_t I = d[size_t(mode - 1)], ms = strides[size_t(mode - 1)];
+            const double* src_b = hx + int64_t(tk.b) * B * slice;
+            const int64_t* bases = W.hbase + (int64_t(tk.b) * N + tk.stage) * S;
+            double* dst = W.hX + W.xoff[size_t(int64_t(tk.b) * N + tk.stage)];
+            for (int64_t c = tk.c0; c < tk.c1; ++c) {
+                const double* f = src_b + bases[c];
+                if (ms == 1) {
+                    for (int64_t i0 = 0; i0 < I; i0 += 32)
+                        std::memcpy(dst + xs_offset(i0, c, S), f + i0, size_t(std::min<int64_t>(32, I - i0)) * 8);
+                } else {
+                    for (int64_t i0 = 0; i0 < I; i0 += 32) {
+                        double* o = dst + xs_offset(i0, c, S);
+                        const int64_t n = std::min<int64_t>(32, I - i0);
+                        const double* fi = f + i0 * ms;
+                        for (int64_t i = 0; i < n; ++i) o[i] = fi[i * ms];
+                    }
+                }
+            }
+        }
+    };
+    st->pool->run(std::min<int>(threads, int(tasks.size())), work);
+}
+
+void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb, uint64_t seed,
+                        uint32_t first_batch_id, int threads, int64_t sub) {
+    rocp_dev* dev = st->dev;
+    check_capacity(st, B * nb);
+    const int64_t slice = prod(st->head);
+    // A CUDA-registered range (e.g. rocp_host_alloc) lets the GPU read the
+    // contiguous mode-1 fibres in place over PCIe while host threads gather the
+    // strided stages; otherwise host threads gather every stage.
+    const double* zc = nullptr;
+    {
+        const double* last = hx + (B * nb * slice - 1);
+        cudaPointerAttributes a0{}, a1{};
+        if (cudaPointerGetAttributes(&a0, hx) == cudaSuccess && cudaPointerGetAttributes(&a1, last) == cudaSuccess &&
+            a0.type == cudaMemoryTypeHost && a1.type == cudaMemoryTypeHost && a0.devicePointer &&
+            a1.devicePointer &&
+            static_cast<const double*>(a1.devicePointer) - static_cast<const double*>(a0.devicePointer) ==
+                last - hx)
+            zc = static_cast<const double*>(a0.devicePointer);
+        cudaGetLastError();  // unregistered memory: not an error here
+    }
+    prepare_window(st, hx, 0, slice, B, nb, nullptr, nullptr, -1, /*host_gather=*/true, zc);
+    Window& W = st->win;
+    const std::vector<int64_t> sd_strides = strides_of(slab_dims(st, B));
+    const size_t xn = W.X.n, bn = size_t(nb * st->N * st->s);
+    if (W.hX_n < xn) {
+        host_free_huge(W.hX, W.hX_n * sizeof(double));
+        W.hX = nullptr;
+        W.hX_n = 0;
+        W.hX = static_cast<double*>(host_alloc_huge(xn * sizeof(double)));
+        if (!W.hX) throw RocpError{ROCP_E_OOM, "host staging allocation failed"};
+        W.hX_n = xn;
+    }
+    if (!st->pool || st->pool->size() < threads) st->pool = std::make_unique<HostPool>(threads);
+    if (W.hbase_n < bn) {
+        if (W.hbase) cudaFreeHost(W.hbase);
+        CK(cudaHostAlloc(&W.hbase, bn * sizeof(int64_t), cudaHostAllocDefault));
+        W.hbase_n = bn;
+    }
+    // K1 on the device; the fibre bases come back (nb x N x S int64)
+    k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
+    after_launch(dev, "k_set_u64");
+    k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
+    after_launch(dev, "k_set_u32");
+    launch_draw(dev, W.jobs);
+    const double tq = std::getenv("ROCP_HOST_TRACE") ? std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() : 0.0;
+    CK(cudaMemcpyAsync(W.hbase, W.base.p, bn * sizeof(int64_t), cudaMemcpyDeviceToHost, dev->stream));
+    CK(cudaStreamSynchronize(dev->stream));
+    if (std::getenv("ROCP_HOST_TRACE"))
+        std::fprintf(stderr, "[rocp host] draw + bases D2H + sync %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() - tq);
+    // sub-windows: gather (host) -> H2D -> chain (device), pipelined
+    if (sub < 1) sub = std::max<int64_t>(1, std::min<int64_t>(nb, 6));
+    static const bool trace = std::getenv("ROCP_HOST_TRACE") != nullptr;
+    auto wall = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double tw = trace ? wall() : 0.0;
+    for (int64_t b0 = 0; b0 < nb; b0 += sub) {
+        const int64_t b1 = std::min(nb, b0 + sub);
+        if (zc && W.zc_tile[size_t(b1)] > W.zc_tile[size_t(b0)]) {  // GPU: contiguous stages, in place
+            k_gather<<<unsigned(W.zc_tile[size_t(b1)] - W.zc_tile[size_t(b0)]), kGatherThreads, 0, dev->stream>>>(
+                W.jobs.gather.p, W.jobs.tiles.p + W.zc_tile[size_t(b0)]);
+            after_launch(dev, "k_gather");
+        }
+        host_gather_range(st, hx, slice, B, b0, b1, threads, zc != nullptr);
+        if (trace) {
+            const double t = wall();
+            std::fprintf(stderr, "[rocp host] batches %lld..%lld gather %.2f ms (%d threads)\n", (long long)b0,
+                         (long long)b1, t - tw, threads);
+            tw = t;
+        }
+        if (!zc) {
+            const int64_t x0 = W.xoff[size_t(b0 * st->N)];
+            const int64_t x1 = (b1 < nb) ? W.xoff[size_t(b1 * st->N)] : int64_t(W.X.n);
+            CK(cudaMemcpyAsync(W.X.p + x0, W.hX + x0, size_t(x1 - x0) * sizeof(double), cudaMemcpyHostToDevice,
+                               dev->stream));
+        } else {  // only the host-gathered (strided) stages cross as copies
+            for (int64_t b = b0; b < b1; ++b)
+                for (int stage = 0; stage < st->N; ++stage) {
+                    const int mode = stage == 0 ? st->N : stage;
+                    if (sd_strides[size_t(mode - 1)] == 1) continue;
+                    const int64_t x0 = W.xoff[size_t(b * st->N + stage)];
+                    const int64_t n = xs_size(st->stage_rows(stage, B), st->s);
+                    CK(cudaMemcpyAsync(W.X.p + x0, W.hX + x0, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                                       dev->stream));
+                }
+        }
+        launch_chain(st, b1 - b0, B, b0);
+        st->t_len += (b1 - b0) * B;
+    }
 }
 
 }  // namespace
@@ -882,6 +1161,10 @@ rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms) {
 }
 
 void* rocp_cuda_stream(rocp_dev* dev) { return dev ? static_cast<void*>(dev->stream) : nullptr; }
+
+void* rocp_host_alloc(size_t bytes) { return host_alloc_huge(bytes); }
+
+void rocp_host_free(void* p, size_t bytes) { host_free_huge(p, bytes); }
 
 rocp_status rocp_synchronize(rocp_dev* dev) {
     return guarded(dev, [&] { CK(cudaStreamSynchronize(dev->stream)); });
@@ -1453,12 +1736,17 @@ rocp_status rocp_stream_consume_host(rocp_stream* st, const double* x_new, int64
         if (batch < 1) throw_domain("batch must hold at least one slice");
         rocp_dev* dev = st->dev;
         const int64_t numel = prod(st->head) * batch;
-        if (st->staging.n < size_t(numel)) {
+        if (st->resid_level >= 2 && st->staging.n < size_t(numel)) {
             CK(cudaStreamSynchronize(dev->stream));
             st->staging.alloc(size_t(numel));
         }
-        CK(cudaMemcpyAsync(st->staging.p, x_new, size_t(numel) * 8, cudaMemcpyHostToDevice, dev->stream));
-        consume_one(st, st->staging.p, batch, seed, batch_id);
+        (void)numel;
+        if (st->resid_level >= 2) {  // every-stage residuals use the per-stage kernels: full slab copy
+            CK(cudaMemcpyAsync(st->staging.p, x_new, size_t(numel) * 8, cudaMemcpyHostToDevice, dev->stream));
+            consume_one(st, st->staging.p, batch, seed, batch_id);
+        } else {
+            consume_range_host(st, x_new, batch, 1, seed, batch_id, st->host_threads, 1);
+        }
     });
 }
 
@@ -1501,6 +1789,15 @@ rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int
             dev->launches += it->second.second;
         }
         st->t_len += batch * nb;
+    });
+}
+
+rocp_status rocp_stream_consume_range_host(rocp_stream* st, const double* x, int64_t batch, int64_t nb,
+                                           uint64_t seed, uint32_t first_batch_id, int threads) {
+    return guarded(st->dev, [&] {
+        if (batch < 1 || nb < 1) throw_domain("consume_range_host: empty range");
+        if (st->resid_level >= 2) throw_domain("consume_range_host: residual level 2 needs device slabs");
+        consume_range_host(st, x, batch, nb, seed, first_batch_id, threads > 0 ? threads : st->host_threads, 0);
     });
 }
 

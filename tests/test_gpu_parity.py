@@ -300,12 +300,29 @@ def test_stream_host_slab_and_range_graph(dev):
         b.consume(H.slab(x, dims, t_init + k * B, B), B, 77, k + 1)
     _cmp_stream(a, b, 3)
     ref = [a.factor(1), a.factor(2), a.temporal()]
-    # (2) restore + the whole range as one CUDA graph, twice (replay)
+    # (2) restore + the whole range as one persistent-kernel window, twice (replay)
     for _ in range(2):
         a.restore()
         a.consume_range(X, t_init, B, nb, 77, 1)
         assert bitwise(a.factor(1), ref[0]) and bitwise(a.factor(2), ref[1])
         assert bitwise(a.temporal(), ref[2])
+    # (3) restore + the whole range from HOST slabs (host gather of sampled fibres only)
+    for threads in (1, 0):
+        a.restore()
+        a.consume_range_host(H.slab(x, dims, t_init, B * nb), B, nb, 77, 1, threads=threads)
+        assert bitwise(a.factor(1), ref[0]) and bitwise(a.factor(2), ref[1])
+        assert bitwise(a.temporal(), ref[2])
+    # (4) the same range in a registered huge-page buffer (rocp_host_alloc): the GPU reads
+    # the mode-1 fibres in place, host threads gather the strided stages
+    slab = H.slab(x, dims, t_init, B * nb)
+    hb = rocp.HostBuffer(slab.size)
+    hb.array[:] = slab
+    for _ in range(2):
+        a.restore()
+        a.consume_range_host(hb.array, B, nb, 77, 1)
+        assert bitwise(a.factor(1), ref[0]) and bitwise(a.factor(2), ref[1])
+        assert bitwise(a.temporal(), ref[2])
+    hb.free()
 
 
 def test_stream_replay_seams_and_pins(dev):
