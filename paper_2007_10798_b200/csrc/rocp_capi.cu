@@ -616,6 +616,8 @@ struct rocp_stream {
     int resid_level = 1;          // 0 none, 1 temporal stage (default), 2 every stage
     int host_threads = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
     std::unique_ptr<HostPool> pool;  // host-slab gather workers (created on first use)
+    cudaStream_t copy_stream = nullptr;       // host-slab path: in-place reads + staging copies
+    std::vector<cudaEvent_t> copy_events;     // one per sub-window, joined by the compute stream
     // checkpoint copies (device)
     std::vector<DBuf<double>> ckU, ckP, ckQ;
     int64_t ck_t_len = -1;
@@ -632,6 +634,8 @@ struct rocp_stream {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        for (cudaEvent_t e : copy_events) cudaEventDestroy(e);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
     int64_t stage_rows(int stage, int64_t batch) const { return stage == 0 ? batch : head[size_t(stage - 1)]; }
 };
@@ -947,62 +951,47 @@ void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uin
 
 // ---- host-slab path ----------------------------------------------------------
 // For inputs that live in host memory (the reference-facing call), only the
-// sampled fibres cross PCIe: the GPU draws the window's indices, host threads
-// gather the fibres from the caller's slabs into pinned staging in the
-// row-tiled X_s layout, and sub-window H2D copies overlap the persistent chain.
-void host_gather_range(rocp_stream* st, const double* hx, int64_t slice, int64_t B, int64_t b0, int64_t b1,
-                       int threads, bool skip_contiguous) {
+// sampled fibres cross PCIe.  The GPU draws the window's indices; host threads
+// gather the sampled fibres of the strided stages from the caller's slabs into
+// pinned staging (row-tiled X_s layout), batch by batch; as soon as a
+// sub-window's batches are complete the calling thread issues, on a copy
+// stream, the in-place GPU read of its contiguous mode-1 fibres (registered
+// ranges only) and the H2D copy of its staging, and joins the persistent chain
+// for it on the compute stream -- so host gather, PCIe and the chain overlap,
+// and no host thread waits at sub-window boundaries.
+struct HostTask {
+    int32_t b, stage;
+    int64_t c0, c1;
+};
+
+void host_gather_task(rocp_stream* st, const double* hx, int64_t slice, int64_t B, const std::vector<int64_t>& d,
+                      const std::vector<int64_t>& strides, const HostTask& tk) {
     Window& W = st->win;
     const int N = st->N;
     const int64_t S = st->s;
-    const std::vector<int64_t> d = slab_dims(st, B);
-    const std::vector<int64_t> strides = strides_of(d);
-    // Tasks of kFib fibres, claimed dynamically; each fibre is walked on its own
-    // (strided rows on 2 MB pages stay TLB-resident, and the out-of-order core
-    // keeps a fibre's independent loads in flight -- tools/host_gather_bench.cpp:
-    // this beats row-interleaved walks and software prefetch on the GPU box).
-    constexpr int64_t kFib = 16;
-    struct Task {
-        int32_t b, stage;
-        int64_t c0, c1;
-    };
-    std::vector<Task> tasks;
-    for (int pass = 0; pass < 2; ++pass)  // strided stages first: they are the heavy ones
-        for (int64_t b = b0; b < b1; ++b)
-            for (int stage = 0; stage < N; ++stage) {
-                const int mode = stage == 0 ? N : stage;
-                if ((strides[size_t(mode - 1)] == 1) != (pass == 1)) continue;
-                if (pass == 1 && skip_contiguous) continue;  // read by the GPU in place
-                for (int64_t c0 = 0; c0 < S; c0 += kFib)
-                    tasks.push_back(Task{int32_t(b), stage, c0, std::min(S, c0 + kFib)});
-            }
-    std::atomic<size_t> next{0};
-    const std::function<void()> work = [&]() {
-        for (size_t k = next.fetch_add(1, std::memory_order_relaxed); k < tasks.size();
-             k = next.fetch_add(1, std::memory_order_relaxed)) {
-            const Task& tk = tasks[k];
-            const int mode = tk.stage == 0 ? N : tk.stage;
-            const int64_t I = d[size_t(mode - 1)], ms = strides[size_t(mode - 1)];
-            const double* src_b = hx + int64_t(tk.b) * B * slice;
-            const int64_t* bases = W.hbase + (int64_t(tk.b) * N + tk.stage) * S;
-            double* dst = W.hX + W.xoff[size_t(int64_t(tk.b) * N + tk.stage)];
-            for (int64_t c = tk.c0; c < tk.c1; ++c) {
-                const double* f = src_b + bases[c];
-                if (ms == 1) {
-                    for (int64_t i0 = 0; i0 < I; i0 += 32)
-                        std::memcpy(dst + xs_offset(i0, c, S), f + i0, size_t(std::min<int64_t>(32, I - i0)) * 8);
-                } else {
-                    for (int64_t i0 = 0; i0 < I; i0 += 32) {
-                        double* o = dst + xs_offset(i0, c, S);
-                        const int64_t n = std::min<int64_t>(32, I - i0);
-                        const double* fi = f + i0 * ms;
-                        for (int64_t i = 0; i < n; ++i) o[i] = fi[i * ms];
-                    }
-                }
+    const int mode = tk.stage == 0 ? N : tk.stage;
+    const int64_t I = d[size_t(mode - 1)], ms = strides[size_t(mode - 1)];
+    const double* src_b = hx + int64_t(tk.b) * B * slice;
+    const int64_t* bases = W.hbase + (int64_t(tk.b) * N + tk.stage) * S;
+    double* dst = W.hX + W.xoff[size_t(int64_t(tk.b) * N + tk.stage)];
+    // Each fibre is walked on its own: strided rows on 2 MB pages stay
+    // TLB-resident and the out-of-order core keeps a fibre's independent loads
+    // in flight (tools/host_gather_bench.cpp: this beats row-interleaved walks
+    // and software prefetch on the GPU box's host).
+    for (int64_t c = tk.c0; c < tk.c1; ++c) {
+        const double* f = src_b + bases[c];
+        if (ms == 1) {
+            for (int64_t i0 = 0; i0 < I; i0 += 32)
+                std::memcpy(dst + xs_offset(i0, c, S), f + i0, size_t(std::min<int64_t>(32, I - i0)) * 8);
+        } else {
+            for (int64_t i0 = 0; i0 < I; i0 += 32) {
+                double* o = dst + xs_offset(i0, c, S);
+                const int64_t n = std::min<int64_t>(32, I - i0);
+                const double* fi = f + i0 * ms;
+                for (int64_t i = 0; i < n; ++i) o[i] = fi[i * ms];
             }
         }
-    };
-    st->pool->run(std::min<int>(threads, int(tasks.size())), work);
+    }
 }
 
 void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb, uint64_t seed,
@@ -1010,6 +999,8 @@ void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb
     rocp_dev* dev = st->dev;
     check_capacity(st, B * nb);
     const int64_t slice = prod(st->head);
+    const int N = st->N;
+    const int64_t S = st->s;
     // A CUDA-registered range (e.g. rocp_host_alloc) lets the GPU read the
     // contiguous mode-1 fibres in place over PCIe while host threads gather the
     // strided stages; otherwise host threads gather every stage.
@@ -1027,8 +1018,9 @@ void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb
     }
     prepare_window(st, hx, 0, slice, B, nb, nullptr, nullptr, -1, /*host_gather=*/true, zc);
     Window& W = st->win;
-    const std::vector<int64_t> sd_strides = strides_of(slab_dims(st, B));
-    const size_t xn = W.X.n, bn = size_t(nb * st->N * st->s);
+    const std::vector<int64_t> d = slab_dims(st, B);
+    const std::vector<int64_t> strides = strides_of(d);
+    const size_t xn = W.X.n, bn = size_t(nb * N * S);
     if (W.hX_n < xn) {
         host_free_huge(W.hX, W.hX_n * sizeof(double));
         W.hX = nullptr;
@@ -1038,61 +1030,115 @@ void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb
         W.hX_n = xn;
     }
     if (!st->pool || st->pool->size() < threads) st->pool = std::make_unique<HostPool>(threads);
+    if (!st->copy_stream) CK(cudaStreamCreateWithFlags(&st->copy_stream, cudaStreamNonBlocking));
     if (W.hbase_n < bn) {
         if (W.hbase) cudaFreeHost(W.hbase);
         CK(cudaHostAlloc(&W.hbase, bn * sizeof(int64_t), cudaHostAllocDefault));
         W.hbase_n = bn;
     }
-    // K1 on the device; the fibre bases come back (nb x N x S int64)
+    // K1 on the device; the fibre bases come back (nb x N x S int64).  The
+    // synchronize also retires every copy of the previous call (joined below).
     k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
     after_launch(dev, "k_set_u64");
     k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
     after_launch(dev, "k_set_u32");
     launch_draw(dev, W.jobs);
-    const double tq = std::getenv("ROCP_HOST_TRACE") ? std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() : 0.0;
     CK(cudaMemcpyAsync(W.hbase, W.base.p, bn * sizeof(int64_t), cudaMemcpyDeviceToHost, dev->stream));
     CK(cudaStreamSynchronize(dev->stream));
-    if (std::getenv("ROCP_HOST_TRACE"))
-        std::fprintf(stderr, "[rocp host] draw + bases D2H + sync %.2f ms\n",
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() - tq);
-    // sub-windows: gather (host) -> H2D -> chain (device), pipelined
-    if (sub < 1) sub = std::max<int64_t>(1, std::min<int64_t>(nb, 6));
-    static const bool trace = std::getenv("ROCP_HOST_TRACE") != nullptr;
-    auto wall = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    double tw = trace ? wall() : 0.0;
-    for (int64_t b0 = 0; b0 < nb; b0 += sub) {
-        const int64_t b1 = std::min(nb, b0 + sub);
-        if (zc && W.zc_tile[size_t(b1)] > W.zc_tile[size_t(b0)]) {  // GPU: contiguous stages, in place
-            k_gather<<<unsigned(W.zc_tile[size_t(b1)] - W.zc_tile[size_t(b0)]), kGatherThreads, 0, dev->stream>>>(
+
+    // host tasks of kFib fibres, batch by batch (strided stages first within a batch)
+    constexpr int64_t kFib = 16;
+    std::vector<HostTask> tasks;
+    std::unique_ptr<std::atomic<int>[]> remaining(new std::atomic<int>[size_t(nb)]);
+    for (int64_t b = 0; b < nb; ++b) {
+        const size_t before = tasks.size();
+        for (int pass = 0; pass < 2; ++pass)
+            for (int stage = 0; stage < N; ++stage) {
+                const int mode = stage == 0 ? N : stage;
+                if ((strides[size_t(mode - 1)] == 1) != (pass == 1)) continue;
+                if (pass == 1 && zc) continue;  // read by the GPU in place
+                for (int64_t c0 = 0; c0 < S; c0 += kFib)
+                    tasks.push_back(HostTask{int32_t(b), stage, c0, std::min(S, c0 + kFib)});
+            }
+        remaining[size_t(b)].store(int(tasks.size() - before), std::memory_order_relaxed);
+    }
+    if (sub < 1) {
+        static const int64_t env_sub = std::getenv("ROCP_HOST_SUB") ? std::atoll(std::getenv("ROCP_HOST_SUB")) : 0;
+        sub = env_sub > 0 ? env_sub : 1;
+    }
+    sub = std::max<int64_t>(1, std::min(sub, nb));
+    const int64_t nsub = (nb + sub - 1) / sub;
+    while (int64_t(st->copy_events.size()) < nsub) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        st->copy_events.push_back(e);
+    }
+    // GPU side of sub-window [b0, b1): in-place mode-1 reads + staging copies on
+    // the copy stream, then the chain on the compute stream.
+    auto issue = [&](int64_t k, int64_t b0, int64_t b1) {
+        cudaStream_t cs = st->copy_stream;
+        if (zc && W.zc_tile[size_t(b1)] > W.zc_tile[size_t(b0)]) {
+            k_gather<<<unsigned(W.zc_tile[size_t(b1)] - W.zc_tile[size_t(b0)]), kGatherThreads, 0, cs>>>(
                 W.jobs.gather.p, W.jobs.tiles.p + W.zc_tile[size_t(b0)]);
             after_launch(dev, "k_gather");
         }
-        host_gather_range(st, hx, slice, B, b0, b1, threads, zc != nullptr);
-        if (trace) {
-            const double t = wall();
-            std::fprintf(stderr, "[rocp host] batches %lld..%lld gather %.2f ms (%d threads)\n", (long long)b0,
-                         (long long)b1, t - tw, threads);
-            tw = t;
-        }
-        if (!zc) {
-            const int64_t x0 = W.xoff[size_t(b0 * st->N)];
-            const int64_t x1 = (b1 < nb) ? W.xoff[size_t(b1 * st->N)] : int64_t(W.X.n);
-            CK(cudaMemcpyAsync(W.X.p + x0, W.hX + x0, size_t(x1 - x0) * sizeof(double), cudaMemcpyHostToDevice,
-                               dev->stream));
-        } else {  // only the host-gathered (strided) stages cross as copies
-            for (int64_t b = b0; b < b1; ++b)
-                for (int stage = 0; stage < st->N; ++stage) {
-                    const int mode = stage == 0 ? st->N : stage;
-                    if (sd_strides[size_t(mode - 1)] == 1) continue;
-                    const int64_t x0 = W.xoff[size_t(b * st->N + stage)];
-                    const int64_t n = xs_size(st->stage_rows(stage, B), st->s);
-                    CK(cudaMemcpyAsync(W.X.p + x0, W.hX + x0, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
-                                       dev->stream));
-                }
-        }
+        for (int64_t b = b0; b < b1; ++b)
+            for (int stage = 0; stage < N; ++stage) {
+                const int mode = stage == 0 ? N : stage;
+                if (zc && strides[size_t(mode - 1)] == 1) continue;
+                const int64_t x0 = W.xoff[size_t(b * N + stage)];
+                const int64_t n = xs_size(st->stage_rows(stage, B), S);
+                CK(cudaMemcpyAsync(W.X.p + x0, W.hX + x0, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cs));
+            }
+        CK(cudaEventRecord(st->copy_events[size_t(k)], cs));
+        CK(cudaStreamWaitEvent(dev->stream, st->copy_events[size_t(k)], 0));
         launch_chain(st, b1 - b0, B, b0);
         st->t_len += (b1 - b0) * B;
-    }
+    };
+    static const bool trace = std::getenv("ROCP_HOST_TRACE") != nullptr;
+    auto wall = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double tw0 = trace ? wall() : 0.0;
+    std::atomic<size_t> next{0};
+    const std::thread::id caller = std::this_thread::get_id();
+    int64_t issued = 0;  // sub-windows issued so far (caller thread only)
+    std::exception_ptr failure;
+    auto ready = [&](int64_t k) {
+        for (int64_t b = k * sub; b < std::min(nb, (k + 1) * sub); ++b)
+            if (remaining[size_t(b)].load(std::memory_order_acquire) != 0) return false;
+        return true;
+    };
+    auto try_issue = [&](bool block) {
+        while (issued < nsub && !failure) {
+            if (!ready(issued)) {
+                if (!block) return;
+                std::this_thread::yield();
+                continue;
+            }
+            try {
+                issue(issued, issued * sub, std::min(nb, (issued + 1) * sub));
+            } catch (...) {
+                failure = std::current_exception();
+            }
+            if (trace)
+                std::fprintf(stderr, "[rocp host] sub-window %lld issued at %.2f ms\n", (long long)issued,
+                             wall() - tw0);
+            ++issued;
+        }
+    };
+    const std::function<void()> work = [&]() {
+        const bool is_caller = std::this_thread::get_id() == caller;
+        for (size_t k = next.fetch_add(1, std::memory_order_relaxed); k < tasks.size();
+             k = next.fetch_add(1, std::memory_order_relaxed)) {
+            host_gather_task(st, hx, slice, B, d, strides, tasks[k]);
+            remaining[size_t(tasks[k].b)].fetch_sub(1, std::memory_order_release);
+            if (is_caller) try_issue(false);
+        }
+        if (is_caller) try_issue(true);
+    };
+    st->pool->run(std::min<int>(threads, int(std::max<size_t>(tasks.size(), 1))), work);
+    if (failure) std::rethrow_exception(failure);
 }
 
 }  // namespace
