@@ -13,8 +13,9 @@ Reported (one JSON line on rank 0):
   value    time slices/s with the tensor resident in HBM (device-timed with
            CUDA events over K steps; max over ranks for N > 1)
   e2e      the same metric through the reference-facing host-slab call
-           (rocp_stream_consume_host): every step copies its 900 slices from
-           pinned host memory and reads the model back
+           (rocp_stream_consume_range_host): every step starts from the 900
+           slices in host memory (a rocp_host_alloc buffer), moves the
+           sampled fibres to the device and reads the model back
   roofline the window gather kernel (sampled-fibre gather, north-star item 1):
            algorithmic sector bytes per launch / its average
            CUDA-event launch time in the timed region, vs MEASURED_PEAKS.json
@@ -37,8 +38,39 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ROCP time-slices/sec and sampled-gather HBM GB/s vs B200 peak"
-CFG = dict(name="configs[1]", dims=[1000, 1000, 1000], rank=20, t_init=100, batch=25, snr_db=20.0,
-           tol=1e-4, max_iters=100)
+# BASELINE.json configs (C1..C5); the default bench line is configs[1].
+CONFIGS = {
+    "c1": dict(name="configs[0]", dims=[200, 200, 500], rank=10, t_init=50, batch=10, snr_db=20.0,
+               tol=1e-6, max_iters=20, family="normal"),
+    "c2": dict(name="configs[1]", dims=[1000, 1000, 1000], rank=20, t_init=100, batch=25, snr_db=20.0,
+               tol=1e-4, max_iters=100, family="normal"),
+    "c3": dict(name="configs[2]", dims=[200, 200, 200, 200], rank=10, t_init=20, batch=10, snr_db=30.0,
+               tol=1e-4, max_iters=100, family="uniform"),
+    "c4": dict(name="configs[3]", dims=[4000, 4000, 500], rank=50, t_init=50, batch=50, snr_db=20.0,
+               tol=1e-4, max_iters=100, family="normal"),
+    "c5": dict(name="configs[4]", dims=[60, 60, 60, 60, 300], rank=16, t_init=10, batch=10, snr_db=10.0,
+               tol=1e-4, max_iters=100, family="congruent"),
+}
+CFG = CONFIGS["c2"]
+
+
+def make_factors(dims, R, family, g):
+    """Seeded factors of the config's family: iid N(0,1), iid U(0,1), or pairwise
+    column congruence 0.9 (G L^T, L = chol(0.9 11^T + 0.1 I))."""
+    if family == "uniform":
+        return [np.asfortranarray(g.random((d, R))) for d in dims]
+    if family == "congruent":
+        L = np.linalg.cholesky(np.full((R, R), 0.9) + 0.1 * np.eye(R))
+        return [np.asfortranarray(g.standard_normal((d, R)) @ L.T) for d in dims]
+    return [np.asfortranarray(g.standard_normal((d, R))) for d in dims]
+
+
+def workload_text(cfg):
+    d = cfg["dims"]
+    nb = (d[-1] - cfg["t_init"]) // cfg["batch"]
+    return (f"{cfg['name']}: {'x'.join(map(str, d))} fp64, R={cfg['rank']}, init {cfg['t_init']} slices "
+            f"(cprand tol {cfg['tol']:g}, <= {cfg['max_iters']} sweeps), stream {nb * cfg['batch']} slices in "
+            f"{nb} batches of {cfg['batch']}, S={auto_s(cfg['rank'])}")
 
 
 def sector_bytes_per_batch(dims, S, B):
@@ -174,22 +206,23 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    CFG = CONFIGS[args.config]
     dims, R, B = CFG["dims"], CFG["rank"], CFG["batch"]
     S = auto_s(R)
     head = dims[:-1]
     g = np.random.default_rng(0)
-    A = [np.asfortranarray(g.standard_normal((d, R))) for d in head]
-    nslab = 4
+    from oracle import oracle as orc
+    A = make_factors(head, R, CFG["family"], g)
+    nslab = 4 if int(np.prod(head)) * B <= 50_000_000 else 2
     slabs = []
-    for k in range(nslab):  # X(:,:,t) = A1 diag(a3_t) A2^T + noise (gen_synthetic semantics)
-        a3 = g.standard_normal((B, R))
-        x = np.einsum("ir,jr,tr->tji", A[0], A[1], a3, optimize=True).reshape(-1)
+    for k in range(nslab):  # [[A_1 .. A_{N-1}, a_t]] + noise at the config's SNR (gen_synthetic semantics)
+        a_t = make_factors([B], R, CFG["family"], g)[0]
+        x = orc.reconstruct(A + [a_t], head + [B])
         e = g.standard_normal(x.size)
         x += np.linalg.norm(x) * 10 ** (-CFG["snr_db"] / 20) / np.linalg.norm(e) * e
         slabs.append(np.ascontiguousarray(x))
     kr = []
-    from oracle import oracle as orc
-    for n in (1, 2):
+    for n in range(1, len(dims)):
         _, dec = orc.draw_samples(head + [CFG["t_init"]], n, S, 7, 0, 0)
         temporal = np.asfortranarray(g.standard_normal((CFG["t_init"], R)))
         kr.append(orc.sampled_khatri_rao(dec, orc.factors_excluding(A + [temporal], n)))
@@ -208,11 +241,11 @@ def reference_arm(args):
         "ms_per_step": 1000.0 * statistics.mean(w for _, _, w in per_step),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{CFG['name']} stream phase: head 1000x1000, R=20, S=600, batch 25",
-                   "sample": f"{nslab} synthetic batches of 25 slices repeated for {budget:.0f} s per step "
+        "config": {"workload": workload_text(CFG),
+                   "sample": f"{nslab} synthetic batches of {B} slices repeated for {budget:.0f} s per step "
                              f"on each of {threads} threads (independent streams, ROCP_THREADS semantics)"},
         "cpu_baseline": {"value": value, "unit": "time-slices/s", "cores": threads, "kind": "port",
-                         "sample": f"oracle port of RocpStream::consume on {nslab} x 25-slice slabs, "
+                         "sample": f"oracle port of RocpStream::consume on {nslab} x {B}-slice slabs, "
                                    f"{threads} threads x {budget:.0f} s per step"},
         "e2e": {"value": value, "unit": "time-slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_buildable": False,
@@ -232,6 +265,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (c2 = configs[1], the headline workload)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -240,6 +275,7 @@ def main():
     import paper_2007_10798_b200 as rocp
 
     world, rank, local, dist, torch = dist_setup()
+    CFG = CONFIGS[args.config]
     dims, R, t_init, B = CFG["dims"], CFG["rank"], CFG["t_init"], CFG["batch"]
     head = dims[:-1]
     S = auto_s(R)
@@ -250,7 +286,7 @@ def main():
     dev = rocp.Device(local)
     # ---- data: [[A1, A2, A3]] + noise at 20 dB, generated on the device
     g = np.random.default_rng(1000 + rank)
-    truth = [np.asfortranarray(g.standard_normal((d, R))) for d in dims]
+    truth = make_factors(dims, R, CFG["family"], g)
     X = dev.tensor(dims)
     X.generate(truth, snr_db=CFG["snr_db"], noise_seed=2000 + rank)
     # ---- init: randomized CP-ALS on the first t_init slices (cprand.cpp:12-69)
@@ -308,7 +344,7 @@ def main():
     # only the sampled fibres cross PCIe (host gather), the model is read back every step
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        slice_ = head[0] * head[1]
+        slice_ = int(np.prod(head))
         hbuf = rocp.HostBuffer(slices_per_step * slice_)  # pinned, 2 MB pages (rocp_host_alloc)
         host = hbuf.array
         X.slab(t_init, slices_per_step).download(out=host)
@@ -330,13 +366,14 @@ def main():
                "h2d_bytes_per_step": int(xs_elems * 8),
                "d2h_bytes_per_step": int(sum(m.size for m in out) * 8 + nb * len(dims) * S * 8),
                "steps": args.e2e_steps, "ms_per_step": statistics.mean(e2e_ms),
-               "path": "rocp_stream_consume_range_host: device draw -> host-thread gather of the sampled "
-                       "fibres from the caller's slabs -> H2D of X_s (sub-window pipelined) -> device chain"}
+               "path": "rocp_stream_consume_range_host: device draw -> host threads gather the strided "
+                       "sampled fibres, the GPU reads the mode-1 fibres in place (zero-copy) -> H2D of "
+                       "X_s per batch on a copy stream -> persistent chain per batch"}
 
     # ---- CPU baseline (rank 0, bounded sample)
     cpu = None
     if rank == 0 and not args.no_cpu:
-        slice_ = head[0] * head[1]
+        slice_ = int(np.prod(head))
         xs = X.slab(t_init, 4 * B).download()
         slabs = [np.ascontiguousarray(xs[k * B * slice_:(k + 1) * B * slice_]) for k in range(4)]
         v, n, wall = cpu_sample_stream(init.model[:-1], init.best_sampled_kr, R, S, t_init, head, slabs, B,
@@ -350,13 +387,14 @@ def main():
             "metric": METRIC, "value": value, "unit": "time-slices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded N(0,1) factors, 20 dB Gaussian noise, generated on device)",
-            "config": {"workload": f"{CFG['name']}: 1000x1000x1000 fp64, R=20, init 100 slices (cprand tol 1e-4), "
-                                   f"stream 900 slices in 36 batches of 25, S=600",
-                       "step": "one full streaming pass (36 x RocpStream::consume) from the post-init state",
-                       "l2": "inputs larger than L2 (8 GB tensor); fresh sampling seed every step",
+            "data": f"synthetic (seeded {CFG['family']} factors, {CFG['snr_db']:g} dB Gaussian noise, "
+                    f"generated on device)",
+            "config": {"workload": workload_text(CFG),
+                       "step": f"one full streaming pass ({nb} x RocpStream::consume) from the post-init state",
+                       "l2": f"inputs larger than L2 ({8 * int(np.prod(dims)) / 1e9:.1f} GB tensor); "
+                             f"fresh sampling seed every step",
                        "parallelism": f"{world} independent stream replica(s), one per GPU (no collective)"},
-            "entries_per_s": value * head[0] * head[1],
+            "entries_per_s": value * int(np.prod(head)),
             "init_seconds": init_seconds, "init_sweeps": init.iterations, "init_fitness": init.best_fitness,
             "gpu_launches": launches,
             "roofline": {"kernel": "k_gather (window sampled-fibre gather)", "bound": "hbm",

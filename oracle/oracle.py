@@ -62,6 +62,9 @@ def lib():
                                         C.POINTER(C.c_void_p)]
         _lib.orc_stream_free.argtypes = [C.c_void_p]
         _lib.orc_stream_consume.argtypes = [C.c_void_p, _f64p, C.c_int64, C.c_uint64, C.c_uint32]
+        _lib.orc_stream_last_residuals.argtypes = [C.c_void_p, _f64p]
+        _lib.orc_stream_consume_sharded.argtypes = [C.c_void_p, _f64p, C.c_int64, C.c_uint64, C.c_uint32,
+                                                    C.c_int]
         _lib.orc_stream_update_last_mode_with.argtypes = [C.c_void_p, _f64p, C.c_int64, _i64p,
                                                           C.c_int64, _f64p, _f64p,
                                                           C.POINTER(C.c_int)]
@@ -326,6 +329,16 @@ class Stream:
     def consume(self, x_new, batch, seed, batch_id):
         x = self._slab(x_new, batch)
         _check(lib().orc_stream_consume(self._h, _p(x), batch, seed, batch_id))
+
+    def consume_sharded(self, x_new, batch, seed, batch_id, virtual_shards):
+        """Mode-1 sharded consume, canonical order of `virtual_shards` row ranges."""
+        x = self._slab(x_new, batch)
+        _check(lib().orc_stream_consume_sharded(self._h, _p(x), batch, seed, batch_id, virtual_shards))
+
+    def last_residuals(self):
+        out = np.zeros(self.order)
+        _check(lib().orc_stream_last_residuals(self._h, _p(out)))
+        return out
 
     def update_last_mode_with(self, x_new, batch, rows):
         x = self._slab(x_new, batch)

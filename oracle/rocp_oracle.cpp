@@ -920,6 +920,113 @@ int orc_stream_consume(orc_stream* st, const double* x_new, int64_t batch, uint6
     return ORC_OK;
 }
 
+// ---- mode-1 sharded consume ---------------------------
+// The multi-GPU form of RocpStream::consume (north star: shard along mode 1,
+// partial contractions / Grams of the non-owned modes combined by an NCCL
+// collective, owned-mode rows local).  Its canonical order is fixed by V
+// virtual shards -- contiguous mode-1 row ranges [floor(v*I1/V),
+// floor((v+1)*I1/V)) -- independent of the GPU count G (G divides V):
+//   * temporal stage and modes n >= 2: the samples are split by the shard of
+//     their mode-1 index, keeping sample order; each shard's Gram and
+//     contraction use the canonical chunked order over its own subsequence;
+//     totals are part_0 + part_1 + ... + part_{V-1} in shard order; then
+//     P + inc, Q + G and solve_gram exactly as the unsharded stream;
+//   * mode 1 (the owned mode): unchanged (every rank updates its own rows);
+//   * sampled residuals: unchanged (per-sample column partials, hsum in
+//     sample order).
+// V = 1 is the unsharded consume.
+static Index shard_of(Index i0, Index I1, int V) { return ((i0 + 1) * V - 1) / I1; }
+
+static IndexSet subset(const IndexSet& idx, const std::vector<Index>& cols) {
+    IndexSet out;
+    out.mode = idx.mode;
+    out.dims = idx.dims;
+    const int no = idx.n_other();
+    for (Index c : cols) {
+        out.rows.push_back(idx.rows[size_t(c)]);
+        for (int k = 0; k < no; ++k) out.decoded.push_back(idx.at(c, k));
+    }
+    return out;
+}
+
+static std::vector<std::vector<Index>> shard_lists(const IndexSet& idx, Index I1, int V) {
+    std::vector<std::vector<Index>> lists(static_cast<size_t>(V));
+    for (Index c = 0; c < idx.count(); ++c) lists[size_t(shard_of(idx.at(c, 0) - 1, I1, V))].push_back(c);
+    return lists;
+}
+
+// sum_v gram(z_v) and sum_v contract(x_v, z_v) in shard order
+static void sharded_partials(const double* x, const Dims& d, const IndexSet& idx, const std::vector<const Mat*>& fs,
+                             Index I1, int V, Mat* g, Mat* inc, Mat* z_full, Mat* x_full) {
+    const std::vector<std::vector<Index>> lists = shard_lists(idx, I1, V);
+    for (int v = 0; v < V; ++v) {
+        const IndexSet sub = subset(idx, lists[size_t(v)]);
+        Mat z;
+        skr(sub, fs, &z);
+        if (z.cols == 0) z = Mat(0, fs[0]->cols);
+        const Mat xs = gather(x, d, sub);
+        const Mat gv = gram_of(z);
+        const Mat iv = contract_of(xs, z);
+        if (v == 0) {
+            *g = gv;
+            *inc = iv;
+        } else {
+            for (size_t e = 0; e < g->v.size(); ++e) g->v[e] = g->v[e] + gv.v[e];
+            for (size_t e = 0; e < inc->v.size(); ++e) inc->v[e] = inc->v[e] + iv.v[e];
+        }
+    }
+    skr(idx, fs, z_full);
+    *x_full = gather(x, d, idx);
+}
+
+int orc_stream_consume_sharded(orc_stream* st, const double* x_new, int64_t batch, uint64_t seed,
+                               uint32_t batch_id, int virtual_shards) {
+    const int V = virtual_shards;
+    const Index I1 = st->head[0];
+    if (V < 1 || V > I1) return fail(ORC_E_DOMAIN, "consume_sharded: need 1 <= virtual shards <= I_1");
+    const Dims d = slab_dims(st, batch);
+    const int N = st->order;
+    const int R = st->rank;
+    const Index s = st->s;
+    // temporal stage (rocp.cpp:71-84)
+    const IndexSet it = draw(d, N, s, seed, batch_id, 0u);
+    Mat g, rhs, z, xs;
+    sharded_partials(x_new, d, it, excluding(st->factors, N), I1, V, &g, &rhs, &z, &xs);
+    bool reg = false;
+    const Mat u = solve_gram_m(g, rhs, &reg);
+    st->last_resid.assign(size_t(N), 0.0);
+    if (st->resid_level >= 1) st->last_resid[0] = sampled_residual(xs, u, z);
+    st->regularized = st->regularized || reg;
+    std::vector<double> u_new(u.v);
+    orc_stream_append_temporal(st, u_new.data(), batch);
+    // modes 1..N-1 (rocp.cpp:115-131)
+    for (int n = 1; n < N; ++n) {
+        const IndexSet idx = draw(d, n, s, seed, batch_id, 0u);
+        if (n == 1) {
+            int r2 = 0;
+            const int rc = orc_stream_update_mode_with(st, x_new, batch, u_new.data(), 1, idx.rows.data(), s,
+                                                       nullptr, nullptr, &r2);
+            if (rc) return rc;
+            continue;
+        }
+        const Mat un = from_ptr(u_new.data(), batch, R);
+        std::vector<const Mat*> fs{&un};
+        for (int k = N - 1; k >= 1; --k)
+            if (k != n) fs.push_back(&st->factors[size_t(k - 1)]);
+        Mat gn, inc, zn, xn;
+        sharded_partials(x_new, d, idx, fs, I1, V, &gn, &inc, &zn, &xn);
+        Mat& p = st->p[size_t(n - 1)];
+        Mat& q = st->q[size_t(n - 1)];
+        for (size_t e = 0; e < p.v.size(); ++e) p.v[e] = p.v[e] + inc.v[e];
+        for (size_t e = 0; e < q.v.size(); ++e) q.v[e] = q.v[e] + gn.v[e];
+        bool r2 = false;
+        st->factors[size_t(n - 1)] = solve_gram_m(q, p, &r2);
+        if (st->resid_level >= 2) st->last_resid[size_t(n)] = sampled_residual(xn, st->factors[size_t(n - 1)], zn);
+    }
+    st->t_len += batch;
+    return ORC_OK;
+}
+
 int orc_stream_get(const orc_stream* st, int what, int mode, double* out) {
     switch (what) {
         case 0: to_ptr(st->factors[size_t(mode - 1)], out); return ORC_OK;

@@ -133,6 +133,11 @@ int orc_stream_last_residuals(const orc_stream* st, double* out);
 int orc_sampled_residual(const double* x, int64_t rows, int64_t s, const double* u,
                          const double* z, int rank, double* out);
 int orc_stream_regularized(const orc_stream* st);
+/* Mode-1 sharded consume with `virtual_shards` fixed row ranges (DESIGN.md
+ * section 7): the canonical order of the multi-GPU stream for any GPU count
+ * dividing virtual_shards.  virtual_shards = 1 equals orc_stream_consume. */
+int orc_stream_consume_sharded(orc_stream* st, const double* x_new, int64_t batch, uint64_t seed,
+                               uint32_t batch_id, int virtual_shards);
 
 /* ---- exact online baseline (baselines.cpp:142-195), test use only --------- */
 int orc_online_full_init(const double* x, const int64_t* dims, int order,
