@@ -267,6 +267,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
                     help="BASELINE.json config (c2 = configs[1], the headline workload)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="one stream sharded along mode 1 across the N GPUs (NCCL exchange; strong "
+                         "scaling, north star for configs[3]/[4]) instead of N independent replicas")
+    ap.add_argument("--virtual-shards", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -283,25 +287,39 @@ def main():
     nb = (T - t_init) // B
     slices_per_step = nb * B
 
-    dev = rocp.Device(local)
-    # ---- data: [[A1, A2, A3]] + noise at 20 dB, generated on the device
-    g = np.random.default_rng(1000 + rank)
+    sharded = args.sharded
+    if sharded and world > 1:  # NCCL bootstrap id from rank 0 over the torch process group
+        box = [rocp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        dev = rocp.Device(local, world, rank, box[0])
+    else:
+        dev = rocp.Device(local)
+    # ---- data: [[A1 .. AN]] + noise at the config's SNR, generated on the device
+    # (replicas: a different tensor per rank; sharded: the same tensor on every rank)
+    dseed = 0 if sharded else rank
+    g = np.random.default_rng(1000 + dseed)
     truth = make_factors(dims, R, CFG["family"], g)
     X = dev.tensor(dims)
-    X.generate(truth, snr_db=CFG["snr_db"], noise_seed=2000 + rank)
+    X.generate(truth, snr_db=CFG["snr_db"], noise_seed=2000 + dseed)
     # ---- init: randomized CP-ALS on the first t_init slices (cprand.cpp:12-69)
     init0 = [np.asfortranarray(g.standard_normal((d, R))) for d in head + [t_init]]
     dev.synchronize()
     t0 = time.perf_counter()
-    init = rocp.cprand_decompose(dev, X.slab(0, t_init), R, init0, seed=3000 + rank,
+    init = rocp.cprand_decompose(dev, X.slab(0, t_init), R, init0, seed=3000 + dseed,
                                  tol=CFG["tol"], max_iters=CFG["max_iters"])
     init_seconds = time.perf_counter() - t0
     stream = rocp.RocpStream(dev, init, S, t_capacity=T + 8)
+    XS = X
+    if sharded:  # this rank keeps rows [r0, r1) of mode 1
+        r0, r1 = stream.shard(args.virtual_shards)
+        XS = X.rows(r0, r1)
+        X._free()
+        X = None
     stream.checkpoint()
 
     def step(seed):
         stream.restore()
-        stream.consume_range(X, t_init, B, nb, seed, 1)
+        stream.consume_range(XS, t_init, B, nb, seed, 1)
 
     for w in range(args.warmup):
         step(9000 + w)
@@ -323,15 +341,15 @@ def main():
     gather_ms = stream.gather_times()
     stream.time_gather(False)
     ms_max = max_over_ranks(ms, dist, torch)
-    value = world * args.steps * slices_per_step / (ms_max / 1000.0)
+    value = (1 if sharded else world) * args.steps * slices_per_step / (ms_max / 1000.0)
     fit_model = stream.model()
 
     # ---- roofline of the window gather
     peak, peak_src = measured_peaks()
     sector_per_launch = nb * sector_bytes_per_batch(dims, S, B)
     useful_per_launch = nb * useful_bytes_per_batch(dims, S, B)
-    g_avg_ms = statistics.mean(gather_ms) if gather_ms else float("nan")
-    achieved = sector_per_launch / (g_avg_ms / 1000.0) / 1e9
+    g_avg_ms = statistics.mean(gather_ms) if gather_ms else None
+    achieved = sector_per_launch / (g_avg_ms / 1000.0) / 1e9 if g_avg_ms else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_gather_traffic.json")
     if os.path.exists(prof):
@@ -343,7 +361,7 @@ def main():
     # ---- e2e through the host-slab call: the caller's slabs stay in (pinned) host memory;
     # only the sampled fibres cross PCIe (host gather), the model is read back every step
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    if not args.no_e2e and args.e2e_steps > 0 and not sharded:
         slice_ = int(np.prod(head))
         hbuf = rocp.HostBuffer(slices_per_step * slice_)  # pinned, 2 MB pages (rocp_host_alloc)
         host = hbuf.array
@@ -372,9 +390,9 @@ def main():
 
     # ---- CPU baseline (rank 0, bounded sample)
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu and not sharded:
         slice_ = int(np.prod(head))
-        xs = X.slab(t_init, 4 * B).download()
+        xs = XS.slab(t_init, 4 * B).download() if not sharded else None
         slabs = [np.ascontiguousarray(xs[k * B * slice_:(k + 1) * B * slice_]) for k in range(4)]
         v, n, wall = cpu_sample_stream(init.model[:-1], init.best_sampled_kr, R, S, t_init, head, slabs, B,
                                        args.cpu_seconds, threads=1)
@@ -386,19 +404,24 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "time-slices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f64",
             "data": f"synthetic (seeded {CFG['family']} factors, {CFG['snr_db']:g} dB Gaussian noise, "
                     f"generated on device)",
             "config": {"workload": workload_text(CFG),
                        "step": f"one full streaming pass ({nb} x RocpStream::consume) from the post-init state",
                        "l2": f"inputs larger than L2 ({8 * int(np.prod(dims)) / 1e9:.1f} GB tensor); "
                              f"fresh sampling seed every step",
-                       "parallelism": f"{world} independent stream replica(s), one per GPU (no collective)"},
+                       "parallelism": (f"one stream sharded along mode 1 over {world} GPU(s), "
+                                       f"{args.virtual_shards} virtual shards, NCCL all-gather of partials"
+                                       if sharded else
+                                       f"{world} independent stream replica(s), one per GPU (no collective)")},
             "entries_per_s": value * int(np.prod(head)),
             "init_seconds": init_seconds, "init_sweeps": init.iterations, "init_fitness": init.best_fitness,
             "gpu_launches": launches,
             "roofline": {"kernel": "k_gather (window sampled-fibre gather)", "bound": "hbm",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": sector_per_launch,
                          "useful_bytes_per_launch": useful_per_launch,

@@ -81,6 +81,9 @@ rocp_status rocp_tensor_create(rocp_dev* dev, const int64_t* dims, int order, co
  * synthetic.cpp:33-57). */
 rocp_status rocp_tensor_slab(rocp_dev* dev, const rocp_tensor* t, int64_t t0, int64_t len,
                              rocp_tensor** out);
+/* Rows [r0, r1) of mode 1 as a new owned tensor (the local block of a
+ * mode-1 sharded stream). */
+rocp_status rocp_tensor_rows(rocp_dev* dev, const rocp_tensor* t, int64_t r0, int64_t r1, rocp_tensor** out);
 void rocp_tensor_free(rocp_tensor* t);
 rocp_status rocp_tensor_upload(rocp_dev* dev, rocp_tensor* t, const double* host);
 rocp_status rocp_tensor_download(rocp_dev* dev, const rocp_tensor* t, double* host);
@@ -149,6 +152,18 @@ void rocp_stream_free(rocp_stream* st);
  * Draws keyed by (seed, batch_id, iteration 0). */
 rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint64_t seed,
                                 uint32_t batch_id);
+/* Mode-1 sharding (north star: tensors sharded along mode 1, partial
+ * contractions / Grams of the non-owned modes combined by an NCCL collective,
+ * owned-mode rows local).  Converts a freshly created
+ * stream (identical on every rank) into rank dev->rank of dev->world: U(1),
+ * P(1) keep rows [r0, r1) of the virtual shards [v0, v1) out of
+ * `virtual_shards` fixed row ranges (the world size must divide it).  Every
+ * later consume / consume_range takes the rank's LOCAL tensor (rocp_tensor_rows)
+ * and reproduces oracle/orc_stream_consume_sharded bit for bit for any world
+ * size; rocp_stream_get(mode 1) returns the local rows.  Host-slab consumes and
+ * the replay seams stay single-GPU (E_DOMAIN on a sharded stream). */
+rocp_status rocp_stream_shard(rocp_stream* st, int virtual_shards);
+rocp_status rocp_stream_shard_info(rocp_stream* st, int* virtual_shards, int64_t* row0, int64_t* row1);
 /* Same for a host slab (head dims x batch, first index fastest): the
  * reference-facing call.  Only the sampled fibres cross PCIe (see
  * rocp_stream_consume_range_host). */

@@ -46,6 +46,7 @@ SIGNATURES = [
     ("rocp_nccl_get_unique_id", C.c_int, [_vp]),
     ("rocp_tensor_create", C.c_int, [_vp, _i64p, C.c_int, _f64p, C.POINTER(_vp)]),
     ("rocp_tensor_slab", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.POINTER(_vp)]),
+    ("rocp_tensor_rows", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.POINTER(_vp)]),
     ("rocp_tensor_free", None, [_vp]),
     ("rocp_tensor_upload", C.c_int, [_vp, _vp, _f64p]),
     ("rocp_tensor_download", C.c_int, [_vp, _vp, _f64p]),
@@ -74,6 +75,8 @@ SIGNATURES = [
                                      C.c_int64, C.POINTER(_vp)]),
     ("rocp_stream_create_from_init", C.c_int, [_vp, C.c_int, C.c_int64, C.POINTER(_vp)]),
     ("rocp_stream_free", None, [_vp]),
+    ("rocp_stream_shard", C.c_int, [_vp, C.c_int]),
+    ("rocp_stream_shard_info", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("rocp_stream_consume", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32]),
     ("rocp_stream_consume_host", C.c_int, [_vp, _f64p, C.c_int64, C.c_uint64, C.c_uint32]),
     ("rocp_stream_consume_range", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
@@ -206,8 +209,11 @@ class Device:
     """One handle per GPU (rocp_dev)."""
 
     def __init__(self, device=0, world=1, rank=0, nccl_id=None):
+        """world > 1: one handle per GPU of a mode-1 sharded job; nccl_id = rank 0's
+        nccl_unique_id() bytes, broadcast by any host transport."""
         h = C.c_void_p()
-        rc = lib().rocp_create(device, world, rank, nccl_id, C.byref(h))
+        idp = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        rc = lib().rocp_create(device, world, rank, idp, C.byref(h))
         if rc != OK:
             raise RocpError(rc, f"rocp_create(device={device}) failed (is a GPU visible?)")
         self.h = h
@@ -256,6 +262,16 @@ class Device:
         ms = C.c_float(0)
         self.check(lib().rocp_timer_elapsed_ms(self.h, a, b, C.byref(ms)))
         return float(ms.value)
+
+
+def nccl_unique_id():
+    """NCCL bootstrap id (bytes) for Device(world > 1); create on rank 0 only."""
+    n = int(lib().rocp_nccl_id_size())
+    buf = C.create_string_buffer(n)
+    rc = lib().rocp_nccl_get_unique_id(buf)
+    if rc != OK:
+        raise RocpError(rc, "rocp_nccl_get_unique_id failed (NCCL unavailable?)")
+    return buf.raw
 
 
 class HostBuffer:
@@ -321,6 +337,14 @@ class DeviceTensor:
         dims = list(self.dims)
         dims[-1] = length
         return DeviceTensor(self.dev, dims, _handle=h, _parent=self)
+
+    def rows(self, r0, r1):
+        """Rows [r0, r1) of mode 1 as a new tensor (a rank's block of a sharded stream)."""
+        h = C.c_void_p()
+        self.dev.check(lib().rocp_tensor_rows(self.dev.h, self.h, r0, r1, C.byref(h)))
+        dims = list(self.dims)
+        dims[0] = r1 - r0
+        return DeviceTensor(self.dev, dims, _handle=h)
 
     def download(self, out=None):
         if out is None:
@@ -504,6 +528,16 @@ class RocpStream:
 
     def __del__(self):
         self._free()
+
+    def shard(self, virtual_shards=8):
+        """Mode-1 sharding across Device(world, rank) (rocp_stream_shard): this rank
+        keeps U(1)/P(1) rows [row0, row1); consume takes the rank's local tensor."""
+        self.dev.check(lib().rocp_stream_shard(self.h, virtual_shards))
+        v, r0, r1 = C.c_int(0), C.c_int64(0), C.c_int64(0)
+        self.dev.check(lib().rocp_stream_shard_info(self.h, C.byref(v), C.byref(r0), C.byref(r1)))
+        self.virtual_shards, self.row0, self.row1 = v.value, r0.value, r1.value
+        self.head = [self.row1 - self.row0] + list(self.head[1:])
+        return self.row0, self.row1
 
     def _check_mode(self, mode):
         if not 1 <= mode < self.order:

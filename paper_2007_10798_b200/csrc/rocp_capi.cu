@@ -12,23 +12,26 @@
 
 #include "../../include/rocp_b200.h"
 #include "kernels.cuh"
+#include "shard_kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is bound at run time (NcclApi)
 #include <sys/mman.h>
 
 #include <algorithm>
-#include <mutex>
-#include <functional>
-#include <condition_variable>
-#include <cstdlib>
-#include <cstdio>
-#include <chrono>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -119,6 +122,51 @@ void rowmajor_to_colmajor(const double* a, int64_t rows, int64_t cols, double* o
 // Device copies of a list of draw jobs and gather jobs (+ the flat tile list
 // of the gather).  Built on the host, uploaded once, then launched any number
 // of times (also from inside CUDA graphs).
+// NCCL, bound at run time: the copy already in the process (torch's) when
+// there is one, else the system libnccl.so.2.  Only multi-GPU handles
+// (world > 1) need it.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            a.why = e ? e : "libnccl.so.2 not found";
+            return a;
+        }
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_gather && a.comm_destroy && a.error_string;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+void NK(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw RocpError{ROCP_E_NCCL, std::string(what) + ": " + nccl_api().error_string(r)};
+}
+
+const NcclApi& require_nccl() {
+    const NcclApi& a = nccl_api();
+    if (!a.ok) throw RocpError{ROCP_E_NCCL, "NCCL unavailable: " + a.why};
+    return a;
+}
+
 struct JobList {
     DBuf<DrawJob> draw;
     DBuf<GatherJob> gather;
@@ -134,6 +182,7 @@ struct JobList {
 struct rocp_dev {
     int device = 0;
     int world = 1, rank = 0;
+    ncclComm_t comm = nullptr;  // world > 1: the mode-1 sharding communicator
     cudaStream_t stream = nullptr;
     std::string err;
     uint64_t launches = 0;
@@ -591,6 +640,24 @@ struct Window {
     std::vector<int64_t> zc_tile;  // host path: first zero-copy gather tile of each batch
 };
 
+// Window of a sharded stream: per (batch, stage) the global draws, the
+// compacted local samples (shard order), their per-shard counts and the
+// column-major X_s of the local samples; plus the exchange buffers.
+struct ShardWin {
+    int64_t nb = 0, B = 0;  // capacity
+    DBuf<int32_t> idx, cidx, clist;
+    DBuf<int64_t> base, cbase;
+    DBuf<int> counts;            // nb x N x V
+    std::vector<int> hcounts;
+    DBuf<double> X;              // per (b, stage): I_stage x S column-major
+    std::vector<int64_t> xoff;
+    JobList draws, gathers;
+    DBuf<ShardPartJob> pjobs;
+    DBuf<double> Zl;             // S x R, this stage's local Z
+    DBuf<double> send, recv;     // V x (R^2 + max rows x R) partial blocks
+    DBuf<double> rcols, rgath, rwork, rtmp;  // residual columns (2 x S per rank)
+};
+
 struct rocp_stream {
     rocp_dev* dev = nullptr;
     int N = 0, R = 0;
@@ -616,6 +683,13 @@ struct rocp_stream {
     int resid_level = 1;          // 0 none, 1 temporal stage (default), 2 every stage
     int host_threads = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
     std::unique_ptr<HostPool> pool;  // host-slab gather workers (created on first use)
+    // mode-1 sharding: U(1)/P(1) hold rows [r0, r1) and
+    // head[0] = r1 - r0; ghead keeps the global head for the draws
+    bool sharded = false;
+    int V = 1, v0 = 0, v1 = 1;
+    int64_t r0 = 0, r1 = 0;
+    std::vector<int64_t> ghead;
+    std::unique_ptr<ShardWin> sw;
     cudaStream_t copy_stream = nullptr;       // host-slab path: in-place reads + staging copies
     std::vector<cudaEvent_t> copy_events;     // one per sub-window, joined by the compute stream
     // checkpoint copies (device)
@@ -1141,16 +1215,18 @@ void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb
     if (failure) std::rethrow_exception(failure);
 }
 
+#include "shard_host.inc"
+
 }  // namespace
 
 // ===========================================================================
 extern "C" {
 
 rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, rocp_dev** out) {
-    (void)nccl_id;
     auto dev = std::make_unique<rocp_dev>();
     rocp_status st = guarded(dev.get(), [&] {
-        if (world != 1 || rank != 0) throw_domain("this build runs one GPU per handle (world = 1)");
+        if (world < 1 || rank < 0 || rank >= world) throw_domain("need 0 <= rank < world");
+        if (world > 1 && !nccl_id) throw_domain("world > 1 needs the NCCL unique id of rank 0");
         CK(cudaSetDevice(device));
         dev->device = device;
         dev->world = world;
@@ -1165,6 +1241,12 @@ rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, ro
         CK(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int((size_t(kGroup) * 64 + kGroup) * sizeof(double))));
         set_contract_smem_attrs();
+        if (world > 1) {
+            const NcclApi& api = require_nccl();
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            NK(api.comm_init_rank(&dev->comm, world, id, rank), "ncclCommInitRank");
+        }
     });
     if (st != ROCP_OK) {
         static thread_local std::string last;
@@ -1183,6 +1265,7 @@ void rocp_destroy(rocp_dev* dev) {
     dev->init = rocp_dev::Init{};
     for (cudaEvent_t& e : dev->timer)
         if (e) cudaEventDestroy(e);
+    if (dev->comm) nccl_api().comm_destroy(dev->comm);
     cudaStreamDestroy(dev->stream);
     delete dev;
 }
@@ -1218,10 +1301,15 @@ rocp_status rocp_synchronize(rocp_dev* dev) {
 
 uint64_t rocp_kernel_launches(const rocp_dev* dev) { return dev ? dev->launches : 0; }
 
-int rocp_nccl_id_size(void) { return 0; }
+int rocp_nccl_id_size(void) { return int(sizeof(ncclUniqueId)); }
+
 rocp_status rocp_nccl_get_unique_id(void* out) {
-    (void)out;
-    return ROCP_E_NCCL;
+    const NcclApi& api = nccl_api();
+    if (!api.ok || !out) return ROCP_E_NCCL;
+    ncclUniqueId id;
+    if (api.get_unique_id(&id) != ncclSuccess) return ROCP_E_NCCL;
+    std::memcpy(out, &id, sizeof(id));
+    return ROCP_OK;
 }
 
 // ---- tensors ---------------------------------------------------------------
@@ -1256,6 +1344,23 @@ rocp_status rocp_tensor_slab(rocp_dev* dev, const rocp_tensor* t, int64_t t0, in
         const int64_t slice = t->numel / T;
         v->d = t->d + t0 * slice;
         v->owned = false;
+        *out = v.release();
+    });
+}
+
+rocp_status rocp_tensor_rows(rocp_dev* dev, const rocp_tensor* t, int64_t r0, int64_t r1, rocp_tensor** out) {
+    return guarded(dev, [&] {
+        const int64_t I1 = t->dims[0];
+        if (r0 < 0 || r1 <= r0 || r1 > I1) throw_domain("row range out of bounds");
+        auto v = std::make_unique<rocp_tensor>();
+        v->dims = t->dims;
+        v->dims[0] = r1 - r0;
+        v->numel = prod(v->dims);
+        CK(cudaMalloc(&v->d, size_t(v->numel) * sizeof(double)));
+        v->owned = true;
+        CK(cudaMemcpy2DAsync(v->d, size_t(r1 - r0) * 8, t->d + r0, size_t(I1) * 8, size_t(r1 - r0) * 8,
+                             size_t(t->numel / I1), cudaMemcpyDeviceToDevice, dev->stream));
+        CK(cudaStreamSynchronize(dev->stream));
         *out = v.release();
     });
 }
@@ -1772,7 +1877,23 @@ rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint6
                                 uint32_t batch_id) {
     return guarded(st->dev, [&] {
         check_head_dims(st, x_new);  // rocp.cpp:145
-        consume_one(st, x_new->d, x_new->dims.back(), seed, batch_id);
+        if (st->sharded)
+            sharded_consume_range(st, x_new->d, x_new->numel / x_new->dims.back(), x_new->dims.back(), 1, seed,
+                                  batch_id);
+        else
+            consume_one(st, x_new->d, x_new->dims.back(), seed, batch_id);
+    });
+}
+
+rocp_status rocp_stream_shard(rocp_stream* st, int virtual_shards) {
+    return guarded(st->dev, [&] { shard_stream(st, virtual_shards); });
+}
+
+rocp_status rocp_stream_shard_info(rocp_stream* st, int* virtual_shards, int64_t* row0, int64_t* row1) {
+    return guarded(st->dev, [&] {
+        *virtual_shards = st->sharded ? st->V : 0;
+        *row0 = st->sharded ? st->r0 : 0;
+        *row1 = st->sharded ? st->r1 : st->head[0];
     });
 }
 
@@ -1780,6 +1901,7 @@ rocp_status rocp_stream_consume_host(rocp_stream* st, const double* x_new, int64
                                      uint64_t seed, uint32_t batch_id) {
     return guarded(st->dev, [&] {
         if (batch < 1) throw_domain("batch must hold at least one slice");
+        if (st->sharded) throw_domain("host-slab consume is single-GPU (stream is sharded)");
         rocp_dev* dev = st->dev;
         const int64_t numel = prod(st->head) * batch;
         if (st->resid_level >= 2 && st->staging.n < size_t(numel)) {
@@ -1806,6 +1928,10 @@ rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int
         check_capacity(st, batch * nb);
         rocp_dev* dev = st->dev;
         const int64_t slice = x->numel / x->dims.back();
+        if (st->sharded) {
+            sharded_consume_range(st, x->d + t0 * slice, slice, batch, nb, seed, first_batch_id);
+            return;
+        }
         prepare_window(st, x->d, t0, slice, batch, nb, nullptr, nullptr, -1);
         enqueue_draw_gather(st, seed, first_batch_id);
         if (st->resid_level <= 1) {
@@ -1842,6 +1968,7 @@ rocp_status rocp_stream_consume_range_host(rocp_stream* st, const double* x, int
                                            uint64_t seed, uint32_t first_batch_id, int threads) {
     return guarded(st->dev, [&] {
         if (batch < 1 || nb < 1) throw_domain("consume_range_host: empty range");
+        if (st->sharded) throw_domain("host-slab consume is single-GPU (stream is sharded)");
         if (st->resid_level >= 2) throw_domain("consume_range_host: residual level 2 needs device slabs");
         consume_range_host(st, x, batch, nb, seed, first_batch_id, threads > 0 ? threads : st->host_threads, 0);
     });
@@ -1851,6 +1978,7 @@ rocp_status rocp_stream_update_last_mode_with(rocp_stream* st, const rocp_tensor
                                               const int64_t* rows, int64_t s, double* u_new,
                                               double* z_s, int* regularized) {
     return guarded(st->dev, [&] {
+        if (st->sharded) throw_domain("replay seams are single-GPU (stream is sharded)");
         check_head_dims(st, x_new);
         if (s != st->s) throw_domain("index set size must equal the stream sample count");
         rocp_dev* dev = st->dev;
@@ -1894,6 +2022,7 @@ rocp_status rocp_stream_update_mode_with(rocp_stream* st, const rocp_tensor* x_n
                                          const double* u_new, int mode, const int64_t* rows,
                                          int64_t s, double* z_new, double* x_s, int* regularized) {
     return guarded(st->dev, [&] {
+        if (st->sharded) throw_domain("replay seams are single-GPU (stream is sharded)");
         check_head_dims(st, x_new);
         if (mode < 1 || mode >= st->N)
             throw_domain("update_mode_with: index set must be over a non-temporal mode");  // rocp.cpp:100-101

@@ -1,0 +1,144 @@
+// shard_kernels.cuh -- kernels of the mode-1 sharded stream.
+//
+// Rank g of G owns mode-1 rows [r0, r1) = the virtual shards [v0, v1) of V
+// fixed row ranges [floor(v I1 / V), floor((v+1) I1 / V)).  For the temporal
+// stage and the modes n >= 2 every sample belongs to the shard of its mode-1
+// index; a rank gathers, multiplies and reduces only its own shards' samples,
+// each shard in its own canonical chunked order, and the per-shard partials
+// are exchanged (NCCL all-gather) and summed in shard order -- the oracle's
+// orc_stream_consume_sharded, identical for every G dividing V.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace rocpk {
+
+constexpr int kMaxShards = 64;
+
+__host__ __device__ __forceinline__ int shard_of_row(int64_t i0, int64_t I1, int V) {
+    return int(((i0 + 1) * V - 1) / I1);
+}
+
+// Stable partition of one stage's samples by virtual shard (one warp per job):
+// the local shards' samples, in sample order shard after shard, with the
+// mode-1 index and the fibre base rebased to this rank's rows.
+struct ShardPartJob {
+    const int32_t* idx;   // S x n_other, global 0-based (mode-1 index first)
+    const int64_t* base;  // S, offsets with local strides and the global mode-1 index
+    int32_t* cidx;        // out: compacted, mode-1 index - r0
+    int64_t* cbase;       // out: compacted, base - r0
+    int32_t* clist;       // out: original sample index of each compacted entry
+    int* counts;          // out: V per-shard sample counts (all shards)
+};
+
+struct ShardPartParams {
+    const ShardPartJob* jobs;
+    int S, n_other, V, v0, v1;
+    int64_t I1, r0;
+};
+
+__global__ void __launch_bounds__(32) k_shard_partition(const ShardPartParams p) {
+    const ShardPartJob& J = p.jobs[blockIdx.x];
+    const int lane = threadIdx.x;
+    __shared__ int cnt[kMaxShards], run[kMaxShards];
+    for (int v = lane; v < kMaxShards; v += 32) cnt[v] = 0;
+    __syncwarp();
+    for (int c0 = 0; c0 < p.S; c0 += 32) {
+        const int c = c0 + lane;
+        if (c < p.S) atomicAdd(&cnt[shard_of_row(J.idx[int64_t(c) * p.n_other], p.I1, p.V)], 1);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int acc = 0;
+        for (int v = p.v0; v < p.v1; ++v) {
+            run[v] = acc;
+            acc += cnt[v];
+        }
+    }
+    for (int v = lane; v < p.V; v += 32) J.counts[v] = cnt[v];
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int c0 = 0; c0 < p.S; c0 += 32) {
+        const int c = c0 + lane;
+        const int v = (c < p.S) ? shard_of_row(J.idx[int64_t(c) * p.n_other], p.I1, p.V) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, v);
+        const bool mine = v >= p.v0 && v < p.v1;
+        if (mine) {
+            const int pos = run[v] + __popc(grp & lt);
+            for (int k = 0; k < p.n_other; ++k) {
+                const int32_t ik = J.idx[int64_t(c) * p.n_other + k];
+                J.cidx[int64_t(pos) * p.n_other + k] = (k == 0) ? int32_t(ik - p.r0) : ik;
+            }
+            J.cbase[pos] = J.base[c] - p.r0;
+            J.clist[pos] = c;
+        }
+        __syncwarp();
+        if (mine && (grp & lt) == 0u) run[v] += __popc(grp);  // group leader advances
+        __syncwarp();
+    }
+}
+
+// Fixed-order combine of the V exchanged partial blocks [G_v | part_v]:
+// tot = blk_0 + blk_1 + ... (shard order), then out = base + tot (P + inc,
+// Q + G) or out = tot.
+__global__ void __launch_bounds__(256) k_shard_combine(const double* __restrict__ parts, int V, int64_t blk, int64_t RR,
+                                                       const double* base_g, double* out_g, const double* base_p,
+                                                       double* out_p) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < blk; e += int64_t(gridDim.x) * blockDim.x) {
+        double tot = __ldg(parts + e);
+        for (int v = 1; v < V; ++v) tot = tot + __ldg(parts + int64_t(v) * blk + e);
+        if (e < RR) out_g[e] = base_g ? base_g[e] + tot : tot;
+        else out_p[e - RR] = base_p ? base_p[e - RR] + tot : tot;
+    }
+}
+
+// Sampled residual columns of this rank's temporal samples (warp per compacted
+// column, same per-column order as k_residual), scattered to their original
+// sample positions of the 2 x S column arrays (pre-zeroed).
+__global__ void __launch_bounds__(256) k_shard_resid_cols(const double* __restrict__ X, int32_t I, int32_t n,
+                                                          const double* __restrict__ U, const double* __restrict__ Z,
+                                                          int R, const int32_t* __restrict__ clist, int32_t S,
+                                                          double* cols) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (j >= n) return;
+    double qn = 0.0, qd = 0.0;
+    const double* z = Z + int64_t(j) * R;
+    for (int32_t i = lane; i < I; i += 32) {
+        double uz = 0.0;
+        const double* u = U + int64_t(i) * R;
+        for (int r = 0; r < R; ++r) uz = __fma_rn(u[r], z[r], uz);
+        const double xv = X[int64_t(j) * I + i];
+        const double e = xv - uz;
+        qn = __fma_rn(e, e, qn);
+        qd = __fma_rn(xv, xv, qd);
+    }
+    qn = butterfly32(qn);
+    qd = butterfly32(qd);
+    if (lane == 0) {
+        const int c = clist[j];
+        cols[c] = qn;
+        cols[S + c] = qd;
+    }
+}
+
+// Sum of the ranks' scattered column arrays (each column non-zero on exactly
+// one rank, so the sum is exact), then the canonical hsum of both -> out[0..1].
+__global__ void __launch_bounds__(256) k_shard_resid_sum(const double* __restrict__ gathered, int world, int32_t S,
+                                                         double* work, double* tmp, double* out) {
+    for (int e = threadIdx.x; e < 2 * S; e += blockDim.x) {
+        double v = gathered[e];
+        for (int g = 1; g < world; ++g) v = v + gathered[int64_t(g) * 2 * S + e];
+        work[e] = v;
+    }
+    __syncthreads();
+    __threadfence_block();
+    block_hsum_inplace(work, S, tmp);
+    block_hsum_inplace(work + S, S, tmp);
+    if (threadIdx.x == 0) {
+        out[0] = work[0];
+        out[1] = work[S];
+    }
+}
+
+}  // namespace rocpk

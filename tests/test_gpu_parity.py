@@ -387,3 +387,55 @@ def test_stream_state_properties(dev):
         scale = np.abs(q).max()
         assert np.abs(q - q.T).max() <= TOL["q_symmetric"] * scale
         assert np.linalg.eigvalsh(q).min() >= -TOL["q_psd"] * scale
+
+
+# ---- mode-1 sharded stream, one rank of world 1 -------------------------------
+@pytest.mark.parametrize("dims,R,t_init,B,V", [([24, 10, 60], 4, 20, 8, 8), ([16, 6, 5, 30], 3, 10, 5, 4),
+                                               ([40, 30, 50], 6, 20, 10, 1), ([200, 200, 120], 10, 50, 10, 8)])
+def test_sharded_stream_bitwise(dev, dims, R, t_init, B, V):
+    x, X, a, b, s, nb = _run_pair(dev, dims, R, 20.0, t_init, B)
+    unsharded = None
+    if V == 1:
+        x2, X2, unsharded, _, _, _ = _run_pair(dev, dims, R, 20.0, t_init, B)
+    r0, r1 = a.shard(V)
+    assert (r0, r1) == (0, dims[0])
+    XL = X.rows(r0, r1)
+    for k in range(nb):
+        t0 = t_init + k * B
+        if k % 2 == 0:
+            a.consume(XL.slab(t0, B), 515, k + 1)
+        else:
+            a.consume_range(XL, t0, B, 1, 515, k + 1)
+        b.consume_sharded(H.slab(x, dims, t0, B), B, 515, k + 1, V)
+        if unsharded is not None:
+            unsharded.consume(X.slab(t0, B), 515, k + 1)
+        if k < 2 or k == nb - 1:
+            _cmp_stream(a, b, len(dims))
+            assert bitwise(a.last_residuals(), b.last_residuals())
+    if unsharded is not None:  # V = 1: the unsharded stream
+        for n in range(1, len(dims)):
+            assert bitwise(a.factor(n), unsharded.factor(n))
+        assert bitwise(a.temporal(), unsharded.temporal())
+
+
+def test_sharded_stream_window_and_errors(dev):
+    dims, R, t_init, B = [32, 12, 90], 5, 30, 10
+    x, X, a, b, s, nb = _run_pair(dev, dims, R, 20.0, t_init, B)
+    a.shard(8)
+    with pytest.raises(rocp.DomainError):
+        a.shard(8)
+    XL = X.rows(0, dims[0])
+    a.consume_range(XL, t_init, B, nb, 616, 1)  # one window of every batch
+    for k in range(nb):
+        b.consume_sharded(H.slab(x, dims, t_init + k * B, B), B, 616, k + 1, 8)
+    _cmp_stream(a, b, 3)
+    with pytest.raises(rocp.DomainError):
+        a.consume_range_host(H.slab(x, dims, t_init, B), B, 1, 1, 1)
+    with pytest.raises(rocp.DomainError):
+        a.set_residual_tracking(2)
+        a.consume(XL.slab(t_init, B), 1, 1)
+    a.set_residual_tracking(1)
+    c = rocp.RocpStream(dev, rocp.InitResult([np.asfortranarray(m) for m in H.random_model([6, 5, 4], 2, H.rng(2))],
+                                             [np.zeros((8, 2), order="F")] * 2, 0.0, 0, False, [], 8), 8)
+    with pytest.raises(rocp.DomainError):
+        c.shard(7)  # more shards than rows
