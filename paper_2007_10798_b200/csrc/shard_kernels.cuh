@@ -78,6 +78,89 @@ __global__ void __launch_bounds__(32) k_shard_partition(const ShardPartParams p)
     }
 }
 
+// Per-shard partials of one stage in ONE launch: for every local shard
+// segment (its samples contiguous in the compacted order) the Gram Z_v^T Z_v
+// and the contraction X_v Z_v, each output by one thread in the canonical
+// chunked order over the segment (32-sample fma chains from +0.0, superchunk
+// and total sums in order) -- the arithmetic of k_gram / k_contract on the
+// segment.  Work item = (segment, Gram output) or (segment, row, 8 outputs).
+struct SegPartParams {
+    const double* Z;      // n_local x R row-major (compacted order)
+    const double* X;      // rows x n_local column-major
+    int64_t rows;
+    int R, nseg;
+    int64_t blk;          // R*R + rows*R doubles per slot
+    double* slots;        // nseg slots [G_v | part_v]
+    int32_t off[kMaxShards + 1];  // segment starts in the compacted order
+};
+
+constexpr int kSegRG = 8;  // contraction outputs per work item
+
+__device__ __forceinline__ void seg_dot8(const double* __restrict__ X, const double* __restrict__ Z, int64_t rows,
+                                         int R, int64_t i, int r0, int nr, int c0, int n, double* out) {
+    double tot[kSegRG], q[kSegRG], pk[kSegRG];
+#pragma unroll
+    for (int j = 0; j < kSegRG; ++j) tot[j] = q[j] = 0.0;
+    for (int m0 = 0; m0 < n; m0 += kSuperSamples) {
+        const int m1 = min(n, m0 + kSuperSamples);
+        for (int k0 = m0; k0 < m1; k0 += kChunk) {
+            const int k1 = min(m1, k0 + kChunk);
+#pragma unroll
+            for (int j = 0; j < kSegRG; ++j) pk[j] = 0.0;
+            for (int c = k0; c < k1; ++c) {
+                const double x = __ldg(X + int64_t(c0 + c) * rows + i);
+                const double* z = Z + int64_t(c0 + c) * R + r0;
+#pragma unroll
+                for (int j = 0; j < kSegRG; ++j)
+                    if (j < nr) pk[j] = __fma_rn(x, __ldg(z + j), pk[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < kSegRG; ++j) q[j] = (k0 == m0) ? pk[j] : q[j] + pk[j];
+        }
+#pragma unroll
+        for (int j = 0; j < kSegRG; ++j) tot[j] = (m0 == 0) ? q[j] : tot[j] + q[j];
+    }
+#pragma unroll
+    for (int j = 0; j < kSegRG; ++j)
+        if (j < nr) out[i * R + r0 + j] = tot[j];
+}
+
+__global__ void __launch_bounds__(256) k_seg_partials(const SegPartParams p) {
+    const int R = p.R;
+    const int64_t RR = int64_t(R) * R;
+    const int ngr = (R + kSegRG - 1) / kSegRG;
+    const int64_t per_seg = RR + p.rows * ngr;  // work items per segment
+    const int64_t total = per_seg * p.nseg;
+    for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
+        const int v = int(w / per_seg);
+        const int64_t t = w - int64_t(v) * per_seg;
+        const int c0 = p.off[v], n = p.off[v + 1] - c0;
+        double* slot = p.slots + int64_t(v) * p.blk;
+        if (t < RR) {  // Gram output (r1, r2), symmetric storage like k_gram
+            const int r1 = int(t % R), r2 = int(t / R);
+            double tot = 0.0, q = 0.0;
+            for (int m0 = 0; m0 < n; m0 += kSuperSamples) {
+                const int m1 = min(n, m0 + kSuperSamples);
+                for (int k0 = m0; k0 < m1; k0 += kChunk) {
+                    const int k1 = min(m1, k0 + kChunk);
+                    double pk = 0.0;
+                    for (int c = k0; c < k1; ++c)
+                        pk = __fma_rn(__ldg(p.Z + int64_t(c0 + c) * R + r1), __ldg(p.Z + int64_t(c0 + c) * R + r2), pk);
+                    q = (k0 == m0) ? pk : q + pk;
+                }
+                tot = (m0 == 0) ? q : tot + q;
+            }
+            slot[t] = tot;
+        } else {  // contraction outputs (i, r0 .. r0 + 7)
+            const int64_t u = t - RR;
+            const int64_t i = u % p.rows;
+            const int g = int(u / p.rows);
+            const int r0 = g * kSegRG, nr = min(kSegRG, R - r0);
+            seg_dot8(p.X, p.Z, p.rows, R, i, r0, nr, c0, n, slot + RR);
+        }
+    }
+}
+
 // Fixed-order combine of the V exchanged partial blocks [G_v | part_v]:
 // tot = blk_0 + blk_1 + ... (shard order), then out = base + tot (P + inc,
 // Q + G) or out = tot.
