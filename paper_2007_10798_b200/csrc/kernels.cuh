@@ -851,6 +851,7 @@ struct ChainParams {
     double* zbuf;             // nb x S x RP: the temporal Z of each batch (window residual pass)
     double* gch;              // N x S x RP: Z of the mode stages
     double* gpart;            // nsuper x R x R Gram superchunk partials
+    double* chpart;           // nchunks x R x R Gram chunk partials (phase 0)
     double* cpart;            // nsuper x rows x R
     double* LD;               // R x R (L(i,k) at [k*R + i], i > k) + R (D)
     int* mode_flag;           // [0]: 0 = zero solution, 1 = solve
@@ -949,16 +950,24 @@ __device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double l
 // Canonical LDL^T for R <= MAXR <= 32 by ONE warp, no block barriers: lane i
 // holds row i of the lower triangle in registers.  Step k: d_k = lane k's
 // r[k] (final), l(i,k) = r[k] / d_k on lanes i > k, then r[j] = fma(-l(i,k),
-// a(j,k), r[j]) for k < j <= i with a(j,k) = lane j's r[k] broadcast by a
-// shuffle.  Identical per-element operation sequence to ldlt_one_sync /
-// k_solve / the oracle.  L(i,k) at A[k*kLdStride + i], D in D[].
+// a(j,k), r[j]) for k < j <= i with a(j,k) = lane j's r[k].  Identical
+// per-element operation sequence to ldlt_one_sync / k_solve / the oracle.
+// L(i,k) at A[k*kLdStride + i], D in D[].
+//
+// Software-pipelined so a step's critical path is divide -> the single fma
+// that finishes the next pivot column entry -> shuffle of d_{k+1}: the other
+// updates of step k (j >= k+2) are deferred to step k+1, where they fill the
+// shuffle latency before the next divide, and column k+1 is read from shared
+// memory (published one step ahead) while the divide runs.  Upper-triangle
+// registers and lanes >= R receive harmless updates but are never read as
+// lower entries; dividends of inactive lanes are 1.0 (a zero dividend takes
+// the divide's slow path).
 template <int MAXR>
 __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, double* A, double* D, double* col) {
-    // Upper-triangle registers (j > lane) and lanes >= R receive harmless
-    // updates but are never read as lower entries.  d_k travels by shuffle
-    // (critical path); the column a(., k) is published to shared memory one
-    // step ahead so its loads overlap the divide.  Dividends of inactive
-    // lanes are 1.0: a zero dividend would take the divide's slow path.
+    // col: three 32-entry column buffers; column k lives in col[(k % 3) * 32]
+    // from step k-1 (published) to step k+1 (read by the deferred updates).
+    // The fmas read the broadcast column straight from shared memory (no
+    // register copy, which the compiler would place in local memory).
     const int lane = threadIdx.x & 31;
     double r[MAXR];
 #pragma unroll
@@ -966,24 +975,32 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
         r[j] = (lane < R && j <= lane) ? ((j == lane) ? G[lane + j * R] + lambda : G[lane + j * R]) : 0.0;
     col[lane] = r[0];
     __syncwarp();
+    double dk = __shfl_sync(0xffffffffu, r[0], 0);
+    double lp = 0.0;  // l(lane, k-1)
 #pragma unroll
     for (int k = 0; k < MAXR; ++k) {
         if (k < R) {
-            const double* cb = col + (k & 1) * 32;
-            const double dk = __shfl_sync(0xffffffffu, r[k], k);
-            double ajk[MAXR];
+            const double* cb = col + (k % 3) * 32;  // column k
+            if (k > 0) {  // deferred updates of step k-1 (j >= k+1): fill the shuffle latency
+                const double* cp = col + ((k + 2) % 3) * 32;  // column k-1
 #pragma unroll
-            for (int j = k + 1; j < MAXR; ++j) ajk[j] = cb[j];
+                for (int j = k + 1; j < MAXR; ++j) r[j] = __fma_rn(-lp, cp[j], r[j]);
+            }
             const bool act = lane > k && lane < R;
             const double num = act ? r[k] : 1.0;
             const double q = num / dk;
             const double l = (act && dk != 0.0) ? q : 0.0;
+            double dn = 0.0;
+            if (k + 1 < MAXR) {  // critical: finish a(., k+1), broadcast d_{k+1}, publish column k+1
+                r[k + 1] = __fma_rn(-l, cb[k + 1], r[k + 1]);
+                dn = __shfl_sync(0xffffffffu, r[k + 1], (k + 1) & 31);
+                col[((k + 1) % 3) * 32 + lane] = r[k + 1];
+            }
             if (lane == 0) D[k] = dk;
             if (act) A[k * kLdStride + lane] = l;
-#pragma unroll
-            for (int j = k + 1; j < MAXR; ++j) r[j] = __fma_rn(-l, ajk[j], r[j]);
-            if (k + 1 < MAXR) col[((k + 1) & 1) * 32 + lane] = r[k + 1];
             __syncwarp();
+            lp = l;
+            dk = dn;
         }
     }
 }
@@ -1087,6 +1104,7 @@ constexpr int kSmFact = 16384;
 constexpr int kSmTotal = 27136;                  // doubles
 constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
 constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
+constexpr int kGramOneBlock = 16384;             // R^2 x chunks combined by one block up to this
 
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
     namespace cg = cooperative_groups;
@@ -1112,28 +1130,36 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
         mbar_init(&bar, 1);
     }
     __syncthreads();
+    // Gram: chunk partials are formed in phase 0 by the blocks that build each
+    // 32-sample chunk of Z; phase 1 only combines them (canonical superchunk
+    // then total order).  Small R^2 x chunks: one block combines everything;
+    // otherwise superchunk items pre-combine and the last arrival finishes.
+    const int nch = (S + kChunk - 1) / kChunk;
+    const int RRp = (RR + 1) & ~1;  // chunk-partial stride: 16-byte multiple for the bulk copy
+    const bool gram_one = int64_t(RRp) * nch <= kGramOneBlock;
     const int n_gram = nsuper * kGramSplitC;
-    const int gram_blocks = min(n_gram, max(1, G / 4));
+    const int gram_blocks = gram_one ? 1 : min(n_gram, max(1, G / 4));
     const int cblocks = G - gram_blocks;  // contraction blocks: [0, cblocks)
     const bool is_gram_block = int(blockIdx.x) >= cblocks;
     double* xs = sm + kSmXs;
     double* zs = sm + kSmZs;
     double* cps = zs + kSuperSamples * RP;
-    const int ztotal = S * RP;
+    const int czt = kChunk * RP;  // Z elements of one chunk
 
-    // idx of this thread's phase-0 Z elements of stage (b, st), in registers; loaded one
-    // phase ahead so the phase-0 critical path is a single L2 gather.
+    // idx of this thread's phase-0 Z elements (chunk blockIdx.x) of stage (b, st), in
+    // registers; loaded one phase ahead so the phase-0 critical path is a single L2 gather.
     int32_t nidx[kZU][kMaxOrder - 1];
     auto load_idx = [&](int b, int st) {
         if (b >= p.nb) return;
         const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
 #pragma unroll
         for (int u = 0; u < kZU; ++u) {
-            const int e = (blockIdx.x + u * G) * blockDim.x + tid;
-            const int c = e / RP;
+            const int e = tid + u * blockDim.x;
+            const int c = int(blockIdx.x) * kChunk + e / RP;
+            const bool ok = int(blockIdx.x) < nch && e < czt && c < S;
 #pragma unroll
             for (int l = 0; l < kMaxOrder - 1; ++l)
-                nidx[u][l] = (e < ztotal && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
+                nidx[u][l] = (ok && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
         }
     };
     load_idx(0, 0);
@@ -1168,46 +1194,70 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                 tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
             }
 
-            // ---------------- phase 0: Z (S x RP, zero padded) over all blocks
-            // (sampling.cpp:90-103: 1.0 * F_0 * F_1 * ... left to right)
-            {
-                double f[kZU][kMaxOrder - 1];
+            // ---------------- phase 0: Z (S x RP, zero padded), one 32-sample chunk per block
+            // (sampling.cpp:90-103: 1.0 * F_0 * F_1 * ... left to right), then the chunk's
+            // Gram partial from shared memory: fma chain over its samples from +0.0
+            // (k_gram's per-chunk sequence), lower pairs mirrored.
+            for (int ch = blockIdx.x; ch < nch; ch += G) {
+                const int c0 = ch * kChunk, cn = min(kChunk, S - c0);
+                double* zc = zs;  // [32][RP]; the contraction Z tile is not loaded before phase 1
+                const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+                if (ch == int(blockIdx.x)) {
+                    double f[kZU][kMaxOrder - 1];
 #pragma unroll
-                for (int u = 0; u < kZU; ++u) {
-                    const int e = (blockIdx.x + u * G) * blockDim.x + tid;
-                    const int c = e / RP, r = e - c * RP;
-                    const bool live = e < ztotal && r < R;
+                    for (int u = 0; u < kZU; ++u) {
+                        const int e = tid + u * blockDim.x;
+                        const int cc = e / RP, r = e - cc * RP;
+                        const bool live = e < czt && cc < cn && r < R;
 #pragma unroll
-                    for (int l = 0; l < kMaxOrder - 1; ++l)
-                        f[u][l] = (live && l < n_other) ? __ldcg(F[l] + int64_t(nidx[u][l]) * R + r) : 1.0;
-                }
+                        for (int l = 0; l < kMaxOrder - 1; ++l)
+                            f[u][l] = (live && l < n_other) ? __ldcg(F[l] + int64_t(nidx[u][l]) * R + r) : 1.0;
+                    }
 #pragma unroll
-                for (int u = 0; u < kZU; ++u) {
-                    const int e = (blockIdx.x + u * G) * blockDim.x + tid;
-                    if (e < ztotal) {
-                        const int r = e % RP;
-                        double z = 0.0;
-                        if (r < R) {
-                            z = 1.0;
+                    for (int u = 0; u < kZU; ++u) {
+                        const int e = tid + u * blockDim.x;
+                        if (e < czt) {
+                            const int cc = e / RP, r = e - cc * RP;
+                            double z = 0.0;
+                            if (cc < cn && r < R) {
+                                z = 1.0;
 #pragma unroll
-                            for (int l = 0; l < kMaxOrder - 1; ++l)
-                                if (l < n_other) z = z * f[u][l];
+                                for (int l = 0; l < kMaxOrder - 1; ++l)
+                                    if (l < n_other) z = z * f[u][l];
+                            }
+                            zc[e] = z;
+                            if (cc < cn) Z[int64_t(c0) * RP + e] = z;
                         }
-                        Z[e] = z;
                     }
                 }
-                for (int e = (blockIdx.x + kZU * G) * blockDim.x + tid; e < ztotal; e += G * blockDim.x) {
-                    // rare tail (S * RP > kZU * G * 256): direct
-                    const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
-                    const int c = e / RP, r = e - c * RP;
+                const int e0 = (ch == int(blockIdx.x)) ? kZU * int(blockDim.x) : 0;
+                for (int e = e0 + tid; e < czt; e += blockDim.x) {  // rare: RP > 32 or extra chunks
+                    const int cc = e / RP, r = e - cc * RP;
                     double z = 0.0;
-                    if (r < R) {
+                    if (cc < cn && r < R) {
                         z = 1.0;
                         for (int l = 0; l < n_other; ++l)
-                            z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c) * n_other + (n_other - 1 - l))) * R + r);
+                            z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c0 + cc) * n_other + (n_other - 1 - l))) * R + r);
                     }
-                    Z[e] = z;
+                    zc[e] = z;
+                    if (cc < cn) Z[int64_t(c0) * RP + e] = z;
                 }
+                __syncthreads();
+                if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[14] = gtimer();
+                for (int q = tid; q < npairs; q += blockDim.x) {
+                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                    double acc = 0.0;
+                    if (cn == kChunk) {
+#pragma unroll 8
+                        for (int cc = 0; cc < kChunk; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                    } else {
+                        for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                    }
+                    p.chpart[int64_t(ch) * RRp + i + j * R] = acc;
+                    p.chpart[int64_t(ch) * RRp + j + i * R] = acc;
+                }
+                __syncthreads();
+                if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[15] = gtimer();
             }
             asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA in phase 1
             grid.sync();
@@ -1215,60 +1265,64 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
 
             // ---------------- phase 1
             if (is_gram_block) {
-                for (int gi = blockIdx.x - cblocks; gi < n_gram; gi += gram_blocks) {
-                    const int m = gi / kGramSplitC, part = gi % kGramSplitC;
-                    const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
-                    const int nk = (cn + kChunk - 1) / kChunk;
-                    const int pp0 = (RR * part) / kGramSplitC, pp1 = (RR * (part + 1)) / kGramSplitC;
-                    const int npp = pp1 - pp0;
-                    double* gz = sm;                       // cn x RP
-                    double* gcp = sm + kSuperSamples * 64;  // [8][npp]
-                    if (tid == 0) {
-                        fence_proxy_async();
-                        tma_load_1d(gz, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
-                        mbar_expect_tx(&bar, unsigned(cn * RP * 8));
+                // superchunk sums of the chunk partials, superchunk m = chunks 8m..8m+7 in order
+                auto super_sum = [&](int m, int pp) {
+                    const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
+                    double v[kSuper];
+#pragma unroll
+                    for (int u = 0; u < kSuper; ++u) v[u] = (k0 + u < k1) ? __ldcg(p.chpart + int64_t(k0 + u) * RRp + pp) : 0.0;
+                    double q = v[0];
+#pragma unroll
+                    for (int u = 1; u < kSuper; ++u)
+                        if (k0 + u < k1) q = q + v[u];
+                    return q;
+                };
+                bool finisher = gram_one;
+                if (!gram_one) {
+                    for (int gi = blockIdx.x - cblocks; gi < n_gram; gi += gram_blocks) {
+                        const int m = gi / kGramSplitC, part = gi % kGramSplitC;
+                        const int pp0 = (RR * part) / kGramSplitC, pp1 = (RR * (part + 1)) / kGramSplitC;
+                        for (int pp = pp0 + tid; pp < pp1; pp += blockDim.x) p.gpart[int64_t(m) * RR + pp] = super_sum(m, pp);
                     }
-                    mbar_wait(&bar, phase);
-                    phase ^= 1u;
-                    for (int u = tid; u < nk * npp; u += blockDim.x) {
-                        const int k = u / npp, pp = pp0 + (u - k * npp);
-                        const int r1 = pp % R, r2 = pp / R;
-                        const int cc0 = k * kChunk, ccn = min(kChunk, cn - cc0);
-                        const double* za = gz + cc0 * RP + r1;
-                        const double* zb = gz + cc0 * RP + r2;
-                        double acc = 0.0;
-                        if (ccn == kChunk) {
-#pragma unroll 8
-                            for (int cc = 0; cc < kChunk; ++cc) acc = __fma_rn(za[cc * RP], zb[cc * RP], acc);
-                        } else {
-                            for (int cc = 0; cc < ccn; ++cc) acc = __fma_rn(za[cc * RP], zb[cc * RP], acc);
-                        }
-                        gcp[k * npp + (pp - pp0)] = acc;
-                    }
-                    __syncthreads();
-                    for (int q = tid; q < npp; q += blockDim.x) {
-                        double v = gcp[q];
-                        for (int k = 1; k < nk; ++k) v = v + gcp[k * npp + q];
-                        p.gpart[int64_t(m) * RR + pp0 + q] = v;
-                    }
-                    __syncthreads();
+                    finisher = last_arrive_of(p.counter, unsigned(gram_blocks));
                 }
-                if (last_arrive_of(p.counter, unsigned(gram_blocks))) {
+                if (finisher) {
                     if (tr && tid == 0) tr[3] = gtimer();
                     double* A = sm + kSmFact;        // [64][65]
                     double* D = A + 64 * kLdStride;  // 64
                     double* Gs = D + 64;             // R x R column-major
-                    double* colb = Gs + 64 * 64;     // 64
-                    // Gram combine in superchunk order; Q += G for the modes (rocp.cpp:108)
+                    double* colb = Gs + 64 * 64;     // 3 x 32 (ldlt_warp column buffers)
+                    // total = superchunk sums in order; Q += G for the modes (rocp.cpp:108)
+                    double* chs = sm;  // gram_one: every chunk partial, one TMA bulk copy (nch x RR <= 16384)
+                    if (gram_one) {
+                        if (tid == 0) {
+                            const unsigned bytes = unsigned(nch * RRp * 8);
+                            fence_proxy_async();
+                            tma_load_1d(chs, p.chpart, bytes, &bar);
+                            mbar_expect_tx(&bar, bytes);
+                        }
+                        mbar_wait(&bar, phase);
+                        phase ^= 1u;
+                    }
                     for (int pp = tid; pp < RR; pp += blockDim.x) {
-                        double v[8];
+                        double tot;
+                        if (gram_one) {
+                            for (int m = 0; m < nsuper; ++m) {
+                                const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
+                                double q = chs[k0 * RRp + pp];
+                                for (int k = k0 + 1; k < k1; ++k) q = q + chs[k * RRp + pp];
+                                tot = (m == 0) ? q : tot + q;
+                            }
+                        } else {
+                            double v[8];
 #pragma unroll
-                        for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * RR + pp) : 0.0;
-                        double tot = v[0];
+                            for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * RR + pp) : 0.0;
+                            tot = v[0];
 #pragma unroll
-                        for (int m = 1; m < 8; ++m)
-                            if (m < nsuper) tot = tot + v[m];
-                        for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * RR + pp);
+                            for (int m = 1; m < 8; ++m)
+                                if (m < nsuper) tot = tot + v[m];
+                            for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * RR + pp);
+                        }
                         if (st > 0) {
                             tot = __ldcg(p.Q[st - 1] + pp) + tot;
                             p.Q[st - 1][pp] = tot;
@@ -1295,7 +1349,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     auto factor = [&](double lambda) {
                         if (R <= 32) {
                             if (warp == 0) {
-                                if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, D, colb);
+                                if (R <= 8) ldlt_warp<8>(Gs, lambda, R, A, D, colb);
+                                else if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, D, colb);
+                                else if (R <= 24) ldlt_warp<24>(Gs, lambda, R, A, D, colb);
                                 else ldlt_warp<32>(Gs, lambda, R, A, D, colb);
                             }
                             __syncthreads();

@@ -673,7 +673,7 @@ struct rocp_stream {
     DBuf<double> resid;           // N x 2 (num, den) of the last batch
     DBuf<double> staging;         // host-slab staging for consume_host
     DBuf<int> flags;              // [0] temporal regularized (stream flag), [2] last mode solve
-    DBuf<double> gpart, LD, rpart, zmodes;  // persistent-chain scratch
+    DBuf<double> gpart, chpart, LD, rpart, zmodes;  // persistent-chain scratch
     DBuf<int> mode_flag;
     bool trace_on = false;             // chain phase timestamps (profiling aid)
     DBuf<unsigned long long> trace;
@@ -968,6 +968,7 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
     p.zbuf = st->win.zT.p + b0 * st->s * RPw;
     p.gch = st->zmodes.p;
     p.gpart = st->gpart.p;
+    p.chpart = st->chpart.p;
     p.cpart = st->dev->contract_partial.p;
     p.LD = st->LD.p;
     p.mode_flag = st->mode_flag.p;
@@ -1792,6 +1793,7 @@ rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int 
     st->seed_dev.alloc(1);
     st->batch_dev.alloc(1);
     st->gpart.alloc(size_t(((s + kSuperSamples - 1) / kSuperSamples) * rank * rank));
+    st->chpart.alloc(size_t(((s + kChunk - 1) / kChunk) * ((rank * rank + 1) & ~1)));
     st->zmodes.alloc(size_t(order * s * (((rank + kCRB - 1) / kCRB) * kCRB)));
     st->LD.alloc(size_t(rank * rank + rank + 2));
     st->rpart.alloc(size_t(3 * s));

@@ -16,7 +16,7 @@ def test_cpp_api_builds():
 
 @pytest.mark.gpu
 def test_cpp_api_suite():
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=240)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
