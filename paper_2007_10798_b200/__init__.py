@@ -654,7 +654,7 @@ class RocpStream:
         self.dev.check(lib().rocp_stream_chain_trace(self.h, int(bool(enable)),
                                                      buf.ctypes.data_as(C.POINTER(C.c_uint64)),
                                                      n.value, C.byref(n)))
-        return buf[: n.value].reshape(-1, 16)
+        return buf[: n.value].reshape(-1, 24)  # kTraceSlots stamps per (batch, stage)
 
     def window_bytes(self):
         u, e = C.c_int64(0), C.c_int64(0)

@@ -852,6 +852,8 @@ struct ChainParams {
     double* gch;              // N x S x RP: Z of the mode stages
     double* gpart;            // nsuper x R x R Gram superchunk partials
     double* chpart;           // nchunks x R x R Gram chunk partials (phase 0)
+    int gram_first;           // first Gram block (-1: the last gram_blocks blocks)
+    int coop_combine;         // 1: combine loads by all threads instead of one bulk copy
     double* cpart;            // nsuper x rows x R
     double* LD;               // R x R (L(i,k) at [k*R + i], i > k) + R (D)
     int* mode_flag;           // [0]: 0 = zero solution, 1 = solve
@@ -1005,6 +1007,8 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
     }
 }
 
+constexpr int kMaxSuperRows = 8;  // superchunk partials prefetched per row entry
+
 // Row solves of phase 2: warp per row, lanes own entries j and j + 32.
 __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
                                              int rows, int R, int nsuper, double* out, const double* Ls,
@@ -1014,23 +1018,38 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
     const bool v0 = j0 < R, v1 = j1 < R;
     for (int row = blockIdx.x + warp * gridDim.x; row < rows; row += gridDim.x * nw) {
         double w0 = 0.0, w1 = 0.0;
+        // every load of the row (superchunk partials, P) in flight at once
+        double c0[kMaxSuperRows], c1[kMaxSuperRows], p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxSuperRows; ++m) {
+            c0[m] = (v0 && m < nsuper) ? __ldcg(cpart + (int64_t(m) * rows + row) * R + j0) : 0.0;
+            c1[m] = (v1 && m < nsuper) ? __ldcg(cpart + (int64_t(m) * rows + row) * R + j1) : 0.0;
+        }
+        if (st > 0) {
+            if (v0) p0 = __ldcg(Prow_base + int64_t(row) * R + j0);
+            if (v1) p1 = __ldcg(Prow_base + int64_t(row) * R + j1);
+        }
         if (v0) {
-            double tot = __ldcg(cpart + int64_t(row) * R + j0);
-            for (int m = 1; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j0);
+            double tot = c0[0];
+#pragma unroll
+            for (int m = 1; m < kMaxSuperRows; ++m)
+                if (m < nsuper) tot = tot + c0[m];
+            for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j0);
             if (st > 0) {
-                double* pr = Prow_base + int64_t(row) * R + j0;
-                tot = __ldcg(pr) + tot;
-                *pr = tot;
+                tot = p0 + tot;
+                Prow_base[int64_t(row) * R + j0] = tot;
             }
             w0 = tot;
         }
         if (v1) {
-            double tot = __ldcg(cpart + int64_t(row) * R + j1);
-            for (int m = 1; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j1);
+            double tot = c1[0];
+#pragma unroll
+            for (int m = 1; m < kMaxSuperRows; ++m)
+                if (m < nsuper) tot = tot + c1[m];
+            for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j1);
             if (st > 0) {
-                double* pr = Prow_base + int64_t(row) * R + j1;
-                tot = __ldcg(pr) + tot;
-                *pr = tot;
+                tot = p1 + tot;
+                Prow_base[int64_t(row) * R + j1] = tot;
             }
             w1 = tot;
         }
@@ -1104,7 +1123,8 @@ constexpr int kSmFact = 16384;
 constexpr int kSmTotal = 27136;                  // doubles
 constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
 constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
-constexpr int kGramOneBlock = 16384;             // R^2 x chunks combined by one block up to this
+constexpr int kGramOneBlock = 16384;
+constexpr int kTraceSlots = 24;                  // globaltimer stamps per stage (profiling aid)             // R^2 x chunks combined by one block up to this
 
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
     namespace cg = cooperative_groups;
@@ -1135,12 +1155,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     // then total order).  Small R^2 x chunks: one block combines everything;
     // otherwise superchunk items pre-combine and the last arrival finishes.
     const int nch = (S + kChunk - 1) / kChunk;
-    const int RRp = (RR + 1) & ~1;  // chunk-partial stride: 16-byte multiple for the bulk copy
-    const bool gram_one = int64_t(RRp) * nch <= kGramOneBlock;
+    const int NPp = (npairs + 1) & ~1;  // chunk-partial stride (lower pairs): 16-byte multiple for the bulk copy
+    const bool gram_one = int64_t(NPp) * nch <= kGramOneBlock;
     const int n_gram = nsuper * kGramSplitC;
     const int gram_blocks = gram_one ? 1 : min(n_gram, max(1, G / 4));
-    const int cblocks = G - gram_blocks;  // contraction blocks: [0, cblocks)
-    const bool is_gram_block = int(blockIdx.x) >= cblocks;
+    const int cblocks = G - gram_blocks;  // contraction blocks
+    const int gb0 = (p.gram_first >= 0 && p.gram_first + gram_blocks <= G) ? p.gram_first : cblocks;
+    const bool is_gram_block = int(blockIdx.x) >= gb0 && int(blockIdx.x) < gb0 + gram_blocks;
+    const int cix = int(blockIdx.x) < gb0 ? int(blockIdx.x) : int(blockIdx.x) - gram_blocks;  // contraction index
     double* xs = sm + kSmXs;
     double* zs = sm + kSmZs;
     double* cps = zs + kSuperSamples * RP;
@@ -1167,13 +1189,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     for (int b = 0; b < p.nb; ++b) {
         double* u_new = p.temporal + (p.t_len0 + int64_t(b) * p.B) * R;
         for (int st = 0; st < N; ++st) {
-            const double* F[kMaxOrder];
-            {
-                int l = 0;
-                if (st > 0) F[l++] = u_new;
-                for (int k = N - 1; k >= 1; --k)
-                    if (k != st) F[l++] = p.U[k - 1];
-                for (; l < kMaxOrder; ++l) F[l] = nullptr;
+            // [u_new (modes)] + U(N-1), ..., U(1) without U(st), built with compile-time
+            // positions so the list stays in registers
+            const double* F[kMaxOrder - 1];
+#pragma unroll
+            for (int l = 0; l < kMaxOrder - 1; ++l) {
+                const int m = (st > 0) ? l - 1 : l;
+                int k = N - 1 - m;
+                if (st > 0 && k <= st) k -= 1;
+                F[l] = (st > 0 && l == 0) ? u_new : ((m >= 0 && k >= 1) ? p.U[k - 1] : nullptr);
             }
             const int rows = (st == 0) ? p.B : p.head[st - 1];
             const double* X = p.X_base + p.xoff[b * N + st];
@@ -1181,17 +1205,32 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * RP : p.gch + int64_t(st) * S * RP;
             const int tiles = (rows + kRowTile - 1) / kRowTile;
             const int n_contract = tiles * nsuper;
-            unsigned long long* tr = p.trace ? p.trace + (int64_t(b) * N + st) * 16 : nullptr;
+            unsigned long long* tr = p.trace ? p.trace + (int64_t(b) * N + st) * kTraceSlots : nullptr;
             if (tr && blockIdx.x == 0 && tid == 0) tr[0] = gtimer();
 
             // stage start: TMA the first X_s tile of this block (independent of factors);
             // its arrive.expect_tx is issued with the Z tile in phase 1.
-            const bool contract_block = !is_gram_block && int(blockIdx.x) < n_contract;
+            const bool contract_block = !is_gram_block && cix < n_contract;
             if (contract_block && tid == 0) {
-                const int item = blockIdx.x, tile = item % tiles, m = item / tiles;
+                const int item = cix, tile = item % tiles, m = item / tiles;
                 const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                 fence_proxy_async();
                 tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+            }
+
+            // the single Gram finisher fetches its Q entries during phase 0 (Q(st) only
+            // changes in this stage's finisher): off the phase-1 critical path, where the
+            // contraction blocks' tile copies congest L2
+            double qa[kMaxPairsPerThread], qb[kMaxPairsPerThread];
+#pragma unroll
+            for (int u = 0; u < kMaxPairsPerThread; ++u) {
+                const int q = tid + u * int(blockDim.x);
+                qa[u] = qb[u] = 0.0;
+                if (is_gram_block && gram_one && st > 0 && q < npairs) {
+                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                    qa[u] = __ldcg(p.Q[st - 1] + i + j * R);
+                    qb[u] = __ldcg(p.Q[st - 1] + j + i * R);
+                }
             }
 
             // ---------------- phase 0: Z (S x RP, zero padded), one 32-sample chunk per block
@@ -1236,8 +1275,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     double z = 0.0;
                     if (cc < cn && r < R) {
                         z = 1.0;
-                        for (int l = 0; l < n_other; ++l)
-                            z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c0 + cc) * n_other + (n_other - 1 - l))) * R + r);
+#pragma unroll
+                        for (int l = 0; l < kMaxOrder - 1; ++l)
+                            if (l < n_other)
+                                z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c0 + cc) * n_other + (n_other - 1 - l))) * R + r);
                     }
                     zc[e] = z;
                     if (cc < cn) Z[int64_t(c0) * RP + e] = z;
@@ -1253,8 +1294,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     } else {
                         for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
                     }
-                    p.chpart[int64_t(ch) * RRp + i + j * R] = acc;
-                    p.chpart[int64_t(ch) * RRp + j + i * R] = acc;
+                    p.chpart[int64_t(ch) * NPp + q] = acc;  // lower pair q; (j, i) is the same value
                 }
                 __syncthreads();
                 if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[15] = gtimer();
@@ -1270,7 +1310,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
                     double v[kSuper];
 #pragma unroll
-                    for (int u = 0; u < kSuper; ++u) v[u] = (k0 + u < k1) ? __ldcg(p.chpart + int64_t(k0 + u) * RRp + pp) : 0.0;
+                    for (int u = 0; u < kSuper; ++u) v[u] = (k0 + u < k1) ? __ldcg(p.chpart + int64_t(k0 + u) * NPp + pp) : 0.0;
                     double q = v[0];
 #pragma unroll
                     for (int u = 1; u < kSuper; ++u)
@@ -1279,10 +1319,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                 };
                 bool finisher = gram_one;
                 if (!gram_one) {
-                    for (int gi = blockIdx.x - cblocks; gi < n_gram; gi += gram_blocks) {
+                    for (int gi = int(blockIdx.x) - gb0; gi < n_gram; gi += gram_blocks) {
                         const int m = gi / kGramSplitC, part = gi % kGramSplitC;
-                        const int pp0 = (RR * part) / kGramSplitC, pp1 = (RR * (part + 1)) / kGramSplitC;
-                        for (int pp = pp0 + tid; pp < pp1; pp += blockDim.x) p.gpart[int64_t(m) * RR + pp] = super_sum(m, pp);
+                        const int pp0 = (npairs * part) / kGramSplitC, pp1 = (npairs * (part + 1)) / kGramSplitC;
+                        for (int pp = pp0 + tid; pp < pp1; pp += blockDim.x) p.gpart[int64_t(m) * NPp + pp] = super_sum(m, pp);
                     }
                     finisher = last_arrive_of(p.counter, unsigned(gram_blocks));
                 }
@@ -1293,41 +1333,67 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     double* Gs = D + 64;             // R x R column-major
                     double* colb = Gs + 64 * 64;     // 3 x 32 (ldlt_warp column buffers)
                     // total = superchunk sums in order; Q += G for the modes (rocp.cpp:108)
-                    double* chs = sm;  // gram_one: every chunk partial, one TMA bulk copy (nch x RR <= 16384)
-                    if (gram_one) {
-                        if (tid == 0) {
-                            const unsigned bytes = unsigned(nch * RRp * 8);
-                            fence_proxy_async();
-                            tma_load_1d(chs, p.chpart, bytes, &bar);
-                            mbar_expect_tx(&bar, bytes);
+                    double* chs = sm;  // gram_one: every chunk partial, one TMA bulk copy (nch x NPp <= 16384)
+                    if (gram_one && !p.coop_combine && tid == 0) {
+                        const unsigned bytes = unsigned(nch * NPp * 8);
+                        fence_proxy_async();
+                        tma_load_1d(chs, p.chpart, bytes, &bar);
+                        mbar_expect_tx(&bar, bytes);
+                    }
+                    if (gram_one && p.coop_combine) {
+                        for (int e = tid; e < nch * NPp; e += blockDim.x) chs[e] = __ldcg(p.chpart + e);
+                    }
+                    // Q entries of this thread's pairs (prefetched in phase 0 when gram_one)
+                    if (!gram_one) {
+#pragma unroll
+                        for (int u = 0; u < kMaxPairsPerThread; ++u) {
+                            const int q = tid + u * int(blockDim.x);
+                            if (st > 0 && q < npairs) {
+                                const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                                qa[u] = __ldcg(p.Q[st - 1] + i + j * R);
+                                qb[u] = __ldcg(p.Q[st - 1] + j + i * R);
+                            }
                         }
+                    }
+                    if (gram_one && !p.coop_combine) {
                         mbar_wait(&bar, phase);
                         phase ^= 1u;
                     }
-                    for (int pp = tid; pp < RR; pp += blockDim.x) {
+                    if (gram_one && p.coop_combine) __syncthreads();
+                    if (tr && tid == 0) tr[18] = gtimer();
+#pragma unroll
+                    for (int u = 0; u < kMaxPairsPerThread; ++u) {
+                        const int q = tid + u * int(blockDim.x);
+                        if (q >= npairs) break;
                         double tot;
                         if (gram_one) {
                             for (int m = 0; m < nsuper; ++m) {
                                 const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
-                                double q = chs[k0 * RRp + pp];
-                                for (int k = k0 + 1; k < k1; ++k) q = q + chs[k * RRp + pp];
-                                tot = (m == 0) ? q : tot + q;
+                                double sq = chs[k0 * NPp + q];
+                                for (int k = k0 + 1; k < k1; ++k) sq = sq + chs[k * NPp + q];
+                                tot = (m == 0) ? sq : tot + sq;
                             }
                         } else {
                             double v[8];
 #pragma unroll
-                            for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * RR + pp) : 0.0;
+                            for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * NPp + q) : 0.0;
                             tot = v[0];
 #pragma unroll
                             for (int m = 1; m < 8; ++m)
                                 if (m < nsuper) tot = tot + v[m];
-                            for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * RR + pp);
+                            for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
                         }
+                        // Q + G entry by entry (rocp.cpp:108); G is symmetric bit for bit
+                        const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                        double ga = tot, gb = tot;
                         if (st > 0) {
-                            tot = __ldcg(p.Q[st - 1] + pp) + tot;
-                            p.Q[st - 1][pp] = tot;
+                            ga = qa[u] + tot;
+                            gb = qb[u] + tot;
+                            p.Q[st - 1][i + j * R] = ga;
+                            p.Q[st - 1][j + i * R] = gb;
                         }
-                        Gs[pp] = tot;
+                        Gs[i + j * R] = ga;
+                        Gs[j + i * R] = gb;
                     }
                     __syncthreads();
                     if (tr && tid == 0) tr[10] = gtimer();
@@ -1390,13 +1456,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
                 }
             } else {
-                for (int item = blockIdx.x; item < n_contract; item += cblocks) {
+                for (int item = cix; item < n_contract; item += cblocks) {
                     const int tile = item % tiles, m = item / tiles;
                     const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                     const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
                     if (tid == 0) {
                         fence_proxy_async();
-                        if (item != int(blockIdx.x))  // later items: X tile now
+                        if (item != cix)  // later items: X tile now
                             tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
                         tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
                         mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + cn * RP * 8));
@@ -1448,10 +1514,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     }
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
+                    if (tr && blockIdx.x == 0 && tid == 0) tr[16] = gtimer();
                     const int mode = __ldcg(p.mode_flag);
                     double* out = (st == 0) ? u_new : p.U[st - 1];
                     chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ls + RR,
                                     mode);
+                    if (tr && blockIdx.x == 0 && tid == 0) tr[17] = gtimer();
                 }
                 load_idx(nb2, ns2);
             }

@@ -44,6 +44,6 @@ for stg in range(N):
     print(f"stage {stg}: z(block0)={med(t[:,14]-t[:,0]):.2f} chunk-gram={med(t[:,15]-t[:,14]):.2f} p0+sync={med(z(1)):.2f} | item0 ready={med(t[:,8]-t[:,1]):.2f} compute={med(t[:,9]-t[:,8]):.2f} | "
           f"gram->factor start={med(t[:,3]-t[:,1]):.2f} combine={med(t[:,10]-t[:,3]):.2f} prologue={med(t[:,12]-t[:,10]):.2f} "
           f"ldlt={med(t[:,13]-t[:,12]):.2f} check={med(t[:,11]-t[:,13]):.2f} publish={med(t[:,4]-t[:,11]):.2f} | "
-          f"sync1 done={med(z(5)):.2f} rows={med(t[:,6]-t[:,5]):.2f} sync2={med(t[:,7]-t[:,6]):.2f} | total={med(t[:,7]-t[:,0]):.2f} us")
+          f"tma-wait={med(t[:,18]-t[:,3]):.2f} | sync1 done={med(z(5)):.2f} LD ready={med(t[:,16]-t[:,5]):.2f} row loop={med(t[:,17]-t[:,16]):.2f} rows={med(t[:,6]-t[:,5]):.2f} sync2={med(t[:,7]-t[:,6]):.2f} | total={med(t[:,7]-t[:,0]):.2f} us")
 print("whole window us:", (tr[-1, 7] - tr[0, 0]) / 1e3)
 print("residual of last batch:", st.last_residuals()[0])
