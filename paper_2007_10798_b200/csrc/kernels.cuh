@@ -1008,6 +1008,7 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
 }
 
 constexpr int kMaxSuperRows = 8;  // superchunk partials prefetched per row entry
+constexpr int kQPre = 3;          // Q pairs per thread prefetched by the Gram finisher
 
 // Row solves of phase 2: warp per row, lanes own entries j and j + 32.
 __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
@@ -1112,6 +1113,61 @@ __device__ __forceinline__ void chain_chunk(const double* __restrict__ xs, const
     for (int a = 0; a < NG * kCRB; ++a) cps[(warp * CW + a) * kRowTile + lane] = acc[a];
 }
 
+constexpr int kRedStride = 33;  // padded row stride of the blocked partials (bank-conflict free)
+
+// Register-blocked contraction item for RP = 4 * CPL > 32 (R in 33..64): warp w
+// = chunk w of the superchunk; lane = (row group rg = lane / 4: rows 4rg..4rg+3)
+// x (column group cg = lane % 4: columns cg*CPL .. cg*CPL + CPL - 1), so one
+// sample costs 2 + CPL/2 shared loads for 4*CPL fmas.  Each output's chunk
+// partial is its fma chain over the chunk's samples from +0.0 (canonical);
+// after the compute the X and Z tile regions (contiguous, 8 x RP x 33 <= 16896
+// of their 8192 + 256 RP doubles) hold every warp's partials and the
+// superchunk partial sums them in chunk order.
+template <int CPL>
+__device__ __noinline__ void chain_contract_blocked(const double* xs, const double* zs, double* red, int cc0, int ccn,
+                                                    int nk, int nrows, int R, double* out_rows) {
+    constexpr int RP = 4 * CPL;  // padded width
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rg = lane >> 2, cg = lane & 3;
+    double acc[4][CPL];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) acc[a][j] = 0.0;
+    for (int cc = 0; cc < ccn; ++cc) {
+        const double2* xp = reinterpret_cast<const double2*>(xs + (cc0 + cc) * kRowTile + 4 * rg);
+        const double2 xa = xp[0], xb = xp[1];
+        const double x[4] = {xa.x, xa.y, xb.x, xb.y};
+        const double2* zp = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RP + cg * CPL);
+#pragma unroll
+        for (int q = 0; q < CPL / 2; ++q) {
+            const double2 zz = zp[q];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                acc[a][2 * q] = __fma_rn(x[a], zz.x, acc[a][2 * q]);
+                acc[a][2 * q + 1] = __fma_rn(x[a], zz.y, acc[a][2 * q + 1]);
+            }
+        }
+    }
+    __syncthreads();  // every warp is done with the X and Z tiles
+    if (warp < nk) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) red[(warp * RP + cg * CPL + j) * kRedStride + 4 * rg + a] = acc[a][j];
+    }
+    __syncthreads();
+    for (int e = tid; e < RP * kRowTile; e += blockDim.x) {
+        const int c = e >> 5, i = e & 31;
+        if (i < nrows && c < R) {
+            double qq = red[c * kRedStride + i];
+            for (int k = 1; k < nk; ++k) qq = qq + red[(k * RP + c) * kRedStride + i];
+            out_rows[int64_t(i) * R + c] = qq;
+        }
+    }
+    __syncthreads();
+}
+
 // Shared-memory map of k_chain (doubles):
 //   [0, 8192)                X_s tile (TMA); phase B: L/D (TMA); Gram items: Z tile + chunk partials
 //   [8192, 8192 + 256*RP)    contraction Z tile (TMA)
@@ -1126,6 +1182,9 @@ constexpr int kGramSplitC = 8;                   // Gram output ranges per super
 constexpr int kGramOneBlock = 16384;
 constexpr int kTraceSlots = 24;                  // globaltimer stamps per stage (profiling aid)             // R^2 x chunks combined by one block up to this
 
+// kWide: R in 33..64 (register-blocked contraction); the R <= 32 instance
+// carries none of that code, so its register allocation is unaffected.
+template <bool kWide>
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -1221,9 +1280,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // the single Gram finisher fetches its Q entries during phase 0 (Q(st) only
             // changes in this stage's finisher): off the phase-1 critical path, where the
             // contraction blocks' tile copies congest L2
-            double qa[kMaxPairsPerThread], qb[kMaxPairsPerThread];
+            double qa[kQPre], qb[kQPre];
 #pragma unroll
-            for (int u = 0; u < kMaxPairsPerThread; ++u) {
+            for (int u = 0; u < kQPre; ++u) {
                 const int q = tid + u * int(blockDim.x);
                 qa[u] = qb[u] = 0.0;
                 if (is_gram_block && gram_one && st > 0 && q < npairs) {
@@ -1343,10 +1402,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (gram_one && p.coop_combine) {
                         for (int e = tid; e < nch * NPp; e += blockDim.x) chs[e] = __ldcg(p.chpart + e);
                     }
-                    // Q entries of this thread's pairs (prefetched in phase 0 when gram_one)
+                    // Q entries of this thread's first kQPre pairs (prefetched in phase 0 when gram_one)
                     if (!gram_one) {
 #pragma unroll
-                        for (int u = 0; u < kMaxPairsPerThread; ++u) {
+                        for (int u = 0; u < kQPre; ++u) {
                             const int q = tid + u * int(blockDim.x);
                             if (st > 0 && q < npairs) {
                                 const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
@@ -1387,8 +1446,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
                         double ga = tot, gb = tot;
                         if (st > 0) {
-                            ga = qa[u] + tot;
-                            gb = qb[u] + tot;
+                            const double qva = (u < kQPre) ? qa[u < kQPre ? u : 0] : __ldcg(p.Q[st - 1] + i + j * R);
+                            const double qvb = (u < kQPre) ? qb[u < kQPre ? u : 0] : __ldcg(p.Q[st - 1] + j + i * R);
+                            ga = qva + tot;
+                            gb = qvb + tot;
                             p.Q[st - 1][i + j * R] = ga;
                             p.Q[st - 1][j + i * R] = gb;
                         }
@@ -1473,7 +1534,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     const int nk = (cn + kChunk - 1) / kChunk;
                     const int cc0 = warp * kChunk;
                     const int ccn = min(kChunk, cn - cc0);
-                    for (int g0 = 0; g0 < ng; g0 += NGP) {
+                    if constexpr (kWide) {  // register-blocked item (R in 33..64)
+                        double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
+                        const int cn0 = max(ccn, 0);
+                        if (RP == 40) chain_contract_blocked<10>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        else if (RP == 48) chain_contract_blocked<12>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        else if (RP == 56) chain_contract_blocked<14>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        else chain_contract_blocked<16>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                    }
+                    for (int g0 = 0; g0 < ng && !kWide; g0 += NGP) {
                         if (ccn > 0) {  // warp w = chunk w of the superchunk; lane = row
                             const int ngp = min(NGP, ng - g0);
                             if (ngp == 4) chain_chunk<4>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
