@@ -42,7 +42,8 @@ typedef enum {
     ROCP_E_CUDA = 3,
     ROCP_E_NCCL = 4,
     ROCP_E_OOM = 5,
-    ROCP_E_STATE = 6
+    ROCP_E_STATE = 6,
+    ROCP_E_IO = 7 /* file records (std::runtime_error in tensor_io.cpp / rocp.cpp) */
 } rocp_status;
 
 typedef struct rocp_dev rocp_dev;       /* one per GPU: stream, scratch, comm */
@@ -84,6 +85,12 @@ rocp_status rocp_tensor_slab(rocp_dev* dev, const rocp_tensor* t, int64_t t0, in
 /* Rows [r0, r1) of mode 1 as a new owned tensor (the local block of a
  * mode-1 sharded stream). */
 rocp_status rocp_tensor_rows(rocp_dev* dev, const rocp_tensor* t, int64_t r0, int64_t r1, rocp_tensor** out);
+/* The reference's binary tensor record ("ROCP", u8 version 1, u32le order,
+ * u64le dims, little-endian binary64 values first index fastest;
+ * write_tensor_file / read_tensor_file, tensor_io.cpp:49-89), streamed through
+ * a pinned staging buffer.  ROCP_E_IO on open/format/truncation errors. */
+rocp_status rocp_tensor_write_file(rocp_dev* dev, const rocp_tensor* t, const char* path);
+rocp_status rocp_tensor_read_file(rocp_dev* dev, const char* path, rocp_tensor** out);
 void rocp_tensor_free(rocp_tensor* t);
 rocp_status rocp_tensor_upload(rocp_dev* dev, rocp_tensor* t, const double* host);
 rocp_status rocp_tensor_download(rocp_dev* dev, const rocp_tensor* t, double* host);
@@ -163,6 +170,18 @@ rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint6
  * size; rocp_stream_get(mode 1) returns the local rows.  Host-slab consumes and
  * the replay seams stay single-GPU (E_DOMAIN on a sharded stream). */
 rocp_status rocp_stream_shard(rocp_stream* st, int virtual_shards);
+/* ComplementaryState records.  write_state writes exactly the reference's
+ * save_state record (rocp.cpp:180-184: P(1..N-1), Q(1..N-1) matrix records,
+ * u64le t_len), readable by its load_state; read_state loads such a record
+ * into a stream of the same shape (rocp.cpp:186-211 + assignment).  A
+ * checkpoint adds what resuming needs (section 8f of SURVEY.md): U(1..N-1)
+ * and temporal records before P and Q, and a tail u64le t_len, s, flags.
+ * Sharded streams: E_DOMAIN (their U(1)/P(1) are partial). */
+rocp_status rocp_stream_write_state(rocp_stream* st, const char* path);
+rocp_status rocp_stream_read_state(rocp_stream* st, const char* path);
+rocp_status rocp_stream_write_checkpoint(rocp_stream* st, const char* path);
+rocp_status rocp_stream_create_from_checkpoint(rocp_dev* dev, const char* path, int64_t t_capacity,
+                                               rocp_stream** out);
 rocp_status rocp_stream_shard_info(rocp_stream* st, int* virtual_shards, int64_t* row0, int64_t* row1);
 /* Same for a host slab (head dims x batch, first index fastest): the
  * reference-facing call.  Only the sampled fibres cross PCIe (see

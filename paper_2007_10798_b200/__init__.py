@@ -29,7 +29,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "librocp_b200.so")
 
 # status codes (include/rocp_b200.h)
-OK, E_DOMAIN, E_NUMERICAL, E_CUDA, E_NCCL, E_OOM, E_STATE = range(7)
+OK, E_DOMAIN, E_NUMERICAL, E_CUDA, E_NCCL, E_OOM, E_STATE, E_IO = range(8)
 
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
@@ -47,6 +47,8 @@ SIGNATURES = [
     ("rocp_tensor_create", C.c_int, [_vp, _i64p, C.c_int, _f64p, C.POINTER(_vp)]),
     ("rocp_tensor_slab", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.POINTER(_vp)]),
     ("rocp_tensor_rows", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.POINTER(_vp)]),
+    ("rocp_tensor_write_file", C.c_int, [_vp, _vp, C.c_char_p]),
+    ("rocp_tensor_read_file", C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
     ("rocp_tensor_free", None, [_vp]),
     ("rocp_tensor_upload", C.c_int, [_vp, _vp, _f64p]),
     ("rocp_tensor_download", C.c_int, [_vp, _vp, _f64p]),
@@ -76,6 +78,10 @@ SIGNATURES = [
     ("rocp_stream_create_from_init", C.c_int, [_vp, C.c_int, C.c_int64, C.POINTER(_vp)]),
     ("rocp_stream_free", None, [_vp]),
     ("rocp_stream_shard", C.c_int, [_vp, C.c_int]),
+    ("rocp_stream_write_state", C.c_int, [_vp, C.c_char_p]),
+    ("rocp_stream_read_state", C.c_int, [_vp, C.c_char_p]),
+    ("rocp_stream_write_checkpoint", C.c_int, [_vp, C.c_char_p]),
+    ("rocp_stream_create_from_checkpoint", C.c_int, [_vp, C.c_char_p, C.c_int64, C.POINTER(_vp)]),
     ("rocp_stream_shard_info", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("rocp_stream_consume", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32]),
     ("rocp_stream_consume_host", C.c_int, [_vp, _f64p, C.c_int64, C.c_uint64, C.c_uint32]),
@@ -153,6 +159,10 @@ class NumericalError(RocpError):
         self.sweep = sweep
 
 
+class RecordError(RocpError, OSError):
+    """File record errors (std::runtime_error in tensor_io.cpp / rocp.cpp)."""
+
+
 def _check(dev_handle, rc, sweep=0):
     if rc == OK:
         return
@@ -162,6 +172,8 @@ def _check(dev_handle, rc, sweep=0):
         raise DomainError(rc, msg)
     if rc == E_NUMERICAL:
         raise NumericalError(rc, msg, sweep)
+    if rc == E_IO:
+        raise RecordError(rc, msg)
     raise RocpError(rc, msg)
 
 
@@ -255,6 +267,12 @@ class Device:
     def tensor(self, dims, host=None):
         return DeviceTensor(self, dims, host)
 
+    def read_tensor(self, path):
+        """A reference tensor record (read_tensor_file, tensor_io.cpp:83-89) on the device."""
+        h = C.c_void_p()
+        self.check(lib().rocp_tensor_read_file(self.h, os.fsencode(path), C.byref(h)))
+        return DeviceTensor(self, _record_dims(path), _handle=h)
+
     def timer_record(self, slot):
         self.check(lib().rocp_timer_record(self.h, slot))
 
@@ -262,6 +280,35 @@ class Device:
         ms = C.c_float(0)
         self.check(lib().rocp_timer_elapsed_ms(self.h, a, b, C.byref(ms)))
         return float(ms.value)
+
+
+# ---- the reference's binary records, host side (tensor_io.cpp:12-101) -----------
+def _record_dims(path):
+    with open(path, "rb") as f:
+        head = f.read(9)
+        if head[:4] != b"ROCP" or head[4] != 1:
+            raise RecordError(E_IO, "bad tensor magic or version")
+        order = int.from_bytes(head[5:9], "little")
+        return [int.from_bytes(f.read(8), "little") for _ in range(order)]
+
+
+def read_records(path):
+    """Every matrix record of a file as column-major arrays (plus nothing of the tail)."""
+    out = []
+    with open(path, "rb") as f:
+        data = f.read()
+    pos = 0
+    while len(data) - pos > 24 or (len(data) - pos > 8 and data[pos:pos + 4] == b"ROCP"):
+        if data[pos:pos + 4] != b"ROCP":
+            break
+        order = int.from_bytes(data[pos + 5:pos + 9], "little")
+        dims = [int.from_bytes(data[pos + 9 + 8 * k:pos + 17 + 8 * k], "little") for k in range(order)]
+        pos += 9 + 8 * order
+        n = int(np.prod(dims))
+        vals = np.frombuffer(data, dtype="<f8", count=n, offset=pos).copy()
+        pos += 8 * n
+        out.append(vals.reshape(dims, order="F"))
+    return out
 
 
 def nccl_unique_id():
@@ -337,6 +384,10 @@ class DeviceTensor:
         dims = list(self.dims)
         dims[-1] = length
         return DeviceTensor(self.dev, dims, _handle=h, _parent=self)
+
+    def write(self, path):
+        """The reference tensor record (write_tensor_file, tensor_io.cpp:77-81)."""
+        self.dev.check(lib().rocp_tensor_write_file(self.dev.h, self.h, os.fsencode(path)))
 
     def rows(self, r0, r1):
         """Rows [r0, r1) of mode 1 as a new tensor (a rank's block of a sharded stream)."""
@@ -660,6 +711,33 @@ class RocpStream:
         u, e = C.c_int64(0), C.c_int64(0)
         self.dev.check(lib().rocp_stream_window_bytes(self.h, C.byref(u), C.byref(e)))
         return int(u.value), int(e.value)
+
+    def write_state(self, path):
+        """save_state record of the ComplementaryState (rocp.cpp:180-184)."""
+        self.dev.check(lib().rocp_stream_write_state(self.h, os.fsencode(path)))
+
+    def read_state(self, path):
+        """load_state record (rocp.cpp:186-211) into this stream: P, Q, t_len."""
+        self.dev.check(lib().rocp_stream_read_state(self.h, os.fsencode(path)))
+
+    def write_checkpoint(self, path):
+        self.dev.check(lib().rocp_stream_write_checkpoint(self.h, os.fsencode(path)))
+
+    @classmethod
+    def from_checkpoint(cls, dev, path, t_capacity=0):
+        """A stream resumed from write_checkpoint's record."""
+        h = C.c_void_p()
+        dev.check(lib().rocp_stream_create_from_checkpoint(dev.h, os.fsencode(path), t_capacity, C.byref(h)))
+        st = cls.__new__(cls)
+        st.dev, st.h = dev, h
+        dev._adopt(st)
+        recs = read_records(path)
+        N = (len(recs) - 1) // 3 + 1
+        st.order = N
+        st.rank = recs[0].shape[1]
+        st.head = [recs[n].shape[0] for n in range(N - 1)]
+        st.s = None
+        return st
 
     def checkpoint(self):
         self.dev.check(lib().rocp_stream_checkpoint(self.h))

@@ -1835,6 +1835,8 @@ void init_pq(rocp_stream* st, const std::vector<const double*>& z_dev, bool lite
     CK(cudaStreamSynchronize(dev->stream));
 }
 
+#include "io_host.inc"
+
 }  // namespace
 
 rocp_status rocp_stream_create(rocp_dev* dev, int order, const int64_t* head_dims, int rank,
@@ -1894,6 +1896,52 @@ rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint6
                                   batch_id);
         else
             consume_one(st, x_new->d, x_new->dims.back(), seed, batch_id);
+    });
+}
+
+rocp_status rocp_tensor_write_file(rocp_dev* dev, const rocp_tensor* t, const char* path) {
+    return guarded(dev, [&] {
+        File out(path, "wb");
+        write_tensor_rec(dev, t, out);
+    });
+}
+
+rocp_status rocp_tensor_read_file(rocp_dev* dev, const char* path, rocp_tensor** out) {
+    return guarded(dev, [&] {
+        File in(path, "rb");
+        *out = read_tensor_rec(dev, in).release();
+    });
+}
+
+rocp_status rocp_stream_write_state(rocp_stream* st, const char* path) {
+    return guarded(st->dev, [&] {
+        if (st->sharded) throw_domain("state records hold the full U(1)/P(1); this stream is sharded");
+        File out(path, "wb");
+        write_state(st, out);
+    });
+}
+
+rocp_status rocp_stream_read_state(rocp_stream* st, const char* path) {
+    return guarded(st->dev, [&] {
+        if (st->sharded) throw_domain("state records hold the full U(1)/P(1); this stream is sharded");
+        File in(path, "rb");
+        read_state(st, in);
+    });
+}
+
+rocp_status rocp_stream_write_checkpoint(rocp_stream* st, const char* path) {
+    return guarded(st->dev, [&] {
+        if (st->sharded) throw_domain("checkpoints hold the full U(1)/P(1); this stream is sharded");
+        File out(path, "wb");
+        write_checkpoint(st, out);
+    });
+}
+
+rocp_status rocp_stream_create_from_checkpoint(rocp_dev* dev, const char* path, int64_t t_capacity,
+                                               rocp_stream** out) {
+    return guarded(dev, [&] {
+        File in(path, "rb");
+        *out = read_checkpoint(dev, in, t_capacity);
     });
 }
 

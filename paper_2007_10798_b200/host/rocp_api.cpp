@@ -27,6 +27,7 @@ void raise(rocp_dev* d, rocp_status st, int sweep = 0) {
     const std::string msg = rocp_last_error(d);
     if (st == ROCP_E_DOMAIN) throw std::domain_error(msg);
     if (st == ROCP_E_NUMERICAL) throw NumericalError(msg, sweep);
+    if (st == ROCP_E_IO) throw std::runtime_error(msg);  // tensor_io.cpp / rocp.cpp record errors
     throw std::runtime_error("rocp_b200 status " + std::to_string(int(st)) + ": " + msg);
 }
 

@@ -439,3 +439,51 @@ def test_sharded_stream_window_and_errors(dev):
                                              [np.zeros((8, 2), order="F")] * 2, 0.0, 0, False, [], 8), 8)
     with pytest.raises(rocp.DomainError):
         c.shard(7)  # more shards than rows
+
+
+def test_exhaustive_sampling_equals_full_update_on_device(dev):
+    """SURVEY 8f-1 / acceptance.cpp:128-170 on the GPU: sampling every column once
+    through the replay seams equals the exact online update (baselines.cpp:161-195)
+    within the reference tolerance."""
+    dims, R, t_init = [5, 6, 30], 2, 12
+    g = H.rng(3001)
+    x, _ = H.gen_synthetic(dims, R, 20.0, g)
+    xi = H.slab(x, dims, 0, t_init)
+    model = orc.cprand_decompose(xi, [5, 6, t_init], R, H.random_model([5, 6, t_init], R, H.rng(3002)),
+                                 seed=3002, tol=1e-10, max_iters=60).model
+    p, q = orc.online_full_init(xi, [5, 6, t_init], model)
+    batch = H.slab(x, dims, t_init, 2)
+    bd = [5, 6, 2]
+    fh = [np.array(m, order="F", copy=True) for m in model[:-1]]
+    pf = [np.array(m, order="F", copy=True) for m in p]
+    qf = [np.array(m, order="F", copy=True) for m in q]
+    u_full = orc.online_full_update(batch, bd, fh, pf, qf)
+
+    def stream_with(s):
+        init = rocp.InitResult([np.asfortranarray(m) for m in model], [np.zeros((s, R), order="F")] * 2,
+                               0.0, 0, False, [], s)
+        st = rocp.RocpStream(dev, init, s, literal_init=True, t_capacity=64)
+        for n in (1, 2):
+            st.set(1, n, p[n - 1])
+            st.set(2, n, q[n - 1])
+        return st
+
+    Xb = dev.tensor(bd, batch)
+    st = stream_with(30)
+    u, _, _ = st.update_last_mode_with(Xb, np.arange(1, 31))
+    worst = np.linalg.norm(u - u_full) / np.linalg.norm(u_full)
+    state_u = [model[0], model[1]]
+    state_p, state_q = list(p), list(q)
+    for n in (1, 2):
+        co = orc.codomain_size(bd, n)
+        sn = stream_with(co)
+        for k in (1, 2):
+            sn.set(0, k, state_u[k - 1])
+            sn.set(1, k, state_p[k - 1])
+            sn.set(2, k, state_q[k - 1])
+        sn.update_mode_with(Xb, u, n, np.arange(1, co + 1))
+        state_u[n - 1], state_p[n - 1], state_q[n - 1] = sn.factor(n), sn.p(n), sn.q(n)
+        worst = max(worst, np.linalg.norm(state_p[n - 1] - pf[n - 1]) / np.linalg.norm(pf[n - 1]))
+        worst = max(worst, np.linalg.norm(state_q[n - 1] - qf[n - 1]) / np.linalg.norm(qf[n - 1]))
+        worst = max(worst, np.linalg.norm(state_u[n - 1] - fh[n - 1]) / np.linalg.norm(fh[n - 1]))
+    assert worst <= TOL["exhaustive_equivalence"], worst
