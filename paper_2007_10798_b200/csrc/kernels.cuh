@@ -728,17 +728,6 @@ __global__ void k_mul_uq(const double* __restrict__ U, int32_t I, int R, const d
     }
 }
 
-// Row-major <-> column-major transpose of an I x R matrix.
-__global__ void k_transpose(const double* __restrict__ in, int64_t rows, int64_t cols,
-                            double* __restrict__ out) {
-    // in: rows x cols row-major -> out: rows x cols column-major
-    const int64_t total = rows * cols;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i = e / cols, j = e - i * cols;
-        out[j * rows + i] = in[e];
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Synthetic data (gen_synthetic semantics, synthetic.cpp:8-31): signal in the
 // canonical x_hat order, Philox/Box-Muller noise keyed by the flat index,
@@ -852,8 +841,6 @@ struct ChainParams {
     double* gch;              // N x S x RP: Z of the mode stages
     double* gpart;            // nsuper x R x R Gram superchunk partials
     double* chpart;           // nchunks x R x R Gram chunk partials (phase 0)
-    int gram_first;           // first Gram block (-1: the last gram_blocks blocks)
-    int coop_combine;         // 1: combine loads by all threads instead of one bulk copy
     double* cpart;            // nsuper x rows x R
     double* LD;               // R x R (L(i,k) at [k*R + i], i > k) + R (D)
     int* mode_flag;           // [0]: 0 = zero solution, 1 = solve
@@ -901,11 +888,8 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 constexpr int kChainThreads = 256;
 constexpr int kCRB = 8;        // padding unit of R (RP = multiple of 8)
 constexpr int kLdStride = 65;  // smem row stride of the factorization triangle (R <= 64)
-constexpr int kGramSplit = 4;  // Gram output ranges per superchunk
-constexpr int kResidCols = 64; // columns per residual item
 constexpr int kMaxPairsPerThread = (64 * 65 / 2 + kChainThreads - 1) / kChainThreads;
 
-__device__ __forceinline__ int chain_zslot(int st, int b, int N) { return st == 0 ? ((b & 1) ? N : 0) : st; }
 
 // Canonical LDL^T of G (R x R column-major in smem) by one block, one barrier
 // per pivot step; same per-element operation sequence as k_solve / the oracle.
@@ -1218,10 +1202,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     const bool gram_one = int64_t(NPp) * nch <= kGramOneBlock;
     const int n_gram = nsuper * kGramSplitC;
     const int gram_blocks = gram_one ? 1 : min(n_gram, max(1, G / 4));
-    const int cblocks = G - gram_blocks;  // contraction blocks
-    const int gb0 = (p.gram_first >= 0 && p.gram_first + gram_blocks <= G) ? p.gram_first : cblocks;
-    const bool is_gram_block = int(blockIdx.x) >= gb0 && int(blockIdx.x) < gb0 + gram_blocks;
-    const int cix = int(blockIdx.x) < gb0 ? int(blockIdx.x) : int(blockIdx.x) - gram_blocks;  // contraction index
+    const int cblocks = G - gram_blocks;  // contraction blocks [0, cblocks), Gram blocks after them
+    const int gb0 = cblocks;
+    const bool is_gram_block = int(blockIdx.x) >= gb0;
+    const int cix = int(blockIdx.x);  // contraction index
     double* xs = sm + kSmXs;
     double* zs = sm + kSmZs;
     double* cps = zs + kSuperSamples * RP;
@@ -1393,14 +1377,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     double* colb = Gs + 64 * 64;     // 3 x 32 (ldlt_warp column buffers)
                     // total = superchunk sums in order; Q += G for the modes (rocp.cpp:108)
                     double* chs = sm;  // gram_one: every chunk partial, one TMA bulk copy (nch x NPp <= 16384)
-                    if (gram_one && !p.coop_combine && tid == 0) {
+                    if (gram_one && tid == 0) {
                         const unsigned bytes = unsigned(nch * NPp * 8);
                         fence_proxy_async();
                         tma_load_1d(chs, p.chpart, bytes, &bar);
                         mbar_expect_tx(&bar, bytes);
-                    }
-                    if (gram_one && p.coop_combine) {
-                        for (int e = tid; e < nch * NPp; e += blockDim.x) chs[e] = __ldcg(p.chpart + e);
                     }
                     // Q entries of this thread's first kQPre pairs (prefetched in phase 0 when gram_one)
                     if (!gram_one) {
@@ -1414,11 +1395,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                             }
                         }
                     }
-                    if (gram_one && !p.coop_combine) {
+                    if (gram_one) {
                         mbar_wait(&bar, phase);
                         phase ^= 1u;
                     }
-                    if (gram_one && p.coop_combine) __syncthreads();
                     if (tr && tid == 0) tr[18] = gtimer();
 #pragma unroll
                     for (int u = 0; u < kMaxPairsPerThread; ++u) {

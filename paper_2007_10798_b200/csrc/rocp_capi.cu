@@ -975,10 +975,6 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
     p.gch = st->zmodes.p;
     p.gpart = st->gpart.p;
     p.chpart = st->chpart.p;
-    static const int gram_first = std::getenv("ROCP_GRAM_FIRST") ? std::atoi(std::getenv("ROCP_GRAM_FIRST")) : -1;
-    static const int coop = std::getenv("ROCP_COOP_COMBINE") ? std::atoi(std::getenv("ROCP_COOP_COMBINE")) : 0;
-    p.gram_first = gram_first;
-    p.coop_combine = coop;
     p.cpart = st->dev->contract_partial.p;
     p.LD = st->LD.p;
     p.mode_flag = st->mode_flag.p;
