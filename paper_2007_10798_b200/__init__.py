@@ -26,7 +26,7 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librocp_b200.so")
+LIB_PATH = os.environ.get("ROCP_B200_LIB") or os.path.join(_HERE, "_lib", "librocp_b200.so")  # override: profiling builds
 
 # status codes (include/rocp_b200.h)
 OK, E_DOMAIN, E_NUMERICAL, E_CUDA, E_NCCL, E_OOM, E_STATE, E_IO = range(8)
