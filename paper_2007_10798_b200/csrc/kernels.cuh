@@ -1104,9 +1104,10 @@ constexpr int kRedStride = 33;  // padded row stride of the blocked partials (ba
 // x (column group cg = lane % 4: columns cg*CPL .. cg*CPL + CPL - 1), so one
 // sample costs 2 + CPL/2 shared loads for 4*CPL fmas.  Each output's chunk
 // partial is its fma chain over the chunk's samples from +0.0 (canonical);
-// after the compute the X and Z tile regions (contiguous, 8 x RP x 33 <= 16896
-// of their 8192 + 256 RP doubles) hold every warp's partials and the
-// superchunk partial sums them in chunk order.
+// after the compute the X tile region holds the partials of one column half at
+// a time (8 x RP/2 x 33 doubles; the Z tile stays resident for the block's
+// next item of the same superchunk) and the superchunk partial sums them in
+// chunk order.
 template <int CPL>
 __device__ __noinline__ void chain_contract_blocked(const double* xs, const double* zs, double* red, int cc0, int ccn,
                                                     int nk, int nrows, int R, double* out_rows) {
@@ -1133,23 +1134,28 @@ __device__ __noinline__ void chain_contract_blocked(const double* xs, const doub
             }
         }
     }
-    __syncthreads();  // every warp is done with the X and Z tiles
-    if (warp < nk) {
+    __syncthreads();  // every warp is done with the X tile (the Z tile stays resident)
+    constexpr int HC = 2 * CPL;  // columns per half
+    constexpr int RS = (8 * HC * kRedStride <= kSuperSamples * kRowTile) ? kRedStride : kRowTile;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+    for (int h = 0; h < 2; ++h) {
+        if ((cg >> 1) == h && warp < nk) {
 #pragma unroll
-            for (int j = 0; j < CPL; ++j) red[(warp * RP + cg * CPL + j) * kRedStride + 4 * rg + a] = acc[a][j];
-    }
-    __syncthreads();
-    for (int e = tid; e < RP * kRowTile; e += blockDim.x) {
-        const int c = e >> 5, i = e & 31;
-        if (i < nrows && c < R) {
-            double qq = red[c * kRedStride + i];
-            for (int k = 1; k < nk; ++k) qq = qq + red[(k * RP + c) * kRedStride + i];
-            out_rows[int64_t(i) * R + c] = qq;
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) red[(warp * HC + (cg & 1) * CPL + j) * RS + 4 * rg + a] = acc[a][j];
         }
+        __syncthreads();
+        for (int e = tid; e < HC * kRowTile; e += blockDim.x) {
+            const int c = e >> 5, i = e & 31, r = h * HC + c;
+            if (i < nrows && r < R) {
+                double qq = red[c * RS + i];
+                for (int k = 1; k < nk; ++k) qq = qq + red[(k * HC + c) * RS + i];
+                out_rows[int64_t(i) * R + r] = qq;
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
 }
 
 // Shared-memory map of k_chain (doubles):
@@ -1164,6 +1170,7 @@ constexpr int kSmTotal = 27136;                  // doubles
 constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
 constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
 constexpr int kGramOneBlock = 16384;
+constexpr int kGramBlocksMax = 4;  // Gram pre-combine blocks when one block does not hold every partial
 constexpr int kTraceSlots = 24;                  // globaltimer stamps per stage (profiling aid)             // R^2 x chunks combined by one block up to this
 
 // kWide: R in 33..64 (register-blocked contraction); the R <= 32 instance
@@ -1201,7 +1208,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     const int NPp = (npairs + 1) & ~1;  // chunk-partial stride (lower pairs): 16-byte multiple for the bulk copy
     const bool gram_one = int64_t(NPp) * nch <= kGramOneBlock;
     const int n_gram = nsuper * kGramSplitC;
-    const int gram_blocks = gram_one ? 1 : min(n_gram, max(1, G / 4));
+    // the superchunk pre-combine is a few microseconds of work: keep nearly every block
+    // on the contraction, which bounds phase 1 for large R (C4)
+    const int gram_blocks = gram_one ? 1 : min(n_gram, kGramBlocksMax);
     const int cblocks = G - gram_blocks;  // contraction blocks [0, cblocks), Gram blocks after them
     const int gb0 = cblocks;
     const bool is_gram_block = int(blockIdx.x) >= gb0;
@@ -1253,9 +1262,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
 
             // stage start: TMA the first X_s tile of this block (independent of factors);
             // its arrive.expect_tx is issued with the Z tile in phase 1.
-            const bool contract_block = !is_gram_block && cix < n_contract;
+            // item schedule: (tile, superchunk) pairs; the wide kernel gives each block one
+            // superchunk (its Z tile, up to 128 KB, is loaded once per stage), the narrow one
+            // strides over all items
+            const bool zreuse = kWide && cblocks >= nsuper;
+            const int zm = cix % nsuper, zrank = cix / nsuper, zcnt = (cblocks - zm + nsuper - 1) / nsuper;
+            const int first_item = zreuse ? ((zrank < tiles) ? zm * tiles + zrank : n_contract) : cix;
+            const bool contract_block = !is_gram_block && first_item < n_contract;
             if (contract_block && tid == 0) {
-                const int item = cix, tile = item % tiles, m = item / tiles;
+                const int tile = first_item % tiles, m = first_item / tiles;
                 const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                 fence_proxy_async();
                 tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
@@ -1497,16 +1512,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
                 }
             } else {
-                for (int item = cix; item < n_contract; item += cblocks) {
+                for (int item = first_item; item < n_contract;
+                     item = zreuse ? ((item % tiles) + zcnt < tiles ? item + zcnt : n_contract) : item + cblocks) {
                     const int tile = item % tiles, m = item / tiles;
                     const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                     const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
                     if (tid == 0) {
                         fence_proxy_async();
-                        if (item != cix)  // later items: X tile now
+                        if (item != first_item)  // later items: X tile now
                             tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
-                        tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
-                        mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + cn * RP * 8));
+                        const bool zload = !zreuse || item == first_item;
+                        if (zload) tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + (zload ? cn * RP * 8 : 0)));
                     }
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
