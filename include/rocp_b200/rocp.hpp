@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <iosfwd>
 #include <random>
 #include <span>
 #include <stdexcept>
@@ -210,6 +211,22 @@ private:
 
 KruskalModel rocp_run(const DenseTensor& x_init, std::span<const DenseTensor> batches, int rank,
                       const CprandOptions& init_opts, Rng& rng, const RocpConfig& cfg = {});
+
+// ---- binary records (tensor_io.hpp:10-27, rocp.hpp:116-117) ------------------------
+// Byte format of the reference: "ROCP", version 1, u32le order, u64le extents,
+// little-endian binary64 values first index fastest (matrices: order-2,
+// column-major).  std::runtime_error on open / format / truncation errors.
+void write_tensor(const DenseTensor& t, std::ostream& out);
+DenseTensor read_tensor(std::istream& in);
+void write_tensor_file(const DenseTensor& t, const std::string& path);
+DenseTensor read_tensor_file(const std::string& path);
+void write_matrix(const Matrix& m, std::ostream& out);
+Matrix read_matrix(std::istream& in);
+void put_u64le(std::ostream& out, std::uint64_t v);
+std::uint64_t get_u64le(std::istream& in);
+// ComplementaryState: P records, Q records, u64le t_len
+void save_state(const ComplementaryState& state, std::ostream& out);
+ComplementaryState load_state(std::istream& in);
 
 // Device selection for this thread's calls (default: device 0, created lazily).
 void set_device(int device);

@@ -1,11 +1,17 @@
 // rocp_api.cpp -- C++ host API (include/rocp_b200/rocp.hpp) over the C ABI.
 // Every call goes to librocp_b200.so (sm_100a kernels); there is no CPU
 // compute path here apart from argument validation, layout bookkeeping and the
-// reference's own host-side random_model.
+// reference's own host-side random_model and binary record IO.
 
 #include "../../include/rocp_b200/rocp.hpp"
 
 #include "../../include/rocp_b200.h"
+
+#include <bit>
+#include <cstring>
+#include <fstream>
+#include <istream>
+#include <ostream>
 
 #include <cmath>
 #include <memory>
@@ -385,6 +391,104 @@ KruskalModel rocp_run(const DenseTensor& x_init, std::span<const DenseTensor> ba
     RocpStream stream(std::move(init), s, cfg, total);
     for (const DenseTensor& b : batches) stream.consume(b, rng);
     return stream.model();
+}
+
+// ---- binary records (tensor_io.cpp:12-101, rocp.cpp:180-211 semantics) ----------
+namespace {
+
+void put_le(std::ostream& out, std::uint64_t v, int bytes) {
+    char b[8];
+    for (int i = 0; i < bytes; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xffu);
+    out.write(b, bytes);
+}
+
+std::uint64_t get_le(std::istream& in, int bytes) {
+    unsigned char b[8] = {};
+    in.read(reinterpret_cast<char*>(b), bytes);
+    if (!in) throw std::runtime_error("tensor record truncated");
+    std::uint64_t v = 0;
+    for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | b[i];
+    return v;
+}
+
+}  // namespace
+
+void put_u64le(std::ostream& out, std::uint64_t v) { put_le(out, v, 8); }
+std::uint64_t get_u64le(std::istream& in) { return get_le(in, 8); }
+
+void write_tensor(const DenseTensor& t, std::ostream& out) {
+    out.write("ROCP", 4);
+    out.put(char(1));
+    put_le(out, static_cast<std::uint64_t>(t.order()), 4);
+    for (Index d : t.dims()) put_le(out, static_cast<std::uint64_t>(d), 8);
+    for (Index i = 0; i < t.size(); ++i) put_le(out, std::bit_cast<std::uint64_t>(t[i]), 8);
+    if (!out) throw std::runtime_error("tensor write failed");
+}
+
+DenseTensor read_tensor(std::istream& in) {
+    char magic[4] = {};
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "ROCP", 4) != 0) throw std::runtime_error("bad tensor magic");
+    if (in.get() != 1) throw std::runtime_error("unsupported tensor format version");
+    const std::uint64_t order = get_le(in, 4);
+    if (order < 2 || order > 64) throw std::runtime_error("implausible tensor order");
+    Dims dims(order);
+    for (Index& d : dims) d = static_cast<Index>(get_le(in, 8));
+    std::vector<double> v(static_cast<size_t>(element_count(dims)));
+    for (double& x : v) x = std::bit_cast<double>(get_le(in, 8));
+    return DenseTensor(std::move(dims), std::move(v));
+}
+
+void write_tensor_file(const DenseTensor& t, const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot open " + path + " for writing");
+    write_tensor(t, out);
+}
+
+DenseTensor read_tensor_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    return read_tensor(in);
+}
+
+void write_matrix(const Matrix& m, std::ostream& out) {
+    write_tensor(DenseTensor({m.rows(), m.cols()}, std::vector<double>(m.data(), m.data() + m.size())), out);
+}
+
+Matrix read_matrix(std::istream& in) {
+    const DenseTensor t = read_tensor(in);
+    if (t.order() != 2) throw std::runtime_error("expected an order-2 record");
+    Matrix m(t.dims()[0], t.dims()[1]);
+    std::copy(t.data(), t.data() + t.size(), m.data());
+    return m;
+}
+
+void save_state(const ComplementaryState& state, std::ostream& out) {
+    for (const Matrix& p : state.p) write_matrix(p, out);
+    for (const Matrix& q : state.q) write_matrix(q, out);
+    put_u64le(out, static_cast<std::uint64_t>(state.t_len));
+}
+
+ComplementaryState load_state(std::istream& in) {
+    // matrix records until only the 8-byte temporal length is left
+    const auto start = in.tellg();
+    in.seekg(0, std::ios::end);
+    const auto end = in.tellg();
+    in.seekg(start);
+    std::vector<Matrix> recs;
+    while (end - in.tellg() > 8) recs.push_back(read_matrix(in));
+    if (recs.empty() || recs.size() % 2 != 0) throw std::runtime_error("state record must hold matching P and Q lists");
+    ComplementaryState st;
+    const size_t half = recs.size() / 2;
+    st.p.assign(recs.begin(), recs.begin() + static_cast<std::ptrdiff_t>(half));
+    st.q.assign(recs.begin() + static_cast<std::ptrdiff_t>(half), recs.end());
+    st.t_len = static_cast<Index>(get_u64le(in));
+    for (size_t n = 0; n < half; ++n) {
+        if (st.q[n].rows() != st.q[n].cols() || st.q[n].rows() != st.p[n].cols())
+            throw std::runtime_error("state record shape mismatch");
+        st.dims_head.push_back(st.p[n].rows());
+    }
+    return st;
 }
 
 }  // namespace rocp

@@ -5,7 +5,9 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <functional>
+#include <sstream>
 #include <random>
 #include <string>
 #include <vector>
@@ -215,10 +217,56 @@ static void test_stream() {  // test_rocp.cpp:235-294
     CHECK(throws<std::domain_error>([&] { st.consume(DenseTensor({20, 21, 1}), rng2); }));
 }
 
+static void test_records() {  // test_tensor_io.cpp-style round trips; rocp.cpp:180-211
+    DenseTensor t({3, 2, 4});
+    for (Index i = 0; i < t.size(); ++i) t[i] = 0.5 * double(i) - 3.0;
+    std::stringstream buf;
+    write_tensor(t, buf);
+    const std::string bytes = buf.str();
+    CHECK(bytes.size() == 4 + 1 + 4 + 3 * 8 + 24 * 8 && bytes.compare(0, 4, "ROCP") == 0 && bytes[4] == 1);
+    const DenseTensor back = read_tensor(buf);
+    CHECK(back.dims() == t.dims());
+    bool same = true;
+    for (Index i = 0; i < t.size(); ++i) same = same && back[i] == t[i];
+    CHECK(same);
+    // 2 x 2 matrix: column-major values after the 25-byte header
+    Matrix m(2, 2);
+    m(0, 0) = 1.0; m(1, 0) = 3.0; m(0, 1) = 2.0; m(1, 1) = 4.0;
+    std::stringstream mb;
+    write_matrix(m, mb);
+    double v[4];
+    std::memcpy(v, mb.str().data() + 25, sizeof(v));
+    CHECK(v[0] == 1.0 && v[1] == 3.0 && v[2] == 2.0 && v[3] == 4.0);
+    CHECK(read_matrix(mb) == m);
+    std::stringstream bad("ROCX\x01");
+    CHECK(throws<std::runtime_error>([&] { read_tensor(bad); }));
+    std::stringstream trunc(bytes.substr(0, bytes.size() - 8));
+    CHECK(throws<std::runtime_error>([&] { read_tensor(trunc); }));
+    CHECK(throws<std::runtime_error>([&] { read_tensor_file("/nonexistent/x.rocp"); }));
+    // save_state / load_state of a live stream
+    Rng rng(91);
+    KruskalModel truth = random_model({12, 10, 40}, 3, rng);
+    const DenseTensor x = reconstruct_loops(truth, {12, 10, 40});
+    DenseTensor xi({12, 10, 16}), xb({12, 10, 8});
+    std::copy(x.data(), x.data() + xi.size(), xi.data());
+    std::copy(x.data() + xi.size(), x.data() + xi.size() + xb.size(), xb.data());
+    RocpStream st(cprand_decompose(xi, 3, {}, rng), auto_sample_count(3), {}, 64);
+    st.consume(xb, rng);
+    const ComplementaryState s0 = st.state();
+    std::stringstream sb;
+    save_state(s0, sb);
+    const ComplementaryState s1 = load_state(sb);
+    CHECK(s1.t_len == s0.t_len && s1.t_len == 24 && s1.dims_head == s0.dims_head);
+    bool eq = s1.p.size() == 2 && s1.q.size() == 2;
+    for (size_t n = 0; eq && n < 2; ++n) eq = s1.p[n] == s0.p[n] && s1.q[n] == s0.q[n];
+    CHECK(eq);
+}
+
 int main() {
     const std::vector<std::pair<const char*, std::function<void()>>> cases = {
         {"index_map", test_index_map}, {"draws_and_gather", test_draws_and_gather}, {"skr", test_skr},
-        {"solve", test_solve},         {"cprand", test_cprand},                     {"stream", test_stream}};
+        {"solve", test_solve},         {"cprand", test_cprand},                     {"stream", test_stream},
+        {"records", test_records}};
     for (const auto& [name, fn] : cases) {
         const int before = g_fail;
         try {
