@@ -656,7 +656,18 @@ struct ShardWin {
     DBuf<double> Zl;             // S x R, this stage's local Z
     DBuf<double> send, recv;     // V x (R^2 + max rows x R) partial blocks
     DBuf<double> rcols, rgath, rwork, rtmp;  // residual columns (2 x S per rank)
+    // fused exchange over peer memory (shard_host.inc setup_exchange)
+    DBuf<double> x_area;           // [counters][landing x 2][residual landing x 2] of this rank
+    DBuf<uint64_t> x_tab;          // device pointer tables into every rank's area
+    std::vector<void*> x_opened;   // peer areas opened through CUDA IPC
+    size_t x_land = 0, x_rland = 0;
+    uint64_t x_target[2] = {0, 0}; // cumulative arrivals expected (partials, residual)
+    int x_parity[2] = {0, 0};
+    ~ShardWin() {
+        for (void* q : x_opened) cudaIpcCloseMemHandle(q);
+    }
 };
+constexpr size_t kXchgHead = 32;  // doubles before the landing buffers (the two counters, padded)
 
 struct rocp_stream {
     rocp_dev* dev = nullptr;

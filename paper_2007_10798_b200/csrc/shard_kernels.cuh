@@ -90,9 +90,38 @@ struct SegPartParams {
     int64_t rows;
     int R, nseg;
     int64_t blk;          // R*R + rows*R doubles per slot
-    double* slots;        // nseg slots [G_v | part_v]
+    double* slots;        // nseg slots [G_v | part_v] (local; when peers == nullptr)
     int32_t off[kMaxShards + 1];  // segment starts in the compacted order
+    // fused exchange over peer memory: slot v of this rank is stored straight into
+    // every rank's landing buffer at global slot slot0 + v, then every block adds 1
+    // to every rank's exchange counter (release, system scope)
+    double* const* peers;                       // world landing bases (device array) or nullptr
+    unsigned long long* const* peer_counters;   // world exchange counters
+    int world;
+    int slot0;
 };
+
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Block-wide wait until an exchange counter reaches `target` (every rank's blocks arrived).
+__device__ __forceinline__ void wait_counter(const unsigned long long* c, unsigned long long target) {
+    if (c && threadIdx.x == 0)
+        while (ld_acquire_sys_u64(c) < target) __nanosleep(64);
+    __syncthreads();
+}
+// Every block: its stores are made visible system-wide, then +1 on each rank's counter.
+__device__ __forceinline__ void arrive_all(unsigned long long* const* counters, int world) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int g = 0; g < world; ++g) red_release_sys_add(counters[g], 1ull);
+}
 
 constexpr int kSegRG = 8;  // contraction outputs per work item
 
@@ -121,8 +150,7 @@ __device__ __forceinline__ void seg_dot8(const double* __restrict__ X, const dou
         for (int j = 0; j < kSegRG; ++j) tot[j] = (m0 == 0) ? q[j] : tot[j] + q[j];
     }
 #pragma unroll
-    for (int j = 0; j < kSegRG; ++j)
-        if (j < nr) out[i * R + r0 + j] = tot[j];
+    for (int j = 0; j < kSegRG; ++j) out[j] = tot[j];  // the caller stores the first nr
 }
 
 __global__ void __launch_bounds__(256) k_seg_partials(const SegPartParams p) {
@@ -150,15 +178,31 @@ __global__ void __launch_bounds__(256) k_seg_partials(const SegPartParams p) {
                 }
                 tot = (m0 == 0) ? q : tot + q;
             }
-            slot[t] = tot;
+            if (p.peers) {
+                for (int gr = 0; gr < p.world; ++gr) p.peers[gr][int64_t(p.slot0 + v) * p.blk + t] = tot;
+            } else {
+                slot[t] = tot;
+            }
         } else {  // contraction outputs (i, r0 .. r0 + 7)
             const int64_t u = t - RR;
             const int64_t i = u % p.rows;
             const int g = int(u / p.rows);
             const int r0 = g * kSegRG, nr = min(kSegRG, R - r0);
-            seg_dot8(p.X, p.Z, p.rows, R, i, r0, nr, c0, n, slot + RR);
+            double vals[kSegRG];
+            seg_dot8(p.X, p.Z, p.rows, R, i, r0, nr, c0, n, vals);
+#pragma unroll
+            for (int j = 0; j < kSegRG; ++j) {
+                if (j >= nr) break;
+                const int64_t o = RR + i * R + r0 + j;
+                if (p.peers) {
+                    for (int gr = 0; gr < p.world; ++gr) p.peers[gr][int64_t(p.slot0 + v) * p.blk + o] = vals[j];
+                } else {
+                    slot[o] = vals[j];
+                }
+            }
         }
     }
+    if (p.peers) arrive_all(p.peer_counters, p.world);
 }
 
 // Fixed-order combine of the V exchanged partial blocks [G_v | part_v]:
@@ -166,10 +210,12 @@ __global__ void __launch_bounds__(256) k_seg_partials(const SegPartParams p) {
 // Q + G) or out = tot.
 __global__ void __launch_bounds__(256) k_shard_combine(const double* __restrict__ parts, int V, int64_t blk, int64_t RR,
                                                        const double* base_g, double* out_g, const double* base_p,
-                                                       double* out_p) {
+                                                       double* out_p, const unsigned long long* counter,
+                                                       unsigned long long target) {
+    wait_counter(counter, target);  // fused exchange: every rank's slots have landed
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < blk; e += int64_t(gridDim.x) * blockDim.x) {
-        double tot = __ldg(parts + e);
-        for (int v = 1; v < V; ++v) tot = tot + __ldg(parts + int64_t(v) * blk + e);
+        double tot = __ldcg(parts + e);
+        for (int v = 1; v < V; ++v) tot = tot + __ldcg(parts + int64_t(v) * blk + e);
         if (e < RR) out_g[e] = base_g ? base_g[e] + tot : tot;
         else out_p[e - RR] = base_p ? base_p[e - RR] + tot : tot;
     }
@@ -207,11 +253,25 @@ __global__ void __launch_bounds__(256) k_shard_resid_cols(const double* __restri
 
 // Sum of the ranks' scattered column arrays (each column non-zero on exactly
 // one rank, so the sum is exact), then the canonical hsum of both -> out[0..1].
+// Fused exchange of the residual columns: this rank's 2 x S column vector into
+// slot `rank` of every rank's landing buffer, then the counters.
+__global__ void __launch_bounds__(256) k_shard_resid_push(const double* __restrict__ cols, int32_t S,
+                                                          double* const* peers, unsigned long long* const* counters,
+                                                          int world, int rank) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * S; e += gridDim.x * blockDim.x) {
+        const double v = cols[e];
+        for (int g = 0; g < world; ++g) peers[g][int64_t(rank) * 2 * S + e] = v;
+    }
+    arrive_all(counters, world);
+}
+
 __global__ void __launch_bounds__(256) k_shard_resid_sum(const double* __restrict__ gathered, int world, int32_t S,
-                                                         double* work, double* tmp, double* out) {
+                                                         double* work, double* tmp, double* out,
+                                                         const unsigned long long* counter, unsigned long long target) {
+    wait_counter(counter, target);
     for (int e = threadIdx.x; e < 2 * S; e += blockDim.x) {
-        double v = gathered[e];
-        for (int g = 1; g < world; ++g) v = v + gathered[int64_t(g) * 2 * S + e];
+        double v = __ldcg(gathered + e);
+        for (int g = 1; g < world; ++g) v = v + __ldcg(gathered + int64_t(g) * 2 * S + e);
         work[e] = v;
     }
     __syncthreads();
