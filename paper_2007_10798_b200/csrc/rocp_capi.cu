@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <immintrin.h>
 #include <nccl.h>  // types only: the library is bound at run time (NcclApi)
 #include <sys/mman.h>
 
@@ -1077,10 +1078,17 @@ void host_gather_task(rocp_stream* st, const double* hx, int64_t slice, int64_t 
                 std::memcpy(dst + xs_offset(i0, c, S), f + i0, size_t(std::min<int64_t>(32, I - i0)) * 8);
         } else {
             for (int64_t i0 = 0; i0 < I; i0 += 32) {
-                double* o = dst + xs_offset(i0, c, S);
+                double* o = dst + xs_offset(i0, c, S);  // 256-byte aligned run of 32
                 const int64_t n = std::min<int64_t>(32, I - i0);
                 const double* fi = f + i0 * ms;
-                for (int64_t i = 0; i < n; ++i) o[i] = fi[i * ms];
+                if (n == 32) {
+                    // streaming stores: the staging lines are written whole, never read for ownership
+                    for (int64_t q = 0; q < 32; q += 4)
+                        _mm256_stream_pd(o + q, _mm256_set_pd(fi[(q + 3) * ms], fi[(q + 2) * ms], fi[(q + 1) * ms],
+                                                              fi[q * ms]));
+                } else {
+                    for (int64_t i = 0; i < n; ++i) o[i] = fi[i * ms];
+                }
             }
         }
     }
@@ -1224,6 +1232,7 @@ void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb
         for (size_t k = next.fetch_add(1, std::memory_order_relaxed); k < tasks.size();
              k = next.fetch_add(1, std::memory_order_relaxed)) {
             host_gather_task(st, hx, slice, B, d, strides, tasks[k]);
+            _mm_sfence();  // this task's streaming stores are globally visible before the batch counts down
             remaining[size_t(tasks[k].b)].fetch_sub(1, std::memory_order_release);
             if (is_caller) try_issue(false);
         }
