@@ -122,6 +122,7 @@ struct GatherJob {
     int32_t s;
     double* out;
     int tiled;   // 0: I x s column-major; 1: row-tiled (see xs_offset)
+    const int32_t* perm;  // row-tiled strided jobs: samples in fibre-base order (or nullptr)
 };
 
 // Row-tiled X_s layout (stream windows): rows in tiles of 32, each tile's
@@ -140,10 +141,36 @@ constexpr int kGatherThreads = 256;
 constexpr int kGatherUnroll = 8;
 constexpr int kGatherTile = kGatherThreads * kGatherUnroll;
 
+// Sorted tiles (J.perm): tile.e0 = group << 16 | i-block; warp w takes the
+// (8 group + w)-th sample in fibre-base order and 8 x 32 consecutive fibre
+// elements, so the 8 warps of a block read neighbouring fibres at the same
+// element (shared DRAM pages) while each warp writes one contiguous tiled run.
+constexpr int kSortedGroup = kGatherThreads / 32;                 // samples per sorted tile
+constexpr int kSortedSpan = 32 * kGatherUnroll;                   // fibre elements per sorted tile
+
 __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherJob* __restrict__ jobs,
                                                            const GatherTile* __restrict__ tiles) {
     const GatherTile tile = tiles[blockIdx.x];
     const GatherJob& J = jobs[tile.job];
+    if (J.perm) {
+        const int q = int(tile.e0 >> 16) * kSortedGroup + int(threadIdx.x >> 5);
+        if (q >= J.s) return;
+        const int c = __ldg(J.perm + q);
+        const double* a = J.t + __ldg(J.base + c);
+        const int i0 = int(tile.e0 & 0xffffu) * kSortedSpan + int(threadIdx.x & 31);
+        double v[kGatherUnroll];
+#pragma unroll
+        for (int u = 0; u < kGatherUnroll; ++u) {
+            const int i = i0 + 32 * u;
+            if (i < J.I) asm volatile("ld.global.cs.L2::64B.f64 %0, [%1];" : "=d"(v[u]) : "l"(a + int64_t(i) * J.ms));
+        }
+#pragma unroll
+        for (int u = 0; u < kGatherUnroll; ++u) {
+            const int i = i0 + 32 * u;
+            if (i < J.I) J.out[xs_offset(i, c, J.s)] = v[u];
+        }
+        return;
+    }
     const uint32_t total = uint32_t(J.I) * uint32_t(J.s);
     const double* __restrict__ t = J.t;
     const int64_t* __restrict__ base = J.base;
@@ -179,6 +206,48 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherJob* __re
             }
         }
     }
+}
+
+// Samples of one stage in fibre-base order (bitonic sort in shared memory,
+// s <= 2048): the sorted gather's visiting order only -- results are unchanged.
+struct SortJob {
+    const int64_t* base;
+    int32_t* perm;
+    int32_t s;
+};
+constexpr int kSortMax = 2048;
+
+__global__ void __launch_bounds__(1024) k_sort_by_base(const SortJob* __restrict__ jobs) {
+    const SortJob J = jobs[blockIdx.x];
+    __shared__ int64_t key[kSortMax];
+    __shared__ int32_t val[kSortMax];
+    int P = 1;
+    while (P < J.s) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        key[i] = (i < J.s) ? J.base[i] : 0x7fffffffffffffffLL;
+        val[i] = i;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const bool gt = key[i] > key[ixj] || (key[i] == key[ixj] && val[i] > val[ixj]);
+                    if (gt == up) {
+                        const int64_t tk = key[i];
+                        key[i] = key[ixj];
+                        key[ixj] = tk;
+                        const int32_t tv = val[i];
+                        val[i] = val[ixj];
+                        val[ixj] = tv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < J.s; i += blockDim.x) J.perm[i] = val[i];
 }
 
 // ---------------------------------------------------------------------------

@@ -172,7 +172,8 @@ struct JobList {
     DBuf<DrawJob> draw;
     DBuf<GatherJob> gather;
     DBuf<GatherTile> tiles;
-    int ndraw = 0, ngather = 0, ntiles = 0;
+    DBuf<SortJob> sort;
+    int ndraw = 0, ngather = 0, ntiles = 0, nsort = 0;
     int64_t max_s = 0;
     int64_t gather_elems = 0;
 };
@@ -283,14 +284,24 @@ GatherJob make_gather(const double* t, const std::vector<int64_t>& d, int mode, 
 }
 
 void upload_jobs(rocp_dev* dev, JobList& L, const std::vector<DrawJob>& dj,
-                 const std::vector<GatherJob>& gj) {
+                 const std::vector<GatherJob>& gj, const std::vector<SortJob>& sj = {}) {
     std::vector<GatherTile> tiles;
     L.gather_elems = 0;
     for (size_t k = 0; k < gj.size(); ++k) {
         const uint32_t total = uint32_t(gj[k].I) * uint32_t(gj[k].s);
         L.gather_elems += total;
-        for (uint32_t e0 = 0; e0 < total; e0 += kGatherTile) tiles.push_back(GatherTile{int32_t(k), e0});
+        if (gj[k].perm) {  // sorted tiles: element block outer, so co-scheduled blocks read adjacent samples
+            for (uint32_t ib = 0; ib < uint32_t((gj[k].I + kSortedSpan - 1) / kSortedSpan); ++ib)
+                for (uint32_t g = 0; g < uint32_t((gj[k].s + kSortedGroup - 1) / kSortedGroup); ++g)
+                    tiles.push_back(GatherTile{int32_t(k), (g << 16) | ib});
+        } else {
+            for (uint32_t e0 = 0; e0 < total; e0 += kGatherTile) tiles.push_back(GatherTile{int32_t(k), e0});
+        }
     }
+    L.sort.ensure(std::max<size_t>(sj.size(), 1));
+    if (!sj.empty())
+        CK(cudaMemcpyAsync(L.sort.p, sj.data(), sj.size() * sizeof(SortJob), cudaMemcpyHostToDevice, dev->stream));
+    L.nsort = int(sj.size());
     L.max_s = 0;
     for (const DrawJob& j : dj) L.max_s = std::max<int64_t>(L.max_s, j.s);
     L.draw.ensure(std::max<size_t>(dj.size(), 1));
@@ -317,6 +328,10 @@ void launch_draw(rocp_dev* dev, const JobList& L) {
 }
 
 void launch_gather(rocp_dev* dev, const JobList& L) {
+    if (L.nsort > 0) {
+        k_sort_by_base<<<L.nsort, 1024, 0, dev->stream>>>(L.sort.p);
+        after_launch(dev, "k_sort_by_base");
+    }
     if (L.ntiles == 0) return;
     k_gather<<<L.ntiles, kGatherThreads, 0, dev->stream>>>(L.gather.p, L.tiles.p);
     after_launch(dev, "k_gather");
@@ -616,6 +631,7 @@ struct Window {
     int64_t nb = 0, B = 0;     // capacity
     DBuf<int32_t> idx;         // [b][stage] S x (N-1)
     DBuf<int64_t> base, rows;  // [b][stage] S
+    DBuf<int32_t> perm;        // [b][stage] S: strided stages' samples in fibre-base order (sorted gather)
     DBuf<double> X;            // [b][stage] I_stage x S (column-major)
     std::vector<int64_t> xoff;
     DBuf<int64_t> xoff_dev;
@@ -753,6 +769,7 @@ void ensure_window(rocp_stream* st, int64_t nb, int64_t B) {
     const int N = st->N;
     const int64_t S = st->s;
     W.idx.alloc(size_t(nbn * N * S * (N - 1)));
+    W.perm.alloc(size_t(nbn * N * S));
     W.base.alloc(size_t(nbn * N * S));
     W.rows.alloc(size_t(nbn * N * S));
     W.xoff.assign(size_t(nbn * N), 0);
@@ -807,6 +824,7 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
     const std::vector<int64_t> d = slab_dims(st, B);
     std::vector<DrawJob> dj;
     std::vector<GatherJob> gj;
+    std::vector<SortJob> sj;
     const std::vector<int64_t> strides = strides_of(d);
     W.zc_tile.assign(size_t(nb + 1), 0);
     int64_t ntile = 0;
@@ -822,7 +840,12 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
             j.batch_ptr = st->batch_dev.p;
             dj.push_back(j);
             if (!host_gather) {
-                gj.push_back(make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage), 1));
+                GatherJob g = make_gather(xb, d, mode, st->s, win_base(st, b, stage), win_x(st, b, stage), 1);
+                if (strides[size_t(mode - 1)] != 1 && st->s <= kSortMax) {  // strided: fibre-base order
+                    g.perm = st->win.perm.p + (b * st->N + stage) * st->s;
+                    sj.push_back(SortJob{win_base(st, b, stage), const_cast<int32_t*>(g.perm), int32_t(st->s)});
+                }
+                gj.push_back(g);
             } else if (zc_src && strides[size_t(mode - 1)] == 1) {
                 gj.push_back(make_gather(zc_src + (t0 + b * B) * slice, d, mode, st->s, win_base(st, b, stage),
                                          win_x(st, b, stage), 1));
@@ -831,7 +854,7 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
         }
     }
     W.zc_tile[size_t(nb)] = ntile;
-    upload_jobs(st->dev, W.jobs, dj, gj);
+    upload_jobs(st->dev, W.jobs, dj, gj, sj);
     W.key_x = x;
     W.key_t0 = t0;
     W.key_B = B;
