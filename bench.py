@@ -339,6 +339,7 @@ def main():
     barrier(dist)
     launches = dev.kernel_launches - l0
     gather_ms = stream.gather_times()
+    chain_ms = stream.chain_times()
     stream.time_gather(False)
     ms_max = max_over_ranks(ms, dist, torch)
     value = (1 if sharded else world) * args.steps * slices_per_step / (ms_max / 1000.0)
@@ -357,6 +358,24 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+
+    # ---- secondary roofline: the persistent chain (K3-K6), latency-bound by design
+    # (SURVEY.md 8d): algorithmic fp64 flops per launch (contraction 2 S R (B + sum I)
+    # + Gram S R (R+1) per stage, per batch) over its CUDA-event launch time, against
+    # the fp64 CUDA-core peak derived from the SM count and max clock (not in
+    # MEASURED_PEAKS.json): SMs x 64 FMA/clk x 2 x clock.
+    chain_roof = None
+    if chain_ms:
+        flops = nb * (2 * S * R * (B + sum(head)) + len(dims) * S * R * (R + 1))
+        c_avg = statistics.mean(chain_ms)
+        fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+        chain_roof = {"kernel": "k_chain (persistent factor-dependent chain, one launch per window)",
+                      "bound": "latency (dependent Gauss-Seidel chain; fp64 pipe as the compute ceiling)",
+                      "achieved": flops / (c_avg / 1000.0) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                      "frac": flops / (c_avg / 1000.0) / 1e12 / fp64_peak,
+                      "peak_source": "derived: 148 SMs x 64 fp64 FMA/clk x 2 x 1.965 GHz",
+                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": c_avg,
+                      "share_of_step": sum(chain_ms) / ms, "launches": len(chain_ms)}
 
     # ---- e2e through the host-slab call: the caller's slabs stay in (pinned) host memory;
     # only the sampled fibres cross PCIe (host gather), the model is read back every step
@@ -427,6 +446,7 @@ def main():
                          "useful_bytes_per_launch": useful_per_launch,
                          "avg_launch_ms": g_avg_ms, "launches": len(gather_ms),
                          "share_of_step": (sum(gather_ms) / ms) if gather_ms else None},
+            "roofline_chain": chain_roof,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -226,14 +226,16 @@ rocp_status rocp_stream_restore(rocp_stream* st);
 /* Sampled residual per batch: 0 off, 1 temporal solve only (default), 2 every
  * stage. */
 rocp_status rocp_stream_set_residual_tracking(rocp_stream* st, int level);
-/* CUDA events around every window gather launch (the HBM-bound kernel):
- * enable, then read the per-launch milliseconds (resets the list). */
+/* CUDA events around every window gather launch (the HBM-bound kernel) and
+ * every persistent chain launch: enable, then read the per-launch
+ * milliseconds (each call resets its list). */
 rocp_status rocp_stream_time_gather(rocp_stream* st, int enable);
 rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* count);
-/* Profiling aid: globaltimer stamps of the persistent chain kernel, 8 per
- * (batch, stage) of the last window: stage start, phase-1 items done (block
- * 0), last-block start/end, after barrier 1, phase 2 done (block 0), after
- * barrier 2.  enable toggles recording; out may be NULL. */
+rocp_status rocp_stream_chain_times(rocp_stream* st, float* ms, int max, int* count);
+/* Profiling aid: globaltimer stamps of the persistent chain kernel, 24 per
+ * (batch, stage) of the last window (phase boundaries, Gram finisher steps,
+ * row solves; tools_trace.py decodes them).  enable toggles recording; out
+ * may be NULL. */
 rocp_status rocp_stream_chain_trace(rocp_stream* st, int enable, uint64_t* out, int64_t max,
                                     int64_t* count);
 /* Elements (and useful bytes) the current window's gather moves per launch. */

@@ -110,6 +110,7 @@ SIGNATURES = [
     ("rocp_stream_set_residual_tracking", C.c_int, [_vp, C.c_int]),
     ("rocp_stream_time_gather", C.c_int, [_vp, C.c_int]),
     ("rocp_stream_gather_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
+    ("rocp_stream_chain_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
     ("rocp_stream_window_bytes", C.c_int, [_vp, _i64p, _i64p]),
     ("rocp_stream_chain_trace", C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
 ]
@@ -693,6 +694,12 @@ class RocpStream:
         buf = (C.c_float * max_n)()
         cnt = C.c_int(0)
         self.dev.check(lib().rocp_stream_gather_times(self.h, buf, max_n, C.byref(cnt)))
+        return [float(buf[k]) for k in range(min(cnt.value, max_n))]
+
+    def chain_times(self, max_n=4096):
+        buf = (C.c_float * max_n)()
+        cnt = C.c_int(0)
+        self.dev.check(lib().rocp_stream_chain_times(self.h, buf, max_n, C.byref(cnt)))
         return [float(buf[k]) for k in range(min(cnt.value, max_n))]
 
     def chain_trace(self, enable=None, fetch=True):

@@ -726,12 +726,16 @@ struct rocp_stream {
     bool ck_reg = false;
     // gather timing (events around each window gather launch)
     bool time_gather = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_events;
-    size_t gather_events_used = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_events, chain_events;
+    size_t gather_events_used = 0, chain_events_used = 0;
     // CUDA graphs of the chain keyed by (nb, B, t_len)
     std::map<std::tuple<int64_t, int64_t, int64_t>, std::pair<cudaGraphExec_t, uint64_t>> graphs;
     ~rocp_stream() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+        for (auto& e : chain_events) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
         for (auto& e : gather_events) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -1025,7 +1029,20 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
     } else {
         p.trace = nullptr;
     }
-    launch_chain_k(st, p);
+    if (st->time_gather) {  // kernel timing: events around the persistent chain too
+        if (st->chain_events_used == st->chain_events.size()) {
+            cudaEvent_t a, e;
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&e));
+            st->chain_events.emplace_back(a, e);
+        }
+        auto& ev = st->chain_events[st->chain_events_used++];
+        CK(cudaEventRecord(ev.first, st->dev->stream));
+        launch_chain_k(st, p);
+        CK(cudaEventRecord(ev.second, st->dev->stream));
+    } else {
+        launch_chain_k(st, p);
+    }
     if (st->resid_level >= 1) {  // sampled residual of every batch's temporal solve (off the chain)
         WinResidParams w{};
         w.N = st->N;
@@ -2245,10 +2262,22 @@ rocp_status rocp_stream_set_residual_tracking(rocp_stream* st, int enable) {
     });
 }
 
+rocp_status rocp_stream_chain_times(rocp_stream* st, float* ms, int max, int* count) {
+    return guarded(st->dev, [&] {
+        CK(cudaStreamSynchronize(st->dev->stream));
+        const int n = int(std::min<size_t>(st->chain_events_used, size_t(std::max(max, 0))));
+        for (int k = 0; k < n; ++k)
+            CK(cudaEventElapsedTime(ms + k, st->chain_events[size_t(k)].first, st->chain_events[size_t(k)].second));
+        *count = int(st->chain_events_used);
+        st->chain_events_used = 0;
+    });
+}
+
 rocp_status rocp_stream_time_gather(rocp_stream* st, int enable) {
     return guarded(st->dev, [&] {
         st->time_gather = enable != 0;
         st->gather_events_used = 0;
+        st->chain_events_used = 0;
     });
 }
 
