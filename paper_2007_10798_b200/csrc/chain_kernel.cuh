@@ -1,0 +1,858 @@
+// chain_kernel.cuh -- K6, the persistent factor-dependent chain of a stream
+// window (k_chain), and the window residual pass that follows it.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace rocpk {
+
+// ===========================================================================
+// K6: persistent stream chain.  One cooperative launch (148 blocks x 256) runs
+// the whole factor-dependent chain of a window of nb batches
+// (RocpStream::consume, rocp.cpp:144-160, after the hoisted draw + gather):
+// for every batch the temporal stage (update_last_mode_with, rocp.cpp:71-84),
+// then modes 1..N-1 (update_mode_with, rocp.cpp:96-113, Gauss-Seidel).  Per
+// stage (DESIGN.md section 5 has the measured phase budget):
+//   stage start  contraction blocks start a TMA bulk copy of their X_s tile
+//                (row-tiled layout: one contiguous block; X_s never depends on
+//                factors); the Gram finisher prefetches its Q entries
+//   phase 0      sampled Khatri-Rao Z (S x RP, zero padded), one 32-sample
+//                chunk per block, and that chunk's Gram partial       | grid barrier
+//   phase 1      concurrently:
+//                - contraction blocks: Z tile by TMA; warp w = chunk w of the
+//                  superchunk; superchunk partials of X_s Z (register-blocked
+//                  variant for R in 33..64, k_chain<true>)
+//                - the Gram finisher: chunk partials summed in order (one TMA
+//                  bulk copy when they fit, else 4 pre-combine blocks), Q += G,
+//                  canonical LDL^T (ldlt_warp for R <= 32), publishes L, D | grid barrier
+//   phase B      warp per row: superchunk partials in order, P += X_s Z,
+//                forward / diagonal / backward solve -> U(n) or u_new row | grid barrier
+// Arithmetic is exactly that of the per-stage kernels (bitwise equal).
+
+struct ChainParams {
+    int N, R, S, nb, B, nsuper, resid_level;
+    int32_t head[kMaxOrder];
+    double* U[kMaxOrder];  // U[n-1], n = 1..N-1, row-major I_n x R
+    double* P[kMaxOrder];
+    double* Q[kMaxOrder];
+    double* temporal;      // row-major; batch b's rows start at t_len0 + b*B
+    int64_t t_len0;
+    const int32_t* idx_base;  // window: [b][stage] S x (N-1)
+    const double* X_base;     // window: [b][stage] row-tiled I_stage x S
+    const int64_t* xoff;      // [b*N + stage]
+    double* zbuf;             // nb x S x RP: the temporal Z of each batch (window residual pass)
+    double* gch;              // N x S x RP: Z of the mode stages
+    double* gpart;            // nsuper x R x R Gram superchunk partials
+    double* chpart;           // nchunks x R x R Gram chunk partials (phase 0)
+    double* cpart;            // nsuper x rows x R
+    double* LD;               // R x R (L(i,k) at [k*R + i], i > k) + R (D)
+    int* mode_flag;           // [0]: 0 = zero solution, 1 = solve
+    int* flags;               // stream flags ([0] temporal regularized, [2] mode solve)
+    double* resid;            // N x 2 (num, den) of the last batch
+    double* rpart;            // 3 x S
+    unsigned int* counter;    // [0] Gram arrivals, [1] residual arrivals
+    unsigned long long* trace;  // optional phase timestamps (globaltimer ns), 16 per stage
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers ----------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int kChainThreads = 256;
+constexpr int kCRB = 8;        // padding unit of R (RP = multiple of 8)
+constexpr int kLdStride = 65;  // smem row stride of the factorization triangle (R <= 64)
+constexpr int kMaxPairsPerThread = (64 * 65 / 2 + kChainThreads - 1) / kChainThreads;
+
+
+// Canonical LDL^T of G (R x R column-major in smem) by one block, one barrier
+// per pivot step; same per-element operation sequence as k_solve / the oracle.
+// Thread t owns the lower-triangle pairs t, t + 256, ... (column order).
+// d_{k+1} is formed redundantly in registers by every thread that needs it
+// (its last update), so the diagonal entry is never written in the step that
+// finishes it.  L(i,k) at A[k*kLdStride + i].
+__device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double lambda, const double* G,
+                                           const unsigned short* pairs, int npairs) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    int pi[kMaxPairsPerThread], pj[kMaxPairsPerThread];
+#pragma unroll
+    for (int u = 0; u < kMaxPairsPerThread; ++u) {
+        const int pp = tid + u * nt;
+        pi[u] = (pp < npairs) ? (pairs[pp] >> 8) : -1;
+        pj[u] = (pp < npairs) ? (pairs[pp] & 0xff) : -1;
+    }
+    for (int t = tid; t < R * R; t += nt) {
+        const int i = t % R, j = t / R;
+        if (i >= j) A[i * kLdStride + j] = (i == j) ? G[t] + lambda : G[t];
+    }
+    __syncthreads();
+    const double d0 = A[0];
+    if (tid == 0) D[0] = d0;
+    for (int i = 1 + tid; i < R; i += nt) A[i] = (d0 != 0.0) ? A[i * kLdStride] / d0 : 0.0;
+    __syncthreads();
+    for (int k = 0; k + 1 < R; ++k) {
+        const double* rowk = A + k * kLdStride;  // L(., k) in the strict upper part
+        const double dn = __fma_rn(-rowk[k + 1], A[(k + 1) * kLdStride + k], A[(k + 1) * kLdStride + k + 1]);
+        if (tid == 0) D[k + 1] = dn;
+#pragma unroll
+        for (int u = 0; u < kMaxPairsPerThread; ++u) {
+            const int i = pi[u], j = pj[u];
+            if (j > k && !(i == j && j == k + 1)) {
+                const double v = __fma_rn(-rowk[i], A[j * kLdStride + k], A[i * kLdStride + j]);
+                if (j == k + 1) A[(k + 1) * kLdStride + i] = (dn != 0.0) ? v / dn : 0.0;
+                A[i * kLdStride + j] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Canonical LDL^T for R <= MAXR <= 32 by ONE warp, no block barriers: lane i
+// holds row i of the lower triangle in registers.  Step k: d_k = lane k's
+// r[k] (final), l(i,k) = r[k] / d_k on lanes i > k, then r[j] = fma(-l(i,k),
+// a(j,k), r[j]) for k < j <= i with a(j,k) = lane j's r[k].  Identical
+// per-element operation sequence to ldlt_one_sync / k_solve / the oracle.
+// L(i,k) at A[k*kLdStride + i], D in D[].
+//
+// Software-pipelined so a step's critical path is divide -> the single fma
+// that finishes the next pivot column entry -> shuffle of d_{k+1}: the other
+// updates of step k (j >= k+2) are deferred to step k+1, where they fill the
+// shuffle latency before the next divide, and column k+1 is read from shared
+// memory (published one step ahead) while the divide runs.  Upper-triangle
+// registers and lanes >= R receive harmless updates but are never read as
+// lower entries; dividends of inactive lanes are 1.0 (a zero dividend takes
+// the divide's slow path).
+template <int MAXR>
+__device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, double* A, double* D, double* col) {
+    // col: three 32-entry column buffers; column k lives in col[(k % 3) * 32]
+    // from step k-1 (published) to step k+1 (read by the deferred updates).
+    // The fmas read the broadcast column straight from shared memory (no
+    // register copy, which the compiler would place in local memory).
+    const int lane = threadIdx.x & 31;
+    double r[MAXR];
+#pragma unroll
+    for (int j = 0; j < MAXR; ++j)
+        r[j] = (lane < R && j <= lane) ? ((j == lane) ? G[lane + j * R] + lambda : G[lane + j * R]) : 0.0;
+    col[lane] = r[0];
+    __syncwarp();
+    double dk = __shfl_sync(0xffffffffu, r[0], 0);
+    double lp = 0.0;  // l(lane, k-1)
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+        if (k < R) {
+            const double* cb = col + (k % 3) * 32;  // column k
+            if (k > 0) {  // deferred updates of step k-1 (j >= k+1): fill the shuffle latency
+                const double* cp = col + ((k + 2) % 3) * 32;  // column k-1
+#pragma unroll
+                for (int j = k + 1; j < MAXR; ++j) r[j] = __fma_rn(-lp, cp[j], r[j]);
+            }
+            const bool act = lane > k && lane < R;
+            const double num = act ? r[k] : 1.0;
+            const double q = num / dk;
+            const double l = (act && dk != 0.0) ? q : 0.0;
+            double dn = 0.0;
+            if (k + 1 < MAXR) {  // critical: finish a(., k+1), broadcast d_{k+1}, publish column k+1
+                r[k + 1] = __fma_rn(-l, cb[k + 1], r[k + 1]);
+                dn = __shfl_sync(0xffffffffu, r[k + 1], (k + 1) & 31);
+                col[((k + 1) % 3) * 32 + lane] = r[k + 1];
+            }
+            if (lane == 0) D[k] = dk;
+            if (act) A[k * kLdStride + lane] = l;
+            __syncwarp();
+            lp = l;
+            dk = dn;
+        }
+    }
+}
+
+constexpr int kMaxSuperRows = 8;  // superchunk partials prefetched per row entry
+constexpr int kQPre = 3;          // Q pairs per thread prefetched by the Gram finisher
+
+// Row solves of phase 2: warp per row, lanes own entries j and j + 32.
+__device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
+                                             int rows, int R, int nsuper, double* out, const double* Ls,
+                                             const double* Ds, int mode) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int j0 = lane, j1 = lane + 32;
+    const bool v0 = j0 < R, v1 = j1 < R;
+    for (int row = blockIdx.x + warp * gridDim.x; row < rows; row += gridDim.x * nw) {
+        double w0 = 0.0, w1 = 0.0;
+        // every load of the row (superchunk partials, P) in flight at once
+        double c0[kMaxSuperRows], c1[kMaxSuperRows], p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxSuperRows; ++m) {
+            c0[m] = (v0 && m < nsuper) ? __ldcg(cpart + (int64_t(m) * rows + row) * R + j0) : 0.0;
+            c1[m] = (v1 && m < nsuper) ? __ldcg(cpart + (int64_t(m) * rows + row) * R + j1) : 0.0;
+        }
+        if (st > 0) {
+            if (v0) p0 = __ldcg(Prow_base + int64_t(row) * R + j0);
+            if (v1) p1 = __ldcg(Prow_base + int64_t(row) * R + j1);
+        }
+        if (v0) {
+            double tot = c0[0];
+#pragma unroll
+            for (int m = 1; m < kMaxSuperRows; ++m)
+                if (m < nsuper) tot = tot + c0[m];
+            for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j0);
+            if (st > 0) {
+                tot = p0 + tot;
+                Prow_base[int64_t(row) * R + j0] = tot;
+            }
+            w0 = tot;
+        }
+        if (v1) {
+            double tot = c1[0];
+#pragma unroll
+            for (int m = 1; m < kMaxSuperRows; ++m)
+                if (m < nsuper) tot = tot + c1[m];
+            for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j1);
+            if (st > 0) {
+                tot = p1 + tot;
+                Prow_base[int64_t(row) * R + j1] = tot;
+            }
+            w1 = tot;
+        }
+        if (mode == 0) {
+            w0 = 0.0;
+            w1 = 0.0;
+        } else {
+            for (int k = 0; k < R; ++k) {  // forward, k increasing
+                const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+                if (v0 && j0 > k) w0 = __fma_rn(-Ls[k * R + j0], wk, w0);
+                if (v1 && j1 > k) w1 = __fma_rn(-Ls[k * R + j1], wk, w1);
+            }
+            if (v0) w0 = (fabs(Ds[j0]) > 2.2250738585072014e-308) ? w0 / Ds[j0] : 0.0;
+            if (v1) w1 = (fabs(Ds[j1]) > 2.2250738585072014e-308) ? w1 / Ds[j1] : 0.0;
+            for (int k = R - 1; k >= 0; --k) {  // backward, k decreasing
+                const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+                if (j0 < k) w0 = __fma_rn(-Ls[j0 * R + k], wk, w0);
+                if (v1 && j1 < k) w1 = __fma_rn(-Ls[j1 * R + k], wk, w1);
+            }
+        }
+        if (v0) out[int64_t(row) * R + j0] = w0;
+        if (v1) out[int64_t(row) * R + j1] = w1;
+    }
+}
+
+// One warp's chunk of the contraction: lane = row, NG groups of 8 r's at a
+// time (x loaded once per sample), z rows read as broadcast 16-byte loads.
+// Partials go to cps[(warp * CW + j) * 32 + lane], j < NG * 8.
+template <int NG>
+__device__ __forceinline__ void chain_chunk(const double* __restrict__ xs, const double* __restrict__ zs, int RP,
+                                           int g0, int cc0, int ccn, int lane, double* cps, int warp, int CW) {
+    double acc[NG * kCRB];
+#pragma unroll
+    for (int a = 0; a < NG * kCRB; ++a) acc[a] = 0.0;
+    if (ccn == kChunk) {
+#pragma unroll 4
+        for (int cc = 0; cc < kChunk; ++cc) {
+            const double x = xs[(cc0 + cc) * kRowTile + lane];
+            const double2* zr = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RP + g0 * kCRB);
+#pragma unroll
+            for (int q = 0; q < NG * kCRB / 2; ++q) {
+                const double2 zz = zr[q];
+                acc[2 * q] = __fma_rn(x, zz.x, acc[2 * q]);
+                acc[2 * q + 1] = __fma_rn(x, zz.y, acc[2 * q + 1]);
+            }
+        }
+    } else {
+        for (int cc = 0; cc < ccn; ++cc) {
+            const double x = xs[(cc0 + cc) * kRowTile + lane];
+            const double2* zr = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RP + g0 * kCRB);
+#pragma unroll
+            for (int q = 0; q < NG * kCRB / 2; ++q) {
+                const double2 zz = zr[q];
+                acc[2 * q] = __fma_rn(x, zz.x, acc[2 * q]);
+                acc[2 * q + 1] = __fma_rn(x, zz.y, acc[2 * q + 1]);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NG * kCRB; ++a) cps[(warp * CW + a) * kRowTile + lane] = acc[a];
+}
+
+constexpr int kRedStride = 33;  // padded row stride of the blocked partials (bank-conflict free)
+
+// Register-blocked contraction item for RP = 4 * CPL > 32 (R in 33..64): warp w
+// = chunk w of the superchunk; lane = (row group rg = lane / 4: rows 4rg..4rg+3)
+// x (column group cg = lane % 4: columns cg*CPL .. cg*CPL + CPL - 1), so one
+// sample costs 2 + CPL/2 shared loads for 4*CPL fmas.  Each output's chunk
+// partial is its fma chain over the chunk's samples from +0.0 (canonical);
+// after the compute the X tile region holds the partials of one column half at
+// a time (8 x RP/2 x 33 doubles; the Z tile stays resident for the block's
+// next item of the same superchunk) and the superchunk partial sums them in
+// chunk order.
+template <int CPL>
+__device__ __noinline__ void chain_contract_blocked(const double* xs, const double* zs, double* red, int cc0, int ccn,
+                                                    int nk, int nrows, int R, double* out_rows) {
+    constexpr int RP = 4 * CPL;  // padded width
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rg = lane >> 2, cg = lane & 3;
+    double acc[4][CPL];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) acc[a][j] = 0.0;
+    for (int cc = 0; cc < ccn; ++cc) {
+        const double2* xp = reinterpret_cast<const double2*>(xs + (cc0 + cc) * kRowTile + 4 * rg);
+        const double2 xa = xp[0], xb = xp[1];
+        const double x[4] = {xa.x, xa.y, xb.x, xb.y};
+        const double2* zp = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RP + cg * CPL);
+#pragma unroll
+        for (int q = 0; q < CPL / 2; ++q) {
+            const double2 zz = zp[q];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                acc[a][2 * q] = __fma_rn(x[a], zz.x, acc[a][2 * q]);
+                acc[a][2 * q + 1] = __fma_rn(x[a], zz.y, acc[a][2 * q + 1]);
+            }
+        }
+    }
+    __syncthreads();  // every warp is done with the X tile (the Z tile stays resident)
+    constexpr int HC = 2 * CPL;  // columns per half
+    constexpr int RS = (8 * HC * kRedStride <= kSuperSamples * kRowTile) ? kRedStride : kRowTile;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if ((cg >> 1) == h && warp < nk) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) red[(warp * HC + (cg & 1) * CPL + j) * RS + 4 * rg + a] = acc[a][j];
+        }
+        __syncthreads();
+        for (int e = tid; e < HC * kRowTile; e += blockDim.x) {
+            const int c = e >> 5, i = e & 31, r = h * HC + c;
+            if (i < nrows && r < R) {
+                double qq = red[c * RS + i];
+                for (int k = 1; k < nk; ++k) qq = qq + red[(k * HC + c) * RS + i];
+                out_rows[int64_t(i) * R + r] = qq;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Shared-memory map of k_chain (doubles):
+//   [0, 8192)                X_s tile (TMA); phase B: L/D (TMA); Gram items: Z tile + chunk partials
+//   [8192, 8192 + 256*RP)    contraction Z tile (TMA)
+//   then                     contraction chunk partials [8][CW][32]
+//   [16384, ...)             factor block: A [64][65], D[64], G [64*64], column buffer [64]
+constexpr int kSmXs = 0;
+constexpr int kSmZs = kSuperSamples * kRowTile;  // 8192
+constexpr int kSmFact = 16384;
+constexpr int kSmTotal = 27136;                  // doubles
+constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
+constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
+constexpr int kGramOneBlock = 16384;
+constexpr int kGramBlocksMax = 4;  // Gram pre-combine blocks when one block does not hold every partial
+constexpr int kTraceSlots = 24;                  // globaltimer stamps per stage (profiling aid)             // R^2 x chunks combined by one block up to this
+
+// kWide: R in 33..64 (register-blocked contraction); the R <= 32 instance
+// carries none of that code, so its register allocation is unaffected.
+template <bool kWide>
+__global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) double sm[];
+    __shared__ unsigned short pairs[64 * 65 / 2];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int s_mode, s_reg;
+    __shared__ double s_tr;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
+    const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
+    const int NGP = (RP <= 32) ? 4 : 1;  // r-groups per contraction pass
+    const int CW = NGP * kCRB;           // chunk-partial width
+    const int RR = R * R;
+    const int G = gridDim.x;
+    const int npairs = R * (R + 1) / 2;
+    unsigned phase = 0;
+    if (tid == 0) {
+        int off = 0;
+        for (int j = 0; j < R; ++j)
+            for (int i = j; i < R; ++i) pairs[off++] = (unsigned short)((i << 8) | j);
+        mbar_init(&bar, 1);
+    }
+    __syncthreads();
+    // Gram: chunk partials are formed in phase 0 by the blocks that build each
+    // 32-sample chunk of Z; phase 1 only combines them (canonical superchunk
+    // then total order).  Small R^2 x chunks: one block combines everything;
+    // otherwise superchunk items pre-combine and the last arrival finishes.
+    const int nch = (S + kChunk - 1) / kChunk;
+    const int NPp = (npairs + 1) & ~1;  // chunk-partial stride (lower pairs): 16-byte multiple for the bulk copy
+    const bool gram_one = int64_t(NPp) * nch <= kGramOneBlock;
+    const int n_gram = nsuper * kGramSplitC;
+    // the superchunk pre-combine is a few microseconds of work: keep nearly every block
+    // on the contraction, which bounds phase 1 for large R (C4)
+    const int gram_blocks = gram_one ? 1 : min(n_gram, kGramBlocksMax);
+    const int cblocks = G - gram_blocks;  // contraction blocks [0, cblocks), Gram blocks after them
+    const int gb0 = cblocks;
+    const bool is_gram_block = int(blockIdx.x) >= gb0;
+    const int cix = int(blockIdx.x);  // contraction index
+    double* xs = sm + kSmXs;
+    double* zs = sm + kSmZs;
+    double* cps = zs + kSuperSamples * RP;
+    const int czt = kChunk * RP;  // Z elements of one chunk
+
+    // idx of this thread's phase-0 Z elements (chunk blockIdx.x) of stage (b, st), in
+    // registers; loaded one phase ahead so the phase-0 critical path is a single L2 gather.
+    int32_t nidx[kZU][kMaxOrder - 1];
+    auto load_idx = [&](int b, int st) {
+        if (b >= p.nb) return;
+        const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+#pragma unroll
+        for (int u = 0; u < kZU; ++u) {
+            const int e = tid + u * blockDim.x;
+            const int c = int(blockIdx.x) * kChunk + e / RP;
+            const bool ok = int(blockIdx.x) < nch && e < czt && c < S;
+#pragma unroll
+            for (int l = 0; l < kMaxOrder - 1; ++l)
+                nidx[u][l] = (ok && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
+        }
+    };
+    load_idx(0, 0);
+
+    for (int b = 0; b < p.nb; ++b) {
+        double* u_new = p.temporal + (p.t_len0 + int64_t(b) * p.B) * R;
+        for (int st = 0; st < N; ++st) {
+            // [u_new (modes)] + U(N-1), ..., U(1) without U(st), built with compile-time
+            // positions so the list stays in registers
+            const double* F[kMaxOrder - 1];
+#pragma unroll
+            for (int l = 0; l < kMaxOrder - 1; ++l) {
+                const int m = (st > 0) ? l - 1 : l;
+                int k = N - 1 - m;
+                if (st > 0 && k <= st) k -= 1;
+                F[l] = (st > 0 && l == 0) ? u_new : ((m >= 0 && k >= 1) ? p.U[k - 1] : nullptr);
+            }
+            const int rows = (st == 0) ? p.B : p.head[st - 1];
+            const double* X = p.X_base + p.xoff[b * N + st];
+            // Z of this stage: the temporal Z is kept per batch for the residual pass
+            double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * RP : p.gch + int64_t(st) * S * RP;
+            const int tiles = (rows + kRowTile - 1) / kRowTile;
+            const int n_contract = tiles * nsuper;
+            unsigned long long* tr = p.trace ? p.trace + (int64_t(b) * N + st) * kTraceSlots : nullptr;
+            if (tr && blockIdx.x == 0 && tid == 0) tr[0] = gtimer();
+
+            // stage start: TMA the first X_s tile of this block (independent of factors);
+            // its arrive.expect_tx is issued with the Z tile in phase 1.
+            // item schedule: (tile, superchunk) pairs; the wide kernel gives each block one
+            // superchunk (its Z tile, up to 128 KB, is loaded once per stage), the narrow one
+            // strides over all items
+            const bool zreuse = kWide && cblocks >= nsuper;
+            const int zm = cix % nsuper, zrank = cix / nsuper, zcnt = (cblocks - zm + nsuper - 1) / nsuper;
+            const int first_item = zreuse ? ((zrank < tiles) ? zm * tiles + zrank : n_contract) : cix;
+            const bool contract_block = !is_gram_block && first_item < n_contract;
+            if (contract_block && tid == 0) {
+                const int tile = first_item % tiles, m = first_item / tiles;
+                const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                fence_proxy_async();
+                tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+            }
+
+            // the single Gram finisher fetches its Q entries during phase 0 (Q(st) only
+            // changes in this stage's finisher): off the phase-1 critical path, where the
+            // contraction blocks' tile copies congest L2
+            double qa[kQPre], qb[kQPre];
+#pragma unroll
+            for (int u = 0; u < kQPre; ++u) {
+                const int q = tid + u * int(blockDim.x);
+                qa[u] = qb[u] = 0.0;
+                if (is_gram_block && gram_one && st > 0 && q < npairs) {
+                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                    qa[u] = __ldcg(p.Q[st - 1] + i + j * R);
+                    qb[u] = __ldcg(p.Q[st - 1] + j + i * R);
+                }
+            }
+
+            // ---------------- phase 0: Z (S x RP, zero padded), one 32-sample chunk per block
+            // (sampling.cpp:90-103: 1.0 * F_0 * F_1 * ... left to right), then the chunk's
+            // Gram partial from shared memory: fma chain over its samples from +0.0
+            // (k_gram's per-chunk sequence), lower pairs mirrored.
+            for (int ch = blockIdx.x; ch < nch; ch += G) {
+                const int c0 = ch * kChunk, cn = min(kChunk, S - c0);
+                double* zc = zs;  // [32][RP]; the contraction Z tile is not loaded before phase 1
+                const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+                if (ch == int(blockIdx.x)) {
+                    double f[kZU][kMaxOrder - 1];
+#pragma unroll
+                    for (int u = 0; u < kZU; ++u) {
+                        const int e = tid + u * blockDim.x;
+                        const int cc = e / RP, r = e - cc * RP;
+                        const bool live = e < czt && cc < cn && r < R;
+#pragma unroll
+                        for (int l = 0; l < kMaxOrder - 1; ++l)
+                            f[u][l] = (live && l < n_other) ? __ldcg(F[l] + int64_t(nidx[u][l]) * R + r) : 1.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kZU; ++u) {
+                        const int e = tid + u * blockDim.x;
+                        if (e < czt) {
+                            const int cc = e / RP, r = e - cc * RP;
+                            double z = 0.0;
+                            if (cc < cn && r < R) {
+                                z = 1.0;
+#pragma unroll
+                                for (int l = 0; l < kMaxOrder - 1; ++l)
+                                    if (l < n_other) z = z * f[u][l];
+                            }
+                            zc[e] = z;
+                            if (cc < cn) Z[int64_t(c0) * RP + e] = z;
+                        }
+                    }
+                }
+                const int e0 = (ch == int(blockIdx.x)) ? kZU * int(blockDim.x) : 0;
+                for (int e = e0 + tid; e < czt; e += blockDim.x) {  // rare: RP > 32 or extra chunks
+                    const int cc = e / RP, r = e - cc * RP;
+                    double z = 0.0;
+                    if (cc < cn && r < R) {
+                        z = 1.0;
+#pragma unroll
+                        for (int l = 0; l < kMaxOrder - 1; ++l)
+                            if (l < n_other)
+                                z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c0 + cc) * n_other + (n_other - 1 - l))) * R + r);
+                    }
+                    zc[e] = z;
+                    if (cc < cn) Z[int64_t(c0) * RP + e] = z;
+                }
+                __syncthreads();
+                if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[14] = gtimer();
+                for (int q = tid; q < npairs; q += blockDim.x) {
+                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                    double acc = 0.0;
+                    if (cn == kChunk) {
+#pragma unroll 8
+                        for (int cc = 0; cc < kChunk; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                    } else {
+                        for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                    }
+                    p.chpart[int64_t(ch) * NPp + q] = acc;  // lower pair q; (j, i) is the same value
+                }
+                __syncthreads();
+                if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[15] = gtimer();
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA in phase 1
+            grid.sync();
+            if (tr && blockIdx.x == 0 && tid == 0) tr[1] = gtimer();
+
+            // ---------------- phase 1
+            if (is_gram_block) {
+                // superchunk sums of the chunk partials, superchunk m = chunks 8m..8m+7 in order
+                auto super_sum = [&](int m, int pp) {
+                    const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
+                    double v[kSuper];
+#pragma unroll
+                    for (int u = 0; u < kSuper; ++u) v[u] = (k0 + u < k1) ? __ldcg(p.chpart + int64_t(k0 + u) * NPp + pp) : 0.0;
+                    double q = v[0];
+#pragma unroll
+                    for (int u = 1; u < kSuper; ++u)
+                        if (k0 + u < k1) q = q + v[u];
+                    return q;
+                };
+                bool finisher = gram_one;
+                if (!gram_one) {
+                    for (int gi = int(blockIdx.x) - gb0; gi < n_gram; gi += gram_blocks) {
+                        const int m = gi / kGramSplitC, part = gi % kGramSplitC;
+                        const int pp0 = (npairs * part) / kGramSplitC, pp1 = (npairs * (part + 1)) / kGramSplitC;
+                        for (int pp = pp0 + tid; pp < pp1; pp += blockDim.x) p.gpart[int64_t(m) * NPp + pp] = super_sum(m, pp);
+                    }
+                    finisher = last_arrive_of(p.counter, unsigned(gram_blocks));
+                }
+                if (finisher) {
+                    if (tr && tid == 0) tr[3] = gtimer();
+                    double* A = sm + kSmFact;        // [64][65]
+                    double* D = A + 64 * kLdStride;  // 64
+                    double* Gs = D + 64;             // R x R column-major
+                    double* colb = Gs + 64 * 64;     // 3 x 32 (ldlt_warp column buffers)
+                    // total = superchunk sums in order; Q += G for the modes (rocp.cpp:108)
+                    double* chs = sm;  // gram_one: every chunk partial, one TMA bulk copy (nch x NPp <= 16384)
+                    if (gram_one && tid == 0) {
+                        const unsigned bytes = unsigned(nch * NPp * 8);
+                        fence_proxy_async();
+                        tma_load_1d(chs, p.chpart, bytes, &bar);
+                        mbar_expect_tx(&bar, bytes);
+                    }
+                    // Q entries of this thread's first kQPre pairs (prefetched in phase 0 when gram_one)
+                    if (!gram_one) {
+#pragma unroll
+                        for (int u = 0; u < kQPre; ++u) {
+                            const int q = tid + u * int(blockDim.x);
+                            if (st > 0 && q < npairs) {
+                                const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                                qa[u] = __ldcg(p.Q[st - 1] + i + j * R);
+                                qb[u] = __ldcg(p.Q[st - 1] + j + i * R);
+                            }
+                        }
+                    }
+                    if (gram_one) {
+                        mbar_wait(&bar, phase);
+                        phase ^= 1u;
+                    }
+                    if (tr && tid == 0) tr[18] = gtimer();
+#pragma unroll
+                    for (int u = 0; u < kMaxPairsPerThread; ++u) {
+                        const int q = tid + u * int(blockDim.x);
+                        if (q >= npairs) break;
+                        double tot;
+                        if (gram_one) {
+                            for (int m = 0; m < nsuper; ++m) {
+                                const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
+                                double sq = chs[k0 * NPp + q];
+                                for (int k = k0 + 1; k < k1; ++k) sq = sq + chs[k * NPp + q];
+                                tot = (m == 0) ? sq : tot + sq;
+                            }
+                        } else {
+                            double v[8];
+#pragma unroll
+                            for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * NPp + q) : 0.0;
+                            tot = v[0];
+#pragma unroll
+                            for (int m = 1; m < 8; ++m)
+                                if (m < nsuper) tot = tot + v[m];
+                            for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
+                        }
+                        // Q + G entry by entry (rocp.cpp:108); G is symmetric bit for bit
+                        const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                        double ga = tot, gb = tot;
+                        if (st > 0) {
+                            const double qva = (u < kQPre) ? qa[u < kQPre ? u : 0] : __ldcg(p.Q[st - 1] + i + j * R);
+                            const double qvb = (u < kQPre) ? qb[u < kQPre ? u : 0] : __ldcg(p.Q[st - 1] + j + i * R);
+                            ga = qva + tot;
+                            gb = qvb + tot;
+                            p.Q[st - 1][i + j * R] = ga;
+                            p.Q[st - 1][j + i * R] = gb;
+                        }
+                        Gs[i + j * R] = ga;
+                        Gs[j + i * R] = gb;
+                    }
+                    __syncthreads();
+                    if (tr && tid == 0) tr[10] = gtimer();
+                    // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
+                    if (tid == 0) {
+                        double maxdiag = Gs[0], trc = Gs[0];
+#pragma unroll 8
+                        for (int k = 1; k < R; ++k) {
+                            const double dg = Gs[k * R + k];
+                            if (dg > maxdiag) maxdiag = dg;
+                            trc = trc + dg;
+                        }
+                        s_tr = trc;
+                        s_mode = (maxdiag <= 0.0) ? 0 : 1;
+                        s_reg = (s_mode == 0) ? 1 : 0;
+                    }
+                    __syncthreads();
+                    if (tr && tid == 0) tr[12] = gtimer();
+                    auto factor = [&](double lambda) {
+                        if (R <= 32) {
+                            if (warp == 0) {
+                                if (R <= 8) ldlt_warp<8>(Gs, lambda, R, A, D, colb);
+                                else if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, D, colb);
+                                else if (R <= 24) ldlt_warp<24>(Gs, lambda, R, A, D, colb);
+                                else ldlt_warp<32>(Gs, lambda, R, A, D, colb);
+                            }
+                            __syncthreads();
+                        } else {
+                            ldlt_one_sync(A, D, R, lambda, Gs, pairs, npairs);
+                        }
+                    };
+                    if (s_mode == 1) {
+                        factor(0.0);
+                        if (tr && tid == 0) tr[13] = gtimer();
+                        if (tid == 0) {
+                            double dmin = D[0], dmax = D[0];
+#pragma unroll 8
+                            for (int k = 0; k < R; ++k) {
+                                const double dk = D[k];
+                                if (dk < dmin) dmin = dk;
+                                if (dk > dmax) dmax = dk;
+                            }
+                            s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+                        }
+                        __syncthreads();
+                        if (s_reg) factor(1e-12 * s_tr);
+                    }
+                    __syncthreads();
+                    if (tr && tid == 0) tr[11] = gtimer();
+                    for (int t = tid; t < RR; t += blockDim.x) {
+                        const int k = t / R, i = t % R;
+                        p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
+                    }
+                    for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
+                    if (tid == 0) {
+                        p.mode_flag[0] = s_mode;
+                        if (s_reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
+                        if (tr) tr[4] = gtimer();
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
+                }
+            } else {
+                for (int item = first_item; item < n_contract;
+                     item = zreuse ? ((item % tiles) + zcnt < tiles ? item + zcnt : n_contract) : item + cblocks) {
+                    const int tile = item % tiles, m = item / tiles;
+                    const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                    const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
+                    if (tid == 0) {
+                        fence_proxy_async();
+                        if (item != first_item)  // later items: X tile now
+                            tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+                        const bool zload = !zreuse || item == first_item;
+                        if (zload) tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + (zload ? cn * RP * 8 : 0)));
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[8] = gtimer();
+                    const int nk = (cn + kChunk - 1) / kChunk;
+                    const int cc0 = warp * kChunk;
+                    const int ccn = min(kChunk, cn - cc0);
+                    if constexpr (kWide) {  // register-blocked item (R in 33..64)
+                        double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
+                        const int cn0 = max(ccn, 0);
+                        if (RP == 40) chain_contract_blocked<10>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        else if (RP == 48) chain_contract_blocked<12>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        else if (RP == 56) chain_contract_blocked<14>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        else chain_contract_blocked<16>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                    }
+                    for (int g0 = 0; g0 < ng && !kWide; g0 += NGP) {
+                        if (ccn > 0) {  // warp w = chunk w of the superchunk; lane = row
+                            const int ngp = min(NGP, ng - g0);
+                            if (ngp == 4) chain_chunk<4>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                            else if (ngp == 3) chain_chunk<3>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                            else if (ngp == 2) chain_chunk<2>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                            else chain_chunk<1>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
+                        }
+                        __syncthreads();
+                        // superchunk partial = chunk partials in increasing chunk order
+                        for (int e = tid; e < CW * kRowTile; e += blockDim.x) {
+                            const int rl = e >> 5, l2 = e & 31, r = g0 * kCRB + rl;
+                            if (l2 < nrows && r < R) {
+                                double qq = cps[rl * kRowTile + l2];
+                                for (int k = 1; k < nk; ++k) qq = qq + cps[(k * CW + rl) * kRowTile + l2];
+                                p.cpart[(int64_t(m) * rows + i0 + l2) * R + r] = qq;
+                            }
+                        }
+                        __syncthreads();
+                    }
+                    if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[9] = gtimer();
+                }
+            }
+            if (tr && blockIdx.x == 0 && tid == 0) tr[2] = gtimer();
+            __syncthreads();
+            grid.sync();
+            if (tr && blockIdx.x == 0 && tid == 0) tr[5] = gtimer();
+
+            // ---------------- phase B: row solves; idle blocks load the next stage's idx
+            {
+                const int nb2 = (st + 1 < N) ? b : b + 1, ns2 = (st + 1 < N) ? st + 1 : 0;
+                if (int(blockIdx.x) < rows) {
+                    double* Ls = sm;  // R x R, L(i,k) at [k*R + i], then D
+                    if (tid == 0) {
+                        const unsigned bytes = unsigned(((RR + R + 1) & ~1) * 8);
+                        fence_proxy_async();
+                        tma_load_1d(Ls, p.LD, bytes, &bar);
+                        mbar_expect_tx(&bar, bytes);
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    if (tr && blockIdx.x == 0 && tid == 0) tr[16] = gtimer();
+                    const int mode = __ldcg(p.mode_flag);
+                    double* out = (st == 0) ? u_new : p.U[st - 1];
+                    chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ls + RR,
+                                    mode);
+                    if (tr && blockIdx.x == 0 && tid == 0) tr[17] = gtimer();
+                }
+                load_idx(nb2, ns2);
+            }
+            if (tr && blockIdx.x == 0 && tid == 0) tr[6] = gtimer();
+            __syncthreads();
+            grid.sync();
+            if (tr && blockIdx.x == 0 && tid == 0) tr[7] = gtimer();
+        }
+    }
+}
+
+// Sampled residual of every batch's temporal solve in a window,
+// after the chain: column partials (warp per column), then hsum per batch.
+struct WinResidParams {
+    int N, R, S, B, RP, nb;
+    const double* temporal;  // row-major; batch b's rows at t_len0 + b*B
+    int64_t t_len0;
+    const double* X_base;
+    const int64_t* xoff;
+    const double* zT;        // nb x S x RP
+    double* cols;            // nb x 3 x S
+    double* out;             // nb x 2 (num, den)
+    double* last_out;        // 2: the last batch's (num, den)
+};
+
+__global__ void __launch_bounds__(256) k_win_resid_cols(const WinResidParams p) {
+    const int b = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + warp;
+    if (c >= p.S) return;
+    const double* u = p.temporal + (p.t_len0 + int64_t(b) * p.B) * p.R;
+    const double* X = p.X_base + p.xoff[b * p.N];
+    const double* z = p.zT + (int64_t(b) * p.S + c) * p.RP;
+    double qn = 0.0, qd = 0.0;
+    for (int i = lane; i < p.B; i += 32) {
+        double uz = 0.0;
+        for (int r = 0; r < p.R; ++r) uz = __fma_rn(u[int64_t(i) * p.R + r], z[r], uz);
+        const double xv = X[xs_offset(i, c, p.S)];
+        const double e = xv - uz;
+        qn = __fma_rn(e, e, qn);
+        qd = __fma_rn(xv, xv, qd);
+    }
+    qn = butterfly32(qn);
+    qd = butterfly32(qd);
+    if (lane == 0) {
+        p.cols[(int64_t(b) * 3 + 0) * p.S + c] = qn;
+        p.cols[(int64_t(b) * 3 + 1) * p.S + c] = qd;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_win_resid_sum(const WinResidParams p) {
+    const int b = blockIdx.x;
+    double* base = p.cols + int64_t(b) * 3 * p.S;
+    block_hsum_inplace(base, p.S, base + 2 * p.S);
+    block_hsum_inplace(base + p.S, p.S, base + 2 * p.S);
+    if (threadIdx.x == 0) {
+        const double num = __ldcg(base), den = __ldcg(base + p.S);
+        p.out[2 * b] = num;
+        p.out[2 * b + 1] = den;
+        if (b == p.nb - 1) {
+            p.last_out[0] = num;
+            p.last_out[1] = den;
+        }
+    }
+}
+
+}  // namespace rocpk

@@ -12,6 +12,7 @@
 
 #include "../../include/rocp_b200.h"
 #include "kernels.cuh"
+#include "chain_kernel.cuh"
 #include "shard_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -1082,205 +1083,7 @@ void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uin
     st->t_len += B;  // rocp.cpp:159
 }
 
-// ---- host-slab path ----------------------------------------------------------
-// For inputs that live in host memory (the reference-facing call), only the
-// sampled fibres cross PCIe.  The GPU draws the window's indices; host threads
-// gather the sampled fibres of the strided stages from the caller's slabs into
-// pinned staging (row-tiled X_s layout), batch by batch; as soon as a
-// sub-window's batches are complete the calling thread issues, on a copy
-// stream, the in-place GPU read of its contiguous mode-1 fibres (registered
-// ranges only) and the H2D copy of its staging, and joins the persistent chain
-// for it on the compute stream -- so host gather, PCIe and the chain overlap,
-// and no host thread waits at sub-window boundaries.
-struct HostTask {
-    int32_t b, stage;
-    int64_t c0, c1;
-};
-
-void host_gather_task(rocp_stream* st, const double* hx, int64_t slice, int64_t B, const std::vector<int64_t>& d,
-                      const std::vector<int64_t>& strides, const HostTask& tk) {
-    Window& W = st->win;
-    const int N = st->N;
-    const int64_t S = st->s;
-    const int mode = tk.stage == 0 ? N : tk.stage;
-    const int64_t I = d[size_t(mode - 1)], ms = strides[size_t(mode - 1)];
-    const double* src_b = hx + int64_t(tk.b) * B * slice;
-    const int64_t* bases = W.hbase + (int64_t(tk.b) * N + tk.stage) * S;
-    double* dst = W.hX + W.xoff[size_t(int64_t(tk.b) * N + tk.stage)];
-    // Each fibre is walked on its own: strided rows on 2 MB pages stay
-    // TLB-resident and the out-of-order core keeps a fibre's independent loads
-    // in flight (tools/host_gather_bench.cpp: this beats row-interleaved walks
-    // and software prefetch on the GPU box's host).
-    for (int64_t c = tk.c0; c < tk.c1; ++c) {
-        const double* f = src_b + bases[c];
-        if (ms == 1) {
-            for (int64_t i0 = 0; i0 < I; i0 += 32)
-                std::memcpy(dst + xs_offset(i0, c, S), f + i0, size_t(std::min<int64_t>(32, I - i0)) * 8);
-        } else {
-            for (int64_t i0 = 0; i0 < I; i0 += 32) {
-                double* o = dst + xs_offset(i0, c, S);  // 256-byte aligned run of 32
-                const int64_t n = std::min<int64_t>(32, I - i0);
-                const double* fi = f + i0 * ms;
-                if (n == 32) {
-                    // streaming stores: the staging lines are written whole, never read for ownership
-                    for (int64_t q = 0; q < 32; q += 4)
-                        _mm256_stream_pd(o + q, _mm256_set_pd(fi[(q + 3) * ms], fi[(q + 2) * ms], fi[(q + 1) * ms],
-                                                              fi[q * ms]));
-                } else {
-                    for (int64_t i = 0; i < n; ++i) o[i] = fi[i * ms];
-                }
-            }
-        }
-    }
-}
-
-void consume_range_host(rocp_stream* st, const double* hx, int64_t B, int64_t nb, uint64_t seed,
-                        uint32_t first_batch_id, int threads, int64_t sub) {
-    rocp_dev* dev = st->dev;
-    check_capacity(st, B * nb);
-    const int64_t slice = prod(st->head);
-    const int N = st->N;
-    const int64_t S = st->s;
-    // A CUDA-registered range (e.g. rocp_host_alloc) lets the GPU read the
-    // contiguous mode-1 fibres in place over PCIe while host threads gather the
-    // strided stages; otherwise host threads gather every stage.
-    const double* zc = nullptr;
-    {
-        const double* last = hx + (B * nb * slice - 1);
-        cudaPointerAttributes a0{}, a1{};
-        if (cudaPointerGetAttributes(&a0, hx) == cudaSuccess && cudaPointerGetAttributes(&a1, last) == cudaSuccess &&
-            a0.type == cudaMemoryTypeHost && a1.type == cudaMemoryTypeHost && a0.devicePointer &&
-            a1.devicePointer &&
-            static_cast<const double*>(a1.devicePointer) - static_cast<const double*>(a0.devicePointer) ==
-                last - hx)
-            zc = static_cast<const double*>(a0.devicePointer);
-        cudaGetLastError();  // unregistered memory: not an error here
-    }
-    prepare_window(st, hx, 0, slice, B, nb, nullptr, nullptr, -1, /*host_gather=*/true, zc);
-    Window& W = st->win;
-    const std::vector<int64_t> d = slab_dims(st, B);
-    const std::vector<int64_t> strides = strides_of(d);
-    const size_t xn = W.X.n, bn = size_t(nb * N * S);
-    if (W.hX_n < xn) {
-        host_free_huge(W.hX, W.hX_n * sizeof(double));
-        W.hX = nullptr;
-        W.hX_n = 0;
-        W.hX = static_cast<double*>(host_alloc_huge(xn * sizeof(double)));
-        if (!W.hX) throw RocpError{ROCP_E_OOM, "host staging allocation failed"};
-        W.hX_n = xn;
-    }
-    if (!st->pool || st->pool->size() < threads) st->pool = std::make_unique<HostPool>(threads);
-    if (!st->copy_stream) CK(cudaStreamCreateWithFlags(&st->copy_stream, cudaStreamNonBlocking));
-    if (W.hbase_n < bn) {
-        if (W.hbase) cudaFreeHost(W.hbase);
-        CK(cudaHostAlloc(&W.hbase, bn * sizeof(int64_t), cudaHostAllocDefault));
-        W.hbase_n = bn;
-    }
-    // K1 on the device; the fibre bases come back (nb x N x S int64).  The
-    // synchronize also retires every copy of the previous call (joined below).
-    k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
-    after_launch(dev, "k_set_u64");
-    k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
-    after_launch(dev, "k_set_u32");
-    launch_draw(dev, W.jobs);
-    CK(cudaMemcpyAsync(W.hbase, W.base.p, bn * sizeof(int64_t), cudaMemcpyDeviceToHost, dev->stream));
-    CK(cudaStreamSynchronize(dev->stream));
-
-    // host tasks of kFib fibres, batch by batch (strided stages first within a batch)
-    constexpr int64_t kFib = 16;
-    std::vector<HostTask> tasks;
-    std::unique_ptr<std::atomic<int>[]> remaining(new std::atomic<int>[size_t(nb)]);
-    for (int64_t b = 0; b < nb; ++b) {
-        const size_t before = tasks.size();
-        for (int pass = 0; pass < 2; ++pass)
-            for (int stage = 0; stage < N; ++stage) {
-                const int mode = stage == 0 ? N : stage;
-                if ((strides[size_t(mode - 1)] == 1) != (pass == 1)) continue;
-                if (pass == 1 && zc) continue;  // read by the GPU in place
-                for (int64_t c0 = 0; c0 < S; c0 += kFib)
-                    tasks.push_back(HostTask{int32_t(b), stage, c0, std::min(S, c0 + kFib)});
-            }
-        remaining[size_t(b)].store(int(tasks.size() - before), std::memory_order_relaxed);
-    }
-    if (sub < 1) {
-        static const int64_t env_sub = std::getenv("ROCP_HOST_SUB") ? std::atoll(std::getenv("ROCP_HOST_SUB")) : 0;
-        sub = env_sub > 0 ? env_sub : 1;
-    }
-    sub = std::max<int64_t>(1, std::min(sub, nb));
-    const int64_t nsub = (nb + sub - 1) / sub;
-    while (int64_t(st->copy_events.size()) < nsub) {
-        cudaEvent_t e;
-        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        st->copy_events.push_back(e);
-    }
-    // GPU side of sub-window [b0, b1): in-place mode-1 reads + staging copies on
-    // the copy stream, then the chain on the compute stream.
-    auto issue = [&](int64_t k, int64_t b0, int64_t b1) {
-        cudaStream_t cs = st->copy_stream;
-        if (zc && W.zc_tile[size_t(b1)] > W.zc_tile[size_t(b0)]) {
-            k_gather<<<unsigned(W.zc_tile[size_t(b1)] - W.zc_tile[size_t(b0)]), kGatherThreads, 0, cs>>>(
-                W.jobs.gather.p, W.jobs.tiles.p + W.zc_tile[size_t(b0)]);
-            after_launch(dev, "k_gather");
-        }
-        for (int64_t b = b0; b < b1; ++b)
-            for (int stage = 0; stage < N; ++stage) {
-                const int mode = stage == 0 ? N : stage;
-                if (zc && strides[size_t(mode - 1)] == 1) continue;
-                const int64_t x0 = W.xoff[size_t(b * N + stage)];
-                const int64_t n = xs_size(st->stage_rows(stage, B), S);
-                CK(cudaMemcpyAsync(W.X.p + x0, W.hX + x0, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cs));
-            }
-        CK(cudaEventRecord(st->copy_events[size_t(k)], cs));
-        CK(cudaStreamWaitEvent(dev->stream, st->copy_events[size_t(k)], 0));
-        launch_chain(st, b1 - b0, B, b0);
-        st->t_len += (b1 - b0) * B;
-    };
-    static const bool trace = std::getenv("ROCP_HOST_TRACE") != nullptr;
-    auto wall = [] {
-        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-    };
-    const double tw0 = trace ? wall() : 0.0;
-    std::atomic<size_t> next{0};
-    const std::thread::id caller = std::this_thread::get_id();
-    int64_t issued = 0;  // sub-windows issued so far (caller thread only)
-    std::exception_ptr failure;
-    auto ready = [&](int64_t k) {
-        for (int64_t b = k * sub; b < std::min(nb, (k + 1) * sub); ++b)
-            if (remaining[size_t(b)].load(std::memory_order_acquire) != 0) return false;
-        return true;
-    };
-    auto try_issue = [&](bool block) {
-        while (issued < nsub && !failure) {
-            if (!ready(issued)) {
-                if (!block) return;
-                std::this_thread::yield();
-                continue;
-            }
-            try {
-                issue(issued, issued * sub, std::min(nb, (issued + 1) * sub));
-            } catch (...) {
-                failure = std::current_exception();
-            }
-            if (trace)
-                std::fprintf(stderr, "[rocp host] sub-window %lld issued at %.2f ms\n", (long long)issued,
-                             wall() - tw0);
-            ++issued;
-        }
-    };
-    const std::function<void()> work = [&]() {
-        const bool is_caller = std::this_thread::get_id() == caller;
-        for (size_t k = next.fetch_add(1, std::memory_order_relaxed); k < tasks.size();
-             k = next.fetch_add(1, std::memory_order_relaxed)) {
-            host_gather_task(st, hx, slice, B, d, strides, tasks[k]);
-            _mm_sfence();  // this task's streaming stores are globally visible before the batch counts down
-            remaining[size_t(tasks[k].b)].fetch_sub(1, std::memory_order_release);
-            if (is_caller) try_issue(false);
-        }
-        if (is_caller) try_issue(true);
-    };
-    st->pool->run(std::min<int>(threads, int(std::max<size_t>(tasks.size(), 1))), work);
-    if (failure) std::rethrow_exception(failure);
-}
+#include "host_slab.inc"
 
 #include "shard_host.inc"
 

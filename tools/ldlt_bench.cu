@@ -1,6 +1,6 @@
 // Profiling aid: cycles of the canonical LDL^T variants on one block.
 #include <cstdio>
-#include "../paper_2007_10798_b200/csrc/kernels.cuh"
+#include "../paper_2007_10798_b200/csrc/chain_kernel.cuh"
 using namespace rocpk;
 
 __global__ void k_ldlt(const double* G, int R, long long* cyc, double* out) {
