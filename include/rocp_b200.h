@@ -182,6 +182,12 @@ rocp_status rocp_stream_read_state(rocp_stream* st, const char* path);
 rocp_status rocp_stream_write_checkpoint(rocp_stream* st, const char* path);
 rocp_status rocp_stream_create_from_checkpoint(rocp_dev* dev, const char* path, int64_t t_capacity,
                                                rocp_stream** out);
+/* File-backed stream: slabs [t0, t0 + nb*batch) of the last mode of a tensor
+ * record (read_tensor_file format) are read into pinned huge-page staging and
+ * consumed exactly as rocp_stream_consume_range_host (same results bit for
+ * bit).  The head extents must match the stream; threads 0 = all cores. */
+rocp_status rocp_stream_consume_file(rocp_stream* st, const char* path, int64_t t0, int64_t batch, int64_t nb,
+                                     uint64_t seed, uint32_t first_batch_id, int threads);
 rocp_status rocp_stream_shard_info(rocp_stream* st, int* virtual_shards, int64_t* row0, int64_t* row1);
 /* Same for a host slab (head dims x batch, first index fastest): the
  * reference-facing call.  Only the sampled fibres cross PCIe (see

@@ -81,6 +81,8 @@ SIGNATURES = [
     ("rocp_stream_write_state", C.c_int, [_vp, C.c_char_p]),
     ("rocp_stream_read_state", C.c_int, [_vp, C.c_char_p]),
     ("rocp_stream_write_checkpoint", C.c_int, [_vp, C.c_char_p]),
+    ("rocp_stream_consume_file", C.c_int, [_vp, C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32,
+                                           C.c_int]),
     ("rocp_stream_create_from_checkpoint", C.c_int, [_vp, C.c_char_p, C.c_int64, C.POINTER(_vp)]),
     ("rocp_stream_shard_info", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("rocp_stream_consume", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32]),
@@ -726,6 +728,11 @@ class RocpStream:
     def read_state(self, path):
         """load_state record (rocp.cpp:186-211) into this stream: P, Q, t_len."""
         self.dev.check(lib().rocp_stream_read_state(self.h, os.fsencode(path)))
+
+    def consume_file(self, path, t0, batch, nb, seed, first_batch_id, threads=0):
+        """nb batches of `batch` slices from a tensor record file, starting at slice t0."""
+        self.dev.check(lib().rocp_stream_consume_file(self.h, os.fsencode(path), t0, batch, nb, seed,
+                                                      first_batch_id, threads))
 
     def write_checkpoint(self, path):
         self.dev.check(lib().rocp_stream_write_checkpoint(self.h, os.fsencode(path)))

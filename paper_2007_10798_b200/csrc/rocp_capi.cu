@@ -719,6 +719,8 @@ struct rocp_stream {
     int64_t r0 = 0, r1 = 0;
     std::vector<int64_t> ghead;
     std::unique_ptr<ShardWin> sw;
+    double* file_buf = nullptr;               // consume_file: huge-page pinned slab staging
+    size_t file_buf_bytes = 0;
     cudaStream_t copy_stream = nullptr;       // host-slab path: in-place reads + staging copies
     std::vector<cudaEvent_t> copy_events;     // one per sub-window, joined by the compute stream
     // checkpoint copies (device)
@@ -743,6 +745,7 @@ struct rocp_stream {
         }
         for (cudaEvent_t e : copy_events) cudaEventDestroy(e);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        host_free_huge(file_buf, file_buf_bytes);
     }
     int64_t stage_rows(int stage, int64_t batch) const { return stage == 0 ? batch : head[size_t(stage - 1)]; }
 };
@@ -1793,6 +1796,15 @@ rocp_status rocp_stream_write_checkpoint(rocp_stream* st, const char* path) {
         if (st->sharded) throw_domain("checkpoints hold the full U(1)/P(1); this stream is sharded");
         File out(path, "wb");
         write_checkpoint(st, out);
+    });
+}
+
+rocp_status rocp_stream_consume_file(rocp_stream* st, const char* path, int64_t t0, int64_t batch, int64_t nb,
+                                     uint64_t seed, uint32_t first_batch_id, int threads) {
+    return guarded(st->dev, [&] {
+        if (st->sharded) throw_domain("file-backed consume is single-GPU (stream is sharded)");
+        if (st->resid_level >= 2) throw_domain("consume_file: residual level 2 needs device slabs");
+        consume_file(st, path, t0, batch, nb, seed, first_batch_id, threads > 0 ? threads : st->host_threads);
     });
 }
 

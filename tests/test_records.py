@@ -119,3 +119,21 @@ def test_checkpoint_resume_is_bitwise(dev):
     for n in range(1, len(dims)):
         assert bitwise(a.factor(n), b.factor(n)) and bitwise(a.p(n), b.p(n)) and bitwise(a.q(n), b.q(n))
     assert bitwise(a.temporal(), b.temporal()) and a.regularized == b.regularized
+
+
+@pytest.mark.gpu
+def test_file_backed_stream_equals_device_range(dev):
+    x, dims, init = _stream_pair(dev)
+    X = dev.tensor(dims, x)
+    a = rocp.RocpStream(dev, init, init.samples, t_capacity=dims[-1])
+    b = rocp.RocpStream(dev, init, init.samples, t_capacity=dims[-1])
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "x.rocp")
+        X.write(p)
+        a.consume_file(p, 20, 10, 5, 73, 1)
+        with pytest.raises(rocp.DomainError):
+            a.consume_file(p, 60, 10, 2, 73, 6)  # past the end of the record
+    b.consume_range(X, 20, 10, 5, 73, 1)
+    for n in range(1, len(dims)):
+        assert bitwise(a.factor(n), b.factor(n)) and bitwise(a.p(n), b.p(n)) and bitwise(a.q(n), b.q(n))
+    assert bitwise(a.temporal(), b.temporal())
