@@ -385,14 +385,17 @@ def main():
         hbuf = rocp.HostBuffer(slices_per_step * slice_)  # pinned, 2 MB pages (rocp_host_alloc)
         host = hbuf.array
         X.slab(t_init, slices_per_step).download(out=host)
+        # replicas share the host: each rank's gather pool takes its share of the cores
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        host_threads = max(1, (os.cpu_count() or 1) // max(1, local_world))
         stream.restore()  # warm the host-slab path once
-        stream.consume_range_host(host, B, nb, 777, 1)
+        stream.consume_range_host(host, B, nb, 777, 1, threads=host_threads)
         dev.synchronize()
         e2e_ms = []
         for k in range(args.e2e_steps):
             stream.restore()
             dev.timer_record(2)
-            stream.consume_range_host(host, B, nb, 20000 + k, 1)
+            stream.consume_range_host(host, B, nb, 20000 + k, 1, threads=host_threads)
             out = stream.model()  # device -> host read of the step's result
             dev.timer_record(3)
             e2e_ms.append(dev.timer_elapsed_ms(2, 3))
@@ -402,7 +405,7 @@ def main():
                "unit": "time-slices/s",
                "h2d_bytes_per_step": int(xs_elems * 8),
                "d2h_bytes_per_step": int(sum(m.size for m in out) * 8 + nb * len(dims) * S * 8),
-               "steps": args.e2e_steps, "ms_per_step": statistics.mean(e2e_ms),
+               "steps": args.e2e_steps, "ms_per_step": statistics.mean(e2e_ms), "host_threads_per_rank": host_threads,
                "path": "rocp_stream_consume_range_host: device draw -> host threads gather the strided "
                        "sampled fibres, the GPU reads the mode-1 fibres in place (zero-copy) -> H2D of "
                        "X_s per batch on a copy stream -> persistent chain per batch"}
