@@ -159,9 +159,14 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
     // register copy, which the compiler would place in local memory).
     const int lane = threadIdx.x & 31;
     double r[MAXR];
+    // branch-free: every load is issued (clamped index), then selected
 #pragma unroll
-    for (int j = 0; j < MAXR; ++j)
-        r[j] = (lane < R && j <= lane) ? ((j == lane) ? G[lane + j * R] + lambda : G[lane + j * R]) : 0.0;
+    for (int j = 0; j < MAXR; ++j) {
+        const bool ok = lane < R && j <= lane;
+        const double g = G[ok ? lane + j * R : 0];
+        const double gl = g + lambda;
+        r[j] = ok ? ((j == lane) ? gl : g) : 0.0;
+    }
     col[lane] = r[0];
     __syncwarp();
     double dk = __shfl_sync(0xffffffffu, r[0], 0);
@@ -170,18 +175,22 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
     for (int k = 0; k < MAXR; ++k) {
         if (k < R) {
             const double* cb = col + (k % 3) * 32;  // column k
+            // a(k+1, k) in a register before the divide: the load would
+            // otherwise sit between the quotient and the critical fma
+            const double ck1 = (k + 1 < MAXR) ? cb[k + 1] : 0.0;
             if (k > 0) {  // deferred updates of step k-1 (j >= k+1): fill the shuffle latency
                 const double* cp = col + ((k + 2) % 3) * 32;  // column k-1
 #pragma unroll
                 for (int j = k + 1; j < MAXR; ++j) r[j] = __fma_rn(-lp, cp[j], r[j]);
             }
             const bool act = lane > k && lane < R;
+            const bool use = act && dk != 0.0;  // known before the quotient
             const double num = act ? r[k] : 1.0;
             const double q = num / dk;
-            const double l = (act && dk != 0.0) ? q : 0.0;
+            const double l = use ? q : 0.0;
             double dn = 0.0;
             if (k + 1 < MAXR) {  // critical: finish a(., k+1), broadcast d_{k+1}, publish column k+1
-                r[k + 1] = __fma_rn(-l, cb[k + 1], r[k + 1]);
+                r[k + 1] = __fma_rn(-l, ck1, r[k + 1]);
                 dn = __shfl_sync(0xffffffffu, r[k + 1], (k + 1) & 31);
                 col[((k + 1) % 3) * 32 + lane] = r[k + 1];
             }
