@@ -21,7 +21,7 @@ namespace rocpk {
 //   phase 1      concurrently:
 //                - contraction blocks: Z tile by TMA; warp w = chunk w of the
 //                  superchunk; superchunk partials of X_s Z (register-blocked
-//                  variant for R in 33..64, k_chain<true>)
+//                  variant for R in 33..64, k_chain<true, .>)
 //                - the Gram finisher: chunk partials summed in order (one TMA
 //                  bulk copy when they fit, else 4 pre-combine blocks), Q += G,
 //                  canonical LDL^T (ldlt_warp for R <= 32), publishes L, D | grid barrier
@@ -58,6 +58,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+// Trace stamp: every thread of the (uniform) caller reads the timer and only
+// 'who' stores, through a predicated store (no branch), so no lane diverges
+// from its warp.  A lane-0-only timer read in
+// front of a warp-synchronous device call (ldlt_warp) left the warp split for
+// the whole call and made it 4x slower in traced runs.
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int slot, bool who) {
+    const unsigned long long t = gtimer();
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.global.u64 [%0], %1;\n}\n" ::"l"(tr + slot), "l"(t),
+        "r"(int(who)));
 }
 
 // ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers ----------------------
@@ -141,7 +152,6 @@ __device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double l
 // r[k] (final), l(i,k) = r[k] / d_k on lanes i > k, then r[j] = fma(-l(i,k),
 // a(j,k), r[j]) for k < j <= i with a(j,k) = lane j's r[k].  Identical
 // per-element operation sequence to ldlt_one_sync / k_solve / the oracle.
-// L(i,k) at A[k*kLdStride + i], D in D[].
 //
 // Software-pipelined so a step's critical path is divide -> the single fma
 // that finishes the next pivot column entry -> shuffle of d_{k+1}: the other
@@ -151,8 +161,13 @@ __device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double l
 // registers and lanes >= R receive harmless updates but are never read as
 // lower entries; dividends of inactive lanes are 1.0 (a zero dividend takes
 // the divide's slow path).
+//
+// L(i,k) goes to L[k*ldl + i] (i > k only) and d_k to D[k].  dmm (if set)
+// receives min_k d_k, max_k d_k, formed with the same compare sequence as the
+// solve_gram condition check (solve.cpp:24-31) from the broadcast d_k.
 template <int MAXR>
-__device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, double* A, double* D, double* col) {
+__device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, double* L, int ldl, double* D,
+                                       double* col, double* dmm) {
     // col: three 32-entry column buffers; column k lives in col[(k % 3) * 32]
     // from step k-1 (published) to step k+1 (read by the deferred updates).
     // The fmas read the broadcast column straight from shared memory (no
@@ -171,9 +186,12 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
     __syncwarp();
     double dk = __shfl_sync(0xffffffffu, r[0], 0);
     double lp = 0.0;  // l(lane, k-1)
+    double dmin = dk, dmax = dk;
 #pragma unroll
     for (int k = 0; k < MAXR; ++k) {
         if (k < R) {
+            if (dk < dmin) dmin = dk;
+            if (dk > dmax) dmax = dk;
             const double* cb = col + (k % 3) * 32;  // column k
             // a(k+1, k) in a register before the divide: the load would
             // otherwise sit between the quotient and the critical fma
@@ -195,11 +213,15 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
                 col[((k + 1) % 3) * 32 + lane] = r[k + 1];
             }
             if (lane == 0) D[k] = dk;
-            if (act) A[k * kLdStride + lane] = l;
+            if (act) L[k * ldl + lane] = l;
             __syncwarp();
             lp = l;
             dk = dn;
         }
+    }
+    if (dmm != nullptr && lane == 0) {
+        dmm[0] = dmin;
+        dmm[1] = dmax;
     }
 }
 
@@ -382,12 +404,15 @@ constexpr int kSmTotal = 27136;                  // doubles
 constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
 constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
 constexpr int kGramOneBlock = 16384;
+constexpr bool kBlockedNarrow = true;  // R <= 32: register-blocked contraction items too
 constexpr int kGramBlocksMax = 4;  // Gram pre-combine blocks when one block does not hold every partial
 constexpr int kTraceSlots = 24;                  // globaltimer stamps per stage (profiling aid)             // R^2 x chunks combined by one block up to this
 
 // kWide: R in 33..64 (register-blocked contraction); the R <= 32 instance
 // carries none of that code, so its register allocation is unaffected.
-template <bool kWide>
+// kTrace: the profiling build (phase stamps into p.trace); the production
+// instance carries no stamp code at all (kTrace = false folds tr to nullptr).
+template <bool kWide, bool kTrace>
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -469,8 +494,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * RP : p.gch + int64_t(st) * S * RP;
             const int tiles = (rows + kRowTile - 1) / kRowTile;
             const int n_contract = tiles * nsuper;
-            unsigned long long* tr = p.trace ? p.trace + (int64_t(b) * N + st) * kTraceSlots : nullptr;
-            if (tr && blockIdx.x == 0 && tid == 0) tr[0] = gtimer();
+            unsigned long long* tr = (kTrace && p.trace) ? p.trace + (int64_t(b) * N + st) * kTraceSlots : nullptr;
+            if (tr) trace_stamp(tr, 0, blockIdx.x == 0 && tid == 0);
 
             // stage start: TMA the first X_s tile of this block (independent of factors);
             // its arrive.expect_tx is issued with the Z tile in phase 1.
@@ -554,7 +579,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (cc < cn) Z[int64_t(c0) * RP + e] = z;
                 }
                 __syncthreads();
-                if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[14] = gtimer();
+                if (tr) trace_stamp(tr, 14, blockIdx.x == 0 && tid == 0 && ch == 0);
                 for (int q = tid; q < npairs; q += blockDim.x) {
                     const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
                     double acc = 0.0;
@@ -567,11 +592,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     p.chpart[int64_t(ch) * NPp + q] = acc;  // lower pair q; (j, i) is the same value
                 }
                 __syncthreads();
-                if (tr && blockIdx.x == 0 && tid == 0 && ch == 0) tr[15] = gtimer();
+                if (tr) trace_stamp(tr, 15, blockIdx.x == 0 && tid == 0 && ch == 0);
             }
             asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA in phase 1
             grid.sync();
-            if (tr && blockIdx.x == 0 && tid == 0) tr[1] = gtimer();
+            if (tr) trace_stamp(tr, 1, blockIdx.x == 0 && tid == 0);
 
             // ---------------- phase 1
             if (is_gram_block) {
@@ -597,7 +622,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     finisher = last_arrive_of(p.counter, unsigned(gram_blocks));
                 }
                 if (finisher) {
-                    if (tr && tid == 0) tr[3] = gtimer();
+                    if (tr) trace_stamp(tr, 3, tid == 0);
                     double* A = sm + kSmFact;        // [64][65]
                     double* D = A + 64 * kLdStride;  // 64
                     double* Gs = D + 64;             // R x R column-major
@@ -626,7 +651,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         mbar_wait(&bar, phase);
                         phase ^= 1u;
                     }
-                    if (tr && tid == 0) tr[18] = gtimer();
+                    if (tr) trace_stamp(tr, 18, tid == 0);
 #pragma unroll
                     for (int u = 0; u < kMaxPairsPerThread; ++u) {
                         const int q = tid + u * int(blockDim.x);
@@ -664,61 +689,97 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         Gs[j + i * R] = gb;
                     }
                     __syncthreads();
-                    if (tr && tid == 0) tr[10] = gtimer();
-                    // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
-                    if (tid == 0) {
-                        double maxdiag = Gs[0], trc = Gs[0];
+                    if (tr) trace_stamp(tr, 10, tid == 0);
+                    int reg;
+                    if (R <= 32) {
+                        // warp 0 factors G at once (the condition check's min / max of D formed
+                        // in the pivot loop) while warp 1 forms the solve_gram prologue
+                        // (solve.cpp:9-22); with maxdiag <= 0 the factors are never read (mode
+                        // 0), so starting early changes nothing
+                        double* dmm = D + 62;  // min d, max d (D holds R <= 32 entries)
+                        auto factor_w = [&](double lambda, double* mm) {
+                            if (R <= 8) ldlt_warp<8>(Gs, lambda, R, A, kLdStride, D, colb, mm);
+                            else if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, kLdStride, D, colb, mm);
+                            else if (R <= 24) ldlt_warp<24>(Gs, lambda, R, A, kLdStride, D, colb, mm);
+                            else ldlt_warp<32>(Gs, lambda, R, A, kLdStride, D, colb, mm);
+                        };
+                        if (tr) trace_stamp(tr, 12, tid == 0);
+                        if (warp == 0) {
+                            factor_w(0.0, dmm);
+                        } else if (warp == 1) {
+                            if (lane == 0) {
+                                double maxdiag = Gs[0], trc = Gs[0];
 #pragma unroll 8
-                        for (int k = 1; k < R; ++k) {
-                            const double dg = Gs[k * R + k];
-                            if (dg > maxdiag) maxdiag = dg;
-                            trc = trc + dg;
-                        }
-                        s_tr = trc;
-                        s_mode = (maxdiag <= 0.0) ? 0 : 1;
-                        s_reg = (s_mode == 0) ? 1 : 0;
-                    }
-                    __syncthreads();
-                    if (tr && tid == 0) tr[12] = gtimer();
-                    auto factor = [&](double lambda) {
-                        if (R <= 32) {
-                            if (warp == 0) {
-                                if (R <= 8) ldlt_warp<8>(Gs, lambda, R, A, D, colb);
-                                else if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, D, colb);
-                                else if (R <= 24) ldlt_warp<24>(Gs, lambda, R, A, D, colb);
-                                else ldlt_warp<32>(Gs, lambda, R, A, D, colb);
+                                for (int k = 1; k < R; ++k) {
+                                    const double dg = Gs[k * R + k];
+                                    if (dg > maxdiag) maxdiag = dg;
+                                    trc = trc + dg;
+                                }
+                                s_tr = trc;
+                                s_mode = (maxdiag <= 0.0) ? 0 : 1;
                             }
-                            __syncthreads();
-                        } else {
-                            ldlt_one_sync(A, D, R, lambda, Gs, pairs, npairs);
-                        }
-                    };
-                    if (s_mode == 1) {
-                        factor(0.0);
-                        if (tr && tid == 0) tr[13] = gtimer();
-                        if (tid == 0) {
-                            double dmin = D[0], dmax = D[0];
-#pragma unroll 8
-                            for (int k = 0; k < R; ++k) {
-                                const double dk = D[k];
-                                if (dk < dmin) dmin = dk;
-                                if (dk > dmax) dmax = dk;
-                            }
-                            s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+                            __syncwarp();
                         }
                         __syncthreads();
-                        if (s_reg) factor(1e-12 * s_tr);
+                        if (tr) trace_stamp(tr, 13, tid == 0);
+                        // solve_gram's regularisation decision (solve.cpp:24-31), by every thread
+                        reg = (s_mode == 0) ? 1
+                                            : ((!(dmm[0] > 0.0) || dmm[1] > kGramConditionLimit * dmm[0]) ? 1 : 0);
+                        if (s_mode == 1 && reg) {
+                            if (warp == 0) factor_w(1e-12 * s_tr, nullptr);
+                            __syncthreads();
+                        }
+                        if (tr) trace_stamp(tr, 11, tid == 0);
+                        // publish the strictly lower L (all the row solves read) and D
+                        for (int t = tid; t < RR; t += blockDim.x) {
+                            const int k = t / R, i = t - k * R;
+                            if (i > k) p.LD[t] = A[k * kLdStride + i];
+                        }
+                        if (tid < R) p.LD[RR + tid] = D[tid];
+                    } else {
+                        // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
+                        if (tid == 0) {
+                            double maxdiag = Gs[0], trc = Gs[0];
+#pragma unroll 8
+                            for (int k = 1; k < R; ++k) {
+                                const double dg = Gs[k * R + k];
+                                if (dg > maxdiag) maxdiag = dg;
+                                trc = trc + dg;
+                            }
+                            s_tr = trc;
+                            s_mode = (maxdiag <= 0.0) ? 0 : 1;
+                            s_reg = (s_mode == 0) ? 1 : 0;
+                        }
+                        __syncthreads();
+                        if (tr) trace_stamp(tr, 12, tid == 0);
+                        if (s_mode == 1) {
+                            ldlt_one_sync(A, D, R, 0.0, Gs, pairs, npairs);
+                            if (tr) trace_stamp(tr, 13, tid == 0);
+                            if (tid == 0) {
+                                double dmin = D[0], dmax = D[0];
+#pragma unroll 8
+                                for (int k = 0; k < R; ++k) {
+                                    const double dk = D[k];
+                                    if (dk < dmin) dmin = dk;
+                                    if (dk > dmax) dmax = dk;
+                                }
+                                s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+                            }
+                            __syncthreads();
+                            if (s_reg) ldlt_one_sync(A, D, R, 1e-12 * s_tr, Gs, pairs, npairs);
+                        }
+                        __syncthreads();
+                        reg = s_reg;
+                        if (tr) trace_stamp(tr, 11, tid == 0);
+                        for (int t = tid; t < RR; t += blockDim.x) {
+                            const int k = t / R, i = t % R;
+                            p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
+                        }
+                        for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
                     }
-                    __syncthreads();
-                    if (tr && tid == 0) tr[11] = gtimer();
-                    for (int t = tid; t < RR; t += blockDim.x) {
-                        const int k = t / R, i = t % R;
-                        p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
-                    }
-                    for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
                     if (tid == 0) {
                         p.mode_flag[0] = s_mode;
-                        if (s_reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
+                        if (reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
                         if (tr) tr[4] = gtimer();
                     }
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
@@ -739,19 +800,26 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     }
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
-                    if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[8] = gtimer();
+                    if (tr) trace_stamp(tr, 8, blockIdx.x == 0 && tid == 0 && item == 0);
                     const int nk = (cn + kChunk - 1) / kChunk;
                     const int cc0 = warp * kChunk;
                     const int ccn = min(kChunk, cn - cc0);
-                    if constexpr (kWide) {  // register-blocked item (R in 33..64)
+                    if (kWide || kBlockedNarrow) {  // register-blocked item
                         double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
                         const int cn0 = max(ccn, 0);
-                        if (RP == 40) chain_contract_blocked<10>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
-                        else if (RP == 48) chain_contract_blocked<12>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
-                        else if (RP == 56) chain_contract_blocked<14>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
-                        else chain_contract_blocked<16>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        if constexpr (kWide) {
+                            if (RP == 40) chain_contract_blocked<10>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else if (RP == 48) chain_contract_blocked<12>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else if (RP == 56) chain_contract_blocked<14>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else chain_contract_blocked<16>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        } else {
+                            if (RP == 8) chain_contract_blocked<2>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else if (RP == 16) chain_contract_blocked<4>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else if (RP == 24) chain_contract_blocked<6>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else chain_contract_blocked<8>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        }
                     }
-                    for (int g0 = 0; g0 < ng && !kWide; g0 += NGP) {
+                    for (int g0 = 0; g0 < ng && !kWide && !kBlockedNarrow; g0 += NGP) {
                         if (ccn > 0) {  // warp w = chunk w of the superchunk; lane = row
                             const int ngp = min(NGP, ng - g0);
                             if (ngp == 4) chain_chunk<4>(xs, zs, RP, g0, cc0, ccn, lane, cps, warp, CW);
@@ -771,13 +839,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         }
                         __syncthreads();
                     }
-                    if (tr && blockIdx.x == 0 && tid == 0 && item == 0) tr[9] = gtimer();
+                    if (tr) trace_stamp(tr, 9, blockIdx.x == 0 && tid == 0 && item == 0);
                 }
             }
-            if (tr && blockIdx.x == 0 && tid == 0) tr[2] = gtimer();
+            if (tr) trace_stamp(tr, 2, blockIdx.x == 0 && tid == 0);
             __syncthreads();
             grid.sync();
-            if (tr && blockIdx.x == 0 && tid == 0) tr[5] = gtimer();
+            if (tr) trace_stamp(tr, 5, blockIdx.x == 0 && tid == 0);
 
             // ---------------- phase B: row solves; idle blocks load the next stage's idx
             {
@@ -792,19 +860,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     }
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
-                    if (tr && blockIdx.x == 0 && tid == 0) tr[16] = gtimer();
+                    if (tr) trace_stamp(tr, 16, blockIdx.x == 0 && tid == 0);
                     const int mode = __ldcg(p.mode_flag);
                     double* out = (st == 0) ? u_new : p.U[st - 1];
                     chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ls + RR,
                                     mode);
-                    if (tr && blockIdx.x == 0 && tid == 0) tr[17] = gtimer();
+                    if (tr) trace_stamp(tr, 17, blockIdx.x == 0 && tid == 0);
                 }
                 load_idx(nb2, ns2);
             }
-            if (tr && blockIdx.x == 0 && tid == 0) tr[6] = gtimer();
+            if (tr) trace_stamp(tr, 6, blockIdx.x == 0 && tid == 0);
             __syncthreads();
             grid.sync();
-            if (tr && blockIdx.x == 0 && tid == 0) tr[7] = gtimer();
+            if (tr) trace_stamp(tr, 7, blockIdx.x == 0 && tid == 0);
         }
     }
 }

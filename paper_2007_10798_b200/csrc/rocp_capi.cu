@@ -962,33 +962,39 @@ size_t chain_smem(int R, int B) {
     return size_t(kSmTotal) * sizeof(double);  // fixed map (kernels.cuh, k_chain)
 }
 
-template <bool kWide>
+template <bool kWide, bool kTrace>
 void launch_chain_inst(rocp_stream* st, const ChainParams& p) {
     rocp_dev* dev = st->dev;
     const size_t smem = chain_smem(st->R, p.B);
-    static int max_dyn = 0;
-    if (max_dyn == 0) {
+    // the dynamic shared memory opt-in is a per-device function attribute
+    constexpr int kMaxDevices = 64;
+    static int max_dyn[kMaxDevices] = {};
+    if (dev->device < 0 || dev->device >= kMaxDevices) throw RocpError{ROCP_E_CUDA, "device ordinal out of range"};
+    int& md = max_dyn[dev->device];
+    if (md == 0) {
         int optin = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device));
         cudaFuncAttributes fa{};
-        CK(cudaFuncGetAttributes(&fa, k_chain<kWide>));
-        max_dyn = optin - int(fa.sharedSizeBytes);
-        CK(cudaFuncSetAttribute(k_chain<kWide>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+        CK(cudaFuncGetAttributes(&fa, k_chain<kWide, kTrace>));
+        CK(cudaFuncSetAttribute(k_chain<kWide, kTrace>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - int(fa.sharedSizeBytes)));
+        md = optin - int(fa.sharedSizeBytes);
     }
-    if (smem > size_t(max_dyn)) throw_domain("batch too large for the persistent chain kernel's shared memory");
+    if (smem > size_t(md)) throw_domain("batch too large for the persistent chain kernel's shared memory");
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<kWide>, kChainThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<kWide, kTrace>, kChainThreads, smem));
     if (per_sm < 1) throw RocpError{ROCP_E_CUDA, "k_chain does not fit on an SM"};
     const int grid = dev->num_sms;  // one persistent block per SM
     void* args[] = {const_cast<ChainParams*>(&p)};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_chain<kWide>), dim3(grid), dim3(kChainThreads),
-                                   args, smem, dev->stream));
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_chain<kWide, kTrace>), dim3(grid),
+                                   dim3(kChainThreads), args, smem, dev->stream));
     after_launch(dev, "k_chain");
 }
 
 void launch_chain_k(rocp_stream* st, const ChainParams& p) {
-    if (p.R > 32) launch_chain_inst<true>(st, p);
-    else launch_chain_inst<false>(st, p);
+    const bool wide = p.R > 32, trace = p.trace != nullptr;
+    if (wide) trace ? launch_chain_inst<true, true>(st, p) : launch_chain_inst<true, false>(st, p);
+    else trace ? launch_chain_inst<false, true>(st, p) : launch_chain_inst<false, false>(st, p);
 }
 
 // The whole factor-dependent chain of the prepared window as ONE cooperative

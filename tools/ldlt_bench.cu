@@ -27,8 +27,8 @@ __global__ void k_ldlt_warp(const double* G, int R, long long* cyc, double* out)
     __syncthreads();
     long long t0 = clock64();
     if (threadIdx.x < 32) {
-        if (R <= 16) ldlt_warp<16>(Gs, 0.0, R, sm, sm + 64 * kLdStride, Gs + R * R);
-        else ldlt_warp<32>(Gs, 0.0, R, sm, sm + 64 * kLdStride, Gs + R * R);
+        if (R <= 16) ldlt_warp<16>(Gs, 0.0, R, sm, kLdStride, sm + 64 * kLdStride, Gs + R * R, nullptr);
+        else ldlt_warp<32>(Gs, 0.0, R, sm, kLdStride, sm + 64 * kLdStride, Gs + R * R, nullptr);
     }
     __syncthreads();
     long long t1 = clock64();
