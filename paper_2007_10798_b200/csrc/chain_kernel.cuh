@@ -228,13 +228,18 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
 constexpr int kMaxSuperRows = 8;  // superchunk partials prefetched per row entry
 constexpr int kQPre = 3;          // Q pairs per thread prefetched by the Gram finisher
 
-// Row solves of phase 2: warp per row, lanes own entries j and j + 32.
+// Row solves of phase 2: warp per row, lanes own entries j and j + 32.  Every
+// load of the row (superchunk partials, P, the mode flag) is issued before the
+// wait for the L / D bulk copy (bar, phase), which none of them depend on.
 __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
                                              int rows, int R, int nsuper, double* out, const double* Ls,
-                                             const double* Ds, int mode) {
+                                             const double* Ds, uint64_t* bar, unsigned phase,
+                                             const int* mode_flag) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int j0 = lane, j1 = lane + 32;
     const bool v0 = j0 < R, v1 = j1 < R;
+    const int mode = __ldcg(mode_flag);
+    bool ld_ready = false;
     for (int row = blockIdx.x + warp * gridDim.x; row < rows; row += gridDim.x * nw) {
         double w0 = 0.0, w1 = 0.0;
         // every load of the row (superchunk partials, P) in flight at once
@@ -247,6 +252,10 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
         if (st > 0) {
             if (v0) p0 = __ldcg(Prow_base + int64_t(row) * R + j0);
             if (v1) p1 = __ldcg(Prow_base + int64_t(row) * R + j1);
+        }
+        if (!ld_ready) {
+            mbar_wait(bar, phase);
+            ld_ready = true;
         }
         if (v0) {
             double tot = c0[0];
@@ -276,6 +285,7 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
             w0 = 0.0;
             w1 = 0.0;
         } else {
+#pragma unroll 4
             for (int k = 0; k < R; ++k) {  // forward, k increasing
                 const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
                 if (v0 && j0 > k) w0 = __fma_rn(-Ls[k * R + j0], wk, w0);
@@ -283,6 +293,7 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
             }
             if (v0) w0 = (fabs(Ds[j0]) > 2.2250738585072014e-308) ? w0 / Ds[j0] : 0.0;
             if (v1) w1 = (fabs(Ds[j1]) > 2.2250738585072014e-308) ? w1 / Ds[j1] : 0.0;
+#pragma unroll 4
             for (int k = R - 1; k >= 0; --k) {  // backward, k decreasing
                 const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
                 if (j0 < k) w0 = __fma_rn(-Ls[j0 * R + k], wk, w0);
@@ -292,6 +303,73 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
         if (v0) out[int64_t(row) * R + j0] = w0;
         if (v1) out[int64_t(row) * R + j1] = w1;
     }
+    if (!ld_ready) mbar_wait(bar, phase);  // the phase completes before the barrier's next use
+}
+
+// Row solves for R <= MAXR <= 32 (one entry per lane): the lane's L entries
+// live in registers and the k loop is unrolled (compile-time shuffle source,
+// uniform exit at k = R), so a substitution step is one shuffle and one fma;
+// same per-element operation sequence as chain_rows_warp.
+template <int MAXR>
+__device__ __noinline__ void chain_rows_narrow(const double* __restrict__ cpart, double* Prow_base, int st,
+                                               int rows, int R, int nsuper, double* out, const double* Ls,
+                                               const double* Ds, uint64_t* bar, unsigned phase,
+                                               const int* mode_flag) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int j0 = lane;
+    const bool v0 = j0 < R;
+    const int mode = __ldcg(mode_flag);
+    bool ld_ready = false;
+    for (int row = blockIdx.x + warp * gridDim.x; row < rows; row += gridDim.x * nw) {
+        double c0[kMaxSuperRows], p0 = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxSuperRows; ++m)
+            c0[m] = (v0 && m < nsuper) ? __ldcg(cpart + (int64_t(m) * rows + row) * R + j0) : 0.0;
+        if (st > 0 && v0) p0 = __ldcg(Prow_base + int64_t(row) * R + j0);
+        if (!ld_ready) {
+            mbar_wait(bar, phase);
+            ld_ready = true;
+        }
+        double lf[MAXR];  // L(j0, k), k < j0 (forward)
+#pragma unroll
+        for (int k = 0; k < MAXR; ++k) lf[k] = (k < R && v0 && j0 > k) ? Ls[k * R + j0] : 0.0;
+        double w0 = 0.0;
+        if (v0) {
+            double tot = c0[0];
+#pragma unroll
+            for (int m = 1; m < kMaxSuperRows; ++m)
+                if (m < nsuper) tot = tot + c0[m];
+            for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j0);
+            if (st > 0) {
+                tot = p0 + tot;
+                Prow_base[int64_t(row) * R + j0] = tot;
+            }
+            w0 = tot;
+        }
+        if (mode == 0) {
+            w0 = 0.0;
+        } else {
+#pragma unroll
+            for (int k = 0; k < MAXR; ++k) {  // forward, k increasing
+                if (k >= R) break;
+                const double wk = __shfl_sync(0xffffffffu, w0, k);
+                if (v0 && j0 > k) w0 = __fma_rn(-lf[k], wk, w0);
+            }
+            double lb[MAXR];  // L(k, j0), k > j0 (backward); loads land under the divide
+#pragma unroll
+            for (int k = 0; k < MAXR; ++k) lb[k] = (k < R && j0 < k) ? Ls[j0 * R + k] : 0.0;
+            if (v0) w0 = (fabs(Ds[j0]) > 2.2250738585072014e-308) ? w0 / Ds[j0] : 0.0;
+#pragma unroll
+            for (int k = MAXR - 1; k >= 0; --k) {  // backward, k decreasing
+                if (k < R) {
+                    const double wk = __shfl_sync(0xffffffffu, w0, k);
+                    if (j0 < k) w0 = __fma_rn(-lb[k], wk, w0);
+                }
+            }
+        }
+        if (v0) out[int64_t(row) * R + j0] = w0;
+    }
+    if (!ld_ready) mbar_wait(bar, phase);  // the phase completes before the barrier's next use
 }
 
 // One warp's chunk of the contraction: lane = row, NG groups of 8 r's at a
@@ -858,13 +936,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         tma_load_1d(Ls, p.LD, bytes, &bar);
                         mbar_expect_tx(&bar, bytes);
                     }
-                    mbar_wait(&bar, phase);
-                    phase ^= 1u;
                     if (tr) trace_stamp(tr, 16, blockIdx.x == 0 && tid == 0);
-                    const int mode = __ldcg(p.mode_flag);
                     double* out = (st == 0) ? u_new : p.U[st - 1];
-                    chain_rows_warp(p.cpart, st > 0 ? p.P[st - 1] : nullptr, st, rows, R, nsuper, out, Ls, Ls + RR,
-                                    mode);
+                    double* Pst = st > 0 ? p.P[st - 1] : nullptr;
+                    if constexpr (kWide) {
+                        chain_rows_warp(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
+                    } else {
+                        if (R <= 8) chain_rows_narrow<8>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
+                        else if (R <= 16) chain_rows_narrow<16>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
+                        else if (R <= 24) chain_rows_narrow<24>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
+                        else chain_rows_narrow<32>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
+                    }
+                    phase ^= 1u;
                     if (tr) trace_stamp(tr, 17, blockIdx.x == 0 && tid == 0);
                 }
                 load_idx(nb2, ns2);
