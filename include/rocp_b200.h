@@ -63,6 +63,13 @@ uint64_t rocp_kernel_launches(const rocp_dev* dev);
  * elapsed milliseconds between two recorded slots (waits for the second). */
 rocp_status rocp_timer_record(rocp_dev* dev, int slot);
 rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms);
+/* SMs reserved for the overlapped window gather of stream windows (DESIGN.md
+ * 5.3): the gather runs on `sms` SMs beside the persistent chain kernel, which
+ * takes the rest; 0 gathers each window on every SM before the chain; < 0
+ * (default, unless ROCP_GATHER_SMS is set) lets a per-stream model choose.
+ * Results are bitwise identical for every setting.  No reference counterpart
+ * (a B200 scheduling knob). */
+rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms);
 /* The handle's cudaStream_t (for callers that interoperate). */
 void* rocp_cuda_stream(rocp_dev* dev);
 /* Page-locked, CUDA-registered host buffer backed by 2 MB (transparent huge)

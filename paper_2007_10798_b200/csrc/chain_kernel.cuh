@@ -29,6 +29,12 @@ namespace rocpk {
 //                forward / diagonal / backward solve -> U(n) or u_new row | grid barrier
 // Arithmetic is exactly that of the per-stage kernels (bitwise equal).
 
+__device__ __forceinline__ unsigned long long gtimer_raw() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct ChainParams {
     int N, R, S, nb, B, nsuper, resid_level;
     int32_t head[kMaxOrder];
@@ -52,7 +58,28 @@ struct ChainParams {
     double* rpart;            // 3 x S
     unsigned int* counter;    // [0] Gram arrivals, [1] residual arrivals
     unsigned long long* trace;  // optional phase timestamps (globaltimer ns), 16 per stage
+    // overlapped window gather (k_gather_warps on reserved SMs): per (b*N + stage) units
+    // published / needed; nullptr when the window was gathered before the launch
+    const unsigned* gdone;
+    const unsigned* gneed;
 };
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+// Waits until the overlapped gather published every unit of one (batch, stage)
+// (seen = a value loaded earlier, usually during the previous phase).  A gather
+// that never arrives traps after ~4 s instead of hanging the device.
+__device__ __noinline__ void wait_gathered(const unsigned* done, unsigned need, unsigned seen) {
+    if (seen >= need) return;
+    const unsigned long long t0 = gtimer_raw();
+    while (ld_acquire_u32(done) < need) {
+        __nanosleep(128);
+        if (gtimer_raw() - t0 > 4000000000ull) __trap();
+    }
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -552,6 +579,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
         }
     };
     load_idx(0, 0);
+    // overlapped gather: the count of the next (batch, stage), loaded a phase ahead
+    unsigned gseen = 0;
+    if (p.gdone && tid == 0) gseen = ld_acquire_u32(p.gdone);
 
     for (int b = 0; b < p.nb; ++b) {
         double* u_new = p.temporal + (p.t_len0 + int64_t(b) * p.B) * R;
@@ -587,6 +617,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             if (contract_block && tid == 0) {
                 const int tile = first_item % tiles, m = first_item / tiles;
                 const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                if (p.gdone) {  // X_s of this (batch, stage) comes from the overlapped gather
+                    wait_gathered(p.gdone + b * N + st, __ldg(p.gneed + b * N + st), gseen);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
+                }
                 fence_proxy_async();
                 tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
             }
@@ -951,6 +985,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (tr) trace_stamp(tr, 17, blockIdx.x == 0 && tid == 0);
                 }
                 load_idx(nb2, ns2);
+                if (p.gdone && tid == 0 && nb2 < p.nb) gseen = ld_acquire_u32(p.gdone + nb2 * N + ns2);
             }
             if (tr) trace_stamp(tr, 6, blockIdx.x == 0 && tid == 0);
             __syncthreads();

@@ -123,6 +123,11 @@ struct GatherJob {
     double* out;
     int tiled;   // 0: I x s column-major; 1: row-tiled (see xs_offset)
     const int32_t* perm;  // row-tiled strided jobs: samples in fibre-base order (or nullptr)
+    // overlapped gather (gather_kernel.cuh): tensor-map view + 1 of this strided job (0 = LSU
+    // loads), box length along the fibre, and the job's slab offset from the window start
+    int32_t tmap1;
+    int32_t tlen;
+    int64_t toff;
 };
 
 // Row-tiled X_s layout (stream windows): rows in tiles of 32, each tile's

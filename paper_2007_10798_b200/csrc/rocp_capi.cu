@@ -14,8 +14,10 @@
 #include "kernels.cuh"
 #include "chain_kernel.cuh"
 #include "shard_kernels.cuh"
+#include "gather_kernel.cuh"
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (the driver entry point is fetched at run time)
 #include <dlfcn.h>
 #include <immintrin.h>
 #include <nccl.h>  // types only: the library is bound at run time (NcclApi)
@@ -175,6 +177,9 @@ struct JobList {
     DBuf<GatherTile> tiles;
     DBuf<SortJob> sort;
     int ndraw = 0, ngather = 0, ntiles = 0, nsort = 0;
+    // overlapped gather (k_gather_warps): unit prefix per job, units published / needed
+    DBuf<uint32_t> ustart;
+    DBuf<unsigned> done, need;
     int64_t max_s = 0;
     int64_t gather_elems = 0;
 };
@@ -198,6 +203,10 @@ struct rocp_dev {
     DBuf<unsigned int> tile_counters;   // per-row-tile arrival counters (self-resetting)
     DBuf<int64_t> rows_in;              // explicit index scratch of the primitives
     cudaEvent_t timer[8] = {};          // rocp_timer_* slots
+    // overlapped window gather: its own stream on SMs reserved beside the chain kernel
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t ev_gready = nullptr, ev_gdone = nullptr;
+    int gather_sms = -1;                // -1: not set (env decides); -2: per-stream model; >= 0: fixed
     int num_sms = 148;
     // device-resident result of the last rocp_cprand (for stream_create_from_init)
     struct Init {
@@ -298,6 +307,18 @@ void upload_jobs(rocp_dev* dev, JobList& L, const std::vector<DrawJob>& dj,
         } else {
             for (uint32_t e0 = 0; e0 < total; e0 += kGatherTile) tiles.push_back(GatherTile{int32_t(k), e0});
         }
+    }
+    {  // warp units of the overlapped gather (k_gather_warps)
+        std::vector<uint32_t> us(gj.size() + 1, 0), nd(std::max<size_t>(gj.size(), 1), 0);
+        for (size_t k = 0; k < gj.size(); ++k) {
+            nd[k] = gather_units(gj[k]);
+            us[k + 1] = us[k] + nd[k];
+        }
+        L.ustart.ensure(us.size());
+        L.need.ensure(nd.size());
+        L.done.ensure(nd.size());
+        CK(cudaMemcpyAsync(L.ustart.p, us.data(), us.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, dev->stream));
+        CK(cudaMemcpyAsync(L.need.p, nd.data(), nd.size() * sizeof(unsigned), cudaMemcpyHostToDevice, dev->stream));
     }
     L.sort.ensure(std::max<size_t>(sj.size(), 1));
     if (!sj.empty())
@@ -656,6 +677,7 @@ struct Window {
     bool key_host = false;
     const double* key_zc = nullptr;
     std::vector<int64_t> zc_tile;  // host path: first zero-copy gather tile of each batch
+    GatherTmaParams gtp{};         // tensor-map views of the strided modes (overlapped gather)
 };
 
 // Window of a sharded stream: per (batch, stage) the global draws, the
@@ -710,6 +732,7 @@ struct rocp_stream {
     DBuf<uint64_t> seed_dev;      // draw seed (device, so graphs need no re-capture)
     DBuf<uint32_t> batch_dev;     // first batch id of the window (device)
     int resid_level = 1;          // 0 none, 1 temporal stage (default), 2 every stage
+    int win_gsms = 0;             // SMs of the current window's overlapped gather (0: none)
     int host_threads = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
     std::unique_ptr<HostPool> pool;  // host-slab gather workers (created on first use)
     // mode-1 sharding: U(1)/P(1) hold rows [r0, r1) and
@@ -812,6 +835,47 @@ int64_t* win_base(rocp_stream* st, int64_t b, int stage) { return st->win.base.p
 int64_t* win_rows(rocp_stream* st, int64_t b, int stage) { return st->win.rows.p + (b * st->N + stage) * st->s; }
 double* win_x(rocp_stream* st, int64_t b, int stage) { return st->win.X.p + st->win.xoff[size_t(b * st->N + stage)]; }
 
+// Tensor-map view for the TMA units of the overlapped gather (gather_kernel.cuh):
+// the window range x (dims wd, time extent = the window's slices) seen as
+// (I1, Ma, In, Mb) for strided mode `mode`, box {2, 1, L, 1} with L = min(256,
+// fibre length); mode 1 as (I1, 1, 1, rest) with box {L, 1, 1, 1}.  Returns false where TMA cannot express it (odd I1: row
+// strides must be 16-byte multiples; a misaligned range; extents past 2^31) or
+// ROCP_GATHER_TMA=0; those jobs use LSU loads.
+bool make_gather_view(const double* x, const std::vector<int64_t>& wd, int mode, int64_t fibre_len, CUtensorMap* map,
+                      GatherView* view) {
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        const char* e = std::getenv("ROCP_GATHER_TMA");
+        if (e && std::atoi(e) == 0) return PFN_cuTensorMapEncodeTiled_v12000(nullptr);
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const int N = int(wd.size());
+    const int64_t I1 = wd[0];
+    if (I1 % 2 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0 || mode < 1 || mode > N) return false;
+    int64_t Ma = 1, Mb = 1;
+    for (int k = 1; k < mode - 1; ++k) Ma *= wd[size_t(k)];
+    for (int k = std::max(mode, 1); k < N; ++k) Mb *= wd[size_t(k)];
+    const int64_t In = mode == 1 ? 1 : wd[size_t(mode - 1)];
+    const int64_t lim = int64_t(1) << 31;
+    if (Ma >= lim || In >= lim || Mb >= lim || I1 >= lim) return false;
+    const cuuint64_t dims[4] = {cuuint64_t(I1), cuuint64_t(Ma), cuuint64_t(In), cuuint64_t(Mb)};
+    const cuuint64_t gstr[3] = {cuuint64_t(I1) * 8, cuuint64_t(I1 * Ma) * 8, cuuint64_t(I1 * Ma * In) * 8};
+    const cuuint32_t L = cuuint32_t(std::min<int64_t>(kGWBox, fibre_len));
+    const cuuint32_t box[4] = {mode == 1 ? L : 2u, 1, mode == 1 ? 1u : L, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    *view = GatherView{I1, Ma, In, mode == 1 ? 1 : 0};
+    return true;
+}
+
 // Builds (or reuses) the draw + gather job lists of nb consecutive slabs of B
 // slices starting at x (device pointer, slice = elements per slice).  Batch
 // ids come from st->batch_dev + b, the seed from st->seed_dev, so the lists
@@ -834,6 +898,14 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
     std::vector<GatherJob> gj;
     std::vector<SortJob> sj;
     const std::vector<int64_t> strides = strides_of(d);
+    // tensor-map views of the strided modes over the whole window range (overlapped gather)
+    bool tma_mode[kMaxOrder + 1] = {};
+    if (!host_gather) {
+        const std::vector<int64_t> wd = [&] { std::vector<int64_t> v = slab_dims(st, B); v.back() = B * nb; return v; }();
+        for (int mode = 1; mode <= st->N; ++mode)
+            tma_mode[mode] = make_gather_view(x + t0 * slice, wd, mode, mode == st->N ? B : wd[size_t(mode - 1)],
+                                              &W.gtp.map[mode - 1], &W.gtp.view[mode - 1]);
+    }
     W.zc_tile.assign(size_t(nb + 1), 0);
     int64_t ntile = 0;
     for (int64_t b = 0; b < nb; ++b) {
@@ -852,6 +924,11 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
                 if (strides[size_t(mode - 1)] != 1 && st->s <= kSortMax) {  // strided: fibre-base order
                     g.perm = st->win.perm.p + (b * st->N + stage) * st->s;
                     sj.push_back(SortJob{win_base(st, b, stage), const_cast<int32_t*>(g.perm), int32_t(st->s)});
+                }
+                if (tma_mode[mode]) {
+                    g.tmap1 = mode;
+                    g.tlen = int32_t(std::min<int64_t>(kGWBox, d[size_t(mode - 1)]));
+                    g.toff = b * B * slice;
                 }
                 gj.push_back(g);
             } else if (zc_src && strides[size_t(mode - 1)] == 1) {
@@ -875,14 +952,85 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
     W.key_zc = zc_src;
 }
 
+// SMs reserved for the overlapped window gather.  ROCP_GATHER_SMS
+// overrides; otherwise a model picks the fewest SMs whose TMA gather (about
+// 1.47 G elements/s per SM, measured) keeps pace with the chain (about 14 us
+// per stage for R <= 32, 110 us for the wide kernel), and 0 -- the whole window
+// gathered on every SM before the chain -- when the gather would be under a
+// tenth of the step (then the SMs are worth more to the chain: C1, C3, C5).
+// The chain keeps one warp per row of its largest stage where that fits on
+// the device (a second row-solve round costs more than the gather saves).
+int gather_sms(rocp_stream* st, int64_t B) {
+    rocp_dev* dev = st->dev;
+    if (!dev->gstream) {  // first use on this device: env override and the gather stream
+        if (dev->gather_sms == -1) {
+            dev->gather_sms = -2;
+            if (const char* e = std::getenv("ROCP_GATHER_SMS")) dev->gather_sms = std::max(0, std::atoi(e));
+        }
+        CK(cudaFuncSetAttribute(k_gather_warps, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGWSmem)));
+        CK(cudaStreamCreateWithFlags(&dev->gstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&dev->ev_gready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&dev->ev_gdone, cudaEventDisableTiming));
+    }
+    int g = dev->gather_sms;
+    if (g == -2) {
+        double elems = double(B), rows_max = double(B);  // gathered elements per sample of one batch
+        for (int64_t I : st->head) {
+            elems += double(I);
+            rows_max = std::max(rows_max, double(I));
+        }
+        elems *= double(st->s);
+        const double t_chain = st->N * (st->R > 32 ? 110.0 : 14.0);     // us per batch
+        const double t_full = elems / (93e3);                             // us, whole-device gather
+        if (t_full < 0.1 * (t_full + t_chain)) return 0;
+        g = int(std::ceil(elems / (1470.0 * t_chain)));
+        const int row_blocks = int(std::ceil(rows_max / (kChainThreads / 32)));
+        if (row_blocks < dev->num_sms) g = std::min(g, dev->num_sms - row_blocks);
+        g = std::max(g, 8);
+    }
+    return std::max(0, std::min(g, dev->num_sms / 2));
+}
+
 // Draw + gather of the prepared window (seed / first batch id set on device).
-void enqueue_draw_gather(rocp_stream* st, uint64_t seed, uint32_t first_batch_id) {
+// overlap: the gather runs as k_gather_warps on the gather stream, concurrently
+// with the chain launched next (launch_chain(..., overlap = true)), which waits
+// per (batch, stage) on the published unit counts.
+void enqueue_draw_gather(rocp_stream* st, uint64_t seed, uint32_t first_batch_id, bool overlap = false) {
+    if (overlap && st->win_gsms <= 0) throw RocpError{ROCP_E_STATE, "overlapped gather without SMs (internal)"};
     rocp_dev* dev = st->dev;
     k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
     after_launch(dev, "k_set_u64");
     k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
     after_launch(dev, "k_set_u32");
-    launch_draw(dev, st->win.jobs);
+    const JobList& L = st->win.jobs;
+    if (overlap) {
+        CK(cudaMemsetAsync(L.done.p, 0, size_t(L.ngather) * sizeof(unsigned), dev->stream));
+        launch_draw(dev, L);
+        if (L.nsort > 0) {
+            k_sort_by_base<<<L.nsort, 1024, 0, dev->stream>>>(L.sort.p);
+            after_launch(dev, "k_sort_by_base");
+        }
+        CK(cudaEventRecord(dev->ev_gready, dev->stream));
+        CK(cudaStreamWaitEvent(dev->gstream, dev->ev_gready, 0));
+        std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+        if (st->time_gather) {
+            if (st->gather_events_used == st->gather_events.size()) {
+                cudaEvent_t a, b;
+                CK(cudaEventCreate(&a));
+                CK(cudaEventCreate(&b));
+                st->gather_events.emplace_back(a, b);
+            }
+            ev = &st->gather_events[st->gather_events_used++];
+            CK(cudaEventRecord(ev->first, dev->gstream));
+        }
+        k_gather_warps<<<st->win_gsms, kGWThreads, kGWSmem, dev->gstream>>>(st->win.gtp, L.gather.p, L.ngather,
+                                                                                L.ustart.p, L.done.p);
+        after_launch(dev, "k_gather_warps");
+        if (ev) CK(cudaEventRecord(ev->second, dev->gstream));
+        CK(cudaEventRecord(dev->ev_gdone, dev->gstream));
+        return;
+    }
+    launch_draw(dev, L);
     if (st->time_gather) {
         if (st->gather_events_used == st->gather_events.size()) {
             cudaEvent_t a, b;
@@ -963,7 +1111,7 @@ size_t chain_smem(int R, int B) {
 }
 
 template <bool kWide, bool kTrace>
-void launch_chain_inst(rocp_stream* st, const ChainParams& p) {
+void launch_chain_inst(rocp_stream* st, const ChainParams& p, int grid) {
     rocp_dev* dev = st->dev;
     const size_t smem = chain_smem(st->R, p.B);
     // the dynamic shared memory opt-in is a per-device function attribute
@@ -984,22 +1132,23 @@ void launch_chain_inst(rocp_stream* st, const ChainParams& p) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<kWide, kTrace>, kChainThreads, smem));
     if (per_sm < 1) throw RocpError{ROCP_E_CUDA, "k_chain does not fit on an SM"};
-    const int grid = dev->num_sms;  // one persistent block per SM
     void* args[] = {const_cast<ChainParams*>(&p)};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_chain<kWide, kTrace>), dim3(grid),
                                    dim3(kChainThreads), args, smem, dev->stream));
     after_launch(dev, "k_chain");
 }
 
-void launch_chain_k(rocp_stream* st, const ChainParams& p) {
+// grid: one persistent block per SM, less the SMs of an overlapped gather
+void launch_chain_k(rocp_stream* st, const ChainParams& p, int grid) {
     const bool wide = p.R > 32, trace = p.trace != nullptr;
-    if (wide) trace ? launch_chain_inst<true, true>(st, p) : launch_chain_inst<true, false>(st, p);
-    else trace ? launch_chain_inst<false, true>(st, p) : launch_chain_inst<false, false>(st, p);
+    if (wide) trace ? launch_chain_inst<true, true>(st, p, grid) : launch_chain_inst<true, false>(st, p, grid);
+    else trace ? launch_chain_inst<false, true>(st, p, grid) : launch_chain_inst<false, false>(st, p, grid);
 }
 
 // The whole factor-dependent chain of the prepared window as ONE cooperative
 // persistent kernel (kernels.cuh K6).
-void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
+// overlap: the window's gather is still running (enqueue_draw_gather(..., true)).
+void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool overlap = false) {
     ChainParams p{};
     p.N = st->N;
     p.R = st->R;
@@ -1031,6 +1180,13 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
     p.resid = st->resid.p;
     p.rpart = st->rpart.p;
     p.counter = st->dev->counters.p + 4;
+    int grid = st->dev->num_sms;
+    if (overlap) {
+        if (b0 != 0) throw RocpError{ROCP_E_STATE, "overlapped gather needs the whole window (internal)"};
+        p.gdone = st->win.jobs.done.p;
+        p.gneed = st->win.jobs.need.p;
+        grid -= st->win_gsms;
+    }
     if (st->trace_on) {
         st->trace.ensure(size_t(nb * st->N * kTraceSlots));
         CK(cudaMemsetAsync(st->trace.p, 0, size_t(nb * st->N * kTraceSlots) * 8, st->dev->stream));
@@ -1048,11 +1204,12 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0) {
         }
         auto& ev = st->chain_events[st->chain_events_used++];
         CK(cudaEventRecord(ev.first, st->dev->stream));
-        launch_chain_k(st, p);
+        launch_chain_k(st, p, grid);
         CK(cudaEventRecord(ev.second, st->dev->stream));
     } else {
-        launch_chain_k(st, p);
+        launch_chain_k(st, p, grid);
     }
+    if (overlap) CK(cudaStreamWaitEvent(st->dev->stream, st->dev->ev_gdone, 0));  // join the gather stream
     if (st->resid_level >= 1) {  // sampled residual of every batch's temporal solve (off the chain)
         WinResidParams w{};
         w.N = st->N;
@@ -1086,8 +1243,10 @@ void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uin
     check_capacity(st, B);
     const int64_t slice = prod(st->head);
     prepare_window(st, x, 0, slice, B, 1, nullptr, nullptr, -1);
-    enqueue_draw_gather(st, seed, batch_id);
-    if (st->resid_level <= 1) launch_chain(st, 1, B);
+    st->win_gsms = st->resid_level <= 1 ? gather_sms(st, B) : 0;
+    const bool overlap = st->win_gsms > 0;
+    enqueue_draw_gather(st, seed, batch_id, overlap);
+    if (st->resid_level <= 1) launch_chain(st, 1, B, 0, overlap);
     else enqueue_chain(st, 1, B);
     st->t_len += B;  // rocp.cpp:159
 }
@@ -1145,11 +1304,25 @@ void rocp_destroy(rocp_dev* dev) {
     for (cudaEvent_t& e : dev->timer)
         if (e) cudaEventDestroy(e);
     if (dev->comm) nccl_api().comm_destroy(dev->comm);
+    if (dev->gstream) {
+        cudaStreamSynchronize(dev->gstream);
+        cudaStreamDestroy(dev->gstream);
+        cudaEventDestroy(dev->ev_gready);
+        cudaEventDestroy(dev->ev_gdone);
+    }
     cudaStreamDestroy(dev->stream);
     delete dev;
 }
 
 const char* rocp_last_error(const rocp_dev* dev) { return dev ? dev->err.c_str() : "null handle"; }
+
+rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms) {
+    return guarded(dev, [&] {
+        if (sms > dev->num_sms / 2) throw_domain("gather SMs: at most half the device");
+        CK(cudaStreamSynchronize(dev->stream));
+        dev->gather_sms = sms < 0 ? -2 : sms;
+    });
+}
 
 rocp_status rocp_timer_record(rocp_dev* dev, int slot) {
     return guarded(dev, [&] {
@@ -1870,9 +2043,11 @@ rocp_status rocp_stream_consume_range(rocp_stream* st, const rocp_tensor* x, int
             return;
         }
         prepare_window(st, x->d, t0, slice, batch, nb, nullptr, nullptr, -1);
-        enqueue_draw_gather(st, seed, first_batch_id);
+        st->win_gsms = st->resid_level <= 1 ? gather_sms(st, batch) : 0;
+        const bool overlap = st->win_gsms > 0;
+        enqueue_draw_gather(st, seed, first_batch_id, overlap);
         if (st->resid_level <= 1) {
-            launch_chain(st, nb, batch);
+            launch_chain(st, nb, batch, 0, overlap);
         } else {
             auto key = std::make_tuple(nb, batch, st->t_len);
             auto it = st->graphs.find(key);
