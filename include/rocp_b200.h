@@ -245,6 +245,16 @@ rocp_status rocp_stream_set_residual_tracking(rocp_stream* st, int level);
 rocp_status rocp_stream_time_gather(rocp_stream* st, int enable);
 rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* count);
 rocp_status rocp_stream_chain_times(rocp_stream* st, float* ms, int max, int* count);
+/* Profiling aid: draw + sort + the window gather of consume_range's window
+ * (t0, batch, nb, seed, first_batch_id) ALONE, as k_gather_warps on `sms` SMs
+ * (<= 0: every SM), event-timed into *ms.  Fills the window scratch only; the
+ * stream's model is untouched.  Used by bench.py for the gather kernel's
+ * whole-device roofline (in a step it runs overlapped on a few SMs). */
+/* SMs the last stream window's gather was overlapped on (0: gathered on every
+ * SM before the chain). */
+rocp_status rocp_stream_last_gather_sms(const rocp_stream* st, int* sms);
+rocp_status rocp_stream_gather_window(rocp_stream* st, const rocp_tensor* x, int64_t t0, int64_t batch, int64_t nb,
+                                      uint64_t seed, uint32_t first_batch_id, int sms, float* ms);
 /* Profiling aid: globaltimer stamps of the persistent chain kernel, 24 per
  * (batch, stage) of the last window (phase boundaries, Gram finisher steps,
  * row solves; tools_trace.py decodes them).  enable toggles recording; out

@@ -114,6 +114,9 @@ SIGNATURES = [
     ("rocp_stream_time_gather", C.c_int, [_vp, C.c_int]),
     ("rocp_stream_gather_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
     ("rocp_stream_chain_times", C.c_int, [_vp, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
+    ("rocp_stream_last_gather_sms", C.c_int, [_vp, C.POINTER(C.c_int)]),
+    ("rocp_stream_gather_window", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32,
+                                            C.c_int, C.POINTER(C.c_float)]),
     ("rocp_stream_window_bytes", C.c_int, [_vp, _i64p, _i64p]),
     ("rocp_stream_chain_trace", C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int64, _i64p]),
 ]
@@ -702,6 +705,20 @@ class RocpStream:
         cnt = C.c_int(0)
         self.dev.check(lib().rocp_stream_gather_times(self.h, buf, max_n, C.byref(cnt)))
         return [float(buf[k]) for k in range(min(cnt.value, max_n))]
+
+    @property
+    def last_gather_sms(self):
+        v = C.c_int(0)
+        self.dev.check(lib().rocp_stream_last_gather_sms(self.h, C.byref(v)))
+        return int(v.value)
+
+    def gather_window(self, x, t0, batch, nb, seed, first_batch_id, sms=0):
+        """Profiling aid: the window gather of consume_range(...) alone on `sms` SMs
+        (0 = all), event-timed; returns milliseconds (rocp_stream_gather_window)."""
+        ms = C.c_float(0)
+        self.dev.check(lib().rocp_stream_gather_window(self.h, x.h, t0, batch, nb, seed, first_batch_id, int(sms),
+                                                       C.byref(ms)))
+        return float(ms.value)
 
     def chain_times(self, max_n=4096):
         buf = (C.c_float * max_n)()

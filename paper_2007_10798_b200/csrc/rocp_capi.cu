@@ -868,8 +868,14 @@ bool make_gather_view(const double* x, const std::vector<int64_t>& wd, int mode,
     const cuuint32_t L = cuuint32_t(std::min<int64_t>(kGWBox, fibre_len));
     const cuuint32_t box[4] = {mode == 1 ? L : 2u, 1, mode == 1 ? 1u : L, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
+    static const CUtensorMapL2promotion promo = [] {
+        const char* e = std::getenv("ROCP_GATHER_PROMO");  // A/B aid: 0 none, 1 64 B (default), 2 128 B
+        const int v = e ? std::atoi(e) : 1;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                      : (v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_64B);
+    }();
     if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, gstr, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, mode == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : promo,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     *view = GatherView{I1, Ma, In, mode == 1 ? 1 : 0};
@@ -2275,6 +2281,49 @@ rocp_status rocp_stream_time_gather(rocp_stream* st, int enable) {
         st->gather_events_used = 0;
         st->chain_events_used = 0;
     });
+}
+
+rocp_status rocp_stream_gather_window(rocp_stream* st, const rocp_tensor* x, int64_t t0, int64_t batch, int64_t nb,
+                                      uint64_t seed, uint32_t first_batch_id, int sms, float* ms) {
+    return guarded(st->dev, [&] {
+        check_head_dims(st, x);
+        if (st->sharded) throw_domain("gather_window: single-GPU streams only");
+        if (batch < 1 || nb < 1 || t0 < 0 || t0 + batch * nb > x->dims.back())
+            throw_domain("gather_window: slab range out of bounds");
+        rocp_dev* dev = st->dev;
+        if (sms <= 0 || sms > dev->num_sms) sms = dev->num_sms;
+        gather_sms(st, batch);  // gather stream + kernel attributes
+        prepare_window(st, x->d, t0, x->numel / x->dims.back(), batch, nb, nullptr, nullptr, -1);
+        const JobList& L = st->win.jobs;
+        k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
+        after_launch(dev, "k_set_u64");
+        k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
+        after_launch(dev, "k_set_u32");
+        CK(cudaMemsetAsync(L.done.p, 0, size_t(L.ngather) * sizeof(unsigned), dev->stream));
+        launch_draw(dev, L);
+        if (L.nsort > 0) {
+            k_sort_by_base<<<L.nsort, 1024, 0, dev->stream>>>(L.sort.p);
+            after_launch(dev, "k_sort_by_base");
+        }
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, dev->stream));
+        k_gather_warps<<<sms, kGWThreads, kGWSmem, dev->stream>>>(st->win.gtp, L.gather.p, L.ngather, L.ustart.p,
+                                                                  L.done.p);
+        after_launch(dev, "k_gather_warps");
+        CK(cudaEventRecord(b, dev->stream));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
+rocp_status rocp_stream_last_gather_sms(const rocp_stream* st, int* sms) {
+    if (!st || !sms) return ROCP_E_DOMAIN;
+    *sms = st->win_gsms;
+    return ROCP_OK;
 }
 
 rocp_status rocp_stream_gather_times(rocp_stream* st, float* ms, int max, int* count) {
