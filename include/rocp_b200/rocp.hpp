@@ -84,6 +84,8 @@ public:
     Index size() const { return static_cast<Index>(data_.size()); }
     double* data() { return data_.data(); }
     const double* data() const { return data_.data(); }
+    std::vector<double>& values() { return data_; }
+    const std::vector<double>& values() const { return data_; }
     double operator[](Index flat) const { return data_[static_cast<size_t>(flat)]; }
     double& operator[](Index flat) { return data_[static_cast<size_t>(flat)]; }
 

@@ -1,6 +1,7 @@
 // C++ API tests, written against include/rocp_b200/rocp.hpp the way the
 // reference's doctest suites exercise include/rocp/*.hpp (reference test
 // file:line cited per case).  Runs on the GPU (tests/test_cpp_api.py, -m gpu).
+#include "rocp_b200/bench.hpp"
 #include "rocp_b200/rocp.hpp"
 
 #include <cmath>
@@ -262,11 +263,137 @@ static void test_records() {  // test_tensor_io.cpp-style round trips; rocp.cpp:
     CHECK(eq);
 }
 
+static void test_synthetic() {  // test_bench.cpp:15-91
+    {
+        Rng rng(501);  // no noise level: the exact low-rank signal
+        const SyntheticTensor d = gen_synthetic({5, 6, 7}, 3, std::nullopt, rng);
+        const DenseTensor sig = reconstruct_loops(d.truth, {5, 6, 7});
+        double worst = 0.0;
+        for (Index i = 0; i < d.x.size(); ++i) worst = std::max(worst, std::abs(d.x[i] - sig[i]));
+        CHECK(worst <= 1e-12);
+    }
+    for (double sir : {20.0, 6.0, 40.0}) {  // noise scaled to the requested level exactly
+        Rng rng(503);
+        const SyntheticTensor d = gen_synthetic({8, 9, 10}, 4, sir, rng);
+        const DenseTensor sig = reconstruct_loops(d.truth, {8, 9, 10});
+        double ss = 0.0, nn = 0.0;
+        for (Index i = 0; i < d.x.size(); ++i) {
+            ss += sig[i] * sig[i];
+            nn += (d.x[i] - sig[i]) * (d.x[i] - sig[i]);
+        }
+        CHECK(std::abs(10.0 * std::log10(ss / nn) - sir) <= 1e-6 * sir);
+    }
+    {
+        Rng rng(507);
+        const SyntheticTensor d = gen_synthetic({60, 60, 60, 200}, 5, 20.0, rng);
+        CHECK((d.x.dims() == Dims{60, 60, 60, 200}) && d.truth.rank == 5 && d.x.size() == 60 * 60 * 60 * 200);
+    }
+    Rng rng(509);
+    {
+        const SyntheticTensor d = gen_synthetic({4, 5, 200}, 2, std::nullopt, rng);
+        const StreamSplit sp = split_stream(d.x, 0.2, 1);
+        bool ones = sp.batches.size() == 160;
+        for (const DenseTensor& b : sp.batches) ones = ones && b.dims().back() == 1;
+        CHECK(sp.init.dims().back() == 40 && ones);
+    }
+    {
+        const SyntheticTensor d = gen_synthetic({3, 3, 10}, 2, std::nullopt, rng);
+        const StreamSplit sp = split_stream(d.x, 0.2, 4);
+        CHECK(sp.init.dims().back() == 2 && sp.batches.size() == 2 && sp.batches[0].dims().back() == 4 &&
+              sp.batches[1].dims().back() == 4);
+    }
+    {
+        const SyntheticTensor d = gen_synthetic({4, 3, 11}, 2, 20.0, rng);
+        const StreamSplit sp = split_stream(d.x, 0.3, 2);
+        std::vector<double> joined = sp.init.values();
+        for (const DenseTensor& b : sp.batches) joined.insert(joined.end(), b.values().begin(), b.values().end());
+        CHECK(joined == d.x.values());
+    }
+    {
+        const SyntheticTensor d = gen_synthetic({3, 3, 4}, 1, std::nullopt, rng);
+        CHECK(throws<std::domain_error>([&] { split_stream(d.x, 0.1, 1); }));
+        CHECK(throws<std::domain_error>([&] { split_stream(d.x, 0.0, 1); }));
+        CHECK(throws<std::domain_error>([&] { split_stream(d.x, 0.5, 0); }));
+    }
+}
+
+static void test_bench_harness() {  // test_bench.cpp:114-207
+    {
+        BenchConfig cfg;  // single-trial smoke run
+        cfg.dims = {8, 8, 20};
+        cfg.rank = 2;
+        cfg.trials = 1;
+        cfg.algorithms = {Algorithm::rocp};
+        cfg.seed = 7;
+        const BenchReport r = run_benchmark(cfg);
+        CHECK(r.rows.size() == 1);
+        const TrialResult& row = r.rows.front();
+        CHECK(row.fitness > 0.0 && row.fitness <= 1.0);
+        CHECK(row.updates == 16 && row.update_seconds.size() == 16);
+        CHECK(r.aggregates.size() == 1 && r.aggregates[0].fitness_mean == row.fitness);
+    }
+    {
+        BenchConfig cfg;  // fitness is deterministic for a fixed config
+        cfg.dims = {6, 6, 15};
+        cfg.rank = 2;
+        cfg.trials = 3;
+        cfg.seed = 11;
+        const BenchReport a = run_benchmark(cfg), b = run_benchmark(cfg);
+        bool same = a.rows.size() == b.rows.size() && a.rows.size() == 3;
+        for (size_t i = 0; same && i < a.rows.size(); ++i) same = a.rows[i].fitness == b.rows[i].fitness;
+        CHECK(same);
+        cfg.algorithms = {Algorithm::rocp, Algorithm::batch_hot};  // baselines are not on this path
+        CHECK(throws<std::domain_error>([&] { run_benchmark(cfg); }));
+    }
+    {
+        BenchConfig cfg;  // aggregates are recomputable from the rows
+        cfg.dims = {6, 6, 15};
+        cfg.rank = 2;
+        cfg.trials = 4;
+        cfg.seed = 13;
+        const BenchReport r = run_benchmark(cfg);
+        double mean = 0.0, var = 0.0;
+        for (const TrialResult& t : r.rows) mean += t.fitness;
+        mean /= 4.0;
+        for (const TrialResult& t : r.rows) var += (t.fitness - mean) * (t.fitness - mean);
+        CHECK(std::abs(r.aggregates[0].fitness_mean - mean) <= 1e-12);
+        CHECK(std::abs(r.aggregates[0].fitness_std - std::sqrt(var / 3.0)) <= 1e-12);
+    }
+    {
+        BenchConfig cfg;  // CSV report carries the mean/std block
+        cfg.dims = {6, 6, 12};
+        cfg.rank = 2;
+        cfg.trials = 2;
+        cfg.seed = 17;
+        const BenchReport r = run_benchmark(cfg);
+        std::stringstream csv, upd;
+        write_csv(r, csv);
+        const std::string text = csv.str();
+        CHECK(text.find("trial,algorithm,fitness,init_seconds,stream_seconds,updates,seconds_per_update") !=
+              std::string::npos);
+        CHECK(text.find("\nmean,rocp,") != std::string::npos && text.find("\nstd,rocp,") != std::string::npos);
+        write_updates_csv(r, upd);
+        CHECK(upd.str().find("trial,algorithm,update,seconds") != std::string::npos);
+    }
+    {
+        BenchConfig cfg;  // config errors are rejected
+        cfg.dims = {6, 6, 12};
+        cfg.trials = 0;
+        CHECK(throws<std::domain_error>([&] { run_benchmark(cfg); }));
+        cfg.trials = 1;
+        cfg.algorithms.clear();
+        CHECK(throws<std::domain_error>([&] { run_benchmark(cfg); }));
+    }
+    for (Algorithm a : {Algorithm::rocp, Algorithm::online_full, Algorithm::batch_hot, Algorithm::batch_cold})
+        CHECK(parse_algorithm(algorithm_name(a)) == a);
+    CHECK(!parse_algorithm("onlinecp").has_value());
+}
+
 int main() {
     const std::vector<std::pair<const char*, std::function<void()>>> cases = {
         {"index_map", test_index_map}, {"draws_and_gather", test_draws_and_gather}, {"skr", test_skr},
         {"solve", test_solve},         {"cprand", test_cprand},                     {"stream", test_stream},
-        {"records", test_records}};
+        {"records", test_records},     {"synthetic", test_synthetic},               {"bench_harness", test_bench_harness}};
     for (const auto& [name, fn] : cases) {
         const int before = g_fail;
         try {
