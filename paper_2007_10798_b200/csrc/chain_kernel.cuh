@@ -117,6 +117,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// X_s tiles are read exactly once: bulk copy with an L2 evict-first hint
+__device__ __forceinline__ void tma_load_1d_once(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
@@ -622,7 +632,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
                 }
                 fence_proxy_async();
-                tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+                tma_load_1d_once(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
             }
 
             // the single Gram finisher fetches its Q entries during phase 0 (Q(st) only
@@ -905,7 +915,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (tid == 0) {
                         fence_proxy_async();
                         if (item != first_item)  // later items: X tile now
-                            tma_load_1d(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+                            tma_load_1d_once(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
                         const bool zload = !zreuse || item == first_item;
                         if (zload) tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
                         mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + (zload ? cn * RP * 8 : 0)));

@@ -58,14 +58,18 @@ __host__ __device__ __forceinline__ uint32_t gather_units(const GatherJob& J) {
                   : uint32_t((int64_t(J.I) * J.s + kGWUnit - 1) / kGWUnit);
 }
 
+// tensor elements are read once: evict-first, so the random fibre reads do not push the chain's
+// working set out of L2 (configs[1]: chain 1.64 -> 1.61 ms beside the gather).  An evict-last hint
+// on the X_s stores, for the chain to read them from L2, measured no different (dropped).
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
+                                            uint64_t* bar, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-        "%5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+
 
 // One warp unit, decoded at issue time (lane 0 computes the TMA coordinates).
 struct GWUnit {
@@ -86,6 +90,8 @@ __global__ void __launch_bounds__(kGWThreads, 1) k_gather_warps(const __grid_con
         for (int d = 0; d < kGWDepth; ++d) mbar_init(&bars[wid][d], 1);
     __syncwarp();
     unsigned phase = 0;  // bit d: parity of slot d
+    uint64_t pol_first;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     const uint32_t W = gridDim.x * kGWWarps;
     const uint32_t total = __ldg(ustart + njobs);
     // issue side: decode unit u (job cursor ji only moves forward) and start its box
@@ -119,8 +125,8 @@ __global__ void __launch_bounds__(kGWThreads, 1) k_gather_warps(const __grid_con
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the slot
             mbar_expect_tx(bar, unsigned(J.tlen) * 8u * unsigned(x.tw));
             double* slot = slots + d * kGWBox * 2;
-            if (v.contig) tma_load_4d(slot, &tp.map[m], x.i0, 0, 0, int(qq), bar);
-            else tma_load_4d(slot, &tp.map[m], int(i1 & ~int64_t(1)), int(a), int(c2) + x.i0, int(c3), bar);
+            if (v.contig) tma_load_4d(slot, &tp.map[m], x.i0, 0, 0, int(qq), bar, pol_first);
+            else tma_load_4d(slot, &tp.map[m], int(i1 & ~int64_t(1)), int(a), int(c2) + x.i0, int(c3), bar, pol_first);
         }
         x.par = __shfl_sync(0xffffffffu, x.par, 0);
         return x;

@@ -993,6 +993,23 @@ int gather_sms(rocp_stream* st, int64_t B) {
         const int row_blocks = int(std::ceil(rows_max / (kChainThreads / 32)));
         if (row_blocks < dev->num_sms) g = std::min(g, dev->num_sms - row_blocks);
         g = std::max(g, 8);
+        // contraction items come in rounds over the chain's blocks: within 20% below the estimate,
+        // take the split with the fewest rounds (ties: more gather SMs).  C4: 1000 items per mode
+        // stage take 10 rounds on 111 blocks (G = 33) but 9 on 112 (G = 32).
+        const int64_t npairs = int64_t(st->R) * (st->R + 1) / 2;
+        const int64_t nch = (st->s + kChunk - 1) / kChunk, nsup = (st->s + kSuperSamples - 1) / kSuperSamples;
+        const int gram_blocks = ((npairs + 1) & ~int64_t(1)) * nch <= kGramOneBlock
+                                    ? 1
+                                    : int(std::min<int64_t>(nsup * kGramSplitC, kGramBlocksMax));
+        const int64_t items = ((int64_t(rows_max) + kRowTile - 1) / kRowTile) * nsup;
+        auto rounds = [&](int G) {
+            const int64_t cb = std::max<int64_t>(1, dev->num_sms - G - gram_blocks);
+            return (items + cb - 1) / cb;
+        };
+        int best = g;
+        for (int G = g; G >= std::max(1, int(std::floor(0.8 * g))); --G)
+            if (rounds(G) < rounds(best)) best = G;
+        g = best;
     }
     return std::max(0, std::min(g, dev->num_sms / 2));
 }
