@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256) k_contract(const double* __restrict__ X, 
 // zero solution if max diag <= 0; unpivoted LDL^T; regularize with
 // 1e-12 tr(G) when a pivot is <= 0 or max/min pivot > 1e12; then per row
 // forward (increasing k), diagonal, backward (decreasing k) substitution.
-// Every block factors G redundantly in shared memory and solves its rows.
+// Every block factors G redundantly in shared memory; each warp then solves one row.
 // flags[0] |= 1 if regularized; flags[1] = nonfinite_code if any output is
 // not finite (cprand's NumericalError check, cprand.cpp:42-43).
 template <int MAXR>
@@ -545,49 +545,35 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
     }
     if (blockIdx.x == 0 && tid == 0 && s_reg && flags) atomicOr(flags, 1);
 
-    const int32_t row = blockIdx.x * blockDim.x + tid;
+    // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64).  Per element the
+    // operation sequence is the row-wise one: forward w_j -= L(j,k) w_k (k increasing), the
+    // diagonal, backward w_j -= L(k,j) w_k (k decreasing) -- the chain's row solves use it too.
+    const int lane = tid & 31;
+    const int32_t row = int32_t(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
     if (row >= rows) return;
-    double w[MAXR];
-#pragma unroll
-    for (int j = 0; j < MAXR; ++j) w[j] = (j < R) ? RHS[int64_t(row) * R + j] : 0.0;
-    bool finite = true;
+    const int j0 = lane, j1 = lane + 32;
+    const bool v0 = j0 < R, v1 = MAXR > 32 && j1 < R;
+    double w0 = v0 ? RHS[int64_t(row) * R + j0] : 0.0;
+    double w1 = v1 ? RHS[int64_t(row) * R + j1] : 0.0;
     if (s_mode == 0) {
-#pragma unroll
-        for (int j = 0; j < MAXR; ++j) w[j] = 0.0;
+        w0 = w1 = 0.0;
     } else {
-        // forward: w[j] -= L(j,k) w[k], k increasing (same bits as the row-wise
-        // oracle loop); L(j,k) = A[k][j]
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-            if (k < R) {
-#pragma unroll
-                for (int j = k + 1; j < MAXR; ++j)
-                    if (j < R) w[j] = __fma_rn(-A[k][j], w[k], w[j]);
-            }
+        for (int k = 0; k < R; ++k) {
+            const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+            if (v0 && j0 > k) w0 = __fma_rn(-A[k][j0], wk, w0);
+            if (v1 && j1 > k) w1 = __fma_rn(-A[k][j1], wk, w1);
         }
-#pragma unroll
-        for (int j = 0; j < MAXR; ++j) {
-            if (j < R) {
-                const double dj = D[j];
-                w[j] = (fabs(dj) > 2.2250738585072014e-308) ? w[j] / dj : 0.0;
-            }
-        }
-        // backward: w[j] -= L(k,j) w[k], k decreasing; L(k,j) = A[j][k]
-#pragma unroll
-        for (int k = MAXR - 1; k >= 0; --k) {
-            if (k < R) {
-#pragma unroll
-                for (int j = 0; j < k; ++j) w[j] = __fma_rn(-A[j][k], w[k], w[j]);
-            }
+        if (v0) w0 = (fabs(D[j0]) > 2.2250738585072014e-308) ? w0 / D[j0] : 0.0;
+        if (v1) w1 = (fabs(D[j1]) > 2.2250738585072014e-308) ? w1 / D[j1] : 0.0;
+        for (int k = R - 1; k >= 0; --k) {
+            const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+            if (v0 && j0 < k) w0 = __fma_rn(-A[j0][k], wk, w0);
+            if (v1 && j1 < k) w1 = __fma_rn(-A[j1][k], wk, w1);
         }
     }
-#pragma unroll
-    for (int j = 0; j < MAXR; ++j) {
-        if (j < R) {
-            OUT[int64_t(row) * R + j] = w[j];
-            finite = finite && isfinite(w[j]);
-        }
-    }
+    if (v0) OUT[int64_t(row) * R + j0] = w0;
+    if (v1) OUT[int64_t(row) * R + j1] = w1;
+    const bool finite = (!v0 || isfinite(w0)) && (!v1 || isfinite(w1));
     if (!finite && flags) flags[1] = nonfinite_code;
 }
 

@@ -455,7 +455,7 @@ void set_contract_smem_attrs() {
 // flags: [0] |= 1 when regularized, [1] = nonfinite_code on a non-finite output.
 void launch_solve(rocp_dev* dev, const double* G, int R, const double* RHS, int64_t rows, double* OUT,
                   int* flags, int nonfinite_code) {
-    const int grid = int(std::max<int64_t>(1, (rows + 255) / 256));
+    const int grid = int(std::max<int64_t>(1, (rows + 7) / 8));  // a warp per row
     if (R <= 16) k_solve<16><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     else if (R <= 32) k_solve<32><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     else k_solve<64><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);

@@ -136,7 +136,8 @@ __device__ __forceinline__ void seg_dot8(const double* __restrict__ X, const dou
             const int k1 = min(m1, k0 + kChunk);
 #pragma unroll
             for (int j = 0; j < kSegRG; ++j) pk[j] = 0.0;
-            for (int c = k0; c < k1; ++c) {
+#pragma unroll 4
+            for (int c = k0; c < k1; ++c) {  // unrolled: the next samples' loads overlap this fma chain
                 const double x = __ldg(X + int64_t(c0 + c) * rows + i);
                 const double* z = Z + int64_t(c0 + c) * R + r0;
 #pragma unroll
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(256) k_seg_partials(const SegPartParams p) {
                 for (int k0 = m0; k0 < m1; k0 += kChunk) {
                     const int k1 = min(m1, k0 + kChunk);
                     double pk = 0.0;
+#pragma unroll 4
                     for (int c = k0; c < k1; ++c)
                         pk = __fma_rn(__ldg(p.Z + int64_t(c0 + c) * R + r1), __ldg(p.Z + int64_t(c0 + c) * R + r2), pk);
                     q = (k0 == m0) ? pk : q + pk;
