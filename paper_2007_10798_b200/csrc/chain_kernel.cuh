@@ -57,6 +57,7 @@ struct ChainParams {
     double* resid;            // N x 2 (num, den) of the last batch
     double* rpart;            // 3 x S
     unsigned int* counter;    // [0] Gram arrivals, [1] residual arrivals
+    unsigned int* zctr;       // phase-0 chunk arrivals: [0] all, [1 + m] superchunk m (cumulative, zeroed per launch)
     unsigned long long* trace;  // optional phase timestamps (globaltimer ns), 16 per stage
     // overlapped window gather (k_gather_warps on reserved SMs): per (b*N + stage) units
     // published / needed; nullptr when the window was gathered before the launch
@@ -572,7 +573,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     double* cps = zs + kSuperSamples * RP;
     const int czt = kChunk * RP;  // Z elements of one chunk
 
-    // idx of this thread's phase-0 Z elements (chunk blockIdx.x) of stage (b, st), in
+    // Phase 0 (chunk Z + chunk Gram partial) runs on the blocks at the TOP of the contraction
+    // range (chunk ch -> block cblocks-1-ch), which have no contraction item when items do not
+    // fill the grid (configs[1]: 96 items, 19 chunks).  There is no grid barrier after phase 0:
+    // each chunk publishes itself (p.zctr), a contraction block waits only for the 8 chunks of
+    // its superchunk before its Z bulk copy, the Gram finisher for all of them.
+    const int ch_first = (int(blockIdx.x) < cblocks) ? cblocks - 1 - int(blockIdx.x) : nch;
+    const bool zreuse = kWide && cblocks >= nsuper;
+    const int zm = cix % nsuper, zrank = cix / nsuper, zcnt = (cblocks - zm + nsuper - 1) / nsuper;
+    auto first_item_of = [&](int tiles) {
+        const int n_contract = tiles * nsuper;
+        return is_gram_block ? n_contract : (zreuse ? ((zrank < tiles) ? zm * tiles + zrank : n_contract) : cix);
+    };
+    // idx of this thread's phase-0 Z elements (chunk ch_first) of stage (b, st), in
     // registers; loaded one phase ahead so the phase-0 critical path is a single L2 gather.
     int32_t nidx[kZU][kMaxOrder - 1];
     auto load_idx = [&](int b, int st) {
@@ -581,8 +594,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
 #pragma unroll
         for (int u = 0; u < kZU; ++u) {
             const int e = tid + u * blockDim.x;
-            const int c = int(blockIdx.x) * kChunk + e / RP;
-            const bool ok = int(blockIdx.x) < nch && e < czt && c < S;
+            const int c = ch_first * kChunk + e / RP;
+            const bool ok = ch_first < nch && e < czt && c < S;
 #pragma unroll
             for (int l = 0; l < kMaxOrder - 1; ++l)
                 nidx[u][l] = (ok && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
@@ -620,10 +633,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // item schedule: (tile, superchunk) pairs; the wide kernel gives each block one
             // superchunk (its Z tile, up to 128 KB, is loaded once per stage), the narrow one
             // strides over all items
-            const bool zreuse = kWide && cblocks >= nsuper;
-            const int zm = cix % nsuper, zrank = cix / nsuper, zcnt = (cblocks - zm + nsuper - 1) / nsuper;
-            const int first_item = zreuse ? ((zrank < tiles) ? zm * tiles + zrank : n_contract) : cix;
-            const bool contract_block = !is_gram_block && first_item < n_contract;
+            const int first_item = first_item_of(tiles);
+            const bool contract_block = first_item < n_contract;
             if (contract_block && tid == 0) {
                 const int tile = first_item % tiles, m = first_item / tiles;
                 const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
@@ -654,11 +665,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // (sampling.cpp:90-103: 1.0 * F_0 * F_1 * ... left to right), then the chunk's
             // Gram partial from shared memory: fma chain over its samples from +0.0
             // (k_gram's per-chunk sequence), lower pairs mirrored.
-            for (int ch = blockIdx.x; ch < nch; ch += G) {
+            for (int ch = ch_first; ch < nch; ch += cblocks) {
                 const int c0 = ch * kChunk, cn = min(kChunk, S - c0);
-                double* zc = zs;  // [32][RP]; the contraction Z tile is not loaded before phase 1
+                double* zc = zs;  // [32][RP]; scratch, before this block's contraction Z
                 const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
-                if (ch == int(blockIdx.x)) {
+                if (ch == ch_first) {
                     double f[kZU][kMaxOrder - 1];
 #pragma unroll
                     for (int u = 0; u < kZU; ++u) {
@@ -686,7 +697,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         }
                     }
                 }
-                const int e0 = (ch == int(blockIdx.x)) ? kZU * int(blockDim.x) : 0;
+                const int e0 = (ch == ch_first) ? kZU * int(blockDim.x) : 0;
                 for (int e = e0 + tid; e < czt; e += blockDim.x) {  // rare: RP > 32 or extra chunks
                     const int cc = e / RP, r = e - cc * RP;
                     double z = 0.0;
@@ -701,7 +712,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (cc < cn) Z[int64_t(c0) * RP + e] = z;
                 }
                 __syncthreads();
-                if (tr) trace_stamp(tr, 14, blockIdx.x == 0 && tid == 0 && ch == 0);
+                if (tr) trace_stamp(tr, 14, tid == 0 && ch == 0);
                 for (int q = tid; q < npairs; q += blockDim.x) {
                     const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
                     double acc = 0.0;
@@ -714,14 +725,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     p.chpart[int64_t(ch) * NPp + q] = acc;  // lower pair q; (j, i) is the same value
                 }
                 __syncthreads();
-                if (tr) trace_stamp(tr, 15, blockIdx.x == 0 && tid == 0 && ch == 0);
+                if (tr) trace_stamp(tr, 15, tid == 0 && ch == 0);
+                if (tid == 0) {  // the chunk's Z rows and Gram partial are in (bar.sync above)
+                    __threadfence();
+                    atomicAdd(p.zctr + 1 + ch / kSuper, 1u);
+                    atomicAdd(p.zctr, 1u);
+                }
             }
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // Z is read by TMA in phase 1
-            grid.sync();
             if (tr) trace_stamp(tr, 1, blockIdx.x == 0 && tid == 0);
 
             // ---------------- phase 1
             if (is_gram_block) {
+                if (tid == 0) {  // every chunk partial of this stage published
+                    wait_gathered(p.zctr, unsigned(b * N + st + 1) * unsigned(nch), 0u);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
+                }
+                __syncthreads();
                 // superchunk sums of the chunk partials, superchunk m = chunks 8m..8m+7 in order
                 auto super_sum = [&](int m, int pp) {
                     const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
@@ -907,6 +926,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
                 }
             } else {
+                int zm_cur = -1;
                 for (int item = first_item; item < n_contract;
                      item = zreuse ? ((item % tiles) + zcnt < tiles ? item + zcnt : n_contract) : item + cblocks) {
                     const int tile = item % tiles, m = item / tiles;
@@ -916,10 +936,16 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         fence_proxy_async();
                         if (item != first_item)  // later items: X tile now
                             tma_load_1d_once(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
-                        const bool zload = !zreuse || item == first_item;
-                        if (zload) tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        const bool zload = m != zm_cur;
+                        if (zload) {  // superchunk m's chunks of Z published (no grid barrier after phase 0)
+                            const unsigned nck = unsigned(min(kSuper, nch - m * kSuper));
+                            wait_gathered(p.zctr + 1 + m, unsigned(b * N + st + 1) * nck, 0u);
+                            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
+                            tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        }
                         mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + (zload ? cn * RP * 8 : 0)));
                     }
+                    zm_cur = m;
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
                     if (tr) trace_stamp(tr, 8, blockIdx.x == 0 && tid == 0 && item == 0);

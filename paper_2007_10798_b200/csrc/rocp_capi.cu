@@ -726,6 +726,7 @@ struct rocp_stream {
     DBuf<int> flags;              // [0] temporal regularized (stream flag), [2] last mode solve
     DBuf<double> gpart, chpart, LD, rpart, zmodes;  // persistent-chain scratch
     DBuf<int> mode_flag;
+    DBuf<unsigned> zctr;               // persistent chain: phase-0 chunk arrival counters
     bool trace_on = false;             // chain phase timestamps (profiling aid)
     DBuf<unsigned long long> trace;
     int64_t trace_n = 0;
@@ -1203,6 +1204,10 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
     p.resid = st->resid.p;
     p.rpart = st->rpart.p;
     p.counter = st->dev->counters.p + 4;
+    // phase-0 chunk arrivals (total, per superchunk), cumulative over the launch's stages
+    if (st->zctr.n < size_t(p.nsuper + 1)) st->zctr.alloc(size_t(p.nsuper + 1));
+    CK(cudaMemsetAsync(st->zctr.p, 0, size_t(p.nsuper + 1) * sizeof(unsigned), st->dev->stream));
+    p.zctr = st->zctr.p;
     int grid = st->dev->num_sms;
     if (overlap) {
         if (b0 != 0) throw RocpError{ROCP_E_STATE, "overlapped gather needs the whole window (internal)"};
