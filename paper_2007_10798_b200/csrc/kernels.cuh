@@ -467,6 +467,82 @@ __global__ void __launch_bounds__(256) k_contract(const double* __restrict__ X, 
     }
 }
 
+// Contraction for R <= 32 (primitives, cprand sweeps, the sharded stream's owned
+// mode): same canonical order as k_contract, but warp w of a 256-thread block
+// forms chunk w of the (32-row tile, superchunk) item -- lane = row, RPAD
+// register accumulators -- and the 8 chunk partials are summed left to right
+// through shared memory.  k_contract used 32 * ceil(R/10) threads per item,
+// each walking all 256 samples (configs[1]: 40 us per mode-1 contraction).
+template <int RPAD>
+__global__ void __launch_bounds__(256) k_contract_chunks(const double* __restrict__ X, int32_t I, int32_t S,
+                                                         const double* __restrict__ Z, int R,
+                                                         const double* base, double* out,
+                                                         double* __restrict__ partial,
+                                                         unsigned int* __restrict__ counters, int tiled) {
+    extern __shared__ double sm[];
+    double* xs = sm;                                 // [256][32]
+    double* zs = sm + kSuperSamples * kRowTile;      // [256][RPAD]
+    double* cps = zs + kSuperSamples * RPAD;         // [8][RPAD][32]
+    const int tile = blockIdx.x, m = blockIdx.y, nsuper = gridDim.y;
+    const int i0 = tile * kRowTile;
+    const int c0 = m * kSuperSamples;
+    const int cn = min(kSuperSamples, S - c0);
+    const int rows = min(kRowTile, I - i0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < kRowTile * cn; e += blockDim.x) {
+        const int c = e >> 5, r = e & 31;
+        if (r < rows) cp_async8(xs + e, X + (tiled ? xs_offset(i0 + r, c0 + c, S) : int64_t(c0 + c) * I + i0 + r));
+        else xs[e] = 0.0;
+    }
+    for (int e = tid; e < cn * RPAD; e += blockDim.x) {
+        const int c = e / RPAD, r = e - c * RPAD;
+        if (r < R) cp_async8(zs + e, Z + int64_t(c0 + c) * R + r);
+        else zs[e] = 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int nk = (cn + kChunk - 1) / kChunk;
+    if (warp < nk) {  // chunk `warp`: fma chain from +0.0 over its samples, increasing order
+        const int cc0 = warp * kChunk, ccn = min(kChunk, cn - cc0);
+        double acc[RPAD];
+#pragma unroll
+        for (int r = 0; r < RPAD; ++r) acc[r] = 0.0;
+        for (int cc = 0; cc < ccn; ++cc) {
+            const double x = xs[(cc0 + cc) * kRowTile + lane];
+            const double2* zr = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RPAD);
+#pragma unroll
+            for (int q = 0; q < RPAD / 2; ++q) {
+                const double2 zz = zr[q];
+                acc[2 * q] = __fma_rn(x, zz.x, acc[2 * q]);
+                acc[2 * q + 1] = __fma_rn(x, zz.y, acc[2 * q + 1]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RPAD; ++r) cps[(warp * RPAD + r) * kRowTile + lane] = acc[r];
+    }
+    __syncthreads();
+    const bool split = nsuper > 1;
+    for (int e = tid; e < RPAD * kRowTile; e += blockDim.x) {
+        const int r = e >> 5, l = e & 31;
+        if (r >= R || l >= rows) continue;
+        double q = cps[r * kRowTile + l];  // superchunk partial: chunk partials left to right
+        for (int k = 1; k < nk; ++k) q = q + cps[(k * RPAD + r) * kRowTile + l];
+        const int64_t o = int64_t(i0 + l) * R + r;
+        if (split) partial[int64_t(m) * I * R + o] = q;
+        else out[o] = base ? base[o] + q : q;
+    }
+    if (!split) return;
+    if (!last_arrive_of(counters + tile, unsigned(nsuper))) return;
+    for (int e = tid; e < RPAD * kRowTile; e += blockDim.x) {
+        const int r = e >> 5, l = e & 31;
+        if (r >= R || l >= rows) continue;
+        const int64_t o = int64_t(i0 + l) * R + r;
+        double tot = __ldcg(partial + o);
+        for (int mm = 1; mm < nsuper; ++mm) tot = tot + __ldcg(partial + int64_t(mm) * I * R + o);
+        out[o] = base ? base[o] + tot : tot;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K5: solve_gram (solve.cpp:9-35), canonical form:
 // zero solution if max diag <= 0; unpivoted LDL^T; regularize with

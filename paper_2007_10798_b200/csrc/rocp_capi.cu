@@ -420,8 +420,26 @@ void reserve_contract(rocp_dev* dev, int64_t I, int64_t s, int R, bool always = 
     }
 }
 
+template <int RPAD>
+void launch_contract_chunks(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
+                            const double* base, double* out, int tiled) {
+    const int tiles = int((I + kRowTile - 1) / kRowTile);
+    const int nsuper = int((s + kSuperSamples - 1) / kSuperSamples);
+    if (nsuper > 1 && (dev->contract_partial.n < size_t(nsuper) * I * R || dev->tile_counters.n < size_t(tiles)))
+        throw RocpError{ROCP_E_STATE, "contraction scratch not reserved (internal)"};
+    const size_t smem = (size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * RPAD + size_t(8) * RPAD * kRowTile) *
+                        sizeof(double);
+    k_contract_chunks<RPAD><<<dim3(unsigned(tiles), unsigned(nsuper), 1u), 256, smem, dev->stream>>>(
+        X, int32_t(I), int32_t(s), Z, R, base, out, dev->contract_partial.p, dev->tile_counters.p, tiled);
+    after_launch(dev, "k_contract_chunks");
+}
+
 void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const double* Z, int R,
                      const double* base, double* out, int tiled = 0) {
+    if (R <= 8) return launch_contract_chunks<8>(dev, X, I, s, Z, R, base, out, tiled);
+    if (R <= 16) return launch_contract_chunks<16>(dev, X, I, s, Z, R, base, out, tiled);
+    if (R <= 24) return launch_contract_chunks<24>(dev, X, I, s, Z, R, base, out, tiled);
+    if (R <= 32) return launch_contract_chunks<32>(dev, X, I, s, Z, R, base, out, tiled);
     int rb;
     const int ng = contract_groups(R, &rb);
     switch (rb) {
@@ -439,6 +457,17 @@ void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const
 }
 
 void set_contract_smem_attrs() {
+    {
+        auto attr = [](const void* f, int rpad) {
+            const int b = int((size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * rpad + size_t(8) * rpad * kRowTile) *
+                              sizeof(double));
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        };
+        attr(reinterpret_cast<const void*>(k_contract_chunks<8>), 8);
+        attr(reinterpret_cast<const void*>(k_contract_chunks<16>), 16);
+        attr(reinterpret_cast<const void*>(k_contract_chunks<24>), 24);
+        attr(reinterpret_cast<const void*>(k_contract_chunks<32>), 32);
+    }
     const int mx = int((size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * 70) * sizeof(double));
     CK(cudaFuncSetAttribute(k_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CK(cudaFuncSetAttribute(k_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
