@@ -18,7 +18,9 @@ Reported (one JSON line on rank 0):
            sampled fibres to the device and reads the model back
   roofline the window gather kernel (sampled-fibre gather, north-star item 1):
            algorithmic sector bytes per launch / its average
-           CUDA-event launch time in the timed region, vs MEASURED_PEAKS.json
+           CUDA-event launch time in the timed region, vs MEASURED_PEAKS.json.
+           In a step it runs overlapped on a few SMs beside the chain (`sms`);
+           `standalone` is the same launch on every SM, timed after the region
   cpu_baseline  the CPU oracle port (single thread) on a bounded sample of the
            same stream
 --impl reference times the CPU port of the reference path on all host threads.

@@ -72,3 +72,26 @@ def test_gather_sms_bounds(gdev):
     with pytest.raises(rocp.DomainError):
         gdev.set_gather_sms(10_000)
     gdev.set_gather_sms(-1)
+
+
+def test_gather_window_profiling_entry(gdev):
+    """rocp_stream_gather_window (bench.py's whole-device gather roofline) only fills the window
+    scratch: the stream's model is untouched and a following window is still bit-identical."""
+    dims, R, t_init, B = [64, 200, 100], 5, 30, 10
+    x, X, a, b, s, nb = _run_pair(gdev, dims, R, 20.0, t_init, B)
+    a.checkpoint()
+    before = [a.factor(n) for n in (1, 2)] + [a.temporal()]
+    for sms in (0, 8):
+        ms = a.gather_window(X, t_init, B, nb, 77, 1, sms)
+        assert ms > 0.0
+    assert all(bitwise(u, v) for u, v in zip(before, [a.factor(n) for n in (1, 2)] + [a.temporal()]))
+    gdev.set_gather_sms(8)
+    a.consume_range(X, t_init, B, nb, 4243, 1)
+    assert a.last_gather_sms == 8
+    for k in range(nb):
+        b.consume(H.slab(x, dims, t_init + k * B, B), B, 4243, k + 1)
+    _cmp_stream(a, b, len(dims))
+    gdev.set_gather_sms(0)
+    a.restore()
+    a.consume_range(X, t_init, B, nb, 4243, 1)
+    assert a.last_gather_sms == 0
