@@ -152,8 +152,12 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # one GPU per rank; more ranks than GPUs only in the functional check below (replicas share)
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # ROCP_BENCH_BACKEND=gloo: exercise the multi-rank plumbing (barrier, max over ranks)
+        # where NCCL cannot run, e.g. two replica ranks sharing one GPU in a functional check
+        dist.init_process_group(os.environ.get("ROCP_BENCH_BACKEND", "nccl"))
         return world, rank, local, dist, torch
     return world, rank, local, None, None
 
@@ -161,7 +165,7 @@ def dist_setup():
 def max_over_ranks(v, dist, torch):
     if dist is None:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -72,13 +72,14 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
 }
 // Waits until the overlapped gather published every unit of one (batch, stage)
 // (seen = a value loaded earlier, usually during the previous phase).  A gather
-// that never arrives traps after ~4 s instead of hanging the device.
+// that never arrives traps after ~20 s instead of hanging the device (long enough
+// for time-slicing with other GPU contexts).
 __device__ __noinline__ void wait_gathered(const unsigned* done, unsigned need, unsigned seen) {
     if (seen >= need) return;
     const unsigned long long t0 = gtimer_raw();
     while (ld_acquire_u32(done) < need) {
         __nanosleep(128);
-        if (gtimer_raw() - t0 > 4000000000ull) __trap();
+        if (gtimer_raw() - t0 > 20000000000ull) __trap();
     }
 }
 
