@@ -1044,35 +1044,53 @@ struct WinResidParams {
     double* cols;            // nb x 3 x S
     double* out;             // nb x 2 (num, den)
     double* last_out;        // 2: the last batch's (num, den)
+    unsigned int* rctr;      // nb arrival counters (self-resetting)
+    int stage_u;             // B x R temporal rows fit in shared memory
 };
 
-__global__ void __launch_bounds__(256) k_win_resid_cols(const WinResidParams p) {
+// One launch for the window: block (x, b) forms the column partials of 8
+// columns of batch b (warp per column, lanes over the B rows, the batch's
+// temporal rows staged in shared memory when they fit), and the last block of
+// batch b to finish (last_arrive_of on rctr[b]) reduces them in the canonical
+// hsum order.  Before, the columns read u row by row from L2 inside a runtime-R
+// loop (one load pair per fma) and the hsum was a second launch: 36 us per
+// configs[1] step, now a few.
+__global__ void __launch_bounds__(256) k_win_resid(const WinResidParams p) {
+    extern __shared__ double us[];  // [8][R] z rows of the block's columns, then B x R temporal rows (stage_u)
     const int b = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * 8 + warp;
-    if (c >= p.S) return;
+    double* zs = us;
+    for (int e = threadIdx.x; e < 8 * p.R; e += blockDim.x) {
+        const int w = e / p.R, r = e - w * p.R, cw = blockIdx.x * 8 + w;
+        zs[e] = (cw < p.S) ? __ldcg(p.zT + (int64_t(b) * p.S + cw) * p.RP + r) : 0.0;
+    }
     const double* u = p.temporal + (p.t_len0 + int64_t(b) * p.B) * p.R;
-    const double* X = p.X_base + p.xoff[b * p.N];
-    const double* z = p.zT + (int64_t(b) * p.S + c) * p.RP;
-    double qn = 0.0, qd = 0.0;
-    for (int i = lane; i < p.B; i += 32) {
-        double uz = 0.0;
-        for (int r = 0; r < p.R; ++r) uz = __fma_rn(u[int64_t(i) * p.R + r], z[r], uz);
-        const double xv = X[xs_offset(i, c, p.S)];
-        const double e = xv - uz;
-        qn = __fma_rn(e, e, qn);
-        qd = __fma_rn(xv, xv, qd);
+    if (p.stage_u) {
+        for (int e = threadIdx.x; e < p.B * p.R; e += blockDim.x) us[8 * p.R + e] = __ldcg(u + e);
+        u = us + 8 * p.R;
     }
-    qn = butterfly32(qn);
-    qd = butterfly32(qd);
-    if (lane == 0) {
-        p.cols[(int64_t(b) * 3 + 0) * p.S + c] = qn;
-        p.cols[(int64_t(b) * 3 + 1) * p.S + c] = qd;
+    __syncthreads();
+    if (c < p.S) {
+        const double* X = p.X_base + p.xoff[b * p.N];
+        const double* z = zs + warp * p.R;
+        double qn = 0.0, qd = 0.0;
+        for (int i = lane; i < p.B; i += 32) {
+            const double xv = __ldcg(X + xs_offset(i, c, p.S));
+            double uz = 0.0;
+            for (int r = 0; r < p.R; ++r) uz = __fma_rn(u[int64_t(i) * p.R + r], z[r], uz);
+            const double e = xv - uz;
+            qn = __fma_rn(e, e, qn);
+            qd = __fma_rn(xv, xv, qd);
+        }
+        qn = butterfly32(qn);
+        qd = butterfly32(qd);
+        if (lane == 0) {
+            p.cols[(int64_t(b) * 3 + 0) * p.S + c] = qn;
+            p.cols[(int64_t(b) * 3 + 1) * p.S + c] = qd;
+        }
     }
-}
-
-__global__ void __launch_bounds__(256) k_win_resid_sum(const WinResidParams p) {
-    const int b = blockIdx.x;
+    if (!last_arrive_of(p.rctr + b, gridDim.x)) return;
     double* base = p.cols + int64_t(b) * 3 * p.S;
     block_hsum_inplace(base, p.S, base + 2 * p.S);
     block_hsum_inplace(base + p.S, p.S, base + 2 * p.S);

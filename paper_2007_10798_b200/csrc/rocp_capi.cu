@@ -687,6 +687,7 @@ struct Window {
     std::vector<int64_t> xoff;
     DBuf<int64_t> xoff_dev;
     DBuf<double> zT, rcols, rhist;  // temporal Z per batch, residual column partials, per-batch residuals
+    DBuf<unsigned> rctr;            // residual pass: per-batch block arrivals (self-resetting)
     JobList jobs;
     // host-slab path: pinned staging of the gathered X_s and of the fibre base offsets
     double* hX = nullptr;
@@ -1288,11 +1289,18 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
         w.cols = st->win.rcols.p;
         w.out = st->win.rhist.p;
         w.last_out = st->resid.p;
+        if (st->win.rctr.n < size_t(nb)) {  // zero once; last_arrive_of resets each counter after use
+            CK(cudaStreamSynchronize(st->dev->stream));
+            st->win.rctr.alloc(size_t(std::max<int64_t>(nb, st->win.nb)));
+            CK(cudaMemset(st->win.rctr.p, 0, st->win.rctr.n * sizeof(unsigned)));
+        }
+        w.rctr = st->win.rctr.p;
+        const size_t zbytes = size_t(8) * size_t(st->R) * sizeof(double);
+        const size_t ubytes = size_t(B) * size_t(st->R) * sizeof(double);
+        w.stage_u = zbytes + ubytes <= 48 * 1024 ? 1 : 0;
         const dim3 g1{unsigned((st->s + 7) / 8), unsigned(nb), 1u};
-        k_win_resid_cols<<<g1, 256, 0, st->dev->stream>>>(w);
-        after_launch(st->dev, "k_win_resid_cols");
-        k_win_resid_sum<<<unsigned(nb), 256, 0, st->dev->stream>>>(w);
-        after_launch(st->dev, "k_win_resid_sum");
+        k_win_resid<<<g1, 256, zbytes + (w.stage_u ? ubytes : 0), st->dev->stream>>>(w);
+        after_launch(st->dev, "k_win_resid");
     }
 }
 
