@@ -79,7 +79,11 @@ __device__ __noinline__ void wait_gathered(const unsigned* done, unsigned need, 
     const unsigned long long t0 = gtimer_raw();
     while (ld_acquire_u32(done) < need) {
         __nanosleep(128);
-        if (gtimer_raw() - t0 > 20000000000ull) __trap();
+        if (gtimer_raw() - t0 > 20000000000ull) {
+            printf("rocp: arrival wait timed out (counter %p at %u of %u, block %d)\n", (const void*)done,
+                   ld_acquire_u32(done), need, int(blockIdx.x));
+            __trap();
+        }
     }
 }
 

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
+#include <cstdio>
 
 namespace rocpk {
 

@@ -1010,6 +1010,15 @@ int gather_sms(rocp_stream* st, int64_t B) {
             if (const char* e = std::getenv("ROCP_GATHER_SMS")) dev->gather_sms = std::max(0, std::atoi(e));
         }
         CK(cudaFuncSetAttribute(k_gather_warps, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGWSmem)));
+        // The overlapped gather and the chain wait on each other's arrivals.  With lazy module
+        // loading (CUDA 12's default) a kernel's first launch loads its code, which can wait for
+        // the device while the other kernel spins: load every kernel of the pair up front.
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, k_chain<false, false>));
+        CK(cudaFuncGetAttributes(&fa, k_chain<true, false>));
+        CK(cudaFuncGetAttributes(&fa, k_chain<false, true>));
+        CK(cudaFuncGetAttributes(&fa, k_chain<true, true>));
+        CK(cudaFuncGetAttributes(&fa, k_gather_warps));
         CK(cudaStreamCreateWithFlags(&dev->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&dev->ev_gready, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&dev->ev_gdone, cudaEventDisableTiming));
