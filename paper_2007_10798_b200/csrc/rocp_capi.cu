@@ -2378,18 +2378,21 @@ rocp_status rocp_stream_gather_window(rocp_stream* st, const rocp_tensor* x, int
             k_sort_by_base<<<L.nsort, 1024, 0, dev->stream>>>(L.sort.p);
             after_launch(dev, "k_sort_by_base");
         }
-        cudaEvent_t a, b;
-        CK(cudaEventCreate(&a));
-        CK(cudaEventCreate(&b));
-        CK(cudaEventRecord(a, dev->stream));
+        struct Ev {  // destroyed on every exit path
+            cudaEvent_t e = nullptr;
+            ~Ev() {
+                if (e) cudaEventDestroy(e);
+            }
+        } a, b;
+        CK(cudaEventCreate(&a.e));
+        CK(cudaEventCreate(&b.e));
+        CK(cudaEventRecord(a.e, dev->stream));
         k_gather_warps<<<sms, kGWThreads, kGWSmem, dev->stream>>>(st->win.gtp, L.gather.p, L.ngather, L.ustart.p,
                                                                   L.done.p);
         after_launch(dev, "k_gather_warps");
-        CK(cudaEventRecord(b, dev->stream));
-        CK(cudaEventSynchronize(b));
-        CK(cudaEventElapsedTime(ms, a, b));
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
+        CK(cudaEventRecord(b.e, dev->stream));
+        CK(cudaEventSynchronize(b.e));
+        CK(cudaEventElapsedTime(ms, a.e, b.e));
     });
 }
 
