@@ -870,9 +870,11 @@ double* win_x(rocp_stream* st, int64_t b, int stage) { return st->win.X.p + st->
 // Tensor-map view for the TMA units of the overlapped gather (gather_kernel.cuh):
 // the window range x (dims wd, time extent = the window's slices) seen as
 // (I1, Ma, In, Mb) for strided mode `mode`, box {2, 1, L, 1} with L = min(256,
-// fibre length); mode 1 as (I1, 1, 1, rest) with box {L, 1, 1, 1}.  Returns false where TMA cannot express it (odd I1: row
-// strides must be 16-byte multiples; a misaligned range; extents past 2^31) or
-// ROCP_GATHER_TMA=0; those jobs use LSU loads.
+// fibre length); mode 1 as (I1, 1, 1, rest) with box {L, 1, 1, 1}.  Returns
+// false where TMA cannot express it (odd I1: row strides must be 16-byte
+// multiples; a misaligned range; extents past 2^31) or ROCP_GATHER_TMA=0; those
+// jobs use LSU loads.  ROCP_GATHER_PROMO selects the strided boxes' L2
+// promotion for A/B runs.
 bool make_gather_view(const double* x, const std::vector<int64_t>& wd, int mode, int64_t fibre_len, CUtensorMap* map,
                       GatherView* view) {
     static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
@@ -906,9 +908,10 @@ bool make_gather_view(const double* x, const std::vector<int64_t>& wd, int mode,
         return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                       : (v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_64B);
     }();
+    const CUtensorMapL2promotion l2 = mode == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : promo;  // mode 1: whole lines
     if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, gstr, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, mode == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : promo,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
         return false;
     *view = GatherView{I1, Ma, In, mode == 1 ? 1 : 0};
     return true;
