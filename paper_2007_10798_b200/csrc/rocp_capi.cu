@@ -1001,8 +1001,9 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
 // overrides; otherwise a model picks the fewest SMs whose TMA gather (about
 // 1.47 G elements/s per SM, measured) keeps pace with the chain (about 14 us
 // per stage for R <= 32, 110 us for the wide kernel), and 0 -- the whole window
-// gathered on every SM before the chain -- when the gather would be under a
-// tenth of the step (then the SMs are worth more to the chain: C1, C3, C5).
+// gathered on every SM before the chain -- when the model puts the gather under
+// 2.5% of the step (C1 and C5 lose 1% or tie beside 8 gather SMs; C3, at 2.6%
+// by the model and 6% measured, gains 4% with 8).
 // The chain keeps one warp per row of its largest stage where that fits on
 // the device (a second row-solve round costs more than the gather saves).
 int gather_sms(rocp_stream* st, int64_t B) {
@@ -1036,7 +1037,7 @@ int gather_sms(rocp_stream* st, int64_t B) {
         elems *= double(st->s);
         const double t_chain = st->N * (st->R > 32 ? 110.0 : 14.0);     // us per batch
         const double t_full = elems / (93e3);                             // us, whole-device gather
-        if (t_full < 0.1 * (t_full + t_chain)) return 0;
+        if (t_full < 0.025 * (t_full + t_chain)) return 0;
         g = int(std::ceil(elems / (1470.0 * t_chain)));
         const int row_blocks = int(std::ceil(rows_max / (kChainThreads / 32)));
         if (row_blocks < dev->num_sms) g = std::min(g, dev->num_sms - row_blocks);
