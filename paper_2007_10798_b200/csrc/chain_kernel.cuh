@@ -513,6 +513,73 @@ __device__ __noinline__ void chain_contract_blocked(const double* xs, const doub
     }
 }
 
+// The wide contraction item on the fp64 tensor cores: warp w forms chunk w of
+// the (32-row tile, superchunk) item with mma.sync m8n8k4 -- 4 row tiles x
+// NT = RP/8 column tiles of 8x8 accumulators, 4 samples per step.  On B200 the
+// fp64 MMA rounds exactly like the sequential fma chain in increasing k
+// (tools/dmma_order.cu: 4.2M of 4.2M outputs bitwise equal), so each chunk
+// partial is bit-identical to chain_contract_blocked's; samples past the chunk
+// end enter as 0 x 0, which leaves an accumulator that started at +0.0
+// unchanged.  Per 4 samples: 4 + NT shared loads and 4 NT MMAs, against 36
+// loads and 16 NT fmas (x4) in the blocked loop.  The chunk partials are then
+// summed left to right exactly as in chain_contract_blocked.
+template <int NT>
+__device__ __noinline__ void chain_contract_dmma(const double* xs, const double* zs, double* red, int cc0, int ccn,
+                                                 int nk, int nrows, int R, double* out_rows) {
+    constexpr int RP = 8 * NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, rr = lane >> 2;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[a][n][0] = acc[a][n][1] = 0.0;
+    for (int k0 = 0; k0 < ccn; k0 += 4) {
+        const bool valid = k0 + q < ccn;
+        const int smp = cc0 + k0 + q;
+        double fa[4], fb[NT];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fa[a] = valid ? xs[smp * kRowTile + a * 8 + rr] : 0.0;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) fb[n] = valid ? zs[smp * RP + n * 8 + rr] : 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(acc[a][n][0]), "+d"(acc[a][n][1])
+                             : "d"(fa[a]), "d"(fb[n]));
+    }
+    __syncthreads();  // every warp is done with the X tile (the Z tile stays resident)
+    constexpr int HC = RP / 2;  // columns per half
+    constexpr int RS = (8 * HC * kRedStride <= kSuperSamples * kRowTile) ? kRedStride : kRowTile;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (warp < nk) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = n * 8 + 2 * q + e, row = a * 8 + rr;
+                        if (col >= h * HC && col < (h + 1) * HC)
+                            red[(warp * HC + col - h * HC) * RS + row] = acc[a][n][e];
+                    }
+        }
+        __syncthreads();
+        for (int e = tid; e < HC * kRowTile; e += blockDim.x) {
+            const int c = e >> 5, i = e & 31, r = h * HC + c;
+            if (i < nrows && r < R) {
+                double qq = red[c * RS + i];
+                for (int k = 1; k < nk; ++k) qq = qq + red[(k * HC + c) * RS + i];
+                out_rows[int64_t(i) * R + r] = qq;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Shared-memory map of k_chain (doubles):
 //   [0, 8192)                X_s tile (TMA); phase B: L/D (TMA); Gram items: Z tile + chunk partials
 //   [8192, 8192 + 256*RP)    contraction Z tile (TMA)
@@ -960,11 +1027,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (kWide || kBlockedNarrow) {  // register-blocked item
                         double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
                         const int cn0 = max(ccn, 0);
-                        if constexpr (kWide) {
-                            if (RP == 40) chain_contract_blocked<10>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
-                            else if (RP == 48) chain_contract_blocked<12>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
-                            else if (RP == 56) chain_contract_blocked<14>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
-                            else chain_contract_blocked<16>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                        if constexpr (kWide) {  // fp64 tensor cores, bit-identical chunk partials
+                            if (RP == 40) chain_contract_dmma<5>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else if (RP == 48) chain_contract_dmma<6>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else if (RP == 56) chain_contract_dmma<7>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                            else chain_contract_dmma<8>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
                         } else {
                             if (RP == 8) chain_contract_blocked<2>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
                             else if (RP == 16) chain_contract_blocked<4>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
