@@ -1055,9 +1055,17 @@ int gather_sms(rocp_stream* st, int64_t B) {
             const int64_t cb = std::max<int64_t>(1, dev->num_sms - G - gram_blocks);
             return (items + cb - 1) / cb;
         };
+        // The wide kernel is compute-bound on its SMs, so among the splits with the fewest rounds
+        // it takes the one that leaves it the most (C4: 28 -> 142k, 32 -> 137k slices/s).
         int best = g;
-        for (int G = g; G >= std::max(1, int(std::floor(0.8 * g))); --G)
-            if (rounds(G) < rounds(best)) best = G;
+        if (st->R > 32) {
+            const int lo = std::max(1, int(std::ceil(0.85 * g)));
+            for (int G = g; G >= lo; --G)
+                if (rounds(G) <= rounds(best)) best = G;
+        } else {
+            for (int G = g; G >= std::max(1, int(std::floor(0.8 * g))); --G)
+                if (rounds(G) < rounds(best)) best = G;
+        }
         g = best;
     }
     return std::max(0, std::min(g, dev->num_sms / 2));
