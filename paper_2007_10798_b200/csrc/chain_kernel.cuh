@@ -580,6 +580,40 @@ __device__ __noinline__ void chain_contract_dmma(const double* xs, const double*
     }
 }
 
+// Chunk Gram partial on the fp64 tensor cores (narrow kernel, RP <= 32): the
+// lower 8x8 tiles of Z_chunk^T Z_chunk, one warp per tile, 8 MMA steps of 4
+// samples over the 32-sample chunk (rows past the chunk end are zero in zc).
+// Bit-identical to the per-pair fma chain from +0.0 in sample order (the MMA
+// rounds like that chain, tools/dmma_order.cu); out[q] for the lower pair q of
+// (i >= j), q = j R - j (j - 1) / 2 + (i - j).
+__device__ __noinline__ void chain_chunk_gram_dmma(const double* zc, int RP, int R, double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int q4 = lane & 3, rr = lane >> 2;
+    const int nt = RP / 8, ntiles = nt * (nt + 1) / 2;
+    for (int t = warp; t < ntiles; t += nw) {
+        int ti = 0, tj = t;  // lower tile (ti >= tj) number t, row-major over the lower triangle
+        while (tj > ti) {
+            tj -= ti + 1;
+            ++ti;
+        }
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < kChunk; k0 += 4) {
+            const double fa = zc[(k0 + q4) * RP + ti * 8 + rr];  // A(i, c) = z[c][i]
+            const double fb = zc[(k0 + q4) * RP + tj * 8 + rr];  // B(c, j) = z[c][j]
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(d0), "+d"(d1)
+                         : "d"(fa), "d"(fb));
+        }
+        const int i = ti * 8 + rr;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = tj * 8 + 2 * q4 + e;
+            if (i < R && j <= i) out[j * R - j * (j - 1) / 2 + (i - j)] = e ? d1 : d0;
+        }
+    }
+}
+
 // Shared-memory map of k_chain (doubles):
 //   [0, 8192)                X_s tile (TMA); phase B: L/D (TMA); Gram items: Z tile + chunk partials
 //   [8192, 8192 + 256*RP)    contraction Z tile (TMA)
@@ -785,16 +819,20 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                 }
                 __syncthreads();
                 if (tr) trace_stamp(tr, 14, tid == 0 && ch == 0);
-                for (int q = tid; q < npairs; q += blockDim.x) {
-                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
-                    double acc = 0.0;
-                    if (cn == kChunk) {
+                if constexpr (!kWide) {
+                    chain_chunk_gram_dmma(zc, RP, R, p.chpart + int64_t(ch) * NPp);
+                } else {
+                    for (int q = tid; q < npairs; q += blockDim.x) {
+                        const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                        double acc = 0.0;
+                        if (cn == kChunk) {
 #pragma unroll 8
-                        for (int cc = 0; cc < kChunk; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
-                    } else {
-                        for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                            for (int cc = 0; cc < kChunk; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                        } else {
+                            for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zc[cc * RP + i], zc[cc * RP + j], acc);
+                        }
+                        p.chpart[int64_t(ch) * NPp + q] = acc;  // lower pair q; (j, i) is the same value
                     }
-                    p.chpart[int64_t(ch) * NPp + q] = acc;  // lower pair q; (j, i) is the same value
                 }
                 __syncthreads();
                 if (tr) trace_stamp(tr, 15, tid == 0 && ch == 0);
