@@ -207,6 +207,7 @@ struct rocp_dev {
     cudaStream_t gstream = nullptr;
     cudaEvent_t ev_gready = nullptr, ev_gdone = nullptr;
     int gather_sms = -1;                // -1: not set (env decides); -2: per-stream model; >= 0: fixed
+    bool counted = false;               // registered in g_handles (live handles per GPU)
     int num_sms = 148;
     // device-resident result of the last rocp_cprand (for stream_create_from_init)
     struct Init {
@@ -997,6 +998,17 @@ void prepare_window(rocp_stream* st, const double* x, int64_t t0, int64_t slice,
     W.key_sort = sort_strided;
 }
 
+// Live handles per GPU in this process.  Two handles' streams run concurrently on
+// one GPU, and two cooperative chains plus their spinning gathers could then hold
+// each other's SMs: the model gathers serially while a GPU has more than one handle.
+std::mutex g_handles_mu;
+std::map<int, int> g_handles;
+int handles_on(int device) {
+    std::lock_guard<std::mutex> lk(g_handles_mu);
+    auto it = g_handles.find(device);
+    return it == g_handles.end() ? 0 : it->second;
+}
+
 // SMs reserved for the overlapped window gather.  ROCP_GATHER_SMS
 // overrides; otherwise a model picks the fewest SMs whose TMA gather (about
 // 1.47 G elements/s per SM, measured) keeps pace with the chain (about 14 us
@@ -1028,6 +1040,7 @@ int gather_sms(rocp_stream* st, int64_t B) {
         CK(cudaEventCreateWithFlags(&dev->ev_gdone, cudaEventDisableTiming));
     }
     int g = dev->gather_sms;
+    if (g == -2 && handles_on(dev->device) > 1) return 0;
     if (g == -2) {
         double elems = double(B), rows_max = double(B);  // gathered elements per sample of one batch
         for (int64_t I : st->head) {
@@ -1358,6 +1371,11 @@ rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, ro
         if (world > 1 && !nccl_id) throw_domain("world > 1 needs the NCCL unique id of rank 0");
         CK(cudaSetDevice(device));
         dev->device = device;
+        {
+            std::lock_guard<std::mutex> lk(g_handles_mu);
+            ++g_handles[device];
+            dev->counted = true;
+        }
         dev->world = world;
         dev->rank = rank;
         CK(cudaStreamCreateWithFlags(&dev->stream, cudaStreamNonBlocking));
@@ -1380,6 +1398,10 @@ rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, ro
     if (st != ROCP_OK) {
         static thread_local std::string last;
         last = dev->err;
+        if (dev->counted) {
+            std::lock_guard<std::mutex> lk(g_handles_mu);
+            if (--g_handles[dev->device] <= 0) g_handles.erase(dev->device);
+        }
         *out = nullptr;
         return st;
     }
@@ -1389,6 +1411,10 @@ rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, ro
 
 void rocp_destroy(rocp_dev* dev) {
     if (!dev) return;
+    if (dev->counted) {
+        std::lock_guard<std::mutex> lk(g_handles_mu);
+        if (--g_handles[dev->device] <= 0) g_handles.erase(dev->device);
+    }
     cudaSetDevice(dev->device);
     cudaStreamSynchronize(dev->stream);
     dev->init = rocp_dev::Init{};

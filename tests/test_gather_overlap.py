@@ -95,3 +95,27 @@ def test_gather_window_profiling_entry(gdev):
     a.restore()
     a.consume_range(X, t_init, B, nb, 4243, 1)
     assert a.last_gather_sms == 0
+
+
+def test_second_handle_on_the_gpu_gathers_serially(gdev):
+    """Two live handles on one GPU: the model stops overlapping (two cooperative chains and their
+    spinning gathers could otherwise hold each other's SMs); results stay bitwise equal."""
+    dims, R, t_init, B = [600, 600, 60], 6, 20, 10  # a gather share the model overlaps
+    x, X, a, b, s, nb = _run_pair(gdev, dims, R, 20.0, t_init, B)
+    gdev.set_gather_sms(-1)
+    a.checkpoint()
+    a.consume_range(X, t_init, B, nb, 99, 1)
+    alone = a.last_gather_sms
+    assert alone > 0
+    ref = [a.factor(n) for n in (1, 2)] + [a.temporal()]
+    other = rocp.Device(0)
+    try:
+        a.restore()
+        a.consume_range(X, t_init, B, nb, 99, 1)
+        assert a.last_gather_sms == 0
+        assert all(bitwise(u, v) for u, v in zip(ref, [a.factor(n) for n in (1, 2)] + [a.temporal()]))
+    finally:
+        other.close()
+    a.restore()
+    a.consume_range(X, t_init, B, nb, 99, 1)
+    assert a.last_gather_sms == alone
