@@ -74,11 +74,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
 // (seen = a value loaded earlier, usually during the previous phase).  A gather
 // that never arrives traps after ~20 s instead of hanging the device (long enough
 // for time-slicing with other GPU contexts).
-__device__ __noinline__ void wait_gathered(const unsigned* done, unsigned need, unsigned seen) {
+// nap: back-off between polls in ns (0: spin; the chain's own arrivals are microseconds apart).
+__device__ __noinline__ void wait_gathered(const unsigned* done, unsigned need, unsigned seen, unsigned nap = 128) {
     if (seen >= need) return;
     const unsigned long long t0 = gtimer_raw();
     while (ld_acquire_u32(done) < need) {
-        __nanosleep(128);
+        if (nap) __nanosleep(nap);
         if (gtimer_raw() - t0 > 20000000000ull) {
             printf("rocp: arrival wait timed out (counter %p at %u of %u, block %d)\n", (const void*)done,
                    ld_acquire_u32(done), need, int(blockIdx.x));
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // ---------------- phase 1
             if (is_gram_block) {
                 if (tid == 0) {  // every chunk partial of this stage published
-                    wait_gathered(p.zctr, unsigned(b * N + st + 1) * unsigned(nch), 0u);
+                    wait_gathered(p.zctr, unsigned(b * N + st + 1) * unsigned(nch), 0u, 0u);
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
                 }
                 __syncthreads();
@@ -1049,7 +1050,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         const bool zload = m != zm_cur;
                         if (zload) {  // superchunk m's chunks of Z published (no grid barrier after phase 0)
                             const unsigned nck = unsigned(min(kSuper, nch - m * kSuper));
-                            wait_gathered(p.zctr + 1 + m, unsigned(b * N + st + 1) * nck, 0u);
+                            wait_gathered(p.zctr + 1 + m, unsigned(b * N + st + 1) * nck, 0u, 0u);
                             asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
                             tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
                         }
