@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(256) k_contract(const double* __restrict__ X, 
 
 // Contraction for R <= 32 (primitives, cprand sweeps, the sharded stream's owned
 // mode): same canonical order as k_contract, but warp w of a 256-thread block
-// forms chunk w of the (32-row tile, superchunk) item -- lane = row, RPAD
-// register accumulators -- and the 8 chunk partials are summed left to right
+// forms chunk w of the (32-row tile, superchunk) item with fp64 mma.sync (4 x
+// RPAD/8 accumulator tiles) and the 8 chunk partials are summed left to right
 // through shared memory.  k_contract used 32 * ceil(R/10) threads per item,
 // each walking all 256 samples (configs[1]: 40 us per mode-1 contraction).
 template <int RPAD>
@@ -503,23 +503,40 @@ __global__ void __launch_bounds__(256) k_contract_chunks(const double* __restric
     cp_async_wait_all();
     __syncthreads();
     const int nk = (cn + kChunk - 1) / kChunk;
-    if (warp < nk) {  // chunk `warp`: fma chain from +0.0 over its samples, increasing order
+    if (warp < nk) {  // chunk `warp`: fma chain from +0.0 over its samples, increasing order, on the
+                      // fp64 tensor cores (mma.sync m8n8k4 rounds like that chain; samples past the
+                      // chunk enter as 0 x 0)
         const int cc0 = warp * kChunk, ccn = min(kChunk, cn - cc0);
-        double acc[RPAD];
+        constexpr int NT = RPAD / 8;
+        const int q4 = lane & 3, rr = lane >> 2;
+        double acc[4][NT][2];
 #pragma unroll
-        for (int r = 0; r < RPAD; ++r) acc[r] = 0.0;
-        for (int cc = 0; cc < ccn; ++cc) {
-            const double x = xs[(cc0 + cc) * kRowTile + lane];
-            const double2* zr = reinterpret_cast<const double2*>(zs + (cc0 + cc) * RPAD);
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int q = 0; q < RPAD / 2; ++q) {
-                const double2 zz = zr[q];
-                acc[2 * q] = __fma_rn(x, zz.x, acc[2 * q]);
-                acc[2 * q + 1] = __fma_rn(x, zz.y, acc[2 * q + 1]);
-            }
+            for (int n = 0; n < NT; ++n) acc[a][n][0] = acc[a][n][1] = 0.0;
+        for (int k0 = 0; k0 < ccn; k0 += 4) {
+            const bool valid = k0 + q4 < ccn;
+            const int smp = cc0 + k0 + q4;
+            double fa[4], fb[NT];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) fa[a] = valid ? xs[smp * kRowTile + a * 8 + rr] : 0.0;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) fb[n] = valid ? zs[smp * RPAD + n * 8 + rr] : 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                 : "+d"(acc[a][n][0]), "+d"(acc[a][n][1])
+                                 : "d"(fa[a]), "d"(fb[n]));
         }
 #pragma unroll
-        for (int r = 0; r < RPAD; ++r) cps[(warp * RPAD + r) * kRowTile + lane] = acc[r];
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    cps[(warp * RPAD + n * 8 + 2 * q4 + e) * kRowTile + a * 8 + rr] = acc[a][n][e];
     }
     __syncthreads();
     const bool split = nsuper > 1;
