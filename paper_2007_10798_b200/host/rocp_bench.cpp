@@ -72,10 +72,53 @@ void csv_row(std::ostream& out, const std::string& label, const std::string& alg
 
 }  // namespace
 
+std::optional<FactorFamily> parse_family(const std::string& name) {
+    if (name == "normal") return FactorFamily::normal;
+    if (name == "uniform") return FactorFamily::uniform;
+    if (name == "congruent") return FactorFamily::congruent;
+    return std::nullopt;
+}
+
 SyntheticTensor gen_synthetic(const Dims& dims, int rank, std::optional<double> sir_db, Rng& rng) {
+    return gen_synthetic(dims, rank, sir_db, rng, FactorFamily::normal);
+}
+
+SyntheticTensor gen_synthetic(const Dims& dims, int rank, std::optional<double> sir_db, Rng& rng, FactorFamily family,
+                              double congruence) {
     if (rank < 1) throw std::domain_error("gen_synthetic: rank must be positive");
     SyntheticTensor out;
-    out.truth = random_model(dims, rank, rng);
+    if (family == FactorFamily::uniform) {  // random_model's draw order with U(0,1)
+        std::uniform_real_distribution<double> unif(0.0, 1.0);
+        out.truth.rank = rank;
+        for (Index d : dims) {
+            Matrix f(d, rank);
+            for (Index i = 0; i < d; ++i)
+                for (int r = 0; r < rank; ++r) f(i, r) = unif(rng);
+            out.truth.factors.push_back(std::move(f));
+        }
+    } else {
+        out.truth = random_model(dims, rank, rng);
+    }
+    if (family == FactorFamily::congruent) {  // F = G L^T, L L^T = c 11^T + (1 - c) I
+        if (!(congruence > -1.0 / std::max(rank - 1, 1) && congruence < 1.0))
+            throw std::domain_error("gen_synthetic: congruence must keep c 11^T + (1 - c) I positive definite");
+        std::vector<double> L(size_t(rank) * rank, 0.0);
+        for (int i = 0; i < rank; ++i)
+            for (int j = 0; j <= i; ++j) {
+                double a = (i == j) ? 1.0 : congruence;
+                for (int k = 0; k < j; ++k) a -= L[size_t(i) * rank + k] * L[size_t(j) * rank + k];
+                L[size_t(i) * rank + j] = (i == j) ? std::sqrt(a) : a / L[size_t(j) * rank + j];
+            }
+        for (Matrix& f : out.truth.factors) {
+            Matrix g = f;
+            for (Index i = 0; i < f.rows(); ++i)
+                for (int r = 0; r < rank; ++r) {
+                    double v = 0.0;
+                    for (int k = 0; k <= r; ++k) v += g(i, k) * L[size_t(r) * rank + k];
+                    f(i, r) = v;
+                }
+        }
+    }
     // planted signal and exactly scaled noise on the device (rocp_generate_synthetic), one
     // noise seed drawn from rng after the factors
     const std::uint64_t noise_seed = sir_db ? rng() : 0;
@@ -173,7 +216,8 @@ BenchReport run_benchmark(const BenchConfig& cfg) {  // bench.cpp:179-213
     report.rows.resize(static_cast<size_t>(cfg.trials) * cfg.algorithms.size());
     for (int trial = 0; trial < cfg.trials; ++trial) {
         Rng data_rng = make_rng(cfg.seed, trial, 0);
-        const DenseTensor full = cfg.input_path.empty() ? gen_synthetic(cfg.dims, cfg.rank, cfg.sir_db, data_rng).x
+        const DenseTensor full = cfg.input_path.empty()
+                                     ? gen_synthetic(cfg.dims, cfg.rank, cfg.sir_db, data_rng, cfg.family, cfg.congruence).x
                                                         : read_tensor_file(cfg.input_path);
         const StreamSplit split = split_stream(full, cfg.init_fraction, cfg.batch_size);
         for (size_t a = 0; a < cfg.algorithms.size(); ++a)

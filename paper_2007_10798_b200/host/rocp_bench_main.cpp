@@ -23,7 +23,7 @@ namespace {
                  "options: --dims I1 .. IN | --input FILE, --rank R, --samples S, --init-frac F, --batch B,\n"
                  "         --algorithms rocp, --trials T, --seed N, --sir-db DB|none, --rocp-tol X,\n"
                  "         --rocp-max-iters K, --als-tol X, --als-max-iters K, --csv FILE, --updates-csv FILE,\n"
-                 "         --device D\n",
+                 "         --device D, --family normal|uniform|congruent, --congruence C\n",
                  msg);
     std::exit(2);
 }
@@ -68,6 +68,11 @@ int main(int argc, char** argv) {
         else if (a == "--csv") csv = value(i);
         else if (a == "--updates-csv") updates_csv = value(i);
         else if (a == "--device") rocp::set_device(std::stoi(value(i)));
+        else if (a == "--family") {
+            const auto f = rocp::parse_family(value(i));
+            if (!f) usage(("unknown factor family " + args[i]).c_str());
+            cfg.family = *f;
+        } else if (a == "--congruence") cfg.congruence = std::stod(value(i));
         else usage(("unknown option " + a).c_str());
     }
     try {

@@ -317,6 +317,35 @@ static void test_synthetic() {  // test_bench.cpp:15-91
     }
 }
 
+static void test_factor_families() {  // BASELINE configs[2] (U(0,1)) and configs[4] (congruence 0.9)
+    Rng r1(601);
+    const SyntheticTensor u = gen_synthetic({30, 20, 10}, 4, 30.0, r1, FactorFamily::uniform);
+    bool in01 = true;
+    for (const Matrix& f : u.truth.factors)
+        for (Index i = 0; i < f.size(); ++i) in01 = in01 && f.data()[i] >= 0.0 && f.data()[i] < 1.0;
+    CHECK(in01 && u.x.size() == 30 * 20 * 10);
+    Rng r2(603);
+    const SyntheticTensor c = gen_synthetic({4000, 8, 6}, 3, std::nullopt, r2, FactorFamily::congruent, 0.9);
+    const Matrix& f = c.truth.factors[0];
+    double worst = 0.0;
+    for (int a = 0; a < 3; ++a)
+        for (int b = a + 1; b < 3; ++b) {
+            double ab = 0, aa = 0, bb = 0;
+            for (Index i = 0; i < f.rows(); ++i) {
+                ab += f(i, a) * f(i, b);
+                aa += f(i, a) * f(i, a);
+                bb += f(i, b) * f(i, b);
+            }
+            worst = std::max(worst, std::abs(ab / std::sqrt(aa * bb) - 0.9));
+        }
+    CHECK(worst < 0.03);  // sample column congruence of 4000 rows
+    Rng r3(605), r4(605);  // the normal family is the reference's gen_synthetic
+    const SyntheticTensor n1 = gen_synthetic({5, 6, 7}, 2, 20.0, r3), n2 = gen_synthetic({5, 6, 7}, 2, 20.0, r4, FactorFamily::normal);
+    CHECK(n1.x.values() == n2.x.values());
+    CHECK(throws<std::domain_error>([&] { Rng r(1); gen_synthetic({4, 4, 4}, 3, std::nullopt, r, FactorFamily::congruent, 1.0); }));
+    CHECK(parse_family("uniform") == FactorFamily::uniform && !parse_family("gamma").has_value());
+}
+
 static void test_bench_harness() {  // test_bench.cpp:114-207
     {
         BenchConfig cfg;  // single-trial smoke run
@@ -393,7 +422,8 @@ int main() {
     const std::vector<std::pair<const char*, std::function<void()>>> cases = {
         {"index_map", test_index_map}, {"draws_and_gather", test_draws_and_gather}, {"skr", test_skr},
         {"solve", test_solve},         {"cprand", test_cprand},                     {"stream", test_stream},
-        {"records", test_records},     {"synthetic", test_synthetic},               {"bench_harness", test_bench_harness}};
+        {"records", test_records},     {"synthetic", test_synthetic},               {"bench_harness", test_bench_harness},
+        {"factor_families", test_factor_families}};
     for (const auto& [name, fn] : cases) {
         const int before = g_fail;
         try {
