@@ -101,6 +101,16 @@ __global__ void __launch_bounds__(128) k_draw(const DrawJob* __restrict__ jobs) 
     }
 }
 
+// Window prologue in one launch: draw seed, first batch id, and (overlapped
+// gather) the per-job unit counters.
+__global__ void k_window_setup(uint64_t* seed_p, uint64_t seed, uint32_t* batch_p, uint32_t batch,
+                               unsigned* done, int ndone) {
+    if (threadIdx.x == 0) {
+        *seed_p = seed;
+        *batch_p = batch;
+    }
+    for (int i = threadIdx.x; i < ndone; i += blockDim.x) done[i] = 0u;
+}
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
 __global__ void k_set_i32(int* p, int n, int v) {

@@ -1091,13 +1091,11 @@ int gather_sms(rocp_stream* st, int64_t B) {
 void enqueue_draw_gather(rocp_stream* st, uint64_t seed, uint32_t first_batch_id, bool overlap = false) {
     if (overlap && st->win_gsms <= 0) throw RocpError{ROCP_E_STATE, "overlapped gather without SMs (internal)"};
     rocp_dev* dev = st->dev;
-    k_set_u64<<<1, 1, 0, dev->stream>>>(st->seed_dev.p, seed);
-    after_launch(dev, "k_set_u64");
-    k_set_u32<<<1, 1, 0, dev->stream>>>(st->batch_dev.p, first_batch_id);
-    after_launch(dev, "k_set_u32");
     const JobList& L = st->win.jobs;
+    k_window_setup<<<1, 256, 0, dev->stream>>>(st->seed_dev.p, seed, st->batch_dev.p, first_batch_id, L.done.p,
+                                                overlap ? L.ngather : 0);
+    after_launch(dev, "k_window_setup");
     if (overlap) {
-        CK(cudaMemsetAsync(L.done.p, 0, size_t(L.ngather) * sizeof(unsigned), dev->stream));
         launch_draw(dev, L);
         if (L.nsort > 0) {
             k_sort_by_base<<<L.nsort, 1024, 0, dev->stream>>>(L.sort.p);
