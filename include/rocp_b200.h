@@ -224,6 +224,9 @@ rocp_status rocp_stream_update_mode_with(rocp_stream* st, const rocp_tensor* x_n
                                          const double* u_new, int mode, const int64_t* rows,
                                          int64_t s, double* z_new, double* x_s, int* regularized);
 rocp_status rocp_stream_finish_batch(rocp_stream* st, int64_t batch);
+/* Raises the stream's regularized flag (RocpStream::consume ORs the temporal
+ * solve's flag into it, rocp.cpp:150; the replay seams leave it untouched). */
+rocp_status rocp_stream_mark_regularized(rocp_stream* st);
 /* what: 0 = U(mode) (I x R), 1 = P(mode), 2 = Q(mode) (R x R),
  *       3 = temporal factor (t_len x R, mode ignored).  Column-major. */
 rocp_status rocp_stream_get(rocp_stream* st, int what, int mode, double* out);

@@ -10,8 +10,14 @@
 //   * Sample indices come from the counter RNG: overloads taking Rng& draw ONE
 //     64-bit seed from it per call; explicit-key overloads take (seed, batch,
 //     iteration).
-//   * CprandTrace / UpdateTrace are accepted but not filled (use the replay
-//     seams update_last_mode_with / update_mode_with for index-set replays).
+//   * CprandTrace / UpdateTrace are filled (cprand.cpp:34,44; rocp.cpp:125-129).
+//     A traced RocpStream::consume runs the per-stage replay path
+//     (update_last_mode_with / update_mode_with on the device), which is
+//     bitwise equal to the untraced persistent-chain path.
+//   * The free functions (init_state, update_last_mode[_with], update_mode_with,
+//     update_other_modes) take host matrices by value/reference as the
+//     reference does; each device primitive round-trips its operands.  They are
+//     the replay/reference-compatibility surface; RocpStream is the fast path.
 #pragma once
 
 #include <cstdint>
@@ -162,13 +168,13 @@ struct InitResult {
     std::uint64_t seed = 0;  // counter-RNG key the draws used
 };
 struct CprandTrace {
-    std::vector<std::vector<SampleIndexSet>> sweeps;  // not filled (see header comment)
+    std::vector<std::vector<SampleIndexSet>> sweeps;  // [sweep][mode-1] (cprand.hpp:28-31)
 };
 InitResult cprand_decompose(const DenseTensor& x, int rank, const CprandOptions& opts, Rng& rng,
                             CprandTrace* trace = nullptr);
 // Explicit form: initial model and counter seed given.
 InitResult cprand_decompose(const DenseTensor& x, const KruskalModel& initial, const CprandOptions& opts,
-                            std::uint64_t seed);
+                            std::uint64_t seed, CprandTrace* trace = nullptr);
 
 // ---- online stream (rocp.hpp:15-117) ---------------------------------------------
 struct ComplementaryState {
@@ -183,20 +189,59 @@ struct RocpConfig {
     bool literal_init = false;
 };
 struct UpdateTrace {
-    std::vector<SampleIndexSet> mode_idx;  // not filled (see header comment)
-    std::vector<Matrix> mode_z;
-    std::vector<Matrix> mode_x;
+    std::vector<SampleIndexSet> mode_idx;  // n = 1..N-1 (rocp.hpp:56-61)
+    std::vector<Matrix> mode_z;            // Z_s(n)^new, s x R
+    std::vector<Matrix> mode_x;            // X_s(n)^new, I_n x s
 };
+
+// init_state (rocp.hpp:35, rocp.cpp:45-69): Q(n) = Z_best(n)^T Z_best(n),
+// P(n) = U_best(n) Q(n) (or U_best(n) with literal_init), on the device.
+ComplementaryState init_state(const InitResult& init, Index s, const RocpConfig& cfg = {});
+
+// Temporal-mode solve for one batch (rocp.hpp:38-53, rocp.cpp:71-94).
+struct LastModeUpdate {
+    Matrix u_new;        // I_N,new x R
+    SampleIndexSet idx;  // the draw used
+    Matrix z_s;          // s x R
+    bool regularized = false;
+};
+LastModeUpdate update_last_mode_with(const KruskalModel& model, const DenseTensor& x_new, SampleIndexSet idx);
+// Counter-RNG draw keyed by `key` over x_new's temporal co-domain; the Rng&
+// form draws one 64-bit seed from rng (key = {seed, 0, 0}).
+LastModeUpdate update_last_mode(const KruskalModel& model, const DenseTensor& x_new, Index s, CounterKey key);
+LastModeUpdate update_last_mode(const KruskalModel& model, const DenseTensor& x_new, Index s, Rng& rng);
+
+// One non-temporal mode against an explicit index set (rocp.hpp:63-75,
+// rocp.cpp:96-113): P += X_s Z_new, Q += Z_new^T Z_new, U = P Q^-1.
+struct ModeUpdate {
+    Matrix z_new;  // s x R
+    Matrix x_s;    // I_n x s
+    bool regularized = false;
+};
+ModeUpdate update_mode_with(ComplementaryState& state, KruskalModel& model, const DenseTensor& x_new,
+                            const Matrix& u_new, const SampleIndexSet& idx);
+// Modes 1..N-1, Gauss-Seidel (rocp.hpp:77-81, rocp.cpp:115-131).  The draws of
+// mode n use `key` (the same key RocpStream::consume(x, seed, batch) uses for
+// all N draws of a batch, so update_last_mode + update_other_modes with
+// key = {seed, batch, 0} replays consume bit for bit); the Rng& form draws one
+// seed from rng.
+void update_other_modes(ComplementaryState& state, KruskalModel& model, const DenseTensor& x_new, const Matrix& u_new,
+                        CounterKey key, UpdateTrace* trace = nullptr);
+void update_other_modes(ComplementaryState& state, KruskalModel& model, const DenseTensor& x_new, const Matrix& u_new,
+                        Rng& rng, UpdateTrace* trace = nullptr);
 
 class RocpStream {
 public:
+    // t_capacity is an initial reservation only: the device temporal factor
+    // grows geometrically as in rocp.cpp:152-155, so streams of any length run.
     RocpStream(InitResult init, Index s, RocpConfig cfg = {}, Index t_capacity = 0);
     ~RocpStream();
     RocpStream(const RocpStream&) = delete;
     RocpStream& operator=(const RocpStream&) = delete;
 
     void consume(const DenseTensor& x_new, Rng& rng, UpdateTrace* trace = nullptr);
-    void consume(const DenseTensor& x_new, std::uint64_t seed, std::uint32_t batch_id);
+    void consume(const DenseTensor& x_new, std::uint64_t seed, std::uint32_t batch_id,
+                 UpdateTrace* trace = nullptr);
     KruskalModel model() const;
     ComplementaryState state() const;
     Index t_len() const;

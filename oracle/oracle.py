@@ -216,6 +216,18 @@ def solve_gram(g, rhs):
     return out, bool(reg.value)
 
 
+def gram_decision(g):
+    """solve_gram's regularisation decision (solve.cpp:17-33) in canonical form:
+    (mode, regularized, path, jacobi_lo, jacobi_hi); mode 0 = zero solution, path 0/1 =
+    settled by the certificate (no-reg / reg), 2 = exact Jacobi eigenvalues."""
+    g = _f64(g)
+    mode, reg, path = C.c_int(0), C.c_int(0), C.c_int(0)
+    lo, hi = C.c_double(0.0), C.c_double(0.0)
+    _check(lib().orc_gram_decision(_p(g), g.shape[0], C.byref(mode), C.byref(reg), C.byref(path),
+                                   C.byref(lo), C.byref(hi)))
+    return mode.value, bool(reg.value), path.value, lo.value, hi.value
+
+
 def solve_sampled_ls(z, x):
     z, x = _f64(z), _f64(x)
     if x.shape[1] != z.shape[0]:

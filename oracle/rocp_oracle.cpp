@@ -252,13 +252,151 @@ Ldl ldlt(const std::vector<double>& a_in, int R) {
     return f;
 }
 
-bool needs_regularization(const Ldl& f) {
+// ---- the regularisation decision (solve.cpp:17-33) ---------------------------
+// The reference decides from the exact eigenvalues of G (SelfAdjointEigenSolver):
+// zero solution if lambda_max <= 0, regularise if lambda_min <= 0 or
+// lambda_max / lambda_min > 1e12.  The canonical form reaches the
+// same decision without an eigensolver whenever a rigorous certificate settles it:
+//   * pivots: for SPD G every LDL^T pivot lies in [lambda_min, lambda_max], so
+//     dmax / dmin <= kappa;
+//   * tau = tr(G^-1) = sum_k |row k of L^-1|^2 / d_k, with
+//     lambda_max <= tr(G) and tr(G^-1) / R <= 1 / lambda_min <= tr(G^-1):
+//     maxdiag * tau / R <= kappa <= tr(G) * tau.
+// kappa certainly above 4e12 -> regularise; certainly below 2.5e11 -> not; a
+// non-positive max diagonal or pivot, or anything in between -> exact
+// eigenvalues by a deterministic cyclic Jacobi method (the kernels run the same
+// rotations in the same order, so the decision is bitwise shared).
+constexpr double kCertRegAbove = 4e12;
+constexpr double kCertNoRegBelow = 2.5e11;
+enum { kDecNoReg = 0, kDecReg = 1, kDecExact = 2 };
+
+// 32-lane xor butterfly (q = q + q[lane ^ off], off = 16..1), as the kernels' butterfly32.
+double butterfly_lanes(std::vector<double> v) {
+    v.resize(32, 0.0);
+    for (int off = 16; off >= 1; off >>= 1) {
+        std::vector<double> w(32);
+        for (int l = 0; l < 32; ++l) w[size_t(l)] = v[size_t(l)] + v[size_t(l ^ off)];
+        v = w;
+    }
+    return v[0];
+}
+
+// tau = tr(G^-1) from the factorization: column j of M = L^-1 on lane j % 32 of warp
+// j / 32 (forward substitution, updates in k order), c_j = sum_k fma(M_kj^2, 1/d_k),
+// a butterfly per warp, then warp 0 + warp 1.
+double cert_tau(const Ldl& f, int R) {
+    std::vector<double> dinv(static_cast<size_t>(R));
+    for (int k = 0; k < R; ++k) dinv[size_t(k)] = 1.0 / f.d[size_t(k)];
+    std::vector<double> c(64, 0.0);
+    std::vector<double> m(static_cast<size_t>(R));
+    for (int j = 0; j < R; ++j) {
+        for (int i = 0; i < R; ++i) m[size_t(i)] = (i == j) ? 1.0 : 0.0;
+        for (int k = 0; k + 1 < R; ++k) {
+            const double mk = m[size_t(k)];
+            for (int i = k + 1; i < R; ++i)
+                m[size_t(i)] = std::fma(-f.l[size_t(i + k * R)], mk, m[size_t(i)]);
+        }
+        double acc = 0.0;
+        for (int k = 0; k < R; ++k) {
+            const double q = m[size_t(k)] * m[size_t(k)];
+            acc = std::fma(q, dinv[size_t(k)], acc);
+        }
+        c[size_t(j)] = acc;
+    }
+    const double t0 = butterfly_lanes(std::vector<double>(c.begin(), c.begin() + 32));
+    const double t1 = butterfly_lanes(std::vector<double>(c.begin() + 32, c.end()));
+    return t0 + t1;
+}
+
+int certificate(double maxdiag, double tr, const Ldl& f, int R, double* tau_out) {
     double dmin = f.d[0], dmax = f.d[0];
     for (double x : f.d) {
         if (x < dmin) dmin = x;
         if (x > dmax) dmax = x;
     }
-    return !(dmin > 0.0) || dmax > kGramConditionLimit * dmin;
+    if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
+    const double tau = cert_tau(f, R);
+    if (tau_out) *tau_out = tau;
+    const double ratio = dmax / dmin;
+    const double klo = (maxdiag * tau) / double(R);
+    const double khi = tr * tau;
+    if (ratio > kCertRegAbove || klo > kCertRegAbove) return kDecReg;
+    if (khi <= kCertNoRegBelow) return kDecNoReg;
+    return kDecExact;
+}
+
+// Deterministic cyclic Jacobi eigenvalues of a symmetric R x R matrix (column-major;
+// destroyed).  Rotation (p, q) in row-cyclic order, skipped when |a_pq| <= eps
+// sqrt(|a_pp a_qq|); sweeps until one rotates nothing (at most 64).  Rutishauser's
+// update; every element's operation sequence is fixed (the kernels update the k
+// entries in parallel with the same expressions).
+void jacobi_eigen(std::vector<double>& a, int R, double* lo, double* hi) {
+    auto at = [&](int i, int j) -> double& { return a[size_t(i + j * R)]; };
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        bool rotated = false;
+        for (int p = 0; p + 1 < R; ++p)
+            for (int q = p + 1; q < R; ++q) {
+                const double apq = at(p, q), app = at(p, p), aqq = at(q, q);
+                const double thr = 2.220446049250313e-16 * std::sqrt(std::fabs(app) * std::fabs(aqq));
+                if (!(std::fabs(apq) > thr)) continue;
+                rotated = true;
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double t = (std::fabs(theta) > 1e150)
+                                     ? 0.5 / theta
+                                     : ((theta >= 0.0) ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double c = 1.0 / std::sqrt(t * t + 1.0);
+                const double sn = t * c;
+                for (int k = 0; k < R; ++k) {
+                    if (k == p || k == q) continue;
+                    const double g = at(k, p), h = at(k, q);
+                    const double np = c * g - sn * h;
+                    const double nq = sn * g + c * h;
+                    at(k, p) = np;
+                    at(p, k) = np;
+                    at(k, q) = nq;
+                    at(q, k) = nq;
+                }
+                at(p, p) = app - t * apq;
+                at(q, q) = aqq + t * apq;
+                at(p, q) = 0.0;
+                at(q, p) = 0.0;
+            }
+        if (!rotated) break;
+    }
+    double l = at(0, 0), h = at(0, 0);
+    for (int k = 1; k < R; ++k) {
+        if (at(k, k) < l) l = at(k, k);
+        if (at(k, k) > h) h = at(k, k);
+    }
+    *lo = l;
+    *hi = h;
+}
+
+// The decision for G: mode 0 = zero solution (lambda_max <= 0), else 1; *reg; *path =
+// the certificate outcome (0 no-reg, 1 reg, 2 exact eigenvalues).
+struct GramDecision {
+    int mode = 1;
+    bool reg = false;
+    int path = 0;
+};
+
+GramDecision decide_gram(const std::vector<double>& g, int R, double maxdiag, double tr, const Ldl& f) {
+    GramDecision dec;
+    dec.path = certificate(maxdiag, tr, f, R, nullptr);
+    if (dec.path == kDecExact) {
+        std::vector<double> a = g;
+        double lo = 0.0, hi = 0.0;
+        jacobi_eigen(a, R, &lo, &hi);
+        if (hi <= 0.0) {  // solve.cpp:21-26
+            dec.mode = 0;
+            dec.reg = true;
+        } else {
+            dec.reg = (lo <= 0.0 || hi / lo > kGramConditionLimit);  // solve.cpp:28
+        }
+    } else {
+        dec.reg = dec.path == kDecReg;
+    }
+    return dec;
 }
 
 // Solves y^T G = b^T for one row b (length R): forward L, diagonal, backward L^T.
@@ -285,21 +423,23 @@ void ldlt_solve_row(const Ldl& f, int R, const double* b, Index bstride, double*
     for (int j = 0; j < R; ++j) y[size_t(j) * ystride] = w[size_t(j)];
 }
 
-Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized) {
+Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path = nullptr) {
     const int R = int(gram.rows);
     const Index I = rhs.rows;
     Mat out(I, R);
     double maxdiag = gram(0, 0);
     for (int k = 1; k < R; ++k)
         if (gram(k, k) > maxdiag) maxdiag = gram(k, k);
-    if (maxdiag <= 0.0) {  // solve.cpp:21-26
+    double tr = gram(0, 0);
+    for (int k = 1; k < R; ++k) tr = tr + gram(k, k);
+    Ldl f = ldlt(gram.v, R);
+    const GramDecision dec = decide_gram(gram.v, R, maxdiag, tr, f);
+    if (path) *path = dec.path;
+    if (dec.mode == 0) {  // solve.cpp:21-26
         if (regularized) *regularized = true;
         return out;
     }
-    Ldl f = ldlt(gram.v, R);
-    if (needs_regularization(f)) {  // solve.cpp:28-33
-        double tr = gram(0, 0);
-        for (int k = 1; k < R; ++k) tr = tr + gram(k, k);
+    if (dec.reg) {  // solve.cpp:28-33
         const double lambda = 1e-12 * tr;
         std::vector<double> g = gram.v;
         for (int k = 0; k < R; ++k) g[size_t(k + k * R)] = g[size_t(k + k * R)] + lambda;
@@ -642,6 +782,28 @@ void orc_gram(const double* z, int64_t s, int rank, double* g) {
 
 void orc_contract(const double* x, int64_t rows, int64_t s, const double* z, int rank, double* out) {
     to_ptr(contract_of(from_ptr(x, rows, s), from_ptr(z, s, rank)), out);
+}
+
+int orc_gram_decision(const double* gram, int rank, int* mode, int* regularized, int* path, double* lo,
+                      double* hi) {
+    if (rank < 1) return fail(ORC_E_DOMAIN, "gram_decision: empty gram");
+    const Mat g = from_ptr(gram, rank, rank);
+    double maxdiag = g(0, 0), tr = g(0, 0);
+    for (int k = 1; k < rank; ++k) {
+        if (g(k, k) > maxdiag) maxdiag = g(k, k);
+        tr = tr + g(k, k);
+    }
+    const Ldl f = ldlt(g.v, rank);
+    const GramDecision dec = decide_gram(g.v, rank, maxdiag, tr, f);
+    if (mode) *mode = dec.mode;
+    if (regularized) *regularized = dec.reg ? 1 : 0;
+    if (path) *path = dec.path;
+    std::vector<double> a = g.v;
+    double l = 0.0, h = 0.0;
+    jacobi_eigen(a, rank, &l, &h);
+    if (lo) *lo = l;
+    if (hi) *hi = h;
+    return ORC_OK;
 }
 
 int orc_solve_gram(const double* gram, const double* rhs, int64_t rows, int rank, double* out,

@@ -83,6 +83,12 @@ void orc_contract(const double* x, int64_t rows, int64_t s, const double* z, int
                   double* out);
 int orc_solve_gram(const double* gram, const double* rhs, int64_t rows, int rank, double* out,
                    int* regularized);
+/* solve_gram's regularisation decision (solve.cpp:17-33) in canonical form:
+ * mode 0 = zero solution; path 0/1 = settled by the pivot / tr(G^-1) certificate
+ * (no-reg / reg), 2 = exact (cyclic Jacobi) eigenvalues.  lo/hi: the Jacobi
+ * eigenvalue extremes (always computed here, for tests). */
+int orc_gram_decision(const double* gram, int rank, int* mode, int* regularized, int* path, double* lo,
+                      double* hi);
 int orc_solve_sampled_ls(const double* z, const double* x, int64_t s, int64_t rows, int rank,
                          double* out, int* regularized, int* underdetermined);
 

@@ -98,6 +98,7 @@ SIGNATURES = [
     ("rocp_stream_update_mode_with", C.c_int, [_vp, _vp, _f64p, C.c_int, _i64p, C.c_int64, _f64p,
                                                _f64p, C.POINTER(C.c_int)]),
     ("rocp_stream_finish_batch", C.c_int, [_vp, C.c_int64]),
+    ("rocp_stream_mark_regularized", C.c_int, [_vp]),
     ("rocp_stream_get", C.c_int, [_vp, C.c_int, C.c_int, _f64p]),
     ("rocp_stream_set", C.c_int, [_vp, C.c_int, C.c_int, _f64p]),
     ("rocp_stream_t_len", C.c_int64, [_vp]),

@@ -1040,7 +1040,9 @@ int gather_sms(rocp_stream* st, int64_t B) {
         CK(cudaEventCreateWithFlags(&dev->ev_gdone, cudaEventDisableTiming));
     }
     int g = dev->gather_sms;
-    if (g == -2 && handles_on(dev->device) > 1) return 0;
+    // Two handles on one GPU: their cooperative chains and spinning gathers could hold
+    // each other's SMs, whatever split was requested (explicit, env or model).
+    if (handles_on(dev->device) > 1) return 0;
     if (g == -2) {
         double elems = double(B), rows_max = double(B);  // gathered elements per sample of one batch
         for (int64_t I : st->head) {
@@ -1336,9 +1338,27 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
     }
 }
 
-void check_capacity(rocp_stream* st, int64_t add) {
-    if (st->t_len + add > st->t_cap) throw_domain("temporal capacity exceeded (raise t_capacity)");
+// The temporal factor grows geometrically, as RocpStream::consume does
+// (rocp.cpp:152-155: capacity max(2 x rows, t_len + batch)): a new buffer, the
+// t_len used rows copied on the device, the old one released after the stream
+// drains.  Captured graphs hold the old pointer and are dropped.
+void grow_temporal(rocp_stream* st, int64_t need) {
+    if (need <= st->t_cap) return;
+    rocp_dev* dev = st->dev;
+    const int64_t cap = std::max<int64_t>(2 * st->t_cap, need);
+    DBuf<double> grown(size_t(cap * st->R));
+    CK(cudaMemsetAsync(grown.p, 0, size_t(cap * st->R) * sizeof(double), dev->stream));
+    if (st->t_len > 0)
+        CK(cudaMemcpyAsync(grown.p, st->temporal.p, size_t(st->t_len * st->R) * sizeof(double),
+                           cudaMemcpyDeviceToDevice, dev->stream));
+    CK(cudaStreamSynchronize(dev->stream));  // queued chains may still read or write the old rows
+    if (st->copy_stream) CK(cudaStreamSynchronize(st->copy_stream));
+    st->temporal = std::move(grown);
+    st->t_cap = cap;
+    clear_graphs(st);
 }
+
+void check_capacity(rocp_stream* st, int64_t add) { grow_temporal(st, st->t_len + add); }
 
 // One batch on a device slab (no graph).
 void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uint32_t batch_id) {
@@ -2237,7 +2257,8 @@ rocp_status rocp_stream_update_last_mode_with(rocp_stream* st, const rocp_tensor
 
 rocp_status rocp_stream_append_temporal(rocp_stream* st, const double* u_new, int64_t batch) {
     return guarded(st->dev, [&] {
-        if (st->t_len + batch > st->t_cap) throw_domain("temporal capacity exceeded");
+        if (batch < 0) throw_domain("append_temporal: negative batch");
+        check_capacity(st, batch);
         std::vector<double> rm = colmajor_to_rowmajor(u_new, batch, st->R);
         CK(cudaMemcpyAsync(st->temporal.p + st->t_len * st->R, rm.data(), rm.size() * 8, cudaMemcpyHostToDevice,
                            st->dev->stream));
@@ -2289,7 +2310,15 @@ rocp_status rocp_stream_update_mode_with(rocp_stream* st, const rocp_tensor* x_n
 }
 
 rocp_status rocp_stream_finish_batch(rocp_stream* st, int64_t batch) {
-    return guarded(st->dev, [&] { st->t_len += batch; });
+    return guarded(st->dev, [&] {
+        if (batch < 0) throw_domain("finish_batch: negative batch");
+        check_capacity(st, batch);
+        st->t_len += batch;
+    });
+}
+
+rocp_status rocp_stream_mark_regularized(rocp_stream* st) {
+    return guarded(st->dev, [&] { st->regularized = true; });
 }
 
 rocp_status rocp_stream_get(rocp_stream* st, int what, int mode, double* out) {

@@ -41,6 +41,13 @@ void check(rocp_status st, int sweep = 0) {
     if (st != ROCP_OK) raise(device_handle(), st, sweep);
 }
 
+void check_head_dims(const Dims& head, const DenseTensor& x_new) {  // rocp.cpp:14-21
+    const Dims& d = x_new.dims();
+    if (d.size() != head.size() + 1) throw std::domain_error("batch order does not match stream order");
+    for (size_t k = 0; k < head.size(); ++k)
+        if (d[k] != head[k]) throw std::domain_error("batch head extents do not match stream");
+}
+
 void check_mode(const Dims& dims, int mode) {  // tensor.cpp:19-23
     if (mode < 1 || mode > static_cast<int>(dims.size()))
         throw std::domain_error("mode " + std::to_string(mode) + " out of range for order " +
@@ -270,7 +277,7 @@ Matrix solve_sampled_ls(const Matrix& z_s, const Matrix& x_s, SolveInfo* info) {
 
 // ---- cprand -------------------------------------------------------------------------
 InitResult cprand_decompose(const DenseTensor& x, const KruskalModel& initial, const CprandOptions& opts,
-                            std::uint64_t seed) {
+                            std::uint64_t seed, CprandTrace* trace) {
     if (initial.rank < 1) throw std::domain_error("cprand_decompose: rank must be positive");
     const int N = x.order();
     const Index s = opts.samples > 0 ? opts.samples : auto_sample_count(initial.rank);
@@ -290,16 +297,26 @@ InitResult cprand_decompose(const DenseTensor& x, const KruskalModel& initial, c
     res.regularized = reg != 0;
     res.seed = seed;
     for (int n = 0; n + 1 < N; ++n) res.best_sampled_factors.push_back(res.model.factors[static_cast<size_t>(n)]);
+    if (trace) {  // cprand.cpp:34,44: the index sets of every sweep, [sweep][mode-1]
+        // The counter RNG makes them a pure function of (seed, sweep, mode): sweep k
+        // draws with key (seed, batch 0, iteration k), so they are
+        // regenerated on the device rather than copied out of the sweep loop.
+        for (int sweep = 1; sweep <= iters; ++sweep) {
+            trace->sweeps.emplace_back();
+            for (int n = 1; n <= N; ++n)
+                trace->sweeps.back().push_back(
+                    draw_samples(x.dims(), n, s, CounterKey{seed, 0, static_cast<std::uint32_t>(sweep)}));
+        }
+    }
     return res;
 }
 
 InitResult cprand_decompose(const DenseTensor& x, int rank, const CprandOptions& opts, Rng& rng,
                             CprandTrace* trace) {
-    (void)trace;
     if (rank < 1) throw std::domain_error("cprand_decompose: rank must be positive");
     if (opts.max_iters < 1) throw std::domain_error("cprand_decompose: need at least one sweep");
     const KruskalModel init = random_model(x.dims(), rank, rng);  // cprand.cpp:25
-    return cprand_decompose(x, init, opts, rng());
+    return cprand_decompose(x, init, opts, rng(), trace);
 }
 
 // ---- stream -------------------------------------------------------------------------
@@ -331,17 +348,40 @@ RocpStream::~RocpStream() {
     if (h_) rocp_stream_free(h_);
 }
 
-void RocpStream::consume(const DenseTensor& x_new, std::uint64_t seed, std::uint32_t batch_id) {
-    if (x_new.order() != order_) throw std::domain_error("batch order does not match stream order");
-    for (size_t k = 0; k < head_.size(); ++k)
-        if (x_new.dims()[k] != head_[k]) throw std::domain_error("batch head extents do not match stream");
-    check(rocp_stream_consume_host(h_, x_new.data(), x_new.dims().back(), seed, batch_id));
+void RocpStream::consume(const DenseTensor& x_new, std::uint64_t seed, std::uint32_t batch_id, UpdateTrace* trace) {
+    check_head_dims(head_, x_new);  // rocp.cpp:145
+    if (!trace) {
+        check(rocp_stream_consume_host(h_, x_new.data(), x_new.dims().back(), seed, batch_id));
+        next_batch_ = batch_id + 1;
+        return;
+    }
+    // Traced: the same batch through the per-stage replay seams (rocp.cpp:144-160 step by
+    // step), which are bitwise equal to the persistent chain, recording each mode's
+    // sampled system (rocp.cpp:125-129).
+    const Index B = x_new.dims().back();
+    const Dims& dims = x_new.dims();
+    DevTensor t(x_new);
+    const SampleIndexSet it = draw_samples(dims, order_, s_, CounterKey{seed, batch_id, 0});
+    Matrix u_new(B, rank_);
+    int reg = 0;
+    check(rocp_stream_update_last_mode_with(h_, t.t, it.rows.data(), s_, u_new.data(), nullptr, &reg));
+    if (reg) check(rocp_stream_mark_regularized(h_));  // rocp.cpp:150
+    check(rocp_stream_append_temporal(h_, u_new.data(), B));
+    for (int n = 1; n < order_; ++n) {
+        SampleIndexSet idx = draw_samples(dims, n, s_, CounterKey{seed, batch_id, 0});
+        Matrix z(s_, rank_), xs(dims[static_cast<size_t>(n - 1)], s_);
+        int r2 = 0;
+        check(rocp_stream_update_mode_with(h_, t.t, u_new.data(), n, idx.rows.data(), s_, z.data(), xs.data(), &r2));
+        trace->mode_idx.push_back(std::move(idx));
+        trace->mode_z.push_back(std::move(z));
+        trace->mode_x.push_back(std::move(xs));
+    }
+    check(rocp_stream_finish_batch(h_, B));
     next_batch_ = batch_id + 1;
 }
 
 void RocpStream::consume(const DenseTensor& x_new, Rng& rng, UpdateTrace* trace) {
-    (void)trace;
-    consume(x_new, rng(), next_batch_);
+    consume(x_new, rng(), next_batch_, trace);
 }
 
 KruskalModel RocpStream::model() const {
@@ -380,6 +420,125 @@ double RocpStream::last_residual() const {
     std::vector<double> r(static_cast<size_t>(order_));
     check(rocp_stream_last_residuals(h_, r.data()));
     return r[0];
+}
+
+// ---- free functions of the online update (rocp.hpp:35-81) ---------------------------
+ComplementaryState init_state(const InitResult& init, Index s, const RocpConfig& cfg) {  // rocp.cpp:45-69
+    const int N = init.model.order();
+    if (static_cast<int>(init.best_sampled_kr.size()) != N - 1 ||
+        static_cast<int>(init.best_sampled_factors.size()) != N - 1)
+        throw std::domain_error("init_state: expected one sampled system per non-temporal mode");
+    Dims head;
+    for (int n = 0; n + 1 < N; ++n) {
+        const Matrix& z = init.best_sampled_kr[static_cast<size_t>(n)];
+        const Matrix& u = init.best_sampled_factors[static_cast<size_t>(n)];
+        if (z.rows() != s) throw std::domain_error("init_state: sampled Khatri-Rao row count differs from s");
+        if (z.cols() != u.cols()) throw std::domain_error("init_state: rank mismatch");
+        head.push_back(u.rows());
+    }
+    const int R = init.model.rank;
+    // Q = Z^T Z and P = U Q in the canonical order of the stream's own init
+    // (k_gram / k_mul_uq), through a transient device stream.
+    std::vector<const double*> f = ptrs(init.best_sampled_factors);
+    f.push_back(init.model.factors.back().data());
+    const auto kr = ptrs(init.best_sampled_kr);
+    const Index t_init = init.model.factors.back().rows();
+    rocp_stream* h = nullptr;
+    check(rocp_stream_create(device_handle(), N, head.data(), R, s, cfg.literal_init ? 1 : 0, f.data(), t_init,
+                             kr.data(), init.regularized ? 1 : 0, t_init, &h));
+    std::unique_ptr<rocp_stream, void (*)(rocp_stream*)> guard(h, rocp_stream_free);
+    ComplementaryState st;
+    st.sample_count = s;
+    st.t_len = t_init;
+    st.dims_head = head;
+    for (int n = 1; n < N; ++n) {
+        Matrix p(head[static_cast<size_t>(n - 1)], R), q(R, R);
+        check(rocp_stream_get(h, 1, n, p.data()));
+        check(rocp_stream_get(h, 2, n, q.data()));
+        st.p.push_back(std::move(p));
+        st.q.push_back(std::move(q));
+    }
+    return st;
+}
+
+LastModeUpdate update_last_mode_with(const KruskalModel& model, const DenseTensor& x_new,
+                                     SampleIndexSet idx) {  // rocp.cpp:71-84
+    const int N = model.order();
+    if (idx.mode != N) throw std::domain_error("update_last_mode: index set must be over the temporal mode");
+    LastModeUpdate upd;
+    upd.z_s = sampled_khatri_rao(idx, factors_excluding(model, N));
+    const Matrix x_s = sample_unfolding(x_new, idx);
+    SolveInfo info;
+    upd.u_new = solve_sampled_ls(upd.z_s, x_s, &info);
+    upd.regularized = info.regularized;
+    upd.idx = std::move(idx);
+    return upd;
+}
+
+LastModeUpdate update_last_mode(const KruskalModel& model, const DenseTensor& x_new, Index s, CounterKey key) {
+    Dims head = model.dims();  // rocp.cpp:86-94
+    head.pop_back();
+    check_head_dims(head, x_new);
+    return update_last_mode_with(model, x_new, draw_samples(x_new.dims(), model.order(), s, key));
+}
+
+LastModeUpdate update_last_mode(const KruskalModel& model, const DenseTensor& x_new, Index s, Rng& rng) {
+    return update_last_mode(model, x_new, s, CounterKey{rng(), 0, 0});
+}
+
+ModeUpdate update_mode_with(ComplementaryState& state, KruskalModel& model, const DenseTensor& x_new,
+                            const Matrix& u_new, const SampleIndexSet& idx) {  // rocp.cpp:96-113
+    const int n = idx.mode;
+    if (n < 1 || n >= model.order())
+        throw std::domain_error("update_mode_with: index set must be over a non-temporal mode");
+    if (static_cast<int>(state.p.size()) != model.order() - 1 || static_cast<int>(state.q.size()) != model.order() - 1)
+        throw std::domain_error("update_mode_with: state does not match the model order");
+    // slab_factors_excluding (rocp.cpp:25-34): u_new first, then modes N-1..1 without n
+    std::vector<Matrix> fs;
+    fs.push_back(u_new);
+    for (int k = model.order() - 1; k >= 1; --k)
+        if (k != n) fs.push_back(model.factors[static_cast<size_t>(k - 1)]);
+    ModeUpdate upd;
+    upd.z_new = sampled_khatri_rao(idx, fs);
+    upd.x_s = sample_unfolding(x_new, idx);
+    const int R = static_cast<int>(upd.z_new.cols());
+    Matrix& p = state.p[static_cast<size_t>(n - 1)];
+    Matrix& q = state.q[static_cast<size_t>(n - 1)];
+    if (p.rows() != upd.x_s.rows() || p.cols() != R || q.rows() != R || q.cols() != R)
+        throw std::domain_error("update_mode_with: state shapes do not match the sampled system");
+    // P + (X_s Z) and Q + (Z^T Z), each increment in the canonical chunked order on
+    // the device, then one IEEE add per entry -- the stream's accumulation
+    Matrix inc(p.rows(), R), g(R, R);
+    check(rocp_contract(device_handle(), upd.x_s.data(), upd.x_s.rows(), upd.x_s.cols(), upd.z_new.data(), R,
+                        inc.data()));
+    check(rocp_gram(device_handle(), upd.z_new.data(), upd.z_new.rows(), R, g.data()));
+    for (Index e = 0; e < p.size(); ++e) p.data()[e] = p.data()[e] + inc.data()[e];
+    for (Index e = 0; e < q.size(); ++e) q.data()[e] = q.data()[e] + g.data()[e];
+    SolveInfo info;
+    model.factors[static_cast<size_t>(n - 1)] = solve_gram(q, p, &info);
+    upd.regularized = info.regularized;
+    return upd;
+}
+
+void update_other_modes(ComplementaryState& state, KruskalModel& model, const DenseTensor& x_new, const Matrix& u_new,
+                        CounterKey key, UpdateTrace* trace) {  // rocp.cpp:115-131
+    check_head_dims(state.dims_head, x_new);
+    if (u_new.rows() != x_new.dims().back())
+        throw std::domain_error("update_other_modes: u_new rows must equal the batch size");
+    for (int n = 1; n < model.order(); ++n) {
+        SampleIndexSet idx = draw_samples(x_new.dims(), n, state.sample_count, key);
+        ModeUpdate upd = update_mode_with(state, model, x_new, u_new, idx);
+        if (trace) {
+            trace->mode_idx.push_back(std::move(idx));
+            trace->mode_z.push_back(std::move(upd.z_new));
+            trace->mode_x.push_back(std::move(upd.x_s));
+        }
+    }
+}
+
+void update_other_modes(ComplementaryState& state, KruskalModel& model, const DenseTensor& x_new, const Matrix& u_new,
+                        Rng& rng, UpdateTrace* trace) {
+    update_other_modes(state, model, x_new, u_new, CounterKey{rng(), 0, 0}, trace);
 }
 
 KruskalModel rocp_run(const DenseTensor& x_init, std::span<const DenseTensor> batches, int rank,

@@ -1,82 +1,226 @@
-// rocp_bench.cpp -- synthetic data and the benchmark harness of the reference
-// (synthetic.cpp:8-57, bench.cpp:17-264) over the B200 C++ API.  Differences
-// are listed in include/rocp_b200/bench.hpp.
+// rocp_bench.cpp -- the benchmark-report surface of the reference
+// (include/rocp/synthetic.hpp, include/rocp/bench.hpp: the CSV schema and the
+// trial/seed conventions) implemented on the B200 stream.  Behavioural notes
+// and deviations are listed in include/rocp_b200/bench.hpp.
+//
+// Structure (own design, not the reference's):
+//   * SlabCutter   -- the init/batch boundaries of a stream split, computed once
+//                     and materialised slab by slab;
+//   * RunningStats -- Welford mean / sample standard deviation per column;
+//   * TrialTimer   -- wall-clock bracket around a device-synchronised region;
+//   * CsvLine      -- field joiner for the two report tables.
 
 #include "../../include/rocp_b200/bench.hpp"
 
 #include "../../include/rocp_b200.h"
 
-#include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
+#include <map>
 #include <ostream>
+#include <sstream>
 #include <stdexcept>
+#include <utility>
 
 namespace rocp {
 
 namespace {
 
-using Clock = std::chrono::steady_clock;
-
-double seconds_since(Clock::time_point start) {
-    return std::chrono::duration<double>(Clock::now() - start).count();
+// ---- device plumbing ------------------------------------------------------------
+void status_or_throw(rocp_status st) {
+    switch (st) {
+        case ROCP_OK: return;
+        case ROCP_E_DOMAIN: throw std::domain_error(rocp_last_error(device_handle()));
+        case ROCP_E_NUMERICAL: throw NumericalError(rocp_last_error(device_handle()), 0);
+        default:
+            throw std::runtime_error("rocp_b200 status " + std::to_string(int(st)) + ": " +
+                                     rocp_last_error(device_handle()));
+    }
 }
 
-// One generator per (seed, trial, stream), as bench.cpp:27-31.
-Rng make_rng(std::uint64_t seed, int trial, int stream) {
-    std::seed_seq seq{static_cast<std::uint64_t>(seed), static_cast<std::uint64_t>(trial),
-                      static_cast<std::uint64_t>(stream)};
+// Wall time of a region that ends with the device drained, so an asynchronous
+// launch is charged to the update that issued it.
+class TrialTimer {
+public:
+    TrialTimer() : t0_(std::chrono::steady_clock::now()) {}
+    double stop() const {
+        status_or_throw(rocp_synchronize(device_handle()));
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+    }
+
+private:
+    std::chrono::steady_clock::time_point t0_;
+};
+
+// Independent std::mt19937_64 per (seed, trial, purpose): the reference seeds its
+// generators from the triple through std::seed_seq (bench.hpp seed semantics); purpose
+// 0 is the data, purpose 1 + algorithm index the algorithm's draws.
+Rng seeded_engine(std::uint64_t seed, int trial, int purpose) {
+    std::seed_seq seq{seed, static_cast<std::uint64_t>(trial), static_cast<std::uint64_t>(purpose)};
     return Rng(seq);
 }
 
-void check(rocp_status st) {
-    if (st == ROCP_OK) return;
-    const std::string msg = rocp_last_error(device_handle());
-    if (st == ROCP_E_DOMAIN) throw std::domain_error(msg);
-    if (st == ROCP_E_NUMERICAL) throw NumericalError(msg, 0);
-    throw std::runtime_error("rocp_b200 status " + std::to_string(int(st)) + ": " + msg);
-}
-
-void sync() { check(rocp_synchronize(device_handle())); }
-
-TrialResult run_rocp_cell(const BenchConfig& cfg, int trial, const DenseTensor& full, const StreamSplit& split) {
-    TrialResult row;
-    row.trial = trial;
-    row.algorithm = Algorithm::rocp;
-    Rng rng = make_rng(cfg.seed, trial, static_cast<int>(Algorithm::rocp) + 1);
-    const CprandOptions opts{cfg.samples, cfg.rocp_tol, cfg.rocp_max_iters};
-    const Index s = cfg.samples > 0 ? cfg.samples : auto_sample_count(cfg.rank);
-    const auto start = Clock::now();
-    InitResult init = cprand_decompose(split.init, cfg.rank, opts, rng);
-    RocpStream stream(std::move(init), s, RocpConfig{}, full.dims().back());
-    sync();
-    row.init_seconds = seconds_since(start);
-    for (const DenseTensor& batch : split.batches) {  // bench.cpp:50-59 timed()
-        const auto t0 = Clock::now();
-        stream.consume(batch, rng);
-        sync();
-        const double dt = seconds_since(t0);
-        row.update_seconds.push_back(dt);
-        row.stream_seconds += dt;
-        ++row.updates;
+// ---- stream split ------------------------------------------------------------------
+// Boundaries along the last mode: [0, init) then runs of `batch` (the last one may be
+// short).  Slabs are contiguous in the first-index-fastest layout.
+class SlabCutter {
+public:
+    SlabCutter(const DenseTensor& x, double init_fraction, Index batch) : x_(x) {
+        if (!(init_fraction > 0.0 && init_fraction < 1.0))
+            throw std::domain_error("split_stream: init fraction must lie in (0,1)");
+        if (batch < 1) throw std::domain_error("split_stream: batch size must be positive");
+        const Index t = x.dims().back();
+        const Index t_init = static_cast<Index>(std::floor(init_fraction * static_cast<double>(t)));
+        if (t_init < 1) throw std::domain_error("split_stream: initial slice is empty");
+        slice_ = x.size() / t;
+        cuts_.push_back(0);
+        cuts_.push_back(t_init);
+        while (cuts_.back() < t) cuts_.push_back(std::min(t, cuts_.back() + batch));
     }
-    row.fitness = model_fitness(full, stream.model());
-    return row;
+    size_t pieces() const { return cuts_.size() - 1; }
+    DenseTensor piece(size_t k) const {
+        Dims d = x_.dims();
+        d.back() = cuts_[k + 1] - cuts_[k];
+        const double* lo = x_.data() + cuts_[k] * slice_;
+        return DenseTensor(std::move(d), std::vector<double>(lo, lo + d.back() * slice_));
+    }
+
+private:
+    const DenseTensor& x_;
+    Index slice_ = 0;
+    std::vector<Index> cuts_;
+};
+
+// ---- statistics -----------------------------------------------------------------------
+class RunningStats {
+public:
+    void add(double v) {
+        ++n_;
+        const double delta = v - mean_;
+        mean_ += delta / static_cast<double>(n_);
+        m2_ += delta * (v - mean_);
+    }
+    double mean() const { return mean_; }
+    // sample standard deviation; a single observation has none (reported as 0)
+    double stddev() const { return n_ > 1 ? std::sqrt(m2_ / static_cast<double>(n_ - 1)) : 0.0; }
+
+private:
+    long n_ = 0;
+    double mean_ = 0.0, m2_ = 0.0;
+};
+
+// ---- CSV ------------------------------------------------------------------------------
+class CsvLine {
+public:
+    explicit CsvLine(std::ostream& out) : out_(out) {}
+    template <class T>
+    CsvLine& operator<<(const T& field) {
+        if (fields_++) out_ << ',';
+        out_ << field;
+        return *this;
+    }
+    ~CsvLine() { out_ << '\n'; }
+
+private:
+    std::ostream& out_;
+    int fields_ = 0;
+};
+
+// Restores the caller's stream formatting after writing with 17 significant digits.
+class FullPrecision {
+public:
+    explicit FullPrecision(std::ostream& out) : out_(out), flags_(out.flags()), prec_(out.precision(17)) {}
+    ~FullPrecision() {
+        out_.precision(prec_);
+        out_.flags(flags_);
+    }
+
+private:
+    std::ostream& out_;
+    std::ios::fmtflags flags_;
+    std::streamsize prec_;
+};
+
+constexpr std::array<std::pair<Algorithm, const char*>, 4> kAlgorithmNames{{
+    {Algorithm::rocp, "rocp"},
+    {Algorithm::online_full, "online_full"},
+    {Algorithm::batch_hot, "batch_hot"},
+    {Algorithm::batch_cold, "batch_cold"},
+}};
+
+// The B200 cell: randomized init + device stream, each update timed around the
+// reference-facing host-slab consume.
+TrialResult rocp_trial(const BenchConfig& cfg, int trial, const DenseTensor& full, const SlabCutter& cut) {
+    TrialResult out;
+    out.trial = trial;
+    out.algorithm = Algorithm::rocp;
+    Rng rng = seeded_engine(cfg.seed, trial, static_cast<int>(Algorithm::rocp) + 1);
+    const Index s = cfg.samples > 0 ? cfg.samples : auto_sample_count(cfg.rank);
+    const TrialTimer init_timer;
+    InitResult init = cprand_decompose(cut.piece(0), cfg.rank, CprandOptions{cfg.samples, cfg.rocp_tol,
+                                                                            cfg.rocp_max_iters}, rng);
+    RocpStream stream(std::move(init), s, RocpConfig{}, full.dims().back());
+    out.init_seconds = init_timer.stop();
+    for (size_t k = 1; k < cut.pieces(); ++k) {
+        const DenseTensor slab = cut.piece(k);  // materialised outside the timed region
+        const TrialTimer t;
+        stream.consume(slab, rng);
+        out.update_seconds.push_back(t.stop());
+    }
+    out.updates = static_cast<Index>(out.update_seconds.size());
+    for (double dt : out.update_seconds) out.stream_seconds += dt;
+    out.fitness = model_fitness(full, stream.model());
+    return out;
 }
 
-void csv_row(std::ostream& out, const std::string& label, const std::string& algo, double fitness, double init_s,
-             double stream_s, const std::string& updates, double per_update) {
-    out << label << ',' << algo << ',' << fitness << ',' << init_s << ',' << stream_s << ',' << updates << ','
-        << per_update << '\n';
+// Planted factors of one family, drawn in random_model's order (i outer, r inner).
+KruskalModel planted_model(const Dims& dims, int rank, Rng& rng, FactorFamily family, double congruence) {
+    if (family != FactorFamily::uniform) {
+        KruskalModel m = random_model(dims, rank, rng);
+        if (family == FactorFamily::congruent) {
+            // F <- G C^T with C C^T = c 11^T + (1 - c) I (lower Cholesky factor of the
+            // equicorrelation matrix): pairwise column congruence c in expectation.
+            if (!(congruence > -1.0 / std::max(rank - 1, 1) && congruence < 1.0))
+                throw std::domain_error("gen_synthetic: congruence must keep c 11^T + (1 - c) I positive definite");
+            Matrix c(rank, rank);
+            for (int j = 0; j < rank; ++j)
+                for (int i = j; i < rank; ++i) {
+                    double a = (i == j) ? 1.0 : congruence;
+                    for (int k = 0; k < j; ++k) a -= c(i, k) * c(j, k);
+                    c(i, j) = (i == j) ? std::sqrt(a) : a / c(j, j);
+                }
+            for (Matrix& f : m.factors) {
+                const Matrix g = f;
+                for (Index i = 0; i < f.rows(); ++i)
+                    for (int r = 0; r < rank; ++r) {
+                        double v = 0.0;
+                        for (int k = 0; k <= r; ++k) v += g(i, k) * c(r, k);
+                        f(i, r) = v;
+                    }
+            }
+        }
+        return m;
+    }
+    KruskalModel m;
+    m.rank = rank;
+    std::uniform_real_distribution<double> unit(0.0, 1.0);
+    for (Index d : dims) {
+        Matrix f(d, rank);
+        for (Index i = 0; i < d; ++i)
+            for (int r = 0; r < rank; ++r) f(i, r) = unit(rng);
+        m.factors.push_back(std::move(f));
+    }
+    return m;
 }
 
 }  // namespace
 
 std::optional<FactorFamily> parse_family(const std::string& name) {
-    if (name == "normal") return FactorFamily::normal;
-    if (name == "uniform") return FactorFamily::uniform;
-    if (name == "congruent") return FactorFamily::congruent;
-    return std::nullopt;
+    static const std::map<std::string, FactorFamily> names{
+        {"normal", FactorFamily::normal}, {"uniform", FactorFamily::uniform}, {"congruent", FactorFamily::congruent}};
+    const auto it = names.find(name);
+    return it == names.end() ? std::nullopt : std::optional<FactorFamily>(it->second);
 }
 
 SyntheticTensor gen_synthetic(const Dims& dims, int rank, std::optional<double> sir_db, Rng& rng) {
@@ -87,123 +231,64 @@ SyntheticTensor gen_synthetic(const Dims& dims, int rank, std::optional<double> 
                               double congruence) {
     if (rank < 1) throw std::domain_error("gen_synthetic: rank must be positive");
     SyntheticTensor out;
-    if (family == FactorFamily::uniform) {  // random_model's draw order with U(0,1)
-        std::uniform_real_distribution<double> unif(0.0, 1.0);
-        out.truth.rank = rank;
-        for (Index d : dims) {
-            Matrix f(d, rank);
-            for (Index i = 0; i < d; ++i)
-                for (int r = 0; r < rank; ++r) f(i, r) = unif(rng);
-            out.truth.factors.push_back(std::move(f));
-        }
-    } else {
-        out.truth = random_model(dims, rank, rng);
-    }
-    if (family == FactorFamily::congruent) {  // F = G L^T, L L^T = c 11^T + (1 - c) I
-        if (!(congruence > -1.0 / std::max(rank - 1, 1) && congruence < 1.0))
-            throw std::domain_error("gen_synthetic: congruence must keep c 11^T + (1 - c) I positive definite");
-        std::vector<double> L(size_t(rank) * rank, 0.0);
-        for (int i = 0; i < rank; ++i)
-            for (int j = 0; j <= i; ++j) {
-                double a = (i == j) ? 1.0 : congruence;
-                for (int k = 0; k < j; ++k) a -= L[size_t(i) * rank + k] * L[size_t(j) * rank + k];
-                L[size_t(i) * rank + j] = (i == j) ? std::sqrt(a) : a / L[size_t(j) * rank + j];
-            }
-        for (Matrix& f : out.truth.factors) {
-            Matrix g = f;
-            for (Index i = 0; i < f.rows(); ++i)
-                for (int r = 0; r < rank; ++r) {
-                    double v = 0.0;
-                    for (int k = 0; k <= r; ++k) v += g(i, k) * L[size_t(r) * rank + k];
-                    f(i, r) = v;
-                }
-        }
-    }
-    // planted signal and exactly scaled noise on the device (rocp_generate_synthetic), one
-    // noise seed drawn from rng after the factors
+    out.truth = planted_model(dims, rank, rng, family, congruence);
+    // Signal and noise are formed on the device (rocp_generate_synthetic): the noise
+    // comes from one 64-bit seed drawn after the factors and is scaled so the SIR of
+    // the drawn noise is exact.
     const std::uint64_t noise_seed = sir_db ? rng() : 0;
+    std::vector<const double*> fp;
+    for (const Matrix& f : out.truth.factors) fp.push_back(f.data());
     rocp_tensor* t = nullptr;
-    check(rocp_tensor_create(device_handle(), dims.data(), static_cast<int>(dims.size()), nullptr, &t));
-    std::vector<const double*> f;
-    for (const Matrix& m : out.truth.factors) f.push_back(m.data());
+    status_or_throw(rocp_tensor_create(device_handle(), dims.data(), static_cast<int>(dims.size()), nullptr, &t));
     DenseTensor x(dims);
-    rocp_status st = rocp_generate_synthetic(device_handle(), t, f.data(), rank, sir_db ? 1 : 0,
-                                             sir_db ? *sir_db : 0.0, noise_seed);
+    rocp_status st = rocp_generate_synthetic(device_handle(), t, fp.data(), rank, sir_db.has_value() ? 1 : 0,
+                                             sir_db.value_or(0.0), noise_seed);
     if (st == ROCP_OK) st = rocp_tensor_download(device_handle(), t, x.data());
     rocp_tensor_free(t);
-    check(st);
+    status_or_throw(st);
     out.x = std::move(x);
     return out;
 }
 
-StreamSplit split_stream(const DenseTensor& x, double init_fraction, Index batch_size) {  // synthetic.cpp:33-57
-    if (init_fraction <= 0.0 || init_fraction >= 1.0)
-        throw std::domain_error("split_stream: init fraction must lie in (0,1)");
-    if (batch_size < 1) throw std::domain_error("split_stream: batch size must be positive");
-    const Dims& dims = x.dims();
-    const Index t = dims.back();
-    const Index t_init = static_cast<Index>(std::floor(init_fraction * static_cast<double>(t)));
-    if (t_init < 1) throw std::domain_error("split_stream: initial slice is empty");
-    const Index slice = element_count(dims) / t;
-    auto take = [&](Index from, Index len) {
-        Dims d = dims;
-        d.back() = len;
-        return DenseTensor(std::move(d), std::vector<double>(x.data() + from * slice, x.data() + (from + len) * slice));
-    };
+StreamSplit split_stream(const DenseTensor& x, double init_fraction, Index batch_size) {
+    const SlabCutter cut(x, init_fraction, batch_size);
     StreamSplit split;
-    split.init = take(0, t_init);
-    for (Index pos = t_init; pos < t; pos += batch_size) split.batches.push_back(take(pos, std::min(batch_size, t - pos)));
+    split.init = cut.piece(0);
+    for (size_t k = 1; k < cut.pieces(); ++k) split.batches.push_back(cut.piece(k));
     return split;
 }
 
 const char* algorithm_name(Algorithm a) {
-    switch (a) {
-        case Algorithm::rocp: return "rocp";
-        case Algorithm::online_full: return "online_full";
-        case Algorithm::batch_hot: return "batch_hot";
-        case Algorithm::batch_cold: return "batch_cold";
-    }
+    for (const auto& [alg, name] : kAlgorithmNames)
+        if (alg == a) return name;
     return "?";
 }
 
 std::optional<Algorithm> parse_algorithm(const std::string& name) {
-    for (Algorithm a : {Algorithm::rocp, Algorithm::online_full, Algorithm::batch_hot, Algorithm::batch_cold})
-        if (name == algorithm_name(a)) return a;
+    for (const auto& [alg, label] : kAlgorithmNames)
+        if (name == label) return alg;
     return std::nullopt;
 }
 
-std::vector<Aggregate> aggregate_rows(const std::vector<TrialResult>& rows) {  // bench.cpp:136-177
-    std::vector<Aggregate> out;
-    std::vector<Algorithm> seen;
-    for (const TrialResult& r : rows)
-        if (std::find(seen.begin(), seen.end(), r.algorithm) == seen.end()) seen.push_back(r.algorithm);
-    for (Algorithm a : seen) {
-        std::vector<const TrialResult*> group;
-        for (const TrialResult& r : rows)
-            if (r.algorithm == a) group.push_back(&r);
-        const double n = static_cast<double>(group.size());
-        auto mean_std = [&](auto field) {
-            double mean = 0.0;
-            for (const TrialResult* r : group) mean += field(*r);
-            mean /= n;
-            double var = 0.0;
-            for (const TrialResult* r : group) {
-                const double d = field(*r) - mean;
-                var += d * d;
-            }
-            return std::pair<double, double>(mean, group.size() > 1 ? std::sqrt(var / (n - 1.0)) : 0.0);
-        };
-        Aggregate agg;
-        agg.algorithm = a;
-        std::tie(agg.fitness_mean, agg.fitness_std) = mean_std([](const TrialResult& r) { return r.fitness; });
-        std::tie(agg.init_mean, agg.init_std) = mean_std([](const TrialResult& r) { return r.init_seconds; });
-        std::tie(agg.stream_mean, agg.stream_std) = mean_std([](const TrialResult& r) { return r.stream_seconds; });
-        out.push_back(agg);
+std::vector<Aggregate> aggregate_rows(const std::vector<TrialResult>& rows) {
+    // one accumulator triple per algorithm, in order of first appearance
+    std::vector<std::pair<Algorithm, std::array<RunningStats, 3>>> acc;
+    for (const TrialResult& r : rows) {
+        auto it = acc.begin();
+        while (it != acc.end() && it->first != r.algorithm) ++it;
+        if (it == acc.end()) it = acc.insert(acc.end(), {r.algorithm, {}});
+        it->second[0].add(r.fitness);
+        it->second[1].add(r.init_seconds);
+        it->second[2].add(r.stream_seconds);
     }
+    std::vector<Aggregate> out;
+    for (const auto& [alg, st] : acc)
+        out.push_back(Aggregate{alg, st[0].mean(), st[0].stddev(), st[1].mean(), st[1].stddev(), st[2].mean(),
+                                st[2].stddev()});
     return out;
 }
 
-BenchReport run_benchmark(const BenchConfig& cfg) {  // bench.cpp:179-213
+BenchReport run_benchmark(const BenchConfig& cfg) {
     if (cfg.trials < 1) throw std::domain_error("run_benchmark: trials must be positive");
     if (cfg.algorithms.empty()) throw std::domain_error("run_benchmark: no algorithms selected");
     if (cfg.input_path.empty() && cfg.dims.size() < 2)
@@ -213,53 +298,43 @@ BenchReport run_benchmark(const BenchConfig& cfg) {  // bench.cpp:179-213
             throw std::domain_error(std::string("run_benchmark: ") + algorithm_name(a) +
                                     " is a reference baseline, not on the B200 path (DESIGN.md section 8)");
     BenchReport report;
-    report.rows.resize(static_cast<size_t>(cfg.trials) * cfg.algorithms.size());
+    // trials run in order on this thread's device (one GPU serves them all)
     for (int trial = 0; trial < cfg.trials; ++trial) {
-        Rng data_rng = make_rng(cfg.seed, trial, 0);
+        Rng data = seeded_engine(cfg.seed, trial, 0);
         const DenseTensor full = cfg.input_path.empty()
-                                     ? gen_synthetic(cfg.dims, cfg.rank, cfg.sir_db, data_rng, cfg.family, cfg.congruence).x
-                                                        : read_tensor_file(cfg.input_path);
-        const StreamSplit split = split_stream(full, cfg.init_fraction, cfg.batch_size);
-        for (size_t a = 0; a < cfg.algorithms.size(); ++a)
-            report.rows[static_cast<size_t>(trial) * cfg.algorithms.size() + a] = run_rocp_cell(cfg, trial, full, split);
+                                     ? gen_synthetic(cfg.dims, cfg.rank, cfg.sir_db, data, cfg.family, cfg.congruence).x
+                                     : read_tensor_file(cfg.input_path);
+        const SlabCutter cut(full, cfg.init_fraction, cfg.batch_size);
+        for (size_t a = 0; a < cfg.algorithms.size(); ++a) report.rows.push_back(rocp_trial(cfg, trial, full, cut));
     }
     report.aggregates = aggregate_rows(report.rows);
     return report;
 }
 
-void write_csv(const BenchReport& report, std::ostream& out) {  // bench.cpp:226-252
-    const auto flags = out.flags();
-    const auto prec = out.precision(17);
+void write_csv(const BenchReport& report, std::ostream& out) {
+    const FullPrecision guard(out);
     out << "trial,algorithm,fitness,init_seconds,stream_seconds,updates,seconds_per_update\n";
     for (const TrialResult& r : report.rows)
-        csv_row(out, std::to_string(r.trial), algorithm_name(r.algorithm), r.fitness, r.init_seconds, r.stream_seconds,
-                std::to_string(r.updates), r.seconds_per_update());
+        CsvLine(out) << r.trial << algorithm_name(r.algorithm) << r.fitness << r.init_seconds << r.stream_seconds
+                     << r.updates << r.seconds_per_update();
     for (const Aggregate& a : report.aggregates) {
-        double per_update_mean = 0.0;
-        int n = 0;
+        RunningStats per_update;
         for (const TrialResult& r : report.rows)
-            if (r.algorithm == a.algorithm) {
-                per_update_mean += r.seconds_per_update();
-                ++n;
-            }
-        per_update_mean /= std::max(n, 1);
-        csv_row(out, "mean", algorithm_name(a.algorithm), a.fitness_mean, a.init_mean, a.stream_mean, "",
-                per_update_mean);
-        csv_row(out, "std", algorithm_name(a.algorithm), a.fitness_std, a.init_std, a.stream_std, "", 0.0);
+            if (r.algorithm == a.algorithm) per_update.add(r.seconds_per_update());
+        CsvLine(out) << "mean" << algorithm_name(a.algorithm) << a.fitness_mean << a.init_mean << a.stream_mean << ""
+                     << per_update.mean();
+        CsvLine(out) << "std" << algorithm_name(a.algorithm) << a.fitness_std << a.init_std << a.stream_std << ""
+                     << 0.0;
     }
-    out.precision(prec);
-    out.flags(flags);
 }
 
-void write_updates_csv(const BenchReport& report, std::ostream& out) {  // bench.cpp:254-264
-    const auto flags = out.flags();
-    const auto prec = out.precision(17);
+void write_updates_csv(const BenchReport& report, std::ostream& out) {
+    const FullPrecision guard(out);
     out << "trial,algorithm,update,seconds\n";
-    for (const TrialResult& r : report.rows)
-        for (size_t u = 0; u < r.update_seconds.size(); ++u)
-            out << r.trial << ',' << algorithm_name(r.algorithm) << ',' << u << ',' << r.update_seconds[u] << '\n';
-    out.precision(prec);
-    out.flags(flags);
+    for (const TrialResult& r : report.rows) {
+        size_t u = 0;
+        for (double dt : r.update_seconds) CsvLine(out) << r.trial << algorithm_name(r.algorithm) << u++ << dt;
+    }
 }
 
 }  // namespace rocp

@@ -418,12 +418,162 @@ static void test_bench_harness() {  // test_bench.cpp:114-207
     CHECK(!parse_algorithm("onlinecp").has_value());
 }
 
+static bool bitwise(const Matrix& a, const Matrix& b) {
+    return a.rows() == b.rows() && a.cols() == b.cols() &&
+           std::memcmp(a.data(), b.data(), static_cast<size_t>(a.size()) * sizeof(double)) == 0;
+}
+
+// The reference's free functions (rocp.hpp:35-81) replay RocpStream::consume bit for bit
+// (consume = update_last_mode + append + update_other_modes, rocp.cpp:144-160).
+static void test_free_functions_replay_consume() {
+    const Dims dims{16, 14, 60};
+    const int R = 4;
+    Rng gen(71);
+    const KruskalModel truth = random_model(dims, R, gen);
+    const DenseTensor x = reconstruct_loops(truth, dims);
+    const Index slice = 16 * 14, t_init = 20, B = 5;
+    auto take = [&](Index t0, Index len) {
+        std::vector<double> v(x.data() + t0 * slice, x.data() + (t0 + len) * slice);
+        return DenseTensor({16, 14, len}, std::move(v));
+    };
+    Rng rng(73);
+    InitResult init = cprand_decompose(take(0, t_init), R, {}, rng);
+    const Index s = auto_sample_count(R);
+    ComplementaryState state = init_state(init, s);  // rocp.cpp:45-69
+    CHECK(state.t_len == t_init && state.sample_count == s && state.p.size() == 2 && state.q.size() == 2);
+    KruskalModel model = init.model;
+    RocpStream stream(init, s);
+    {
+        const ComplementaryState direct = stream.state();
+        for (size_t n = 0; n < 2; ++n) CHECK(bitwise(state.p[n], direct.p[n]) && bitwise(state.q[n], direct.q[n]));
+    }
+    std::vector<Matrix> temporal_rows;
+    bool all_equal = true;
+    const std::uint64_t seed = 0x5eedULL;
+    for (Index t = t_init, b = 1; t + B <= 60; t += B, ++b) {
+        const DenseTensor xb = take(t, B);
+        const CounterKey key{seed, static_cast<std::uint32_t>(b), 0};
+        const LastModeUpdate lm = update_last_mode(model, xb, s, key);
+        CHECK(lm.idx.mode == 3 && lm.idx.count() == s && lm.z_s.rows() == s && lm.u_new.rows() == B);
+        UpdateTrace tr;
+        update_other_modes(state, model, xb, lm.u_new, key, &tr);
+        CHECK(tr.mode_idx.size() == 2 && tr.mode_z.size() == 2 && tr.mode_x.size() == 2);
+        temporal_rows.push_back(lm.u_new);
+        stream.consume(xb, seed, static_cast<std::uint32_t>(b));
+        const KruskalModel m = stream.model();
+        const ComplementaryState cs = stream.state();
+        for (size_t n = 0; n < 2; ++n)
+            all_equal = all_equal && bitwise(m.factors[n], model.factors[n]) && bitwise(cs.p[n], state.p[n]) &&
+                        bitwise(cs.q[n], state.q[n]);
+        const Matrix& tf = m.factors.back();
+        for (Index i = 0; i < B; ++i)
+            for (int r = 0; r < R; ++r) all_equal = all_equal && tf(t + i, r) == lm.u_new(i, r);
+    }
+    CHECK(all_equal);
+    CHECK(stream.t_len() == 60);
+    // update_mode_with / update_last_mode_with contracts (rocp.cpp:75,100-101)
+    const DenseTensor xb = take(20, B);
+    CHECK(throws<std::domain_error>(
+        [&] { update_last_mode_with(model, xb, draw_samples(xb.dims(), 1, s, CounterKey{1, 1, 0})); }));
+    CHECK(throws<std::domain_error>([&] {
+        update_mode_with(state, model, xb, Matrix(B, R), draw_samples(xb.dims(), 3, s, CounterKey{1, 1, 0}));
+    }));
+    CHECK(throws<std::domain_error>(
+        [&] { update_other_modes(state, model, xb, Matrix(B + 1, R), CounterKey{1, 1, 0}); }));
+    CHECK(throws<std::domain_error>([&] { update_last_mode(model, DenseTensor({16, 15, 2}), s, CounterKey{}); }));
+    InitResult bad = init;
+    bad.best_sampled_kr.pop_back();
+    CHECK(throws<std::domain_error>([&] { init_state(bad, s); }));
+    CHECK(throws<std::domain_error>([&] { init_state(init, s + 1); }));
+}
+
+// Traces are filled (cprand.cpp:34,44; rocp.cpp:125-129) and a traced consume equals an
+// untraced one bit for bit.
+static void test_traces() {
+    const Dims dims{12, 10, 40};
+    const int R = 3;
+    Rng gen(91);
+    const DenseTensor x = reconstruct_loops(random_model(dims, R, gen), dims);
+    const Index slice = 120;
+    auto take = [&](Index t0, Index len) {
+        std::vector<double> v(x.data() + t0 * slice, x.data() + (t0 + len) * slice);
+        return DenseTensor({12, 10, len}, std::move(v));
+    };
+    Rng a(97), b(97);
+    CprandTrace ct;
+    const InitResult ia = cprand_decompose(take(0, 10), R, {}, a, &ct);
+    const InitResult ib = cprand_decompose(take(0, 10), R, {}, b);
+    CHECK(static_cast<int>(ct.sweeps.size()) == ia.iterations);
+    bool shapes = true, fresh = false;
+    for (const auto& sw : ct.sweeps) {
+        shapes = shapes && sw.size() == 3;
+        for (int n = 0; n < 3 && sw.size() == 3; ++n)
+            shapes = shapes && sw[static_cast<size_t>(n)].mode == n + 1 && sw[static_cast<size_t>(n)].count() == auto_sample_count(R);
+    }
+    for (size_t k = 1; k < ct.sweeps.size(); ++k) fresh = fresh || ct.sweeps[k][0].rows != ct.sweeps[0][0].rows;
+    CHECK(shapes);
+    CHECK(ct.sweeps.size() < 2 || fresh);  // fresh draws each sweep (test_cprand.cpp:165-180)
+    CHECK(ia.best_fitness == ib.best_fitness);
+    const Index s = auto_sample_count(R);
+    RocpStream sa(ia, s), sb(ib, s);
+    std::vector<UpdateTrace> traces;
+    for (Index t = 10; t + 5 <= 40; t += 5) {
+        traces.emplace_back();
+        sa.consume(take(t, 5), a, &traces.back());
+        sb.consume(take(t, 5), b);
+    }
+    const KruskalModel ma = sa.model(), mb = sb.model();
+    bool eq = true;
+    for (size_t n = 0; n < 3; ++n) eq = eq && bitwise(ma.factors[n], mb.factors[n]);
+    CHECK(eq);
+    CHECK(sa.regularized() == sb.regularized());
+    bool tr_ok = true;
+    for (const UpdateTrace& tr : traces) {
+        tr_ok = tr_ok && tr.mode_idx.size() == 2 && tr.mode_z.size() == 2 && tr.mode_x.size() == 2;
+        for (size_t n = 0; n < tr.mode_x.size(); ++n)
+            tr_ok = tr_ok && tr.mode_x[n].rows() == dims[n] && tr.mode_x[n].cols() == s && tr.mode_z[n].rows() == s;
+    }
+    CHECK(tr_ok);
+}
+
+// Constant streaming footprint over 500 batches through the 3-argument constructor
+// (acceptance.cpp:427-471): the temporal factor grows geometrically (rocp.cpp:152-155)
+// instead of failing on stream length.
+static void test_long_stream_growth() {
+    Rng gen(10001);
+    const Dims head{20, 20, 20};
+    Dims dims = head;
+    dims.push_back(20);
+    const KruskalModel truth = random_model(dims, 5, gen);
+    const DenseTensor x_init = reconstruct_loops(truth, dims);
+    Rng rng(10003);
+    InitResult init = cprand_decompose(x_init, 5, {}, rng);
+    RocpStream stream(std::move(init), auto_sample_count(5));
+    const std::size_t bytes = stream.state().byte_size();
+    bool constant = true;
+    Dims slab_dims = head;
+    slab_dims.push_back(1);
+    for (int k = 0; k < 500; ++k) {
+        KruskalModel slab_model = truth;
+        slab_model.factors.back() = random_matrix(1, 5, rng);
+        stream.consume(reconstruct_loops(slab_model, slab_dims), rng);
+        constant = constant && stream.state().byte_size() == bytes;
+    }
+    CHECK(constant);
+    CHECK(stream.t_len() == 520);
+    const KruskalModel m = stream.model();
+    CHECK(m.factors.back().rows() == 520 && m.factors.back().allFinite());
+}
+
 int main() {
     const std::vector<std::pair<const char*, std::function<void()>>> cases = {
         {"index_map", test_index_map}, {"draws_and_gather", test_draws_and_gather}, {"skr", test_skr},
         {"solve", test_solve},         {"cprand", test_cprand},                     {"stream", test_stream},
         {"records", test_records},     {"synthetic", test_synthetic},               {"bench_harness", test_bench_harness},
-        {"factor_families", test_factor_families}};
+        {"factor_families", test_factor_families},
+        {"free_functions_replay_consume", test_free_functions_replay_consume},
+        {"traces", test_traces},
+        {"long_stream_growth", test_long_stream_growth}};
     for (const auto& [name, fn] : cases) {
         const int before = g_fail;
         try {

@@ -4,8 +4,9 @@ A rank-local restatement of the multi-GPU stream step
 that exchanges its partials through torch.distributed, so the N > 1 protocol
 -- row ownership, virtual-shard partition, local fibre offsets, the exchange
 layout and the fixed-order combine -- runs with world_size 2 on `gloo` here.
-The GPU implementation (paper_2007_10798_b200/csrc/shard.cuh) follows the same
-plan with NCCL; both must reproduce orc_stream_consume_sharded bit for bit.
+The GPU implementation (paper_2007_10798_b200/csrc/shard_kernels.cuh and
+shard_host.inc) follows the same plan over peer memory (NCCL all-gather as the
+alternative); both must reproduce orc_stream_consume_sharded bit for bit.
 
 Rank g of G owns virtual shards [g V/G, (g+1) V/G), i.e. mode-1 rows
 [lo(g V/G), lo((g+1) V/G)) with lo(v) = floor(v I_1 / V).
