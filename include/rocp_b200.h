@@ -70,6 +70,16 @@ rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms);
  * Results are bitwise identical for every setting.  No reference counterpart
  * (a B200 scheduling knob). */
 rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms);
+/* Measurement aid (no reference counterpart): event-timed kernel of `reads`
+ * independent 8-byte loads at hashed offsets of t on every SM -- the device's
+ * isolated random-read ceiling that bounds the strided sampled-fibre gather
+ * (DESIGN.md section 5).  *ms = the timed launch (after one warm-up launch). */
+rocp_status rocp_probe_random_reads(rocp_dev* dev, const rocp_tensor* t, int64_t reads, uint64_t seed, float* ms);
+/* solve_gram regularisation decisions taken on this device since the last reset
+ * (DESIGN.md 3.4): counts[0] no regularisation, [1] regularised, [2] settled by
+ * exact (Jacobi) eigenvalues, [3] needed the tier-2 tr(G^-1) certificate.
+ * Diagnostic (no reference counterpart). */
+rocp_status rocp_decision_stats(rocp_dev* dev, uint64_t* counts, int reset);
 /* The handle's cudaStream_t (for callers that interoperate). */
 void* rocp_cuda_stream(rocp_dev* dev);
 /* Page-locked, CUDA-registered host buffer backed by 2 MB (transparent huge)

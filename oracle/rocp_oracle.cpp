@@ -11,10 +11,13 @@
 #include "rocp_oracle.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -256,12 +259,14 @@ Ldl ldlt(const std::vector<double>& a_in, int R) {
 // The reference decides from the exact eigenvalues of G (SelfAdjointEigenSolver):
 // zero solution if lambda_max <= 0, regularise if lambda_min <= 0 or
 // lambda_max / lambda_min > 1e12.  The canonical form reaches the
-// same decision without an eigensolver whenever a rigorous certificate settles it:
-//   * pivots: for SPD G every LDL^T pivot lies in [lambda_min, lambda_max], so
-//     dmax / dmin <= kappa;
-//   * tau = tr(G^-1) = sum_k |row k of L^-1|^2 / d_k, with
-//     lambda_max <= tr(G) and tr(G^-1) / R <= 1 / lambda_min <= tr(G^-1):
-//     maxdiag * tau / R <= kappa <= tr(G) * tau.
+// same decision without an eigensolver whenever a rigorous certificate settles it
+// (pivots d_k > 0 of G = L D L^T):
+//   * lower bound: every pivot of an SPD matrix lies in [lambda_min, lambda_max],
+//     so dmax / dmin <= kappa;
+//   * upper bound: lambda_max <= |G|_inf (max absolute row sum) and
+//     1 / lambda_min = |L^-T D^-1 L^-1|_2 <= |L^-1|_2^2 / dmin <= R |L^-1|_inf^2 / dmin,
+//     with |L^-1|_inf <= max_i y_i, y = (I - |N|)^-1 1 for L = I - N (|L^-1| <= (I - |N|)^-1
+//     entrywise): y_i = 1 + sum_{k<i} |l_ik| y_k, one forward substitution.
 // kappa certainly above 4e12 -> regularise; certainly below 2.5e11 -> not; a
 // non-positive max diagonal or pivot, or anything in between -> exact
 // eigenvalues by a deterministic cyclic Jacobi method (the kernels run the same
@@ -270,98 +275,224 @@ constexpr double kCertRegAbove = 4e12;
 constexpr double kCertNoRegBelow = 2.5e11;
 enum { kDecNoReg = 0, kDecReg = 1, kDecExact = 2 };
 
-// 32-lane xor butterfly (q = q + q[lane ^ off], off = 16..1), as the kernels' butterfly32.
-double butterfly_lanes(std::vector<double> v) {
+double max_of(double a, double b) { return (b > a) ? b : a; }
+
+// 32-lane xor butterfly max (v = max(v, v[lane ^ off]), off = 16..1), the kernels' order.
+double butterfly_max_lanes(std::vector<double> v) {
     v.resize(32, 0.0);
     for (int off = 16; off >= 1; off >>= 1) {
         std::vector<double> w(32);
-        for (int l = 0; l < 32; ++l) w[size_t(l)] = v[size_t(l)] + v[size_t(l ^ off)];
+        for (int l = 0; l < 32; ++l) w[size_t(l)] = max_of(v[size_t(l)], v[size_t(l ^ off)]);
         v = w;
     }
     return v[0];
 }
 
-// tau = tr(G^-1) from the factorization: column j of M = L^-1 on lane j % 32 of warp
-// j / 32 (forward substitution, updates in k order), c_j = sum_k fma(M_kj^2, 1/d_k),
-// a butterfly per warp, then warp 0 + warp 1.
-double cert_tau(const Ldl& f, int R) {
-    std::vector<double> dinv(static_cast<size_t>(R));
-    for (int k = 0; k < R; ++k) dinv[size_t(k)] = 1.0 / f.d[size_t(k)];
-    std::vector<double> c(64, 0.0);
-    std::vector<double> m(static_cast<size_t>(R));
-    for (int j = 0; j < R; ++j) {
-        for (int i = 0; i < R; ++i) m[size_t(i)] = (i == j) ? 1.0 : 0.0;
-        for (int k = 0; k + 1 < R; ++k) {
-            const double mk = m[size_t(k)];
-            for (int i = k + 1; i < R; ++i)
-                m[size_t(i)] = std::fma(-f.l[size_t(i + k * R)], mk, m[size_t(i)]);
-        }
-        double acc = 0.0;
-        for (int k = 0; k < R; ++k) {
-            const double q = m[size_t(k)] * m[size_t(k)];
-            acc = std::fma(q, dinv[size_t(k)], acc);
-        }
-        c[size_t(j)] = acc;
+// Lane values of a row quantity r_i (rows i and i + 32 on lane i, 0 past R), max-combined.
+double lanes_max(const std::vector<double>& r, int R) {
+    std::vector<double> v(32, 0.0);
+    for (int l = 0; l < 32; ++l) {
+        double a = (l < R) ? r[size_t(l)] : 0.0;
+        if (l + 32 < R) a = max_of(a, r[size_t(l + 32)]);
+        v[size_t(l)] = a;
     }
-    const double t0 = butterfly_lanes(std::vector<double>(c.begin(), c.begin() + 32));
-    const double t1 = butterfly_lanes(std::vector<double>(c.begin() + 32, c.end()));
-    return t0 + t1;
+    return butterfly_max_lanes(v);
 }
 
-int certificate(double maxdiag, double tr, const Ldl& f, int R, double* tau_out) {
+// max_i y_i, y_i = 1 + sum_{k<i} |l_ik| y_k: lane i's fma chain in k order.
+double cert_ymax(const Ldl& f, int R) {
+    std::vector<double> y(static_cast<size_t>(R), 1.0);
+    for (int k = 0; k + 1 < R; ++k) {
+        const double yk = y[size_t(k)];
+        for (int i = k + 1; i < R; ++i) y[size_t(i)] = std::fma(std::fabs(f.l[size_t(i + k * R)]), yk, y[size_t(i)]);
+    }
+    return lanes_max(y, R);
+}
+
+// tau = tr(G^-1) = sum_i (sum_j M_ij^2) / d_i from the factorization (M = L^-1),
+// in the kernels' order: columns in groups of 8 (group g = columns 8g..8g+7, one
+// warp, lane i owning rows i and i + 32); each column by forward substitution
+// (updates in k order; the steps k < j leave column j unchanged); per row a
+// group partial p_gi = fma chain over the group's columns; s_i = p_0i + p_1i + ...;
+// t_i = s_i / d_i; v_lane = t_lane + t_{lane+32} (+0 past R); a 32-lane butterfly sum.
+double cert_tau(const Ldl& f, int R) {
+    const int ng = (R + 7) / 8;
+    std::vector<double> s(64, 0.0);
+    std::vector<double> m(static_cast<size_t>(R));
+    for (int g = 0; g < ng; ++g) {
+        std::vector<double> p(static_cast<size_t>(R), 0.0);
+        for (int j = 8 * g; j < std::min(R, 8 * g + 8); ++j) {
+            for (int i = 0; i < R; ++i) m[size_t(i)] = (i == j) ? 1.0 : 0.0;
+            for (int k = 0; k + 1 < R; ++k) {
+                const double mk = m[size_t(k)];
+                for (int i = k + 1; i < R; ++i)
+                    m[size_t(i)] = std::fma(-f.l[size_t(i + k * R)], mk, m[size_t(i)]);
+            }
+            for (int i = 0; i < R; ++i) p[size_t(i)] = std::fma(m[size_t(i)], m[size_t(i)], p[size_t(i)]);
+        }
+        for (int i = 0; i < R; ++i) s[size_t(i)] = (g == 0) ? p[size_t(i)] : s[size_t(i)] + p[size_t(i)];
+    }
+    std::vector<double> v(32, 0.0);
+    for (int l = 0; l < 32; ++l) {
+        const double t0 = (l < R) ? s[size_t(l)] / f.d[size_t(l)] : 0.0;
+        const double t1 = (l + 32 < R) ? s[size_t(l + 32)] / f.d[size_t(l + 32)] : 0.0;
+        v[size_t(l)] = t0 + t1;
+    }
+    std::vector<double> w = v;
+    for (int off = 16; off >= 1; off >>= 1) {
+        std::vector<double> u(32);
+        for (int l = 0; l < 32; ++l) u[size_t(l)] = w[size_t(l)] + w[size_t(l ^ off)];
+        w = u;
+    }
+    return w[0];
+}
+
+// |G|_inf: row i's absolute sum in column order, max over rows.
+double gram_inf_norm(const std::vector<double>& g, int R) {
+    std::vector<double> rs(static_cast<size_t>(R), 0.0);
+    for (int i = 0; i < R; ++i) {
+        double a = 0.0;
+        for (int j = 0; j < R; ++j) a = a + std::fabs(g[size_t(i + j * R)]);
+        rs[size_t(i)] = a;
+    }
+    return lanes_max(rs, R);
+}
+
+int64_t g_decision_paths[4] = {0, 0, 0, 0};  // test statistics (orc_decision_stats); [3]: tier 2 used
+
+// Tier 1 (every Gram, folded into the factorization on the device): pivots and ymax.
+// Tier 2 (only when tier 1 leaves the band, i.e. kappa within a few decades of the
+// limit): tau = tr(G^-1), maxdiag tau / R <= kappa <= |G|_inf tau.  Tier 3: Jacobi.
+int certificate(double maxdiag, double gnorm, const Ldl& f, int R) {
     double dmin = f.d[0], dmax = f.d[0];
     for (double x : f.d) {
         if (x < dmin) dmin = x;
         if (x > dmax) dmax = x;
     }
     if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
-    const double tau = cert_tau(f, R);
-    if (tau_out) *tau_out = tau;
     const double ratio = dmax / dmin;
-    const double klo = (maxdiag * tau) / double(R);
-    const double khi = tr * tau;
-    if (ratio > kCertRegAbove || klo > kCertRegAbove) return kDecReg;
+    if (ratio > kCertRegAbove) return kDecReg;
+    const double ym = cert_ymax(f, R);
+    const double khi = ((gnorm / dmin) * double(R)) * (ym * ym);
     if (khi <= kCertNoRegBelow) return kDecNoReg;
+    ++g_decision_paths[3];
+    const double tau = cert_tau(f, R);
+    const double klo2 = (maxdiag * tau) / double(R);
+    const double khi2 = gnorm * tau;
+    if (klo2 > kCertRegAbove) return kDecReg;
+    if (khi2 <= kCertNoRegBelow) return kDecNoReg;
     return kDecExact;
 }
 
-// Deterministic cyclic Jacobi eigenvalues of a symmetric R x R matrix (column-major;
-// destroyed).  Rotation (p, q) in row-cyclic order, skipped when |a_pq| <= eps
-// sqrt(|a_pp a_qq|); sweeps until one rotates nothing (at most 64).  Rutishauser's
-// update; every element's operation sequence is fixed (the kernels update the k
-// entries in parallel with the same expressions).
+// Deterministic parallel (round-robin) Jacobi eigenvalues of a symmetric R x R
+// matrix (column-major; destroyed).  Indices 0..n-1 (n = R rounded up to even; an
+// odd R gets a dummy index that never rotates) meet in n - 1 rounds per sweep by
+// the circle method: round r pairs (r, n-1) and ((r+k) mod (n-1), (r-k) mod (n-1)),
+// k = 1..n/2-1.  Per pair: skip when |a_pq| <= eps sqrt(|a_pp a_qq|), else
+// Rutishauser's (t, c, s).  The round applies A <- J^T A J for the block-diagonal J
+// of its rotations: each 2 x 2 block (P, Q), P <= Q, rows transformed by pair P
+// first, then columns by pair Q, mirrored to (Q, P); a rotated diagonal block
+// becomes diag(a_pp - t a_pq, a_qq + t a_pq).  Sweeps until one rotates nothing
+// (at most 64).  The kernels give every block pair of a round to its own thread with
+// the same expressions, so the eigenvalues are bitwise shared.
+void jacobi_pair(int r, int k, int n, int* p, int* q) {
+    int a, b;
+    if (k == 0) {
+        a = r;
+        b = n - 1;
+    } else {
+        a = (r + k) % (n - 1);
+        b = (r - k + (n - 1)) % (n - 1);
+    }
+    *p = std::min(a, b);
+    *q = std::max(a, b);
+}
+
 void jacobi_eigen(std::vector<double>& a, int R, double* lo, double* hi) {
     auto at = [&](int i, int j) -> double& { return a[size_t(i + j * R)]; };
-    for (int sweep = 0; sweep < 64; ++sweep) {
-        bool rotated = false;
-        for (int p = 0; p + 1 < R; ++p)
-            for (int q = p + 1; q < R; ++q) {
+    const int n = R + (R & 1), np = n / 2;
+    std::vector<int> pp(static_cast<size_t>(np)), qq(static_cast<size_t>(np));
+    std::vector<double> cc(static_cast<size_t>(np)), ss(static_cast<size_t>(np)), tt(static_cast<size_t>(np));
+    std::vector<char> rot(static_cast<size_t>(np));
+    for (int sweep = 0; sweep < 64 && R > 1; ++sweep) {
+        bool any = false;
+        for (int r = 0; r + 1 < n; ++r) {
+            for (int k = 0; k < np; ++k) {
+                int p, q;
+                jacobi_pair(r, k, n, &p, &q);
+                pp[size_t(k)] = p;
+                qq[size_t(k)] = q;
+                rot[size_t(k)] = 0;
+                if (q >= R) continue;  // the dummy index
                 const double apq = at(p, q), app = at(p, p), aqq = at(q, q);
                 const double thr = 2.220446049250313e-16 * std::sqrt(std::fabs(app) * std::fabs(aqq));
                 if (!(std::fabs(apq) > thr)) continue;
-                rotated = true;
                 const double theta = (aqq - app) / (2.0 * apq);
                 const double t = (std::fabs(theta) > 1e150)
                                      ? 0.5 / theta
                                      : ((theta >= 0.0) ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
                 const double c = 1.0 / std::sqrt(t * t + 1.0);
-                const double sn = t * c;
-                for (int k = 0; k < R; ++k) {
-                    if (k == p || k == q) continue;
-                    const double g = at(k, p), h = at(k, q);
-                    const double np = c * g - sn * h;
-                    const double nq = sn * g + c * h;
-                    at(k, p) = np;
-                    at(p, k) = np;
-                    at(k, q) = nq;
-                    at(q, k) = nq;
-                }
-                at(p, p) = app - t * apq;
-                at(q, q) = aqq + t * apq;
-                at(p, q) = 0.0;
-                at(q, p) = 0.0;
+                tt[size_t(k)] = t;
+                cc[size_t(k)] = c;
+                ss[size_t(k)] = t * c;
+                rot[size_t(k)] = 1;
+                any = true;
             }
-        if (!rotated) break;
+            // new blocks from the old matrix (a round's blocks are disjoint reads of `a`)
+            std::vector<double> nb = a;
+            auto nat = [&](int i, int j) -> double& { return nb[size_t(i + j * R)]; };
+            for (int P = 0; P < np; ++P)
+                for (int Q = P; Q < np; ++Q) {
+                    const int p = pp[size_t(P)], q = qq[size_t(P)], u = pp[size_t(Q)], v = qq[size_t(Q)];
+                    if (P == Q) {
+                        if (!rot[size_t(P)]) continue;
+                        const double apq = at(p, q), app = at(p, p), aqq = at(q, q), t = tt[size_t(P)];
+                        nat(p, p) = app - t * apq;
+                        nat(q, q) = aqq + t * apq;
+                        nat(p, q) = 0.0;
+                        nat(q, p) = 0.0;
+                        continue;
+                    }
+                    if (!rot[size_t(P)] && !rot[size_t(Q)]) continue;
+                    const bool qv = q < R, vv = v < R;
+                    double x_pu = at(p, u), x_pv = vv ? at(p, v) : 0.0;
+                    double x_qu = qv ? at(q, u) : 0.0, x_qv = (qv && vv) ? at(q, v) : 0.0;
+                    if (rot[size_t(P)]) {  // rows by pair P
+                        const double c = cc[size_t(P)], sn = ss[size_t(P)];
+                        const double y_pu = c * x_pu - sn * x_qu, y_qu = sn * x_pu + c * x_qu;
+                        const double y_pv = c * x_pv - sn * x_qv, y_qv = sn * x_pv + c * x_qv;
+                        x_pu = y_pu;
+                        x_qu = y_qu;
+                        x_pv = y_pv;
+                        x_qv = y_qv;
+                    }
+                    if (rot[size_t(Q)]) {  // then columns by pair Q
+                        const double c = cc[size_t(Q)], sn = ss[size_t(Q)];
+                        const double z_pu = c * x_pu - sn * x_pv, z_pv = sn * x_pu + c * x_pv;
+                        const double z_qu = c * x_qu - sn * x_qv, z_qv = sn * x_qu + c * x_qv;
+                        x_pu = z_pu;
+                        x_pv = z_pv;
+                        x_qu = z_qu;
+                        x_qv = z_qv;
+                    }
+                    nat(p, u) = x_pu;
+                    nat(u, p) = x_pu;
+                    if (vv) {
+                        nat(p, v) = x_pv;
+                        nat(v, p) = x_pv;
+                    }
+                    if (qv) {
+                        nat(q, u) = x_qu;
+                        nat(u, q) = x_qu;
+                    }
+                    if (qv && vv) {
+                        nat(q, v) = x_qv;
+                        nat(v, q) = x_qv;
+                    }
+                }
+            a.swap(nb);
+        }
+        if (!any) break;
     }
     double l = at(0, 0), h = at(0, 0);
     for (int k = 1; k < R; ++k) {
@@ -380,9 +511,10 @@ struct GramDecision {
     int path = 0;
 };
 
-GramDecision decide_gram(const std::vector<double>& g, int R, double maxdiag, double tr, const Ldl& f) {
+GramDecision decide_gram(const std::vector<double>& g, int R, double maxdiag, const Ldl& f) {
     GramDecision dec;
-    dec.path = certificate(maxdiag, tr, f, R, nullptr);
+    dec.path = certificate(maxdiag, gram_inf_norm(g, R), f, R);
+    ++g_decision_paths[dec.path];
     if (dec.path == kDecExact) {
         std::vector<double> a = g;
         double lo = 0.0, hi = 0.0;
@@ -433,7 +565,7 @@ Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path =
     double tr = gram(0, 0);
     for (int k = 1; k < R; ++k) tr = tr + gram(k, k);
     Ldl f = ldlt(gram.v, R);
-    const GramDecision dec = decide_gram(gram.v, R, maxdiag, tr, f);
+    const GramDecision dec = decide_gram(gram.v, R, maxdiag, f);
     if (path) *path = dec.path;
     if (dec.mode == 0) {  // solve.cpp:21-26
         if (regularized) *regularized = true;
@@ -567,6 +699,9 @@ double hsum(std::vector<double> v) {
     return v[0];
 }
 
+void fit_fibre(const double* t, const Dims& d, const std::vector<Mat>* fs, Index I1, int N, Index R, Index j,
+               std::vector<Index>& multi, std::vector<double>& w, std::vector<double>& fib);
+
 // Returns sum of squares of (x_hat - x) (or of x when factors == nullptr).
 double fit_sumsq(const double* t, const Dims& d, const std::vector<Mat>* fs) {
     const Index I1 = d[0];
@@ -574,9 +709,34 @@ double fit_sumsq(const double* t, const Dims& d, const std::vector<Mat>* fs) {
     const int N = int(d.size());
     const Index R = fs ? (*fs)[0].cols : 0;
     std::vector<double> fib(static_cast<size_t>(nfib));
-    std::vector<Index> multi(static_cast<size_t>(N - 1));
-    std::vector<double> w(static_cast<size_t>(R));
-    for (Index j = 0; j < nfib; ++j) {
+    // Fibre values are independent and combined afterwards by hsum in fibre order, so
+    // the fibres are spread over threads (ORC_THREADS, default all cores) with bitwise
+    // identical results; test infrastructure speed only (the timed CPU baselines stream,
+    // they never evaluate the full fit).
+    static const int nthreads = [] {
+        const char* e = std::getenv("ORC_THREADS");
+        const int n = e ? std::atoi(e) : int(std::thread::hardware_concurrency());
+        return std::max(1, std::min(n, 64));
+    }();
+    const Index per = 4096;
+    std::atomic<Index> next{0};
+    auto work = [&] {
+        std::vector<Index> multi(static_cast<size_t>(N - 1));
+        std::vector<double> w(static_cast<size_t>(R));
+        for (Index j0 = next.fetch_add(per); j0 < nfib; j0 = next.fetch_add(per))
+            for (Index j = j0; j < std::min(nfib, j0 + per); ++j) fit_fibre(t, d, fs, I1, N, R, j, multi, w, fib);
+    };
+    const int nt = int(std::min<Index>(nthreads, (nfib + per - 1) / per));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < nt; ++k) pool.emplace_back(work);
+    work();
+    for (std::thread& th : pool) th.join();
+    return hsum(std::move(fib));
+}
+
+void fit_fibre(const double* t, const Dims& d, const std::vector<Mat>* fs, Index I1, int N, Index R, Index j,
+               std::vector<Index>& multi, std::vector<double>& w, std::vector<double>& fib) {
+    {
         if (fs) {
             decode(j + 1, d, 1, multi.data());  // (i_2..i_N)
             for (Index r = 0; r < R; ++r) {
@@ -599,7 +759,6 @@ double fit_sumsq(const double* t, const Dims& d, const std::vector<Mat>* fs) {
         }
         fib[size_t(j)] = butterfly32(q);
     }
-    return hsum(std::move(fib));
 }
 
 // Sampled residual |X_s - U Z^T|_F / |X_s|_F (north-star item 5; no reference
@@ -784,6 +943,13 @@ void orc_contract(const double* x, int64_t rows, int64_t s, const double* z, int
     to_ptr(contract_of(from_ptr(x, rows, s), from_ptr(z, s, rank)), out);
 }
 
+void orc_decision_stats(int64_t* counts, int reset) {
+    for (int k = 0; k < 4; ++k) {
+        if (counts) counts[k] = g_decision_paths[k];
+        if (reset) g_decision_paths[k] = 0;
+    }
+}
+
 int orc_gram_decision(const double* gram, int rank, int* mode, int* regularized, int* path, double* lo,
                       double* hi) {
     if (rank < 1) return fail(ORC_E_DOMAIN, "gram_decision: empty gram");
@@ -794,7 +960,7 @@ int orc_gram_decision(const double* gram, int rank, int* mode, int* regularized,
         tr = tr + g(k, k);
     }
     const Ldl f = ldlt(g.v, rank);
-    const GramDecision dec = decide_gram(g.v, rank, maxdiag, tr, f);
+    const GramDecision dec = decide_gram(g.v, rank, maxdiag, f);
     if (mode) *mode = dec.mode;
     if (regularized) *regularized = dec.reg ? 1 : 0;
     if (path) *path = dec.path;

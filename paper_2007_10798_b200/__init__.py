@@ -98,6 +98,8 @@ SIGNATURES = [
     ("rocp_stream_update_mode_with", C.c_int, [_vp, _vp, _f64p, C.c_int, _i64p, C.c_int64, _f64p,
                                                _f64p, C.POINTER(C.c_int)]),
     ("rocp_stream_finish_batch", C.c_int, [_vp, C.c_int64]),
+    ("rocp_probe_random_reads", C.c_int, [_vp, _vp, C.c_int64, C.c_uint64, C.POINTER(C.c_float)]),
+    ("rocp_decision_stats", C.c_int, [_vp, C.POINTER(C.c_uint64), C.c_int]),
     ("rocp_stream_mark_regularized", C.c_int, [_vp]),
     ("rocp_stream_get", C.c_int, [_vp, C.c_int, C.c_int, _f64p]),
     ("rocp_stream_set", C.c_int, [_vp, C.c_int, C.c_int, _f64p]),
@@ -284,6 +286,18 @@ class Device:
         h = C.c_void_p()
         self.check(lib().rocp_tensor_read_file(self.h, os.fsencode(path), C.byref(h)))
         return DeviceTensor(self, _record_dims(path), _handle=h)
+
+    def decision_stats(self, reset=False):
+        """[no-reg, reg, exact-eigenvalue, tier-2-used] solve_gram decisions since the last reset."""
+        c = (C.c_uint64 * 4)()
+        self.check(lib().rocp_decision_stats(self.h, c, int(bool(reset))))
+        return [int(v) for v in c]
+
+    def probe_random_reads(self, tensor, reads, seed=1):
+        """Isolated 8-byte random reads per second over `tensor` (the gather's access ceiling)."""
+        ms = C.c_float(0)
+        self.check(lib().rocp_probe_random_reads(self.h, tensor.h, int(reads), seed, C.byref(ms)))
+        return reads / (ms.value / 1000.0), float(ms.value)
 
     def timer_record(self, slot):
         self.check(lib().rocp_timer_record(self.h, slot))

@@ -643,7 +643,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     __shared__ unsigned short pairs[64 * 65 / 2];
     __shared__ __align__(8) uint64_t bar;
     __shared__ int s_mode, s_reg;
-    __shared__ double s_tr;
+    __shared__ double s_tr, s_maxdiag;
+    __shared__ double s_ymax, s_gnorm, s_tau;  // regularisation certificate (kernels.cuh gram_certificate)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
     const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
@@ -943,12 +944,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     __syncthreads();
                     if (tr) trace_stamp(tr, 10, tid == 0);
                     int reg;
-                    if (R <= 32) {
+                    if constexpr (!kWide) {  // R <= 32 (the wide instance serves R > 32)
                         // warp 0 factors G at once (the condition check's min / max of D formed
                         // in the pivot loop) while warp 1 forms the solve_gram prologue
                         // (solve.cpp:9-22); with maxdiag <= 0 the factors are never read (mode
                         // 0), so starting early changes nothing
-                        double* dmm = D + 62;  // min d, max d (D holds R <= 32 entries)
+                        double* dmm = D + 61;  // min d, max d, ymax (D holds R <= 32 entries)
                         auto factor_w = [&](double lambda, double* mm) {
                             if (R <= 8) ldlt_warp<8>(Gs, lambda, R, A, kLdStride, D, colb, mm);
                             else if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, kLdStride, D, colb, mm);
@@ -968,26 +969,64 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                                     trc = trc + dg;
                                 }
                                 s_tr = trc;
-                                s_mode = (maxdiag <= 0.0) ? 0 : 1;
+                                s_maxdiag = maxdiag;
                             }
                             __syncwarp();
+                        } else if (warp == 2) {
+                            const double gn = gram_inf_norm_warp(Gs, R, R);
+                            if (lane == 0) s_gnorm = gn;
                         }
                         __syncthreads();
                         if (tr) trace_stamp(tr, 13, tid == 0);
-                        // solve_gram's regularisation decision (solve.cpp:24-31), by every thread
-                        reg = (s_mode == 0) ? 1
-                                            : ((!(dmm[0] > 0.0) || dmm[1] > kGramConditionLimit * dmm[0]) ? 1 : 0);
+                        // solve_gram's regularisation decision (solve.cpp:17-33): warp 0 forms the
+                        // tier-1 certificate's ymax while the other warps publish the unregularised
+                        // L and D (republished below in the rare regularised case)
+                        if (warp == 0) {
+                            const double y = cert_ymax_warp(A, kLdStride, R);
+                            if (lane == 0) dmm[2] = y;
+                        } else {
+                            for (int t = tid - 32; t < RR; t += blockDim.x - 32) {
+                                const int k = t / R, i = t - k * R;
+                                if (i > k) p.LD[t] = A[k * kLdStride + i];
+                            }
+                            if (tid - 32 < R) p.LD[RR + tid - 32] = D[tid - 32];
+                        }
+                        __syncthreads();
+                        int path = gram_certificate(s_maxdiag, s_gnorm, dmm[0], dmm[1], dmm[2], R);
+                        const bool tier2 = path == kDecTier2;
+                        if (tier2)  // rare: tr(G^-1) in the free chunk area
+                            path = gram_tier2_block<1>(A, kLdStride, D, R, s_maxdiag, s_gnorm, sm + 8192, &s_tau);
+                        if (tid == 0) count_decision(path, tier2);
+                        if (path == kDecExact) {  // rare: Jacobi on a copy of G in the free chunk area
+                            double* ja = sm;
+                            for (int t = tid; t < RR; t += blockDim.x) ja[t] = Gs[t];
+                            __syncthreads();
+                            double lo, hi;
+                            jacobi_eigen_block(ja, R, R, sm + 8192, &s_reg, &lo, &hi);
+                            if (tid == 0) {
+                                int md, rg;
+                                exact_decision(lo, hi, &md, &rg);
+                                s_mode = md;
+                                s_reg = rg;
+                            }
+                            __syncthreads();
+                            reg = s_reg;
+                        } else {
+                            if (tid == 0) s_mode = 1;
+                            reg = (path == kDecReg) ? 1 : 0;
+                        }
+                        __syncthreads();
                         if (s_mode == 1 && reg) {
                             if (warp == 0) factor_w(1e-12 * s_tr, nullptr);
                             __syncthreads();
+                            // publish the regularised strictly lower L and D instead
+                            for (int t = tid; t < RR; t += blockDim.x) {
+                                const int k = t / R, i = t - k * R;
+                                if (i > k) p.LD[t] = A[k * kLdStride + i];
+                            }
+                            if (tid < R) p.LD[RR + tid] = D[tid];
                         }
                         if (tr) trace_stamp(tr, 11, tid == 0);
-                        // publish the strictly lower L (all the row solves read) and D
-                        for (int t = tid; t < RR; t += blockDim.x) {
-                            const int k = t / R, i = t - k * R;
-                            if (i > k) p.LD[t] = A[k * kLdStride + i];
-                        }
-                        if (tid < R) p.LD[RR + tid] = D[tid];
                     } else {
                         // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
                         if (tid == 0) {
@@ -999,27 +1038,61 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                                 trc = trc + dg;
                             }
                             s_tr = trc;
-                            s_mode = (maxdiag <= 0.0) ? 0 : 1;
-                            s_reg = (s_mode == 0) ? 1 : 0;
+                            s_maxdiag = maxdiag;
                         }
                         __syncthreads();
                         if (tr) trace_stamp(tr, 12, tid == 0);
-                        if (s_mode == 1) {
-                            ldlt_one_sync(A, D, R, 0.0, Gs, pairs, npairs);
-                            if (tr) trace_stamp(tr, 13, tid == 0);
-                            if (tid == 0) {
-                                double dmin = D[0], dmax = D[0];
+                        ldlt_one_sync(A, D, R, 0.0, Gs, pairs, npairs);
+                        if (tr) trace_stamp(tr, 13, tid == 0);
+                        // regularisation decision (solve.cpp:17-33): certificate over two warps
+                        // (columns 0..31, 32..63), exact eigenvalues in the band
+                        if (warp == 0) {
+                            const double y = cert_ymax_warp(A, kLdStride, R);
+                            if (lane == 0) s_ymax = y;
+                        } else if (warp == 1) {
+                            const double gn = gram_inf_norm_warp(Gs, R, R);
+                            if (lane == 0) s_gnorm = gn;
+                        }
+                        __syncthreads();
+                        if (tid == 0) {
+                            double dmin = D[0], dmax = D[0];
 #pragma unroll 8
-                                for (int k = 0; k < R; ++k) {
-                                    const double dk = D[k];
-                                    if (dk < dmin) dmin = dk;
-                                    if (dk > dmax) dmax = dk;
-                                }
-                                s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
+                            for (int k = 0; k < R; ++k) {
+                                const double dk = D[k];
+                                if (dk < dmin) dmin = dk;
+                                if (dk > dmax) dmax = dk;
+                            }
+                            s_mode = gram_certificate(s_maxdiag, s_gnorm, dmin, dmax, s_ymax, R);
+                        }
+                        __syncthreads();
+                        {
+                            int path = s_mode;
+                            const bool tier2 = path == kDecTier2;
+                            if (tier2)  // rare: tr(G^-1) in the free chunk area
+                                path = gram_tier2_block<2>(A, kLdStride, D, R, s_maxdiag, s_gnorm, sm + 8192, &s_tau);
+                            if (tid == 0) count_decision(path, tier2);
+                            __syncthreads();
+                            if (tid == 0) {
+                                s_mode = (path == kDecExact) ? -1 : 1;
+                                s_reg = (path == kDecReg) ? 1 : 0;
+                            }
+                        }
+                        __syncthreads();
+                        if (s_mode < 0) {  // rare: Jacobi on a copy of G in the free chunk area
+                            double* ja = sm;
+                            for (int t = tid; t < RR; t += blockDim.x) ja[t] = Gs[t];
+                            __syncthreads();
+                            double lo, hi;
+                            jacobi_eigen_block(ja, R, R, sm + 8192, &s_reg, &lo, &hi);
+                            if (tid == 0) {
+                                int md, rg;
+                                exact_decision(lo, hi, &md, &rg);
+                                s_mode = md;
+                                s_reg = rg;
                             }
                             __syncthreads();
-                            if (s_reg) ldlt_one_sync(A, D, R, 1e-12 * s_tr, Gs, pairs, npairs);
                         }
+                        if (s_mode == 1 && s_reg) ldlt_one_sync(A, D, R, 1e-12 * s_tr, Gs, pairs, npairs);
                         __syncthreads();
                         reg = s_reg;
                         if (tr) trace_stamp(tr, 11, tid == 0);

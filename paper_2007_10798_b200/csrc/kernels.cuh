@@ -572,6 +572,333 @@ __global__ void __launch_bounds__(256) k_contract_chunks(const double* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Random-access ceiling probe (measurement only; no reference counterpart): every
+// thread issues kProbeILP independent 8-byte loads at hashed offsets of x, the
+// access pattern of the strided gather (each element its own DRAM page), so
+// bench.py can state the gather against the device's isolated-read rate.
+constexpr int kProbeILP = 8;
+__global__ void __launch_bounds__(256) k_probe_random_reads(const double* __restrict__ x, uint64_t n,
+                                                           int64_t reads, uint64_t seed, double* sink) {
+    double acc = 0.0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x * kProbeILP;
+    for (int64_t base = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kProbeILP; base < reads; base += stride) {
+        double v[kProbeILP];
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) {
+            uint64_t h = seed + uint64_t(base + u) * 0x9E3779B97F4A7C15ull;  // splitmix64
+            h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
+            h = (h ^ (h >> 27)) * 0x94D049BB133111EBull;
+            h ^= h >> 31;
+            v[u] = (base + u < reads) ? __ldcs(x + __umul64hi(h, n)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) acc = acc + v[u];
+    }
+    if (acc == 1.2345678e300) *sink = acc;  // keeps the loads
+}
+
+// ---------------------------------------------------------------------------
+// solve_gram's regularisation decision (solve.cpp:17-33), canonical form
+// (oracle certificate / jacobi_eigen / decide_gram).  The
+// reference decides from exact eigenvalues: zero solution if lambda_max <= 0,
+// regularise if lambda_min <= 0 or lambda_max / lambda_min > 1e12.  Rigorous
+// certificate first: dmax / dmin <= kappa (pivots of an SPD matrix lie in
+// [lambda_min, lambda_max]) and kappa <= |G|_inf R ymax^2 / dmin with
+// ymax >= |L^-1|_inf (cert_ymax_warp).  Certainly above 4e12 -> regularise;
+// certainly below 2.5e11 -> not; a non-positive max diagonal or pivot, or the
+// band in between -> exact eigenvalues by the deterministic cyclic Jacobi method.
+constexpr double kCertRegAbove = 4e12;
+constexpr double kCertNoRegBelow = 2.5e11;
+constexpr int kDecNoReg = 0, kDecReg = 1, kDecExact = 2;
+
+__device__ __forceinline__ double butterfly32(double q) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) q = q + __shfl_xor_sync(0xffffffffu, q, off);
+    return q;
+}
+
+// max(a, b) of the canonical row maxima: (b > a) ? b : a.
+__device__ __forceinline__ double max_of(double a, double b) { return (b > a) ? b : a; }
+__device__ __forceinline__ double butterfly_max32(double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = max_of(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+// max_i y_i, y = (I - |N|)^-1 1 for L = I - N: lane i owns rows i and i + 32,
+// y_i = fma(|l_ik|, y_k, y_i) in k order from 1.0 (oracle cert_ymax).  One warp.
+// L(i,k) at L[k*ld + i] (i > k).
+__device__ __noinline__ double cert_ymax_warp(const double* L, int ld, int R) {
+    const int lane = threadIdx.x & 31;
+    double y0 = 1.0, y1 = 1.0;
+    for (int k = 0; k + 1 < R; ++k) {
+        const double yk = __shfl_sync(0xffffffffu, (k < 32) ? y0 : y1, k & 31);
+        if (lane > k && lane < R) y0 = __fma_rn(fabs(L[k * ld + lane]), yk, y0);
+        if (lane + 32 > k && lane + 32 < R) y1 = __fma_rn(fabs(L[k * ld + lane + 32]), yk, y1);
+    }
+    double v = (lane < R) ? y0 : 0.0;
+    if (lane + 32 < R) v = max_of(v, y1);
+    return butterfly_max32(v);
+}
+
+// |G|_inf (max absolute row sum; row sums in column order), one warp; a(i,j) at G[i + j*ldg].
+__device__ __noinline__ double gram_inf_norm_warp(const double* G, int ldg, int R) {
+    const int lane = threadIdx.x & 31;
+    double r0 = 0.0, r1 = 0.0;
+    for (int j = 0; j < R; ++j) {
+        if (lane < R) r0 = r0 + fabs(G[lane + j * ldg]);
+        if (lane + 32 < R) r1 = r1 + fabs(G[lane + 32 + j * ldg]);
+    }
+    double v = (lane < R) ? r0 : 0.0;
+    if (lane + 32 < R) v = max_of(v, r1);
+    return butterfly_max32(v);
+}
+
+constexpr int kDecTier2 = 3;  // tier 1 left the band: form tau = tr(G^-1)
+
+// Device-wide decision statistics (rocp_decision_stats): [0] no-reg, [1] reg, [2] exact
+// eigenvalues, [3] decisions that needed tier 2.  One atomic per solve, off the chain's
+// critical path (issued by the thread that publishes the decision).
+__device__ unsigned long long g_dec_paths[4];
+__device__ __forceinline__ void count_decision(int final_path, bool used_tier2) {
+    atomicAdd(&g_dec_paths[final_path], 1ull);
+    if (used_tier2) atomicAdd(&g_dec_paths[3], 1ull);
+}
+
+// Tier 1 (every Gram; ymax folded into the factorization).
+__device__ __forceinline__ int gram_certificate(double maxdiag, double gnorm, double dmin, double dmax, double ymax,
+                                                int R) {
+    if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
+    const double ratio = dmax / dmin;
+    if (ratio > kCertRegAbove) return kDecReg;
+    const double khi = ((gnorm / dmin) * double(R)) * (ymax * ymax);
+    if (khi <= kCertNoRegBelow) return kDecNoReg;
+    return kDecTier2;
+}
+
+// Tier 2: maxdiag tau / R <= kappa <= |G|_inf tau (tau = tr(G^-1) >= 1 / lambda_min).
+__device__ __forceinline__ int gram_certificate2(double maxdiag, double gnorm, double tau, int R) {
+    const double klo = (maxdiag * tau) / double(R);
+    const double khi = gnorm * tau;
+    if (klo > kCertRegAbove) return kDecReg;
+    if (khi <= kCertNoRegBelow) return kDecNoReg;
+    return kDecExact;
+}
+
+// tau = tr(G^-1) = sum_i (sum_j M_ij^2) / d_i, M = L^-1 (oracle cert_tau), tier 2 only.
+// cert_group_warp: one warp forms the columns 8g..8g+7 of M by forward substitution,
+// lane i owning rows i and i + 32 (NRB row blocks), M(k, .) of step k broadcast by
+// shuffle from its owner; a rolled k loop (small code).  Writes the group's row
+// partials p_gi = fma chain over its columns to part[g * 64 + i].  L(i,k) at
+// L[k*ld + i] (i > k).
+template <int NRB>
+__device__ __noinline__ void cert_group_warp(const double* L, int ld, int R, int g, double* part) {
+    const int lane = threadIdx.x & 31;
+    const int c0 = 8 * g;
+    double m[NRB][8];
+#pragma unroll
+    for (int rb = 0; rb < NRB; ++rb)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) m[rb][c] = (lane + 32 * rb == c0 + c) ? 1.0 : 0.0;
+    for (int k = c0; k + 1 < R; ++k) {
+        const int src = k & 31;
+        double mk[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            double own = m[0][c];
+            if (NRB > 1 && k >= 32) own = m[NRB - 1][c];
+            mk[c] = __shfl_sync(0xffffffffu, own, src);
+        }
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb) {
+            const int i = lane + 32 * rb;
+            if (i > k && i < R) {
+                const double l = L[k * ld + i];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) m[rb][c] = __fma_rn(-l, mk[c], m[rb][c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int rb = 0; rb < NRB; ++rb) {
+        double pp = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c0 + c < R) pp = __fma_rn(m[rb][c], m[rb][c], pp);
+        part[g * 64 + lane + 32 * rb] = pp;
+    }
+}
+
+// One warp: s_i = p_0i + p_1i + ..., t_i = s_i / d_i, v = t_lane + t_{lane+32}, butterfly sum.
+__device__ __noinline__ double cert_combine_warp(const double* part, const double* D, int R) {
+    const int lane = threadIdx.x & 31;
+    const int ng = (R + 7) / 8;
+    double t[2];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) {
+        const int i = lane + 32 * rb;
+        if (i < R) {
+            double sacc = part[i];
+            for (int gg = 1; gg < ng; ++gg) sacc = sacc + part[gg * 64 + i];
+            t[rb] = sacc / D[i];
+        } else {
+            t[rb] = 0.0;
+        }
+    }
+    return butterfly32(t[0] + t[1]);
+}
+
+// Tier 2 by a whole block (every warp < ceil(R/8) forms one column group; part: 8 x 64
+// doubles of shared scratch); returns the tier-2 path on every thread.  Block-uniform call.
+template <int NRB>
+__device__ __noinline__ int gram_tier2_block(const double* L, int ld, const double* D, int R, double maxdiag,
+                                             double gnorm, double* part, double* s_tau) {
+    const int warp = threadIdx.x >> 5;
+    if (warp < (R + 7) / 8) cert_group_warp<NRB>(L, ld, R, warp, part);
+    __syncthreads();
+    if (warp == 0) {
+        const double t = cert_combine_warp(part, D, R);
+        if ((threadIdx.x & 31) == 0) *s_tau = t;
+    }
+    __syncthreads();
+    return gram_certificate2(maxdiag, gnorm, *s_tau, R);
+}
+
+// Deterministic parallel (round-robin) Jacobi eigenvalue extremes of a symmetric
+// R x R matrix (a(i,j) at a[i + j*lda], destroyed) by a whole block: the oracle's
+// jacobi_eigen round for round -- the pairs of a round (circle method) get their
+// (t, c, s) from one thread each, then every 2 x 2 block (P, Q), P <= Q, is
+// transformed by one thread (rows by pair P, then columns by pair Q, mirrored), in
+// place: a block is the only reader of its own entries in a round.  prm: 4 * 32
+// doubles of shared scratch, flag: a shared int.  Block-uniform call.  Rare path
+// (the certificate settles every Gram of the BASELINE configs but a few of C5's).
+__device__ __forceinline__ void jacobi_pair(int r, int k, int n, int* p, int* q) {
+    int a, b;
+    if (k == 0) {
+        a = r;
+        b = n - 1;
+    } else {
+        a = (r + k) % (n - 1);
+        b = (r - k + (n - 1)) % (n - 1);
+    }
+    *p = min(a, b);
+    *q = max(a, b);
+}
+
+__device__ __noinline__ void jacobi_eigen_block(double* a, int lda, int R, double* prm, int* flag, double* lo,
+                                                double* hi) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int n = R + (R & 1), np = n / 2;
+    for (int sweep = 0; sweep < 64 && R > 1; ++sweep) {
+        if (tid == 0) *flag = 0;
+        __syncthreads();
+        for (int r = 0; r + 1 < n; ++r) {
+            for (int k = tid; k < np; k += nt) {
+                int p, q;
+                jacobi_pair(r, k, n, &p, &q);
+                double rotk = 0.0, c = 1.0, sn = 0.0, t = 0.0;
+                if (q < R) {
+                    const double apq = a[p + q * lda], app = a[p + p * lda], aqq = a[q + q * lda];
+                    const double thr = 2.220446049250313e-16 * sqrt(fabs(app) * fabs(aqq));
+                    if (fabs(apq) > thr) {
+                        const double theta = (aqq - app) / (2.0 * apq);
+                        t = (fabs(theta) > 1e150)
+                                ? 0.5 / theta
+                                : ((theta >= 0.0) ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        c = 1.0 / sqrt(t * t + 1.0);
+                        sn = t * c;
+                        rotk = 1.0;
+                        *flag = 1;
+                    }
+                }
+                prm[4 * k + 0] = c;
+                prm[4 * k + 1] = sn;
+                prm[4 * k + 2] = t;
+                prm[4 * k + 3] = rotk;
+            }
+            __syncthreads();
+            for (int idx = tid; idx < np * np; idx += nt) {
+                const int P = idx / np, Q = idx - (idx / np) * np;
+                if (Q < P) continue;
+                const bool rP = prm[4 * P + 3] != 0.0, rQ = prm[4 * Q + 3] != 0.0;
+                int p, q, u, v;
+                jacobi_pair(r, P, n, &p, &q);
+                jacobi_pair(r, Q, n, &u, &v);
+                if (P == Q) {
+                    if (!rP) continue;
+                    const double apq = a[p + q * lda], app = a[p + p * lda], aqq = a[q + q * lda];
+                    const double t = prm[4 * P + 2];
+                    a[p + p * lda] = app - t * apq;
+                    a[q + q * lda] = aqq + t * apq;
+                    a[p + q * lda] = 0.0;
+                    a[q + p * lda] = 0.0;
+                    continue;
+                }
+                if (!rP && !rQ) continue;
+                const bool qv = q < R, vv = v < R;
+                double x_pu = a[p + u * lda], x_pv = vv ? a[p + v * lda] : 0.0;
+                double x_qu = qv ? a[q + u * lda] : 0.0, x_qv = (qv && vv) ? a[q + v * lda] : 0.0;
+                if (rP) {  // rows by pair P
+                    const double c = prm[4 * P], sn = prm[4 * P + 1];
+                    const double y_pu = c * x_pu - sn * x_qu, y_qu = sn * x_pu + c * x_qu;
+                    const double y_pv = c * x_pv - sn * x_qv, y_qv = sn * x_pv + c * x_qv;
+                    x_pu = y_pu;
+                    x_qu = y_qu;
+                    x_pv = y_pv;
+                    x_qv = y_qv;
+                }
+                if (rQ) {  // then columns by pair Q
+                    const double c = prm[4 * Q], sn = prm[4 * Q + 1];
+                    const double z_pu = c * x_pu - sn * x_pv, z_pv = sn * x_pu + c * x_pv;
+                    const double z_qu = c * x_qu - sn * x_qv, z_qv = sn * x_qu + c * x_qv;
+                    x_pu = z_pu;
+                    x_pv = z_pv;
+                    x_qu = z_qu;
+                    x_qv = z_qv;
+                }
+                a[p + u * lda] = x_pu;
+                a[u + p * lda] = x_pu;
+                if (vv) {
+                    a[p + v * lda] = x_pv;
+                    a[v + p * lda] = x_pv;
+                }
+                if (qv) {
+                    a[q + u * lda] = x_qu;
+                    a[u + q * lda] = x_qu;
+                }
+                if (qv && vv) {
+                    a[q + v * lda] = x_qv;
+                    a[v + q * lda] = x_qv;
+                }
+            }
+            __syncthreads();
+        }
+        const int any = *flag;
+        __syncthreads();
+        if (!any) break;
+    }
+    double l = a[0], h = a[0];
+    for (int k = 1; k < R; ++k) {
+        const double v = a[k + k * lda];
+        if (v < l) l = v;
+        if (v > h) h = v;
+    }
+    *lo = l;
+    *hi = h;
+}
+
+// The exact branch: (mode, reg) from the Jacobi extremes (solve.cpp:21-33).
+__device__ __forceinline__ void exact_decision(double lo, double hi, int* mode, int* reg) {
+    if (hi <= 0.0) {
+        *mode = 0;
+        *reg = 1;
+    } else {
+        *mode = 1;
+        *reg = (lo <= 0.0 || hi / lo > kGramConditionLimit) ? 1 : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K5: solve_gram (solve.cpp:9-35), canonical form:
 // zero solution if max diag <= 0; unpivoted LDL^T; regularize with
 // 1e-12 tr(G) when a pivot is <= 0 or max/min pivot > 1e12; then per row
@@ -617,6 +944,10 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
         __syncthreads();
     };
 
+    __shared__ double s_ymax, s_gnorm, s_tau;
+    __shared__ int s_path;
+    __shared__ double s_t2[8 * 64];  // tier-2 certificate row partials
+    __shared__ double s_maxdiag;
     for (int k = tid; k < R; k += blockDim.x) D[k] = G[k * R + k];  // diagonal, staged
     __syncthreads();
     if (tid == 0) {
@@ -626,26 +957,63 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
         double tr = D[0];
         for (int k = 1; k < R; ++k) tr = tr + D[k];
         s_tr = tr;
-        s_mode = (maxdiag <= 0.0) ? 0 : 1;
-        s_reg = (s_mode == 0) ? 1 : 0;
+        s_maxdiag = maxdiag;
+    }
+    load(0.0);
+    factor();
+    {
+        const int warp = tid >> 5;
+        if (warp == 0) {
+            const double y = cert_ymax_warp(&A[0][0], MAXR + 1, R);
+            if (tid == 0) s_ymax = y;
+        } else if (warp == 1) {
+            const double gn = gram_inf_norm_warp(G, R, R);
+            if ((tid & 31) == 0) s_gnorm = gn;
+        }
     }
     __syncthreads();
-    if (s_mode == 1) {
-        load(0.0);
-        factor();
+    if (tid == 0) {
+        double dmin = D[0], dmax = D[0];
+        for (int k = 0; k < R; ++k) {
+            if (D[k] < dmin) dmin = D[k];
+            if (D[k] > dmax) dmax = D[k];
+        }
+        s_path = gram_certificate(s_maxdiag, s_gnorm, dmin, dmax, s_ymax, R);
+    }
+    __syncthreads();
+    {
+        int path = s_path;
+        if (path == kDecTier2)  // rare: tier 2 in the scratch of the (finished) staging
+            path = gram_tier2_block<(MAXR > 32) ? 2 : 1>(&A[0][0], MAXR + 1, D, R, s_maxdiag, s_gnorm, s_t2, &s_tau);
+        if (tid == 0 && blockIdx.x == 0) count_decision(path, s_path == kDecTier2);
         if (tid == 0) {
-            double dmin = D[0], dmax = D[0];
-            for (int k = 0; k < R; ++k) {
-                if (D[k] < dmin) dmin = D[k];
-                if (D[k] > dmax) dmax = D[k];
+            s_mode = (path == kDecExact) ? -1 : 1;
+            s_reg = (path == kDecReg) ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    if (s_mode < 0) {  // exact eigenvalues: G in A as a full symmetric matrix (lda MAXR + 1)
+        double* a = &A[0][0];
+        for (int t = tid; t < R * R; t += blockDim.x) a[(t % R) + (t / R) * (MAXR + 1)] = G[t];
+        __syncthreads();
+        {
+            double lo, hi;
+            jacobi_eigen_block(a, MAXR + 1, R, s_t2, &s_path, &lo, &hi);
+            if (tid == 0) {
+                int mode, reg;
+                exact_decision(lo, hi, &mode, &reg);
+                s_mode = mode;
+                s_reg = reg;
             }
-            s_reg = (!(dmin > 0.0) || dmax > kGramConditionLimit * dmin) ? 1 : 0;
         }
         __syncthreads();
-        if (s_reg) {
-            load(1e-12 * s_tr);
+        if (s_mode == 1) {  // A was overwritten: the factorization of G or G + lambda I again
+            load(s_reg ? 1e-12 * s_tr : 0.0);
             factor();
         }
+    } else if (s_reg) {
+        load(1e-12 * s_tr);
+        factor();
     }
     if (blockIdx.x == 0 && tid == 0 && s_reg && flags) atomicOr(flags, 1);
 
@@ -682,12 +1050,8 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
 }
 
 // ---------------------------------------------------------------------------
-// Warp / group reductions of the canonical fitness order.
-__device__ __forceinline__ double butterfly32(double q) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) q = q + __shfl_xor_sync(0xffffffffu, q, off);
-    return q;
-}
+// Warp / group reductions of the canonical fitness order:
+// butterfly32 above.
 
 // Sum of v[0..n) (n <= 256, missing = +0.0) by one warp: lane-strided then butterfly.
 // GLOBAL = true reads through L2 (__ldcg): the values may have been written by

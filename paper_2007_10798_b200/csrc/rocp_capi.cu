@@ -1451,6 +1451,40 @@ void rocp_destroy(rocp_dev* dev) {
 
 const char* rocp_last_error(const rocp_dev* dev) { return dev ? dev->err.c_str() : "null handle"; }
 
+rocp_status rocp_probe_random_reads(rocp_dev* dev, const rocp_tensor* t, int64_t reads, uint64_t seed, float* ms) {
+    return guarded(dev, [&] {
+        if (reads < 1 || !t || t->numel < 1) throw_domain("probe: need reads and a non-empty tensor");
+        DBuf<double> sink(1);
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        const int grid = dev->num_sms * 8;
+        k_probe_random_reads<<<grid, 256, 0, dev->stream>>>(t->d, uint64_t(t->numel), reads, seed, sink.p);  // warm
+        after_launch(dev, "k_probe_random_reads");
+        CK(cudaEventRecord(e0, dev->stream));
+        k_probe_random_reads<<<grid, 256, 0, dev->stream>>>(t->d, uint64_t(t->numel), reads, seed + 1, sink.p);
+        after_launch(dev, "k_probe_random_reads");
+        CK(cudaEventRecord(e1, dev->stream));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
+rocp_status rocp_decision_stats(rocp_dev* dev, uint64_t* counts, int reset) {
+    return guarded(dev, [&] {
+        CK(cudaStreamSynchronize(dev->stream));
+        unsigned long long h[4];
+        CK(cudaMemcpyFromSymbol(h, g_dec_paths, sizeof(h)));
+        for (int k = 0; k < 4; ++k) counts[k] = h[k];
+        if (reset) {
+            const unsigned long long z[4] = {0, 0, 0, 0};
+            CK(cudaMemcpyToSymbol(g_dec_paths, z, sizeof(z)));
+        }
+    });
+}
+
 rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms) {
     return guarded(dev, [&] {
         if (sms > dev->num_sms / 2) throw_domain("gather SMs: at most half the device");
