@@ -187,6 +187,19 @@ rocp_status rocp_stream_consume(rocp_stream* st, const rocp_tensor* x_new, uint6
  * size; rocp_stream_get(mode 1) returns the local rows.  Host-slab consumes and
  * the replay seams stay single-GPU (E_DOMAIN on a sharded stream). */
 rocp_status rocp_stream_shard(rocp_stream* st, int virtual_shards);
+/* Emulated ranks (a test/measurement harness for the sharded path when fewer GPUs
+ * than ranks exist): a handle that is rank `rank` of `world`
+ * on `device` without NCCL.  Streams on such handles, sharded as usual, run together
+ * through rocp_emulated_group_consume_range: every member's action is issued in
+ * turn, the members' exchange tables point at each other's areas in device memory
+ * (the peer-memory protocol of the real multi-GPU path, minus IPC), and all members'
+ * producers are joined (events) before any consumer, so no kernel waits on a peer
+ * that is not yet launched.  Results equal a real world-size run bit for bit
+ * (oracle orc_stream_consume_sharded). */
+rocp_status rocp_create_emulated_rank(int device, int world, int rank, rocp_dev** out);
+rocp_status rocp_emulated_group_consume_range(rocp_stream* const* ranks, int world, const rocp_tensor* const* x_local,
+                                              int64_t t0, int64_t batch, int64_t nb, uint64_t seed,
+                                              uint32_t first_batch_id);
 /* ComplementaryState records.  write_state writes exactly the reference's
  * save_state record (rocp.cpp:180-184: P(1..N-1), Q(1..N-1) matrix records,
  * u64le t_len), readable by its load_state; read_state loads such a record

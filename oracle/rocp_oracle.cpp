@@ -358,7 +358,7 @@ double gram_inf_norm(const std::vector<double>& g, int R) {
     return lanes_max(rs, R);
 }
 
-int64_t g_decision_paths[4] = {0, 0, 0, 0};  // test statistics (orc_decision_stats); [3]: tier 2 used
+int64_t g_decision_paths[5] = {0, 0, 0, 0, 0};  // test statistics (orc_decision_stats); [3]: tier 2 used, [4]: Jacobi sweeps
 
 // Tier 1 (every Gram, folded into the factorization on the device): pivots and ymax.
 // Tier 2 (only when tier 1 leaves the band, i.e. kappa within a few decades of the
@@ -492,6 +492,7 @@ void jacobi_eigen(std::vector<double>& a, int R, double* lo, double* hi) {
                 }
             a.swap(nb);
         }
+        ++g_decision_paths[4];
         if (!any) break;
     }
     double l = at(0, 0), h = at(0, 0);
@@ -944,7 +945,7 @@ void orc_contract(const double* x, int64_t rows, int64_t s, const double* z, int
 }
 
 void orc_decision_stats(int64_t* counts, int reset) {
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
         if (counts) counts[k] = g_decision_paths[k];
         if (reset) g_decision_paths[k] = 0;
     }

@@ -38,6 +38,9 @@ _vp = C.c_void_p
 # Every symbol declared in include/rocp_b200.h: (name, restype, argtypes).
 SIGNATURES = [
     ("rocp_create", C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
+    ("rocp_create_emulated_rank", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    ("rocp_emulated_group_consume_range", C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.c_int64, C.c_int64,
+                                                    C.c_int64, C.c_uint64, C.c_uint32]),
     ("rocp_destroy", None, [_vp]),
     ("rocp_last_error", C.c_char_p, [_vp]),
     ("rocp_set_gather_sms", C.c_int, [_vp, C.c_int]),
@@ -230,12 +233,17 @@ def _close_all_devices():
 class Device:
     """One handle per GPU (rocp_dev)."""
 
-    def __init__(self, device=0, world=1, rank=0, nccl_id=None):
+    def __init__(self, device=0, world=1, rank=0, nccl_id=None, emulated=False):
         """world > 1: one handle per GPU of a mode-1 sharded job; nccl_id = rank 0's
-        nccl_unique_id() bytes, broadcast by any host transport."""
+        nccl_unique_id() bytes, broadcast by any host transport.  emulated=True: rank
+        `rank` of `world` emulated on `device` (no NCCL; rocp_create_emulated_rank),
+        driven with emulated_group_consume_range."""
         h = C.c_void_p()
-        idp = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
-        rc = lib().rocp_create(device, world, rank, idp, C.byref(h))
+        if emulated:
+            rc = lib().rocp_create_emulated_rank(device, world, rank, C.byref(h))
+        else:
+            idp = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+            rc = lib().rocp_create(device, world, rank, idp, C.byref(h))
         if rc != OK:
             raise RocpError(rc, f"rocp_create(device={device}) failed (is a GPU visible?)")
         self.h = h
@@ -345,6 +353,15 @@ def nccl_unique_id():
     if rc != OK:
         raise RocpError(rc, "rocp_nccl_get_unique_id failed (NCCL unavailable?)")
     return buf.raw
+
+
+def emulated_group_consume_range(streams, local_tensors, t0, batch, nb, seed, first_batch_id):
+    """One window on every rank of an emulated group (rocp_emulated_group_consume_range):
+    streams[g] / local_tensors[g] belong to the emulated-rank handles of one device."""
+    w = len(streams)
+    hs = (_vp * w)(*[s_.h for s_ in streams])
+    xs = (_vp * w)(*[t.h for t in local_tensors])
+    streams[0].dev.check(lib().rocp_emulated_group_consume_range(hs, w, xs, t0, batch, nb, seed, first_batch_id))
 
 
 class HostBuffer:

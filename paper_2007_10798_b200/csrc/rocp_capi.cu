@@ -190,6 +190,7 @@ struct JobList {
 struct rocp_dev {
     int device = 0;
     int world = 1, rank = 0;
+    bool emulated = false;      // one of several ranks emulated on one device (no NCCL, no IPC)
     ncclComm_t comm = nullptr;  // world > 1: the mode-1 sharding communicator
     cudaStream_t stream = nullptr;
     std::string err;
@@ -717,6 +718,7 @@ struct Window {
 // column-major X_s of the local samples; plus the exchange buffers.
 struct ShardWin {
     int64_t nb = 0, B = 0;  // capacity
+    int64_t B_cur = 0;      // batch size of the window being run
     DBuf<int32_t> idx, cidx, clist;
     DBuf<int64_t> base, cbase;
     DBuf<int> counts;            // nb x N x V
@@ -1382,11 +1384,31 @@ void consume_one(rocp_stream* st, const double* x, int64_t B, uint64_t seed, uin
 // ===========================================================================
 extern "C" {
 
+static rocp_status create_dev(int device, int world, int rank, const void* nccl_id, bool emulated, rocp_dev** out);
+
 rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, rocp_dev** out) {
+    return create_dev(device, world, rank, nccl_id, false, out);
+}
+
+rocp_status rocp_create_emulated_rank(int device, int world, int rank, rocp_dev** out) {
+    return create_dev(device, world, rank, nullptr, true, out);
+}
+
+rocp_status rocp_emulated_group_consume_range(rocp_stream* const* ranks, int world, const rocp_tensor* const* x_local,
+                                              int64_t t0, int64_t batch, int64_t nb, uint64_t seed,
+                                              uint32_t first_batch_id) {
+    if (!ranks || world < 1 || !ranks[0]) return ROCP_E_DOMAIN;
+    return guarded(ranks[0]->dev, [&] {
+        emulated_group_consume(ranks, world, x_local, t0, batch, nb, seed, first_batch_id);
+    });
+}
+
+static rocp_status create_dev(int device, int world, int rank, const void* nccl_id, bool emulated, rocp_dev** out) {
     auto dev = std::make_unique<rocp_dev>();
     rocp_status st = guarded(dev.get(), [&] {
         if (world < 1 || rank < 0 || rank >= world) throw_domain("need 0 <= rank < world");
-        if (world > 1 && !nccl_id) throw_domain("world > 1 needs the NCCL unique id of rank 0");
+        if (world > 1 && !nccl_id && !emulated) throw_domain("world > 1 needs the NCCL unique id of rank 0");
+        dev->emulated = emulated;
         CK(cudaSetDevice(device));
         dev->device = device;
         {
@@ -1406,7 +1428,7 @@ rocp_status rocp_create(int device, int world, int rank, const void* nccl_id, ro
         CK(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int((size_t(kGroup) * 64 + kGroup) * sizeof(double))));
         set_contract_smem_attrs();
-        if (world > 1) {
+        if (world > 1 && !emulated) {
             const NcclApi& api = require_nccl();
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));

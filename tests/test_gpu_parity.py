@@ -487,3 +487,58 @@ def test_exhaustive_sampling_equals_full_update_on_device(dev):
         worst = max(worst, np.linalg.norm(state_q[n - 1] - qf[n - 1]) / np.linalg.norm(qf[n - 1]))
         worst = max(worst, np.linalg.norm(state_u[n - 1] - fh[n - 1]) / np.linalg.norm(fh[n - 1]))
     assert worst <= TOL["exhaustive_equivalence"], worst
+
+
+# ---- emulated multi-rank groups: the sharded product path at world 2 / 4 / 8 on one GPU ---------------
+@pytest.mark.parametrize("dims,R,t_init,B,V,world", [([24, 10, 60], 4, 20, 8, 8, 2), ([24, 10, 60], 4, 20, 8, 8, 4),
+                                                     ([16, 6, 5, 30], 3, 10, 5, 4, 2), ([64, 20, 70], 6, 20, 10, 8, 8),
+                                                     ([9, 4, 4, 3, 20], 2, 8, 4, 4, 4), ([200, 200, 120], 10, 50, 10, 8, 8)])
+def test_emulated_group_equals_oracle_sharded(dev, dims, R, t_init, B, V, world):
+    """World-size runs of the product's sharded path with `world` emulated ranks on this GPU
+    (rocp_create_emulated_rank + rocp_emulated_group_consume_range): k_shard_partition,
+    k_seg_partials storing into every rank's landing slots and releasing every rank's counter,
+    k_shard_combine / k_shard_resid_sum acquiring them, parity double-buffering across stages and
+    windows.  Every rank's local U(1)/P(1) rows, the replicated factors, P, Q, the temporal factor,
+    the flag and the residuals equal orc_stream_consume_sharded bit for bit."""
+    g = H.rng(sum(dims) + world)
+    x, _ = H.gen_synthetic(dims, R, 20.0, g)
+    head = dims[:-1]
+    s = orc.auto_sample_count(R)
+    init = H.init_from_model(H.random_model(head + [t_init], R, H.rng(3)), head + [t_init], s, 5)
+    X = dev.tensor(dims, x)
+    b = orc.Stream(init.model, t_init, init.best_sampled_kr, s)
+    devs = [rocp.Device(0, world, r, emulated=True) for r in range(world)]
+    try:
+        sts, xls, rows = [], [], []
+        for r in range(world):
+            st = rocp.RocpStream(devs[r], init, s, t_capacity=dims[-1])
+            r0, r1 = st.shard(V)
+            rows.append((r0, r1))
+            sts.append(st)
+            xls.append(X.rows(r0, r1))
+        assert rows[0][0] == 0 and rows[-1][1] == dims[0]
+        nb = (dims[-1] - t_init) // B
+        windows = [1, nb - 1] if nb > 1 else [1]
+        t0, bid = t_init, 1
+        for w in windows:
+            rocp.emulated_group_consume_range(sts, xls, t0, B, w, 616, bid)
+            for k in range(w):
+                b.consume_sharded(H.slab(x, dims, t0 + k * B, B), B, 616, bid + k, V)
+            t0, bid = t0 + w * B, bid + w
+            for r, st in enumerate(sts):
+                r0, r1 = rows[r]
+                assert bitwise(st.factor(1), b.factor(1)[r0:r1]), f"rank {r} U1 rows"
+                assert bitwise(st.p(1), b.p(1)[r0:r1]), f"rank {r} P1 rows"
+                assert bitwise(st.q(1), b.q(1)), f"rank {r} Q1"
+                for n in range(2, len(dims)):
+                    assert bitwise(st.factor(n), b.factor(n)), f"rank {r} U{n}"
+                    assert bitwise(st.p(n), b.p(n)), f"rank {r} P{n}"
+                    assert bitwise(st.q(n), b.q(n)), f"rank {r} Q{n}"
+                assert bitwise(st.temporal(), b.temporal()), f"rank {r} temporal"
+                assert st.t_len == b.t_len and st.regularized == b.regularized
+                assert bitwise(st.last_residuals(), b.last_residuals()), f"rank {r} residuals"
+        with pytest.raises(rocp.DomainError):  # a sharded member of the wrong world is rejected
+            rocp.emulated_group_consume_range(sts[:1], xls[:1], t_init, B, 1, 1, 1)
+    finally:
+        for d in devs:
+            d.close()
