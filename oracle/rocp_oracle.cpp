@@ -408,6 +408,10 @@ void jacobi_pair(int r, int k, int n, int* p, int* q) {
     *q = std::max(a, b);
 }
 
+// Off-diagonal tolerance relative to sqrt(|a_pp a_qq|): the diagonal then carries the
+// eigenvalues to ~1e-18 relative (second order), far below what the 1e12 test needs.
+constexpr double kJacobiTol = 1e-9;
+
 void jacobi_eigen(std::vector<double>& a, int R, double* lo, double* hi) {
     auto at = [&](int i, int j) -> double& { return a[size_t(i + j * R)]; };
     const int n = R + (R & 1), np = n / 2;
@@ -425,12 +429,13 @@ void jacobi_eigen(std::vector<double>& a, int R, double* lo, double* hi) {
                 rot[size_t(k)] = 0;
                 if (q >= R) continue;  // the dummy index
                 const double apq = at(p, q), app = at(p, p), aqq = at(q, q);
-                const double thr = 2.220446049250313e-16 * std::sqrt(std::fabs(app) * std::fabs(aqq));
+                const double thr = kJacobiTol * std::sqrt(std::fabs(app) * std::fabs(aqq));
                 if (!(std::fabs(apq) > thr)) continue;
-                const double theta = (aqq - app) / (2.0 * apq);
-                const double t = (std::fabs(theta) > 1e150)
-                                     ? 0.5 / theta
-                                     : ((theta >= 0.0) ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                // Rutishauser's t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (a_qq - a_pp) / 2a_pq,
+                // with numerator and denominator scaled by 2|a_pq| (one quotient fewer)
+                const double dl = aqq - app, h = std::sqrt(dl * dl + 4.0 * (apq * apq));
+                const double sg = ((dl >= 0.0) == (apq >= 0.0)) ? 1.0 : -1.0;
+                const double t = sg * (2.0 * std::fabs(apq)) / (std::fabs(dl) + h);
                 const double c = 1.0 / std::sqrt(t * t + 1.0);
                 tt[size_t(k)] = t;
                 cc[size_t(k)] = c;
@@ -556,6 +561,38 @@ void ldlt_solve_row(const Ldl& f, int R, const double* b, Index bstride, double*
     for (int j = 0; j < R; ++j) y[size_t(j) * ystride] = w[size_t(j)];
 }
 
+// Rows of solve_gram for R > 32: u = b G^-1 with the explicit inverse
+// formed once per solve, so the kernels solve thousands of rows as a skinny GEMM
+// instead of 2R-step substitutions.  M = L^-1 column by column (forward substitution,
+// updates in k order, as cert_tau), dinv_k = 1 / d_k (0 if |d_k| <= DBL_MIN), then
+// G^-1(i, j) = G^-1(j, i) = fma chain over k = j..R-1 of M(k, i) (M(k, j) dinv_k) for
+// i <= j; a row is u_j = fma chain over k = 0..R-1 of b_k G^-1(k, j) from +0.0.
+constexpr int kRowsByInverseAbove = 32;
+
+std::vector<double> gram_inverse(const Ldl& f, int R) {
+    std::vector<double> M(size_t(R) * R, 0.0), gi(size_t(R) * R, 0.0);
+    std::vector<double> m(static_cast<size_t>(R));
+    for (int j = 0; j < R; ++j) {
+        for (int i = 0; i < R; ++i) m[size_t(i)] = (i == j) ? 1.0 : 0.0;
+        for (int k = 0; k + 1 < R; ++k) {
+            const double mk = m[size_t(k)];
+            for (int i = k + 1; i < R; ++i) m[size_t(i)] = std::fma(-f.l[size_t(i + k * R)], mk, m[size_t(i)]);
+        }
+        for (int i = 0; i < R; ++i) M[size_t(i + j * R)] = m[size_t(i)];
+    }
+    std::vector<double> dinv(static_cast<size_t>(R));
+    for (int k = 0; k < R; ++k)
+        dinv[size_t(k)] = (std::fabs(f.d[size_t(k)]) > std::numeric_limits<double>::min()) ? 1.0 / f.d[size_t(k)] : 0.0;
+    for (int j = 0; j < R; ++j)
+        for (int i = 0; i <= j; ++i) {
+            double acc = 0.0;
+            for (int k = j; k < R; ++k) acc = std::fma(M[size_t(k + i * R)], M[size_t(k + j * R)] * dinv[size_t(k)], acc);
+            gi[size_t(i + j * R)] = acc;
+            gi[size_t(j + i * R)] = acc;
+        }
+    return gi;
+}
+
 Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path = nullptr) {
     const int R = int(gram.rows);
     const Index I = rhs.rows;
@@ -578,6 +615,16 @@ Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path =
         for (int k = 0; k < R; ++k) g[size_t(k + k * R)] = g[size_t(k + k * R)] + lambda;
         f = ldlt(g, R);
         if (regularized) *regularized = true;
+    }
+    if (R > kRowsByInverseAbove) {  // wide ranks: rows against the explicit inverse
+        const std::vector<double> gi = gram_inverse(f, R);
+        for (Index i = 0; i < I; ++i)
+            for (int j = 0; j < R; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < R; ++k) acc = std::fma(rhs.v[size_t(i + k * I)], gi[size_t(k + j * R)], acc);
+                out.v[size_t(i + j * I)] = acc;
+            }
+        return out;
     }
     for (Index i = 0; i < I; ++i) ldlt_solve_row(f, R, &rhs.v[size_t(i)], I, &out.v[size_t(i)], I);
     return out;

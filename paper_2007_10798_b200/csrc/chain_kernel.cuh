@@ -272,9 +272,10 @@ __device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, do
 constexpr int kMaxSuperRows = 8;  // superchunk partials prefetched per row entry
 constexpr int kQPre = 3;          // Q pairs per thread prefetched by the Gram finisher
 
-// Row solves of phase 2: warp per row, lanes own entries j and j + 32.  Every
-// load of the row (superchunk partials, P, the mode flag) is issued before the
-// wait for the L / D bulk copy (bar, phase), which none of them depend on.
+// Row solves of phase 2 for R > 32: warp per row, lanes own entries j and j + 32,
+// u = b G^-1 against the explicit inverse the finisher published (Ls).  Every load
+// of the row (superchunk partials, P, the mode flag) is issued before the wait for
+// the bulk copy (bar, phase), which none of them depend on.
 __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
                                              int rows, int R, int nsuper, double* out, const double* Ls,
                                              const double* Ds, uint64_t* bar, unsigned phase,
@@ -328,21 +329,16 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
         if (mode == 0) {
             w0 = 0.0;
             w1 = 0.0;
-        } else {
+        } else {  // u_j = fma chain over k of b_k G^-1(k, j) (Ls holds G^-1, R > 32)
+            double a0 = 0.0, a1 = 0.0;
 #pragma unroll 4
-            for (int k = 0; k < R; ++k) {  // forward, k increasing
-                const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
-                if (v0 && j0 > k) w0 = __fma_rn(-Ls[k * R + j0], wk, w0);
-                if (v1 && j1 > k) w1 = __fma_rn(-Ls[k * R + j1], wk, w1);
+            for (int k = 0; k < R; ++k) {
+                const double bk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+                if (v0) a0 = __fma_rn(bk, Ls[k + j0 * R], a0);
+                if (v1) a1 = __fma_rn(bk, Ls[k + j1 * R], a1);
             }
-            if (v0) w0 = (fabs(Ds[j0]) > 2.2250738585072014e-308) ? w0 / Ds[j0] : 0.0;
-            if (v1) w1 = (fabs(Ds[j1]) > 2.2250738585072014e-308) ? w1 / Ds[j1] : 0.0;
-#pragma unroll 4
-            for (int k = R - 1; k >= 0; --k) {  // backward, k decreasing
-                const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
-                if (j0 < k) w0 = __fma_rn(-Ls[j0 * R + k], wk, w0);
-                if (v1 && j1 < k) w1 = __fma_rn(-Ls[j1 * R + k], wk, w1);
-            }
+            w0 = a0;
+            w1 = a1;
         }
         if (v0) out[int64_t(row) * R + j0] = w0;
         if (v1) out[int64_t(row) * R + j1] = w1;
@@ -1096,11 +1092,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         __syncthreads();
                         reg = s_reg;
                         if (tr) trace_stamp(tr, 11, tid == 0);
-                        for (int t = tid; t < RR; t += blockDim.x) {
-                            const int k = t / R, i = t % R;
-                            p.LD[t] = (i > k) ? A[k * kLdStride + i] : 0.0;
+                        // R > 32: rows against the explicit inverse (form_ginv_block),
+                        // formed here once and published for the row phase
+                        if (s_mode == 1) {
+                            double* gi = sm + 12288;
+                            form_ginv_block(A, kLdStride, D, R, sm + 8192, colb, gi);
+                            for (int t = tid; t < RR; t += blockDim.x) p.LD[t] = gi[t];
                         }
-                        for (int k = tid; k < R; k += blockDim.x) p.LD[RR + k] = D[k];
                     }
                     if (tid == 0) {
                         p.mode_flag[0] = s_mode;

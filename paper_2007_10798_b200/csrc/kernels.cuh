@@ -729,6 +729,66 @@ __device__ __noinline__ void cert_group_warp(const double* L, int ld, int R, int
     }
 }
 
+// Rows of solve_gram for R > 32 (oracle gram_inverse): the explicit
+// inverse, formed once per solve by one block.  inv_unit_lower_warp: columns 8g..8g+7
+// of M = L^-1 (cert_group_warp's substitution) to M(i, j) at M[i + j*R].
+__device__ __noinline__ void inv_unit_lower_warp(const double* L, int ld, int R, int g, double* M) {
+    const int lane = threadIdx.x & 31;
+    const int c0 = 8 * g;
+    double m[2][8];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) m[rb][c] = (lane + 32 * rb == c0 + c) ? 1.0 : 0.0;
+    for (int k = c0; k + 1 < R; ++k) {
+        const int src = k & 31;
+        double mk[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mk[c] = __shfl_sync(0xffffffffu, (k >= 32) ? m[1][c] : m[0][c], src);
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+            const int i = lane + 32 * rb;
+            if (i > k && i < R) {
+                const double l = L[k * ld + i];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) m[rb][c] = __fma_rn(-l, mk[c], m[rb][c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) {
+        const int i = lane + 32 * rb;
+        if (i < R)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c0 + c < R) M[i + (c0 + c) * R] = m[rb][c];
+    }
+}
+
+// G^-1 (i, j) = G^-1 (j, i) = fma chain over k = j..R-1 of M(k, i) (M(k, j) dinv_k), i <= j,
+// by a whole block into Gi (R x R, either layout: symmetric).  M: R x R shared scratch.
+// Block-uniform call.
+__device__ __noinline__ void form_ginv_block(const double* L, int ld, const double* D, int R, double* M,
+                                             double* dinv, double* Gi) {
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp < (R + 7) / 8) inv_unit_lower_warp(L, ld, R, warp, M);
+    for (int k = tid; k < R; k += blockDim.x) dinv[k] = (fabs(D[k]) > 2.2250738585072014e-308) ? 1.0 / D[k] : 0.0;
+    __syncthreads();
+    const int npair = R * (R + 1) / 2;
+    for (int t = tid; t < npair; t += blockDim.x) {
+        // t -> (i, j), i <= j, column by column
+        int j = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+        while (j * (j + 1) / 2 > t) --j;
+        while ((j + 1) * (j + 2) / 2 <= t) ++j;
+        const int i = t - j * (j + 1) / 2;
+        double acc = 0.0;
+        for (int k = j; k < R; ++k) acc = __fma_rn(M[k + i * R], M[k + j * R] * dinv[k], acc);
+        Gi[i + j * R] = acc;
+        Gi[j + i * R] = acc;
+    }
+    __syncthreads();
+}
+
 // One warp: s_i = p_0i + p_1i + ..., t_i = s_i / d_i, v = t_lane + t_{lane+32}, butterfly sum.
 __device__ __noinline__ double cert_combine_warp(const double* part, const double* D, int R) {
     const int lane = threadIdx.x & 31;
@@ -799,12 +859,11 @@ __device__ __noinline__ void jacobi_eigen_block(double* a, int lda, int R, doubl
                 double rotk = 0.0, c = 1.0, sn = 0.0, t = 0.0;
                 if (q < R) {
                     const double apq = a[p + q * lda], app = a[p + p * lda], aqq = a[q + q * lda];
-                    const double thr = 2.220446049250313e-16 * sqrt(fabs(app) * fabs(aqq));
+                    const double thr = 1e-9 * sqrt(fabs(app) * fabs(aqq));  // oracle kJacobiTol
                     if (fabs(apq) > thr) {
-                        const double theta = (aqq - app) / (2.0 * apq);
-                        t = (fabs(theta) > 1e150)
-                                ? 0.5 / theta
-                                : ((theta >= 0.0) ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        const double dl = aqq - app, h = sqrt(dl * dl + 4.0 * (apq * apq));
+                        const double sg = ((dl >= 0.0) == (apq >= 0.0)) ? 1.0 : -1.0;
+                        t = sg * (2.0 * fabs(apq)) / (fabs(dl) + h);
                         c = 1.0 / sqrt(t * t + 1.0);
                         sn = t * c;
                         rotk = 1.0;
@@ -1017,9 +1076,15 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
     }
     if (blockIdx.x == 0 && tid == 0 && s_reg && flags) atomicOr(flags, 1);
 
-    // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64).  Per element the
-    // operation sequence is the row-wise one: forward w_j -= L(j,k) w_k (k increasing), the
-    // diagonal, backward w_j -= L(k,j) w_k (k decreasing) -- the chain's row solves use it too.
+    // R > 32: the explicit inverse (form_ginv_block) in dynamic shared memory
+    extern __shared__ double ks_dyn[];  // MAXR > 32 only: M (R x R), G^-1 (R x R), 1 / d
+    if constexpr (MAXR > 32) {
+        if (s_mode == 1) form_ginv_block(&A[0][0], MAXR + 1, D, R, ks_dyn, ks_dyn + 2 * R * R, ks_dyn + R * R);
+    }
+    // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64).  R <= 32: per element
+    // the row-wise substitution -- forward w_j -= L(j,k) w_k (k increasing), the diagonal,
+    // backward w_j -= L(k,j) w_k (k decreasing), as the narrow chain's row solves; R > 32:
+    // u_j = fma chain over k of b_k G^-1(k, j), as the wide chain's.
     const int lane = tid & 31;
     const int32_t row = int32_t(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
     if (row >= rows) return;
@@ -1029,6 +1094,16 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
     double w1 = v1 ? RHS[int64_t(row) * R + j1] : 0.0;
     if (s_mode == 0) {
         w0 = w1 = 0.0;
+    } else if (MAXR > 32) {
+        const double* Gi = ks_dyn + R * R;
+        double a0 = 0.0, a1 = 0.0;
+        for (int k = 0; k < R; ++k) {
+            const double bk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+            if (v0) a0 = __fma_rn(bk, Gi[k + j0 * R], a0);
+            if (v1) a1 = __fma_rn(bk, Gi[k + j1 * R], a1);
+        }
+        w0 = a0;
+        w1 = a1;
     } else {
         for (int k = 0; k < R; ++k) {
             const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);

@@ -458,7 +458,11 @@ void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const
     }
 }
 
+constexpr int kSolveWideSmem = (3 * 64 * 64) * int(sizeof(double));  // k_solve<64>: M, 1/d, G^-1
+
 void set_contract_smem_attrs() {
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_solve<64>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kSolveWideSmem));
     {
         auto attr = [](const void* f, int rpad) {
             const int b = int((size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * rpad + size_t(8) * rpad * kRowTile) *
@@ -489,7 +493,7 @@ void launch_solve(rocp_dev* dev, const double* G, int R, const double* RHS, int6
     const int grid = int(std::max<int64_t>(1, (rows + 7) / 8));  // a warp per row
     if (R <= 16) k_solve<16><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     else if (R <= 32) k_solve<32><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
-    else k_solve<64><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    else k_solve<64><<<grid, 256, kSolveWideSmem, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     after_launch(dev, "k_solve");
 }
 
@@ -696,9 +700,27 @@ struct Window {
     size_t hX_n = 0;
     int64_t* hbase = nullptr;
     size_t hbase_n = 0;
+    // pageable host-slab path (consume_pageable_host): host-drawn indices, double-buffered
+    // pinned staging so a call's host gather overlaps the previous call's copies and chain
+    int par = 0;
+    double* hXp[2] = {nullptr, nullptr};
+    size_t hXp_n[2] = {0, 0};
+    int32_t* hidxp[2] = {nullptr, nullptr};
+    size_t hidxp_n[2] = {0, 0};
+    std::vector<int64_t> hbase_h;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};  // the copies that last read staging parity p
+    cudaEvent_t chain_ev = nullptr;                 // the last chain that read the window arena
+    std::vector<DrawJob> hdraw;                     // host copies of the window's draw jobs
+    int64_t hdraw_B = -1, hdraw_nb = -1;
     ~Window() {
         host_free_huge(hX, hX_n * sizeof(double));
         if (hbase) cudaFreeHost(hbase);
+        for (int q = 0; q < 2; ++q) {
+            host_free_huge(hXp[q], hXp_n[q] * sizeof(double));
+            if (hidxp[q]) cudaFreeHost(hidxp[q]);
+            if (stage_ev[q]) cudaEventDestroy(stage_ev[q]);
+        }
+        if (chain_ev) cudaEventDestroy(chain_ev);
     }
     // key of the uploaded job list
     const double* key_x = nullptr;
