@@ -224,53 +224,65 @@ Mat contract_of(const Mat& x, const Mat& z) {
 // solve.hpp:15); zero solution when max diag <= 0 (solve.cpp:21-26).
 constexpr double kGramConditionLimit = 1e12;
 
-struct Ldl {
-    std::vector<double> l;  // R x R column-major unit lower (strict part used)
-    std::vector<double> d;  // R
+// solve_gram's factorization in canonical form: the symmetric sweep
+// (Gauss-Jordan elimination without pivoting on the lower triangle), which yields G^-1
+// directly, plus the pivots d_k (the Schur complements, i.e. the LDL^T pivots of G) for the
+// regularisation certificate.  The reference factors with Eigen's LDLT (solve.cpp:34); the
+// row solves here are u = b G^-1 (solve_gram_m), so one elimination replaces the
+// factorization AND the substitutions, and on the device a step is one block barrier,
+// one reciprocal and one fma per entry (kernels.cuh sweep_block).  For k = 0..R-1, with
+// c_x = A(x, k) for x >= k and A(k, x) for x < k (column k through symmetry; A = G +
+// lambda I at the start, lower triangle only) and r = 1 / c_k (0 if |c_k| <= DBL_MIN):
+//   A(i, k) = c_i r (i > k),  A(k, k) = -r,  A(k, j) = fma(c_j, r, +0) (j < k),
+//   A(i, j) = fma(-(c_i r), c_j, A(i, j)) (i >= j, i != k, j != k);
+// then G^-1(i, j) = G^-1(j, i) = -A(i, j).
+struct Sweep {
+    std::vector<double> gi;  // R x R, symmetric: G^-1(i, j) at gi[i + j * R]
+    std::vector<double> d;   // pivots
 };
 
-// Returns the factorization of a (R x R, symmetric, column-major).  Updates
-// only i >= j, then mirrors, so every element sees the same operation sequence.
-Ldl ldlt(const std::vector<double>& a_in, int R) {
-    std::vector<double> a = a_in;
-    Ldl f;
-    f.l.assign(size_t(R) * R, 0.0);
-    f.d.assign(size_t(R), 0.0);
-    std::vector<double> lk(size_t(R), 0.0);
+Sweep gram_sweep(const std::vector<double>& g, int R, double lambda) {
+    std::vector<double> A = g;  // lower triangle used
+    for (int k = 0; k < R; ++k) A[size_t(k + k * R)] = A[size_t(k + k * R)] + lambda;
+    Sweep sw;
+    sw.gi.assign(size_t(R) * R, 0.0);
+    sw.d.assign(size_t(R), 0.0);
+    std::vector<double> c(static_cast<size_t>(R));
     for (int k = 0; k < R; ++k) {
-        const double dk = a[size_t(k + k * R)];
-        f.d[size_t(k)] = dk;
-        for (int i = k + 1; i < R; ++i)
-            lk[size_t(i)] = (dk != 0.0) ? a[size_t(i + k * R)] / dk : 0.0;
-        for (int j = k + 1; j < R; ++j) {
-            const double ajk = a[size_t(j + k * R)];
-            for (int i = j; i < R; ++i)
-                a[size_t(i + j * R)] = std::fma(-lk[size_t(i)], ajk, a[size_t(i + j * R)]);
-        }
-        for (int j = k + 1; j < R; ++j)
-            for (int i = j; i < R; ++i) a[size_t(j + i * R)] = a[size_t(i + j * R)];
-        for (int i = k + 1; i < R; ++i) f.l[size_t(i + k * R)] = lk[size_t(i)];
-        f.l[size_t(k + k * R)] = 1.0;
+        for (int x = 0; x < R; ++x) c[size_t(x)] = (x >= k) ? A[size_t(x + k * R)] : A[size_t(k + x * R)];
+        const double dk = c[size_t(k)];
+        sw.d[size_t(k)] = dk;
+        const double r = (std::fabs(dk) > std::numeric_limits<double>::min()) ? 1.0 / dk : 0.0;
+        for (int j = 0; j < R; ++j)
+            for (int i = j; i < R; ++i) {
+                double& a = A[size_t(i + j * R)];
+                if (j == k) a = (i == k) ? -r : c[size_t(i)] * r;
+                else if (i == k) a = std::fma(c[size_t(j)], r, 0.0);
+                else a = std::fma(-(c[size_t(i)] * r), c[size_t(j)], a);
+            }
     }
-    return f;
+    for (int j = 0; j < R; ++j)
+        for (int i = j; i < R; ++i) sw.gi[size_t(i + j * R)] = sw.gi[size_t(j + i * R)] = -A[size_t(i + j * R)];
+    return sw;
 }
 
 // ---- the regularisation decision (solve.cpp:17-33) ---------------------------
 // The reference decides from the exact eigenvalues of G (SelfAdjointEigenSolver):
 // zero solution if lambda_max <= 0, regularise if lambda_min <= 0 or
 // lambda_max / lambda_min > 1e12.  The canonical form reaches the
-// same decision without an eigensolver whenever a rigorous certificate settles it
-// (pivots d_k > 0 of G = L D L^T):
-//   * lower bound: every pivot of an SPD matrix lies in [lambda_min, lambda_max],
-//     so dmax / dmin <= kappa;
-//   * upper bound: lambda_max <= |G|_inf (max absolute row sum) and
-//     1 / lambda_min = |L^-T D^-1 L^-1|_2 <= |L^-1|_2^2 / dmin <= R |L^-1|_inf^2 / dmin,
-//     with |L^-1|_inf <= max_i y_i, y = (I - |N|)^-1 1 for L = I - N (|L^-1| <= (I - |N|)^-1
-//     entrywise): y_i = 1 + sum_{k<i} |l_ik| y_k, one forward substitution.
+// same decision without an eigensolver whenever a certificate settles it (the sweep's
+// pivots d_k, which are the LDL^T pivots of G, and the G^-1 it yields, gram_sweep above):
+//   * every pivot of an SPD matrix lies in [lambda_min, lambda_max], so
+//     dmax / dmin <= kappa;
+//   * tau = tr(G^-1) = sum_k G^-1(k, k) (k increasing) lies in
+//     [1 / lambda_min, R / lambda_min], and maxdiag <= lambda_max <= |G|_inf, so
+//     maxdiag tau / R <= kappa <= |G|_inf tau.
 // kappa certainly above 4e12 -> regularise; certainly below 2.5e11 -> not; a
 // non-positive max diagonal or pivot, or anything in between -> exact
 // eigenvalues by a deterministic cyclic Jacobi method (the kernels run the same
-// rotations in the same order, so the decision is bitwise shared).
+// rotations in the same order, so the decision is bitwise shared).  The margins
+// (4x either side of 1e12) absorb the rounding of tau, which is relative
+// kappa * 1e-16 at worst.
 constexpr double kCertRegAbove = 4e12;
 constexpr double kCertNoRegBelow = 2.5e11;
 enum { kDecNoReg = 0, kDecReg = 1, kDecExact = 2 };
@@ -299,54 +311,6 @@ double lanes_max(const std::vector<double>& r, int R) {
     return butterfly_max_lanes(v);
 }
 
-// max_i y_i, y_i = 1 + sum_{k<i} |l_ik| y_k: lane i's fma chain in k order.
-double cert_ymax(const Ldl& f, int R) {
-    std::vector<double> y(static_cast<size_t>(R), 1.0);
-    for (int k = 0; k + 1 < R; ++k) {
-        const double yk = y[size_t(k)];
-        for (int i = k + 1; i < R; ++i) y[size_t(i)] = std::fma(std::fabs(f.l[size_t(i + k * R)]), yk, y[size_t(i)]);
-    }
-    return lanes_max(y, R);
-}
-
-// tau = tr(G^-1) = sum_i (sum_j M_ij^2) / d_i from the factorization (M = L^-1),
-// in the kernels' order: columns in groups of 8 (group g = columns 8g..8g+7, one
-// warp, lane i owning rows i and i + 32); each column by forward substitution
-// (updates in k order; the steps k < j leave column j unchanged); per row a
-// group partial p_gi = fma chain over the group's columns; s_i = p_0i + p_1i + ...;
-// t_i = s_i / d_i; v_lane = t_lane + t_{lane+32} (+0 past R); a 32-lane butterfly sum.
-double cert_tau(const Ldl& f, int R) {
-    const int ng = (R + 7) / 8;
-    std::vector<double> s(64, 0.0);
-    std::vector<double> m(static_cast<size_t>(R));
-    for (int g = 0; g < ng; ++g) {
-        std::vector<double> p(static_cast<size_t>(R), 0.0);
-        for (int j = 8 * g; j < std::min(R, 8 * g + 8); ++j) {
-            for (int i = 0; i < R; ++i) m[size_t(i)] = (i == j) ? 1.0 : 0.0;
-            for (int k = 0; k + 1 < R; ++k) {
-                const double mk = m[size_t(k)];
-                for (int i = k + 1; i < R; ++i)
-                    m[size_t(i)] = std::fma(-f.l[size_t(i + k * R)], mk, m[size_t(i)]);
-            }
-            for (int i = 0; i < R; ++i) p[size_t(i)] = std::fma(m[size_t(i)], m[size_t(i)], p[size_t(i)]);
-        }
-        for (int i = 0; i < R; ++i) s[size_t(i)] = (g == 0) ? p[size_t(i)] : s[size_t(i)] + p[size_t(i)];
-    }
-    std::vector<double> v(32, 0.0);
-    for (int l = 0; l < 32; ++l) {
-        const double t0 = (l < R) ? s[size_t(l)] / f.d[size_t(l)] : 0.0;
-        const double t1 = (l + 32 < R) ? s[size_t(l + 32)] / f.d[size_t(l + 32)] : 0.0;
-        v[size_t(l)] = t0 + t1;
-    }
-    std::vector<double> w = v;
-    for (int off = 16; off >= 1; off >>= 1) {
-        std::vector<double> u(32);
-        for (int l = 0; l < 32; ++l) u[size_t(l)] = w[size_t(l)] + w[size_t(l ^ off)];
-        w = u;
-    }
-    return w[0];
-}
-
 // |G|_inf: row i's absolute sum in column order, max over rows.
 double gram_inf_norm(const std::vector<double>& g, int R) {
     std::vector<double> rs(static_cast<size_t>(R), 0.0);
@@ -358,12 +322,13 @@ double gram_inf_norm(const std::vector<double>& g, int R) {
     return lanes_max(rs, R);
 }
 
-int64_t g_decision_paths[5] = {0, 0, 0, 0, 0};  // test statistics (orc_decision_stats); [3]: tier 2 used, [4]: Jacobi sweeps
+// test statistics (orc_decision_stats): [0] no-reg, [1] reg, [2] exact, [3] settled by
+// the tau bounds (the pivot ratio did not settle it), [4] Jacobi sweeps
+int64_t g_decision_paths[5] = {0, 0, 0, 0, 0};
 
-// Tier 1 (every Gram, folded into the factorization on the device): pivots and ymax.
-// Tier 2 (only when tier 1 leaves the band, i.e. kappa within a few decades of the
-// limit): tau = tr(G^-1), maxdiag tau / R <= kappa <= |G|_inf tau.  Tier 3: Jacobi.
-int certificate(double maxdiag, double gnorm, const Ldl& f, int R) {
+// The certificate: pivot ratio, then the tau bounds from the unregularised inverse gi.
+int certificate(double maxdiag, double gnorm, const Sweep& f, int R) {
+    const std::vector<double>& gi = f.gi;
     double dmin = f.d[0], dmax = f.d[0];
     for (double x : f.d) {
         if (x < dmin) dmin = x;
@@ -372,15 +337,13 @@ int certificate(double maxdiag, double gnorm, const Ldl& f, int R) {
     if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
     const double ratio = dmax / dmin;
     if (ratio > kCertRegAbove) return kDecReg;
-    const double ym = cert_ymax(f, R);
-    const double khi = ((gnorm / dmin) * double(R)) * (ym * ym);
-    if (khi <= kCertNoRegBelow) return kDecNoReg;
     ++g_decision_paths[3];
-    const double tau = cert_tau(f, R);
-    const double klo2 = (maxdiag * tau) / double(R);
-    const double khi2 = gnorm * tau;
-    if (klo2 > kCertRegAbove) return kDecReg;
-    if (khi2 <= kCertNoRegBelow) return kDecNoReg;
+    double tau = gi[0];
+    for (int k = 1; k < R; ++k) tau = tau + gi[size_t(k + k * R)];
+    const double klo = (maxdiag * tau) / double(R);
+    const double khi = gnorm * tau;
+    if (klo > kCertRegAbove) return kDecReg;
+    if (khi <= kCertNoRegBelow) return kDecNoReg;
     return kDecExact;
 }
 
@@ -517,7 +480,7 @@ struct GramDecision {
     int path = 0;
 };
 
-GramDecision decide_gram(const std::vector<double>& g, int R, double maxdiag, const Ldl& f) {
+GramDecision decide_gram(const std::vector<double>& g, int R, double maxdiag, const Sweep& f) {
     GramDecision dec;
     dec.path = certificate(maxdiag, gram_inf_norm(g, R), f, R);
     ++g_decision_paths[dec.path];
@@ -537,62 +500,8 @@ GramDecision decide_gram(const std::vector<double>& g, int R, double maxdiag, co
     return dec;
 }
 
-// Solves y^T G = b^T for one row b (length R): forward L, diagonal, backward L^T.
-void ldlt_solve_row(const Ldl& f, int R, const double* b, Index bstride, double* y,
-                    Index ystride) {
-    std::vector<double> w(static_cast<size_t>(R));
-    for (int j = 0; j < R; ++j) {
-        double acc = b[size_t(j) * bstride];
-        for (int k = 0; k < j; ++k) acc = std::fma(-f.l[size_t(j + k * R)], w[size_t(k)], acc);
-        w[size_t(j)] = acc;
-    }
-    for (int j = 0; j < R; ++j) {
-        const double dj = f.d[size_t(j)];
-        w[size_t(j)] = (std::fabs(dj) > std::numeric_limits<double>::min()) ? w[size_t(j)] / dj
-                                                                            : 0.0;
-    }
-    // Backward substitution, updates applied in DEcreasing k.
-    for (int j = R - 1; j >= 0; --j) {
-        double acc = w[size_t(j)];
-        for (int k = R - 1; k > j; --k)
-            acc = std::fma(-f.l[size_t(k + j * R)], w[size_t(k)], acc);
-        w[size_t(j)] = acc;
-    }
-    for (int j = 0; j < R; ++j) y[size_t(j) * ystride] = w[size_t(j)];
-}
-
-// Rows of solve_gram for R > 32: u = b G^-1 with the explicit inverse
-// formed once per solve, so the kernels solve thousands of rows as a skinny GEMM
-// instead of 2R-step substitutions.  M = L^-1 column by column (forward substitution,
-// updates in k order, as cert_tau), dinv_k = 1 / d_k (0 if |d_k| <= DBL_MIN), then
-// G^-1(i, j) = G^-1(j, i) = fma chain over k = j..R-1 of M(k, i) (M(k, j) dinv_k) for
-// i <= j; a row is u_j = fma chain over k = 0..R-1 of b_k G^-1(k, j) from +0.0.
-constexpr int kRowsByInverseAbove = 32;
-
-std::vector<double> gram_inverse(const Ldl& f, int R) {
-    std::vector<double> M(size_t(R) * R, 0.0), gi(size_t(R) * R, 0.0);
-    std::vector<double> m(static_cast<size_t>(R));
-    for (int j = 0; j < R; ++j) {
-        for (int i = 0; i < R; ++i) m[size_t(i)] = (i == j) ? 1.0 : 0.0;
-        for (int k = 0; k + 1 < R; ++k) {
-            const double mk = m[size_t(k)];
-            for (int i = k + 1; i < R; ++i) m[size_t(i)] = std::fma(-f.l[size_t(i + k * R)], mk, m[size_t(i)]);
-        }
-        for (int i = 0; i < R; ++i) M[size_t(i + j * R)] = m[size_t(i)];
-    }
-    std::vector<double> dinv(static_cast<size_t>(R));
-    for (int k = 0; k < R; ++k)
-        dinv[size_t(k)] = (std::fabs(f.d[size_t(k)]) > std::numeric_limits<double>::min()) ? 1.0 / f.d[size_t(k)] : 0.0;
-    for (int j = 0; j < R; ++j)
-        for (int i = 0; i <= j; ++i) {
-            double acc = 0.0;
-            for (int k = j; k < R; ++k) acc = std::fma(M[size_t(k + i * R)], M[size_t(k + j * R)] * dinv[size_t(k)], acc);
-            gi[size_t(i + j * R)] = acc;
-            gi[size_t(j + i * R)] = acc;
-        }
-    return gi;
-}
-
+// solve_gram (solve.cpp:9-35) in canonical form: the sweep of G, the decision, the sweep of
+// G + 1e-12 tr(G) I when it regularises; rows u_j = fma chain over k of b_k G^-1(k, j).
 Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path = nullptr) {
     const int R = int(gram.rows);
     const Index I = rhs.rows;
@@ -602,7 +511,7 @@ Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path =
         if (gram(k, k) > maxdiag) maxdiag = gram(k, k);
     double tr = gram(0, 0);
     for (int k = 1; k < R; ++k) tr = tr + gram(k, k);
-    Ldl f = ldlt(gram.v, R);
+    Sweep f = gram_sweep(gram.v, R, 0.0);
     const GramDecision dec = decide_gram(gram.v, R, maxdiag, f);
     if (path) *path = dec.path;
     if (dec.mode == 0) {  // solve.cpp:21-26
@@ -610,23 +519,16 @@ Mat solve_gram_m(const Mat& gram, const Mat& rhs, bool* regularized, int* path =
         return out;
     }
     if (dec.reg) {  // solve.cpp:28-33
-        const double lambda = 1e-12 * tr;
-        std::vector<double> g = gram.v;
-        for (int k = 0; k < R; ++k) g[size_t(k + k * R)] = g[size_t(k + k * R)] + lambda;
-        f = ldlt(g, R);
+        f = gram_sweep(gram.v, R, 1e-12 * tr);
         if (regularized) *regularized = true;
     }
-    if (R > kRowsByInverseAbove) {  // wide ranks: rows against the explicit inverse
-        const std::vector<double> gi = gram_inverse(f, R);
-        for (Index i = 0; i < I; ++i)
-            for (int j = 0; j < R; ++j) {
-                double acc = 0.0;
-                for (int k = 0; k < R; ++k) acc = std::fma(rhs.v[size_t(i + k * I)], gi[size_t(k + j * R)], acc);
-                out.v[size_t(i + j * I)] = acc;
-            }
-        return out;
-    }
-    for (Index i = 0; i < I; ++i) ldlt_solve_row(f, R, &rhs.v[size_t(i)], I, &out.v[size_t(i)], I);
+    const std::vector<double>& gi = f.gi;
+    for (Index i = 0; i < I; ++i)
+        for (int j = 0; j < R; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < R; ++k) acc = std::fma(rhs.v[size_t(i + k * I)], gi[size_t(k + j * R)], acc);
+            out.v[size_t(i + j * I)] = acc;
+        }
     return out;
 }
 
@@ -1007,7 +909,7 @@ int orc_gram_decision(const double* gram, int rank, int* mode, int* regularized,
         if (g(k, k) > maxdiag) maxdiag = g(k, k);
         tr = tr + g(k, k);
     }
-    const Ldl f = ldlt(g.v, rank);
+    const Sweep f = gram_sweep(g.v, rank, 0.0);
     const GramDecision dec = decide_gram(g.v, rank, maxdiag, f);
     if (mode) *mode = dec.mode;
     if (regularized) *regularized = dec.reg ? 1 : 0;

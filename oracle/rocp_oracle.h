@@ -88,8 +88,8 @@ int orc_solve_gram(const double* gram, const double* rhs, int64_t rows, int rank
  * (no-reg / reg), 2 = exact (cyclic Jacobi) eigenvalues.  lo/hi: the Jacobi
  * eigenvalue extremes (always computed here, for tests). */
 /* How many solve_gram decisions took each certificate path since the last reset
- * (0 no-reg, 1 reg, 2 exact eigenvalues; [3] = decisions that needed the tier-2
- * tr(G^-1) certificate); test statistics.  counts: 5 entries ([4] = Jacobi sweeps run). */
+ * (0 no-reg, 1 reg, 2 exact eigenvalues; [3] = decisions the pivot ratio did not
+ * settle, i.e. that reached the tr(G^-1) bounds); test statistics.  counts: 5 entries ([4] = Jacobi sweeps run). */
 void orc_decision_stats(int64_t* counts, int reset);
 int orc_gram_decision(const double* gram, int rank, int* mode, int* regularized, int* path, double* lo,
                       double* hi);

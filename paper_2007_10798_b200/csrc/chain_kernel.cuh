@@ -24,7 +24,8 @@ namespace rocpk {
 //                  variant for R in 33..64, k_chain<true, .>)
 //                - the Gram finisher: chunk partials summed in order (one TMA
 //                  bulk copy when they fit, else 4 pre-combine blocks), Q += G,
-//                  canonical LDL^T (ldlt_warp for R <= 32), publishes L, D | grid barrier
+//                  solve_gram in canonical form (the sweep, kernels.cuh gram_solve_block),
+//                  publishes G^-1                                        | grid barrier
 //   phase B      warp per row: superchunk partials in order, P += X_s Z,
 //                forward / diagonal / backward solve -> U(n) or u_new row | grid barrier
 // Arithmetic is exactly that of the per-stage kernels (bitwise equal).
@@ -63,6 +64,12 @@ struct ChainParams {
     // published / needed; nullptr when the window was gathered before the launch
     const unsigned* gdone;
     const unsigned* gneed;
+    // k_flow (flow_kernel.cuh) only
+    double* ginv;     // 2 slots of G^-1 (stage parity)
+    int* gmode;       // 2 mode flags (0 = zero solution)
+    double* wtemp;    // B x R summed temporal right-hand sides of the current batch
+    unsigned* fctr;   // dependency counters (flow_kernel.cuh)
+    int maxtiles;     // row tiles of the largest stage
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
@@ -96,7 +103,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Trace stamp: every thread of the (uniform) caller reads the timer and only
 // 'who' stores, through a predicated store (no branch), so no lane diverges
 // from its warp.  A lane-0-only timer read in
-// front of a warp-synchronous device call (ldlt_warp) left the warp split for
+// front of a warp-synchronous device call (a warp LDL^T) left the warp split for
 // the whole call and made it 4x slower in traced runs.
 __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int slot, bool who) {
     const unsigned long long t = gtimer();
@@ -149,136 +156,16 @@ constexpr int kLdStride = 65;  // smem row stride of the factorization triangle 
 constexpr int kMaxPairsPerThread = (64 * 65 / 2 + kChainThreads - 1) / kChainThreads;
 
 
-// Canonical LDL^T of G (R x R column-major in smem) by one block, one barrier
-// per pivot step; same per-element operation sequence as k_solve / the oracle.
-// Thread t owns the lower-triangle pairs t, t + 256, ... (column order).
-// d_{k+1} is formed redundantly in registers by every thread that needs it
-// (its last update), so the diagonal entry is never written in the step that
-// finishes it.  L(i,k) at A[k*kLdStride + i].
-__device__ __noinline__ void ldlt_one_sync(double* A, double* D, int R, double lambda, const double* G,
-                                           const unsigned short* pairs, int npairs) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    int pi[kMaxPairsPerThread], pj[kMaxPairsPerThread];
-#pragma unroll
-    for (int u = 0; u < kMaxPairsPerThread; ++u) {
-        const int pp = tid + u * nt;
-        pi[u] = (pp < npairs) ? (pairs[pp] >> 8) : -1;
-        pj[u] = (pp < npairs) ? (pairs[pp] & 0xff) : -1;
-    }
-    for (int t = tid; t < R * R; t += nt) {
-        const int i = t % R, j = t / R;
-        if (i >= j) A[i * kLdStride + j] = (i == j) ? G[t] + lambda : G[t];
-    }
-    __syncthreads();
-    const double d0 = A[0];
-    if (tid == 0) D[0] = d0;
-    for (int i = 1 + tid; i < R; i += nt) A[i] = (d0 != 0.0) ? A[i * kLdStride] / d0 : 0.0;
-    __syncthreads();
-    for (int k = 0; k + 1 < R; ++k) {
-        const double* rowk = A + k * kLdStride;  // L(., k) in the strict upper part
-        const double dn = __fma_rn(-rowk[k + 1], A[(k + 1) * kLdStride + k], A[(k + 1) * kLdStride + k + 1]);
-        if (tid == 0) D[k + 1] = dn;
-#pragma unroll
-        for (int u = 0; u < kMaxPairsPerThread; ++u) {
-            const int i = pi[u], j = pj[u];
-            if (j > k && !(i == j && j == k + 1)) {
-                const double v = __fma_rn(-rowk[i], A[j * kLdStride + k], A[i * kLdStride + j]);
-                if (j == k + 1) A[(k + 1) * kLdStride + i] = (dn != 0.0) ? v / dn : 0.0;
-                A[i * kLdStride + j] = v;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Canonical LDL^T for R <= MAXR <= 32 by ONE warp, no block barriers: lane i
-// holds row i of the lower triangle in registers.  Step k: d_k = lane k's
-// r[k] (final), l(i,k) = r[k] / d_k on lanes i > k, then r[j] = fma(-l(i,k),
-// a(j,k), r[j]) for k < j <= i with a(j,k) = lane j's r[k].  Identical
-// per-element operation sequence to ldlt_one_sync / k_solve / the oracle.
-//
-// Software-pipelined so a step's critical path is divide -> the single fma
-// that finishes the next pivot column entry -> shuffle of d_{k+1}: the other
-// updates of step k (j >= k+2) are deferred to step k+1, where they fill the
-// shuffle latency before the next divide, and column k+1 is read from shared
-// memory (published one step ahead) while the divide runs.  Upper-triangle
-// registers and lanes >= R receive harmless updates but are never read as
-// lower entries; dividends of inactive lanes are 1.0 (a zero dividend takes
-// the divide's slow path).
-//
-// L(i,k) goes to L[k*ldl + i] (i > k only) and d_k to D[k].  dmm (if set)
-// receives min_k d_k, max_k d_k, formed with the same compare sequence as the
-// solve_gram condition check (solve.cpp:24-31) from the broadcast d_k.
-template <int MAXR>
-__device__ __noinline__ void ldlt_warp(const double* G, double lambda, int R, double* L, int ldl, double* D,
-                                       double* col, double* dmm) {
-    // col: three 32-entry column buffers; column k lives in col[(k % 3) * 32]
-    // from step k-1 (published) to step k+1 (read by the deferred updates).
-    // The fmas read the broadcast column straight from shared memory (no
-    // register copy, which the compiler would place in local memory).
-    const int lane = threadIdx.x & 31;
-    double r[MAXR];
-    // branch-free: every load is issued (clamped index), then selected
-#pragma unroll
-    for (int j = 0; j < MAXR; ++j) {
-        const bool ok = lane < R && j <= lane;
-        const double g = G[ok ? lane + j * R : 0];
-        const double gl = g + lambda;
-        r[j] = ok ? ((j == lane) ? gl : g) : 0.0;
-    }
-    col[lane] = r[0];
-    __syncwarp();
-    double dk = __shfl_sync(0xffffffffu, r[0], 0);
-    double lp = 0.0;  // l(lane, k-1)
-    double dmin = dk, dmax = dk;
-#pragma unroll
-    for (int k = 0; k < MAXR; ++k) {
-        if (k < R) {
-            if (dk < dmin) dmin = dk;
-            if (dk > dmax) dmax = dk;
-            const double* cb = col + (k % 3) * 32;  // column k
-            // a(k+1, k) in a register before the divide: the load would
-            // otherwise sit between the quotient and the critical fma
-            const double ck1 = (k + 1 < MAXR) ? cb[k + 1] : 0.0;
-            if (k > 0) {  // deferred updates of step k-1 (j >= k+1): fill the shuffle latency
-                const double* cp = col + ((k + 2) % 3) * 32;  // column k-1
-#pragma unroll
-                for (int j = k + 1; j < MAXR; ++j) r[j] = __fma_rn(-lp, cp[j], r[j]);
-            }
-            const bool act = lane > k && lane < R;
-            const bool use = act && dk != 0.0;  // known before the quotient
-            const double num = act ? r[k] : 1.0;
-            const double q = num / dk;
-            const double l = use ? q : 0.0;
-            double dn = 0.0;
-            if (k + 1 < MAXR) {  // critical: finish a(., k+1), broadcast d_{k+1}, publish column k+1
-                r[k + 1] = __fma_rn(-l, ck1, r[k + 1]);
-                dn = __shfl_sync(0xffffffffu, r[k + 1], (k + 1) & 31);
-                col[((k + 1) % 3) * 32 + lane] = r[k + 1];
-            }
-            if (lane == 0) D[k] = dk;
-            if (act) L[k * ldl + lane] = l;
-            __syncwarp();
-            lp = l;
-            dk = dn;
-        }
-    }
-    if (dmm != nullptr && lane == 0) {
-        dmm[0] = dmin;
-        dmm[1] = dmax;
-    }
-}
-
 constexpr int kMaxSuperRows = 8;  // superchunk partials prefetched per row entry
 constexpr int kQPre = 3;          // Q pairs per thread prefetched by the Gram finisher
 
-// Row solves of phase 2 for R > 32: warp per row, lanes own entries j and j + 32,
-// u = b G^-1 against the explicit inverse the finisher published (Ls).  Every load
+// Row solves of phase B: warp per row, lanes own entries j and j + 32, u = b G^-1
+// against the explicit inverse the finisher published (Ls).  Every load
 // of the row (superchunk partials, P, the mode flag) is issued before the wait for
 // the bulk copy (bar, phase), which none of them depend on.
 __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, double* Prow_base, int st,
                                              int rows, int R, int nsuper, double* out, const double* Ls,
-                                             const double* Ds, uint64_t* bar, unsigned phase,
+                                             uint64_t* bar, unsigned phase,
                                              const int* mode_flag) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int j0 = lane, j1 = lane + 32;
@@ -342,72 +229,6 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
         }
         if (v0) out[int64_t(row) * R + j0] = w0;
         if (v1) out[int64_t(row) * R + j1] = w1;
-    }
-    if (!ld_ready) mbar_wait(bar, phase);  // the phase completes before the barrier's next use
-}
-
-// Row solves for R <= MAXR <= 32 (one entry per lane): the lane's L entries
-// live in registers and the k loop is unrolled (compile-time shuffle source,
-// uniform exit at k = R), so a substitution step is one shuffle and one fma;
-// same per-element operation sequence as chain_rows_warp.
-template <int MAXR>
-__device__ __noinline__ void chain_rows_narrow(const double* __restrict__ cpart, double* Prow_base, int st,
-                                               int rows, int R, int nsuper, double* out, const double* Ls,
-                                               const double* Ds, uint64_t* bar, unsigned phase,
-                                               const int* mode_flag) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int j0 = lane;
-    const bool v0 = j0 < R;
-    const int mode = __ldcg(mode_flag);
-    bool ld_ready = false;
-    for (int row = blockIdx.x + warp * gridDim.x; row < rows; row += gridDim.x * nw) {
-        double c0[kMaxSuperRows], p0 = 0.0;
-#pragma unroll
-        for (int m = 0; m < kMaxSuperRows; ++m)
-            c0[m] = (v0 && m < nsuper) ? __ldcg(cpart + (int64_t(m) * rows + row) * R + j0) : 0.0;
-        if (st > 0 && v0) p0 = __ldcg(Prow_base + int64_t(row) * R + j0);
-        if (!ld_ready) {
-            mbar_wait(bar, phase);
-            ld_ready = true;
-        }
-        double lf[MAXR];  // L(j0, k), k < j0 (forward)
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) lf[k] = (k < R && v0 && j0 > k) ? Ls[k * R + j0] : 0.0;
-        double w0 = 0.0;
-        if (v0) {
-            double tot = c0[0];
-#pragma unroll
-            for (int m = 1; m < kMaxSuperRows; ++m)
-                if (m < nsuper) tot = tot + c0[m];
-            for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cpart + (int64_t(m) * rows + row) * R + j0);
-            if (st > 0) {
-                tot = p0 + tot;
-                Prow_base[int64_t(row) * R + j0] = tot;
-            }
-            w0 = tot;
-        }
-        if (mode == 0) {
-            w0 = 0.0;
-        } else {
-#pragma unroll
-            for (int k = 0; k < MAXR; ++k) {  // forward, k increasing
-                if (k >= R) break;
-                const double wk = __shfl_sync(0xffffffffu, w0, k);
-                if (v0 && j0 > k) w0 = __fma_rn(-lf[k], wk, w0);
-            }
-            double lb[MAXR];  // L(k, j0), k > j0 (backward); loads land under the divide
-#pragma unroll
-            for (int k = 0; k < MAXR; ++k) lb[k] = (k < R && j0 < k) ? Ls[j0 * R + k] : 0.0;
-            if (v0) w0 = (fabs(Ds[j0]) > 2.2250738585072014e-308) ? w0 / Ds[j0] : 0.0;
-#pragma unroll
-            for (int k = MAXR - 1; k >= 0; --k) {  // backward, k decreasing
-                if (k < R) {
-                    const double wk = __shfl_sync(0xffffffffu, w0, k);
-                    if (j0 < k) w0 = __fma_rn(-lb[k], wk, w0);
-                }
-            }
-        }
-        if (v0) out[int64_t(row) * R + j0] = w0;
     }
     if (!ld_ready) mbar_wait(bar, phase);  // the phase completes before the barrier's next use
 }
@@ -638,9 +459,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     extern __shared__ __align__(128) double sm[];
     __shared__ unsigned short pairs[64 * 65 / 2];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ int s_mode, s_reg;
-    __shared__ double s_tr, s_maxdiag;
-    __shared__ double s_ymax, s_gnorm, s_tau;  // regularisation certificate (kernels.cuh gram_certificate)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
     const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
@@ -875,7 +693,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     double* A = sm + kSmFact;        // [64][65]
                     double* D = A + 64 * kLdStride;  // 64
                     double* Gs = D + 64;             // R x R column-major
-                    double* colb = Gs + 64 * 64;     // 3 x 32 (ldlt_warp column buffers)
+                    double* colb = Gs + 64 * 64;     // 128: the sweep's column buffers
                     // total = superchunk sums in order; Q += G for the modes (rocp.cpp:108)
                     double* chs = sm;  // gram_one: every chunk partial, one TMA bulk copy (nch x NPp <= 16384)
                     if (gram_one && tid == 0) {
@@ -939,167 +757,24 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     }
                     __syncthreads();
                     if (tr) trace_stamp(tr, 10, tid == 0);
-                    int reg;
-                    if constexpr (!kWide) {  // R <= 32 (the wide instance serves R > 32)
-                        // warp 0 factors G at once (the condition check's min / max of D formed
-                        // in the pivot loop) while warp 1 forms the solve_gram prologue
-                        // (solve.cpp:9-22); with maxdiag <= 0 the factors are never read (mode
-                        // 0), so starting early changes nothing
-                        double* dmm = D + 61;  // min d, max d, ymax (D holds R <= 32 entries)
-                        auto factor_w = [&](double lambda, double* mm) {
-                            if (R <= 8) ldlt_warp<8>(Gs, lambda, R, A, kLdStride, D, colb, mm);
-                            else if (R <= 16) ldlt_warp<16>(Gs, lambda, R, A, kLdStride, D, colb, mm);
-                            else if (R <= 24) ldlt_warp<24>(Gs, lambda, R, A, kLdStride, D, colb, mm);
-                            else ldlt_warp<32>(Gs, lambda, R, A, kLdStride, D, colb, mm);
-                        };
-                        if (tr) trace_stamp(tr, 12, tid == 0);
-                        if (warp == 0) {
-                            factor_w(0.0, dmm);
-                        } else if (warp == 1) {
-                            if (lane == 0) {
-                                double maxdiag = Gs[0], trc = Gs[0];
-#pragma unroll 8
-                                for (int k = 1; k < R; ++k) {
-                                    const double dg = Gs[k * R + k];
-                                    if (dg > maxdiag) maxdiag = dg;
-                                    trc = trc + dg;
-                                }
-                                s_tr = trc;
-                                s_maxdiag = maxdiag;
-                            }
-                            __syncwarp();
-                        } else if (warp == 2) {
-                            const double gn = gram_inf_norm_warp(Gs, R, R);
-                            if (lane == 0) s_gnorm = gn;
-                        }
-                        __syncthreads();
-                        if (tr) trace_stamp(tr, 13, tid == 0);
-                        // solve_gram's regularisation decision (solve.cpp:17-33): warp 0 forms the
-                        // tier-1 certificate's ymax while the other warps publish the unregularised
-                        // L and D (republished below in the rare regularised case)
-                        if (warp == 0) {
-                            const double y = cert_ymax_warp(A, kLdStride, R);
-                            if (lane == 0) dmm[2] = y;
-                        } else {
-                            for (int t = tid - 32; t < RR; t += blockDim.x - 32) {
-                                const int k = t / R, i = t - k * R;
-                                if (i > k) p.LD[t] = A[k * kLdStride + i];
-                            }
-                            if (tid - 32 < R) p.LD[RR + tid - 32] = D[tid - 32];
-                        }
-                        __syncthreads();
-                        int path = gram_certificate(s_maxdiag, s_gnorm, dmm[0], dmm[1], dmm[2], R);
-                        const bool tier2 = path == kDecTier2;
-                        if (tier2)  // rare: tr(G^-1) in the free chunk area
-                            path = gram_tier2_block<1>(A, kLdStride, D, R, s_maxdiag, s_gnorm, sm + 8192, &s_tau);
-                        if (tid == 0) count_decision(path, tier2);
-                        if (path == kDecExact) {  // rare: Jacobi on a copy of G in the free chunk area
-                            double* ja = sm;
-                            for (int t = tid; t < RR; t += blockDim.x) ja[t] = Gs[t];
-                            __syncthreads();
-                            double lo, hi;
-                            jacobi_eigen_block(ja, R, R, sm + 8192, &s_reg, &lo, &hi);
-                            if (tid == 0) {
-                                int md, rg;
-                                exact_decision(lo, hi, &md, &rg);
-                                s_mode = md;
-                                s_reg = rg;
-                            }
-                            __syncthreads();
-                            reg = s_reg;
-                        } else {
-                            if (tid == 0) s_mode = 1;
-                            reg = (path == kDecReg) ? 1 : 0;
-                        }
-                        __syncthreads();
-                        if (s_mode == 1 && reg) {
-                            if (warp == 0) factor_w(1e-12 * s_tr, nullptr);
-                            __syncthreads();
-                            // publish the regularised strictly lower L and D instead
-                            for (int t = tid; t < RR; t += blockDim.x) {
-                                const int k = t / R, i = t - k * R;
-                                if (i > k) p.LD[t] = A[k * kLdStride + i];
-                            }
-                            if (tid < R) p.LD[RR + tid] = D[tid];
-                        }
-                        if (tr) trace_stamp(tr, 11, tid == 0);
+                    // solve_gram (solve.cpp:9-35) in canonical form: the sweep of G, the
+                    // regularisation decision, the regularised sweep when it applies
+                    // (kernels.cuh gram_solve_block); G^-1 feeds the row solves of phase B
+                    double* gi = sm + 12288;
+                    if (tr) trace_stamp(tr, 12, tid == 0);
+                    int2 mr;
+                    if constexpr (!kWide) {
+                        if (npairs <= 256) mr = gram_solve_block<1>(Gs, R, gi, D, colb, sm, true);
+                        else if (npairs <= 512) mr = gram_solve_block<2>(Gs, R, gi, D, colb, sm, true);
+                        else mr = gram_solve_block<3>(Gs, R, gi, D, colb, sm, true);
                     } else {
-                        // canonical solve_gram prologue (solve.cpp:9-35; same sequence as k_solve)
-                        if (tid == 0) {
-                            double maxdiag = Gs[0], trc = Gs[0];
-#pragma unroll 8
-                            for (int k = 1; k < R; ++k) {
-                                const double dg = Gs[k * R + k];
-                                if (dg > maxdiag) maxdiag = dg;
-                                trc = trc + dg;
-                            }
-                            s_tr = trc;
-                            s_maxdiag = maxdiag;
-                        }
-                        __syncthreads();
-                        if (tr) trace_stamp(tr, 12, tid == 0);
-                        ldlt_one_sync(A, D, R, 0.0, Gs, pairs, npairs);
-                        if (tr) trace_stamp(tr, 13, tid == 0);
-                        // regularisation decision (solve.cpp:17-33): certificate over two warps
-                        // (columns 0..31, 32..63), exact eigenvalues in the band
-                        if (warp == 0) {
-                            const double y = cert_ymax_warp(A, kLdStride, R);
-                            if (lane == 0) s_ymax = y;
-                        } else if (warp == 1) {
-                            const double gn = gram_inf_norm_warp(Gs, R, R);
-                            if (lane == 0) s_gnorm = gn;
-                        }
-                        __syncthreads();
-                        if (tid == 0) {
-                            double dmin = D[0], dmax = D[0];
-#pragma unroll 8
-                            for (int k = 0; k < R; ++k) {
-                                const double dk = D[k];
-                                if (dk < dmin) dmin = dk;
-                                if (dk > dmax) dmax = dk;
-                            }
-                            s_mode = gram_certificate(s_maxdiag, s_gnorm, dmin, dmax, s_ymax, R);
-                        }
-                        __syncthreads();
-                        {
-                            int path = s_mode;
-                            const bool tier2 = path == kDecTier2;
-                            if (tier2)  // rare: tr(G^-1) in the free chunk area
-                                path = gram_tier2_block<2>(A, kLdStride, D, R, s_maxdiag, s_gnorm, sm + 8192, &s_tau);
-                            if (tid == 0) count_decision(path, tier2);
-                            __syncthreads();
-                            if (tid == 0) {
-                                s_mode = (path == kDecExact) ? -1 : 1;
-                                s_reg = (path == kDecReg) ? 1 : 0;
-                            }
-                        }
-                        __syncthreads();
-                        if (s_mode < 0) {  // rare: Jacobi on a copy of G in the free chunk area
-                            double* ja = sm;
-                            for (int t = tid; t < RR; t += blockDim.x) ja[t] = Gs[t];
-                            __syncthreads();
-                            double lo, hi;
-                            jacobi_eigen_block(ja, R, R, sm + 8192, &s_reg, &lo, &hi);
-                            if (tid == 0) {
-                                int md, rg;
-                                exact_decision(lo, hi, &md, &rg);
-                                s_mode = md;
-                                s_reg = rg;
-                            }
-                            __syncthreads();
-                        }
-                        if (s_mode == 1 && s_reg) ldlt_one_sync(A, D, R, 1e-12 * s_tr, Gs, pairs, npairs);
-                        __syncthreads();
-                        reg = s_reg;
-                        if (tr) trace_stamp(tr, 11, tid == 0);
-                        // R > 32: rows against the explicit inverse (form_ginv_block),
-                        // formed here once and published for the row phase
-                        if (s_mode == 1) {
-                            double* gi = sm + 12288;
-                            form_ginv_block(A, kLdStride, D, R, sm + 8192, colb, gi);
-                            for (int t = tid; t < RR; t += blockDim.x) p.LD[t] = gi[t];
-                        }
+                        if (npairs <= 1280) mr = gram_solve_block<5>(Gs, R, gi, D, colb, sm, true);
+                        else mr = gram_solve_block<9>(Gs, R, gi, D, colb, sm, true);
                     }
+                    const int s_mode = mr.x, reg = mr.y;
+                    if (tr) trace_stamp(tr, 11, tid == 0);
+                    if (s_mode == 1)
+                        for (int t = tid; t < RR; t += blockDim.x) p.LD[t] = gi[t];
                     if (tid == 0) {
                         p.mode_flag[0] = s_mode;
                         if (reg) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
@@ -1191,14 +866,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (tr) trace_stamp(tr, 16, blockIdx.x == 0 && tid == 0);
                     double* out = (st == 0) ? u_new : p.U[st - 1];
                     double* Pst = st > 0 ? p.P[st - 1] : nullptr;
-                    if constexpr (kWide) {
-                        chain_rows_warp(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
-                    } else {
-                        if (R <= 8) chain_rows_narrow<8>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
-                        else if (R <= 16) chain_rows_narrow<16>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
-                        else if (R <= 24) chain_rows_narrow<24>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
-                        else chain_rows_narrow<32>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, Ls + RR, &bar, phase, p.mode_flag);
-                    }
+                    chain_rows_warp(p.cpart, Pst, st, rows, R, nsuper, out, Ls, &bar, phase, p.mode_flag);
                     phase ^= 1u;
                     if (tr) trace_stamp(tr, 17, blockIdx.x == 0 && tid == 0);
                 }

@@ -1,0 +1,422 @@
+// flow_kernel.cuh -- K6 for R <= 32 as a dataflow kernel (k_flow): the persistent
+// factor-dependent chain of a stream window without grid barriers.
+#pragma once
+
+#include "chain_kernel.cuh"
+
+namespace rocpk {
+
+// ===========================================================================
+// k_flow.  Same work and arithmetic as k_chain<false>
+// (RocpStream::consume, rocp.cpp:144-160: per batch the temporal stage, then
+// modes 1..N-1, Gauss-Seidel), reorganised around one observation: a stage's
+// solve U(n) = solve_gram(Q(n), P(n)) recomputes EVERY row from P and Q
+// (rocp.cpp:110), and the next stage reads only the S sampled rows of it.  So a
+// stage publishes the explicit inverse G^-1 instead of waiting
+// for all of its rows:
+//   chunk blocks   (one 32-sample chunk of Z each) compute the sampled rows of
+//                  the factor the previous stage just solved themselves, one
+//                  length-R dot product per entry against its G^-1, and read
+//                  every older factor from memory; then the chunk's Gram partial
+//   Gram finisher  (last block) sums the chunk partials, Q += G, forms G^-1 and
+//                  the regularisation decision (the sweep, kernels.cuh
+//                  gram_solve_block), publishes G^-1 (two slots, by stage
+//                  parity) and bumps the finished-stage counter
+//   contraction    items of X_s Z as in k_chain; the last item of a 32-row tile
+//                  sums the tile's superchunk partials into P in place (or the
+//                  temporal right-hand sides into wtemp)
+//   materialisers  (the blocks without a chunk, at the start of the next stage)
+//                  write every row of the solved factor, off the critical path
+// Dependencies are counters (release: __threadfence + atomicAdd; acquire:
+// ld.acquire.gpu polls by one thread per block, then a block barrier), so the
+// critical path per stage is: previous G^-1 -> sampled rows -> Z chunk ->
+// chunk Gram -> combine -> sweep (G^-1) -> publish.  Reuse hazards are ordered
+// by the same chain: a stage's chunk blocks wait for the previous
+// stage's tile sums and the rows of the stage before it, which transitively
+// orders every buffer's next writer after its last reader.
+// Counters (p.fctr, zeroed per launch, cumulative over the launch's stages):
+//   [0] finished stages; [1 + st] tile sums of stage st; [1 + N + st] rows of
+//   stage st written; [1 + 2N + st * maxtiles + t] item arrivals of tile t.
+
+constexpr int kGinvSlot = 32 * 32;  // doubles per G^-1 slot (R <= 32)
+
+// MAXR = RP (R padded to a multiple of 8, <= 32): every loop over R is unrolled.
+template <int MAXR, bool kTrace>
+__global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ unsigned short pairs[32 * 33 / 2];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int s_last;
+    constexpr int RP = MAXR;
+    constexpr int kW = kChainThreads / 32;  // warps per block
+    constexpr int kSPW = kChunk / kW;       // chunk samples per warp
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
+    const int RR = R * R, npairs = R * (R + 1) / 2;
+    const int G = gridDim.x;
+    const int nch = (S + kChunk - 1) / kChunk;
+    const int NPp = (npairs + 1) & ~1;
+    const int cblocks = G - 1;  // block G - 1 is the Gram finisher
+    const bool is_fin = int(blockIdx.x) == G - 1;
+    const int nmat = cblocks - nch;  // materialisers [0, nmat); chunk ch on block cblocks - 1 - ch (host: nmat >= 8)
+    const int ch = is_fin ? nch : cblocks - 1 - int(blockIdx.x);
+    const bool chunk_block = ch >= 0 && ch < nch;
+    const bool lr = lane < R;
+    unsigned* fin_ctr = p.fctr;
+    unsigned* tsum_ctr = p.fctr + 1;
+    unsigned* rows_ctr = p.fctr + 1 + N;
+    unsigned* tile_ctr = p.fctr + 1 + 2 * N;
+    double* xs = sm + kSmXs;
+    double* zs = sm + kSmZs;
+    double* wsm = sm + kSmFact;  // per warp: the right-hand-side rows it turns into factor rows [8][4][32]
+    unsigned phase = 0;
+    if (tid == 0) {
+        int off = 0;
+        for (int j = 0; j < R; ++j)
+            for (int i = j; i < R; ++i) pairs[off++] = (unsigned short)((i << 8) | j);
+        mbar_init(&bar, 1);
+    }
+    __syncthreads();
+
+    auto rows_of = [&](int st) { return (st == 0) ? p.B : int(p.head[st - 1]); };
+    auto tiles_of = [&](int st) { return (rows_of(st) + kRowTile - 1) / kRowTile; };
+    auto wrows_of = [&](int st) -> double* { return (st == 0) ? p.wtemp : p.P[st - 1]; };
+    auto out_of = [&](int b, int st) -> double* {
+        return (st == 0) ? p.temporal + (p.t_len0 + int64_t(b) * p.B) * R : p.U[st - 1];
+    };
+    // mode of factor l in stage st's list ([u_new,] U(N-1), ..., U(1) without U(st); 0 = temporal)
+    auto mode_at = [&](int st, int l) -> int {
+        if (st == 0) return N - 1 - l;
+        if (l == 0) return 0;
+        int k = N - 1 - (l - 1);
+        if (k <= st) k -= 1;
+        return k;
+    };
+    auto wait_ge = [&](const unsigned* c, unsigned need) {
+        if (tid == 0) wait_gathered(c, need, 0u, 0u);
+    };
+    // column `lane` of the G^-1 of stage sp (symmetric: G^-1(k, lane) = slot[k R + lane])
+    auto load_gcol = [&](int sp, double* g) {
+        const double* slot = p.ginv + (sp & 1) * kGinvSlot;
+#pragma unroll
+        for (int k = 0; k < MAXR; ++k) g[k] = (lr && k < R) ? __ldcg(slot + k * R + lane) : 0.0;
+    };
+    // u_lane = fma chain over k of w_k G^-1(k, lane) (oracle solve_gram_m), w in shared memory
+    auto row_dot = [&](const double* w, const double* g) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXR; ++k) {  // branch-free (w has MAXR readable entries)
+            const double v = __fma_rn(w[k], g[k], acc);
+            acc = (k < R) ? v : acc;
+        }
+        return acc;
+    };
+
+    // idx of this warp's chunk samples (cc = warp + 8q), loaded a stage ahead
+    int32_t nidx[kSPW][kMaxOrder - 1];
+    auto load_idx = [&](int b, int st) {
+        if (b >= p.nb || !chunk_block) return;
+        const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
+#pragma unroll
+        for (int q = 0; q < kSPW; ++q) {
+            const int c = ch * kChunk + warp + kW * q;
+#pragma unroll
+            for (int l = 0; l < kMaxOrder - 1; ++l)
+                nidx[q][l] = (c < S && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
+        }
+    };
+    load_idx(0, 0);
+
+    // rows of the stage sp = (bp, stp) solved before, by this block's warps: warp-global index
+    // gw, rows gw, gw + nw_total, ...
+    auto materialise = [&](int bp, int stp, int gw, int nw_total) {
+        const int rows = rows_of(stp);
+        if (gw >= rows) return;
+        const double* W = wrows_of(stp);
+        double* out = out_of(bp, stp);
+        const int md = __ldcg(p.gmode + ((bp * N + stp) & 1));
+        double g[MAXR];
+        load_gcol(bp * N + stp, g);
+        double* wr = wsm + warp * 32;
+        for (int row = gw; row < rows; row += nw_total) {
+            const double w = lr ? __ldcg(W + int64_t(row) * R + lane) : 0.0;
+            __syncwarp();
+            wr[lane] = w;
+            __syncwarp();
+            const double u = row_dot(wr, g);
+            if (lr) out[int64_t(row) * R + lane] = md ? u : 0.0;
+        }
+    };
+
+    for (int b = 0; b < p.nb; ++b) {
+        double* u_new = p.temporal + (p.t_len0 + int64_t(b) * p.B) * R;
+        for (int st = 0; st < N; ++st) {
+            const int sg = b * N + st;
+            const int b1 = (st > 0) ? b : b - 1, st1 = (st > 0) ? st - 1 : N - 1;  // stage sg - 1
+            const int rows = rows_of(st);
+            const double* X = p.X_base + p.xoff[b * N + st];
+            double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * RP : p.gch + int64_t(st) * S * RP;
+            const int tiles = (rows + kRowTile - 1) / kRowTile;
+            const int n_contract = tiles * nsuper;
+            unsigned long long* tr = (kTrace && p.trace) ? p.trace + int64_t(sg) * kTraceSlots : nullptr;
+
+            if (!is_fin) {
+                const int first_item = int(blockIdx.x);
+                if (chunk_block) {
+                    // ------------- Z chunk (sampling.cpp:90-103), warp per sample, lane = r; the
+                    // sampled rows of the factor solved by stage sg - 1 (list position lod) are
+                    // formed here from its summed right-hand sides and G^-1
+                    const double* F[kMaxOrder - 1];
+                    int lod = -1;
+#pragma unroll
+                    for (int l = 0; l < kMaxOrder - 1; ++l) {
+                        F[l] = nullptr;
+                        if (l < n_other) {
+                            const int md = mode_at(st, l);
+                            F[l] = (md == 0) ? u_new : p.U[md - 1];
+                            if (sg >= 1 && md == st1) lod = l;
+                        }
+                    }
+                    if (sg >= 2) {  // rows of stage sg - 2 (factors read from memory)
+                        const int b2 = (st1 > 0) ? b1 : b1 - 1, st2 = (st1 > 0) ? st1 - 1 : N - 1;
+                        wait_ge(rows_ctr + st2, unsigned(b2 + 1) * unsigned(rows_of(st2)));
+                        __syncthreads();
+                    }
+                    const int c0 = ch * kChunk, cn = min(kChunk, S - c0);
+                    double f[kSPW][kMaxOrder - 1];
+#pragma unroll
+                    for (int q = 0; q < kSPW; ++q) {
+                        const bool live = warp + kW * q < cn && lr;
+#pragma unroll
+                        for (int l = 0; l < kMaxOrder - 1; ++l)
+                            f[q][l] = (live && l < n_other && l != lod) ? __ldcg(F[l] + int64_t(nidx[q][l]) * R + lane) : 1.0;
+                    }
+                    if (sg >= 1) {
+                        wait_ge(fin_ctr, unsigned(sg));
+                        wait_ge(tsum_ctr + st1, unsigned(b1 + 1) * unsigned(tiles_of(st1)));
+                        __syncthreads();
+                        if (tr) trace_stamp(tr, 0, ch == 0 && tid == 0);
+                        double g[MAXR];
+                        load_gcol(sg - 1, g);
+                        const double* W = wrows_of(st1);
+                        const int md = __ldcg(p.gmode + ((sg - 1) & 1));
+#pragma unroll
+                        for (int q = 0; q < kSPW; ++q) {
+                            int32_t iw = 0;
+#pragma unroll
+                            for (int l = 0; l < kMaxOrder - 1; ++l)
+                                if (l == lod) iw = nidx[q][l];
+                            const bool live = warp + kW * q < cn && lr;
+                            wsm[(warp * kSPW + q) * 32 + lane] = live ? __ldcg(W + int64_t(iw) * R + lane) : 0.0;
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int q = 0; q < kSPW; ++q) {
+                            const double u = row_dot(wsm + (warp * kSPW + q) * 32, g);
+#pragma unroll
+                            for (int l = 0; l < kMaxOrder - 1; ++l)
+                                if (l == lod) f[q][l] = md ? u : 0.0;
+                        }
+                        if (tr) trace_stamp(tr, 12, ch == 0 && tid == 0);
+                    }
+                    double* zc = zs;  // [32][RP]
+#pragma unroll
+                    for (int q = 0; q < kSPW; ++q) {
+                        const int cc = warp + kW * q;
+                        if (lane < RP) {
+                            double z = 0.0;
+                            if (cc < cn && lr) {
+                                z = 1.0;
+#pragma unroll
+                                for (int l = 0; l < kMaxOrder - 1; ++l)
+                                    if (l < n_other) z = z * f[q][l];
+                            }
+                            zc[cc * RP + lane] = z;
+                            if (cc < cn) Z[int64_t(c0 + cc) * RP + lane] = z;
+                        }
+                    }
+                    __syncthreads();
+                    if (tr) trace_stamp(tr, 14, ch == 0 && tid == 0);
+                    chain_chunk_gram_dmma(zc, RP, R, p.chpart + int64_t(ch) * NPp);
+                    __syncthreads();
+                    if (tid == 0) {
+                        __threadfence();
+                        atomicAdd(p.zctr + 1 + ch / kSuper, 1u);
+                        atomicAdd(p.zctr, 1u);
+                    }
+                    if (tr) trace_stamp(tr, 1, ch == 0 && tid == 0);
+                    const int nb2 = (st + 1 < N) ? b : b + 1, ns2 = (st + 1 < N) ? st + 1 : 0;
+                    load_idx(nb2, ns2);
+                } else if (sg >= 1) {
+                    // ------------- materialise every row of stage sg - 1 (off the critical path)
+                    wait_ge(fin_ctr, unsigned(sg));
+                    wait_ge(tsum_ctr + st1, unsigned(b1 + 1) * unsigned(tiles_of(st1)));
+                    __syncthreads();
+                    const int nwt = nmat * kW;
+                    const int gw = (nmat - 1 - int(blockIdx.x)) + warp * nmat;
+                    materialise(b1, st1, gw, nwt);
+                    __syncthreads();
+                    if (tid == 0) {
+                        const int rows1 = rows_of(st1);
+                        unsigned n = 0;
+                        for (int w = 0; w < kW; ++w) {
+                            const int g0 = (nmat - 1 - int(blockIdx.x)) + w * nmat;
+                            if (g0 < rows1) n += unsigned((rows1 - 1 - g0) / nwt + 1);
+                        }
+                        if (n) {
+                            __threadfence();
+                            atomicAdd(rows_ctr + st1, n);
+                        }
+                        if (tr && blockIdx.x == 0) tr[5] = gtimer();
+                    }
+                }
+
+                // ------------- contraction items (tile, superchunk), stride cblocks
+                int zm_cur = -1;
+                for (int item = first_item; item < n_contract; item += cblocks) {
+                    const int tile = item % tiles, m = item / tiles;
+                    const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                    const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
+                    if (tid == 0) {  // X_s tile (from the overlapped gather when it runs) and Z tile
+                        if (p.gdone) {
+                            wait_gathered(p.gdone + b * N + st, __ldg(p.gneed + b * N + st), 0u);
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                        }
+                        if (tr && blockIdx.x == 0 && item == first_item) tr[7] = gtimer();
+                        fence_proxy_async();
+                        tma_load_1d_once(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
+                        const bool zload = m != zm_cur;
+                        if (zload) {  // superchunk m's chunks of Z published
+                            const unsigned nck = unsigned(min(kSuper, nch - m * kSuper));
+                            wait_gathered(p.zctr + 1 + m, unsigned(sg + 1) * nck, 0u, 0u);
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                            tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
+                        }
+                        mbar_expect_tx(&bar, unsigned(cn * kRowTile * 8 + (zload ? cn * RP * 8 : 0)));
+                    }
+                    zm_cur = m;
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    if (tr) trace_stamp(tr, 8, blockIdx.x == 0 && tid == 0 && item == first_item);
+                    const int nk = (cn + kChunk - 1) / kChunk;
+                    const int cc0 = warp * kChunk;
+                    const int cn0 = max(min(kChunk, cn - cc0), 0);
+                    double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
+                    chain_contract_blocked<MAXR / 4>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                    // the tile's last item sums its superchunk partials (rocp.cpp:107: P += X_s Z)
+                    if (tid == 0) {
+                        __threadfence();
+                        const unsigned prev = atomicAdd(tile_ctr + st * p.maxtiles + tile, 1u);
+                        s_last = (prev + 1 == unsigned(b + 1) * unsigned(nsuper)) ? 1 : 0;
+                    }
+                    __syncthreads();
+                    if (s_last) {
+                        __threadfence();
+                        double* W = wrows_of(st);
+                        for (int e = tid; e < nrows * R; e += kChainThreads) {
+                            const int64_t o = int64_t(i0) * R + e;
+                            double tot = __ldcg(p.cpart + o);
+                            for (int mm = 1; mm < nsuper; ++mm) tot = tot + __ldcg(p.cpart + int64_t(mm) * rows * R + o);
+                            W[o] = (st > 0) ? __ldcg(W + o) + tot : tot;
+                        }
+                        __syncthreads();
+                        if (tid == 0) {
+                            __threadfence();
+                            atomicAdd(tsum_ctr + st, 1u);
+                            if (tr) tr[6] = gtimer();  // the last tile sum of the stage overwrites
+                        }
+                    }
+                    if (tr) trace_stamp(tr, 9, blockIdx.x == 0 && tid == 0 && item == first_item);
+                }
+            } else {
+                // ------------- the Gram finisher
+                double* D = sm + kSmFact;  // the sweep's pivots (64)
+                double* Gs = D + 64;       // R x R column-major
+                double* colb = Gs + 64 * 64;  // 128: the sweep's column buffers
+                double* gi = sm + 12288;   // G^-1 (row-major, symmetric)
+                double qa[kQPre], qb[kQPre];
+#pragma unroll
+                for (int u = 0; u < kQPre; ++u) {
+                    const int q = tid + u * kChainThreads;
+                    qa[u] = qb[u] = 0.0;
+                    if (st > 0 && q < npairs) {
+                        const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                        qa[u] = __ldcg(p.Q[st - 1] + i + j * R);
+                        qb[u] = __ldcg(p.Q[st - 1] + j + i * R);
+                    }
+                }
+                if (tid == 0) {  // every chunk partial of this stage published
+                    wait_gathered(p.zctr, unsigned(sg + 1) * unsigned(nch), 0u, 0u);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    const unsigned bytes = unsigned(nch * NPp * 8);
+                    fence_proxy_async();
+                    tma_load_1d(sm, p.chpart, bytes, &bar);
+                    mbar_expect_tx(&bar, bytes);
+                }
+                if (tr) trace_stamp(tr, 3, tid == 0);
+                mbar_wait(&bar, phase);
+                phase ^= 1u;
+#pragma unroll
+                for (int u = 0; u < kMaxPairsPerThread; ++u) {
+                    const int q = tid + u * kChainThreads;
+                    if (q >= npairs) break;
+                    double tot = 0.0;
+                    for (int m = 0; m < nsuper; ++m) {
+                        const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
+                        double v[kSuper];
+#pragma unroll
+                        for (int k = 0; k < kSuper; ++k) v[k] = (k0 + k < k1) ? sm[(k0 + k) * NPp + q] : 0.0;
+                        double sq = v[0];
+#pragma unroll
+                        for (int k = 1; k < kSuper; ++k)
+                            if (k0 + k < k1) sq = sq + v[k];
+                        tot = (m == 0) ? sq : tot + sq;
+                    }
+                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                    double ga = tot, gb = tot;
+                    if (st > 0) {  // Q + G entry by entry (rocp.cpp:108)
+                        const double qva = (u < kQPre) ? qa[u < kQPre ? u : 0] : __ldcg(p.Q[st - 1] + i + j * R);
+                        const double qvb = (u < kQPre) ? qb[u < kQPre ? u : 0] : __ldcg(p.Q[st - 1] + j + i * R);
+                        ga = qva + tot;
+                        gb = qvb + tot;
+                        p.Q[st - 1][i + j * R] = ga;
+                        p.Q[st - 1][j + i * R] = gb;
+                    }
+                    Gs[i + j * R] = ga;
+                    Gs[j + i * R] = gb;
+                }
+                __syncthreads();
+                if (tr) trace_stamp(tr, 10, tid == 0);
+                // solve_gram (solve.cpp:9-35) in canonical form (kernels.cuh gram_solve_block)
+                int2 mr;
+                if (npairs <= 256) mr = gram_solve_block<1>(Gs, R, gi, D, colb, sm, true);
+                else if (npairs <= 512) mr = gram_solve_block<2>(Gs, R, gi, D, colb, sm, true);
+                else mr = gram_solve_block<3>(Gs, R, gi, D, colb, sm, true);
+                if (tr) trace_stamp(tr, 11, tid == 0);
+                double* slot = p.ginv + (sg & 1) * kGinvSlot;
+                for (int t = tid; t < RR; t += kChainThreads) slot[t] = gi[t];
+                if (tid == 0) {
+                    p.gmode[sg & 1] = mr.x;
+                    if (mr.y) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    atomicAdd(fin_ctr, 1u);
+                }
+                if (tr) trace_stamp(tr, 4, tid == 0);
+            }
+        }
+    }
+    // the last stage's rows, by every block
+    {
+        const int sl = p.nb * N - 1;
+        const int bl = p.nb - 1, stl = N - 1;
+        wait_ge(fin_ctr, unsigned(sl + 1));
+        wait_ge(tsum_ctr + stl, unsigned(bl + 1) * unsigned(tiles_of(stl)));
+        __syncthreads();
+        materialise(bl, stl, int(blockIdx.x) + warp * G, G * kW);
+    }
+}
+
+}  // namespace rocpk

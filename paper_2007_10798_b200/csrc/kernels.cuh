@@ -601,12 +601,13 @@ __global__ void __launch_bounds__(256) k_probe_random_reads(const double* __rest
 // solve_gram's regularisation decision (solve.cpp:17-33), canonical form
 // (oracle certificate / jacobi_eigen / decide_gram).  The
 // reference decides from exact eigenvalues: zero solution if lambda_max <= 0,
-// regularise if lambda_min <= 0 or lambda_max / lambda_min > 1e12.  Rigorous
-// certificate first: dmax / dmin <= kappa (pivots of an SPD matrix lie in
-// [lambda_min, lambda_max]) and kappa <= |G|_inf R ymax^2 / dmin with
-// ymax >= |L^-1|_inf (cert_ymax_warp).  Certainly above 4e12 -> regularise;
-// certainly below 2.5e11 -> not; a non-positive max diagonal or pivot, or the
-// band in between -> exact eigenvalues by the deterministic cyclic Jacobi method.
+// regularise if lambda_min <= 0 or lambda_max / lambda_min > 1e12.  Certificate
+// first: dmax / dmin <= kappa (pivots of an SPD matrix lie in [lambda_min,
+// lambda_max]) and maxdiag tau / R <= kappa <= |G|_inf tau with tau = tr(G^-1)
+// from the explicit inverse the row solves use anyway.  Certainly above 4e12 ->
+// regularise; certainly below 2.5e11 -> not; a non-positive max diagonal or
+// pivot, or the band in between -> exact eigenvalues by the deterministic
+// cyclic Jacobi method.
 constexpr double kCertRegAbove = 4e12;
 constexpr double kCertNoRegBelow = 2.5e11;
 constexpr int kDecNoReg = 0, kDecReg = 1, kDecExact = 2;
@@ -625,22 +626,6 @@ __device__ __forceinline__ double butterfly_max32(double v) {
     return v;
 }
 
-// max_i y_i, y = (I - |N|)^-1 1 for L = I - N: lane i owns rows i and i + 32,
-// y_i = fma(|l_ik|, y_k, y_i) in k order from 1.0 (oracle cert_ymax).  One warp.
-// L(i,k) at L[k*ld + i] (i > k).
-__device__ __noinline__ double cert_ymax_warp(const double* L, int ld, int R) {
-    const int lane = threadIdx.x & 31;
-    double y0 = 1.0, y1 = 1.0;
-    for (int k = 0; k + 1 < R; ++k) {
-        const double yk = __shfl_sync(0xffffffffu, (k < 32) ? y0 : y1, k & 31);
-        if (lane > k && lane < R) y0 = __fma_rn(fabs(L[k * ld + lane]), yk, y0);
-        if (lane + 32 > k && lane + 32 < R) y1 = __fma_rn(fabs(L[k * ld + lane + 32]), yk, y1);
-    }
-    double v = (lane < R) ? y0 : 0.0;
-    if (lane + 32 < R) v = max_of(v, y1);
-    return butterfly_max32(v);
-}
-
 // |G|_inf (max absolute row sum; row sums in column order), one warp; a(i,j) at G[i + j*ldg].
 __device__ __noinline__ double gram_inf_norm_warp(const double* G, int ldg, int R) {
     const int lane = threadIdx.x & 31;
@@ -654,30 +639,24 @@ __device__ __noinline__ double gram_inf_norm_warp(const double* G, int ldg, int 
     return butterfly_max32(v);
 }
 
-constexpr int kDecTier2 = 3;  // tier 1 left the band: form tau = tr(G^-1)
-
 // Device-wide decision statistics (rocp_decision_stats): [0] no-reg, [1] reg, [2] exact
-// eigenvalues, [3] decisions that needed tier 2.  One atomic per solve, off the chain's
-// critical path (issued by the thread that publishes the decision).
+// eigenvalues, [3] decisions that reached the tau bounds (the pivot ratio did not settle
+// them).  One atomic per solve, off the chain's critical path.
 __device__ unsigned long long g_dec_paths[4];
-__device__ __forceinline__ void count_decision(int final_path, bool used_tier2) {
+__device__ __forceinline__ void count_decision(int final_path, bool used_tau) {
     atomicAdd(&g_dec_paths[final_path], 1ull);
-    if (used_tier2) atomicAdd(&g_dec_paths[3], 1ull);
+    if (used_tau) atomicAdd(&g_dec_paths[3], 1ull);
 }
 
-// Tier 1 (every Gram; ymax folded into the factorization).
-__device__ __forceinline__ int gram_certificate(double maxdiag, double gnorm, double dmin, double dmax, double ymax,
-                                                int R) {
+// The certificate (oracle certificate): pivot ratio, then the tau bounds.  *used_tau:
+// whether the tau bounds were reached.
+__device__ __forceinline__ int gram_certificate(double maxdiag, double gnorm, double dmin, double dmax, double tau,
+                                                int R, bool* used_tau) {
+    *used_tau = false;
     if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
     const double ratio = dmax / dmin;
     if (ratio > kCertRegAbove) return kDecReg;
-    const double khi = ((gnorm / dmin) * double(R)) * (ymax * ymax);
-    if (khi <= kCertNoRegBelow) return kDecNoReg;
-    return kDecTier2;
-}
-
-// Tier 2: maxdiag tau / R <= kappa <= |G|_inf tau (tau = tr(G^-1) >= 1 / lambda_min).
-__device__ __forceinline__ int gram_certificate2(double maxdiag, double gnorm, double tau, int R) {
+    *used_tau = true;
     const double klo = (maxdiag * tau) / double(R);
     const double khi = gnorm * tau;
     if (klo > kCertRegAbove) return kDecReg;
@@ -685,143 +664,90 @@ __device__ __forceinline__ int gram_certificate2(double maxdiag, double gnorm, d
     return kDecExact;
 }
 
-// tau = tr(G^-1) = sum_i (sum_j M_ij^2) / d_i, M = L^-1 (oracle cert_tau), tier 2 only.
-// cert_group_warp: one warp forms the columns 8g..8g+7 of M by forward substitution,
-// lane i owning rows i and i + 32 (NRB row blocks), M(k, .) of step k broadcast by
-// shuffle from its owner; a rolled k loop (small code).  Writes the group's row
-// partials p_gi = fma chain over its columns to part[g * 64 + i].  L(i,k) at
-// L[k*ld + i] (i > k).
-template <int NRB>
-__device__ __noinline__ void cert_group_warp(const double* L, int ld, int R, int g, double* part) {
-    const int lane = threadIdx.x & 31;
-    const int c0 = 8 * g;
-    double m[NRB][8];
+// tau = G^-1(0,0) + G^-1(1,1) + ... in k order (oracle certificate); Gi R x R.
+__device__ __forceinline__ double ginv_trace(const double* Gi, int R) {
+    double t = Gi[0];
+    for (int k = 1; k < R; ++k) t = t + Gi[k + k * R];
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// G^-1 by the symmetric sweep (Gauss-Jordan without pivoting, oracle
+// gram_sweep).  For k = 0..R-1, with c = column k of the working matrix A (A = G +
+// lambda I at the start) and r = 1 / c_k (0 when |c_k| <= DBL_MIN):
+//   A(i, k) = c_i r (i != k),  A(k, k) = -r,
+//   A(k, j) = fma(c_j, r, +0) (j != k),
+//   A(i, j) = fma(-(c_i r), c_j, A(i, j)) (i, j != k);
+// then G^-1 = -A.  The pivots d_k = c_k are the LDL^T pivots of G (Schur complements)
+// and feed the regularisation certificate.  One elimination, no separate triangular
+// inverse: the critical path per step is one reciprocal, one multiply and one fma.
+
+// The sweep by a whole block on the LOWER triangle (the canonical form, oracle gram_sweep:
+// entries (i, j), i >= j, each step reading column k through symmetry, c_x = A(x, k) for
+// x >= k and A(k, x) for x < k; G^-1 symmetric by construction).  R <= 64 with
+// R (R + 1) / 2 <= EPT * blockDim: thread t owns the lower entries t, t + blockDim, ...
+// (column by column) in registers, indices formed once.  Column k + 1 is published in cbuf
+// (2 x 64, by step parity) by the owners of its entries as they update them, so a step is
+// one block barrier, one reciprocal (formed redundantly by every thread) and one fma per
+// entry.  Writes G^-1 to gi (both triangles; gi[i * R + j] = G^-1(i, j)); piv (if set)
+// gets d_k at [k].  Block-uniform call.
+template <int EPT>
+__device__ __noinline__ void sweep_block(const double* G, double lambda, int R, double* cbuf, double* gi,
+                                         double* piv) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int np = R * (R + 1) / 2;
+    double a[EPT];
+    int ii[EPT], jj[EPT];
 #pragma unroll
-    for (int rb = 0; rb < NRB; ++rb)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) m[rb][c] = (lane + 32 * rb == c0 + c) ? 1.0 : 0.0;
-    for (int k = c0; k + 1 < R; ++k) {
-        const int src = k & 31;
-        double mk[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            double own = m[0][c];
-            if (NRB > 1 && k >= 32) own = m[NRB - 1][c];
-            mk[c] = __shfl_sync(0xffffffffu, own, src);
-        }
-#pragma unroll
-        for (int rb = 0; rb < NRB; ++rb) {
-            const int i = lane + 32 * rb;
-            if (i > k && i < R) {
-                const double l = L[k * ld + i];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) m[rb][c] = __fma_rn(-l, mk[c], m[rb][c]);
+    for (int q = 0; q < EPT; ++q) {
+        const int e = tid + q * nt;
+        int i = 0, j = -1;  // j = -1: no entry
+        if (e < np) {       // lower entry e, column by column: column j holds R - j entries
+            int rem = e;
+            j = 0;
+            while (rem >= R - j) {
+                rem -= R - j;
+                ++j;
             }
+            i = j + rem;
         }
+        ii[q] = i;
+        jj[q] = j;
+        const double g = (j >= 0) ? G[i + j * R] : 0.0;
+        a[q] = (i == j) ? g + lambda : g;
+        if (j == 0) cbuf[i] = a[q];
     }
+    __syncthreads();
+    for (int k = 0; k < R; ++k) {
+        const double* c = cbuf + (k & 1) * 64;
+        double* cn = cbuf + ((k + 1) & 1) * 64;
+        const double d = c[k];
+        if (piv && tid == 0) piv[k] = d;
+        const double r = (fabs(d) > 2.2250738585072014e-308) ? 1.0 / d : 0.0;
 #pragma unroll
-    for (int rb = 0; rb < NRB; ++rb) {
-        double pp = 0.0;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            if (c0 + c < R) pp = __fma_rn(m[rb][c], m[rb][c], pp);
-        part[g * 64 + lane + 32 * rb] = pp;
-    }
-}
-
-// Rows of solve_gram for R > 32 (oracle gram_inverse): the explicit
-// inverse, formed once per solve by one block.  inv_unit_lower_warp: columns 8g..8g+7
-// of M = L^-1 (cert_group_warp's substitution) to M(i, j) at M[i + j*R].
-__device__ __noinline__ void inv_unit_lower_warp(const double* L, int ld, int R, int g, double* M) {
-    const int lane = threadIdx.x & 31;
-    const int c0 = 8 * g;
-    double m[2][8];
-#pragma unroll
-    for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) m[rb][c] = (lane + 32 * rb == c0 + c) ? 1.0 : 0.0;
-    for (int k = c0; k + 1 < R; ++k) {
-        const int src = k & 31;
-        double mk[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) mk[c] = __shfl_sync(0xffffffffu, (k >= 32) ? m[1][c] : m[0][c], src);
-#pragma unroll
-        for (int rb = 0; rb < 2; ++rb) {
-            const int i = lane + 32 * rb;
-            if (i > k && i < R) {
-                const double l = L[k * ld + i];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) m[rb][c] = __fma_rn(-l, mk[c], m[rb][c]);
-            }
+        for (int q = 0; q < EPT; ++q) {
+            const int i = ii[q], j = jj[q];
+            const double ci = c[i], cj = c[j < 0 ? 0 : j];
+            const double l = ci * r;
+            const double ov = __fma_rn(-l, cj, a[q]);
+            const double pv = __fma_rn(cj, r, 0.0);
+            const bool jk = j == k, ik = i == k;
+            const double v = jk ? (ik ? -r : l) : (ik ? pv : ov);
+            a[q] = v;
+            // column k + 1: below the diagonal (and the diagonal) from column k + 1, above it
+            // through row k + 1 (one predicated store)
+            const int tgt = (j == k + 1) ? i : ((i == k + 1 && j >= 0) ? j : -1);
+            if (tgt >= 0) cn[tgt] = v;
         }
+        __syncthreads();
     }
 #pragma unroll
-    for (int rb = 0; rb < 2; ++rb) {
-        const int i = lane + 32 * rb;
-        if (i < R)
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (c0 + c < R) M[i + (c0 + c) * R] = m[rb][c];
-    }
-}
-
-// G^-1 (i, j) = G^-1 (j, i) = fma chain over k = j..R-1 of M(k, i) (M(k, j) dinv_k), i <= j,
-// by a whole block into Gi (R x R, either layout: symmetric).  M: R x R shared scratch.
-// Block-uniform call.
-__device__ __noinline__ void form_ginv_block(const double* L, int ld, const double* D, int R, double* M,
-                                             double* dinv, double* Gi) {
-    const int tid = threadIdx.x, warp = tid >> 5;
-    if (warp < (R + 7) / 8) inv_unit_lower_warp(L, ld, R, warp, M);
-    for (int k = tid; k < R; k += blockDim.x) dinv[k] = (fabs(D[k]) > 2.2250738585072014e-308) ? 1.0 / D[k] : 0.0;
-    __syncthreads();
-    const int npair = R * (R + 1) / 2;
-    for (int t = tid; t < npair; t += blockDim.x) {
-        // t -> (i, j), i <= j, column by column
-        int j = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-        while (j * (j + 1) / 2 > t) --j;
-        while ((j + 1) * (j + 2) / 2 <= t) ++j;
-        const int i = t - j * (j + 1) / 2;
-        double acc = 0.0;
-        for (int k = j; k < R; ++k) acc = __fma_rn(M[k + i * R], M[k + j * R] * dinv[k], acc);
-        Gi[i + j * R] = acc;
-        Gi[j + i * R] = acc;
-    }
-    __syncthreads();
-}
-
-// One warp: s_i = p_0i + p_1i + ..., t_i = s_i / d_i, v = t_lane + t_{lane+32}, butterfly sum.
-__device__ __noinline__ double cert_combine_warp(const double* part, const double* D, int R) {
-    const int lane = threadIdx.x & 31;
-    const int ng = (R + 7) / 8;
-    double t[2];
-#pragma unroll
-    for (int rb = 0; rb < 2; ++rb) {
-        const int i = lane + 32 * rb;
-        if (i < R) {
-            double sacc = part[i];
-            for (int gg = 1; gg < ng; ++gg) sacc = sacc + part[gg * 64 + i];
-            t[rb] = sacc / D[i];
-        } else {
-            t[rb] = 0.0;
+    for (int q = 0; q < EPT; ++q)
+        if (jj[q] >= 0) {
+            gi[ii[q] * R + jj[q]] = -a[q];
+            gi[jj[q] * R + ii[q]] = -a[q];
         }
-    }
-    return butterfly32(t[0] + t[1]);
-}
-
-// Tier 2 by a whole block (every warp < ceil(R/8) forms one column group; part: 8 x 64
-// doubles of shared scratch); returns the tier-2 path on every thread.  Block-uniform call.
-template <int NRB>
-__device__ __noinline__ int gram_tier2_block(const double* L, int ld, const double* D, int R, double maxdiag,
-                                             double gnorm, double* part, double* s_tau) {
-    const int warp = threadIdx.x >> 5;
-    if (warp < (R + 7) / 8) cert_group_warp<NRB>(L, ld, R, warp, part);
     __syncthreads();
-    if (warp == 0) {
-        const double t = cert_combine_warp(part, D, R);
-        if ((threadIdx.x & 31) == 0) *s_tau = t;
-    }
-    __syncthreads();
-    return gram_certificate2(maxdiag, gnorm, *s_tau, R);
 }
 
 // Deterministic parallel (round-robin) Jacobi eigenvalue extremes of a symmetric
@@ -957,166 +883,111 @@ __device__ __forceinline__ void exact_decision(double lo, double hi, int* mode, 
     }
 }
 
+// solve_gram (solve.cpp:9-35) for a block in canonical form: the sweep of G
+// (sweep_block), the regularisation decision (pivot ratio and tau bounds; exact Jacobi
+// eigenvalues in the band), the sweep of G + 1e-12 tr(G) I when it regularises.  G: R x R
+// (column-major, symmetric; not modified), gi: G^-1 (row-major, symmetric) when the mode
+// is 1, piv: R pivots, cbuf: 128 doubles, jscr: R * R + 128 doubles (exact path).  Returns
+// (mode, reg), mode 0 = zero solution.  count: add the path to the decision statistics.
+// Block-uniform call.
+template <int EPT>
+__device__ __noinline__ int2 gram_solve_block(const double* G, int R, double* gi, double* piv, double* cbuf,
+                                              double* jscr, bool count) {
+    __shared__ double s_tr, s_maxdiag, s_gnorm;
+    __shared__ int s_path, s_mode, s_reg, s_jflag;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) {
+        if (lane == 0) {  // solve.cpp:9-16 prologue: max diagonal, trace (k order)
+            double maxdiag = G[0], trc = G[0];
+            for (int k = 1; k < R; ++k) {
+                const double dg = G[k * R + k];
+                if (dg > maxdiag) maxdiag = dg;
+                trc = trc + dg;
+            }
+            s_tr = trc;
+            s_maxdiag = maxdiag;
+        }
+    } else if (warp == 1) {
+        const double gn = gram_inf_norm_warp(G, R, R);
+        if (lane == 0) s_gnorm = gn;
+    }
+    sweep_block<EPT>(G, 0.0, R, cbuf, gi, piv);
+    if (tid == 0) {
+        double dmin = piv[0], dmax = piv[0], tau = gi[0];
+        for (int k = 0; k < R; ++k) {
+            const double dk = piv[k];
+            if (dk < dmin) dmin = dk;
+            if (dk > dmax) dmax = dk;
+            if (k > 0) tau = tau + gi[k * R + k];
+        }
+        bool ut;
+        const int path = gram_certificate(s_maxdiag, s_gnorm, dmin, dmax, tau, R, &ut);
+        if (count) count_decision(path, ut);
+        s_path = path;
+        s_mode = 1;
+        s_reg = (path == kDecReg) ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_path == kDecExact) {  // rare: Jacobi eigenvalues of a copy of G
+        for (int t = tid; t < R * R; t += blockDim.x) jscr[t] = G[t];
+        __syncthreads();
+        double lo, hi;
+        jacobi_eigen_block(jscr, R, R, jscr + R * R, &s_jflag, &lo, &hi);
+        if (tid == 0) {
+            int md, rg;
+            exact_decision(lo, hi, &md, &rg);
+            s_mode = md;
+            s_reg = rg;
+        }
+        __syncthreads();
+    }
+    if (s_mode == 1 && s_reg) sweep_block<EPT>(G, 1e-12 * s_tr, R, cbuf, gi, piv);
+    const int2 res = make_int2(s_mode, s_reg);
+    __syncthreads();  // the shared scalars are reused by the next call
+    return res;
+}
+
 // ---------------------------------------------------------------------------
-// K5: solve_gram (solve.cpp:9-35), canonical form:
-// zero solution if max diag <= 0; unpivoted LDL^T; regularize with
-// 1e-12 tr(G) when a pivot is <= 0 or max/min pivot > 1e12; then per row
-// forward (increasing k), diagonal, backward (decreasing k) substitution.
-// Every block factors G redundantly in shared memory; each warp then solves one row.
-// flags[0] |= 1 if regularized; flags[1] = nonfinite_code if any output is
-// not finite (cprand's NumericalError check, cprand.cpp:42-43).
+// K5: solve_gram (solve.cpp:9-35), canonical form: gram_solve_block (sweep,
+// decision, regularised sweep), then rows u_j = fma chain over k of b_k G^-1(k, j).  Every
+// block solves G redundantly in shared memory; each warp then solves one row.
+// flags[0] |= 1 if regularized; flags[1] = nonfinite_code if any output is not finite
+// (cprand's NumericalError check, cprand.cpp:42-43).
+// Dynamic shared memory: ksolve_smem_bytes(MAXR).
+__host__ __device__ constexpr int ksolve_smem_bytes(int maxr) { return (2 * maxr * maxr + maxr + 2 * 128) * 8; }
+
 template <int MAXR>
 __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int R,
                                                const double* __restrict__ RHS, int32_t rows,
                                                double* __restrict__ OUT, int* flags,
                                                int nonfinite_code) {
-    // A holds the working lower triangle (A[i][j], i >= j); the strict upper
-    // triangle stores the multipliers, L(i, k) at A[k][i] (never touched by
-    // the trailing updates, which only write i >= j > k).
-    __shared__ double A[MAXR][MAXR + 1];
-    __shared__ double D[MAXR];
-    __shared__ int s_mode;  // 0 = zero solution, 1 = solve
-    __shared__ int s_reg;
-    __shared__ double s_tr;
-    const int tid = threadIdx.x;
-
-    auto load = [&](double lambda) {
-        for (int t = tid; t < R * R; t += blockDim.x) {
-            const int i = t % R, j = t / R;
-            if (i >= j) A[i][j] = (i == j) ? G[t] + lambda : G[t];
-        }
-    };
-    auto factor = [&]() {
-        for (int k = 0; k < R; ++k) {
-            __syncthreads();
-            const double dk = A[k][k];
-            for (int i = k + 1 + tid; i < R; i += blockDim.x)
-                A[k][i] = (dk != 0.0) ? A[i][k] / dk : 0.0;
-            if (tid == 0) D[k] = dk;
-            __syncthreads();
-            const int m = R - k - 1;  // trailing size
-            for (int t = tid; t < m * m; t += blockDim.x) {
-                const int i = k + 1 + t % m, j = k + 1 + t / m;
-                if (j <= i) A[i][j] = __fma_rn(-A[k][i], A[j][k], A[i][j]);
-            }
-        }
-        __syncthreads();
-    };
-
-    __shared__ double s_ymax, s_gnorm, s_tau;
-    __shared__ int s_path;
-    __shared__ double s_t2[8 * 64];  // tier-2 certificate row partials
-    __shared__ double s_maxdiag;
-    for (int k = tid; k < R; k += blockDim.x) D[k] = G[k * R + k];  // diagonal, staged
-    __syncthreads();
-    if (tid == 0) {
-        double maxdiag = D[0];
-        for (int k = 1; k < R; ++k)
-            if (D[k] > maxdiag) maxdiag = D[k];
-        double tr = D[0];
-        for (int k = 1; k < R; ++k) tr = tr + D[k];
-        s_tr = tr;
-        s_maxdiag = maxdiag;
-    }
-    load(0.0);
-    factor();
-    {
-        const int warp = tid >> 5;
-        if (warp == 0) {
-            const double y = cert_ymax_warp(&A[0][0], MAXR + 1, R);
-            if (tid == 0) s_ymax = y;
-        } else if (warp == 1) {
-            const double gn = gram_inf_norm_warp(G, R, R);
-            if ((tid & 31) == 0) s_gnorm = gn;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double dmin = D[0], dmax = D[0];
-        for (int k = 0; k < R; ++k) {
-            if (D[k] < dmin) dmin = D[k];
-            if (D[k] > dmax) dmax = D[k];
-        }
-        s_path = gram_certificate(s_maxdiag, s_gnorm, dmin, dmax, s_ymax, R);
-    }
-    __syncthreads();
-    {
-        int path = s_path;
-        if (path == kDecTier2)  // rare: tier 2 in the scratch of the (finished) staging
-            path = gram_tier2_block<(MAXR > 32) ? 2 : 1>(&A[0][0], MAXR + 1, D, R, s_maxdiag, s_gnorm, s_t2, &s_tau);
-        if (tid == 0 && blockIdx.x == 0) count_decision(path, s_path == kDecTier2);
-        if (tid == 0) {
-            s_mode = (path == kDecExact) ? -1 : 1;
-            s_reg = (path == kDecReg) ? 1 : 0;
-        }
-    }
-    __syncthreads();
-    if (s_mode < 0) {  // exact eigenvalues: G in A as a full symmetric matrix (lda MAXR + 1)
-        double* a = &A[0][0];
-        for (int t = tid; t < R * R; t += blockDim.x) a[(t % R) + (t / R) * (MAXR + 1)] = G[t];
-        __syncthreads();
-        {
-            double lo, hi;
-            jacobi_eigen_block(a, MAXR + 1, R, s_t2, &s_path, &lo, &hi);
-            if (tid == 0) {
-                int mode, reg;
-                exact_decision(lo, hi, &mode, &reg);
-                s_mode = mode;
-                s_reg = reg;
-            }
-        }
-        __syncthreads();
-        if (s_mode == 1) {  // A was overwritten: the factorization of G or G + lambda I again
-            load(s_reg ? 1e-12 * s_tr : 0.0);
-            factor();
-        }
-    } else if (s_reg) {
-        load(1e-12 * s_tr);
-        factor();
-    }
-    if (blockIdx.x == 0 && tid == 0 && s_reg && flags) atomicOr(flags, 1);
-
-    // R > 32: the explicit inverse (form_ginv_block) in dynamic shared memory
-    extern __shared__ double ks_dyn[];  // MAXR > 32 only: M (R x R), G^-1 (R x R), 1 / d
-    if constexpr (MAXR > 32) {
-        if (s_mode == 1) form_ginv_block(&A[0][0], MAXR + 1, D, R, ks_dyn, ks_dyn + 2 * R * R, ks_dyn + R * R);
-    }
-    // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64).  R <= 32: per element
-    // the row-wise substitution -- forward w_j -= L(j,k) w_k (k increasing), the diagonal,
-    // backward w_j -= L(k,j) w_k (k decreasing), as the narrow chain's row solves; R > 32:
-    // u_j = fma chain over k of b_k G^-1(k, j), as the wide chain's.
-    const int lane = tid & 31;
+    extern __shared__ double ks_dyn[];  // G^-1 (R x R), jscr (R x R + 128), pivots (R), cbuf (128)
+    double* gi = ks_dyn;
+    double* jscr = gi + R * R;
+    double* piv = jscr + R * R + 128;
+    double* cbuf = piv + R;
+    constexpr int kEpt = (MAXR * (MAXR + 1) / 2 + 255) / 256;  // lower entries per thread (256 threads)
+    const int2 mr = gram_solve_block<kEpt>(G, R, gi, piv, cbuf, jscr, blockIdx.x == 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && mr.y && flags) atomicOr(flags, 1);
+    // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64)
+    const int tid = threadIdx.x, lane = tid & 31;
     const int32_t row = int32_t(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
     if (row >= rows) return;
     const int j0 = lane, j1 = lane + 32;
     const bool v0 = j0 < R, v1 = MAXR > 32 && j1 < R;
     double w0 = v0 ? RHS[int64_t(row) * R + j0] : 0.0;
     double w1 = v1 ? RHS[int64_t(row) * R + j1] : 0.0;
-    if (s_mode == 0) {
+    if (mr.x == 0) {
         w0 = w1 = 0.0;
-    } else if (MAXR > 32) {
-        const double* Gi = ks_dyn + R * R;
+    } else {
         double a0 = 0.0, a1 = 0.0;
         for (int k = 0; k < R; ++k) {
             const double bk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
-            if (v0) a0 = __fma_rn(bk, Gi[k + j0 * R], a0);
-            if (v1) a1 = __fma_rn(bk, Gi[k + j1 * R], a1);
+            if (v0) a0 = __fma_rn(bk, gi[k * R + j0], a0);
+            if (v1) a1 = __fma_rn(bk, gi[k * R + j1], a1);
         }
         w0 = a0;
         w1 = a1;
-    } else {
-        for (int k = 0; k < R; ++k) {
-            const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
-            if (v0 && j0 > k) w0 = __fma_rn(-A[k][j0], wk, w0);
-            if (v1 && j1 > k) w1 = __fma_rn(-A[k][j1], wk, w1);
-        }
-        if (v0) w0 = (fabs(D[j0]) > 2.2250738585072014e-308) ? w0 / D[j0] : 0.0;
-        if (v1) w1 = (fabs(D[j1]) > 2.2250738585072014e-308) ? w1 / D[j1] : 0.0;
-        for (int k = R - 1; k >= 0; --k) {
-            const double wk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
-            if (v0 && j0 < k) w0 = __fma_rn(-A[j0][k], wk, w0);
-            if (v1 && j1 < k) w1 = __fma_rn(-A[j1][k], wk, w1);
-        }
     }
     if (v0) OUT[int64_t(row) * R + j0] = w0;
     if (v1) OUT[int64_t(row) * R + j1] = w1;

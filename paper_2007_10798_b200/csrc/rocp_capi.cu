@@ -13,6 +13,7 @@
 #include "../../include/rocp_b200.h"
 #include "kernels.cuh"
 #include "chain_kernel.cuh"
+#include "flow_kernel.cuh"
 #include "shard_kernels.cuh"
 #include "gather_kernel.cuh"
 
@@ -458,11 +459,9 @@ void launch_contract(rocp_dev* dev, const double* X, int64_t I, int64_t s, const
     }
 }
 
-constexpr int kSolveWideSmem = (3 * 64 * 64) * int(sizeof(double));  // k_solve<64>: M, 1/d, G^-1
-
 void set_contract_smem_attrs() {
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_solve<64>), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kSolveWideSmem));
+                            ksolve_smem_bytes(64)));
     {
         auto attr = [](const void* f, int rpad) {
             const int b = int((size_t(kSuperSamples) * kRowTile + size_t(kSuperSamples) * rpad + size_t(8) * rpad * kRowTile) *
@@ -491,9 +490,9 @@ void set_contract_smem_attrs() {
 void launch_solve(rocp_dev* dev, const double* G, int R, const double* RHS, int64_t rows, double* OUT,
                   int* flags, int nonfinite_code) {
     const int grid = int(std::max<int64_t>(1, (rows + 7) / 8));  // a warp per row
-    if (R <= 16) k_solve<16><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
-    else if (R <= 32) k_solve<32><<<grid, 256, 0, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
-    else k_solve<64><<<grid, 256, kSolveWideSmem, dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    if (R <= 16) k_solve<16><<<grid, 256, ksolve_smem_bytes(16), dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    else if (R <= 32) k_solve<32><<<grid, 256, ksolve_smem_bytes(32), dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
+    else k_solve<64><<<grid, 256, ksolve_smem_bytes(64), dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     after_launch(dev, "k_solve");
 }
 
@@ -783,6 +782,9 @@ struct rocp_stream {
     DBuf<double> gpart, chpart, LD, rpart, zmodes;  // persistent-chain scratch
     DBuf<int> mode_flag;
     DBuf<unsigned> zctr;               // persistent chain: phase-0 chunk arrival counters
+    DBuf<double> ginv, wtemp;          // k_flow: G^-1 slots, temporal right-hand sides
+    DBuf<int> gmode;                   // k_flow: mode flags of the G^-1 slots
+    DBuf<unsigned> fctr;               // k_flow: dependency counters
     bool trace_on = false;             // chain phase timestamps (profiling aid)
     DBuf<unsigned long long> trace;
     int64_t trace_n = 0;
@@ -1058,6 +1060,14 @@ int gather_sms(rocp_stream* st, int64_t B) {
         CK(cudaFuncGetAttributes(&fa, k_chain<true, false>));
         CK(cudaFuncGetAttributes(&fa, k_chain<false, true>));
         CK(cudaFuncGetAttributes(&fa, k_chain<true, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<8, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<16, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<24, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<32, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<8, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<16, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<24, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<32, true>));
         CK(cudaFuncGetAttributes(&fa, k_gather_warps));
         CK(cudaStreamCreateWithFlags(&dev->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&dev->ev_gready, cudaEventDisableTiming));
@@ -1227,39 +1237,67 @@ size_t chain_smem(int R, int B) {
     return size_t(kSmTotal) * sizeof(double);  // fixed map (kernels.cuh, k_chain)
 }
 
-template <bool kWide, bool kTrace>
-void launch_chain_inst(rocp_stream* st, const ChainParams& p, int grid) {
+// One cooperative persistent launch of a chain kernel (k_chain<., .> or k_flow<.>):
+// grid = one block per SM, less the SMs of an overlapped gather.
+void launch_coop(rocp_stream* st, const void* fn, const char* name, const ChainParams& p, int grid) {
     rocp_dev* dev = st->dev;
     const size_t smem = chain_smem(st->R, p.B);
     // the dynamic shared memory opt-in is a per-device function attribute
     constexpr int kMaxDevices = 64;
-    static int max_dyn[kMaxDevices] = {};
+    static std::map<std::pair<const void*, int>, int> max_dyn;
+    static std::mutex max_dyn_mu;
     if (dev->device < 0 || dev->device >= kMaxDevices) throw RocpError{ROCP_E_CUDA, "device ordinal out of range"};
-    int& md = max_dyn[dev->device];
+    std::lock_guard<std::mutex> lk(max_dyn_mu);
+    int& md = max_dyn[std::make_pair(fn, dev->device)];
     if (md == 0) {
         int optin = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device));
         cudaFuncAttributes fa{};
-        CK(cudaFuncGetAttributes(&fa, k_chain<kWide, kTrace>));
-        CK(cudaFuncSetAttribute(k_chain<kWide, kTrace>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                optin - int(fa.sharedSizeBytes)));
+        CK(cudaFuncGetAttributes(&fa, fn));
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(fa.sharedSizeBytes)));
         md = optin - int(fa.sharedSizeBytes);
     }
     if (smem > size_t(md)) throw_domain("batch too large for the persistent chain kernel's shared memory");
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<kWide, kTrace>, kChainThreads, smem));
-    if (per_sm < 1) throw RocpError{ROCP_E_CUDA, "k_chain does not fit on an SM"};
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kChainThreads, smem));
+    if (per_sm < 1) throw RocpError{ROCP_E_CUDA, "chain kernel does not fit on an SM"};
     void* args[] = {const_cast<ChainParams*>(&p)};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_chain<kWide, kTrace>), dim3(grid),
-                                   dim3(kChainThreads), args, smem, dev->stream));
-    after_launch(dev, "k_chain");
+    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kChainThreads), args, smem, dev->stream));
+    after_launch(dev, name);
+}
+
+// k_flow (flow_kernel.cuh) serves R <= 32 when one finisher block holds every chunk
+// Gram partial and at least 8 blocks are left to write rows; k_chain otherwise (and
+// when ROCP_CHAIN=barrier asks for the grid-barrier kernel).
+bool use_flow(const rocp_stream* st, int grid) {
+    static const bool barrier_env = [] {
+        const char* e = std::getenv("ROCP_CHAIN");
+        return e && std::string(e) == "barrier";
+    }();
+    if (barrier_env || st->R > 32) return false;
+    const int64_t nch = (st->s + kChunk - 1) / kChunk;
+    const int64_t NPp = ((int64_t(st->R) * (st->R + 1) / 2) + 1) & ~int64_t(1);
+    return NPp * nch <= kGramOneBlock && grid - 1 - nch >= 8;
 }
 
 // grid: one persistent block per SM, less the SMs of an overlapped gather
-void launch_chain_k(rocp_stream* st, const ChainParams& p, int grid) {
+void launch_chain_k(rocp_stream* st, const ChainParams& p, int grid, bool flow) {
     const bool wide = p.R > 32, trace = p.trace != nullptr;
-    if (wide) trace ? launch_chain_inst<true, true>(st, p, grid) : launch_chain_inst<true, false>(st, p, grid);
-    else trace ? launch_chain_inst<false, true>(st, p, grid) : launch_chain_inst<false, false>(st, p, grid);
+    if (flow) {
+        const int rp = ((p.R + kCRB - 1) / kCRB) * kCRB;
+        const void* fn = nullptr;
+        if (rp == 8) fn = trace ? reinterpret_cast<const void*>(k_flow<8, true>) : reinterpret_cast<const void*>(k_flow<8, false>);
+        else if (rp == 16) fn = trace ? reinterpret_cast<const void*>(k_flow<16, true>) : reinterpret_cast<const void*>(k_flow<16, false>);
+        else if (rp == 24) fn = trace ? reinterpret_cast<const void*>(k_flow<24, true>) : reinterpret_cast<const void*>(k_flow<24, false>);
+        else fn = trace ? reinterpret_cast<const void*>(k_flow<32, true>) : reinterpret_cast<const void*>(k_flow<32, false>);
+        launch_coop(st, fn, "k_flow", p, grid);
+    } else if (wide) {
+        if (trace) launch_coop(st, reinterpret_cast<const void*>(k_chain<true, true>), "k_chain", p, grid);
+        else launch_coop(st, reinterpret_cast<const void*>(k_chain<true, false>), "k_chain", p, grid);
+    } else {
+        if (trace) launch_coop(st, reinterpret_cast<const void*>(k_chain<false, true>), "k_chain", p, grid);
+        else launch_coop(st, reinterpret_cast<const void*>(k_chain<false, false>), "k_chain", p, grid);
+    }
 }
 
 // The whole factor-dependent chain of the prepared window as ONE cooperative
@@ -1308,6 +1346,22 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
         p.gneed = st->win.jobs.need.p;
         grid -= st->win_gsms;
     }
+    const bool flow = use_flow(st, grid);
+    if (flow) {
+        int maxtiles = int((B + kRowTile - 1) / kRowTile);
+        for (int64_t I : st->head) maxtiles = std::max(maxtiles, int((I + kRowTile - 1) / kRowTile));
+        const size_t nctr = size_t(1 + 2 * st->N + st->N * maxtiles);
+        st->fctr.ensure(nctr);
+        st->ginv.ensure(size_t(2 * kGinvSlot));
+        st->gmode.ensure(2);
+        st->wtemp.ensure(size_t(B * st->R));
+        CK(cudaMemsetAsync(st->fctr.p, 0, nctr * sizeof(unsigned), st->dev->stream));
+        p.ginv = st->ginv.p;
+        p.gmode = st->gmode.p;
+        p.wtemp = st->wtemp.p;
+        p.fctr = st->fctr.p;
+        p.maxtiles = maxtiles;
+    }
     if (st->trace_on) {
         st->trace.ensure(size_t(nb * st->N * kTraceSlots));
         CK(cudaMemsetAsync(st->trace.p, 0, size_t(nb * st->N * kTraceSlots) * 8, st->dev->stream));
@@ -1325,10 +1379,10 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
         }
         auto& ev = st->chain_events[st->chain_events_used++];
         CK(cudaEventRecord(ev.first, st->dev->stream));
-        launch_chain_k(st, p, grid);
+        launch_chain_k(st, p, grid, flow);
         CK(cudaEventRecord(ev.second, st->dev->stream));
     } else {
-        launch_chain_k(st, p, grid);
+        launch_chain_k(st, p, grid, flow);
     }
     if (overlap) CK(cudaStreamWaitEvent(st->dev->stream, st->dev->ev_gdone, 0));  // join the gather stream
     if (st->resid_level >= 1) {  // sampled residual of every batch's temporal solve (off the chain)
