@@ -25,7 +25,7 @@ namespace rocpk {
 //   contraction    items of X_s Z as in k_chain; the last item of a 32-row tile
 //                  sums the tile's superchunk partials into P in place (or the
 //                  temporal right-hand sides into wtemp)
-//   materialisers  (the blocks without a chunk, at the start of the next stage)
+//   materialise    the chunk blocks, once their chunk of the next stage is out,
 //                  write every row of the solved factor, off the critical path
 // Dependencies are counters (release: __threadfence + atomicAdd; acquire:
 // ld.acquire.gpu polls by one thread per block, then a block barrier), so the
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     const int NPp = (npairs + 1) & ~1;
     const int cblocks = G - 1;  // block G - 1 is the Gram finisher
     const bool is_fin = int(blockIdx.x) == G - 1;
-    const int nmat = cblocks - nch;  // materialisers [0, nmat); chunk ch on block cblocks - 1 - ch (host: nmat >= 8)
+    // chunk ch on block cblocks - 1 - ch (the host keeps at least 8 blocks without a chunk)
     const int ch = is_fin ? nch : cblocks - 1 - int(blockIdx.x);
     const bool chunk_block = ch >= 0 && ch < nch;
     const bool lr = lane < R;
@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     unsigned* tile_ctr = p.fctr + 1 + 2 * N;
     double* xs = sm + kSmXs;
     double* zs = sm + kSmZs;
-    double* wsm = sm + kSmFact;  // per warp: the right-hand-side rows it turns into factor rows [8][4][32]
+    double* wsm = sm + kSmFact;         // per warp: the right-hand-side rows it turns into factor rows [8][4][32]
+    double* gsm = sm + kSmFact + 1024;  // G^-1 of the stage whose rows this block forms
     unsigned phase = 0;
     if (tid == 0) {
         int off = 0;
@@ -96,10 +97,16 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
         if (tid == 0) wait_gathered(c, need, 0u, 0u);
     };
     // column `lane` of the G^-1 of stage sp (symmetric: G^-1(k, lane) = slot[k R + lane])
-    auto load_gcol = [&](int sp, double* g) {
+    // G^-1 of stage sp into shared memory, once per block (a per-warp load of the same few
+    // lines from L2 by every warp of every chunk block queues at the L2 slices); block-uniform,
+    // the caller synchronises before load_gcol
+    auto stage_ginv = [&](int sp) {
         const double* slot = p.ginv + (sp & 1) * kGinvSlot;
+        for (int t = tid; t < RR; t += kChainThreads) gsm[t] = __ldcg(slot + t);
+    };
+    auto load_gcol = [&](double* g) {
 #pragma unroll
-        for (int k = 0; k < MAXR; ++k) g[k] = (lr && k < R) ? __ldcg(slot + k * R + lane) : 0.0;
+        for (int k = 0; k < MAXR; ++k) g[k] = (lr && k < R) ? gsm[k * R + lane] : 0.0;
     };
     // u_lane = fma chain over k of w_k G^-1(k, lane) (oracle solve_gram_m), w in shared memory
     auto row_dot = [&](const double* w, const double* g) {
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     load_idx(0, 0);
 
     // rows of the stage sp = (bp, stp) solved before, by this block's warps: warp-global index
-    // gw, rows gw, gw + nw_total, ...
+    // gw, rows gw, gw + nw_total, ...; four rows at a time, their loads issued together
     auto materialise = [&](int bp, int stp, int gw, int nw_total) {
         const int rows = rows_of(stp);
         if (gw >= rows) return;
@@ -136,15 +143,25 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
         double* out = out_of(bp, stp);
         const int md = __ldcg(p.gmode + ((bp * N + stp) & 1));
         double g[MAXR];
-        load_gcol(bp * N + stp, g);
-        double* wr = wsm + warp * 32;
-        for (int row = gw; row < rows; row += nw_total) {
-            const double w = lr ? __ldcg(W + int64_t(row) * R + lane) : 0.0;
+        load_gcol(g);  // gsm holds the G^-1 of (bp, stp)
+        double* wr = wsm + warp * (4 * 32);
+        for (int row0 = gw; row0 < rows; row0 += 4 * nw_total) {
+            double w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int row = row0 + q * nw_total;
+                w[q] = (lr && row < rows) ? __ldcg(W + int64_t(row) * R + lane) : 0.0;
+            }
             __syncwarp();
-            wr[lane] = w;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) wr[q * 32 + lane] = w[q];
             __syncwarp();
-            const double u = row_dot(wr, g);
-            if (lr) out[int64_t(row) * R + lane] = md ? u : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int row = row0 + q * nw_total;
+                const double u = row_dot(wr + q * 32, g);
+                if (lr && row < rows) out[int64_t(row) * R + lane] = md ? u : 0.0;
+            }
         }
     };
 
@@ -196,10 +213,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         wait_ge(tsum_ctr + st1, unsigned(b1 + 1) * unsigned(tiles_of(st1)));
                         __syncthreads();
                         if (tr) trace_stamp(tr, 0, ch == 0 && tid == 0);
-                        double g[MAXR];
-                        load_gcol(sg - 1, g);
                         const double* W = wrows_of(st1);
-                        const int md = __ldcg(p.gmode + ((sg - 1) & 1));
+                        double wq[kSPW];
 #pragma unroll
                         for (int q = 0; q < kSPW; ++q) {
                             int32_t iw = 0;
@@ -207,8 +222,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                             for (int l = 0; l < kMaxOrder - 1; ++l)
                                 if (l == lod) iw = nidx[q][l];
                             const bool live = warp + kW * q < cn && lr;
-                            wsm[(warp * kSPW + q) * 32 + lane] = live ? __ldcg(W + int64_t(iw) * R + lane) : 0.0;
+                            wq[q] = live ? __ldcg(W + int64_t(iw) * R + lane) : 0.0;
                         }
+                        const int md = __ldcg(p.gmode + ((sg - 1) & 1));
+                        stage_ginv(sg - 1);
+                        __syncthreads();
+                        double g[MAXR];
+                        load_gcol(g);
+#pragma unroll
+                        for (int q = 0; q < kSPW; ++q) wsm[(warp * kSPW + q) * 32 + lane] = wq[q];
                         __syncwarp();
 #pragma unroll
                         for (int q = 0; q < kSPW; ++q) {
@@ -247,27 +269,26 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     if (tr) trace_stamp(tr, 1, ch == 0 && tid == 0);
                     const int nb2 = (st + 1 < N) ? b : b + 1, ns2 = (st + 1 < N) ? st + 1 : 0;
                     load_idx(nb2, ns2);
-                } else if (sg >= 1) {
-                    // ------------- materialise every row of stage sg - 1 (off the critical path)
-                    wait_ge(fin_ctr, unsigned(sg));
-                    wait_ge(tsum_ctr + st1, unsigned(b1 + 1) * unsigned(tiles_of(st1)));
-                    __syncthreads();
-                    const int nwt = nmat * kW;
-                    const int gw = (nmat - 1 - int(blockIdx.x)) + warp * nmat;
-                    materialise(b1, st1, gw, nwt);
-                    __syncthreads();
-                    if (tid == 0) {
-                        const int rows1 = rows_of(st1);
-                        unsigned n = 0;
-                        for (int w = 0; w < kW; ++w) {
-                            const int g0 = (nmat - 1 - int(blockIdx.x)) + w * nmat;
-                            if (g0 < rows1) n += unsigned((rows1 - 1 - g0) / nwt + 1);
+                    if (sg >= 1) {
+                        // ------------- every row of stage sg - 1, off the critical path: the chunk
+                        // blocks are idle until the next stage (its chunks need these rows only
+                        // two stages on, rows_ctr)
+                        const int nwt = nch * kW;
+                        materialise(b1, st1, ch + warp * nch, nwt);
+                        __syncthreads();
+                        if (tid == 0) {
+                            const int rows1 = rows_of(st1);
+                            unsigned n = 0;
+                            for (int w = 0; w < kW; ++w) {
+                                const int g0 = ch + w * nch;
+                                if (g0 < rows1) n += unsigned((rows1 - 1 - g0) / nwt + 1);
+                            }
+                            if (n) {
+                                __threadfence();
+                                atomicAdd(rows_ctr + st1, n);
+                            }
+                            if (tr && ch == 0) tr[5] = gtimer();
                         }
-                        if (n) {
-                            __threadfence();
-                            atomicAdd(rows_ctr + st1, n);
-                        }
-                        if (tr && blockIdx.x == 0) tr[5] = gtimer();
                     }
                 }
 
@@ -302,7 +323,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     const int cc0 = warp * kChunk;
                     const int cn0 = max(min(kChunk, cn - cc0), 0);
                     double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
-                    chain_contract_blocked<MAXR / 4>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                    // fp64 tensor cores (bit-identical to the register-blocked fma chains:
+                    // tools/contract_bench.cu; 7270 -> 5842 cycles per R = 20 item)
+                    chain_contract_dmma<MAXR / 8>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
                     // the tile's last item sums its superchunk partials (rocp.cpp:107: P += X_s Z)
                     if (tid == 0) {
                         __threadfence();
@@ -414,6 +437,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
         const int bl = p.nb - 1, stl = N - 1;
         wait_ge(fin_ctr, unsigned(sl + 1));
         wait_ge(tsum_ctr + stl, unsigned(bl + 1) * unsigned(tiles_of(stl)));
+        __syncthreads();
+        stage_ginv(sl);
         __syncthreads();
         materialise(bl, stl, int(blockIdx.x) + warp * G, G * kW);
     }

@@ -896,9 +896,13 @@ __device__ __noinline__ int2 gram_solve_block(const double* G, int R, double* gi
     __shared__ double s_tr, s_maxdiag, s_gnorm;
     __shared__ int s_path, s_mode, s_reg, s_jflag;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    sweep_block<EPT>(G, 0.0, R, cbuf, gi, piv);
+    // the certificate's inputs, three warps in parallel (off the sweep's chain)
+    __shared__ double s_dmin, s_dmax, s_tau;
     if (warp == 0) {
         if (lane == 0) {  // solve.cpp:9-16 prologue: max diagonal, trace (k order)
             double maxdiag = G[0], trc = G[0];
+#pragma unroll 4
             for (int k = 1; k < R; ++k) {
                 const double dg = G[k * R + k];
                 if (dg > maxdiag) maxdiag = dg;
@@ -910,18 +914,23 @@ __device__ __noinline__ int2 gram_solve_block(const double* G, int R, double* gi
     } else if (warp == 1) {
         const double gn = gram_inf_norm_warp(G, R, R);
         if (lane == 0) s_gnorm = gn;
-    }
-    sweep_block<EPT>(G, 0.0, R, cbuf, gi, piv);
-    if (tid == 0) {
+    } else if (warp == 2 && lane == 0) {
         double dmin = piv[0], dmax = piv[0], tau = gi[0];
+#pragma unroll 4
         for (int k = 0; k < R; ++k) {
             const double dk = piv[k];
             if (dk < dmin) dmin = dk;
             if (dk > dmax) dmax = dk;
             if (k > 0) tau = tau + gi[k * R + k];
         }
+        s_dmin = dmin;
+        s_dmax = dmax;
+        s_tau = tau;
+    }
+    __syncthreads();
+    if (tid == 0) {
         bool ut;
-        const int path = gram_certificate(s_maxdiag, s_gnorm, dmin, dmax, tau, R, &ut);
+        const int path = gram_certificate(s_maxdiag, s_gnorm, s_dmin, s_dmax, s_tau, R, &ut);
         if (count) count_decision(path, ut);
         s_path = path;
         s_mode = 1;
