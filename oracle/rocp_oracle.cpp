@@ -274,7 +274,7 @@ Sweep gram_sweep(const std::vector<double>& g, int R, double lambda) {
 // pivots d_k, which are the LDL^T pivots of G, and the G^-1 it yields, gram_sweep above):
 //   * every pivot of an SPD matrix lies in [lambda_min, lambda_max], so
 //     dmax / dmin <= kappa;
-//   * tau = tr(G^-1) = sum_k G^-1(k, k) (k increasing) lies in
+//   * tau = tr(G^-1) (summed in the kernels' 32-lane butterfly order) lies in
 //     [1 / lambda_min, R / lambda_min], and maxdiag <= lambda_max <= |G|_inf, so
 //     maxdiag tau / R <= kappa <= |G|_inf tau.
 // kappa certainly above 4e12 -> regularise; certainly below 2.5e11 -> not; a
@@ -326,24 +326,36 @@ double gram_inf_norm(const std::vector<double>& g, int R) {
 // the tau bounds (the pivot ratio did not settle it), [4] Jacobi sweeps
 int64_t g_decision_paths[5] = {0, 0, 0, 0, 0};
 
-// The certificate: pivot ratio, then the tau bounds from the unregularised inverse gi.
+// The certificate: pivot ratio, then the tau bounds (products, no quotients: the device
+// forms them on its critical path).  tau = tr(G^-1) in the kernels' 32-lane order: lane l
+// holds G^-1(l, l) + G^-1(l + 32, l + 32) (0 past R), then an xor butterfly (16, 8, 4, 2, 1).
+double ginv_trace_lanes(const std::vector<double>& gi, int R) {
+    std::vector<double> v(32, 0.0);
+    for (int l = 0; l < 32; ++l) {
+        const double a = (l < R) ? gi[size_t(l + l * R)] : 0.0;
+        const double b = (l + 32 < R) ? gi[size_t((l + 32) + (l + 32) * R)] : 0.0;
+        v[size_t(l)] = a + b;
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+        std::vector<double> w(32);
+        for (int l = 0; l < 32; ++l) w[size_t(l)] = v[size_t(l)] + v[size_t(l ^ off)];
+        v = w;
+    }
+    return v[0];
+}
+
 int certificate(double maxdiag, double gnorm, const Sweep& f, int R) {
-    const std::vector<double>& gi = f.gi;
     double dmin = f.d[0], dmax = f.d[0];
     for (double x : f.d) {
         if (x < dmin) dmin = x;
         if (x > dmax) dmax = x;
     }
     if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
-    const double ratio = dmax / dmin;
-    if (ratio > kCertRegAbove) return kDecReg;
+    if (dmax > kCertRegAbove * dmin) return kDecReg;  // dmax / dmin <= kappa
     ++g_decision_paths[3];
-    double tau = gi[0];
-    for (int k = 1; k < R; ++k) tau = tau + gi[size_t(k + k * R)];
-    const double klo = (maxdiag * tau) / double(R);
-    const double khi = gnorm * tau;
-    if (klo > kCertRegAbove) return kDecReg;
-    if (khi <= kCertNoRegBelow) return kDecNoReg;
+    const double tau = ginv_trace_lanes(f.gi, R);
+    if (maxdiag * tau > kCertRegAbove * double(R)) return kDecReg;  // maxdiag tau / R <= kappa
+    if (gnorm * tau <= kCertNoRegBelow) return kDecNoReg;         // kappa <= |G|_inf tau
     return kDecExact;
 }
 

@@ -764,12 +764,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (tr) trace_stamp(tr, 12, tid == 0);
                     int2 mr;
                     if constexpr (!kWide) {
-                        if (npairs <= 256) mr = gram_solve_block<1>(Gs, R, gi, D, colb, sm, true);
-                        else if (npairs <= 512) mr = gram_solve_block<2>(Gs, R, gi, D, colb, sm, true);
-                        else mr = gram_solve_block<3>(Gs, R, gi, D, colb, sm, true);
+                        if (npairs <= 224) mr = gram_solve_block<1>(Gs, R, pairs, gi, colb, sm, true);
+                        else if (npairs <= 448) mr = gram_solve_block<2>(Gs, R, pairs, gi, colb, sm, true);
+                        else mr = gram_solve_block<3>(Gs, R, pairs, gi, colb, sm, true);
                     } else {
-                        if (npairs <= 1280) mr = gram_solve_block<5>(Gs, R, gi, D, colb, sm, true);
-                        else mr = gram_solve_block<9>(Gs, R, gi, D, colb, sm, true);
+                        if (npairs <= 1344) mr = gram_solve_block<6>(Gs, R, pairs, gi, colb, sm, true);
+                        else mr = gram_solve_block<10>(Gs, R, pairs, gi, colb, sm, true);
                     }
                     const int s_mode = mr.x, reg = mr.y;
                     if (tr) trace_stamp(tr, 11, tid == 0);

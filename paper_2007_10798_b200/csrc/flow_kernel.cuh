@@ -40,6 +40,70 @@ namespace rocpk {
 
 constexpr int kGinvSlot = 32 * 32;  // doubles per G^-1 slot (R <= 32)
 
+// One contraction item of k_flow on the fp64 tensor cores: rows [8 a0, 8 (a0 + AT)) of a
+// 32-row X_s tile against a superchunk of Z (warp w = chunk w), AT row tiles of 8 x NT column
+// tiles of 8x8 accumulators per warp.  The same per-output operation sequence as
+// chain_contract_dmma (chunk partial = fma chain over the chunk's samples from +0.0, the
+// mma rounding like that chain; superchunk partial = chunk partials left to right), so a
+// stage with few items can split each tile's rows over 2 or 4 blocks bit-identically.
+template <int NT, int AT>
+__device__ __noinline__ void flow_contract_dmma(const double* xs, const double* zs, double* red, int cc0, int ccn,
+                                                int nk, int a0, int nrows, int R, double* out_rows) {
+    constexpr int RP = 8 * NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, rr = lane >> 2;
+    double acc[AT][NT][2];
+#pragma unroll
+    for (int a = 0; a < AT; ++a)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[a][n][0] = acc[a][n][1] = 0.0;
+    for (int k0 = 0; k0 < ccn; k0 += 4) {
+        const bool valid = k0 + q < ccn;
+        const int smp = cc0 + k0 + q;
+        double fa[AT], fb[NT];
+#pragma unroll
+        for (int a = 0; a < AT; ++a) fa[a] = valid ? xs[smp * kRowTile + (a0 + a) * 8 + rr] : 0.0;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) fb[n] = valid ? zs[smp * RP + n * 8 + rr] : 0.0;
+#pragma unroll
+        for (int a = 0; a < AT; ++a)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(acc[a][n][0]), "+d"(acc[a][n][1])
+                             : "d"(fa[a]), "d"(fb[n]));
+    }
+    __syncthreads();  // every warp is done with the X tile (the Z tile stays resident)
+    constexpr int HC = RP / 2;  // columns per half
+    constexpr int RS = (8 * HC * kRedStride <= kSuperSamples * kRowTile) ? kRedStride : kRowTile;
+    constexpr int NR = 8 * AT;  // rows of this item
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (warp < nk) {
+#pragma unroll
+            for (int a = 0; a < AT; ++a)
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = n * 8 + 2 * q + e, row = a * 8 + rr;
+                        if (col >= h * HC && col < (h + 1) * HC)
+                            red[(warp * HC + col - h * HC) * RS + row] = acc[a][n][e];
+                    }
+        }
+        __syncthreads();
+        for (int e = tid; e < HC * NR; e += blockDim.x) {
+            const int c = e / NR, il = e - c * NR, r = h * HC + c, i = a0 * 8 + il;
+            if (i < nrows && r < R) {
+                double qq = red[c * RS + il];
+                for (int k = 1; k < nk; ++k) qq = qq + red[(k * HC + c) * RS + il];
+                out_rows[int64_t(i) * R + r] = qq;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // MAXR = RP (R padded to a multiple of 8, <= 32): every loop over R is unrolled.
 template <int MAXR, bool kTrace>
 __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) {
@@ -292,10 +356,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     }
                 }
 
-                // ------------- contraction items (tile, superchunk), stride cblocks
+                // ------------- contraction items (tile, superchunk[, row part]), stride cblocks; a
+                // stage with few items splits each tile's rows over F = 2 or 4 blocks
+                const int F = (4 * n_contract <= cblocks) ? 4 : ((2 * n_contract <= cblocks) ? 2 : 1);
                 int zm_cur = -1;
-                for (int item = first_item; item < n_contract; item += cblocks) {
-                    const int tile = item % tiles, m = item / tiles;
+                for (int item = first_item; item < F * n_contract; item += cblocks) {
+                    const int part = item % F, base = item / F;
+                    const int tile = base % tiles, m = base / tiles;
                     const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                     const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
                     if (tid == 0) {  // X_s tile (from the overlapped gather when it runs) and Z tile
@@ -325,12 +392,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     double* orow = p.cpart + (int64_t(m) * rows + i0) * R;
                     // fp64 tensor cores (bit-identical to the register-blocked fma chains:
                     // tools/contract_bench.cu; 7270 -> 5842 cycles per R = 20 item)
-                    chain_contract_dmma<MAXR / 8>(xs, zs, xs, cc0, cn0, nk, nrows, R, orow);
+                    if (F == 1) flow_contract_dmma<MAXR / 8, 4>(xs, zs, xs, cc0, cn0, nk, 0, nrows, R, orow);
+                    else if (F == 2) flow_contract_dmma<MAXR / 8, 2>(xs, zs, xs, cc0, cn0, nk, 2 * part, nrows, R, orow);
+                    else flow_contract_dmma<MAXR / 8, 1>(xs, zs, xs, cc0, cn0, nk, part, nrows, R, orow);
                     // the tile's last item sums its superchunk partials (rocp.cpp:107: P += X_s Z)
                     if (tid == 0) {
                         __threadfence();
                         const unsigned prev = atomicAdd(tile_ctr + st * p.maxtiles + tile, 1u);
-                        s_last = (prev + 1 == unsigned(b + 1) * unsigned(nsuper)) ? 1 : 0;
+                        s_last = (prev + 1 == unsigned(b + 1) * unsigned(F * nsuper)) ? 1 : 0;
                     }
                     __syncthreads();
                     if (s_last) {
@@ -412,9 +481,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                 if (tr) trace_stamp(tr, 10, tid == 0);
                 // solve_gram (solve.cpp:9-35) in canonical form (kernels.cuh gram_solve_block)
                 int2 mr;
-                if (npairs <= 256) mr = gram_solve_block<1>(Gs, R, gi, D, colb, sm, true);
-                else if (npairs <= 512) mr = gram_solve_block<2>(Gs, R, gi, D, colb, sm, true);
-                else mr = gram_solve_block<3>(Gs, R, gi, D, colb, sm, true);
+                if (npairs <= 224) mr = gram_solve_block<1>(Gs, R, pairs, gi, colb, sm, true);
+                else if (npairs <= 448) mr = gram_solve_block<2>(Gs, R, pairs, gi, colb, sm, true);
+                else mr = gram_solve_block<3>(Gs, R, pairs, gi, colb, sm, true);
                 if (tr) trace_stamp(tr, 11, tid == 0);
                 double* slot = p.ginv + (sg & 1) * kGinvSlot;
                 for (int t = tid; t < RR; t += kChainThreads) slot[t] = gi[t];

@@ -627,12 +627,24 @@ __device__ __forceinline__ double butterfly_max32(double v) {
 }
 
 // |G|_inf (max absolute row sum; row sums in column order), one warp; a(i,j) at G[i + j*ldg].
+// The loads of 8 columns are issued before their adds (the sum is the only dependency).
 __device__ __noinline__ double gram_inf_norm_warp(const double* G, int ldg, int R) {
     const int lane = threadIdx.x & 31;
     double r0 = 0.0, r1 = 0.0;
-    for (int j = 0; j < R; ++j) {
-        if (lane < R) r0 = r0 + fabs(G[lane + j * ldg]);
-        if (lane + 32 < R) r1 = r1 + fabs(G[lane + 32 + j * ldg]);
+    for (int j0 = 0; j0 < R; j0 += 8) {
+        double v0[8], v1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + u;
+            v0[u] = (j < R && lane < R) ? fabs(G[lane + j * ldg]) : 0.0;
+            v1[u] = (j < R && lane + 32 < R) ? fabs(G[lane + 32 + j * ldg]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (j0 + u < R) {
+                r0 = r0 + v0[u];
+                r1 = r1 + v1[u];
+            }
     }
     double v = (lane < R) ? r0 : 0.0;
     if (lane + 32 < R) v = max_of(v, r1);
@@ -648,28 +660,19 @@ __device__ __forceinline__ void count_decision(int final_path, bool used_tau) {
     if (used_tau) atomicAdd(&g_dec_paths[3], 1ull);
 }
 
-// The certificate (oracle certificate): pivot ratio, then the tau bounds.  *used_tau:
-// whether the tau bounds were reached.
+// The certificate (oracle certificate): pivot ratio, then the tau bounds, as products (no
+// quotient on the finisher's chain).  *used_tau: whether the tau bounds were reached.
 __device__ __forceinline__ int gram_certificate(double maxdiag, double gnorm, double dmin, double dmax, double tau,
                                                 int R, bool* used_tau) {
     *used_tau = false;
     if (!(maxdiag > 0.0) || !(dmin > 0.0)) return kDecExact;
-    const double ratio = dmax / dmin;
-    if (ratio > kCertRegAbove) return kDecReg;
+    if (dmax > kCertRegAbove * dmin) return kDecReg;
     *used_tau = true;
-    const double klo = (maxdiag * tau) / double(R);
-    const double khi = gnorm * tau;
-    if (klo > kCertRegAbove) return kDecReg;
-    if (khi <= kCertNoRegBelow) return kDecNoReg;
+    if (maxdiag * tau > kCertRegAbove * double(R)) return kDecReg;
+    if (gnorm * tau <= kCertNoRegBelow) return kDecNoReg;
     return kDecExact;
 }
 
-// tau = G^-1(0,0) + G^-1(1,1) + ... in k order (oracle certificate); Gi R x R.
-__device__ __forceinline__ double ginv_trace(const double* Gi, int R) {
-    double t = Gi[0];
-    for (int k = 1; k < R; ++k) t = t + Gi[k + k * R];
-    return t;
-}
 
 // ---------------------------------------------------------------------------
 // G^-1 by the symmetric sweep (Gauss-Jordan without pivoting, oracle
@@ -685,68 +688,84 @@ __device__ __forceinline__ double ginv_trace(const double* Gi, int R) {
 // The sweep by a whole block on the LOWER triangle (the canonical form, oracle gram_sweep:
 // entries (i, j), i >= j, each step reading column k through symmetry, c_x = A(x, k) for
 // x >= k and A(k, x) for x < k; G^-1 symmetric by construction).  R <= 64 with
-// R (R + 1) / 2 <= EPT * blockDim: thread t owns the lower entries t, t + blockDim, ...
-// (column by column) in registers, indices formed once.  Column k + 1 is published in cbuf
-// (2 x 64, by step parity) by the owners of its entries as they update them, so a step is
-// one block barrier, one reciprocal (formed redundantly by every thread) and one fma per
-// entry.  Writes G^-1 to gi (both triangles; gi[i * R + j] = G^-1(i, j)); piv (if set)
-// gets d_k at [k].  Block-uniform call.
+// R (R + 1) / 2 <= EPT * (blockDim - 32): thread t owns the lower entries t, t + nt, ...
+// (column by column; pairs[e] = (i << 8) | j when the caller has the table) in registers.
+// Column k + 1 is published in cbuf (2 x 64, by step parity) by the owners of its entries as
+// they update them, so a step is one block barrier, one reciprocal (formed redundantly by
+// every thread) and one fma per entry.  Writes G^-1 to gi (both triangles; gi[i * R + j] =
+// G^-1(i, j)); thread 0 gets min_k d_k, max_k d_k in *dmin, *dmax.  Block-uniform call.
 template <int EPT>
-__device__ __noinline__ void sweep_block(const double* G, double lambda, int R, double* cbuf, double* gi,
-                                         double* piv) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+__device__ __noinline__ void sweep_block(const double* G, double lambda, int R, const unsigned short* pairs,
+                                         double* cbuf, double* gi, double* dmin, double* dmax) {
+    // warps 0 .. nw-2 (blockDim - 32 threads, named barrier 1); the last warp is free for
+    // the caller's independent work and joins at the final block barrier
+    const int tid = threadIdx.x, nt = blockDim.x - 32;
     const int np = R * (R + 1) / 2;
-    double a[EPT];
-    int ii[EPT], jj[EPT];
-#pragma unroll
-    for (int q = 0; q < EPT; ++q) {
-        const int e = tid + q * nt;
-        int i = 0, j = -1;  // j = -1: no entry
-        if (e < np) {       // lower entry e, column by column: column j holds R - j entries
-            int rem = e;
-            j = 0;
-            while (rem >= R - j) {
-                rem -= R - j;
-                ++j;
-            }
-            i = j + rem;
-        }
-        ii[q] = i;
-        jj[q] = j;
-        const double g = (j >= 0) ? G[i + j * R] : 0.0;
-        a[q] = (i == j) ? g + lambda : g;
-        if (j == 0) cbuf[i] = a[q];
-    }
-    __syncthreads();
-    for (int k = 0; k < R; ++k) {
-        const double* c = cbuf + (k & 1) * 64;
-        double* cn = cbuf + ((k + 1) & 1) * 64;
-        const double d = c[k];
-        if (piv && tid == 0) piv[k] = d;
-        const double r = (fabs(d) > 2.2250738585072014e-308) ? 1.0 / d : 0.0;
+    if (tid < nt) {
+        double a[EPT];
+        int ii[EPT], jj[EPT];
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
-            const int i = ii[q], j = jj[q];
-            const double ci = c[i], cj = c[j < 0 ? 0 : j];
-            const double l = ci * r;
-            const double ov = __fma_rn(-l, cj, a[q]);
-            const double pv = __fma_rn(cj, r, 0.0);
-            const bool jk = j == k, ik = i == k;
-            const double v = jk ? (ik ? -r : l) : (ik ? pv : ov);
-            a[q] = v;
-            // column k + 1: below the diagonal (and the diagonal) from column k + 1, above it
-            // through row k + 1 (one predicated store)
-            const int tgt = (j == k + 1) ? i : ((i == k + 1 && j >= 0) ? j : -1);
-            if (tgt >= 0) cn[tgt] = v;
+            const int e = tid + q * nt;
+            int i = 0, j = -1;  // j = -1: no entry
+            if (e < np) {
+                if (pairs) {
+                    i = pairs[e] >> 8;
+                    j = pairs[e] & 0xff;
+                } else {  // lower entry e, column by column: column j holds R - j entries
+                    int rem = e;
+                    j = 0;
+                    while (rem >= R - j) {
+                        rem -= R - j;
+                        ++j;
+                    }
+                    i = j + rem;
+                }
+            }
+            ii[q] = i;
+            jj[q] = j;
+            const double g = (j >= 0) ? G[i + j * R] : 0.0;
+            a[q] = (i == j) ? g + lambda : g;
+            if (j == 0) cbuf[i] = a[q];
         }
-        __syncthreads();
-    }
+        asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+        double lo = 0.0, hi = 0.0;
+        for (int k = 0; k < R; ++k) {
+            const double* c = cbuf + (k & 1) * 64;
+            double* cn = cbuf + ((k + 1) & 1) * 64;
+            const double d = c[k];
+            if (k == 0) lo = hi = d;
+            if (d < lo) lo = d;
+            if (d > hi) hi = d;
+            const double r = (fabs(d) > 2.2250738585072014e-308) ? 1.0 / d : 0.0;
 #pragma unroll
-    for (int q = 0; q < EPT; ++q)
-        if (jj[q] >= 0) {
-            gi[ii[q] * R + jj[q]] = -a[q];
-            gi[jj[q] * R + ii[q]] = -a[q];
+            for (int q = 0; q < EPT; ++q) {
+                const int i = ii[q], j = jj[q];
+                const double ci = c[i], cj = c[j < 0 ? 0 : j];
+                const double l = ci * r;
+                const double ov = __fma_rn(-l, cj, a[q]);
+                const double pv = __fma_rn(cj, r, 0.0);
+                const bool jk = j == k, ik = i == k;
+                const double v = jk ? (ik ? -r : l) : (ik ? pv : ov);
+                a[q] = v;
+                // column k + 1: below the diagonal (and the diagonal) from column k + 1, above it
+                // through row k + 1 (one predicated store)
+                const int tgt = (j == k + 1) ? i : ((i == k + 1 && j >= 0) ? j : -1);
+                if (tgt >= 0) cn[tgt] = v;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
         }
+#pragma unroll
+        for (int q = 0; q < EPT; ++q)
+            if (jj[q] >= 0) {
+                gi[ii[q] * R + jj[q]] = -a[q];
+                gi[jj[q] * R + ii[q]] = -a[q];
+            }
+        if (tid == 0) {
+            *dmin = lo;
+            *dmax = hi;
+        }
+    }
     __syncthreads();
 }
 
@@ -886,23 +905,23 @@ __device__ __forceinline__ void exact_decision(double lo, double hi, int* mode, 
 // solve_gram (solve.cpp:9-35) for a block in canonical form: the sweep of G
 // (sweep_block), the regularisation decision (pivot ratio and tau bounds; exact Jacobi
 // eigenvalues in the band), the sweep of G + 1e-12 tr(G) I when it regularises.  G: R x R
-// (column-major, symmetric; not modified), gi: G^-1 (row-major, symmetric) when the mode
-// is 1, piv: R pivots, cbuf: 128 doubles, jscr: R * R + 128 doubles (exact path).  Returns
-// (mode, reg), mode 0 = zero solution.  count: add the path to the decision statistics.
-// Block-uniform call.
+// (column-major, symmetric; not modified), pairs: the lower-pair table or nullptr, gi: G^-1
+// (row-major, symmetric) when the mode is 1, cbuf: 128 doubles, jscr: R * R + 128 doubles
+// (exact path).  Returns (mode, reg), mode 0 = zero solution.  count: add the path to the
+// decision statistics.  Block-uniform call.
 template <int EPT>
-__device__ __noinline__ int2 gram_solve_block(const double* G, int R, double* gi, double* piv, double* cbuf,
-                                              double* jscr, bool count) {
-    __shared__ double s_tr, s_maxdiag, s_gnorm;
+__device__ __noinline__ int2 gram_solve_block(const double* G, int R, const unsigned short* pairs, double* gi,
+                                              double* cbuf, double* jscr, bool count) {
+    __shared__ double s_tr, s_maxdiag, s_gnorm, s_dmin, s_dmax;
     __shared__ int s_path, s_mode, s_reg, s_jflag;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    sweep_block<EPT>(G, 0.0, R, cbuf, gi, piv);
-    // the certificate's inputs, three warps in parallel (off the sweep's chain)
-    __shared__ double s_dmin, s_dmax, s_tau;
-    if (warp == 0) {
-        if (lane == 0) {  // solve.cpp:9-16 prologue: max diagonal, trace (k order)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    // the last warp forms |G|_inf, the max diagonal and the trace (k order, solve.cpp:9-16)
+    // while the others run the sweep
+    if (warp == nw - 1) {
+        const double gn = gram_inf_norm_warp(G, R, R);
+        if (lane == 0) {
+            s_gnorm = gn;
             double maxdiag = G[0], trc = G[0];
-#pragma unroll 4
             for (int k = 1; k < R; ++k) {
                 const double dg = G[k * R + k];
                 if (dg > maxdiag) maxdiag = dg;
@@ -911,30 +930,20 @@ __device__ __noinline__ int2 gram_solve_block(const double* G, int R, double* gi
             s_tr = trc;
             s_maxdiag = maxdiag;
         }
-    } else if (warp == 1) {
-        const double gn = gram_inf_norm_warp(G, R, R);
-        if (lane == 0) s_gnorm = gn;
-    } else if (warp == 2 && lane == 0) {
-        double dmin = piv[0], dmax = piv[0], tau = gi[0];
-#pragma unroll 4
-        for (int k = 0; k < R; ++k) {
-            const double dk = piv[k];
-            if (dk < dmin) dmin = dk;
-            if (dk > dmax) dmax = dk;
-            if (k > 0) tau = tau + gi[k * R + k];
-        }
-        s_dmin = dmin;
-        s_dmax = dmax;
-        s_tau = tau;
     }
-    __syncthreads();
-    if (tid == 0) {
-        bool ut;
-        const int path = gram_certificate(s_maxdiag, s_gnorm, s_dmin, s_dmax, s_tau, R, &ut);
-        if (count) count_decision(path, ut);
-        s_path = path;
-        s_mode = 1;
-        s_reg = (path == kDecReg) ? 1 : 0;
+    sweep_block<EPT>(G, 0.0, R, pairs, cbuf, gi, &s_dmin, &s_dmax);
+    if (warp == 0) {  // tau = tr(G^-1), lane pairs then butterfly (oracle ginv_trace_lanes)
+        double v = (lane < R) ? gi[lane * R + lane] : 0.0;
+        v = v + ((lane + 32 < R) ? gi[(lane + 32) * R + lane + 32] : 0.0);
+        v = butterfly32(v);
+        if (lane == 0) {
+            bool ut;
+            const int path = gram_certificate(s_maxdiag, s_gnorm, s_dmin, s_dmax, v, R, &ut);
+            if (count) count_decision(path, ut);
+            s_path = path;
+            s_mode = 1;
+            s_reg = (path == kDecReg) ? 1 : 0;
+        }
     }
     __syncthreads();
     if (s_path == kDecExact) {  // rare: Jacobi eigenvalues of a copy of G
@@ -950,7 +959,10 @@ __device__ __noinline__ int2 gram_solve_block(const double* G, int R, double* gi
         }
         __syncthreads();
     }
-    if (s_mode == 1 && s_reg) sweep_block<EPT>(G, 1e-12 * s_tr, R, cbuf, gi, piv);
+    if (s_mode == 1 && s_reg) {
+        double dlo, dhi;
+        sweep_block<EPT>(G, 1e-12 * s_tr, R, pairs, cbuf, gi, &dlo, &dhi);
+    }
     const int2 res = make_int2(s_mode, s_reg);
     __syncthreads();  // the shared scalars are reused by the next call
     return res;
@@ -970,13 +982,12 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
                                                const double* __restrict__ RHS, int32_t rows,
                                                double* __restrict__ OUT, int* flags,
                                                int nonfinite_code) {
-    extern __shared__ double ks_dyn[];  // G^-1 (R x R), jscr (R x R + 128), pivots (R), cbuf (128)
+    extern __shared__ double ks_dyn[];  // G^-1 (R x R), jscr (R x R + 128), cbuf (128)
     double* gi = ks_dyn;
     double* jscr = gi + R * R;
-    double* piv = jscr + R * R + 128;
-    double* cbuf = piv + R;
-    constexpr int kEpt = (MAXR * (MAXR + 1) / 2 + 255) / 256;  // lower entries per thread (256 threads)
-    const int2 mr = gram_solve_block<kEpt>(G, R, gi, piv, cbuf, jscr, blockIdx.x == 0);
+    double* cbuf = jscr + R * R + 128;
+    constexpr int kEpt = (MAXR * (MAXR + 1) / 2 + 223) / 224;  // lower entries per thread (224 sweep threads)
+    const int2 mr = gram_solve_block<kEpt>(G, R, nullptr, gi, cbuf, jscr, blockIdx.x == 0);
     if (blockIdx.x == 0 && threadIdx.x == 0 && mr.y && flags) atomicOr(flags, 1);
     // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64)
     const int tid = threadIdx.x, lane = tid & 31;

@@ -1088,6 +1088,17 @@ int gather_sms(rocp_stream* st, int64_t B) {
         const double t_full = elems / (93e3);                             // us, whole-device gather
         if (t_full < 0.025 * (t_full + t_chain)) return 0;
         g = int(std::ceil(elems / (1470.0 * t_chain)));
+        if (st->R <= 32) {
+            // the dataflow chain (k_flow) runs a stage in ~11 us on C2: size the gather for that
+            // with 20% headroom, as long as every contraction item of the largest stage still
+            // gets its own block (tools/runs: C2 G = 20 -> 592k, 24..32 -> 611k, 36 -> 516k)
+            const int64_t nch = (st->s + kChunk - 1) / kChunk, nsup = (st->s + kSuperSamples - 1) / kSuperSamples;
+            int64_t tiles = (B + kRowTile - 1) / kRowTile;
+            for (int64_t I : st->head) tiles = std::max<int64_t>(tiles, (I + kRowTile - 1) / kRowTile);
+            const int limit = int(dev->num_sms - 1 - nch - tiles * nsup);
+            const int gf = int(std::ceil(1.2 * elems / (1470.0 * st->N * 11.0)));
+            if (limit >= 8) return std::max(8, std::min(gf, limit));
+        }
         const int row_blocks = int(std::ceil(rows_max / (kChainThreads / 32)));
         if (row_blocks < dev->num_sms) g = std::min(g, dev->num_sms - row_blocks);
         g = std::max(g, 8);

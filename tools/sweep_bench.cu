@@ -1,5 +1,5 @@
-// Profiling aid: cycles of the Gram-inverse variants of the chain finisher on one warp /
-// block (148 independent blocks, block 0 timed with clock64), and a bitwise check of the
+// Profiling aid: cycles of the Gram-inverse sweep of the chain finisher (kernels.cuh sweep_block)
+// on one block (148 independent blocks, block 0 timed with clock64), and a bitwise check of the
 // sweep against a host restatement of the canonical order (oracle gram_sweep).
 #include <cmath>
 #include <cstdio>
@@ -29,102 +29,30 @@ static std::vector<double> host_sweep(const std::vector<double>& g, int R) {
     return gi;
 }
 
-// experiment variants of sweep_warp: V bit0: __drcp_rn; bit1: select instead of divergent
-// zeroing; bit2: no reciprocal at all (timing only)
-template <int MAXR, int V>
-__device__ __noinline__ void sweep_warp_x(const double* G, double lambda, int R, double* gi, double* cbuf) {
-    const int lane = threadIdx.x & 31;
-    double a[MAXR];
-#pragma unroll
-    for (int j = 0; j < MAXR; ++j) {
-        const bool ok = lane < R && j < R;
-        const double g = G[ok ? lane + j * R : 0];
-        a[j] = ok ? ((j == lane) ? g + lambda : g) : 0.0;
-    }
-    cbuf[lane] = a[0];
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < MAXR; ++k) {
-        if (k < R) {
-            const double* c = cbuf + (k & 1) * 32;
-            double cv[MAXR];
-#pragma unroll
-            for (int j = 0; j < MAXR; ++j) cv[j] = c[j];
-            const double d = cv[k];
-            double r;
-            if (V & 4) r = d * 0.5;
-            else if (V & 1) r = (fabs(d) > 2.2250738585072014e-308) ? __drcp_rn(d) : 0.0;
-            else r = (fabs(d) > 2.2250738585072014e-308) ? 1.0 / d : 0.0;
-            const bool me = lane == k;
-            const double l = a[k] * r;
-            const double mult = me ? r : -l;
-            if (!(V & 2)) {
-                if (me) {
-#pragma unroll
-                    for (int j = 0; j < MAXR; ++j) a[j] = 0.0;
-                }
-            }
-            if (k + 1 < MAXR) {
-                a[k + 1] = __fma_rn(cv[k + 1], mult, (V & 2) ? (me ? 0.0 : a[k + 1]) : a[k + 1]);
-                cbuf[((k + 1) & 1) * 32 + lane] = a[k + 1];
-            }
-#pragma unroll
-            for (int j = 0; j < MAXR; ++j)
-                if (j != k && j != k + 1) a[j] = __fma_rn(cv[j], mult, (V & 2) ? (me ? 0.0 : a[j]) : a[j]);
-            a[k] = me ? -r : l;
-            __syncwarp();
-        }
-    }
-    if (lane < R) {
-#pragma unroll
-        for (int j = 0; j < MAXR; ++j)
-            if (j < R) gi[lane * R + j] = -a[j];
-    }
-}
-
-// mode 0: ldlt_warp + flow_ginv (current); 1: sweep_warp; 2: sweep_block
+// the block sweep (kernels.cuh sweep_block), block 0 timed
 template <int MAXR>
 __global__ void __launch_bounds__(256, 1) k_bench(const double* G, int R, int mode, int reps, long long* cyc, double* out) {
     extern __shared__ double sm[];
-    __shared__ unsigned short pairs[32 * 33 / 2];
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        int off = 0;
-        for (int j = 0; j < R; ++j)
-            for (int i = j; i < R; ++i) pairs[off++] = (unsigned short)((i << 8) | j);
-    }
-    double* A = sm;                       // 64 x 65
-    double* D = A + 64 * kLdStride;       // 64
-    double* Gs = D + 64;                  // 64 x 64
-    double* colb = Gs + 64 * 64;          // 96 + 64
-    double* ms = colb + 256;              // 1024
-    double* gi = ms + 4096;               // 4096
+    double* Gs = sm;               // 64 x 64
+    double* colb = Gs + 64 * 64;   // 128
+    double* gi = colb + 128;       // 4096
+    double* dd = gi + 4096;        // 2
     for (int t = tid; t < R * R; t += blockDim.x) Gs[t] = G[t];
     __syncthreads();
     for (int rep = 0; rep < reps; ++rep) {
         const long long t0 = clock64();
-        if (mode == 0) {
-            if (tid < 32) ldlt_warp<MAXR>(Gs, 0.0, R, A, kLdStride, D, colb, D + 61);
-            __syncthreads();
-            flow_ginv<MAXR>(A, kLdStride, D, R, ms, colb + 96, gi, pairs, R * (R + 1) / 2);
-        } else if (mode == 1) {
-            if (tid < 32) sweep_warp<MAXR>(Gs, 0.0, R, gi, colb, D + 61, D);
-            __syncthreads();
-        } else if (mode == 2) {
-            const int np = R * (R + 1) / 2;
-            if (np <= 256) sweep_block<1>(Gs, 0.0, R, colb, gi, D);
-            else if (np <= 512) sweep_block<2>(Gs, 0.0, R, colb, gi, D);
-            else if (np <= 768) sweep_block<3>(Gs, 0.0, R, colb, gi, D);
-            else sweep_block<5>(Gs, 0.0, R, colb, gi, D);
-        } else {
-            if (tid < 32) {
-                if (mode == 3) sweep_warp_x<MAXR, 1>(Gs, 0.0, R, gi, colb);
-                else if (mode == 4) sweep_warp_x<MAXR, 3>(Gs, 0.0, R, gi, colb);
-                else if (mode == 5) sweep_warp_x<MAXR, 2>(Gs, 0.0, R, gi, colb);
-                else sweep_warp_x<MAXR, 6>(Gs, 0.0, R, gi, colb);
-            }
-            __syncthreads();
-        }
+        const int np = R * (R + 1) / 2;
+        if (mode == 1) {
+            double* jscr = dd + 8;
+            if (np <= 224) gram_solve_block<1>(Gs, R, nullptr, gi, colb, jscr, false);
+            else if (np <= 448) gram_solve_block<2>(Gs, R, nullptr, gi, colb, jscr, false);
+            else if (np <= 672) gram_solve_block<3>(Gs, R, nullptr, gi, colb, jscr, false);
+            else gram_solve_block<6>(Gs, R, nullptr, gi, colb, jscr, false);
+        } else if (np <= 224) sweep_block<1>(Gs, 0.0, R, nullptr, colb, gi, dd, dd + 1);
+        else if (np <= 448) sweep_block<2>(Gs, 0.0, R, nullptr, colb, gi, dd, dd + 1);
+        else if (np <= 672) sweep_block<3>(Gs, 0.0, R, nullptr, colb, gi, dd, dd + 1);
+        else sweep_block<6>(Gs, 0.0, R, nullptr, colb, gi, dd, dd + 1);
         const long long t1 = clock64();
         if (blockIdx.x == 0 && tid == 0) cyc[rep] = t1 - t0;
         __syncthreads();
@@ -154,11 +82,10 @@ void run(int R, std::mt19937_64& gen) {
     cudaMalloc(&dout, 64 * 64 * 8);
     cudaMalloc(&dc, 64 * 8);
     cudaMemcpy(dG, g.data(), g.size() * 8, cudaMemcpyHostToDevice);
-    const int smem = (64 * 65 + 64 + 4096 + 256 + 4096 + 4096) * 8;
+    const int smem = (4096 + 128 + 4096 + 8 + 4096 + 128) * 8;
     cudaFuncSetAttribute(k_bench<MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const char* names[7] = {"ldlt_warp+flow_ginv", "sweep_warp", "sweep_block", "sweep drcp", "sweep drcp+sel", "sweep sel", "sweep sel no-rcp"};
-    for (int mode = 0; mode < 7; ++mode) {
-        if (R > 32 && mode != 2) continue;
+    const char* names[2] = {"sweep_block", "gram_solve_block"};
+    for (int mode = 0; mode < 2; ++mode) {
         k_bench<MAXR><<<148, 256, smem>>>(dG, R, mode, 6, dc, dout);
         cudaError_t e = cudaDeviceSynchronize();
         long long c[6];
