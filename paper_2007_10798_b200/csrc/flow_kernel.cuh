@@ -27,8 +27,8 @@ namespace rocpk {
 //                  temporal right-hand sides into wtemp)
 //   materialise    the chunk blocks, once their chunk of the next stage is out,
 //                  write every row of the solved factor, off the critical path
-// Dependencies are counters (release: __threadfence + atomicAdd; acquire:
-// ld.acquire.gpu polls by one thread per block, then a block barrier), so the
+// Dependencies are counters (release: block barrier + red.release.gpu by one
+// thread; acquire: ld.acquire.gpu polls by one thread, then a block barrier), so the
 // critical path per stage is: previous G^-1 -> sampled rows -> Z chunk ->
 // chunk Gram -> combine -> sweep (G^-1) -> publish.  Reuse hazards are ordered
 // by the same chain: a stage's chunk blocks wait for the previous
@@ -159,6 +159,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     };
     auto wait_ge = [&](const unsigned* c, unsigned need) {
         if (tid == 0) wait_gathered(c, need, 0u, 0u);
+    };
+    auto publish = [&](unsigned* c, unsigned v) {  // after a block barrier, by one thread
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(c), "r"(v) : "memory");
     };
     // column `lane` of the G^-1 of stage sp (symmetric: G^-1(k, lane) = slot[k R + lane])
     // G^-1 of stage sp into shared memory, once per block (a per-warp load of the same few
@@ -325,10 +328,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     if (tr) trace_stamp(tr, 14, ch == 0 && tid == 0);
                     chain_chunk_gram_dmma(zc, RP, R, p.chpart + int64_t(ch) * NPp);
                     __syncthreads();
-                    if (tid == 0) {
-                        __threadfence();
-                        atomicAdd(p.zctr + 1 + ch / kSuper, 1u);
-                        atomicAdd(p.zctr, 1u);
+                    if (tid == 0) {  // one release fence for both counters
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.zctr + 1 + ch / kSuper) : "memory");
+                        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.zctr) : "memory");
                     }
                     if (tr) trace_stamp(tr, 1, ch == 0 && tid == 0);
                     const int nb2 = (st + 1 < N) ? b : b + 1, ns2 = (st + 1 < N) ? st + 1 : 0;
@@ -347,10 +350,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                                 const int g0 = ch + w * nch;
                                 if (g0 < rows1) n += unsigned((rows1 - 1 - g0) / nwt + 1);
                             }
-                            if (n) {
-                                __threadfence();
-                                atomicAdd(rows_ctr + st1, n);
-                            }
+                            if (n) publish(rows_ctr + st1, n);
                             if (tr && ch == 0) tr[5] = gtimer();
                         }
                     }
@@ -397,13 +397,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     else flow_contract_dmma<MAXR / 8, 1>(xs, zs, xs, cc0, cn0, nk, part, nrows, R, orow);
                     // the tile's last item sums its superchunk partials (rocp.cpp:107: P += X_s Z)
                     if (tid == 0) {
-                        __threadfence();
-                        const unsigned prev = atomicAdd(tile_ctr + st * p.maxtiles + tile, 1u);
+                        unsigned prev;
+                        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                                     : "=r"(prev) : "l"(tile_ctr + st * p.maxtiles + tile) : "memory");
                         s_last = (prev + 1 == unsigned(b + 1) * unsigned(F * nsuper)) ? 1 : 0;
                     }
                     __syncthreads();
                     if (s_last) {
-                        __threadfence();
                         double* W = wrows_of(st);
                         for (int e = tid; e < nrows * R; e += kChainThreads) {
                             const int64_t o = int64_t(i0) * R + e;
@@ -413,8 +413,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         }
                         __syncthreads();
                         if (tid == 0) {
-                            __threadfence();
-                            atomicAdd(tsum_ctr + st, 1u);
+                            publish(tsum_ctr + st, 1u);
                             if (tr) tr[6] = gtimer();  // the last tile sum of the stage overwrites
                         }
                     }
@@ -492,10 +491,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     if (mr.y) atomicOr(p.flags + (st == 0 ? 0 : 2), 1);
                 }
                 __syncthreads();
-                if (tid == 0) {
-                    __threadfence();
-                    atomicAdd(fin_ctr, 1u);
-                }
+                if (tid == 0) publish(fin_ctr, 1u);
                 if (tr) trace_stamp(tr, 4, tid == 0);
             }
         }
