@@ -626,10 +626,12 @@ std::vector<const Mat*> excluding(const std::vector<Mat>& fs, int mode) {
 
 // ---------------------------------------------------------------------------
 // Canonical fitness (kruskal.cpp:55-89 semantics).
-// Per mode-1 fibre: lane partial l = fma chain over i1 = l, l+32, ... of d*d;
-// butterfly combine (offsets 16,8,4,2,1), value of lane 0.  Fibre values are
-// combined by hsum (groups of 256: 8 lane-strided adds then a butterfly,
-// repeated until one value).
+// x_hat(i1, j) = fma chain over r of U1(i1, r) w_r(j) from +0.0 (w_r = U_N(i_N, r) * ... *
+// U_2(i_2, r) left to right); d = x_hat - x (x_hat = +0 for the norm of X alone).  Per
+// mode-1 fibre: eight partials p_m = fma chain of d*d over i1 = m, m+8, m+16, ... (the
+// fp64 MMA fragment rows of the kernel), then ((p0 + p1) + (p2 + p3)) + ((p4 + p5) +
+// (p6 + p7)).  Fibre values are combined by hsum (groups of 256: 8 lane-strided adds then a
+// butterfly, repeated until one value).
 double butterfly32(double q[32]) {
     for (int off = 16; off >= 1; off >>= 1) {
         double nq[32];
@@ -707,19 +709,18 @@ void fit_fibre(const double* t, const Dims& d, const std::vector<Mat>* fs, Index
                 w[size_t(r)] = acc;
             }
         }
-        double q[32];
-        for (int l = 0; l < 32; ++l) q[l] = 0.0;
+        double q[8];
+        for (int l = 0; l < 8; ++l) q[l] = 0.0;
         const double* col = t + j * I1;
         for (Index i = 0; i < I1; ++i) {
             double v = col[i];
-            if (fs) {
-                double xh = 0.0;
+            double xh = 0.0;
+            if (fs)
                 for (Index r = 0; r < R; ++r) xh = std::fma((*fs)[0](i, r), w[size_t(r)], xh);
-                v = xh - v;
-            }
-            q[i % 32] = std::fma(v, v, q[i % 32]);
+            v = xh - v;
+            q[i % 8] = std::fma(v, v, q[i % 8]);
         }
-        fib[size_t(j)] = butterfly32(q);
+        fib[size_t(j)] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
     }
 }
 

@@ -1080,77 +1080,136 @@ struct FitJob {
     double* out;            // 1 value
 };
 
-constexpr int kFitFibres = 8;
-
+// K7: fused fitness (kruskal.cpp:55-89 semantics) on the fp64 tensor cores.
+// A block takes a group of 256 mode-1 fibres: thread per fibre forms w_r (U_N ... U_2 left to
+// right) into shared memory; warp w of 8 takes the fibre tiles w, w + 8, w + 16, w + 24 (8
+// fibres each; for R > 20 two tiles at a time, registers) and streams the fibres' rows in
+// blocks of 32: x_hat = U1 . W^T with mma.sync m8n8k4
+// (A = 8 rows of U1, loaded once per row block for the warp's four tiles; B = the tile's w,
+// held in registers), so x_hat(i1, j) is the fma chain over r from +0.0 (the mma rounds
+// like that chain); the C fragment puts row i1 = 32 rb + 8 a + (lane >> 2) on the lane,
+// so the lane's partial of d^2 runs over i1 = m, m + 8, ... (m = lane >> 2) in increasing
+// i1, and the 8 partials of a fibre meet in an xor butterfly over lane bits 2..4.  The
+// tensor is read once, streaming.  KS = padded R / 4 (w and U1 are zero past R).
+template <int KS>
 __global__ void __launch_bounds__(256) k_fitness(const FitJob J) {
     extern __shared__ double smem[];
-    double* W = smem;                       // 256 x R
-    double* F = smem + kGroup * J.R;        // 256
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int RP4 = 4 * KS;
+    double* W = smem;                 // [256][RP4]
+    double* F = smem + kGroup * RP4;  // 256
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int q = lane & 3, rr = lane >> 2;
+    constexpr int kFW = 8;                   // warps: warp w takes fibre tiles w, w + 8, ...
+    constexpr int kTW = KS <= 5 ? 4 : 2;     // fibre tiles (of 8) per warp and pass (registers)
+    constexpr int kPass = kGroup / 8 / (kFW * kTW);
+    const int R = J.R;
+    const int64_t I1 = J.I1;
+    const int64_t nrb = (I1 + 31) / 32;
     const int64_t ngroups = (J.nfib + kGroup - 1) / kGroup;
+    const double* U1 = J.U[0];
     for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
         const int64_t j0 = g * kGroup;
+        const int n = int(min64(kGroup, J.nfib - j0));
         __syncthreads();
-        if (J.with_model) {
-            const int64_t j = j0 + threadIdx.x;
-            if (j < J.nfib) {
+        {
+            double w[RP4];
+#pragma unroll
+            for (int r = 0; r < RP4; ++r) w[r] = 0.0;
+            if (J.with_model && tid < n && tid < kGroup) {
                 int64_t idx[kMaxOrder];
-                int64_t rem = j;
+                int64_t rem = j0 + tid;
                 for (int m = 1; m < J.N; ++m) {
-                    const int64_t q = rem / J.dims[m];
-                    idx[m] = rem - q * J.dims[m];
-                    rem = q;
+                    const int64_t qq = rem / J.dims[m];
+                    idx[m] = rem - qq * J.dims[m];
+                    rem = qq;
                 }
-                for (int r = 0; r < J.R; ++r) {
-                    double acc = J.U[J.N - 1][idx[J.N - 1] * J.R + r];
-                    for (int m = J.N - 2; m >= 1; --m) acc = acc * J.U[m][idx[m] * J.R + r];
-                    W[threadIdx.x * J.R + r] = acc;
+#pragma unroll
+                for (int r = 0; r < RP4; ++r) {
+                    if (r < R) {
+                        double acc = J.U[J.N - 1][idx[J.N - 1] * R + r];
+                        for (int m = J.N - 2; m >= 1; --m) acc = acc * J.U[m][idx[m] * R + r];
+                        w[r] = acc;
+                    }
                 }
             }
+            if (tid < kGroup)
+#pragma unroll
+                for (int r = 0; r < RP4; ++r) W[tid * RP4 + r] = w[r];
         }
         __syncthreads();
-        for (int pass = 0; pass < 32 / kFitFibres; ++pass) {
-            const int jj = warp * 32 + pass * kFitFibres;
-            double acc[kFitFibres];
+      for (int pass = 0; pass < kPass; ++pass) {
+        double bf[kTW][KS], acc[kTW][2];
 #pragma unroll
-            for (int q = 0; q < kFitFibres; ++q) acc[q] = 0.0;
-            int nv = int(min64(kFitFibres, J.nfib - (j0 + jj)));
-            if (nv > 0) {
-                for (int64_t i1 = lane; i1 < J.I1; i1 += 32) {
-                    double x[kFitFibres], xh[kFitFibres];
+        for (int t = 0; t < kTW; ++t) {
+            const int fb = 8 * (warp + kFW * (t + kTW * pass));
 #pragma unroll
-                    for (int q = 0; q < kFitFibres; ++q) {
-                        x[q] = (q < nv) ? __ldcs(J.t + (j0 + jj + q) * J.I1 + i1) : 0.0;
-                        xh[q] = 0.0;
-                    }
-                    if (J.with_model) {
-                        const double* u = J.U[0] + i1 * J.R;
-                        for (int r = 0; r < J.R; ++r) {
-                            const double ur = __ldg(u + r);
+            for (int ks = 0; ks < KS; ++ks) bf[t][ks] = W[(fb + rr) * RP4 + 4 * ks + q];
+            acc[t][0] = acc[t][1] = 0.0;
+        }
+        const double* tg = J.t + j0 * I1;
+        // the row block's 32 tensor values per lane are loaded a block ahead (two register
+        // buffers, the loop unrolled by two), so every warp keeps 32 streaming loads in flight
+        double xa[4][kTW][2], xb[4][kTW][2];
+        auto load_x = [&](int64_t rb, double (&xv)[4][kTW][2]) {
 #pragma unroll
-                            for (int q = 0; q < kFitFibres; ++q)
-                                xh[q] = __fma_rn(ur, W[(jj + q) * J.R + r], xh[q]);
-                        }
+            for (int a = 0; a < 4; ++a) {
+                const int64_t i1 = rb * 32 + 8 * a + rr;
+                const bool rowok = rb < nrb && i1 < I1;
 #pragma unroll
-                        for (int q = 0; q < kFitFibres; ++q) {
-                            const double d = xh[q] - x[q];
-                            acc[q] = __fma_rn(d, d, acc[q]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < kFitFibres; ++q) acc[q] = __fma_rn(x[q], x[q], acc[q]);
-                    }
+                for (int t = 0; t < kTW; ++t) {
+                    const int f = 8 * (warp + kFW * (t + kTW * pass)) + 2 * q;
+                    xv[a][t][0] = (rowok && f < n) ? __ldcs(tg + int64_t(f) * I1 + i1) : 0.0;
+                    xv[a][t][1] = (rowok && f + 1 < n) ? __ldcs(tg + int64_t(f + 1) * I1 + i1) : 0.0;
                 }
             }
+        };
+        auto block = [&](int64_t rb, const double (&xv)[4][kTW][2]) {
 #pragma unroll
-            for (int q = 0; q < kFitFibres; ++q) {
-                const double f = butterfly32(acc[q]);
-                if (lane == 0) F[jj + q] = (q < nv) ? f : 0.0;
+            for (int a = 0; a < 4; ++a) {
+                const int64_t i1 = rb * 32 + 8 * a + rr;
+                const bool rowok = i1 < I1;
+                double af[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+                    af[ks] = (J.with_model && rowok && 4 * ks + q < R) ? __ldg(U1 + i1 * R + 4 * ks + q) : 0.0;
+#pragma unroll
+                for (int t = 0; t < kTW; ++t) {
+                    double c0 = 0.0, c1 = 0.0;
+                    if (J.with_model) {
+#pragma unroll
+                        for (int ks = 0; ks < KS; ++ks)
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                         : "+d"(c0), "+d"(c1)
+                                         : "d"(af[ks]), "d"(bf[t][ks]));
+                    }
+                    const double d0 = c0 - xv[a][t][0], d1 = c1 - xv[a][t][1];
+                    acc[t][0] = __fma_rn(d0, d0, acc[t][0]);
+                    acc[t][1] = __fma_rn(d1, d1, acc[t][1]);
+                }
             }
+        };
+        load_x(0, xa);
+        for (int64_t rb = 0; rb < nrb; rb += 2) {
+            load_x(rb + 1, xb);
+            block(rb, xa);
+            if (rb + 1 >= nrb) break;
+            load_x(rb + 2, xa);
+            block(rb + 1, xb);
         }
+#pragma unroll
+        for (int t = 0; t < kTW; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double v = acc[t][e];
+                v = v + __shfl_xor_sync(0xffffffffu, v, 4);
+                v = v + __shfl_xor_sync(0xffffffffu, v, 8);
+                v = v + __shfl_xor_sync(0xffffffffu, v, 16);
+                const int f = 8 * (warp + kFW * (t + kTW * pass)) + 2 * q + e;
+                if (rr == 0) F[f] = (f < n) ? v : 0.0;
+            }
+      }
         __syncthreads();
         if (warp == 0) {
-            const int n = int(min64(kGroup, J.nfib - j0));
             const double r = group_sum256_warp<false>(F, n, lane);
             if (lane == 0) J.group_partial[g] = r;
         }

@@ -518,9 +518,21 @@ void launch_fitness(rocp_dev* dev, const rocp_tensor* t, const std::vector<const
     j.group_tmp = dev->scratch_b.p;
     j.counter = dev->counters.p + 1;
     j.out = dev->scalars.p + slot;
-    const size_t smem = (size_t(kGroup) * j.R + kGroup) * sizeof(double);
-    const int grid = int(std::min<int64_t>(ngroups, int64_t(dev->num_sms) * 4));
-    k_fitness<<<grid, 256, smem, dev->stream>>>(j);
+    // k-steps of 4 over R (w and U1 are zero-padded past R); instances 1..5, 8, 13, 16
+    const int need = std::max(1, (j.R + 3) / 4);
+    const int ks = need <= 5 ? need : (need <= 8 ? 8 : (need <= 13 ? 13 : 16));
+    const size_t smem = (size_t(kGroup) * 4 * ks + kGroup) * sizeof(double);
+    const int grid = int(std::min<int64_t>(ngroups, int64_t(dev->num_sms)));
+    switch (ks) {
+        case 1: k_fitness<1><<<grid, 256, smem, dev->stream>>>(j); break;
+        case 2: k_fitness<2><<<grid, 256, smem, dev->stream>>>(j); break;
+        case 3: k_fitness<3><<<grid, 256, smem, dev->stream>>>(j); break;
+        case 4: k_fitness<4><<<grid, 256, smem, dev->stream>>>(j); break;
+        case 5: k_fitness<5><<<grid, 256, smem, dev->stream>>>(j); break;
+        case 8: k_fitness<8><<<grid, 256, smem, dev->stream>>>(j); break;
+        case 13: k_fitness<13><<<grid, 256, smem, dev->stream>>>(j); break;
+        default: k_fitness<16><<<grid, 256, smem, dev->stream>>>(j); break;
+    }
     after_launch(dev, "k_fitness");
 }
 
@@ -1512,8 +1524,12 @@ static rocp_status create_dev(int device, int world, int rank, const void* nccl_
         dev->flags.alloc(4);
         CK(cudaMemset(dev->flags.p, 0, 4 * sizeof(int)));
         dev->scalars.alloc(16);
-        CK(cudaFuncSetAttribute(k_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int((size_t(kGroup) * 64 + kGroup) * sizeof(double))));
+        {
+            const int fs = int((size_t(kGroup) * 64 + kGroup) * sizeof(double));
+            CK(cudaFuncSetAttribute(k_fitness<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs));
+            CK(cudaFuncSetAttribute(k_fitness<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs));
+            CK(cudaFuncSetAttribute(k_fitness<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs));
+        }
         set_contract_smem_attrs();
         if (world > 1 && !emulated) {
             const NcclApi& api = require_nccl();
