@@ -1089,6 +1089,11 @@ int gather_sms(rocp_stream* st, int64_t B) {
     // Two handles on one GPU: their cooperative chains and spinning gathers could hold
     // each other's SMs, whatever split was requested (explicit, env or model).
     if (handles_on(dev->device) > 1) return 0;
+    // Under MPS the process may not get every SM at once: the chain spins on the overlapped
+    // gather's arrivals, and only a private GPU guarantees that both grids are resident, so an
+    // MPS client gathers serially
+    static const bool mps = std::getenv("CUDA_MPS_PIPE_DIRECTORY") || std::getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE");
+    if (mps) return 0;
     if (g == -2) {
         double elems = double(B), rows_max = double(B);  // gathered elements per sample of one batch
         for (int64_t I : st->head) {
