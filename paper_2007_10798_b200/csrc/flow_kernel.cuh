@@ -38,7 +38,7 @@ namespace rocpk {
 //   [0] finished stages; [1 + st] tile sums of stage st; [1 + N + st] rows of
 //   stage st written; [1 + 2N + st * maxtiles + t] item arrivals of tile t.
 
-constexpr int kGinvSlot = 32 * 32;  // doubles per G^-1 slot (R <= 32)
+constexpr int kGinvSlot = 64 * 64;  // doubles per G^-1 slot (R <= 64)
 
 // One contraction item of k_flow on the fp64 tensor cores: rows [8 a0, 8 (a0 + AT)) of a
 // 32-row X_s tile against a superchunk of Z (warp w = chunk w), AT row tiles of 8 x NT column
@@ -104,11 +104,19 @@ __device__ __noinline__ void flow_contract_dmma(const double* xs, const double* 
     }
 }
 
-// MAXR = RP (R padded to a multiple of 8, <= 32): every loop over R is unrolled.
+// MAXR = RP (R padded to a multiple of 8, <= 64): every loop over R is unrolled.  R > 32
+// (the wide instances, C4): a lane owns columns lane and lane + 32, the factor lists hold at
+// most kMO factors (N <= 5), G^-1 is read from shared memory in the row dot products, the
+// items keep one superchunk's Z tile resident (each block takes one superchunk's tiles), and
+// the chunk Gram partials are pre-summed per superchunk by the superchunk's last chunk (the
+// finisher cannot hold them all).
 template <int MAXR, bool kTrace>
 __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) {
     extern __shared__ __align__(128) double sm[];
-    __shared__ unsigned short pairs[32 * 33 / 2];
+    constexpr bool kWideF = MAXR > 32;
+    constexpr int kCW = kWideF ? 2 : 1;               // columns per lane
+    constexpr int kMO = kWideF ? 4 : kMaxOrder - 1;   // factors per list
+    __shared__ unsigned short pairs[MAXR * (MAXR + 1) / 2];
     __shared__ __align__(8) uint64_t bar;
     __shared__ int s_last;
     constexpr int RP = MAXR;
@@ -120,20 +128,21 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     const int G = gridDim.x;
     const int nch = (S + kChunk - 1) / kChunk;
     const int NPp = (npairs + 1) & ~1;
+    const bool gram_one = int64_t(NPp) * nch <= kGramOneBlock;  // the finisher bulk-copies every chunk partial
     const int cblocks = G - 1;  // block G - 1 is the Gram finisher
     const bool is_fin = int(blockIdx.x) == G - 1;
     // chunk ch on block cblocks - 1 - ch (the host keeps at least 8 blocks without a chunk)
     const int ch = is_fin ? nch : cblocks - 1 - int(blockIdx.x);
     const bool chunk_block = ch >= 0 && ch < nch;
-    const bool lr = lane < R;
     unsigned* fin_ctr = p.fctr;
     unsigned* tsum_ctr = p.fctr + 1;
     unsigned* rows_ctr = p.fctr + 1 + N;
     unsigned* tile_ctr = p.fctr + 1 + 2 * N;
+    unsigned* gsum_ctr = p.fctr + 1 + 2 * N + N * p.maxtiles;  // superchunk Gram sums (!gram_one)
     double* xs = sm + kSmXs;
     double* zs = sm + kSmZs;
-    double* wsm = sm + kSmFact;         // per warp: the right-hand-side rows it turns into factor rows [8][4][32]
-    double* gsm = sm + kSmFact + 1024;  // G^-1 of the stage whose rows this block forms
+    double* wsm = sm + kSmFact;  // per warp: the right-hand-side rows it turns into factor rows [8][4][32 kCW]
+    double* gsm = sm + kSmFact + 1024 * kCW;  // G^-1 of the stage whose rows this block forms
     unsigned phase = 0;
     if (tid == 0) {
         int off = 0;
@@ -163,31 +172,37 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     auto publish = [&](unsigned* c, unsigned v) {  // after a block barrier, by one thread
         asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(c), "r"(v) : "memory");
     };
-    // column `lane` of the G^-1 of stage sp (symmetric: G^-1(k, lane) = slot[k R + lane])
     // G^-1 of stage sp into shared memory, once per block (a per-warp load of the same few
     // lines from L2 by every warp of every chunk block queues at the L2 slices); block-uniform,
-    // the caller synchronises before load_gcol
+    // the caller synchronises before use
     auto stage_ginv = [&](int sp) {
         const double* slot = p.ginv + (sp & 1) * kGinvSlot;
         for (int t = tid; t < RR; t += kChainThreads) gsm[t] = __ldcg(slot + t);
     };
+    // narrow: column `lane` of G^-1 in registers (symmetric: G^-1(k, lane) = gsm[k R + lane])
     auto load_gcol = [&](double* g) {
 #pragma unroll
-        for (int k = 0; k < MAXR; ++k) g[k] = (lr && k < R) ? gsm[k * R + lane] : 0.0;
+        for (int k = 0; k < MAXR; ++k) g[k] = (lane < R && k < R) ? gsm[k * R + lane] : 0.0;
     };
-    // u_lane = fma chain over k of w_k G^-1(k, lane) (oracle solve_gram_m), w in shared memory
-    auto row_dot = [&](const double* w, const double* g) {
+    // u_c = fma chain over k of w_k G^-1(k, c) (oracle solve_gram_m), w in shared memory;
+    // narrow: G^-1 column in registers (g), wide: from shared memory (column c)
+    auto row_dot = [&](const double* w, const double* g, int c) {
         double acc = 0.0;
+        if constexpr (!kWideF) {
 #pragma unroll
-        for (int k = 0; k < MAXR; ++k) {  // branch-free (w has MAXR readable entries)
-            const double v = __fma_rn(w[k], g[k], acc);
-            acc = (k < R) ? v : acc;
+            for (int k = 0; k < MAXR; ++k) {  // branch-free (w has MAXR readable entries)
+                const double v = __fma_rn(w[k], g[k], acc);
+                acc = (k < R) ? v : acc;
+            }
+        } else {  // a rolled loop: hoisting every load of an unrolled one spills
+#pragma unroll 4
+            for (int k = 0; k < R; ++k) acc = __fma_rn(w[k], gsm[k * R + c], acc);
         }
         return acc;
     };
 
     // idx of this warp's chunk samples (cc = warp + 8q), loaded a stage ahead
-    int32_t nidx[kSPW][kMaxOrder - 1];
+    int32_t nidx[kSPW][kMO];
     auto load_idx = [&](int b, int st) {
         if (b >= p.nb || !chunk_block) return;
         const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
@@ -195,7 +210,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
         for (int q = 0; q < kSPW; ++q) {
             const int c = ch * kChunk + warp + kW * q;
 #pragma unroll
-            for (int l = 0; l < kMaxOrder - 1; ++l)
+            for (int l = 0; l < kMO; ++l)
                 nidx[q][l] = (c < S && l < n_other) ? __ldg(idx + int64_t(c) * n_other + (n_other - 1 - l)) : 0;
         }
     };
@@ -209,25 +224,35 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
         const double* W = wrows_of(stp);
         double* out = out_of(bp, stp);
         const int md = __ldcg(p.gmode + ((bp * N + stp) & 1));
-        double g[MAXR];
-        load_gcol(g);  // gsm holds the G^-1 of (bp, stp)
-        double* wr = wsm + warp * (4 * 32);
+        double g[kWideF ? 1 : MAXR];
+        if constexpr (!kWideF) load_gcol(g);  // gsm holds the G^-1 of (bp, stp)
+        double* wr = wsm + warp * (4 * 32 * kCW);
         for (int row0 = gw; row0 < rows; row0 += 4 * nw_total) {
-            double w[4];
+            double w[4][kCW];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int row = row0 + q * nw_total;
-                w[q] = (lr && row < rows) ? __ldcg(W + int64_t(row) * R + lane) : 0.0;
+#pragma unroll
+                for (int cw = 0; cw < kCW; ++cw) {
+                    const int c = lane + 32 * cw;
+                    w[q][cw] = (c < R && row < rows) ? __ldcg(W + int64_t(row) * R + c) : 0.0;
+                }
             }
             __syncwarp();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) wr[q * 32 + lane] = w[q];
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int cw = 0; cw < kCW; ++cw) wr[q * 32 * kCW + lane + 32 * cw] = w[q][cw];
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int row = row0 + q * nw_total;
-                const double u = row_dot(wr + q * 32, g);
-                if (lr && row < rows) out[int64_t(row) * R + lane] = md ? u : 0.0;
+#pragma unroll
+                for (int cw = 0; cw < kCW; ++cw) {
+                    const int c = lane + 32 * cw;
+                    const double u = row_dot(wr + q * 32 * kCW, g, c);
+                    if (c < R && row < rows) out[int64_t(row) * R + c] = md ? u : 0.0;
+                }
             }
         }
     };
@@ -245,15 +270,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
             unsigned long long* tr = (kTrace && p.trace) ? p.trace + int64_t(sg) * kTraceSlots : nullptr;
 
             if (!is_fin) {
-                const int first_item = int(blockIdx.x);
                 if (chunk_block) {
-                    // ------------- Z chunk (sampling.cpp:90-103), warp per sample, lane = r; the
-                    // sampled rows of the factor solved by stage sg - 1 (list position lod) are
-                    // formed here from its summed right-hand sides and G^-1
-                    const double* F[kMaxOrder - 1];
+                    // ------------- Z chunk (sampling.cpp:90-103), warp per sample, lane = r (and
+                    // r + 32); the sampled rows of the factor solved by stage sg - 1 (list
+                    // position lod) are formed here from its summed right-hand sides and G^-1
+                    const double* F[kMO];
                     int lod = -1;
 #pragma unroll
-                    for (int l = 0; l < kMaxOrder - 1; ++l) {
+                    for (int l = 0; l < kMO; ++l) {
                         F[l] = nullptr;
                         if (l < n_other) {
                             const int md = mode_at(st, l);
@@ -267,102 +291,159 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         __syncthreads();
                     }
                     const int c0 = ch * kChunk, cn = min(kChunk, S - c0);
-                    double f[kSPW][kMaxOrder - 1];
+                    double f[kSPW][kMO][kCW];
 #pragma unroll
-                    for (int q = 0; q < kSPW; ++q) {
-                        const bool live = warp + kW * q < cn && lr;
+                    for (int q = 0; q < kSPW; ++q)
 #pragma unroll
-                        for (int l = 0; l < kMaxOrder - 1; ++l)
-                            f[q][l] = (live && l < n_other && l != lod) ? __ldcg(F[l] + int64_t(nidx[q][l]) * R + lane) : 1.0;
-                    }
+                        for (int cw = 0; cw < kCW; ++cw) {
+                            const int c = lane + 32 * cw;
+                            const bool live = warp + kW * q < cn && c < R;
+#pragma unroll
+                            for (int l = 0; l < kMO; ++l)
+                                f[q][l][cw] = (live && l < n_other && l != lod) ? __ldcg(F[l] + int64_t(nidx[q][l]) * R + c) : 1.0;
+                        }
                     if (sg >= 1) {
                         wait_ge(fin_ctr, unsigned(sg));
                         wait_ge(tsum_ctr + st1, unsigned(b1 + 1) * unsigned(tiles_of(st1)));
                         __syncthreads();
                         if (tr) trace_stamp(tr, 0, ch == 0 && tid == 0);
                         const double* W = wrows_of(st1);
-                        double wq[kSPW];
+                        double wq[kSPW][kCW];
 #pragma unroll
                         for (int q = 0; q < kSPW; ++q) {
                             int32_t iw = 0;
 #pragma unroll
-                            for (int l = 0; l < kMaxOrder - 1; ++l)
+                            for (int l = 0; l < kMO; ++l)
                                 if (l == lod) iw = nidx[q][l];
-                            const bool live = warp + kW * q < cn && lr;
-                            wq[q] = live ? __ldcg(W + int64_t(iw) * R + lane) : 0.0;
+#pragma unroll
+                            for (int cw = 0; cw < kCW; ++cw) {
+                                const int c = lane + 32 * cw;
+                                const bool live = warp + kW * q < cn && c < R;
+                                wq[q][cw] = live ? __ldcg(W + int64_t(iw) * R + c) : 0.0;
+                            }
                         }
                         const int md = __ldcg(p.gmode + ((sg - 1) & 1));
                         stage_ginv(sg - 1);
                         __syncthreads();
-                        double g[MAXR];
-                        load_gcol(g);
+                        double g[kWideF ? 1 : MAXR];
+                        if constexpr (!kWideF) load_gcol(g);
 #pragma unroll
-                        for (int q = 0; q < kSPW; ++q) wsm[(warp * kSPW + q) * 32 + lane] = wq[q];
+                        for (int q = 0; q < kSPW; ++q)
+#pragma unroll
+                            for (int cw = 0; cw < kCW; ++cw) wsm[(warp * kSPW + q) * 32 * kCW + lane + 32 * cw] = wq[q][cw];
                         __syncwarp();
 #pragma unroll
-                        for (int q = 0; q < kSPW; ++q) {
-                            const double u = row_dot(wsm + (warp * kSPW + q) * 32, g);
+                        for (int q = 0; q < kSPW; ++q)
 #pragma unroll
-                            for (int l = 0; l < kMaxOrder - 1; ++l)
-                                if (l == lod) f[q][l] = md ? u : 0.0;
-                        }
+                            for (int cw = 0; cw < kCW; ++cw) {
+                                const double u = row_dot(wsm + (warp * kSPW + q) * 32 * kCW, g, lane + 32 * cw);
+#pragma unroll
+                                for (int l = 0; l < kMO; ++l)
+                                    if (l == lod) f[q][l][cw] = md ? u : 0.0;
+                            }
                         if (tr) trace_stamp(tr, 12, ch == 0 && tid == 0);
                     }
                     double* zc = zs;  // [32][RP]
 #pragma unroll
                     for (int q = 0; q < kSPW; ++q) {
                         const int cc = warp + kW * q;
-                        if (lane < RP) {
-                            double z = 0.0;
-                            if (cc < cn && lr) {
-                                z = 1.0;
 #pragma unroll
-                                for (int l = 0; l < kMaxOrder - 1; ++l)
-                                    if (l < n_other) z = z * f[q][l];
+                        for (int cw = 0; cw < kCW; ++cw) {
+                            const int c = lane + 32 * cw;
+                            if (c < RP) {
+                                double z = 0.0;
+                                if (cc < cn && c < R) {
+                                    z = 1.0;
+#pragma unroll
+                                    for (int l = 0; l < kMO; ++l)
+                                        if (l < n_other) z = z * f[q][l][cw];
+                                }
+                                zc[cc * RP + c] = z;
+                                if (cc < cn) Z[int64_t(c0 + cc) * RP + c] = z;
                             }
-                            zc[cc * RP + lane] = z;
-                            if (cc < cn) Z[int64_t(c0 + cc) * RP + lane] = z;
                         }
                     }
                     __syncthreads();
                     if (tr) trace_stamp(tr, 14, ch == 0 && tid == 0);
                     chain_chunk_gram_dmma(zc, RP, R, p.chpart + int64_t(ch) * NPp);
                     __syncthreads();
+                    const int msup = ch / kSuper;
                     if (tid == 0) {  // one release fence for both counters
                         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.zctr + 1 + ch / kSuper) : "memory");
+                        if (gram_one) {
+                            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.zctr + 1 + msup) : "memory");
+                        } else {  // the superchunk's last chunk pre-sums its Gram partials
+                            unsigned prev;
+                            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.zctr + 1 + msup) : "memory");
+                            const unsigned nck = unsigned(min(kSuper, nch - msup * kSuper));
+                            s_last = (prev + 1 == unsigned(sg + 1) * nck) ? 1 : 0;
+                        }
                         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.zctr) : "memory");
+                    }
+                    if (!gram_one) {
+                        __syncthreads();
+                        if (s_last) {  // superchunk sum of the chunk partials, chunks in order (k_chain's)
+                            const int k0 = msup * kSuper, k1 = min(nch, k0 + kSuper);
+                            for (int pp = tid; pp < npairs; pp += kChainThreads) {
+                                double v = __ldcg(p.chpart + int64_t(k0) * NPp + pp);
+                                for (int k = k0 + 1; k < k1; ++k) v = v + __ldcg(p.chpart + int64_t(k) * NPp + pp);
+                                p.gpart[int64_t(msup) * NPp + pp] = v;
+                            }
+                            __syncthreads();
+                            if (tid == 0) publish(gsum_ctr, 1u);
+                        }
                     }
                     if (tr) trace_stamp(tr, 1, ch == 0 && tid == 0);
                     const int nb2 = (st + 1 < N) ? b : b + 1, ns2 = (st + 1 < N) ? st + 1 : 0;
                     load_idx(nb2, ns2);
-                    if (sg >= 1) {
-                        // ------------- every row of stage sg - 1, off the critical path: the chunk
-                        // blocks are idle until the next stage (its chunks need these rows only
-                        // two stages on, rows_ctr)
-                        const int nwt = nch * kW;
-                        materialise(b1, st1, ch + warp * nch, nwt);
-                        __syncthreads();
-                        if (tid == 0) {
-                            const int rows1 = rows_of(st1);
-                            unsigned n = 0;
-                            for (int w = 0; w < kW; ++w) {
-                                const int g0 = ch + w * nch;
-                                if (g0 < rows1) n += unsigned((rows1 - 1 - g0) / nwt + 1);
-                            }
-                            if (n) publish(rows_ctr + st1, n);
-                            if (tr && ch == 0) tr[5] = gtimer();
-                        }
-                    }
                 }
+                // ------------- every row of stage sg - 1, off the critical path, by the chunk
+                // blocks (the next stage's chunks need these rows only two stages on, rows_ctr):
+                // narrow right after their chunk (they are idle until the next stage), wide
+                // after their contraction items (every block has items there)
+                auto materialise_prev = [&]() {
+                    if (!chunk_block || sg < 1) return;
+                    const int nwt = nch * kW;
+                    materialise(b1, st1, ch + warp * nch, nwt);
+                    __syncthreads();
+                    if (tid == 0) {
+                        const int rows1 = rows_of(st1);
+                        unsigned n = 0;
+                        for (int w = 0; w < kW; ++w) {
+                            const int g0 = ch + w * nch;
+                            if (g0 < rows1) n += unsigned((rows1 - 1 - g0) / nwt + 1);
+                        }
+                        if (n) publish(rows_ctr + st1, n);
+                        if (tr && ch == 0) tr[5] = gtimer();
+                    }
+                };
+                if constexpr (!kWideF) materialise_prev();
 
-                // ------------- contraction items (tile, superchunk[, row part]), stride cblocks; a
-                // stage with few items splits each tile's rows over F = 2 or 4 blocks
+                // ------------- contraction items (tile, superchunk[, row part]); a stage with few
+                // items splits each tile's rows over F = 2 or 4 blocks.  Narrow: item i on block
+                // i mod cblocks.  Wide: block c takes superchunk c mod nsuper and every
+                // (cblocks / nsuper)-th tile of it, so its Z tile (up to 128 KB) loads once.
                 const int F = (4 * n_contract <= cblocks) ? 4 : ((2 * n_contract <= cblocks) ? 2 : 1);
+                const bool zr = kWideF && F == 1 && cblocks >= nsuper;
+                const int cix = int(blockIdx.x);
+                const int zm = cix % nsuper, zrank = cix / nsuper, zcnt = (cblocks - zm + nsuper - 1) / nsuper;
                 int zm_cur = -1;
-                for (int item = first_item; item < F * n_contract; item += cblocks) {
-                    const int part = item % F, base = item / F;
-                    const int tile = base % tiles, m = base / tiles;
+                for (int it = 0;; ++it) {
+                    int tile, m, part;
+                    if (zr) {
+                        const int t = zrank + it * zcnt;
+                        if (t >= tiles) break;
+                        tile = t;
+                        m = zm;
+                        part = 0;
+                    } else {
+                        const int item = cix + it * cblocks;
+                        if (item >= F * n_contract) break;
+                        part = item % F;
+                        const int base = item / F;
+                        tile = base % tiles;
+                        m = base / tiles;
+                    }
                     const int c0 = m * kSuperSamples, cn = min(kSuperSamples, S - c0);
                     const int i0 = tile * kRowTile, nrows = min(kRowTile, rows - i0);
                     if (tid == 0) {  // X_s tile (from the overlapped gather when it runs) and Z tile
@@ -370,7 +451,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                             wait_gathered(p.gdone + b * N + st, __ldg(p.gneed + b * N + st), 0u);
                             asm volatile("fence.proxy.async.global;" ::: "memory");
                         }
-                        if (tr && blockIdx.x == 0 && item == first_item) tr[7] = gtimer();
+                        if (tr && blockIdx.x == 0 && it == 0) tr[7] = gtimer();
                         fence_proxy_async();
                         tma_load_1d_once(xs, X + (int64_t(tile) * S + c0) * kRowTile, unsigned(cn * kRowTile * 8), &bar);
                         const bool zload = m != zm_cur;
@@ -385,7 +466,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     zm_cur = m;
                     mbar_wait(&bar, phase);
                     phase ^= 1u;
-                    if (tr) trace_stamp(tr, 8, blockIdx.x == 0 && tid == 0 && item == first_item);
+                    if (tr) trace_stamp(tr, 8, blockIdx.x == 0 && tid == 0 && it == 0);
                     const int nk = (cn + kChunk - 1) / kChunk;
                     const int cc0 = warp * kChunk;
                     const int cn0 = max(min(kChunk, cn - cc0), 0);
@@ -417,7 +498,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                             if (tr) tr[6] = gtimer();  // the last tile sum of the stage overwrites
                         }
                     }
-                    if (tr) trace_stamp(tr, 9, blockIdx.x == 0 && tid == 0 && item == first_item);
+                    if (tr) trace_stamp(tr, 9, blockIdx.x == 0 && tid == 0 && it == 0);
+                }
+                if constexpr (kWideF) {  // the G^-1 in shared memory was overwritten by Z tiles
+                    if (chunk_block && sg >= 1) {
+                        stage_ginv(sg - 1);
+                        __syncthreads();
+                    }
+                    materialise_prev();
                 }
             } else {
                 // ------------- the Gram finisher
@@ -436,32 +524,43 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         qb[u] = __ldcg(p.Q[st - 1] + j + i * R);
                     }
                 }
-                if (tid == 0) {  // every chunk partial of this stage published
-                    wait_gathered(p.zctr, unsigned(sg + 1) * unsigned(nch), 0u, 0u);
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    const unsigned bytes = unsigned(nch * NPp * 8);
-                    fence_proxy_async();
-                    tma_load_1d(sm, p.chpart, bytes, &bar);
-                    mbar_expect_tx(&bar, bytes);
+                if (gram_one) {
+                    if (tid == 0) {  // every chunk partial of this stage published
+                        wait_gathered(p.zctr, unsigned(sg + 1) * unsigned(nch), 0u, 0u);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        const unsigned bytes = unsigned(nch * NPp * 8);
+                        fence_proxy_async();
+                        tma_load_1d(sm, p.chpart, bytes, &bar);
+                        mbar_expect_tx(&bar, bytes);
+                    }
+                    if (tr) trace_stamp(tr, 3, tid == 0);
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                } else {  // every superchunk's Gram sum published
+                    wait_ge(gsum_ctr, unsigned(sg + 1) * unsigned(nsuper));
+                    __syncthreads();
+                    if (tr) trace_stamp(tr, 3, tid == 0);
                 }
-                if (tr) trace_stamp(tr, 3, tid == 0);
-                mbar_wait(&bar, phase);
-                phase ^= 1u;
 #pragma unroll
                 for (int u = 0; u < kMaxPairsPerThread; ++u) {
                     const int q = tid + u * kChainThreads;
                     if (q >= npairs) break;
                     double tot = 0.0;
-                    for (int m = 0; m < nsuper; ++m) {
-                        const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
-                        double v[kSuper];
+                    if (gram_one) {
+                        for (int m = 0; m < nsuper; ++m) {
+                            const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
+                            double v[kSuper];
 #pragma unroll
-                        for (int k = 0; k < kSuper; ++k) v[k] = (k0 + k < k1) ? sm[(k0 + k) * NPp + q] : 0.0;
-                        double sq = v[0];
+                            for (int k = 0; k < kSuper; ++k) v[k] = (k0 + k < k1) ? sm[(k0 + k) * NPp + q] : 0.0;
+                            double sq = v[0];
 #pragma unroll
-                        for (int k = 1; k < kSuper; ++k)
-                            if (k0 + k < k1) sq = sq + v[k];
-                        tot = (m == 0) ? sq : tot + sq;
+                            for (int k = 1; k < kSuper; ++k)
+                                if (k0 + k < k1) sq = sq + v[k];
+                            tot = (m == 0) ? sq : tot + sq;
+                        }
+                    } else {  // the superchunk sums in order
+                        tot = __ldcg(p.gpart + q);
+                        for (int m = 1; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
                     }
                     const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
                     double ga = tot, gb = tot;
@@ -480,9 +579,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                 if (tr) trace_stamp(tr, 10, tid == 0);
                 // solve_gram (solve.cpp:9-35) in canonical form (kernels.cuh gram_solve_block)
                 int2 mr;
-                if (npairs <= 224) mr = gram_solve_block<1>(Gs, R, pairs, gi, colb, sm, true);
-                else if (npairs <= 448) mr = gram_solve_block<2>(Gs, R, pairs, gi, colb, sm, true);
-                else mr = gram_solve_block<3>(Gs, R, pairs, gi, colb, sm, true);
+                if constexpr (!kWideF) {
+                    if (npairs <= 224) mr = gram_solve_block<1>(Gs, R, pairs, gi, colb, sm, true);
+                    else if (npairs <= 448) mr = gram_solve_block<2>(Gs, R, pairs, gi, colb, sm, true);
+                    else mr = gram_solve_block<3>(Gs, R, pairs, gi, colb, sm, true);
+                } else {
+                    if (npairs <= 1344) mr = gram_solve_block<6>(Gs, R, pairs, gi, colb, sm, true);
+                    else mr = gram_solve_block<10>(Gs, R, pairs, gi, colb, sm, true);
+                }
                 if (tr) trace_stamp(tr, 11, tid == 0);
                 double* slot = p.ginv + (sg & 1) * kGinvSlot;
                 for (int t = tid; t < RR; t += kChainThreads) slot[t] = gi[t];

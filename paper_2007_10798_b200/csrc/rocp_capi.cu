@@ -1076,10 +1076,18 @@ int gather_sms(rocp_stream* st, int64_t B) {
         CK(cudaFuncGetAttributes(&fa, k_flow<16, false>));
         CK(cudaFuncGetAttributes(&fa, k_flow<24, false>));
         CK(cudaFuncGetAttributes(&fa, k_flow<32, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<40, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<48, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<56, false>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<64, false>));
         CK(cudaFuncGetAttributes(&fa, k_flow<8, true>));
         CK(cudaFuncGetAttributes(&fa, k_flow<16, true>));
         CK(cudaFuncGetAttributes(&fa, k_flow<24, true>));
         CK(cudaFuncGetAttributes(&fa, k_flow<32, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<40, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<48, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<56, true>));
+        CK(cudaFuncGetAttributes(&fa, k_flow<64, true>));
         CK(cudaFuncGetAttributes(&fa, k_gather_warps));
         CK(cudaStreamCreateWithFlags(&dev->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&dev->ev_gready, cudaEventDisableTiming));
@@ -1294,18 +1302,22 @@ void launch_coop(rocp_stream* st, const void* fn, const char* name, const ChainP
     after_launch(dev, name);
 }
 
-// k_flow (flow_kernel.cuh) serves R <= 32 when one finisher block holds every chunk
-// Gram partial and at least 8 blocks are left to write rows; k_chain otherwise (and
-// when ROCP_CHAIN=barrier asks for the grid-barrier kernel).
+// k_flow (flow_kernel.cuh) serves R <= 32 when at least 8 blocks are left without a chunk;
+// k_chain otherwise (and when ROCP_CHAIN=barrier asks for the grid-barrier kernel).  The wide
+// k_flow instances (R in 33..64, N <= 5) are bit-identical but slower on C4 than k_chain
+// (95k vs 147k slices/s): ROCP_CHAIN=flow selects them.
 bool use_flow(const rocp_stream* st, int grid) {
-    static const bool barrier_env = [] {
+    static const int chain_env = [] {
         const char* e = std::getenv("ROCP_CHAIN");
-        return e && std::string(e) == "barrier";
+        if (!e) return 0;
+        if (std::string(e) == "barrier") return 1;
+        if (std::string(e) == "flow") return 2;
+        return 0;
     }();
-    if (barrier_env || st->R > 32) return false;
+    if (chain_env == 1 || st->R > 64 || (st->R > 32 && st->N > 5)) return false;
+    if (st->R > 32 && chain_env != 2) return false;
     const int64_t nch = (st->s + kChunk - 1) / kChunk;
-    const int64_t NPp = ((int64_t(st->R) * (st->R + 1) / 2) + 1) & ~int64_t(1);
-    return NPp * nch <= kGramOneBlock && grid - 1 - nch >= 8;
+    return grid - 1 - nch >= 8;
 }
 
 // grid: one persistent block per SM, less the SMs of an overlapped gather
@@ -1314,10 +1326,18 @@ void launch_chain_k(rocp_stream* st, const ChainParams& p, int grid, bool flow) 
     if (flow) {
         const int rp = ((p.R + kCRB - 1) / kCRB) * kCRB;
         const void* fn = nullptr;
-        if (rp == 8) fn = trace ? reinterpret_cast<const void*>(k_flow<8, true>) : reinterpret_cast<const void*>(k_flow<8, false>);
-        else if (rp == 16) fn = trace ? reinterpret_cast<const void*>(k_flow<16, true>) : reinterpret_cast<const void*>(k_flow<16, false>);
-        else if (rp == 24) fn = trace ? reinterpret_cast<const void*>(k_flow<24, true>) : reinterpret_cast<const void*>(k_flow<24, false>);
-        else fn = trace ? reinterpret_cast<const void*>(k_flow<32, true>) : reinterpret_cast<const void*>(k_flow<32, false>);
+#define ROCP_FLOW_FN(RPV) (trace ? reinterpret_cast<const void*>(k_flow<RPV, true>) : reinterpret_cast<const void*>(k_flow<RPV, false>))
+        switch (rp) {
+            case 8: fn = ROCP_FLOW_FN(8); break;
+            case 16: fn = ROCP_FLOW_FN(16); break;
+            case 24: fn = ROCP_FLOW_FN(24); break;
+            case 32: fn = ROCP_FLOW_FN(32); break;
+            case 40: fn = ROCP_FLOW_FN(40); break;
+            case 48: fn = ROCP_FLOW_FN(48); break;
+            case 56: fn = ROCP_FLOW_FN(56); break;
+            default: fn = ROCP_FLOW_FN(64); break;
+        }
+#undef ROCP_FLOW_FN
         launch_coop(st, fn, "k_flow", p, grid);
     } else if (wide) {
         if (trace) launch_coop(st, reinterpret_cast<const void*>(k_chain<true, true>), "k_chain", p, grid);
@@ -1378,7 +1398,7 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
     if (flow) {
         int maxtiles = int((B + kRowTile - 1) / kRowTile);
         for (int64_t I : st->head) maxtiles = std::max(maxtiles, int((I + kRowTile - 1) / kRowTile));
-        const size_t nctr = size_t(1 + 2 * st->N + st->N * maxtiles);
+        const size_t nctr = size_t(1 + 2 * st->N + st->N * maxtiles + 1);
         st->fctr.ensure(nctr);
         st->ginv.ensure(size_t(2 * kGinvSlot));
         st->gmode.ensure(2);

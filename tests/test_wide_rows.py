@@ -1,9 +1,9 @@
-"""Rows of solve_gram for R > 32: u = b G^-1 against the explicit
-inverse (formed once per solve from the LDL^T factors) instead of a 2R-step
-substitution per row.  The canonical order changed for wide ranks, so this pins
-it against independent solves: the reference's solve_gram is an LDLT solve
-(solve.cpp:34), and the sampled-LS properties of test_cprand.cpp:25-57 must hold
-at wide ranks with the same tolerances."""
+"""Rows of solve_gram: u = b G^-1 against the explicit inverse that the
+symmetric sweep forms, instead of an LDL^T factorisation and a 2R-step substitution per
+row.  The canonical order differs from the reference's, so this pins it against
+independent solves at wide ranks: the reference's solve_gram is an LDLT solve
+(solve.cpp:34), and the sampled-LS properties of test_cprand.cpp:25-57 must hold with the
+same tolerances."""
 import json
 import os
 

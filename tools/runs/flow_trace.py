@@ -10,7 +10,8 @@ sys.path.insert(0, ROOT)
 import paper_2007_10798_b200 as rocp  # noqa: E402
 
 CFG = {"c1": ([200, 200, 500], 10, 50, 10), "c2": ([1000, 1000, 1000], 20, 100, 25),
-       "c3": ([200, 200, 200, 200], 10, 20, 10), "c5": ([60, 60, 60, 60, 300], 16, 10, 10)}
+       "c3": ([200, 200, 200, 200], 10, 20, 10), "c5": ([60, 60, 60, 60, 300], 16, 10, 10),
+       "c4": ([4000, 4000, 500], 50, 50, 50)}
 dims, R, t_init, B = CFG[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 S = max(R, int(np.ceil(10 * R * np.log(R))))
 g = np.random.default_rng(0)
