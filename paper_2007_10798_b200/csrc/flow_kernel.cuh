@@ -189,11 +189,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
     auto row_dot = [&](const double* w, const double* g, int c) {
         double acc = 0.0;
         if constexpr (!kWideF) {
+            // w and g are zero past R, and fma(+0, +0, acc) = acc (acc is never -0 here), so the
+            // padded steps change nothing: no select on the chain
 #pragma unroll
-            for (int k = 0; k < MAXR; ++k) {  // branch-free (w has MAXR readable entries)
-                const double v = __fma_rn(w[k], g[k], acc);
-                acc = (k < R) ? v : acc;
-            }
+            for (int k = 0; k < MAXR; ++k) acc = __fma_rn(w[k], g[k], acc);
         } else {  // a rolled loop: hoisting every load of an unrolled one spills
 #pragma unroll 4
             for (int k = 0; k < R; ++k) acc = __fma_rn(w[k], gsm[k * R + c], acc);
@@ -325,6 +324,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         const int md = __ldcg(p.gmode + ((sg - 1) & 1));
                         stage_ginv(sg - 1);
                         __syncthreads();
+                        if (tr) trace_stamp(tr, 15, ch == 0 && tid == 0);
                         double g[kWideF ? 1 : MAXR];
                         if constexpr (!kWideF) load_gcol(g);
 #pragma unroll
@@ -332,14 +332,30 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
 #pragma unroll
                             for (int cw = 0; cw < kCW; ++cw) wsm[(warp * kSPW + q) * 32 * kCW + lane + 32 * cw] = wq[q][cw];
                         __syncwarp();
+                        if (tr) trace_stamp(tr, 16, ch == 0 && tid == 0);
+                        double uq[kSPW][kCW];
+                        if constexpr (!kWideF) {  // the four samples' chains interleaved
+                            const double* wb = wsm + warp * kSPW * 32;
+#pragma unroll
+                            for (int q = 0; q < kSPW; ++q) uq[q][0] = 0.0;
+#pragma unroll
+                            for (int k = 0; k < MAXR; ++k)
+#pragma unroll
+                                for (int q = 0; q < kSPW; ++q) uq[q][0] = __fma_rn(wb[q * 32 + k], g[k], uq[q][0]);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < kSPW; ++q)
+#pragma unroll
+                                for (int cw = 0; cw < kCW; ++cw)
+                                    uq[q][cw] = row_dot(wsm + (warp * kSPW + q) * 32 * kCW, g, lane + 32 * cw);
+                        }
 #pragma unroll
                         for (int q = 0; q < kSPW; ++q)
 #pragma unroll
                             for (int cw = 0; cw < kCW; ++cw) {
-                                const double u = row_dot(wsm + (warp * kSPW + q) * 32 * kCW, g, lane + 32 * cw);
 #pragma unroll
                                 for (int l = 0; l < kMO; ++l)
-                                    if (l == lod) f[q][l][cw] = md ? u : 0.0;
+                                    if (l == lod) f[q][l][cw] = md ? uq[q][cw] : 0.0;
                             }
                         if (tr) trace_stamp(tr, 12, ch == 0 && tid == 0);
                     }

@@ -47,7 +47,7 @@ print(f"gather SMs {st.last_gather_sms}")
 for stg in range(N):
     t = tr[stg::N]
     p0 = prev[stg::N]
-    print(f"stage {stg}: chunk start={med(t[:,0]-p0):.2f} chunk pub={med(t[:,1]-t[:,0]):.2f} (od={med(t[:,12]-t[:,0]):.2f} z={med(t[:,14]-t[:,12]):.2f}) | "
+    print(f"stage {stg}: chunk start={med(t[:,0]-p0):.2f} chunk pub={med(t[:,1]-t[:,0]):.2f} (od={med(t[:,12]-t[:,0]):.2f} [ginv staged {med(t[:,15]-t[:,0]):.2f} w in {med(t[:,16]-t[:,0]):.2f}] z={med(t[:,14]-t[:,12]):.2f}) | "
           f"fin wait done={med(t[:,3]-t[:,1]):.2f} combine={med(t[:,10]-t[:,3]):.2f} solve={med(t[:,11]-t[:,10]):.2f} publish={med(t[:,4]-t[:,11]):.2f} | stage={med(t[:,4]-p0):.2f} | "
           f"mat0 done={med(t[:,5]-p0):.2f} item0 gather ok={med(t[:,7]-p0):.2f} item0 start={med(t[:,8]-p0):.2f} "
           f"computed={med(t[:,19]-p0):.2f} end={med(t[:,9]-p0):.2f} last tsum={med(t[:,6]-p0):.2f} us")
