@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     if (F == 1) flow_contract_dmma<MAXR / 8, 4>(xs, zs, xs, cc0, cn0, nk, 0, nrows, R, orow);
                     else if (F == 2) flow_contract_dmma<MAXR / 8, 2>(xs, zs, xs, cc0, cn0, nk, 2 * part, nrows, R, orow);
                     else flow_contract_dmma<MAXR / 8, 1>(xs, zs, xs, cc0, cn0, nk, part, nrows, R, orow);
+                    if (tr) trace_stamp(tr, 19, blockIdx.x == 0 && tid == 0 && it == 0);
                     // the tile's last item sums its superchunk partials (rocp.cpp:107: P += X_s Z)
                     if (tid == 0) {
                         unsigned prev;
@@ -501,12 +502,34 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                     }
                     __syncthreads();
                     if (s_last) {
+                        // every load of the thread's entries issued before the sums (a load-add
+                        // chain per superchunk took ~3 us of L2 round trips)
                         double* W = wrows_of(st);
-                        for (int e = tid; e < nrows * R; e += kChainThreads) {
+                        constexpr int kTE = (32 * MAXR + kChainThreads - 1) / kChainThreads;  // entries per thread
+                        constexpr int kTU = 4;  // superchunk partials loaded up front
+                        double cv[kTE][kTU], pv[kTE];
+#pragma unroll
+                        for (int u = 0; u < kTE; ++u) {
+                            const int e = tid + u * kChainThreads;
+                            const bool ok = e < nrows * R;
                             const int64_t o = int64_t(i0) * R + e;
-                            double tot = __ldcg(p.cpart + o);
-                            for (int mm = 1; mm < nsuper; ++mm) tot = tot + __ldcg(p.cpart + int64_t(mm) * rows * R + o);
-                            W[o] = (st > 0) ? __ldcg(W + o) + tot : tot;
+#pragma unroll
+                            for (int mm = 0; mm < kTU; ++mm)
+                                cv[u][mm] = (ok && mm < nsuper) ? __ldcg(p.cpart + int64_t(mm) * rows * R + o) : 0.0;
+                            pv[u] = (ok && st > 0) ? __ldcg(W + o) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < kTE; ++u) {
+                            const int e = tid + u * kChainThreads;
+                            if (e < nrows * R) {
+                                const int64_t o = int64_t(i0) * R + e;
+                                double tot = cv[u][0];
+#pragma unroll
+                                for (int mm = 1; mm < kTU; ++mm)
+                                    if (mm < nsuper) tot = tot + cv[u][mm];
+                                for (int mm = kTU; mm < nsuper; ++mm) tot = tot + __ldcg(p.cpart + int64_t(mm) * rows * R + o);
+                                W[o] = (st > 0) ? pv[u] + tot : tot;
+                            }
                         }
                         __syncthreads();
                         if (tid == 0) {
