@@ -401,8 +401,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         if (s_last) {  // superchunk sum of the chunk partials, chunks in order (k_chain's)
                             const int k0 = msup * kSuper, k1 = min(nch, k0 + kSuper);
                             for (int pp = tid; pp < npairs; pp += kChainThreads) {
-                                double v = __ldcg(p.chpart + int64_t(k0) * NPp + pp);
-                                for (int k = k0 + 1; k < k1; ++k) v = v + __ldcg(p.chpart + int64_t(k) * NPp + pp);
+                                double cv[kSuper];  // every load before the sums
+#pragma unroll
+                                for (int k = 0; k < kSuper; ++k)
+                                    cv[k] = (k0 + k < k1) ? __ldcg(p.chpart + int64_t(k0 + k) * NPp + pp) : 0.0;
+                                double v = cv[0];
+#pragma unroll
+                                for (int k = 1; k < kSuper; ++k)
+                                    if (k0 + k < k1) v = v + cv[k];
                                 p.gpart[int64_t(msup) * NPp + pp] = v;
                             }
                             __syncthreads();
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         // chain per superchunk took ~3 us of L2 round trips)
                         double* W = wrows_of(st);
                         constexpr int kTE = (32 * MAXR + kChainThreads - 1) / kChainThreads;  // entries per thread
-                        constexpr int kTU = 4;  // superchunk partials loaded up front
+                        constexpr int kTU = kWideF ? 8 : 4;  // superchunk partials loaded up front
                         double cv[kTE][kTU], pv[kTE];
 #pragma unroll
                         for (int u = 0; u < kTE; ++u) {
@@ -597,9 +603,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                                 if (k0 + k < k1) sq = sq + v[k];
                             tot = (m == 0) ? sq : tot + sq;
                         }
-                    } else {  // the superchunk sums in order
-                        tot = __ldcg(p.gpart + q);
-                        for (int m = 1; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
+                    } else {  // the superchunk sums in order, every load first
+                        double gv[kSuper];
+#pragma unroll
+                        for (int m = 0; m < kSuper; ++m) gv[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * NPp + q) : 0.0;
+                        tot = gv[0];
+#pragma unroll
+                        for (int m = 1; m < kSuper; ++m)
+                            if (m < nsuper) tot = tot + gv[m];
+                        for (int m = kSuper; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
                     }
                     const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
                     double ga = tot, gb = tot;
