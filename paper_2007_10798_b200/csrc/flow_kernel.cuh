@@ -334,14 +334,39 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_flow(const ChainParams p) 
                         __syncwarp();
                         if (tr) trace_stamp(tr, 16, ch == 0 && tid == 0);
                         double uq[kSPW][kCW];
-                        if constexpr (!kWideF) {  // the four samples' chains interleaved
+                        if constexpr (!kWideF) {
+                            // U(4 samples x RP) = W . G^-1 on the fp64 tensor cores, one m8n8k4 tile
+                            // row block (rows 4..7 empty): the mma accumulates in increasing k like
+                            // the fma chain (w and G^-1 are zero past R), bit-identical
                             const double* wb = wsm + warp * kSPW * 32;
+                            double* ub = sm + kSmFact + 2048 + warp * kSPW * 32;
+                            const int rr = lane >> 2, q4 = lane & 3;
+                            constexpr int NTc = MAXR / 8, KSc = MAXR / 4;
+                            double c0[NTc], c1[NTc];
 #pragma unroll
-                            for (int q = 0; q < kSPW; ++q) uq[q][0] = 0.0;
+                            for (int n = 0; n < NTc; ++n) c0[n] = c1[n] = 0.0;
 #pragma unroll
-                            for (int k = 0; k < MAXR; ++k)
+                            for (int ks = 0; ks < KSc; ++ks) {
+                                const int k = 4 * ks + q4;
+                                const double a = (rr < kSPW) ? wb[rr * 32 + k] : 0.0;
 #pragma unroll
-                                for (int q = 0; q < kSPW; ++q) uq[q][0] = __fma_rn(wb[q * 32 + k], g[k], uq[q][0]);
+                                for (int n = 0; n < NTc; ++n) {
+                                    const int col = n * 8 + rr;
+                                    const double bb = (k < R && col < R) ? gsm[k * R + col] : 0.0;
+                                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                                 : "+d"(c0[n]), "+d"(c1[n])
+                                                 : "d"(a), "d"(bb));
+                                }
+                            }
+                            if (rr < kSPW)
+#pragma unroll
+                                for (int n = 0; n < NTc; ++n) {
+                                    ub[rr * 32 + n * 8 + 2 * q4] = c0[n];
+                                    ub[rr * 32 + n * 8 + 2 * q4 + 1] = c1[n];
+                                }
+                            __syncwarp();
+#pragma unroll
+                            for (int q = 0; q < kSPW; ++q) uq[q][0] = (lane < MAXR) ? ub[q * 32 + lane] : 0.0;
                         } else {
 #pragma unroll
                             for (int q = 0; q < kSPW; ++q)
