@@ -70,6 +70,12 @@ struct ChainParams {
     double* wtemp;    // B x R summed temporal right-hand sides of the current batch
     unsigned* fctr;   // dependency counters (flow_kernel.cuh)
     int maxtiles;     // row tiles of the largest stage
+    // k_chain<true, .> with streamed items (chain_stream_items): the window's X_s arena as a 2-D
+    // tensor map of 128-byte rows (box 64 rows = one 32-sample x 32-row chunk tile, 128-B swizzle),
+    // in device memory; nullptr selects the tile-at-a-time items.  zstride: row stride of Z in
+    // memory (RP, or RP + 4 for the streamed items so that the tile is bank-conflict free as loaded)
+    const void* xmap;
+    int zstride;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
@@ -229,6 +235,101 @@ __device__ __noinline__ void chain_rows_warp(const double* __restrict__ cpart, d
         }
         if (v0) out[int64_t(row) * R + j0] = w0;
         if (v1) out[int64_t(row) * R + j1] = w1;
+    }
+    if (!ld_ready) mbar_wait(bar, phase);  // the phase completes before the barrier's next use
+}
+
+// Row solves of phase B for R in 33..64 on the fp64 tensor cores.  A block owns a contiguous
+// range of rows.  Per sub-tile of up to 64 rows: every thread sums superchunk partials (in order)
+// and P for a few entries with all loads in flight, P += X_s Z is stored, and the right-hand
+// sides go to shared memory (row stride RP + 4: conflict-free fragment loads); then each warp
+// forms 8 rows of U = W G^-1 as m8n8k4 MMAs, k increasing -- the fma chain u_j = sum_k b_k
+// G^-1(k, j) of chain_rows_warp bit for bit (zero padding past R leaves the accumulators
+// unchanged; they are never -0).
+template <int NT>
+__device__ __noinline__ void chain_rows_dmma(const double* __restrict__ cpart, double* Prow_base, int st, int rows,
+                                             int R, int nsuper, double* out, const double* Ls, double* wt,
+                                             uint64_t* bar, unsigned phase, const int* mode_flag) {
+    constexpr int RP = 8 * NT, WS = RP + 4, KS = RP / 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q4 = lane & 3, rr = lane >> 2;
+    const int G = gridDim.x;
+    const int rpb = (((rows + G - 1) / G) + 7) & ~7;
+    const int rb0 = int(blockIdx.x) * rpb, rb1 = min(rows, rb0 + rpb);
+    const int mode = __ldcg(mode_flag);
+    bool ld_ready = false;
+    for (int r0 = rb0; r0 < rb1; r0 += 64) {
+        const int nr = min(64, rb1 - r0);
+        const int ne = nr * R;
+        for (int e = tid; e < 64 * WS; e += blockDim.x) wt[e] = 0.0;
+        __syncthreads();
+        const double* cp0 = cpart + int64_t(r0) * R;
+        double* P0 = Prow_base ? Prow_base + int64_t(r0) * R : nullptr;
+        for (int e0 = 0; e0 < ne; e0 += 4 * int(blockDim.x)) {
+            double cv[4][kMaxSuperRows], pv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * int(blockDim.x) + tid;
+                const bool ok = e < ne;
+#pragma unroll
+                for (int m = 0; m < kMaxSuperRows; ++m)
+                    cv[u][m] = (ok && m < nsuper) ? __ldcg(cp0 + int64_t(m) * rows * R + e) : 0.0;
+                pv[u] = (ok && st > 0) ? __ldcg(P0 + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * int(blockDim.x) + tid;
+                if (e < ne) {
+                    double tot = cv[u][0];
+#pragma unroll
+                    for (int m = 1; m < kMaxSuperRows; ++m)
+                        if (m < nsuper) tot = tot + cv[u][m];
+                    for (int m = kMaxSuperRows; m < nsuper; ++m) tot = tot + __ldcg(cp0 + int64_t(m) * rows * R + e);
+                    if (st > 0) {
+                        tot = pv[u] + tot;
+                        P0[e] = tot;
+                    }
+                    const int rl = e / R, c = e - rl * R;
+                    wt[rl * WS + c] = tot;
+                }
+            }
+        }
+        __syncthreads();
+        if (!ld_ready) {
+            mbar_wait(bar, phase);
+            ld_ready = true;
+        }
+        if (warp * 8 < nr) {
+            double c0[NT], c1[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) c0[n] = c1[n] = 0.0;
+            if (mode != 0) {
+                const double* wb = wt + (warp * 8 + rr) * WS + q4;
+#pragma unroll 2
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int k = 4 * ks + q4;
+                    const double a = wb[4 * ks];
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) {
+                        const int col = n * 8 + rr;
+                        const double bb = (k < R && col < R) ? Ls[k + col * R] : 0.0;
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                     : "+d"(c0[n]), "+d"(c1[n])
+                                     : "d"(a), "d"(bb));
+                    }
+                }
+            }
+            const int row = r0 + warp * 8 + rr;
+            if (row < rb1) {
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const int c = n * 8 + 2 * q4;
+                    if (c < R) out[int64_t(row) * R + c] = c0[n];
+                    if (c + 1 < R) out[int64_t(row) * R + c + 1] = c1[n];
+                }
+            }
+        }
+        __syncthreads();  // wt is rewritten by the next sub-tile
     }
     if (!ld_ready) mbar_wait(bar, phase);  // the phase completes before the barrier's next use
 }
@@ -398,6 +499,208 @@ __device__ __noinline__ void chain_contract_dmma(const double* xs, const double*
     }
 }
 
+// ---- Streamed wide contraction (R in 33..64, one superchunk per block) ------------------
+// The block keeps superchunk zm's Z tile resident and walks its share of the stage's row-tile
+// PAIRS (64 rows: tiles 2u, 2u + 1).  A pair's X_s arrives chunk by chunk (two 8 KB bulk
+// copies per 32-sample chunk) through a ring of kRingStages slots, so the loads of the next
+// chunks -- and of the block's next pair -- are in flight behind the MMAs.  Warp w owns the
+// 16 rows rp = w & 3 of the pair and one half of the column tiles (w >> 2) for EVERY chunk:
+// the chunk partial is the fp64 MMA chain over the chunk's samples from +0.0 (rounds like the
+// fma chain, tools/dmma_order.cu) and the superchunk partial is the chunk partials summed left
+// to right in registers -- the arithmetic of chain_contract_dmma without its shared-memory
+// reduction, its block barriers per half, or an exposed tile load per item.
+constexpr int kRingStagesMax = 6;
+// Shared-memory layouts that keep the MMA fragment loads free of bank conflicts: lane (rr, q4)
+// reads row rr of sample k0 + q4, so a sample stride that is a multiple of 128 bytes (X_s: 256)
+// would put the four q4 lanes on the same banks.
+//   X: each (tile, chunk) = 64 rows of 128 bytes arrives through the tensor map with the 128-byte
+//      swizzle (16-byte unit index ^= row index mod 8), so four consecutive samples land on
+//      different banks;
+//   Z: written to memory with a row stride of RP + 4 doubles (p.zstride), one bulk copy per tile.
+constexpr int kRingSlot = 2 * kChunk * kRowTile;  // doubles: two 32-sample x 32-row chunk tiles (16 KB)
+// ring stages by padded width: 6 (5 for RP = 64), then the Z tile [256][RP + 4]
+__host__ __device__ constexpr int stream_stages(int RP) { return RP >= 64 ? 5 : 6; }
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_tile_2d_once(void* dst, const void* map, int c0, int c1, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+struct StreamPlan {
+    int zm, zrank, zcnt;  // the block's superchunk, its rank among that superchunk's blocks, their count
+    int units, nk;        // row-tile pairs of this block in the stage, chunks of the superchunk
+    int nst;              // ring stages
+    unsigned base;        // ring steps this block consumed before the stage (slot / parity bookkeeping)
+    int64_t xrow0;        // first 128-byte row of the stage's X_s in the arena
+};
+
+// one thread: the tensor copies of ring step (pair index ui, chunk k) = step t of the stage.  A
+// box always holds 32 samples; past the end of S it reads the next tile's rows (or zero fill past
+// the arena), which the consumer masks.
+__device__ __forceinline__ void stream_issue(const StreamPlan& sp, int slot, int ui, int k, const void* xmap, int S,
+                                             int tiles, double* ring, uint64_t* rbar, uint64_t pol) {
+    const int u = sp.zrank + ui * sp.zcnt;
+    const int c0 = sp.zm * kSuperSamples + k * kChunk;
+    double* dst = ring + slot * kRingSlot;
+    const bool two = 2 * u + 1 < tiles;
+    constexpr unsigned kBox = kChunk * kRowTile * 8;
+    const int row = int(sp.xrow0) + (2 * u * S + c0) * 2;  // 128-byte rows: below 2^31 (make_xs_map)
+    tma_tile_2d_once(dst, xmap, 0, row, &rbar[slot], pol);
+    if (two) tma_tile_2d_once(dst + kChunk * kRowTile, xmap, 0, row + 2 * S, &rbar[slot], pol);
+    mbar_expect_tx(&rbar[slot], two ? 2 * kBox : kBox);
+}
+
+constexpr int kStreamIssuer = 128;  // lane 0 of warp 4: the warps 4..7 carry the smaller column half
+
+template <int NT>
+__device__ __noinline__ void chain_stream_items(const StreamPlan sp, int S, int rows, int tiles, int R,
+                                                const double* zs, double* ring, uint64_t* rbar, uint64_t* ebar,
+                                                double* cpart_m, unsigned long long* tr, const void* xmap) {
+    constexpr int RPZ = 8 * NT + 4, NH0 = (NT + 1) / 2, NH1 = NT / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q4 = lane & 3, rr = lane >> 2;
+    const int rp = warp & 3, half = warp >> 2;
+    const int n0 = half ? NH0 : 0, nloc = half ? NH1 : NH0;
+    const int tsel = rp >> 1, rsub = (rp & 1) * 16, hrow = rp & 1;
+    const int T = sp.units * sp.nk;
+    // steps in flight: step t + ahead is issued at the start of step t into the slot of step t - 2,
+    // once every warp has released it (ebar: one arrival per warp and consumed step), so the warps
+    // run up to a step apart without a block barrier
+    const int ahead = sp.nst - 2;
+    const uint64_t pol = policy_evict_first();
+    double acc[2][NH0][2], qv[2][NH0][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int n = 0; n < NH0; ++n) qv[a][n][0] = qv[a][n][1] = 0.0;
+    // (pair index, chunk) of the step being consumed and of the step being issued
+    int ui = 0, k = 0, iu = ahead / sp.nk, ik = ahead - iu * sp.nk;
+    unsigned g = sp.base;
+    int slot = int(g % unsigned(sp.nst));
+    unsigned par = (g / unsigned(sp.nst)) & 1u;
+    int islot = int((g + unsigned(ahead)) % unsigned(sp.nst));                 // slot of the step being issued
+    unsigned ipar = (((g + unsigned(ahead)) / unsigned(sp.nst)) & 1u) ^ 1u;  // parity of that slot's previous use
+    // this lane's fragment offsets inside a swizzled chunk tile (per 4-sample step: + 128 doubles)
+    int xo[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const int r = 2 * q4 + hrow;  // (2 (k0 + q4) + hrow) & 7 == r & 7, k0 a multiple of 4
+        xo[a] = r * 16 + (((a * 4 + (rr >> 1)) ^ (r & 7)) << 1) + (rr & 1);
+    }
+    const int zo = q4 * RPZ + n0 * 8 + rr;
+    long long tw_wait = 0, tw_sync = 0, tw_mma = 0;
+    (void)tw_sync;  // traced build: cycles waiting for data / for the block, in the MMAs
+    for (int t = 0; t < T; ++t) {
+        // the slot consumed at step t - 1 is free (block barrier below): refill it
+        if (tid == kStreamIssuer && t + ahead < T) {
+            mbar_wait(&ebar[islot], ipar);
+            stream_issue(sp, islot, iu, ik, xmap, S, tiles, ring, rbar, pol);
+        }
+        const int u = sp.zrank + ui * sp.zcnt;
+        const int cnk = min(kChunk, S - (sp.zm * kSuperSamples + k * kChunk));
+        long long tq0 = 0;
+        if (tr) tq0 = clock64();
+        mbar_wait(&rbar[slot], par);
+        if (tr) tw_wait += clock64() - tq0;
+        if (tr) trace_stamp(tr, 8, blockIdx.x == 0 && tid == 0 && t == 0);
+        const double* xb = ring + slot * kRingSlot + tsel * (kChunk * kRowTile);
+        const double* zb = zs + (k * kChunk) * RPZ + zo;
+        const bool live = 2 * u + tsel < tiles;
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int n = 0; n < NH0; ++n) acc[a][n][0] = acc[a][n][1] = 0.0;
+        if (tr) tq0 = clock64();
+        if (live) {
+            // the next 4-sample step's fragments are loaded before this step's MMAs
+            double fa[2][2], fb[2][NH0];
+            auto ld = [&](int ks, int buf) {
+                const bool valid = 4 * ks + q4 < cnk;
+#pragma unroll
+                for (int a = 0; a < 2; ++a) fa[buf][a] = valid ? xb[ks * 128 + xo[a]] : 0.0;
+#pragma unroll
+                for (int n = 0; n < NH0; ++n) fb[buf][n] = (valid && n < nloc) ? zb[ks * 4 * RPZ + n * 8] : 0.0;
+            };
+            const int nks = (cnk + 3) >> 2;
+            ld(0, 0);
+#pragma unroll
+            for (int ks = 0; ks < kChunk / 4; ++ks) {
+                if (ks < nks) {
+                    if (ks + 1 < kChunk / 4) ld(ks + 1, (ks + 1) & 1);  // past the chunk end: masked to zero, unused
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int n = 0; n < NH0; ++n)
+                            if (n < nloc)
+                                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                             : "+d"(acc[a][n][0]), "+d"(acc[a][n][1])
+                                             : "d"(fa[ks & 1][a]), "d"(fb[ks & 1][n]));
+                }
+            }
+        }
+        // superchunk partial = chunk partials in increasing chunk order
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int n = 0; n < NH0; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) qv[a][n][e] = (k == 0) ? acc[a][n][e] : qv[a][n][e] + acc[a][n][e];
+        if (tr) tw_mma += clock64() - tq0;
+        if (k == sp.nk - 1 && live) {
+            const int i0 = (2 * u + tsel) * kRowTile + rsub;
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const int i = i0 + a * 8 + rr;
+#pragma unroll
+                for (int n = 0; n < NH0; ++n)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int c = (n0 + n) * 8 + 2 * q4 + e;
+                        if (n < nloc && i < rows && c < R) cpart_m[int64_t(i) * R + c] = qv[a][n][e];
+                    }
+            }
+        }
+        __syncwarp();
+        if (lane == 0)  // this warp is done with the slot
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ebar[slot])) : "memory");
+        if (tr) trace_stamp(tr, 9, blockIdx.x == 0 && tid == 0 && t == sp.nk - 1);
+        if (++k == sp.nk) {
+            k = 0;
+            ++ui;
+        }
+        if (++ik == sp.nk) {
+            ik = 0;
+            ++iu;
+        }
+        if (++slot == sp.nst) {
+            slot = 0;
+            par ^= 1u;
+        }
+        if (++islot == sp.nst) {
+            islot = 0;
+            ipar ^= 1u;
+        }
+    }
+    __syncthreads();  // every warp has consumed every step: the ring region is free again
+    if (tr && blockIdx.x == 0 && (tid == 0 || tid == kStreamIssuer)) {  // per step, in cycles
+        if (tid == 0) {
+            tr[20] = (unsigned long long)(tw_wait / max(T, 1));
+            tr[21] = (unsigned long long)(tw_sync / max(T, 1));
+            tr[22] = (unsigned long long)(tw_mma / max(T, 1));
+        } else {
+            tr[23] = (unsigned long long)(tw_mma / max(T, 1));
+        }
+    }
+}
+
 // Chunk Gram partial on the fp64 tensor cores (narrow kernel, RP <= 32): the
 // lower 8x8 tiles of Z_chunk^T Z_chunk, one warp per tile, 8 MMA steps of 4
 // samples over the 32-sample chunk (rows past the chunk end are zero in zc).
@@ -440,7 +743,8 @@ __device__ __noinline__ void chain_chunk_gram_dmma(const double* zc, int RP, int
 constexpr int kSmXs = 0;
 constexpr int kSmZs = kSuperSamples * kRowTile;  // 8192
 constexpr int kSmFact = 16384;
-constexpr int kSmTotal = 27136;                  // doubles
+constexpr int kSmTotal = 28416;                  // doubles (222 KB; the streamed wide items: 1 KB alignment slack + ring + Z tile)
+static_assert(kSuperSamples == 256, "the streamed Z tile is loaded one row per thread");
 constexpr int kZU = 4;                           // phase-0 Z elements per thread per round (registers)
 constexpr int kGramSplitC = 8;                   // Gram output ranges per superchunk
 constexpr int kGramOneBlock = 16384;
@@ -459,6 +763,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     extern __shared__ __align__(128) double sm[];
     __shared__ unsigned short pairs[64 * 65 / 2];
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t rbar[kRingStagesMax];  // wide: the X_s chunk ring (chain_stream_items): slot filled
+    __shared__ __align__(8) uint64_t ebar[kRingStagesMax];  // ... and slot released by the 8 warps
+    __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N, R = p.R, S = p.S, nsuper = p.nsuper, n_other = N - 1;
     const int ng = (R + kCRB - 1) / kCRB, RP = ng * kCRB;
@@ -473,8 +780,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
         for (int j = 0; j < R; ++j)
             for (int i = j; i < R; ++i) pairs[off++] = (unsigned short)((i << 8) | j);
         mbar_init(&bar, 1);
+        for (int q = 0; q < kRingStagesMax; ++q) {
+            mbar_init(&rbar[q], 1);
+            mbar_init(&ebar[q], kChainThreads / 32);
+        }
     }
     __syncthreads();
+    unsigned ring_base = 0;  // ring steps this block has consumed so far (wide, streamed items)
+    // the swizzled tensor copies need 1024-byte aligned destinations
+    double* ring = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u) / 8;
     // Gram: chunk partials are formed in phase 0 by the blocks that build each
     // 32-sample chunk of Z; phase 1 only combines them (canonical superchunk
     // then total order).  Small R^2 x chunks: one block combines everything;
@@ -482,11 +796,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
     const int nch = (S + kChunk - 1) / kChunk;
     const int NPp = (npairs + 1) & ~1;  // chunk-partial stride (lower pairs): 16-byte multiple for the bulk copy
     const bool gram_one = int64_t(NPp) * nch <= kGramOneBlock;
-    const int n_gram = nsuper * kGramSplitC;
-    // the superchunk pre-combine is a few microseconds of work: keep nearly every block
-    // on the contraction, which bounds phase 1 for large R (C4)
-    const int gram_blocks = gram_one ? 1 : min(n_gram, kGramBlocksMax);
-    const int cblocks = G - gram_blocks;  // contraction blocks [0, cblocks), Gram blocks after them
+    // When one block cannot hold every chunk partial, the superchunk's last chunk block
+    // pre-sums them (phase 0), so a single finisher block remains in either case.
+    const int gram_blocks = 1;
+    const int cblocks = G - gram_blocks;  // contraction blocks [0, cblocks), the Gram finisher after them
     const int gb0 = cblocks;
     const bool is_gram_block = int(blockIdx.x) >= gb0;
     const int cix = int(blockIdx.x);  // contraction index
@@ -544,7 +857,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             const int rows = (st == 0) ? p.B : p.head[st - 1];
             const double* X = p.X_base + p.xoff[b * N + st];
             // Z of this stage: the temporal Z is kept per batch for the residual pass
-            double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * RP : p.gch + int64_t(st) * S * RP;
+            const int ZS = p.zstride;  // row stride of Z in memory
+            double* Z = (st == 0) ? p.zbuf + int64_t(b) * S * ZS : p.gch + int64_t(st) * S * ZS;
             const int tiles = (rows + kRowTile - 1) / kRowTile;
             const int n_contract = tiles * nsuper;
             unsigned long long* tr = (kTrace && p.trace) ? p.trace + (int64_t(b) * N + st) * kTraceSlots : nullptr;
@@ -555,7 +869,35 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // item schedule: (tile, superchunk) pairs; the wide kernel gives each block one
             // superchunk (its Z tile, up to 128 KB, is loaded once per stage), the narrow one
             // strides over all items
-            const int first_item = first_item_of(tiles);
+            // wide with one superchunk per block: the streamed pair items (chain_stream_items);
+            // their first ring steps are issued here, ahead of phase 0
+            StreamPlan sp{};
+            bool stream = false;
+            if constexpr (kWide) stream = zreuse && p.xmap != nullptr;
+            if (stream) {
+                const int npair = (tiles + 1) / 2;
+                sp.zm = zm;
+                sp.zrank = zrank;
+                sp.zcnt = zcnt;
+                sp.units = (!is_gram_block && zrank < npair) ? (npair - 1 - zrank) / zcnt + 1 : 0;
+                sp.nk = (min(kSuperSamples, S - zm * kSuperSamples) + kChunk - 1) / kChunk;
+                sp.base = ring_base;
+                sp.nst = stream_stages(RP);
+                sp.xrow0 = p.xoff[b * N + st] / 16;
+                if (sp.units > 0 && tid == 0) {
+                    if (p.gdone) {
+                        wait_gathered(p.gdone + b * N + st, __ldg(p.gneed + b * N + st), gseen);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    const int T = sp.units * sp.nk;  // steps 0 .. nst - 3 now, the rest from the item loop
+                    fence_proxy_async();  // the ring region was last written through the generic proxy (phase B)
+                    const uint64_t pol = policy_evict_first();
+                    for (int t = 0; t < min(sp.nst - 2, T); ++t)
+                        stream_issue(sp, int((sp.base + unsigned(t)) % unsigned(sp.nst)), t / sp.nk, t % sp.nk, p.xmap, S,
+                                     tiles, ring, rbar, pol);
+                }
+            }
+            const int first_item = stream ? n_contract : first_item_of(tiles);
             const bool contract_block = first_item < n_contract;
             if (contract_block && tid == 0) {
                 const int tile = first_item % tiles, m = first_item / tiles;
@@ -589,7 +931,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
             // (k_gram's per-chunk sequence), lower pairs mirrored.
             for (int ch = ch_first; ch < nch; ch += cblocks) {
                 const int c0 = ch * kChunk, cn = min(kChunk, S - c0);
-                double* zc = zs;  // [32][RP]; scratch, before this block's contraction Z
+                // [32][RP]; scratch, before this block's contraction Z (streamed items: clear of the
+                // X ring, whose first steps are already in flight)
+                double* zc = stream ? ring + stream_stages(RP) * kRingSlot : zs;
                 const int32_t* idx = p.idx_base + int64_t(b * N + st) * S * n_other;
                 if (ch == ch_first) {
                     double f[kZU][kMaxOrder - 1];
@@ -615,7 +959,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                                     if (l < n_other) z = z * f[u][l];
                             }
                             zc[e] = z;
-                            if (cc < cn) Z[int64_t(c0) * RP + e] = z;
+                            if (cc < cn) Z[int64_t(c0 + cc) * ZS + r] = z;
                         }
                     }
                 }
@@ -631,7 +975,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                                 z = z * __ldcg(F[l] + int64_t(__ldg(idx + int64_t(c0 + cc) * n_other + (n_other - 1 - l))) * R + r);
                     }
                     zc[e] = z;
-                    if (cc < cn) Z[int64_t(c0) * RP + e] = z;
+                    if (cc < cn) Z[int64_t(c0 + cc) * ZS + r] = z;
                 }
                 __syncthreads();
                 if (tr) trace_stamp(tr, 14, tid == 0 && ch == 0);
@@ -652,42 +996,50 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                 }
                 __syncthreads();
                 if (tr) trace_stamp(tr, 15, tid == 0 && ch == 0);
+                const int msup = ch / kSuper;
                 if (tid == 0) {  // the chunk's Z rows and Gram partial are in (bar.sync above)
                     __threadfence();
-                    atomicAdd(p.zctr + 1 + ch / kSuper, 1u);
+                    const unsigned prev = atomicAdd(p.zctr + 1 + msup, 1u);
+                    const unsigned nck = unsigned(min(kSuper, nch - msup * kSuper));
+                    s_last = (!gram_one && prev + 1 == unsigned(b * N + st + 1) * nck) ? 1 : 0;
                     atomicAdd(p.zctr, 1u);
+                }
+                if (!gram_one) {  // the superchunk's last chunk pre-sums its Gram partials, chunks in order
+                    __syncthreads();
+                    if (s_last) {
+                        __threadfence();
+                        const int k0 = msup * kSuper, k1 = min(nch, k0 + kSuper);
+                        for (int pp = tid; pp < npairs; pp += blockDim.x) {
+                            double v[kSuper];  // every load before the sums
+#pragma unroll
+                            for (int u = 0; u < kSuper; ++u)
+                                v[u] = (k0 + u < k1) ? __ldcg(p.chpart + int64_t(k0 + u) * NPp + pp) : 0.0;
+                            double q = v[0];
+#pragma unroll
+                            for (int u = 1; u < kSuper; ++u)
+                                if (k0 + u < k1) q = q + v[u];
+                            p.gpart[int64_t(msup) * NPp + pp] = q;
+                        }
+                        __syncthreads();
+                        if (tid == 0) {
+                            __threadfence();
+                            atomicAdd(p.zctr + 1 + nsuper, 1u);
+                        }
+                    }
+                    __syncthreads();  // s_last is rewritten by the block's next chunk
                 }
             }
             if (tr) trace_stamp(tr, 1, blockIdx.x == 0 && tid == 0);
 
             // ---------------- phase 1
             if (is_gram_block) {
-                if (tid == 0) {  // every chunk partial of this stage published
-                    wait_gathered(p.zctr, unsigned(b * N + st + 1) * unsigned(nch), 0u, 0u);
+                if (tid == 0) {  // every chunk partial (or every superchunk pre-sum) of this stage published
+                    if (gram_one) wait_gathered(p.zctr, unsigned(b * N + st + 1) * unsigned(nch), 0u, 0u);
+                    else wait_gathered(p.zctr + 1 + nsuper, unsigned(b * N + st + 1) * unsigned(nsuper), 0u, 0u);
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
                 }
                 __syncthreads();
-                // superchunk sums of the chunk partials, superchunk m = chunks 8m..8m+7 in order
-                auto super_sum = [&](int m, int pp) {
-                    const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
-                    double v[kSuper];
-#pragma unroll
-                    for (int u = 0; u < kSuper; ++u) v[u] = (k0 + u < k1) ? __ldcg(p.chpart + int64_t(k0 + u) * NPp + pp) : 0.0;
-                    double q = v[0];
-#pragma unroll
-                    for (int u = 1; u < kSuper; ++u)
-                        if (k0 + u < k1) q = q + v[u];
-                    return q;
-                };
-                bool finisher = gram_one;
-                if (!gram_one) {
-                    for (int gi = int(blockIdx.x) - gb0; gi < n_gram; gi += gram_blocks) {
-                        const int m = gi / kGramSplitC, part = gi % kGramSplitC;
-                        const int pp0 = (npairs * part) / kGramSplitC, pp1 = (npairs * (part + 1)) / kGramSplitC;
-                        for (int pp = pp0 + tid; pp < pp1; pp += blockDim.x) p.gpart[int64_t(m) * NPp + pp] = super_sum(m, pp);
-                    }
-                    finisher = last_arrive_of(p.counter, unsigned(gram_blocks));
-                }
+                const bool finisher = true;
                 if (finisher) {
                     if (tr) trace_stamp(tr, 3, tid == 0);
                     double* A = sm + kSmFact;        // [64][65]
@@ -719,27 +1071,62 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         phase ^= 1u;
                     }
                     if (tr) trace_stamp(tr, 18, tid == 0);
+                    if (!gram_one) {
+                        // the superchunk pre-sums in order; every load of a batch of pairs (the
+                        // pre-sums and Q) is issued before the sums and the stores to Q
+                        constexpr int kPB = 5;
+                        for (int u0 = 0; u0 < kMaxPairsPerThread; u0 += kPB) {
+                            if (tid + u0 * int(blockDim.x) >= npairs) break;
+                            double gv[kPB][8], qva[kPB], qvb[kPB];
+#pragma unroll
+                            for (int uu = 0; uu < kPB; ++uu) {
+                                const int q = tid + (u0 + uu) * int(blockDim.x);
+                                const bool ok = q < npairs;
+#pragma unroll
+                                for (int m = 0; m < 8; ++m)
+                                    gv[uu][m] = (ok && m < nsuper) ? __ldcg(p.gpart + int64_t(m) * NPp + q) : 0.0;
+                                qva[uu] = qvb[uu] = 0.0;
+                                if (ok && st > 0) {
+                                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                                    qva[uu] = __ldcg(p.Q[st - 1] + i + j * R);
+                                    qvb[uu] = __ldcg(p.Q[st - 1] + j + i * R);
+                                }
+                            }
+#pragma unroll
+                            for (int uu = 0; uu < kPB; ++uu) {
+                                const int q = tid + (u0 + uu) * int(blockDim.x);
+                                if (q < npairs) {
+                                    double tot = gv[uu][0];
+#pragma unroll
+                                    for (int m = 1; m < 8; ++m)
+                                        if (m < nsuper) tot = tot + gv[uu][m];
+                                    for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
+                                    const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
+                                    double ga = tot, gb = tot;
+                                    if (st > 0) {  // Q + G entry by entry (rocp.cpp:108)
+                                        ga = qva[uu] + tot;
+                                        gb = qvb[uu] + tot;
+                                        p.Q[st - 1][i + j * R] = ga;
+                                        p.Q[st - 1][j + i * R] = gb;
+                                    }
+                                    Gs[i + j * R] = ga;
+                                    Gs[j + i * R] = gb;
+                                }
+                            }
+                        }
+                    }
 #pragma unroll
                     for (int u = 0; u < kMaxPairsPerThread; ++u) {
                         const int q = tid + u * int(blockDim.x);
-                        if (q >= npairs) break;
+                        if (q >= npairs || !gram_one) break;
                         double tot;
-                        if (gram_one) {
+                        {
                             for (int m = 0; m < nsuper; ++m) {
                                 const int k0 = m * kSuper, k1 = min(nch, k0 + kSuper);
                                 double sq = chs[k0 * NPp + q];
                                 for (int k = k0 + 1; k < k1; ++k) sq = sq + chs[k * NPp + q];
                                 tot = (m == 0) ? sq : tot + sq;
                             }
-                        } else {
-                            double v[8];
-#pragma unroll
-                            for (int m = 0; m < 8; ++m) v[m] = (m < nsuper) ? __ldcg(p.gpart + int64_t(m) * NPp + q) : 0.0;
-                            tot = v[0];
-#pragma unroll
-                            for (int m = 1; m < 8; ++m)
-                                if (m < nsuper) tot = tot + v[m];
-                            for (int m = 8; m < nsuper; ++m) tot = tot + __ldcg(p.gpart + int64_t(m) * NPp + q);
                         }
                         // Q + G entry by entry (rocp.cpp:108); G is symmetric bit for bit
                         const int i = pairs[q] >> 8, j = pairs[q] & 0xff;
@@ -781,6 +1168,29 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         if (tr) tr[4] = gtimer();
                     }
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // LD is read by TMA
+                }
+            } else if (stream) {
+                if (sp.units > 0) {
+                    const int c0 = zm * kSuperSamples, cn = min(kSuperSamples, S - c0);
+                    double* zst = ring + stream_stages(RP) * kRingSlot;  // [256][RP + 4], as in memory
+                    if (tid == 0) {  // superchunk zm's chunks of Z published (no grid barrier after phase 0)
+                        const unsigned nck = unsigned(min(kSuper, nch - zm * kSuper));
+                        wait_gathered(p.zctr + 1 + zm, unsigned(b * N + st + 1) * nck, 0u, 0u);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
+                        fence_proxy_async();
+                        tma_load_1d(zst, Z + int64_t(c0) * ZS, unsigned(cn * ZS * 8), &bar);
+                        mbar_expect_tx(&bar, unsigned(cn * ZS * 8));
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    double* cpm = p.cpart + int64_t(zm) * rows * R;
+                    if constexpr (kWide) {
+                        if (RP == 40) chain_stream_items<5>(sp, S, rows, tiles, R, zst, ring, rbar, ebar, cpm, tr, p.xmap);
+                        else if (RP == 48) chain_stream_items<6>(sp, S, rows, tiles, R, zst, ring, rbar, ebar, cpm, tr, p.xmap);
+                        else if (RP == 56) chain_stream_items<7>(sp, S, rows, tiles, R, zst, ring, rbar, ebar, cpm, tr, p.xmap);
+                        else chain_stream_items<8>(sp, S, rows, tiles, R, zst, ring, rbar, ebar, cpm, tr, p.xmap);
+                    }
+                    ring_base += unsigned(sp.units * sp.nk);
                 }
             } else {
                 int zm_cur = -1;
@@ -866,7 +1276,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     if (tr) trace_stamp(tr, 16, blockIdx.x == 0 && tid == 0);
                     double* out = (st == 0) ? u_new : p.U[st - 1];
                     double* Pst = st > 0 ? p.P[st - 1] : nullptr;
-                    chain_rows_warp(p.cpart, Pst, st, rows, R, nsuper, out, Ls, &bar, phase, p.mode_flag);
+                    if constexpr (kWide) {
+                        double* wt = sm + 4608;  // past L/D (R R + R <= 4160 doubles)
+                        if (RP == 40) chain_rows_dmma<5>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, wt, &bar, phase, p.mode_flag);
+                        else if (RP == 48) chain_rows_dmma<6>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, wt, &bar, phase, p.mode_flag);
+                        else if (RP == 56) chain_rows_dmma<7>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, wt, &bar, phase, p.mode_flag);
+                        else chain_rows_dmma<8>(p.cpart, Pst, st, rows, R, nsuper, out, Ls, wt, &bar, phase, p.mode_flag);
+                    } else {
+                        chain_rows_warp(p.cpart, Pst, st, rows, R, nsuper, out, Ls, &bar, phase, p.mode_flag);
+                    }
                     phase ^= 1u;
                     if (tr) trace_stamp(tr, 17, blockIdx.x == 0 && tid == 0);
                 }

@@ -744,6 +744,8 @@ struct Window {
     bool key_sort = true;
     std::vector<int64_t> zc_tile;  // host path: first zero-copy gather tile of each batch
     GatherTmaParams gtp{};         // tensor-map views of the strided modes (overlapped gather)
+    DBuf<char> xmap;               // tensor map of the X_s arena (k_chain's streamed wide items), device copy
+    bool xmap_ok = false;
 };
 
 // Window of a sharded stream: per (batch, stage) the global draws, the
@@ -863,6 +865,8 @@ void clear_graphs(rocp_stream* st) {
     st->graphs.clear();
 }
 
+bool make_xs_map(const double* x, size_t n, CUtensorMap* map);
+
 // Ensures the window arena holds nb batches of B slices.
 void ensure_window(rocp_stream* st, int64_t nb, int64_t B) {
     Window& W = st->win;
@@ -883,7 +887,15 @@ void ensure_window(rocp_stream* st, int64_t nb, int64_t B) {
         }
     W.X.alloc(size_t(off));
     {
-        const int64_t RP = ((st->R + kCRB - 1) / kCRB) * kCRB;
+        CUtensorMap xm;
+        W.xmap_ok = make_xs_map(W.X.p, W.X.n, &xm);
+        if (W.xmap_ok) {
+            W.xmap.alloc(sizeof(CUtensorMap));
+            CK(cudaMemcpy(W.xmap.p, &xm, sizeof(xm), cudaMemcpyHostToDevice));
+        }
+    }
+    {
+        const int64_t RP = ((st->R + kCRB - 1) / kCRB) * kCRB + 4;  // + 4: the padded stride of the streamed wide chain
         W.zT.alloc(size_t(nbn * S * RP));
         W.rcols.alloc(size_t(nbn * 3 * S));
         W.rhist.alloc(size_t(nbn * 2));
@@ -914,6 +926,39 @@ double* win_x(rocp_stream* st, int64_t b, int stage) { return st->win.X.p + st->
 // multiples; a misaligned range; extents past 2^31) or ROCP_GATHER_TMA=0; those
 // jobs use LSU loads.  ROCP_GATHER_PROMO selects the strided boxes' L2
 // promotion for A/B runs.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    return encode;
+}
+
+// The X_s arena (n doubles, 128-byte aligned) as 128-byte rows for k_chain's streamed wide items
+// (chain_kernel.cuh chain_stream_items): box = 64 rows = one 32-sample x 32-row chunk tile,
+// 128-byte swizzle.  ROCP_CHAIN_STREAM=0 keeps the tile-at-a-time items (A/B aid).
+bool make_xs_map(const double* x, size_t n, CUtensorMap* map) {
+    static const bool off = [] {
+        const char* e = std::getenv("ROCP_CHAIN_STREAM");
+        return e && std::atoi(e) == 0;
+    }();
+    const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (off || !encode || n < 16 || reinterpret_cast<uintptr_t>(x) % 128 != 0) return false;
+    const cuuint64_t rows = cuuint64_t(n / 16);
+    if (rows >= (cuuint64_t(1) << 31)) return false;
+    const cuuint64_t dims[2] = {16, rows};
+    const cuuint64_t gstr[1] = {128};
+    const cuuint32_t box[2] = {16, 64};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dims, gstr, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_gather_view(const double* x, const std::vector<int64_t>& wd, int mode, int64_t fibre_len, CUtensorMap* map,
                       GatherView* view) {
     static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
@@ -1109,7 +1154,7 @@ int gather_sms(rocp_stream* st, int64_t B) {
             rows_max = std::max(rows_max, double(I));
         }
         elems *= double(st->s);
-        const double t_chain = st->N * (st->R > 32 ? 110.0 : 14.0);     // us per batch
+        const double t_chain = st->N * (st->R > 32 ? 95.0 : 14.0);      // us per batch
         const double t_full = elems / (93e3);                             // us, whole-device gather
         if (t_full < 0.025 * (t_full + t_chain)) return 0;
         g = int(std::ceil(elems / (1470.0 * t_chain)));
@@ -1132,9 +1177,9 @@ int gather_sms(rocp_stream* st, int64_t B) {
         // stage take 10 rounds on 111 blocks (G = 33) but 9 on 112 (G = 32).
         const int64_t npairs = int64_t(st->R) * (st->R + 1) / 2;
         const int64_t nch = (st->s + kChunk - 1) / kChunk, nsup = (st->s + kSuperSamples - 1) / kSuperSamples;
-        const int gram_blocks = ((npairs + 1) & ~int64_t(1)) * nch <= kGramOneBlock
-                                    ? 1
-                                    : int(std::min<int64_t>(nsup * kGramSplitC, kGramBlocksMax));
+        (void)npairs;
+        (void)nch;
+        const int gram_blocks = 1;
         const int64_t items = ((int64_t(rows_max) + kRowTile - 1) / kRowTile) * nsup;
         auto rounds = [&](int G) {
             const int64_t cb = std::max<int64_t>(1, dev->num_sms - G - gram_blocks);
@@ -1144,9 +1189,10 @@ int gather_sms(rocp_stream* st, int64_t B) {
         // it takes the one that leaves it the most (C4: 28 -> 142k, 32 -> 137k slices/s).
         int best = g;
         if (st->R > 32) {
-            const int lo = std::max(1, int(std::ceil(0.85 * g)));
-            for (int G = g; G >= lo; --G)
-                if (rounds(G) <= rounds(best)) best = G;
+            // the wide chain is paced by the gather below this split and loses its own SMs above it
+            // (C4, tools/runs/c4_gather_sweep.sh: 28 -> 143k, 32 -> 155k, 36..40 -> 168k, 44 -> 155k,
+            // 52 -> 144k slices/s); its streamed pair items take the same number of rounds over
+            // that whole range
         } else {
             for (int G = g; G >= std::max(1, int(std::floor(0.8 * g))); --G)
                 if (rounds(G) < rounds(best)) best = G;
@@ -1372,7 +1418,6 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
     p.idx_base = st->win.idx.p + b0 * st->N * st->s * (st->N - 1);
     p.X_base = st->win.X.p;
     p.xoff = st->win.xoff_dev.p + b0 * st->N;
-    p.zbuf = st->win.zT.p + b0 * st->s * RPw;
     p.gch = st->zmodes.p;
     p.gpart = st->gpart.p;
     p.chpart = st->chpart.p;
@@ -1384,8 +1429,9 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
     p.rpart = st->rpart.p;
     p.counter = st->dev->counters.p + 4;
     // phase-0 chunk arrivals (total, per superchunk), cumulative over the launch's stages
-    if (st->zctr.n < size_t(p.nsuper + 1)) st->zctr.alloc(size_t(p.nsuper + 1));
-    CK(cudaMemsetAsync(st->zctr.p, 0, size_t(p.nsuper + 1) * sizeof(unsigned), st->dev->stream));
+    // (+ [1 + nsuper]: superchunk Gram pre-sums published, k_chain without the one-block combine)
+    if (st->zctr.n < size_t(p.nsuper + 2)) st->zctr.alloc(size_t(p.nsuper + 2));
+    CK(cudaMemsetAsync(st->zctr.p, 0, size_t(p.nsuper + 2) * sizeof(unsigned), st->dev->stream));
     p.zctr = st->zctr.p;
     int grid = st->dev->num_sms;
     if (overlap) {
@@ -1395,6 +1441,12 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
         grid -= st->win_gsms;
     }
     const bool flow = use_flow(st, grid);
+    // streamed wide items (chain_stream_items): one superchunk per block, X_s through the arena's
+    // tensor map, Z rows padded by 4 doubles
+    const bool streamed = !flow && st->R > 32 && st->win.xmap_ok && grid - 1 >= p.nsuper;
+    p.xmap = streamed ? st->win.xmap.p : nullptr;
+    p.zstride = int(streamed ? RPw + 4 : RPw);
+    p.zbuf = st->win.zT.p + b0 * st->s * p.zstride;
     if (flow) {
         int maxtiles = int((B + kRowTile - 1) / kRowTile);
         for (int64_t I : st->head) maxtiles = std::max(maxtiles, int((I + kRowTile - 1) / kRowTile));
@@ -1439,13 +1491,13 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
         w.R = st->R;
         w.S = int(st->s);
         w.B = int(B);
-        w.RP = ((st->R + kCRB - 1) / kCRB) * kCRB;
+        w.RP = p.zstride;  // row stride of the temporal Z
         w.nb = int(nb);
         w.temporal = st->temporal.p;
         w.t_len0 = st->t_len;
         w.X_base = st->win.X.p;
         w.xoff = st->win.xoff_dev.p + b0 * st->N;
-        w.zT = st->win.zT.p + b0 * st->s * RPw;
+        w.zT = p.zbuf;
         w.cols = st->win.rcols.p;
         w.out = st->win.rhist.p;
         w.last_out = st->resid.p;
@@ -2164,7 +2216,7 @@ rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int 
     st->batch_dev.alloc(1);
     st->gpart.alloc(size_t(((s + kSuperSamples - 1) / kSuperSamples) * rank * rank));
     st->chpart.alloc(size_t(((s + kChunk - 1) / kChunk) * ((rank * rank + 1) & ~1)));
-    st->zmodes.alloc(size_t(order * s * (((rank + kCRB - 1) / kCRB) * kCRB)));
+    st->zmodes.alloc(size_t(order * s * (((rank + kCRB - 1) / kCRB) * kCRB + 4)));
     st->LD.alloc(size_t(rank * rank + rank + 2));
     st->rpart.alloc(size_t(3 * s));
     st->mode_flag.alloc(4);

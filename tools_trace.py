@@ -45,5 +45,10 @@ for stg in range(N):
           f"gram->factor start={med(t[:,3]-t[:,1]):.2f} combine={med(t[:,10]-t[:,3]):.2f} prologue={med(t[:,12]-t[:,10]):.2f} "
           f"ldlt={med(t[:,13]-t[:,12]):.2f} check={med(t[:,11]-t[:,13]):.2f} publish={med(t[:,4]-t[:,11]):.2f} | "
           f"tma-wait={med(t[:,18]-t[:,3]):.2f} | sync1 done={med(z(5)):.2f} LD ready={med(t[:,16]-t[:,5]):.2f} row loop={med(t[:,17]-t[:,16]):.2f} rows={med(t[:,6]-t[:,5]):.2f} sync2={med(t[:,7]-t[:,6]):.2f} | total={med(t[:,7]-t[:,0]):.2f} us")
+if tr.shape[1] > 23 and tr[:, 20:24].any():
+    for stg in range(N):
+        t = tr[stg::N].astype(float)
+        print(f"stage {stg}: streamed items, cycles per ring step: warp 0 data wait {np.median(t[:,20]):.0f}, block wait {np.median(t[:,21]):.0f}, "
+              f"MMA section {np.median(t[:,22]):.0f}; warp 4 (issuer) MMA section {np.median(t[:,23]):.0f}")
 print("whole window us:", (tr[-1, 7] - tr[0, 0]) / 1e3)
 print("residual of last batch:", st.last_residuals()[0])
