@@ -558,7 +558,9 @@ def main():
         flops = nb * (2 * S * R * (B + sum(head)) + len(dims) * S * R * (R + 1))
         c_avg = statistics.mean(chain_ms)
         fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
-        chain_roof = {"kernel": "k_chain (persistent factor-dependent chain, one launch per window)",
+        chain_name = ("k_flow (dataflow chain, no grid barriers)" if R <= 32 and os.environ.get("ROCP_CHAIN") != "barrier"
+                      else "k_chain (grid-barrier chain" + (", streamed fp64-MMA pair items)" if R > 32 else ")"))
+        chain_roof = {"kernel": chain_name + ": the persistent factor-dependent chain, one launch per window",
                       "bound": "latency (dependent Gauss-Seidel chain; fp64 pipe as the compute ceiling)",
                       "achieved": flops / (c_avg / 1000.0) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
                       "frac": flops / (c_avg / 1000.0) / 1e12 / fp64_peak,
@@ -674,7 +676,7 @@ def main():
             "gram_decisions": {"counts": dec_stats, "keys": ["no_reg", "reg", "exact_eigen", "tier2_used"],
                                "note": "solve_gram regularisation decisions since init (DESIGN.md 3.4)"},
             "roofline": {"kernel": ("k_gather_warps (window sampled-fibre gather, TMA boxes), overlapped on "
-                                    f"{gather_sms} SMs beside k_chain" if gather_sms else
+                                    f"{gather_sms} SMs beside the persistent chain" if gather_sms else
                                     "k_gather (window sampled-fibre gather, every SM, before the chain)"),
                          "bound": "hbm", "sms": gather_sms or 148,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
