@@ -421,6 +421,66 @@ def device_config_run(rocp, dev, cfg, steps, warmup):
     return out
 
 
+def multi_stream_run(rocp, cfg, K, steps, warmup, num_sms=148, chain_sms=0):
+    """K independent streams of one config sharing the GPU, one handle (CUDA stream, scratch,
+    tensor) each -- the reference's trial-level parallelism (bench.cpp:190-213, ROCP_THREADS; what
+    the reference arm times on the host cores).  Every handle's persistent chain takes
+    num_sms // K blocks (rocp_set_chain_sms), so the K cooperative chains are co-resident; the
+    window gathers run serially per stream (several handles on one GPU) and overlap the other
+    streams' chains.  Timed on the host around device synchronisations AND with CUDA events per
+    handle; the slower of the two is reported."""
+    dims, R, t_init, B = cfg["dims"], cfg["rank"], cfg["t_init"], cfg["batch"]
+    nb = (dims[-1] - t_init) // B
+    sms = chain_sms if chain_sms else max(16, num_sms // K)
+    devs, Xs, sts = [], [], []
+    for i in range(K):
+        d = rocp.Device(0)
+        d.set_chain_sms(sms)
+        g = np.random.default_rng(1000 + i)
+        X = d.tensor(dims)
+        X.generate(make_factors(dims, R, cfg["family"], g), snr_db=cfg["snr_db"], noise_seed=2000 + i)
+        init = rocp.cprand_decompose(d, X.slab(0, t_init), R, init_factors(cfg, i), seed=3000 + i, tol=cfg["tol"],
+                                     max_iters=cfg["max_iters"])
+        st = rocp.RocpStream(d, init, auto_s(R), t_capacity=dims[-1] + 8)
+        st.checkpoint()
+        devs.append(d)
+        Xs.append(X)
+        sts.append(st)
+    for w in range(warmup):
+        for i in range(K):
+            sts[i].restore()
+            sts[i].consume_range(Xs[i], t_init, B, nb, 9000 + w, 1)
+    for d in devs:
+        d.synchronize()
+    t0 = time.perf_counter()
+    for d in devs:
+        d.timer_record(6)
+    for k in range(steps):
+        for i in range(K):
+            sts[i].restore()
+            sts[i].consume_range(Xs[i], t_init, B, nb, 10000 + k, 1)
+    for d in devs:
+        d.timer_record(7)
+    for d in devs:
+        d.synchronize()
+    wall_ms = 1000.0 * (time.perf_counter() - t0)
+    ev_ms = max(d.timer_elapsed_ms(6, 7) for d in devs)
+    ms = max(wall_ms, ev_ms)
+    out = {"streams": K, "chain_sms_per_stream": sms, "value": K * steps * nb * B / (ms / 1000.0),
+           "unit": "time-slices/s", "steps": steps, "ms_per_round": ms / steps, "wall_ms": wall_ms,
+           "event_ms_max": ev_ms,
+           "note": "aggregate of K independent streams on one GPU (one handle each); the slower of host wall "
+                   "time around device synchronisations and the per-handle CUDA-event time"}
+    for st in sts:
+        st._free()
+    for X in Xs:
+        X._free()
+    for d in devs:
+        d.synchronize()
+        d.close()
+    return out
+
+
 # --------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -659,6 +719,12 @@ def main():
                 continue
             configs_line[key] = device_config_run(rocp, dev, CONFIGS[key], steps=3, warmup=3)
 
+    # ---- K independent streams sharing this GPU (the reference arm's shape: independent streams
+    # on all host threads), a secondary key beside the single-stream headline
+    multi = None
+    if rank == 0 and world == 1 and not sharded and not args.no_configs and int(np.prod(dims)) * 8 <= 9e9:
+        multi = multi_stream_run(rocp, CFG, 4, steps=5, warmup=3, chain_sms=30)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "time-slices/s", "n_gpus": world,
@@ -698,6 +764,7 @@ def main():
             "e2e_per_batch": e2e_pb,
             "cpu_baseline": cpu,
             "configs": configs_line,
+            "multi_stream": multi,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

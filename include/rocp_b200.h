@@ -70,6 +70,13 @@ rocp_status rocp_timer_elapsed_ms(rocp_dev* dev, int a, int b, float* ms);
  * Results are bitwise identical for every setting.  No reference counterpart
  * (a B200 scheduling knob). */
 rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms);
+/* Blocks of this handle's persistent chain kernel (0 = one per SM, the default;
+ * otherwise 16 .. SM count).  For several independent streams on one GPU, one
+ * handle each -- the reference's trial-level parallelism (bench.cpp:190-213,
+ * ROCP_THREADS): with K handles at SMs/K blocks each, the K cooperative chains are
+ * co-resident and the GPU's otherwise idle SMs serve the other streams.  Results
+ * are bitwise identical for every setting.  No reference counterpart. */
+rocp_status rocp_set_chain_sms(rocp_dev* dev, int sms);
 /* Measurement aid (no reference counterpart): event-timed kernel of `reads`
  * independent 8-byte loads at hashed offsets of t on every SM -- the device's
  * isolated random-read ceiling that bounds the strided sampled-fibre gather

@@ -44,6 +44,7 @@ SIGNATURES = [
     ("rocp_destroy", None, [_vp]),
     ("rocp_last_error", C.c_char_p, [_vp]),
     ("rocp_set_gather_sms", C.c_int, [_vp, C.c_int]),
+    ("rocp_set_chain_sms", C.c_int, [_vp, C.c_int]),
     ("rocp_synchronize", C.c_int, [_vp]),
     ("rocp_kernel_launches", C.c_uint64, [_vp]),
     ("rocp_nccl_id_size", C.c_int, []),
@@ -285,6 +286,10 @@ class Device:
     def set_gather_sms(self, sms):
         """SMs of the overlapped window gather (rocp_set_gather_sms; < 0 = model)."""
         self.check(lib().rocp_set_gather_sms(self.h, int(sms)))
+
+    def set_chain_sms(self, sms):
+        """Blocks of this handle's persistent chain (rocp_set_chain_sms; 0 = every SM)."""
+        self.check(lib().rocp_set_chain_sms(self.h, int(sms)))
 
     def tensor(self, dims, host=None):
         return DeviceTensor(self, dims, host)

@@ -209,6 +209,7 @@ struct rocp_dev {
     cudaStream_t gstream = nullptr;
     cudaEvent_t ev_gready = nullptr, ev_gdone = nullptr;
     int gather_sms = -1;                // -1: not set (env decides); -2: per-stream model; >= 0: fixed
+    int chain_sms = 0;                  // blocks of the persistent chain (0: every SM); rocp_set_chain_sms
     bool counted = false;               // registered in g_handles (live handles per GPU)
     int num_sms = 148;
     // device-resident result of the last rocp_cprand (for stream_create_from_init)
@@ -1440,6 +1441,9 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
         p.gneed = st->win.jobs.need.p;
         grid -= st->win_gsms;
     }
+    // several independent streams sharing the GPU (one handle each): each chain takes its share of
+    // the SMs, so the chains of different handles are co-resident (rocp_set_chain_sms)
+    if (st->dev->chain_sms > 0) grid = std::max(1, std::min(grid, st->dev->chain_sms));
     const bool flow = use_flow(st, grid);
     // streamed wide items (chain_stream_items): one superchunk per block, X_s through the arena's
     // tensor map, Z rows padded by 4 doubles
@@ -1692,6 +1696,15 @@ rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms) {
         if (sms > dev->num_sms / 2) throw_domain("gather SMs: at most half the device");
         CK(cudaStreamSynchronize(dev->stream));
         dev->gather_sms = sms < 0 ? -2 : sms;
+    });
+}
+
+rocp_status rocp_set_chain_sms(rocp_dev* dev, int sms) {
+    return guarded(dev, [&] {
+        if (sms < 0 || sms > dev->num_sms) throw_domain("chain SMs: 0 (every SM) .. the device's SM count");
+        if (sms != 0 && sms < 16) throw_domain("chain SMs: at least 16");
+        CK(cudaStreamSynchronize(dev->stream));
+        dev->chain_sms = sms;
     });
 }
 
