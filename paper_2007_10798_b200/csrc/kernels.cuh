@@ -315,10 +315,17 @@ __device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
 // ---------------------------------------------------------------------------
 // K4a: Gram G = Z^T Z (solve.cpp:41, rocp.cpp:108) in the canonical chunked
 // order.  One block per 32-sample chunk writes its R x R chunk partials; the
-// last block sums them in increasing chunk order and optionally accumulates
-// (Q + G, rocp.cpp:108).
+// last block of each superchunk (8 chunks) sums them in increasing chunk order
+// into the superchunk partial, and the last of those blocks sums the
+// superchunk partials in order and optionally accumulates (Q + G,
+// rocp.cpp:108).  Every load of a batch of outputs is issued before its sums
+// (a single block combining every chunk partial with one load round trip per
+// superchunk took 83 us at R = 50, S = 1957).
+__device__ __forceinline__ bool last_arrive_of(unsigned int* counter, unsigned int expected);
+
 __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int32_t s, int R,
-                                              double* __restrict__ partial, unsigned int* counter,
+                                              double* __restrict__ partial, double* __restrict__ spart,
+                                              unsigned int* counter, unsigned int* sc_counters,
                                               const double* acc_base, double* __restrict__ out) {
     extern __shared__ double zs[];  // kChunk x R
     const int k = blockIdx.x;
@@ -336,24 +343,54 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int3
         for (int cc = 0; cc < cn; ++cc) acc = __fma_rn(zs[cc * R + r1], zs[cc * R + r2], acc);
         partial[int64_t(k) * RR + p] = acc;
     }
-    if (!last_block_arrive(counter)) return;
     const int nk = gridDim.x;
-    for (int p = threadIdx.x; p < RR; p += blockDim.x) {
-        // two-level canonical combine: superchunks of kSuper chunks
-        double tot = 0.0;
-        for (int m0 = 0; m0 < nk; m0 += kSuper) {
-            const int m1 = min(nk, m0 + kSuper);
-            double pk[kSuper];
+    const int msup = k / kSuper, m0 = msup * kSuper, m1 = min(nk, m0 + kSuper);
+    if (!last_arrive_of(sc_counters + msup, unsigned(m1 - m0))) return;
+    constexpr int kOB = 4;  // outputs per batch of loads
+    for (int pb = threadIdx.x; pb < RR; pb += kOB * blockDim.x) {
+        double pk[kOB][kSuper];
+#pragma unroll
+        for (int o = 0; o < kOB; ++o) {
+            const int p = pb + o * int(blockDim.x);
 #pragma unroll
             for (int u = 0; u < kSuper; ++u)
-                pk[u] = (m0 + u < m1) ? __ldcg(partial + int64_t(m0 + u) * RR + p) : 0.0;
-            double q = pk[0];
-#pragma unroll
-            for (int u = 1; u < kSuper; ++u)
-                if (m0 + u < m1) q = q + pk[u];
-            tot = (m0 == 0) ? q : tot + q;
+                pk[o][u] = (p < RR && m0 + u < m1) ? __ldcg(partial + int64_t(m0 + u) * RR + p) : 0.0;
         }
-        out[p] = acc_base ? acc_base[p] + tot : tot;  // column-major == row-major (symmetric)
+#pragma unroll
+        for (int o = 0; o < kOB; ++o) {
+            const int p = pb + o * int(blockDim.x);
+            if (p < RR) {
+                double q = pk[o][0];
+#pragma unroll
+                for (int u = 1; u < kSuper; ++u)
+                    if (m0 + u < m1) q = q + pk[o][u];
+                spart[int64_t(msup) * RR + p] = q;
+            }
+        }
+    }
+    const int nsup = (nk + kSuper - 1) / kSuper;
+    if (!last_arrive_of(counter, unsigned(nsup))) return;
+    for (int pb = threadIdx.x; pb < RR; pb += kOB * blockDim.x) {
+        double sv[kOB][kSuper], bv[kOB];
+#pragma unroll
+        for (int o = 0; o < kOB; ++o) {
+            const int p = pb + o * int(blockDim.x);
+#pragma unroll
+            for (int u = 0; u < kSuper; ++u) sv[o][u] = (p < RR && u < nsup) ? __ldcg(spart + int64_t(u) * RR + p) : 0.0;
+            bv[o] = (p < RR && acc_base) ? acc_base[p] : 0.0;
+        }
+#pragma unroll
+        for (int o = 0; o < kOB; ++o) {
+            const int p = pb + o * int(blockDim.x);
+            if (p < RR) {
+                double tot = sv[o][0];
+#pragma unroll
+                for (int u = 1; u < kSuper; ++u)
+                    if (u < nsup) tot = tot + sv[o][u];
+                for (int u = kSuper; u < nsup; ++u) tot = tot + __ldcg(spart + int64_t(u) * RR + p);
+                out[p] = acc_base ? bv[o] + tot : tot;  // column-major == row-major (symmetric)
+            }
+        }
     }
 }
 
@@ -990,29 +1027,30 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ G, int
     const int2 mr = gram_solve_block<kEpt>(G, R, nullptr, gi, cbuf, jscr, blockIdx.x == 0);
     if (blockIdx.x == 0 && threadIdx.x == 0 && mr.y && flags) atomicOr(flags, 1);
     // rows: one warp per row, lane j holds entries j and j + 32 (R <= 64)
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int32_t row = int32_t(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
-    if (row >= rows) return;
+    // (the grid is capped at one block per SM: a block pays for the sweep once and walks its rows)
+    const int tid = threadIdx.x, lane = tid & 31, nw = blockDim.x >> 5;
     const int j0 = lane, j1 = lane + 32;
     const bool v0 = j0 < R, v1 = MAXR > 32 && j1 < R;
-    double w0 = v0 ? RHS[int64_t(row) * R + j0] : 0.0;
-    double w1 = v1 ? RHS[int64_t(row) * R + j1] : 0.0;
-    if (mr.x == 0) {
-        w0 = w1 = 0.0;
-    } else {
-        double a0 = 0.0, a1 = 0.0;
-        for (int k = 0; k < R; ++k) {
-            const double bk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
-            if (v0) a0 = __fma_rn(bk, gi[k * R + j0], a0);
-            if (v1) a1 = __fma_rn(bk, gi[k * R + j1], a1);
+    for (int32_t row = int32_t(blockIdx.x) * nw + (tid >> 5); row < rows; row += int32_t(gridDim.x) * nw) {
+        double w0 = v0 ? RHS[int64_t(row) * R + j0] : 0.0;
+        double w1 = v1 ? RHS[int64_t(row) * R + j1] : 0.0;
+        if (mr.x == 0) {
+            w0 = w1 = 0.0;
+        } else {
+            double a0 = 0.0, a1 = 0.0;
+            for (int k = 0; k < R; ++k) {
+                const double bk = __shfl_sync(0xffffffffu, k < 32 ? w0 : w1, k & 31);
+                if (v0) a0 = __fma_rn(bk, gi[k * R + j0], a0);
+                if (v1) a1 = __fma_rn(bk, gi[k * R + j1], a1);
+            }
+            w0 = a0;
+            w1 = a1;
         }
-        w0 = a0;
-        w1 = a1;
+        if (v0) OUT[int64_t(row) * R + j0] = w0;
+        if (v1) OUT[int64_t(row) * R + j1] = w1;
+        const bool finite = (!v0 || isfinite(w0)) && (!v1 || isfinite(w1));
+        if (!finite && flags) flags[1] = nonfinite_code;
     }
-    if (v0) OUT[int64_t(row) * R + j0] = w0;
-    if (v1) OUT[int64_t(row) * R + j1] = w1;
-    const bool finite = (!v0 || isfinite(w0)) && (!v1 || isfinite(w1));
-    if (!finite && flags) flags[1] = nonfinite_code;
 }
 
 // ---------------------------------------------------------------------------

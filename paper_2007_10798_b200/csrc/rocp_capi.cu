@@ -203,6 +203,7 @@ struct rocp_dev {
     JobList jobs;                       // draw/gather job scratch of the primitives and cprand
     DBuf<double> contract_partial;      // split-superchunk contraction partials
     DBuf<unsigned int> tile_counters;   // per-row-tile arrival counters (self-resetting)
+    DBuf<unsigned int> gram_counters;   // k_gram: per-superchunk arrival counters (self-resetting)
     DBuf<int64_t> rows_in;              // explicit index scratch of the primitives
     cudaEvent_t timer[8] = {};          // rocp_timer_* slots
     // overlapped window gather: its own stream on SMs reserved beside the chain kernel
@@ -371,9 +372,16 @@ void launch_skr(rocp_dev* dev, const SkrJob& j) {
 void launch_gram(rocp_dev* dev, const double* Z, int64_t s, int R, const double* acc_base,
                  double* out) {
     const int nk = int((s + kChunk - 1) / kChunk);
-    dev->scratch_a.ensure(size_t(nk) * R * R);
+    const int nsup = (nk + kSuper - 1) / kSuper;
+    dev->scratch_a.ensure(size_t(nk + nsup) * R * R);
+    if (dev->gram_counters.n < size_t(nsup)) {  // self-resetting arrival counters, one per superchunk
+        CK(cudaStreamSynchronize(dev->stream));
+        dev->gram_counters.alloc(size_t(std::max(nsup, 64)));
+        CK(cudaMemset(dev->gram_counters.p, 0, dev->gram_counters.n * sizeof(unsigned int)));
+    }
     k_gram<<<nk, 256, size_t(kChunk) * R * sizeof(double), dev->stream>>>(
-        Z, int32_t(s), R, dev->scratch_a.p, dev->counters.p + 0, acc_base, out);
+        Z, int32_t(s), R, dev->scratch_a.p, dev->scratch_a.p + size_t(nk) * R * R, dev->counters.p + 0,
+        dev->gram_counters.p, acc_base, out);
     after_launch(dev, "k_gram");
 }
 
@@ -490,7 +498,8 @@ void set_contract_smem_attrs() {
 // flags: [0] |= 1 when regularized, [1] = nonfinite_code on a non-finite output.
 void launch_solve(rocp_dev* dev, const double* G, int R, const double* RHS, int64_t rows, double* OUT,
                   int* flags, int nonfinite_code) {
-    const int grid = int(std::max<int64_t>(1, (rows + 7) / 8));  // a warp per row
+    // a warp per row; at most one block per SM (every block repeats the sweep of G)
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>((rows + 7) / 8, dev->num_sms)));
     if (R <= 16) k_solve<16><<<grid, 256, ksolve_smem_bytes(16), dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     else if (R <= 32) k_solve<32><<<grid, 256, ksolve_smem_bytes(32), dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
     else k_solve<64><<<grid, 256, ksolve_smem_bytes(64), dev->stream>>>(G, R, RHS, int32_t(rows), OUT, flags, nonfinite_code);
@@ -1602,6 +1611,8 @@ static rocp_status create_dev(int device, int world, int rank, const void* nccl_
         CK(cudaDeviceGetAttribute(&dev->num_sms, cudaDevAttrMultiProcessorCount, device));
         dev->counters.alloc(16);
         CK(cudaMemset(dev->counters.p, 0, 16 * sizeof(unsigned int)));
+        dev->gram_counters.alloc(64);
+        CK(cudaMemset(dev->gram_counters.p, 0, 64 * sizeof(unsigned int)));
         dev->flags.alloc(4);
         CK(cudaMemset(dev->flags.p, 0, 4 * sizeof(int)));
         dev->scalars.alloc(16);
@@ -2235,7 +2246,7 @@ rocp_stream* new_stream(rocp_dev* dev, int order, const int64_t* head_dims, int 
     st->mode_flag.alloc(4);
     CK(cudaMemsetAsync(st->flags.p, 0, 4 * sizeof(int), dev->stream));
     // Reduction scratch sized once: consume (and its CUDA graph) never allocates.
-    dev->scratch_a.ensure(size_t((s + kChunk - 1) / kChunk) * rank * rank);
+    dev->scratch_a.ensure(size_t((s + kChunk - 1) / kChunk + (s + kSuperSamples - 1) / kSuperSamples) * rank * rank);
     dev->scratch_b.ensure(size_t(3 * s));
     CK(cudaMemsetAsync(st->resid.p, 0, size_t(2 * order) * 8, dev->stream));
     ensure_window(st.get(), 1, 1);
