@@ -45,6 +45,30 @@ def test_streamed_wide_chain_bitwise(dev, dims, R, t_init, B, sms):
         dev.set_gather_sms(-1)
 
 
+def test_streamed_wide_chain_host_slabs_and_single_batches(dev):
+    """The same bits through the reference-facing calls: consume() batch by batch on host slabs,
+    and the whole range from host memory (sampled fibres gathered by host threads, chain per batch)."""
+    import paper_2007_10798_b200 as rocp
+    dims, R, t_init, B = [96, 130, 40], 50, 20, 10
+    x, X, a, b, s, nb = _run_pair(dev, dims, R, 20.0, t_init, B, nbatches=2, kw=dict(max_iters=4))
+    a.checkpoint()
+    for k in range(nb):
+        a.consume(H.slab(x, dims, t_init + k * B, B), 777, k + 1)
+        b.consume(H.slab(x, dims, t_init + k * B, B), B, 777, k + 1)
+    _cmp_stream(a, b, len(dims))
+    ref = [a.factor(1), a.factor(2), a.temporal()]
+    a.restore()
+    a.consume_range_host(H.slab(x, dims, t_init, B * nb), B, nb, 777, 1)
+    assert bitwise(a.factor(1), ref[0]) and bitwise(a.factor(2), ref[1]) and bitwise(a.temporal(), ref[2])
+    slab = H.slab(x, dims, t_init, B * nb)
+    hb = rocp.HostBuffer(slab.size)
+    hb.array[:] = slab
+    a.restore()
+    a.consume_range_host(hb.array, B, nb, 777, 1)
+    assert bitwise(a.factor(1), ref[0]) and bitwise(a.factor(2), ref[1]) and bitwise(a.temporal(), ref[2])
+    hb.free()
+
+
 CHILD = r'''
 import numpy as np
 import paper_2007_10798_b200 as rocp
