@@ -979,6 +979,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                 }
                 __syncthreads();
                 if (tr) trace_stamp(tr, 14, tid == 0 && ch == 0);
+                if (tid == 0) {  // the chunk's Z rows are in: the contraction does not wait for its Gram partial
+                    __threadfence();
+                    atomicAdd(p.zctr + 2 + nsuper + ch / kSuper, 1u);
+                }
                 if constexpr (!kWide) {
                     chain_chunk_gram_dmma(zc, RP, R, p.chpart + int64_t(ch) * NPp);
                 } else {
@@ -1175,7 +1179,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                     double* zst = ring + stream_stages(RP) * kRingSlot;  // [256][RP + 4], as in memory
                     if (tid == 0) {  // superchunk zm's chunks of Z published (no grid barrier after phase 0)
                         const unsigned nck = unsigned(min(kSuper, nch - zm * kSuper));
-                        wait_gathered(p.zctr + 1 + zm, unsigned(b * N + st + 1) * nck, 0u, 0u);
+                        wait_gathered(p.zctr + 2 + nsuper + zm, unsigned(b * N + st + 1) * nck, 0u, 0u);
                         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
                         fence_proxy_async();
                         tma_load_1d(zst, Z + int64_t(c0) * ZS, unsigned(cn * ZS * 8), &bar);
@@ -1206,7 +1210,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const ChainParams p)
                         const bool zload = m != zm_cur;
                         if (zload) {  // superchunk m's chunks of Z published (no grid barrier after phase 0)
                             const unsigned nck = unsigned(min(kSuper, nch - m * kSuper));
-                            wait_gathered(p.zctr + 1 + m, unsigned(b * N + st + 1) * nck, 0u, 0u);
+                            wait_gathered(p.zctr + 2 + nsuper + m, unsigned(b * N + st + 1) * nck, 0u, 0u);
                             asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk copy
                             tma_load_1d(zs, Z + int64_t(c0) * RP, unsigned(cn * RP * 8), &bar);
                         }

@@ -1164,7 +1164,7 @@ int gather_sms(rocp_stream* st, int64_t B) {
             rows_max = std::max(rows_max, double(I));
         }
         elems *= double(st->s);
-        const double t_chain = st->N * (st->R > 32 ? 95.0 : 14.0);      // us per batch
+        const double t_chain = st->N * (st->R > 32 ? 100.0 : 14.0);     // us per batch
         const double t_full = elems / (93e3);                             // us, whole-device gather
         if (t_full < 0.025 * (t_full + t_chain)) return 0;
         g = int(std::ceil(elems / (1470.0 * t_chain)));
@@ -1440,8 +1440,9 @@ void launch_chain(rocp_stream* st, int64_t nb, int64_t B, int64_t b0 = 0, bool o
     p.counter = st->dev->counters.p + 4;
     // phase-0 chunk arrivals (total, per superchunk), cumulative over the launch's stages
     // (+ [1 + nsuper]: superchunk Gram pre-sums published, k_chain without the one-block combine)
-    if (st->zctr.n < size_t(p.nsuper + 2)) st->zctr.alloc(size_t(p.nsuper + 2));
-    CK(cudaMemsetAsync(st->zctr.p, 0, size_t(p.nsuper + 2) * sizeof(unsigned), st->dev->stream));
+    // (+ [2 + nsuper + m]: Z rows of superchunk m's chunks published, ahead of their Gram partials)
+    if (st->zctr.n < size_t(2 * p.nsuper + 2)) st->zctr.alloc(size_t(2 * p.nsuper + 2));
+    CK(cudaMemsetAsync(st->zctr.p, 0, size_t(2 * p.nsuper + 2) * sizeof(unsigned), st->dev->stream));
     p.zctr = st->zctr.p;
     int grid = st->dev->num_sms;
     if (overlap) {
