@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
     ([96, 130, 60], 50, 20, 10, 36),   # the wide chain with streamed items
     ([60, 50, 90], 20, 30, 10, 16),    # too few blocks for the dataflow chain: the grid-barrier chain, two chunks per block
     ([50, 40, 60], 32, 24, 12, 16),    # the same with the chunk blocks' superchunk pre-sums
+    ([96, 130, 60], 50, 20, 10, 16),   # the wide chain with one or two blocks per superchunk
 ])
 def test_concurrent_streams_bitwise(dims, R, t_init, B, sms):
     K = 3
