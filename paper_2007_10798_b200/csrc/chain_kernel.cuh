@@ -501,8 +501,8 @@ __device__ __noinline__ void chain_contract_dmma(const double* xs, const double*
 
 // ---- Streamed wide contraction (R in 33..64, one superchunk per block) ------------------
 // The block keeps superchunk zm's Z tile resident and walks its share of the stage's row-tile
-// PAIRS (64 rows: tiles 2u, 2u + 1).  A pair's X_s arrives chunk by chunk (two 8 KB bulk
-// copies per 32-sample chunk) through a ring of kRingStages slots, so the loads of the next
+// PAIRS (64 rows: tiles 2u, 2u + 1).  A pair's X_s arrives chunk by chunk (two 8 KB tensor-map
+// boxes per 32-sample chunk) through a ring of stream_stages(RP) slots, so the loads of the next
 // chunks -- and of the block's next pair -- are in flight behind the MMAs.  Warp w owns the
 // 16 rows rp = w & 3 of the pair and one half of the column tiles (w >> 2) for EVERY chunk:
 // the chunk partial is the fp64 MMA chain over the chunk's samples from +0.0 (rounds like the
