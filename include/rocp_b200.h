@@ -77,6 +77,8 @@ rocp_status rocp_set_gather_sms(rocp_dev* dev, int sms);
  * co-resident and the GPU's otherwise idle SMs serve the other streams.  Results
  * are bitwise identical for every setting.  No reference counterpart. */
 rocp_status rocp_set_chain_sms(rocp_dev* dev, int sms);
+/* The device's SM count (to size rocp_set_chain_sms shares). */
+rocp_status rocp_sm_count(rocp_dev* dev, int* sms);
 /* Measurement aid (no reference counterpart): event-timed kernel of `reads`
  * independent 8-byte loads at hashed offsets of t on every SM -- the device's
  * isolated random-read ceiling that bounds the strided sampled-fibre gather

@@ -277,6 +277,7 @@ ComplementaryState load_state(std::istream& in);
 
 // Device selection for this thread's calls (default: device 0, created lazily).
 void set_device(int device);
+int current_device();  // the calling thread's device ordinal (set_device; default 0)
 rocp_dev* device_handle();
 
 }  // namespace rocp

@@ -45,6 +45,7 @@ SIGNATURES = [
     ("rocp_last_error", C.c_char_p, [_vp]),
     ("rocp_set_gather_sms", C.c_int, [_vp, C.c_int]),
     ("rocp_set_chain_sms", C.c_int, [_vp, C.c_int]),
+    ("rocp_sm_count", C.c_int, [_vp, C.POINTER(C.c_int)]),
     ("rocp_synchronize", C.c_int, [_vp]),
     ("rocp_kernel_launches", C.c_uint64, [_vp]),
     ("rocp_nccl_id_size", C.c_int, []),
@@ -290,6 +291,12 @@ class Device:
     def set_chain_sms(self, sms):
         """Blocks of this handle's persistent chain (rocp_set_chain_sms; 0 = every SM)."""
         self.check(lib().rocp_set_chain_sms(self.h, int(sms)))
+
+    @property
+    def sm_count(self):
+        n = C.c_int(0)
+        self.check(lib().rocp_sm_count(self.h, C.byref(n)))
+        return n.value
 
     def tensor(self, dims, host=None):
         return DeviceTensor(self, dims, host)

@@ -1720,6 +1720,13 @@ rocp_status rocp_set_chain_sms(rocp_dev* dev, int sms) {
     });
 }
 
+rocp_status rocp_sm_count(rocp_dev* dev, int* sms) {
+    return guarded(dev, [&] {
+        if (!sms) throw_domain("null output");
+        *sms = dev->num_sms;
+    });
+}
+
 rocp_status rocp_timer_record(rocp_dev* dev, int slot) {
     return guarded(dev, [&] {
         if (slot < 0 || slot >= 8) throw_domain("timer slot out of range");

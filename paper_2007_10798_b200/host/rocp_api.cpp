@@ -81,6 +81,8 @@ void set_device(int device) {
     g_dev.device = device;
 }
 
+int current_device() { return g_dev.device; }
+
 rocp_dev* device_handle() {
     if (!g_dev.h) {
         rocp_dev* d = nullptr;

@@ -14,8 +14,13 @@
 
 #include "../../include/rocp_b200.h"
 
+#include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
+#include <cstdlib>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <map>
 #include <ostream>
@@ -298,14 +303,46 @@ BenchReport run_benchmark(const BenchConfig& cfg) {
             throw std::domain_error(std::string("run_benchmark: ") + algorithm_name(a) +
                                     " is a reference baseline, not on the B200 path (DESIGN.md section 8)");
     BenchReport report;
-    // trials run in order on this thread's device (one GPU serves them all)
-    for (int trial = 0; trial < cfg.trials; ++trial) {
+    const size_t per_trial = cfg.algorithms.size();
+    report.rows.resize(size_t(cfg.trials) * per_trial);
+    auto run_trial = [&](int trial) {
         Rng data = seeded_engine(cfg.seed, trial, 0);
         const DenseTensor full = cfg.input_path.empty()
                                      ? gen_synthetic(cfg.dims, cfg.rank, cfg.sir_db, data, cfg.family, cfg.congruence).x
                                      : read_tensor_file(cfg.input_path);
         const SlabCutter cut(full, cfg.init_fraction, cfg.batch_size);
-        for (size_t a = 0; a < cfg.algorithms.size(); ++a) report.rows.push_back(rocp_trial(cfg, trial, full, cut));
+        for (size_t a = 0; a < per_trial; ++a) report.rows[size_t(trial) * per_trial + a] = rocp_trial(cfg, trial, full, cut);
+    };
+    // ROCP_THREADS (reference bench.cpp:190-213; default 1 = serial, which keeps the per-update
+    // wall times honest): K trials at a time, each worker thread on its own device handle with
+    // 1/K of the SMs for its persistent chain (rocp_set_chain_sms), so the trials share the GPU
+    // side by side.  Every cell derives its generators from (seed, trial): the fitness values do
+    // not depend on K.
+    int workers = 1;
+    if (const char* e = std::getenv("ROCP_THREADS")) workers = std::max(1, std::atoi(e));
+    workers = std::min(workers, cfg.trials);
+    if (workers == 1) {
+        for (int trial = 0; trial < cfg.trials; ++trial) run_trial(trial);
+    } else {
+        const int device = current_device();
+        std::atomic<int> next{0};
+        std::vector<std::exception_ptr> errs(static_cast<size_t>(workers));
+        std::vector<std::thread> pool;
+        for (int w = 0; w < workers; ++w)
+            pool.emplace_back([&, w] {
+                try {
+                    set_device(device);
+                    int sms = 0;
+                    if (rocp_sm_count(device_handle(), &sms) == ROCP_OK && sms / workers >= 16)
+                        rocp_set_chain_sms(device_handle(), std::max(16, (sms - sms / 8) / workers));
+                    for (int trial = next++; trial < cfg.trials; trial = next++) run_trial(trial);
+                } catch (...) {
+                    errs[size_t(w)] = std::current_exception();
+                }
+            });
+        for (std::thread& t : pool) t.join();
+        for (const std::exception_ptr& e : errs)
+            if (e) std::rethrow_exception(e);
     }
     report.aggregates = aggregate_rows(report.rows);
     return report;

@@ -5,6 +5,7 @@
 #include "rocp_b200/rocp.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -373,6 +374,23 @@ static void test_bench_harness() {  // test_bench.cpp:114-207
         CHECK(same);
         cfg.algorithms = {Algorithm::rocp, Algorithm::batch_hot};  // baselines are not on this path
         CHECK(throws<std::domain_error>([&] { run_benchmark(cfg); }));
+    }
+    {
+        BenchConfig cfg;  // ROCP_THREADS: trials side by side on one GPU, fitness independent of the parallelism
+        cfg.dims = {10, 9, 24};
+        cfg.rank = 3;
+        cfg.trials = 5;
+        cfg.seed = 19;
+        const BenchReport serial = run_benchmark(cfg);
+        setenv("ROCP_THREADS", "3", 1);
+        const BenchReport par = run_benchmark(cfg);
+        unsetenv("ROCP_THREADS");
+        bool same = serial.rows.size() == 5 && par.rows.size() == 5;
+        for (size_t i = 0; same && i < 5; ++i)
+            same = serial.rows[i].trial == int(i) && par.rows[i].trial == int(i) &&
+                   serial.rows[i].fitness == par.rows[i].fitness && par.rows[i].updates == serial.rows[i].updates;
+        CHECK(same);
+        CHECK(par.aggregates.size() == 1 && par.aggregates[0].fitness_mean == serial.aggregates[0].fitness_mean);
     }
     {
         BenchConfig cfg;  // aggregates are recomputable from the rows
