@@ -44,3 +44,4 @@ def test_chain_sms_domain(dev):
     with pytest.raises(ValueError):
         dev.set_chain_sms(100000)
     dev.set_chain_sms(0)
+    assert dev.sm_count >= 16
